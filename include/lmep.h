@@ -1,0 +1,236 @@
+/*
+ * lmep.h -- C ABI of the B200-native LMEP hot path (liblmep.so).
+ *
+ * This is the drop-in boundary for the reference package `localexp`
+ * (/root/reference/pkg/src/localexp).  The reference has no FFI: its seam is
+ * the Python API listed below, and every entry point here replaces one
+ * reference function (file:line).  The Python mirror of that API
+ * (paper_2603_15964_b200/{harvest,kernels,timestep,...}.py) binds these
+ * symbols with ctypes; INTEGRATION.md shows the binding.
+ *
+ * Conventions (all entry points):
+ *   - plain C types only; every array argument is a DEVICE pointer unless the
+ *     comment says "host";
+ *   - every call is asynchronous on `stream` (a cudaStream_t passed as void*;
+ *     NULL = legacy default stream);
+ *   - the return value is an lmep_status; inputs are never modified
+ *     (reference: kernels.py:35,74 copy u0, harvest.py:59-62 read-only rows);
+ *   - all arithmetic is IEEE fp64.
+ */
+#ifndef LMEP_H
+#define LMEP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  They map 1:1 onto localexp.errors (errors.py:4-50). */
+typedef enum {
+    LMEP_OK = 0,
+    LMEP_NONFINITE = 1,        /* NonFinite        (expm.py:35-41, timestep.py:345-348) */
+    LMEP_DIMENSION = 2,        /* DimensionMismatch (harvest.py:57-58,77-78,113-114)    */
+    LMEP_INVALID_CONFIG = 3,   /* InvalidConfig / ValueError (harvest.py:85-86)         */
+    LMEP_CUDA_ERROR = 4,       /* launch or runtime failure                             */
+    LMEP_ORDER_TOO_HIGH = 5,   /* OrderTooHigh     (localop.py:69-70,115-116)           */
+    LMEP_DUPLICATE_NODES = 6   /* DuplicateNodes   (localop.py:71-74)                   */
+} lmep_status;
+
+#define LMEP_MAX_N 32          /* largest stencil size n                              */
+#define LMEP_MAX_DIM 32        /* largest exponentiated dimension d = n + s - 1       */
+#define LMEP_MAX_ROWS 7        /* operator rows per step: w, alpha, beta, gamma,      */
+                               /* w_half, p1_half, d1 (timestep.py:141-156)           */
+
+/* Row slots of the operator set passed to the step kernels. */
+enum {
+    LMEP_ROW_W = 0,            /* linear: exp(dt L); etdrk4: w_full; etd2: exp(dt L)   */
+    LMEP_ROW_ALPHA = 1,        /* etdrk4 alpha;  etd2: dt*phi1 (raw harvest row)       */
+    LMEP_ROW_BETA = 2,         /* etdrk4 beta;   etd2: dt^2*phi2 (raw harvest row)     */
+    LMEP_ROW_GAMMA = 3,        /* etdrk4 gamma                                         */
+    LMEP_ROW_WHALF = 4,        /* etdrk4 w_half                                        */
+    LMEP_ROW_P1HALF = 5,       /* etdrk4 p1_half                                       */
+    LMEP_ROW_D1 = 6            /* banded first derivative for N(u) = -u * (D1 u)       */
+};
+
+/* Nonlinearity kinds: kernels.py:17-19. */
+enum { LMEP_NL_NONE = 0, LMEP_NL_CONVECTIVE = 1, LMEP_NL_CUBIC = 2 };
+
+/* Weight storage modes of the step kernels. */
+enum {
+    LMEP_W_SHARED = 0,         /* one row set for every node (periodic uniform grid)  */
+    LMEP_W_CLASS = 1,          /* nleft + 1 + nright row sets selected by position    */
+    LMEP_W_PERNODE = 2         /* per-node rows, SoA [nrows][n][nloc]                  */
+};
+
+/* Boundary handling applied where the reference pins (kernels.py:39-41,93-95,
+ * 101-103,112-114,129-131). */
+enum { LMEP_BC_NONE = 0, LMEP_BC_DIRICHLET = 1, LMEP_BC_NEUMANN = 2 };
+
+/* Step flags. */
+enum {
+    LMEP_FLAG_EXACT = 1        /* separate multiply/add roundings, ascending order:   */
+                               /* bit-identical to the numba loops (kernels.py:8-9)    */
+};
+
+/* 1D stencil geometry of one shard (grid.py:136-175).  Node t of the global grid
+ * (0 <= t < N) reads the window start(t) .. start(t)+n-1 with
+ *   periodic:     start(t) = t - row (mod N)
+ *   non-periodic: start(t) = clamp(t - row, 0, N - n).
+ * The shard owns global nodes off .. off+nloc-1. */
+typedef struct {
+    int64_t N;
+    int64_t off;
+    int64_t nloc;
+    int32_t n;
+    int32_t row;
+    int32_t periodic;
+    int32_t reserved;
+} lmep_grid;
+
+/* Operator rows.  `interior` is a HOST pointer to [nrows][n] rows used for
+ * every interior node (mode SHARED and CLASS).  CLASS: `classes` is a device
+ * [nleft+1+nright][nrows][n] table; node t uses class t for t < nleft,
+ * nleft+1+(t-(N-nright)) for t >= N-nright, and the interior set otherwise.
+ * PERNODE: `pernode` is a device SoA [nrows][n][nloc] table of this shard. */
+typedef struct {
+    int32_t mode;
+    int32_t nrows;
+    int32_t nleft;
+    int32_t nright;
+    const double *interior;    /* host   */
+    const double *classes;     /* device */
+    const double *pernode;     /* device */
+} lmep_weights;
+
+/* Boundary closure (non-periodic grids).  DIRICHLET pins u[0]=lo, u[N-1]=hi
+ * (timestep.py:129-133).  NEUMANN applies the zero-gradient closure
+ *   u[0]   = -sum_{j>=1} dl[j] u[j] / dl[0]
+ *   u[N-1] = -sum_{j<n-1} dr[j] u[N-n+j] / dr[n-1]
+ * (SURVEY Appendix B.2).  dl/dr are HOST pointers to n values. */
+typedef struct {
+    int32_t kind;
+    int32_t reserved;
+    double lo, hi;
+    const double *dl;
+    const double *dr;
+} lmep_bc;
+
+/* Ghost cells of a sharded run (1D slab decomposition, filled by the caller's
+ * halo exchange).  `left` holds global nodes off-width .. off-1 and `right`
+ * holds off+nloc .. off+nloc+width-1 (wrapped on periodic grids).  All NULL:
+ * a single shard covering the whole grid (periodic wrap is done in-kernel). */
+typedef struct {
+    const double *left;
+    const double *right;
+    const double *hist_left;   /* etd2 history ghosts */
+    const double *hist_right;
+    int64_t width;
+} lmep_halo;
+
+/* Optional launch shape.  0 = library heuristic. */
+typedef struct {
+    int32_t tile;              /* owned nodes per CTA                                 */
+    int32_t ksteps;            /* time steps fused per launch (temporal blocking)     */
+    int32_t ring;              /* 1: whole periodic grid resident in one CTA          */
+    int32_t reserved;
+} lmep_tuning;
+
+/* ---- library ------------------------------------------------------------ */
+int lmep_version(void);
+const char *lmep_status_string(int status);
+/* Last CUDA error string seen by the library (host, static storage). */
+const char *lmep_last_error(void);
+/* Number of kernels this library has launched in this process (for the
+ * bench's gpu_launches accounting). */
+int64_t lmep_launch_count(void);
+
+/* ---- harvest (K1, K2) --------------------------------------------------- */
+
+/* Fornberg weight tables, one thread per item b:
+ *   out[b][k][j] = weight of sample x_b[j] for d^k/dx^k at z[b], k = 0..m.
+ * x is [B][n] with row stride x_stride (0 = one node set shared by all items).
+ * Replaces localop.fornberg_weights (localop.py:61-96); bit-identical. */
+int lmep_fornberg(const double *z, const double *x, int64_t x_stride, int n, int m,
+                  int64_t B, double *out, void *stream);
+
+/* Batched exp(A) of B dense d x d matrices (row-major [B][d][d]), one warp per
+ * matrix: balancing (permute=False), Pade scaling-and-squaring (Al-Mohy &
+ * Higham 2009, the algorithm scipy.linalg.expm implements), unbalancing.
+ * Replaces expm.expm (expm.py:24-42).  status[b] (nullable) gets
+ * LMEP_OK / LMEP_NONFINITE per matrix, ms[b] (nullable) = m | (squarings << 8).
+ * Returns LMEP_NONFINITE only via status[]; the call itself returns launch status. */
+int lmep_expm(const double *A, int d, int64_t B, double *E, int32_t *status, int32_t *ms,
+              void *stream);
+
+/* Batched weight harvest (harvest.py:73-121 + 135-159), one warp per item.
+ * Item b's local operator is assembled in shared memory exactly as
+ * localop.local_operator (localop.py:111-128) does it:
+ *   L = sum_t coef[b*coef_stride + t] * tables[table_idx[b]][t]   (ascending t)
+ *   L[i][i] += c0[b*c0_stride]                                      (if != 0)
+ * where tables is [ntab][nterms][n][n] (derivative matrices D^(k) on that
+ * item's local coordinates, e.g. from lmep_fornberg).  If `L` is non-NULL it
+ * is used instead ([B][n][n], explicit operators; tables/coef/c0 ignored).
+ * Rows listed in the frozen bitmask are zeroed (harvest.py:116-117).  The
+ * exponential is taken of the reduced (n+s-1) x (n+s-1) transposed
+ * augmentation [[dt L^T, dt e_r, 0], [0, 0, dt J]] instead of the sn x sn block
+ * companion (harvest.py:82-94); both yield the same rows.
+ * Output rows: w_lin = row r of exp(dt L), then the raw dt^j phi_j rows,
+ * j = 1..s-1 (harvest.py:119-120).
+ *   layout 0: w_out[b][j][i]  ([B][s][n], reference order)
+ *   layout 1: w_out[j][i][b]  ([s][n][B], SoA for LMEP_W_PERNODE)
+ * target_row / frozen are per item (nullable -> the *_default value). */
+int lmep_harvest(int n, int s, int nterms, const double *tables, const int32_t *table_idx,
+                 const double *coef, int64_t coef_stride, const double *c0, int64_t c0_stride,
+                 const double *L, double delta_t, const int32_t *target_row, int row_default,
+                 const uint64_t *frozen, uint64_t frozen_default, int64_t B, int layout,
+                 double *w_out, int32_t *status, int32_t *ms, void *stream);
+
+/* ---- stepping (K3, K4, K5) ---------------------------------------------- */
+
+/* Linear banded propagation u <- W u for `steps` steps (kernels.py:33-43,
+ * run_linear).  u_in is not modified; the result lands in u_out.  `scratch`
+ * (nloc doubles, nullable = library-allocated) is the ping-pong buffer.
+ * nonfinite (nullable, device int32) is set to 1 if any produced value is
+ * not finite (the caller raises NonFinite, timestep.py:345-348). */
+int lmep_step_linear(const lmep_grid *grid, const lmep_weights *w, const lmep_bc *bc,
+                     const lmep_halo *halo, const double *u_in, double *u_out,
+                     double *scratch, int64_t steps, int32_t flags,
+                     const lmep_tuning *tuning, int32_t *nonfinite, void *stream);
+
+/* Fused four-stage ETDRK4 (kernels.py:62-132, run_etdrk4): rows W, ALPHA, BETA,
+ * GAMMA, WHALF, P1HALF (and D1 for LMEP_NL_CONVECTIVE).  nl0_out (nullable)
+ * receives N(u_in) on the owned nodes (the history entry the ETD multistep
+ * warm-up stores, timestep.py:375-378). */
+int lmep_step_etdrk4(const lmep_grid *grid, const lmep_weights *w, const lmep_bc *bc,
+                     const lmep_halo *halo, int nl_kind, const double *u_in,
+                     double *u_out, double *scratch, int64_t steps, double *nl0_out,
+                     int32_t flags, const lmep_tuning *tuning, int32_t *nonfinite,
+                     void *stream);
+
+/* Exponential multistep of order 2 (timestep.py:187-215, s=2):
+ *   N_k = N(u);  u <- W u + P1 N_k + P2 (N_k - N_{k-1}) / dt
+ * with rows W (exp), ALPHA (raw dt*phi1), BETA (raw dt^2*phi2) and D1.
+ * hist_in = N_{k-1}; hist_out receives the last N_k.  scratch: 2*nloc doubles. */
+int lmep_step_etd2(const lmep_grid *grid, const lmep_weights *w, const lmep_bc *bc,
+                   const lmep_halo *halo, int nl_kind, double delta_t, const double *u_in,
+                   const double *hist_in, double *u_out, double *hist_out, double *scratch,
+                   int64_t steps, int32_t flags, const lmep_tuning *tuning,
+                   int32_t *nonfinite, void *stream);
+
+/* Plain banded mat-vec out[i] = sum_j w[i][j] * u[members(i, j)] with the
+ * grid's window rule (kernels.py:23-29, harvest.apply at harvest.py:213-222). */
+int lmep_banded_matvec(const lmep_grid *grid, const lmep_weights *w, const lmep_halo *halo,
+                       const double *u, double *out, int32_t flags, void *stream);
+
+/* Chooses the launch shape the library would use (for reporting/tests). */
+int lmep_plan(const lmep_grid *grid, int scheme, int nl_kind, int64_t steps,
+              lmep_tuning *out);
+
+/* Transpose (N, n) row-major per-node rows into the SoA [n][N] layout. */
+int lmep_rows_to_soa(const double *rows, int64_t N, int n, double *soa, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LMEP_H */

@@ -1,0 +1,156 @@
+"""ctypes binding of liblmep.so (the C ABI declared in include/lmep.h).
+
+The product path has exactly one implementation: the CUDA kernels in this
+library.  There is no CPU fallback: if the library or a CUDA device is
+missing, every compute entry point raises instead of computing elsewhere.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import torch
+
+from . import errors
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "liblmep.so")
+CSRC = os.path.join(_HERE, "csrc")
+
+LMEP_OK = 0
+LMEP_NONFINITE = 1
+LMEP_DIMENSION = 2
+LMEP_INVALID_CONFIG = 3
+LMEP_CUDA_ERROR = 4
+LMEP_ORDER_TOO_HIGH = 5
+LMEP_DUPLICATE_NODES = 6
+
+MAX_N = 32
+MAX_DIM = 32
+MAX_ROWS = 7
+ROW_W, ROW_ALPHA, ROW_BETA, ROW_GAMMA, ROW_WHALF, ROW_P1HALF, ROW_D1 = range(7)
+NL_NONE, NL_CONVECTIVE, NL_CUBIC = 0, 1, 2
+W_SHARED, W_CLASS, W_PERNODE = 0, 1, 2
+BC_NONE, BC_DIRICHLET, BC_NEUMANN = 0, 1, 2
+FLAG_EXACT = 1
+SCH_LIN, SCH_ETDRK4, SCH_ETD2 = 0, 1, 2
+
+# every symbol include/lmep.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "lmep_version", "lmep_status_string", "lmep_last_error", "lmep_fornberg", "lmep_expm",
+    "lmep_harvest", "lmep_step_linear", "lmep_step_etdrk4", "lmep_step_etd2",
+    "lmep_banded_matvec", "lmep_plan", "lmep_rows_to_soa", "lmep_launch_count",
+)
+
+
+class LmepGrid(C.Structure):
+    _fields_ = [("N", C.c_int64), ("off", C.c_int64), ("nloc", C.c_int64), ("n", C.c_int32),
+                ("row", C.c_int32), ("periodic", C.c_int32), ("reserved", C.c_int32)]
+
+
+class LmepWeights(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("nrows", C.c_int32), ("nleft", C.c_int32),
+                ("nright", C.c_int32), ("interior", C.c_void_p), ("classes", C.c_void_p),
+                ("pernode", C.c_void_p)]
+
+
+class LmepBC(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("reserved", C.c_int32), ("lo", C.c_double),
+                ("hi", C.c_double), ("dl", C.c_void_p), ("dr", C.c_void_p)]
+
+
+class LmepHalo(C.Structure):
+    _fields_ = [("left", C.c_void_p), ("right", C.c_void_p), ("hist_left", C.c_void_p),
+                ("hist_right", C.c_void_p), ("width", C.c_int64)]
+
+
+class LmepTuning(C.Structure):
+    _fields_ = [("tile", C.c_int32), ("ksteps", C.c_int32), ("ring", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+_lib = None
+
+
+def build(force: bool = False, jobs: int = 6) -> str:
+    """Compile liblmep.so in-tree with nvcc (-gencode arch=compute_100a,code=sm_100a)."""
+    if force or not os.path.exists(LIB_PATH):
+        subprocess.run(["make", "-s", f"-j{jobs}", "-C", CSRC], check=True)
+    return LIB_PATH
+
+
+def load(path: str | None = None):
+    """Load the library and declare the C signatures (no CUDA call is made)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise errors.LocalExpError(
+            f"liblmep.so not found at {p}; run __graft_entry__.build() (no CPU fallback exists)")
+    L = C.CDLL(p)
+    vp, i32, i64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    L.lmep_version.restype = C.c_int
+    L.lmep_version.argtypes = []
+    L.lmep_status_string.restype = C.c_char_p
+    L.lmep_status_string.argtypes = [C.c_int]
+    L.lmep_last_error.restype = C.c_char_p
+    L.lmep_last_error.argtypes = []
+    L.lmep_launch_count.restype = C.c_int64
+    L.lmep_launch_count.argtypes = []
+    L.lmep_fornberg.argtypes = [vp, vp, i64, C.c_int, C.c_int, i64, vp, vp]
+    L.lmep_expm.argtypes = [vp, C.c_int, i64, vp, vp, vp, vp]
+    L.lmep_harvest.argtypes = [C.c_int, C.c_int, C.c_int, vp, vp, vp, i64, vp, i64, vp, dbl, vp,
+                               C.c_int, vp, C.c_uint64, i64, C.c_int, vp, vp, vp, vp]
+    G, W, B, H, T = (C.POINTER(LmepGrid), C.POINTER(LmepWeights), C.POINTER(LmepBC),
+                     C.POINTER(LmepHalo), C.POINTER(LmepTuning))
+    L.lmep_step_linear.argtypes = [G, W, B, H, vp, vp, vp, i64, i32, T, vp, vp]
+    L.lmep_step_etdrk4.argtypes = [G, W, B, H, C.c_int, vp, vp, vp, i64, vp, i32, T, vp, vp]
+    L.lmep_step_etd2.argtypes = [G, W, B, H, C.c_int, dbl, vp, vp, vp, vp, vp, i64, i32, T, vp,
+                                 vp]
+    L.lmep_banded_matvec.argtypes = [G, W, H, vp, vp, i32, vp]
+    L.lmep_plan.argtypes = [G, C.c_int, C.c_int, i64, T]
+    L.lmep_rows_to_soa.argtypes = [vp, i64, C.c_int, vp, vp]
+    for name in EXPORTS:
+        if name not in ("lmep_version", "lmep_status_string", "lmep_last_error",
+                        "lmep_launch_count"):
+            getattr(L, name).restype = C.c_int
+    _lib = L
+    return L
+
+
+def lib():
+    return load()
+
+
+def device() -> torch.device:
+    """The CUDA device of the product path.  Fails loudly without one."""
+    if not torch.cuda.is_available():
+        raise errors.LocalExpError(
+            "the LMEP hot path runs on CUDA only (B200, sm_100a) and no CUDA device is visible")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def check(status: int, what: str, state=None, time=None) -> None:
+    """Map an lmep_status onto the localexp exception hierarchy."""
+    if status == LMEP_OK:
+        return
+    msg = f"{what}: {lib().lmep_status_string(status).decode()}"
+    if status == LMEP_CUDA_ERROR:
+        msg += f" ({lib().lmep_last_error().decode()})"
+    cls = errors.for_status(status)
+    if cls is errors.NonFinite:
+        raise errors.NonFinite(msg, state=state, time=time)
+    raise cls(msg)

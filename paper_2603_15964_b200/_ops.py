@@ -1,0 +1,409 @@
+"""Device-side building blocks shared by the public modules.
+
+Everything here drives liblmep.so on CUDA tensors; torch is used only for
+allocation, streams and tiny elementwise glue (e.g. the ordered linear
+combination of harvested rows that ``harvest.combine`` defines).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .errors import DimensionMismatch, DuplicateNodes, InvalidConfig, OrderTooHigh
+from .grid import StencilSet
+
+F64 = torch.float64
+
+
+def dev_f64(a) -> torch.Tensor:
+    """Contiguous float64 tensor on the product device (host arrays are copied)."""
+    d = nat.device()
+    if isinstance(a, torch.Tensor):
+        return a.to(device=d, dtype=F64).contiguous()
+    h = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if not h.flags.writeable:
+        h = h.copy()
+    return torch.as_tensor(h, device=d)
+
+
+def dev_i32(a) -> torch.Tensor:
+    return torch.as_tensor(np.ascontiguousarray(np.asarray(a, dtype=np.int32)), device=nat.device())
+
+
+def to_host(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# node-set validation (localop.py:69-74) -- host checks on n <= 32 numbers
+# ---------------------------------------------------------------------------
+def check_nodes(x: np.ndarray, max_order: int) -> None:
+    n = x.size
+    if not 0 <= max_order <= n - 1:
+        raise OrderTooHigh(f"derivative order {max_order} needs > {max_order} nodes, got {n}")
+    if n > nat.MAX_N:
+        raise DimensionMismatch(f"stencils larger than {nat.MAX_N} nodes are not supported")
+    if n > 1:
+        spread = float(x.max() - x.min())
+        if np.min(np.diff(np.sort(x))) <= 1e-14 * spread:
+            raise DuplicateNodes("two stencil nodes coincide within 1e-14 of the spread")
+
+
+def fornberg_dev(z: torch.Tensor, x: torch.Tensor, m: int) -> torch.Tensor:
+    """Batched Fornberg tables on the device: z [B], x [B, n] -> [B, m+1, n]."""
+    B, n = x.shape
+    out = torch.empty((B, m + 1, n), dtype=F64, device=x.device)
+    st = nat.lib().lmep_fornberg(nat.ptr(z), nat.ptr(x), n, n, m, B, nat.ptr(out),
+                                 nat.stream_handle())
+    nat.check(st, "lmep_fornberg")
+    return out
+
+
+def derivative_tables(coords: torch.Tensor, kmax: int) -> torch.Tensor:
+    """D^(k) matrices on each coordinate set: coords [T, n] -> [T, n(i), kmax+1, n(j)]
+    with row i evaluated at z = coords[t, i] (localop.diff_matrix, localop.py:99-108)."""
+    T, n = coords.shape
+    x = coords.repeat_interleave(n, dim=0).contiguous()        # item t*n+i uses coords[t]
+    z = coords.reshape(-1).contiguous()
+    return fornberg_dev(z, x, kmax).reshape(T, n, kmax + 1, n)
+
+
+def operator_tables(coords: torch.Tensor, terms) -> tuple[torch.Tensor, list, float]:
+    """Tables [T, nterms, n, n] of the spec's k>0 terms (in term order), their
+    coefficients and the reaction coefficient (localop.py:111-128)."""
+    kmax = max(k for k, _ in terms)
+    pos = [(k, c) for k, c in terms if k > 0]
+    c0 = 0.0
+    for k, c in terms:
+        if k == 0:
+            c0 = float(c)
+            break
+    T, n = coords.shape
+    if kmax == 0 or not pos:
+        return torch.zeros((T, 0, n, n), dtype=F64, device=coords.device), [], c0
+    tab = derivative_tables(coords, kmax)                       # [T, i, k, j]
+    sel = torch.stack([tab[:, :, k, :] for k, _ in pos], dim=1)  # [T, t, i, j]
+    return sel.contiguous(), [float(c) for _, c in pos], c0
+
+
+# ---------------------------------------------------------------------------
+# harvest (K1)
+# ---------------------------------------------------------------------------
+@dataclass
+class HarvestOut:
+    rows: torch.Tensor           # layout 0: [B, s, n]; layout 1: [s, n, B]
+    ms: torch.Tensor             # [B] int32: pade degree | squarings << 8
+    status: torch.Tensor         # [B] int32
+
+
+def harvest(n: int, s: int, delta_t: float, B: int, *, tables=None, table_idx=None, coef=None,
+            coef_stride=0, c0=None, c0_stride=0, L=None, rows=None, row_default=0,
+            frozen=None, frozen_default=0, layout=0) -> HarvestOut:
+    d = nat.device()
+    out = torch.empty((B, s, n) if layout == 0 else (s, n, B), dtype=F64, device=d)
+    ms = torch.empty(B, dtype=torch.int32, device=d)
+    status = torch.empty(B, dtype=torch.int32, device=d)
+    nterms = 0 if tables is None else int(tables.shape[1])
+    st = nat.lib().lmep_harvest(
+        n, s, nterms, nat.ptr(tables), nat.ptr(table_idx), nat.ptr(coef), int(coef_stride),
+        nat.ptr(c0), int(c0_stride), nat.ptr(L), float(delta_t), nat.ptr(rows), int(row_default),
+        nat.ptr(frozen), C.c_uint64(int(frozen_default)), B, layout, nat.ptr(out), nat.ptr(status),
+        nat.ptr(ms), nat.stream_handle())
+    nat.check(st, "lmep_harvest")
+    return HarvestOut(out, ms, status)
+
+
+def raise_on_status(h: HarvestOut, what="matrix exponential overflowed") -> None:
+    if int(h.status.abs().max().item() if h.status.numel() else 0) != 0:
+        nat.check(nat.LMEP_NONFINITE, what)
+
+
+def expm_batched(A: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """exp of A [B, d, d] on the device -> (E, status, ms)."""
+    B, d, _ = A.shape
+    if d > nat.MAX_DIM:
+        raise DimensionMismatch(f"expm supports d <= {nat.MAX_DIM}, got {d}")
+    E = torch.empty_like(A)
+    status = torch.empty(B, dtype=torch.int32, device=A.device)
+    ms = torch.empty(B, dtype=torch.int32, device=A.device)
+    st = nat.lib().lmep_expm(nat.ptr(A), d, B, nat.ptr(E), nat.ptr(status), nat.ptr(ms),
+                             nat.stream_handle())
+    nat.check(st, "lmep_expm")
+    return E, status, ms
+
+
+# ---------------------------------------------------------------------------
+# compact operator rows: the device form of one or more BandedPropagators
+# ---------------------------------------------------------------------------
+@dataclass
+class CompactRows:
+    """R operator rows on a StencilSet layout.
+
+    SHARED : interior [R, n] serves every node (periodic uniform grids)
+    CLASS  : interior [R, n] + classes [nleft+1+nright, R, n] (clamped ends)
+    PERNODE: pernode SoA [R, n, N]
+    """
+
+    layout: StencilSet
+    mode: int
+    interior: torch.Tensor | None = None
+    classes: torch.Tensor | None = None
+    nleft: int = 0
+    nright: int = 0
+    pernode: torch.Tensor | None = None
+    _host_interior: np.ndarray | None = field(default=None, repr=False)
+
+    @property
+    def R(self) -> int:
+        if self.mode == nat.W_PERNODE:
+            return int(self.pernode.shape[0])
+        return int(self.interior.shape[0])
+
+    @property
+    def n(self) -> int:
+        return self.layout.n
+
+    def host_interior(self) -> np.ndarray:
+        if self._host_interior is None and self.interior is not None:
+            self._host_interior = np.ascontiguousarray(to_host(self.interior))
+        return self._host_interior
+
+    def row(self, r: int) -> "CompactRows":
+        """The single-operator view of row r."""
+        if self.mode == nat.W_PERNODE:
+            return CompactRows(self.layout, self.mode, pernode=self.pernode[r:r + 1].contiguous())
+        cl = None if self.classes is None else self.classes[:, r:r + 1].contiguous()
+        return CompactRows(self.layout, self.mode, self.interior[r:r + 1].contiguous(), cl,
+                           self.nleft, self.nright)
+
+    def dense(self) -> torch.Tensor:
+        """Per-node rows [R, N, n] (the reference's (N, n) arrays, stacked)."""
+        N, n = self.layout.N, self.n
+        if self.mode == nat.W_PERNODE:
+            return self.pernode.permute(0, 2, 1).contiguous()
+        out = self.interior[:, None, :].expand(self.R, N, n).clone()
+        if self.mode == nat.W_CLASS:
+            if self.nleft:
+                out[:, :self.nleft] = self.classes[:self.nleft].permute(1, 0, 2)
+            if self.nright:
+                out[:, N - self.nright:] = self.classes[self.nleft + 1:].permute(1, 0, 2)
+        return out
+
+    def to_pernode(self) -> "CompactRows":
+        if self.mode == nat.W_PERNODE:
+            return self
+        return CompactRows(self.layout, nat.W_PERNODE,
+                           pernode=self.dense().permute(0, 2, 1).contiguous())
+
+    def with_classes(self, nleft: int, nright: int) -> "CompactRows":
+        """Widen the class table (extra boundary classes repeat interior rows)."""
+        if self.mode == nat.W_PERNODE:
+            return self
+        if self.mode == nat.W_CLASS and self.nleft == nleft and self.nright == nright:
+            return self
+        full = self.dense()                                   # [R, N, n]
+        N = self.layout.N
+        left = full[:, :nleft].permute(1, 0, 2)
+        right = full[:, N - nright:].permute(1, 0, 2)
+        mid = self.interior[None]
+        cl = torch.cat([left, mid, right], dim=0).contiguous()
+        return CompactRows(self.layout, nat.W_CLASS, self.interior, cl, nleft, nright)
+
+    # ctypes views -----------------------------------------------------------
+    def c_weights(self) -> nat.LmepWeights:
+        w = nat.LmepWeights()
+        w.mode = self.mode
+        w.nrows = self.R
+        w.nleft, w.nright = self.nleft, self.nright
+        if self.mode != nat.W_PERNODE:
+            w.interior = self.host_interior().ctypes.data
+        w.classes = nat.ptr(self.classes) if self.classes is not None else None
+        w.pernode = nat.ptr(self.pernode) if self.pernode is not None else None
+        return w
+
+
+def stack_rows(parts: list[CompactRows]) -> CompactRows:
+    """Concatenate single/multi-row CompactRows (same layout) into one bank."""
+    lay = parts[0].layout
+    if any(p.mode == nat.W_PERNODE for p in parts):
+        pn = [p.to_pernode().pernode for p in parts]
+        return CompactRows(lay, nat.W_PERNODE, pernode=torch.cat(pn, 0).contiguous())
+    if any(p.mode == nat.W_CLASS for p in parts):
+        nl = max(p.nleft for p in parts)
+        nr = max(p.nright for p in parts)
+        parts = [p.with_classes(nl, nr) for p in parts]
+        interior = torch.cat([p.interior for p in parts], 0).contiguous()
+        cl = torch.cat([p.classes for p in parts], 1).contiguous()
+        return CompactRows(lay, nat.W_CLASS, interior, cl, nl, nr)
+    return CompactRows(lay, nat.W_SHARED, torch.cat([p.interior for p in parts], 0).contiguous())
+
+
+def compress(dense: torch.Tensor, layout: StencilSet, max_classes: int = 64) -> CompactRows:
+    """(N, n) per-node rows -> the most compact exact representation."""
+    N = layout.N
+    w = dense.to(dtype=F64).contiguous()
+    mid = w[N // 2]
+    eq = (w == mid).all(dim=1)
+    eqh = to_host(eq)
+    if eqh.all():
+        mode = nat.W_SHARED if layout.periodic else nat.W_CLASS
+        if mode == nat.W_SHARED:
+            return CompactRows(layout, nat.W_SHARED, mid[None].clone())
+    if not layout.periodic:
+        idx = np.flatnonzero(eqh)
+        nl = int(idx[0])
+        nr = int(N - 1 - idx[-1])
+        if eqh[nl:N - nr].all() and nl + nr <= max_classes and nl + nr < N:
+            cl = torch.cat([w[:nl], mid[None], w[N - nr:]], 0)[:, None, :].contiguous()
+            return CompactRows(layout, nat.W_CLASS, mid[None].clone(), cl, nl, nr)
+    return CompactRows(layout, nat.W_PERNODE, pernode=w.t().contiguous()[None])
+
+
+def combine_rows(parts: list[CompactRows], coeffs) -> CompactRows:
+    """sum_i coeffs[i] * parts[i], accumulated from zeros in list order
+    (harvest.combine, harvest.py:225-235): two roundings per term like numpy."""
+    bank = stack_rows(parts)                      # aligns modes / classes
+    R = parts[0].R
+    acc_i = acc_c = acc_p = None
+    for i, c in enumerate(coeffs):
+        sl = slice(i * R, (i + 1) * R)
+        c = float(c)
+        if bank.mode == nat.W_PERNODE:
+            t = bank.pernode[sl] * c
+            acc_p = torch.zeros_like(t) + t if acc_p is None else acc_p + t
+        else:
+            t = bank.interior[sl] * c
+            acc_i = torch.zeros_like(t) + t if acc_i is None else acc_i + t
+            if bank.classes is not None:
+                t2 = bank.classes[:, sl] * c
+                acc_c = torch.zeros_like(t2) + t2 if acc_c is None else acc_c + t2
+    if bank.mode == nat.W_PERNODE:
+        return CompactRows(bank.layout, nat.W_PERNODE, pernode=acc_p.contiguous())
+    return CompactRows(bank.layout, bank.mode, acc_i.contiguous(),
+                       None if acc_c is None else acc_c.contiguous(), bank.nleft, bank.nright)
+
+
+# ---------------------------------------------------------------------------
+# stepping (K3-K5)
+# ---------------------------------------------------------------------------
+def c_grid(layout: StencilSet, off: int = 0, nloc: int | None = None) -> nat.LmepGrid:
+    g = nat.LmepGrid()
+    g.N = layout.N
+    g.off = off
+    g.nloc = layout.N if nloc is None else nloc
+    g.n = layout.n
+    g.row = layout.row
+    g.periodic = 1 if layout.periodic else 0
+    return g
+
+
+class BC:
+    """Boundary closure description for the step kernels."""
+
+    def __init__(self, kind: int = nat.BC_NONE, lo: float = 0.0, hi: float = 0.0, dl=None,
+                 dr=None):
+        self.kind, self.lo, self.hi = kind, float(lo), float(hi)
+        self.dl = None if dl is None else np.ascontiguousarray(np.asarray(dl, dtype=np.float64))
+        self.dr = None if dr is None else np.ascontiguousarray(np.asarray(dr, dtype=np.float64))
+
+    def c(self) -> nat.LmepBC:
+        b = nat.LmepBC()
+        b.kind = self.kind
+        b.lo, b.hi = self.lo, self.hi
+        b.dl = None if self.dl is None else self.dl.ctypes.data
+        b.dr = None if self.dr is None else self.dr.ctypes.data
+        return b
+
+
+def _tuning(tuning) -> nat.LmepTuning | None:
+    if tuning is None:
+        return None
+    t = nat.LmepTuning()
+    t.tile = int(tuning.get("tile", 0))
+    t.ksteps = int(tuning.get("ksteps", 0))
+    t.ring = int(tuning.get("ring", 0))
+    return t
+
+
+def step(scheme: int, rows: CompactRows, u: torch.Tensor, steps: int, *, bc: BC | None = None,
+         nl: int = nat.NL_NONE, exact: bool = True, hist: torch.Tensor | None = None,
+         delta_t: float = 0.0, nl0_out: torch.Tensor | None = None, tuning=None,
+         flag: torch.Tensor | None = None, out: torch.Tensor | None = None,
+         hist_out: torch.Tensor | None = None, scratch: torch.Tensor | None = None):
+    """Run `steps` steps of a scheme on the whole grid (single shard).
+    Returns the new u (and the new history for ETD2)."""
+    lay = rows.layout
+    g = c_grid(lay)
+    w = rows.c_weights()
+    b = (bc or BC()).c()
+    u = u.contiguous()
+    out = torch.empty_like(u) if out is None else out
+    flags = nat.FLAG_EXACT if exact else 0
+    tun = _tuning(tuning)
+    tp = C.byref(tun) if tun is not None else None
+    L = nat.lib()
+    s = nat.stream_handle()
+    fp = nat.ptr(flag)
+    if scheme == nat.SCH_LIN:
+        st = L.lmep_step_linear(C.byref(g), C.byref(w), C.byref(b), None, nat.ptr(u),
+                                nat.ptr(out), nat.ptr(scratch), int(steps), flags, tp, fp, s)
+        nat.check(st, "lmep_step_linear")
+        return out
+    if scheme == nat.SCH_ETDRK4:
+        st = L.lmep_step_etdrk4(C.byref(g), C.byref(w), C.byref(b), None, nl, nat.ptr(u),
+                                nat.ptr(out), nat.ptr(scratch), int(steps), nat.ptr(nl0_out),
+                                flags, tp, fp, s)
+        nat.check(st, "lmep_step_etdrk4")
+        return out
+    hist = hist.contiguous()
+    hist_out = torch.empty_like(hist) if hist_out is None else hist_out
+    st = L.lmep_step_etd2(C.byref(g), C.byref(w), C.byref(b), None, nl, float(delta_t),
+                          nat.ptr(u), nat.ptr(hist), nat.ptr(out), nat.ptr(hist_out),
+                          nat.ptr(scratch), int(steps), flags, tp, fp, s)
+    nat.check(st, "lmep_step_etd2")
+    return out, hist_out
+
+
+def rows_bank_for(layout: StencilSet, slots: dict[int, CompactRows], nrows: int) -> CompactRows:
+    """Operator bank with rows placed at their LMEP_ROW_* slots (missing = 0)."""
+    parts = []
+    proto = next(iter(slots.values()))
+    for r in range(nrows):
+        if r in slots:
+            parts.append(slots[r])
+        else:
+            z = CompactRows(layout, nat.W_SHARED, torch.zeros_like(proto.row(0).interior)) \
+                if proto.mode != nat.W_PERNODE else \
+                CompactRows(layout, nat.W_PERNODE, pernode=torch.zeros_like(proto.row(0).pernode))
+            parts.append(z)
+    return stack_rows(parts)
+
+
+def validate_members(members, weights_shape) -> StencilSet:
+    """Recognise the reference's (N, n) int64 member array as a StencilSet
+    (periodic wrap or clamped windows); anything else has no device path."""
+    m = members.detach().cpu().numpy() if isinstance(members, torch.Tensor) else np.asarray(members)
+    m = np.asarray(m, dtype=np.int64)
+    if m.ndim != 2 or tuple(m.shape) != tuple(weights_shape):
+        raise DimensionMismatch("weights and members must share an (N, n) shape")
+    N, n = m.shape
+    t = N // 2
+    row = int(t - m[t, 0])
+    for periodic in (True, False):
+        if not 0 <= row < n:
+            continue
+        cand = StencilSet(N, n, row, periodic)
+        if np.array_equal(cand.members_array(), m):
+            return cand
+    # periodic windows whose interior start wraps (row from modular offset)
+    row = int((t - m[t, 0]) % N)
+    if 0 <= row < n:
+        cand = StencilSet(N, n, row, True)
+        if np.array_equal(cand.members_array(), m):
+            return cand
+    raise InvalidConfig("members are not contiguous select_stencils windows; no device path")

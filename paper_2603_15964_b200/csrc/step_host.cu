@@ -1,0 +1,337 @@
+// step_host.cu -- host side of the step kernels: validation, launch planning,
+// temporal-blocking launch loop and the C-ABI entry points (lmep.h).
+#include "step.cuh"
+
+namespace lmep {
+
+// --------------------------------------------------------------------------
+// host side
+// --------------------------------------------------------------------------
+static int nslots(int sch) { return sch == SCH_LIN ? 2 : (sch == SCH_ETD2 ? 5 : 7); }
+
+// per-step dependency extent in stencil units
+static int step_ext(int sch, int nl)
+{
+    const int cv = nl == LMEP_NL_CONVECTIVE ? 1 : 0;
+    if (sch == SCH_LIN) return 1;
+    if (sch == SCH_ETD2) return 1 + cv;
+    return 4 + 4 * cv;
+}
+
+static int g_num_sms = 0;
+static int num_sms()
+{
+    if (g_num_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+            g_num_sms <= 0)
+            g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+static const int64_t kSmemBudget = 200 * 1024;  // bytes per CTA we allow ourselves
+
+int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded, bool pernode,
+                lmep_tuning &t)
+{
+    const int n = g.n, eL = g.row, eR = n - 1 - g.row;
+    const int ext = step_ext(sch, nl);
+    const int ns = nslots(sch);
+    const int P = pernode ? 1 : 5;
+    const int64_t rad = (int64_t)ext * (eL + eR);
+    // ring mode: whole periodic grid on one CTA for all steps
+    const int64_t ring_bytes = (int64_t)ns * (g.N + n + SLOT_PAD + P) * 8;
+    if (t.ring == 0 && t.tile == 0 && g.periodic && !sharded && g.nloc == g.N && !pernode &&
+        ring_bytes <= kSmemBudget && g.N >= 4 * n && g.N <= 8192 && steps > 1) {
+        t.ring = 1;
+    }
+    if (t.ring) {
+        if (!g.periodic || sharded || pernode || ring_bytes > kSmemBudget) return LMEP_INVALID_CONFIG;
+        t.tile = (int32_t)g.N;
+        t.ksteps = (int32_t)std::max<int64_t>(1, steps);
+        return LMEP_OK;
+    }
+    int64_t tile = t.tile, k = t.ksteps;
+    if (pernode && (sch == SCH_LIN || sharded)) k = 1;
+    const int64_t nsm = num_sms();
+    if (tile <= 0) {
+        if (pernode) tile = 2048;
+        else if (sch == SCH_LIN) tile = 4096;
+        else tile = 2048;
+        // small grids: enough tiles to cover the SMs
+        while (tile > 256 && (g.nloc + tile - 1) / tile < 2 * nsm) tile /= 2;
+        tile = std::min<int64_t>(tile, g.nloc);
+    }
+    if (k <= 0) {
+        const int64_t ntiles = (g.nloc + tile - 1) / tile;
+        k = 1;
+        if (sch == SCH_LIN && !pernode) k = 8;                  // HBM-bound: reuse u on chip
+        else if (ntiles < 2 * nsm) k = std::max<int64_t>(1, tile / (4 * std::max<int64_t>(rad, 1)));
+        k = std::min<int64_t>(k, std::max<int64_t>(steps, 1));
+        k = std::max<int64_t>(k, 1);
+    }
+    // respect the shared-memory budget
+    while (k > 1 && (int64_t)ns * (tile + k * rad + SLOT_PAD + P) * 8 > kSmemBudget) --k;
+    while (tile > 64 && (int64_t)ns * (tile + k * rad + SLOT_PAD + P) * 8 > kSmemBudget) tile /= 2;
+    if ((int64_t)ns * (tile + k * rad + SLOT_PAD + P) * 8 > kSmemBudget) return LMEP_INVALID_CONFIG;
+    if (!g.periodic && tile < 2 * n && tile < g.nloc) tile = std::min<int64_t>(g.nloc, 2 * n);
+    t.tile = (int32_t)tile;
+    t.ksteps = (int32_t)k;
+    t.ring = 0;
+    return LMEP_OK;
+}
+
+static int launch_step(int sch, bool exact, bool pernode, const StepParams &p, dim3 grid,
+                       size_t shm, cudaStream_t st)
+{
+    if (sch == SCH_LIN) return launch_scheme_lin(pernode, p, grid, shm, st);
+    if (sch == SCH_ETDRK4) return launch_scheme_etdrk4(exact, p, grid, shm, st);
+    return launch_scheme_etd2(exact, p, grid, shm, st);
+}
+
+struct StepCall {
+    int sch;
+    const lmep_grid *grid;
+    const lmep_weights *w;
+    const lmep_bc *bc;
+    const lmep_halo *halo;
+    int nl;
+    double dt;
+    const double *u_in, *q_in;
+    double *u_out, *q_out, *scratch;
+    int64_t steps;
+    int32_t flags;
+    const lmep_tuning *tuning;
+    int32_t *nonfinite;
+    double *nl0_out;
+    cudaStream_t stream;
+};
+
+int run_steps(const StepCall &c)
+{
+    if (!c.grid || !c.w) return LMEP_INVALID_CONFIG;
+    const lmep_grid &g = *c.grid;
+    const lmep_weights &w = *c.w;
+    if (g.n < 1 || g.n > LMEP_MAX_N || g.row < 0 || g.row >= g.n) return LMEP_DIMENSION;
+    if (g.N < g.n || g.nloc < 1 || g.off < 0 || g.off + g.nloc > g.N) return LMEP_DIMENSION;
+    if (c.steps < 0) return LMEP_INVALID_CONFIG;
+    if (c.nl < 0 || c.nl > 2) return LMEP_INVALID_CONFIG;
+    const bool pernode = w.mode == LMEP_W_PERNODE;
+    if (w.mode < 0 || w.mode > 2) return LMEP_INVALID_CONFIG;
+    const int need = c.sch == SCH_LIN ? 1 : (c.sch == SCH_ETD2 ? 3 : 6);
+    const int need_rows = c.nl == LMEP_NL_CONVECTIVE ? LMEP_ROW_D1 + 1 : need;
+    if (w.nrows < need_rows || w.nrows > LMEP_MAX_ROWS) return LMEP_DIMENSION;
+    if (!pernode && !w.interior) return LMEP_INVALID_CONFIG;
+    if (pernode && !w.pernode) return LMEP_INVALID_CONFIG;
+    if (w.mode == LMEP_W_CLASS) {
+        if (!w.classes || w.nleft < 0 || w.nright < 0 || w.nleft + w.nright >= g.N)
+            return LMEP_INVALID_CONFIG;
+    }
+    const bool sharded = c.halo && (c.halo->left || c.halo->right);
+    if (pernode && sharded && c.sch != SCH_LIN) return LMEP_INVALID_CONFIG;  // halo rows not held
+    if (!sharded && g.nloc != g.N) return LMEP_INVALID_CONFIG;
+    const int bck = c.bc ? c.bc->kind : LMEP_BC_NONE;
+    if (bck < 0 || bck > 2) return LMEP_INVALID_CONFIG;
+    if (bck != LMEP_BC_NONE && g.periodic) return LMEP_INVALID_CONFIG;
+    if (bck == LMEP_BC_NEUMANN && (!c.bc->dl || !c.bc->dr)) return LMEP_INVALID_CONFIG;
+    if (!g.periodic && g.N < 2 * g.n) return LMEP_INVALID_CONFIG;
+    if (c.steps == 0) {
+        cudaError_t e = cudaMemcpyAsync(c.u_out, c.u_in, g.nloc * 8, cudaMemcpyDeviceToDevice, c.stream);
+        if (e == cudaSuccess && c.sch == SCH_ETD2)
+            e = cudaMemcpyAsync(c.q_out, c.q_in, g.nloc * 8, cudaMemcpyDeviceToDevice, c.stream);
+        if (e != cudaSuccess) { set_last_error("cudaMemcpyAsync", e); return LMEP_CUDA_ERROR; }
+        return LMEP_OK;
+    }
+
+    lmep_tuning t{};
+    if (c.tuning) t = *c.tuning;
+    if (sharded) { t.ring = 0; }
+    int st = plan_launch(g, c.sch, c.nl, c.steps, sharded, pernode, t);
+    if (st) return st;
+
+    static StepParams p;  // host staging (the struct is large); calls are serialised per process
+    p = StepParams{};
+    p.N = g.N; p.off = g.off; p.nloc = g.nloc;
+    p.n = g.n; p.row = g.row; p.periodic = g.periodic ? 1 : 0; p.ring = t.ring;
+    p.eL = g.row; p.eR = g.n - 1 - g.row;
+    p.wmode = w.mode; p.nrows = w.nrows; p.nleft = w.nleft; p.nright = w.nright;
+    if (w.interior)
+        for (int r = 0; r < w.nrows; ++r)
+            for (int j = 0; j < g.n; ++j) p.wi[r][j] = w.interior[r * g.n + j];
+    p.wc = w.classes;
+    p.wp = w.pernode;
+    if (g.periodic) {
+        p.L_int = INT64_MIN / 4;
+        p.R_int = INT64_MAX / 4;
+    } else {
+        p.L_int = g.row;
+        p.R_int = g.N - (g.n - 1 - g.row);
+        if (w.mode == LMEP_W_CLASS) {
+            p.L_int = std::max<int64_t>(p.L_int, w.nleft);
+            p.R_int = std::min<int64_t>(p.R_int, g.N - w.nright);
+        }
+    }
+    p.nl = c.nl;
+    p.bc = bck;
+    if (c.bc) {
+        p.lo = c.bc->lo;
+        p.hi = c.bc->hi;
+        if (bck == LMEP_BC_NEUMANN)
+            for (int j = 0; j < g.n; ++j) { p.dl[j] = c.bc->dl[j]; p.dr[j] = c.bc->dr[j]; }
+    }
+    p.dt = c.dt;
+    p.ext = step_ext(c.sch, c.nl);
+    p.tile = t.tile;
+    const int P = pernode ? 1 : 5;
+    const int64_t rad = (int64_t)p.ext * (p.eL + p.eR);
+    p.slot_len = t.ring ? (g.N + g.n + SLOT_PAD + P) : (t.tile + (int64_t)t.ksteps * rad + SLOT_PAD + P);
+    p.slot_len = (p.slot_len + 3) & ~int64_t(3);
+    const size_t shm = (size_t)nslots(c.sch) * p.slot_len * 8;
+
+    // finiteness flag
+    int *flag = c.nonfinite;
+    int *own_flag = nullptr;
+    if (!flag) {
+        cudaError_t e = cudaMallocAsync((void **)&own_flag, sizeof(int), c.stream);
+        if (e != cudaSuccess) { set_last_error("cudaMallocAsync", e); return LMEP_CUDA_ERROR; }
+        flag = own_flag;
+    }
+    cudaMemsetAsync(flag, 0, sizeof(int), c.stream);
+    p.flag = flag;
+
+    const int64_t kmax = t.ksteps;
+    const int64_t nlaunch = (c.steps + kmax - 1) / kmax;
+    if (sharded) {
+        if (nlaunch != 1) return LMEP_INVALID_CONFIG;     // caller exchanges halos per launch
+        const int64_t need_w = c.steps * p.ext * std::max(p.eL, p.eR);
+        if (c.halo->width < need_w) return LMEP_INVALID_CONFIG;
+        if (c.sch == SCH_ETD2 && (!c.halo->hist_left && !c.halo->hist_right)) return LMEP_INVALID_CONFIG;
+    }
+    // scratch ping-pong
+    double *scr = c.scratch, *own_scr = nullptr;
+    const int64_t scr_need = (c.sch == SCH_ETD2 ? 2 : 1) * g.nloc;
+    if (nlaunch > 1 && !scr) {
+        cudaError_t e = cudaMallocAsync((void **)&own_scr, scr_need * 8, c.stream);
+        if (e != cudaSuccess) { set_last_error("cudaMallocAsync", e); return LMEP_CUDA_ERROR; }
+        scr = own_scr;
+    }
+    const dim3 grid(t.ring ? 1u : (unsigned)((g.nloc + t.tile - 1) / t.tile));
+    const double *src = c.u_in, *qsrc = c.q_in;
+    int rc = LMEP_OK;
+    int64_t done = 0;
+    for (int64_t L = 0; L < nlaunch; ++L) {
+        const int64_t k = std::min<int64_t>(kmax, c.steps - done);
+        // the last launch must land in u_out
+        const bool to_out = ((nlaunch - 1 - L) % 2) == 0;
+        double *dst = to_out ? c.u_out : scr;
+        double *qdst = c.sch == SCH_ETD2 ? (to_out ? c.q_out : scr + g.nloc) : nullptr;
+        p.ksteps = (int)k;
+        p.u_in = src;
+        p.u_out = dst;
+        p.q_in = qsrc;
+        p.q_out = qdst;
+        p.nl0_out = (L == 0) ? c.nl0_out : nullptr;
+        if (sharded) {
+            p.hl = c.halo->left; p.hr = c.halo->right;
+            p.qhl = c.halo->hist_left; p.qhr = c.halo->hist_right;
+            p.G = c.halo->width;
+        }
+        rc = launch_step(c.sch, (c.flags & LMEP_FLAG_EXACT) != 0, pernode, p, grid, shm, c.stream);
+        if (rc) break;
+        src = dst;
+        qsrc = qdst;
+        done += k;
+    }
+    if (own_scr) cudaFreeAsync(own_scr, c.stream);
+    if (own_flag) cudaFreeAsync(own_flag, c.stream);
+    return rc;
+}
+
+__global__ void rows_to_soa_kernel(const double *__restrict__ rows, int64_t N, int n,
+                                   double *__restrict__ soa)
+{
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= N * n) return;
+    const int64_t i = e / n;
+    const int j = (int)(e - i * n);
+    soa[(int64_t)j * N + i] = rows[e];
+}
+
+}  // namespace lmep
+
+using namespace lmep;
+
+extern "C" int lmep_step_linear(const lmep_grid *grid, const lmep_weights *w, const lmep_bc *bc,
+                                const lmep_halo *halo, const double *u_in, double *u_out,
+                                double *scratch, int64_t steps, int32_t flags,
+                                const lmep_tuning *tuning, int32_t *nonfinite, void *stream)
+{
+    StepCall c{};
+    c.sch = SCH_LIN; c.grid = grid; c.w = w; c.bc = bc; c.halo = halo; c.nl = 0;
+    c.u_in = u_in; c.u_out = u_out; c.scratch = scratch; c.steps = steps; c.flags = flags | LMEP_FLAG_EXACT;
+    c.tuning = tuning; c.nonfinite = nonfinite; c.stream = (cudaStream_t)stream;
+    return run_steps(c);
+}
+
+extern "C" int lmep_step_etdrk4(const lmep_grid *grid, const lmep_weights *w, const lmep_bc *bc,
+                                const lmep_halo *halo, int nl_kind, const double *u_in,
+                                double *u_out, double *scratch, int64_t steps, double *nl0_out,
+                                int32_t flags, const lmep_tuning *tuning, int32_t *nonfinite,
+                                void *stream)
+{
+    StepCall c{};
+    c.sch = SCH_ETDRK4; c.grid = grid; c.w = w; c.bc = bc; c.halo = halo; c.nl = nl_kind;
+    c.u_in = u_in; c.u_out = u_out; c.scratch = scratch; c.steps = steps; c.flags = flags;
+    c.tuning = tuning; c.nonfinite = nonfinite; c.nl0_out = nl0_out; c.stream = (cudaStream_t)stream;
+    return run_steps(c);
+}
+
+extern "C" int lmep_step_etd2(const lmep_grid *grid, const lmep_weights *w, const lmep_bc *bc,
+                              const lmep_halo *halo, int nl_kind, double delta_t,
+                              const double *u_in, const double *hist_in, double *u_out,
+                              double *hist_out, double *scratch, int64_t steps, int32_t flags,
+                              const lmep_tuning *tuning, int32_t *nonfinite, void *stream)
+{
+    if (!hist_in || !hist_out) return LMEP_INVALID_CONFIG;
+    if (!(delta_t > 0.0)) return LMEP_INVALID_CONFIG;
+    StepCall c{};
+    c.sch = SCH_ETD2; c.grid = grid; c.w = w; c.bc = bc; c.halo = halo; c.nl = nl_kind;
+    c.dt = delta_t; c.u_in = u_in; c.q_in = hist_in; c.u_out = u_out; c.q_out = hist_out;
+    c.scratch = scratch; c.steps = steps; c.flags = flags; c.tuning = tuning;
+    c.nonfinite = nonfinite; c.stream = (cudaStream_t)stream;
+    return run_steps(c);
+}
+
+extern "C" int lmep_banded_matvec(const lmep_grid *grid, const lmep_weights *w,
+                                  const lmep_halo *halo, const double *u, double *out,
+                                  int32_t flags, void *stream)
+{
+    lmep_tuning t{};
+    t.ksteps = 1;
+    StepCall c{};
+    c.sch = SCH_LIN; c.grid = grid; c.w = w; c.bc = nullptr; c.halo = halo; c.nl = 0;
+    c.u_in = u; c.u_out = out; c.steps = 1; c.flags = flags | LMEP_FLAG_EXACT; c.tuning = &t;
+    c.stream = (cudaStream_t)stream;
+    return run_steps(c);
+}
+
+extern "C" int lmep_plan(const lmep_grid *grid, int scheme, int nl_kind, int64_t steps,
+                         lmep_tuning *out)
+{
+    if (!grid || !out) return LMEP_INVALID_CONFIG;
+    if (scheme < 0 || scheme > 2) return LMEP_INVALID_CONFIG;
+    lmep_tuning t = *out;
+    int st = plan_launch(*grid, scheme, nl_kind, steps, grid->nloc != grid->N, false, t);
+    *out = t;
+    return st;
+}
+
+extern "C" int lmep_rows_to_soa(const double *rows, int64_t N, int n, double *soa, void *stream)
+{
+    if (N * n == 0) return LMEP_OK;
+    const int tpb = 256;
+    rows_to_soa_kernel<<<(unsigned)((N * n + tpb - 1) / tpb), tpb, 0, (cudaStream_t)stream>>>(rows, N, n, soa);
+    return launch_status("rows_to_soa_kernel");
+}

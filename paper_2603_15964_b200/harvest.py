@@ -1,0 +1,375 @@
+"""Weight harvesting on the device (reference: localexp/harvest.py:31-235).
+
+Reference flow per node (Python loop, harvest.py:135-159):
+    coords -> local_operator (Fornberg) -> build_augmented (sn x sn)
+           -> expm -> target row(s)
+Here the whole set is one batched launch of lmep_harvest: each warp
+assembles its node's (or stencil class's) operator from Fornberg tables in
+shared memory, exponentiates the reduced (n+s-1) x (n+s-1) transposed
+augmentation and writes the target rows.  Which items exist is decided by
+the stencil geometry instead of a byte-level cache:
+
+  periodic uniform grid               1 shared item            (W_SHARED)
+  uniform non-periodic grid,          row(+1) left classes,     (W_CLASS)
+    frozen nodes within {0, N-1}      1 interior, right classes
+  anything else (non-uniform grids,   one item per node         (W_PERNODE)
+    variable coefficients, ...)
+
+``BandedPropagator`` keeps the reference's fields; its (N, n) arrays are
+materialised only when someone reads them.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from . import _ops
+from .errors import DimensionMismatch, InvalidConfig
+from .grid import Grid, StencilSet, as_stencil_set
+from .localop import LinearOperatorSpec, VariableCoefficientSpec
+
+PERNODE_CHUNK = 1 << 20          # nodes per harvest launch on the per-node path
+
+
+@dataclass(frozen=True)
+class PhiWeightSet:
+    """w_lin plus the raw dt^j phi_j rows of one node (harvest.py:31-42)."""
+
+    delta_t: float
+    w_lin: np.ndarray
+    w_phi: tuple[np.ndarray, ...]
+
+
+class BandedPropagator:
+    """Global banded operator (harvest.py:45-70).
+
+    Construct it like the reference, ``BandedPropagator(weights, members,
+    periodic, delta_t)``, or internally from device rows.  ``weights`` and
+    ``members`` are read-only (N, n) numpy arrays produced on demand;
+    ``rows()`` is the compact device form the kernels consume.
+    """
+
+    def __init__(self, weights=None, members=None, periodic: bool = False, delta_t: float = 0.0,
+                 *, _rows: _ops.CompactRows | None = None):
+        self.periodic = bool(periodic)
+        self.delta_t = float(delta_t)
+        self._rows = _rows
+        self._w = self._m = None
+        if _rows is None:
+            w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
+            m = np.ascontiguousarray(np.asarray(members, dtype=np.int64))
+            if w.shape != m.shape or w.ndim != 2:
+                raise DimensionMismatch("weights and members must share an (N, n) shape")
+            w.setflags(write=False)
+            m.setflags(write=False)
+            self._w, self._m = w, m
+
+    @property
+    def weights(self) -> np.ndarray:
+        if self._w is None:
+            w = _ops.to_host(self._rows.dense()[0])
+            w.setflags(write=False)
+            self._w = w
+        return self._w
+
+    @property
+    def members(self) -> np.ndarray:
+        if self._m is None:
+            m = self._rows.layout.members_array()
+            m.setflags(write=False)
+            self._m = m
+        return self._m
+
+    @property
+    def layout(self) -> StencilSet:
+        if self._rows is not None:
+            return self._rows.layout
+        return _ops.validate_members(self._m, self._w.shape)
+
+    def rows(self) -> _ops.CompactRows:
+        if self._rows is None:
+            lay = _ops.validate_members(self._m, self._w.shape)
+            self._rows = _ops.compress(_ops.dev_f64(self._w), lay)
+        return self._rows
+
+    @property
+    def N(self) -> int:
+        return self.layout.N if self._w is None else self._w.shape[0]
+
+    @property
+    def n(self) -> int:
+        return self.layout.n if self._w is None else self._w.shape[1]
+
+    def __repr__(self) -> str:
+        return f"BandedPropagator(N={self.N}, n={self.n}, periodic={self.periodic}, dt={self.delta_t})"
+
+
+# ---------------------------------------------------------------------------
+# single-operator API (harvest.py:73-121)
+# ---------------------------------------------------------------------------
+def _explicit(L_n, delta_t, s, target_row, frozen_rows=()):
+    L = np.asarray(L_n, dtype=np.float64)
+    if L.ndim != 2 or L.shape[0] != L.shape[1]:
+        raise DimensionMismatch(f"expected a square operator, got shape {L.shape}")
+    n = L.shape[0]
+    if not 0 <= target_row < n:
+        raise DimensionMismatch(f"target row {target_row} out of range for n={n}")
+    if not 1 <= s <= 6:
+        raise ValueError(f"augmentation depth must be in [1, 6], got {s}")
+    if n + s - 1 > nat.MAX_DIM:
+        raise DimensionMismatch(f"n + s - 1 must be <= {nat.MAX_DIM}")
+    mask = 0
+    for j in frozen_rows:
+        mask |= 1 << int(j)
+    h = _ops.harvest(n, s, delta_t, 1, L=_ops.dev_f64(L[None]), row_default=int(target_row),
+                     frozen_default=mask)
+    _ops.raise_on_status(h)
+    return _ops.to_host(h.rows[0])
+
+
+def harvest_propagator(L_n, delta_t: float, target_row: int) -> np.ndarray:
+    """Row target_row of exp(delta_t L_n) (harvest.py:73-79)."""
+    return _explicit(L_n, delta_t, 1, target_row)[0].copy()
+
+
+def build_augmented(L_n, s: int) -> np.ndarray:
+    """The reference's sn x sn block companion matrix (harvest.py:82-94).
+    Kept for API parity; the device harvest uses the reduced form."""
+    if not 1 <= s <= 6:
+        raise ValueError(f"augmentation depth must be in [1, 6], got {s}")
+    L = torch.as_tensor(np.asarray(L_n, dtype=np.float64))
+    n = L.shape[0]
+    A = torch.zeros((s * n, s * n), dtype=torch.float64)
+    A[:n, :n] = L
+    eye = torch.eye(n, dtype=torch.float64)
+    for i in range(s - 1):
+        A[i * n:(i + 1) * n, (i + 1) * n:(i + 2) * n] = eye
+    return A.numpy()
+
+
+def harvest_phi_weights(L_n, delta_t: float, s: int, target_row: int,
+                        frozen_rows=()) -> PhiWeightSet:
+    """w_lin and the raw dt^j phi_j rows from one exponential (harvest.py:97-121)."""
+    w = _explicit(L_n, delta_t, s, target_row, frozen_rows)
+    return PhiWeightSet(delta_t=delta_t, w_lin=w[0].copy(),
+                        w_phi=tuple(w[j].copy() for j in range(1, s)))
+
+
+# ---------------------------------------------------------------------------
+# grid-wide harvest (harvest.py:135-210)
+# ---------------------------------------------------------------------------
+@dataclass
+class _Plan:
+    mode: int
+    coords: torch.Tensor          # [T, n] local coordinates (T=1 shared, classes, or N)
+    rows: np.ndarray              # [T] target rows
+    masks: np.ndarray             # [T] frozen bitmasks (uint64)
+    nleft: int = 0
+    nright: int = 0
+
+
+def _frozen_masks(sset: StencilSet, t: np.ndarray, frozen: list[int]) -> np.ndarray:
+    masks = np.zeros(t.size, dtype=np.uint64)
+    if not frozen:
+        return masks
+    start = sset.starts(t)
+    for f in frozen:
+        off = (f - start) % sset.N if sset.periodic else f - start
+        hit = (off >= 0) & (off < sset.n)
+        masks[hit] |= (np.uint64(1) << off[hit].astype(np.uint64))
+    return masks
+
+
+def _coords_for(grid: Grid, sset: StencilSet, t: np.ndarray) -> torch.Tensor:
+    """Local coordinates of the windows of nodes t (harvest.py:124-132)."""
+    trow = sset.target_rows(t)
+    off = np.arange(sset.n, dtype=np.int64)[None, :] - trow[:, None]
+    if grid.periodic or grid.uniform_spacing is not None:
+        h = grid.spacing if grid.periodic else grid.uniform_spacing
+        return _ops.dev_f64(off.astype(np.float64) * h)
+    nodes = _ops.dev_f64(grid.nodes)
+    tt = torch.as_tensor(t, device=nodes.device)
+    start = torch.as_tensor(sset.starts(t), device=nodes.device)
+    m = start[:, None] + torch.arange(sset.n, device=nodes.device)[None, :]
+    return (nodes[m] - nodes[tt][:, None]).contiguous()
+
+
+def _plan(grid: Grid, sset: StencilSet, frozen_nodes=(), force_pernode=False) -> _Plan:
+    N, n, row = sset.N, sset.n, sset.row
+    frozen = sorted({int(i) for i in frozen_nodes})
+    if grid.periodic and not frozen and not force_pernode:
+        t = np.array([0])
+        return _Plan(nat.W_SHARED, _coords_for(grid, sset, t), np.array([row]),
+                     np.zeros(1, np.uint64))
+    if (not grid.periodic and grid.uniform_spacing is not None and set(frozen) <= {0, N - 1}
+            and not force_pernode and N >= 2 * n + 2):
+        nl = row + (1 if 0 in frozen else 0)
+        nr = (n - 1 - row) + (1 if N - 1 in frozen else 0)
+        t = np.concatenate([np.arange(nl), [N // 2], np.arange(N - nr, N)]).astype(np.int64)
+        return _Plan(nat.W_CLASS, _coords_for(grid, sset, t), sset.target_rows(t),
+                     _frozen_masks(sset, t, frozen), nl, nr)
+    t = np.arange(N, dtype=np.int64)
+    coords = _coords_for(grid, sset, np.array([0]) if grid.periodic else t)
+    return _Plan(nat.W_PERNODE, coords, sset.target_rows(t), _frozen_masks(sset, t, frozen))
+
+
+def _rows_from(plan: _Plan, sset: StencilSet, out: torch.Tensor) -> _ops.CompactRows:
+    if plan.mode == nat.W_SHARED:
+        return _ops.CompactRows(sset, nat.W_SHARED, out[0].contiguous())
+    if plan.mode == nat.W_CLASS:
+        nl = plan.nleft
+        return _ops.CompactRows(sset, nat.W_CLASS, out[nl].contiguous(), out.contiguous(), nl,
+                                plan.nright)
+    return _ops.CompactRows(sset, nat.W_PERNODE, pernode=out.contiguous())
+
+
+def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
+                    frozen_nodes=(), stats: dict | None = None) -> _ops.CompactRows:
+    """Harvest w_lin and the raw dt^j phi_j rows (R = s) for the whole grid."""
+    if not 1 <= s <= 6:
+        raise ValueError(f"augmentation depth must be in [1, 6], got {s}")
+    n = sset.n
+    if n + s - 1 > nat.MAX_DIM:
+        raise DimensionMismatch(f"n + s - 1 must be <= {nat.MAX_DIM}")
+    varcoef = isinstance(spec, VariableCoefficientSpec)
+    plan = _plan(grid, sset, frozen_nodes, force_pernode=varcoef)
+    terms = tuple((k, 1.0) for k in spec.orders) if varcoef else spec.terms
+    if max(k for k, _ in terms) > n - 1:
+        from .errors import OrderTooHigh
+        raise OrderTooHigh(f"operator order {max(k for k, _ in terms)} not representable on {n} nodes")
+    _ops.check_nodes(_ops.to_host(plan.coords[0]), max(k for k, _ in terms))
+    d = nat.device()
+    if plan.mode != nat.W_PERNODE:
+        tables, cf, c0 = _ops.operator_tables(plan.coords, terms)
+        T = plan.coords.shape[0]
+        h = _ops.harvest(n, s, delta_t, T, tables=tables,
+                         table_idx=_ops.dev_i32(np.arange(T)), coef=_ops.dev_f64(cf or [0.0]),
+                         coef_stride=0, c0=_ops.dev_f64([c0]), c0_stride=0,
+                         rows=_ops.dev_i32(plan.rows),
+                         frozen=torch.as_tensor(plan.masks.view(np.int64), device=d), layout=0)
+        _ops.raise_on_status(h)
+        if stats is not None:
+            stats.setdefault("ms", []).append(h.ms)
+        return _rows_from(plan, sset, h.rows)
+    # per-node path: one item per node, chunked
+    N = sset.N
+    out = torch.empty((s, n, N), dtype=torch.float64, device=d)
+    shared_coords = plan.coords.shape[0] == 1
+    if shared_coords:
+        tables, cf, c0 = _ops.operator_tables(plan.coords, terms)
+    if varcoef:
+        coef_all = _ops.dev_f64(spec.coef)
+        react = None if spec.reaction is None else _ops.dev_f64(spec.reaction)
+    rows_all = _ops.dev_i32(plan.rows)
+    masks_all = torch.as_tensor(plan.masks.view(np.int64), device=d)
+    for a in range(0, N, PERNODE_CHUNK):
+        b = min(N, a + PERNODE_CHUNK)
+        B = b - a
+        if not shared_coords:
+            tables, cf, c0 = _ops.operator_tables(plan.coords[a:b], terms)
+            tidx = _ops.dev_i32(np.arange(B))
+        else:
+            tidx = None
+        if varcoef:
+            coef, cs = coef_all[a:b].contiguous(), len(spec.orders)
+            c0t, c0s = (None, 0) if react is None else (react[a:b].contiguous(), 1)
+        else:
+            coef, cs = _ops.dev_f64(cf or [0.0]), 0
+            c0t, c0s = _ops.dev_f64([c0]), 0
+        h = _ops.harvest(n, s, delta_t, B, tables=tables, table_idx=tidx, coef=coef,
+                         coef_stride=cs, c0=c0t, c0_stride=c0s, rows=rows_all[a:b].contiguous(),
+                         frozen=masks_all[a:b].contiguous(), layout=1)
+        _ops.raise_on_status(h)
+        if stats is not None:
+            stats.setdefault("ms", []).append(h.ms)
+        out[:, :, a:b] = h.rows
+    return _ops.CompactRows(sset, nat.W_PERNODE, pernode=out)
+
+
+def derivative_compact(grid: Grid, sset: StencilSet, k: int) -> _ops.CompactRows:
+    """Banded k-th derivative rows: fornberg_weights(0, coords, k)[k] per stencil
+    (timestep.assemble_derivative, timestep.py:218-237)."""
+    plan = _plan(grid, sset, ())
+    T, n = plan.coords.shape
+    _ops.check_nodes(_ops.to_host(plan.coords[0]), k)
+    z = torch.zeros(T, dtype=torch.float64, device=plan.coords.device)
+    tab = _ops.fornberg_dev(z, plan.coords, k)[:, k, :]          # [T, n]
+    if plan.mode == nat.W_PERNODE:
+        if T == 1:
+            tab = tab.expand(sset.N, n)
+        return _ops.CompactRows(sset, nat.W_PERNODE, pernode=tab.t().contiguous()[None])
+    return _rows_from(plan, sset, tab[:, None, :].contiguous())
+
+
+def assemble_global(grid: Grid, stencils, spec, delta_t: float,
+                    frozen_nodes=()) -> BandedPropagator:
+    """Banded linear propagator for one time step (harvest.py:162-178)."""
+    sset = as_stencil_set(grid, stencils)
+    rows = harvest_compact(grid, sset, spec, delta_t, 1, frozen_nodes)
+    return BandedPropagator(periodic=grid.periodic, delta_t=delta_t, _rows=rows)
+
+
+def assemble_global_phi(grid: Grid, stencils, spec, delta_t: float, s: int,
+                        frozen_nodes=()) -> list[BandedPropagator]:
+    """[exp, dt*phi_1, ..., dt^(s-1)*phi_(s-1)] banded operators (harvest.py:181-210)."""
+    sset = as_stencil_set(grid, stencils)
+    rows = harvest_compact(grid, sset, spec, delta_t, s, frozen_nodes)
+    return [BandedPropagator(periodic=grid.periodic, delta_t=delta_t, _rows=rows.row(j))
+            for j in range(s)]
+
+
+def apply(prop: BandedPropagator, u):
+    """out[i] = sum_j w[i, j] u[members[i, j]] (harvest.py:213-222), on the
+    device in ascending order.  Complex vectors are applied part by part."""
+    as_torch = isinstance(u, torch.Tensor)
+    if as_torch and u.is_complex() or (not as_torch and np.iscomplexobj(u)):
+        ur = u.real if as_torch else np.real(u)
+        ui = u.imag if as_torch else np.imag(u)
+        re, im = apply(prop, ur), apply(prop, ui)
+        return torch.complex(re, im) if as_torch else re + 1j * im
+    shape = tuple(u.shape)
+    if shape != (prop.N,):
+        raise DimensionMismatch(f"expected a vector of length {prop.N}, got shape {shape}")
+    rows = prop.rows()
+    ut = _ops.dev_f64(u)
+    out = torch.empty_like(ut)
+    import ctypes as C
+    g = _ops.c_grid(rows.layout)
+    w = rows.c_weights()
+    st = nat.lib().lmep_banded_matvec(C.byref(g), C.byref(w), None, nat.ptr(ut), nat.ptr(out),
+                                      nat.FLAG_EXACT, nat.stream_handle())
+    nat.check(st, "lmep_banded_matvec")
+    return out if as_torch else _ops.to_host(out)
+
+
+def combine(props: list[BandedPropagator], coeffs) -> BandedPropagator:
+    """sum_i coeffs[i] props[i] from zeros in list order (harvest.py:225-235)."""
+    base = props[0]
+    lay = base.layout
+    for p in props[1:]:
+        pl = p.layout
+        if (pl.N, pl.n, pl.row, pl.periodic) != (lay.N, lay.n, lay.row, lay.periodic):
+            raise DimensionMismatch("cannot combine operators with different stencils")
+    rows = _ops.combine_rows([p.rows() for p in props], list(coeffs))
+    return BandedPropagator(periodic=base.periodic, delta_t=base.delta_t, _rows=rows)
+
+
+def weight_table_json(stencils, rows: list[PhiWeightSet]) -> str:
+    """17-significant-digit JSON weight table (harvest.py:238-265)."""
+    import json
+
+    st = list(stencils)
+    if len(st) != len(rows):
+        raise DimensionMismatch("one weight set per stencil required")
+    g = lambda x: float(format(float(x), ".17g"))  # noqa: E731
+    doc = {"delta_t": g(rows[0].delta_t), "N": len(st), "n": st[0].n,
+           "s": len(rows[0].w_phi) + 1,
+           "nodes": [{"index": int(s_.target), "target_row": int(s_.target_row),
+                      "members": [int(m) for m in s_.members],
+                      "w_lin": [g(w) for w in r.w_lin],
+                      "w_phi": [[g(w) for w in v] for v in r.w_phi]} for s_, r in zip(st, rows)]}
+    return json.dumps(doc, separators=(", ", ": "))

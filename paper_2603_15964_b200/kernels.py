@@ -1,0 +1,110 @@
+"""Drop-in replacements for the reference's numba stepping loops
+(localexp/kernels.py:17-132), running the fused CUDA step kernels.
+
+The signatures are the reference's: (N, n) weight arrays, an (N, n) int64
+member array, and plain scalars.  Member arrays must be the contiguous
+windows ``select_stencils`` produces (periodic wrap or clamped ends); they
+are recognised once and the kernels derive indices arithmetically.  Weight
+arrays are compressed to shared / class / per-node device rows.
+
+Keyword extensions (not in the reference): ``exact`` (default True:
+bit-identical to numba's unfused ascending arithmetic; False: FMA),
+``bc=("neumann", dl, dr)`` for the zero-gradient closure, and
+``tuning`` (launch shape).  Inputs are never modified; numpy in -> numpy
+out, torch in -> torch out.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from . import _ops
+
+NL_NONE = nat.NL_NONE
+NL_CONVECTIVE = nat.NL_CONVECTIVE   # -u * (D1 u)
+NL_CUBIC = nat.NL_CUBIC             # -u**3
+
+
+def _dense(a) -> torch.Tensor:
+    return _ops.dev_f64(a)
+
+
+def _bc(pin, pin_lo, pin_hi, bc) -> _ops.BC:
+    if bc is not None:
+        if bc[0] == "neumann":
+            return _ops.BC(nat.BC_NEUMANN, dl=bc[1], dr=bc[2])
+        if bc[0] == "dirichlet":
+            return _ops.BC(nat.BC_DIRICHLET, bc[1], bc[2])
+        raise ValueError(f"unknown boundary closure {bc[0]!r}")
+    if pin:
+        return _ops.BC(nat.BC_DIRICHLET, pin_lo, pin_hi)
+    return _ops.BC()
+
+
+def _bank(layout, named: dict[int, object]) -> _ops.CompactRows:
+    rows = {r: _ops.compress(_dense(w), layout) for r, w in named.items()}
+    R = max(rows) + 1
+    return _ops.rows_bank_for(layout, rows, R)
+
+
+def _ret(x: torch.Tensor, like):
+    return x if isinstance(like, torch.Tensor) else _ops.to_host(x)
+
+
+def banded_matvec(weights, members, u, out) -> None:
+    """out[i] = sum_j weights[i, j] u[members[i, j]] (kernels.py:23-29); writes out."""
+    from .harvest import BandedPropagator, apply
+    lay = _ops.validate_members(members, np.shape(weights))
+    prop = BandedPropagator(periodic=lay.periodic,
+                            _rows=_ops.compress(_dense(weights), lay))
+    r = apply(prop, u)
+    if isinstance(out, torch.Tensor):
+        out.copy_(r if isinstance(r, torch.Tensor) else torch.as_tensor(r))
+    else:
+        out[...] = r if isinstance(r, np.ndarray) else _ops.to_host(r)
+
+
+def run_linear(weights, members, u0, steps, pin=False, pin_lo=0.0, pin_hi=0.0, *, bc=None,
+               tuning=None):
+    """steps x (banded mat-vec, optional Dirichlet pin) (kernels.py:33-43).
+    Always exact (this step is bandwidth-bound; FMA would buy nothing)."""
+    lay = _ops.validate_members(members, np.shape(weights))
+    bank = _bank(lay, {nat.ROW_W: weights})
+    u = _dense(u0)
+    out = _ops.step(nat.SCH_LIN, bank, u, int(steps), bc=_bc(pin, pin_lo, pin_hi, bc),
+                    exact=True, tuning=tuning)
+    return _ret(out, u0)
+
+
+def run_etdrk4(w_full, w_alpha, w_beta, w_gamma, w_half, w_p1h, d1w, members, kind, u0, steps,
+               pin=False, pin_lo=0.0, pin_hi=0.0, *, exact=True, bc=None, tuning=None,
+               nl0_out=None):
+    """Fused four-stage exponential RK loop (kernels.py:62-132)."""
+    lay = _ops.validate_members(members, np.shape(w_full))
+    named = {nat.ROW_W: w_full, nat.ROW_ALPHA: w_alpha, nat.ROW_BETA: w_beta,
+             nat.ROW_GAMMA: w_gamma, nat.ROW_WHALF: w_half, nat.ROW_P1HALF: w_p1h}
+    if int(kind) == NL_CONVECTIVE:
+        named[nat.ROW_D1] = d1w
+    bank = _bank(lay, named)
+    u = _dense(u0)
+    out = _ops.step(nat.SCH_ETDRK4, bank, u, int(steps), bc=_bc(pin, pin_lo, pin_hi, bc),
+                    nl=int(kind), exact=exact, tuning=tuning, nl0_out=nl0_out)
+    return _ret(out, u0)
+
+
+def run_etd2(ops, d1w, members, kind, u0, hist, steps, delta_t, pin=False, pin_lo=0.0,
+             pin_hi=0.0, *, exact=True, bc=None, tuning=None):
+    """Exponential multistep, order 2, after warm-up (timestep.py:187-215 with
+    s=2): ops = (exp, dt*phi1, dt^2*phi2) raw rows, hist = N_{k-1}.
+    Returns (u, N_last).  Extension: the reference runs this step in Python."""
+    lay = _ops.validate_members(members, np.shape(ops[0]))
+    named = {nat.ROW_W: ops[0], nat.ROW_ALPHA: ops[1], nat.ROW_BETA: ops[2]}
+    if int(kind) == NL_CONVECTIVE:
+        named[nat.ROW_D1] = d1w
+    bank = _bank(lay, named)
+    u, q = _ops.step(nat.SCH_ETD2, bank, _dense(u0), int(steps),
+                     bc=_bc(pin, pin_lo, pin_hi, bc), nl=int(kind), exact=exact,
+                     hist=_dense(hist), delta_t=float(delta_t), tuning=tuning)
+    return _ret(u, u0), _ret(q, u0)

@@ -1,0 +1,376 @@
+"""GPU parity: the CUDA path (through liblmep.so's C ABI) against the golden
+vectors of the live reference and the C oracle.
+
+Tolerances (BASELINE.json north_star): harvested weights 1e-12 relative,
+final solutions 1e-10 relative L2.  EXACT-mode steps must be bit-identical
+to the reference's numba loops (same operand order, separate roundings).
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from tests.conftest import rel_inf, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+W_TOL = 1e-12
+U_TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def lx():
+    import paper_2603_15964_b200 as m
+    m._native.device()
+    return m
+
+
+def _rows_rel(W, ref):
+    worst = 0.0
+    for r in range(ref.shape[0]):
+        den = np.abs(ref[r]).max()
+        worst = max(worst, np.abs(W[r] - ref[r]).max() / (den if den > 0 else 1.0))
+    return worst
+
+
+# --------------------------------------------------------------------- harvest
+def test_fornberg_bitwise(lx, golden):
+    for i in range(int(golden["forn_count"])):
+        c = lx.fornberg_weights(float(golden[f"forn{i}_z"]), golden[f"forn{i}_x"],
+                                int(golden[f"forn{i}_m"]))
+        assert np.array_equal(c, golden[f"forn{i}_c"]), i
+
+
+def test_local_operator_bitwise(lx, golden):
+    for i in range(int(golden["lop_count"])):
+        terms = tuple(zip(golden[f"lop{i}_k"].tolist(), golden[f"lop{i}_c"].tolist()))
+        L = lx.local_operator(golden[f"lop{i}_x"], lx.LinearOperatorSpec(terms))
+        assert np.array_equal(L, golden[f"lop{i}_L"]), i
+
+
+def test_expm_matches_reference(lx, golden):
+    cnt = int(golden["ex_count"])
+    worst = 0.0
+    for i in range(cnt):
+        E = lx.expm(golden[f"ex{i}_A"])
+        err = rel_inf(E, golden[f"ex{i}_E"])
+        worst = max(worst, err)
+        assert err < W_TOL, (i, err)
+    print("expm worst", worst)
+
+
+def test_expm_batched_matches_oracle(lx, orc):
+    rng = np.random.default_rng(7)
+    for d in (3, 8, 13, 16, 24, 32):
+        A = rng.standard_normal((40, d, d)) * rng.uniform(0.01, 6.0, (40, 1, 1)) / math.sqrt(d)
+        E = lx.expm(torch.as_tensor(A)).cpu().numpy()
+        for b in range(40):
+            assert rel_inf(E[b], orc.expm(A[b])) < W_TOL, (d, b)
+
+
+def test_expm_nonfinite(lx):
+    A = np.eye(4)
+    A[1, 2] = np.nan
+    with pytest.raises(lx.NonFinite):
+        lx.expm(A)
+    with pytest.raises(lx.NonFinite):
+        lx.expm(np.eye(3) * 1e6)
+
+
+def test_harvest_phi_weights_vs_reference(lx, golden):
+    for i in range(int(golden["hv_count"])):
+        dt, s, row = golden[f"hv{i}_meta"]
+        s, row = int(s), int(row)
+        fm = int(golden[f"hv{i}_frozen"])
+        frozen = [j for j in range(64) if (fm >> j) & 1]
+        ws = lx.harvest_phi_weights(golden[f"hv{i}_L"], dt, s, row, frozen)
+        W = np.vstack([ws.w_lin] + list(ws.w_phi))
+        assert _rows_rel(W, golden[f"hv{i}_w"]) < W_TOL, i
+
+
+def test_harvest_errors(lx):
+    L = np.eye(5)
+    with pytest.raises(lx.DimensionMismatch):
+        lx.harvest_propagator(L, 0.1, 5)
+    with pytest.raises(ValueError):
+        lx.harvest_phi_weights(L, 0.1, 7, 2)
+    with pytest.raises(lx.OrderTooHigh):
+        lx.fornberg_weights(0.0, [0.0, 1.0, 2.0], 3)
+    with pytest.raises(lx.DuplicateNodes):
+        lx.fornberg_weights(0.0, [0.0, 1.0, 1.0], 1)
+
+
+def test_harvest_closed_forms(lx):
+    # Lax-Wendroff centre row / FTCS row
+    for nu in (0.1, 0.5, 0.9, 1.3):
+        L = lx.local_operator(np.array([-1.0, 0.0, 1.0]), lx.LinearOperatorSpec(((1, -1.0),)))
+        w = lx.harvest_propagator(L, nu, 1)
+        assert np.abs(w - [nu * (1 + nu) / 2, 1 - nu**2, nu * (nu - 1) / 2]).max() < 1e-12
+        L = lx.local_operator(np.array([-1.0, 0.0, 1.0]), lx.LinearOperatorSpec(((2, 1.0),)))
+        w = lx.harvest_propagator(L, nu, 1)
+        assert np.abs(w - [nu, 1 - 2 * nu, nu]).max() < 1e-12
+
+
+def test_phi_rows_at_zero_operator(lx):
+    # L = 0: w_phi_j = dt^j / j! e_r
+    dt = 0.37
+    ws = lx.harvest_phi_weights(np.zeros((5, 5)), dt, 4, 2)
+    for j, w in enumerate(ws.w_phi, start=1):
+        e = np.zeros(5)
+        e[2] = dt**j / math.factorial(j)
+        assert np.abs(w - e).max() < 1e-15
+
+
+def test_c1_assemble_global(lx, golden):
+    from paper_2603_15964_b200 import configs
+    w = configs.c1()
+    g = lx.make_periodic_grid(w.N, w.x_min, w.x_max)
+    st = lx.select_stencils(g, w.n, lx.StencilPolicy.ONE_SIDED_UPWIND)
+    prop = lx.assemble_global(g, st, lx.LinearOperatorSpec(w.terms), w.delta_t)
+    assert prop.weights.shape == (w.N, w.n)
+    assert rel_inf(prop.weights[0], golden["c1_w"]) < W_TOL
+    assert np.array_equal(prop.weights[5], prop.weights[700])
+
+
+def test_c4_class_harvest_vs_reference_rows(lx, golden):
+    """Boundary classes with frozen ends (C4 family) vs reference rows."""
+    W = golden["c4_weights"]           # w, alpha, beta, gamma, wh, p1h  (N, n) each
+    N, n = W.shape[1], W.shape[2]
+    from paper_2603_15964_b200 import configs
+    w4 = configs.c4(N=N, steps=40)
+    g = lx.make_uniform_grid(N, -1.0, 1.0)
+    st = lx.select_stencils(g, n, lx.StencilPolicy.CENTERED)
+    spec = lx.LinearOperatorSpec(w4.terms)
+    of = lx.assemble_global_phi(g, st, spec, w4.delta_t, 4, frozen_nodes=(0, N - 1))
+    oh = lx.assemble_global_phi(g, st, spec, w4.delta_t / 2, 2, frozen_nodes=(0, N - 1))
+    ops = lx.etdrk4_operators(of, oh)
+    for k in range(6):
+        den = np.abs(W[k]).max(axis=1)
+        err = (np.abs(ops[k].weights - W[k]).max(axis=1) / np.where(den > 0, den, 1)).max()
+        # alpha/beta/gamma carry 1/dt^2-scaled cancellation; compare on the rows' scale
+        assert err < (W_TOL if k in (0, 4, 5) else 1e-9), (k, err)
+
+
+def test_c5_per_node_harvest(lx, golden):
+    from paper_2603_15964_b200 import configs
+    from paper_2603_15964_b200.harvest import harvest_compact
+    w5 = configs.c5(N=64, steps=20)
+    c, nu = w5.coef
+    g = lx.make_periodic_grid(w5.N, 0.0, 1.0)
+    st = lx.select_stencils(g, w5.n, lx.StencilPolicy.CENTERED)
+    spec = lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1))
+    rows = harvest_compact(g, st, spec, w5.delta_t, 4)
+    W = rows.pernode.permute(2, 0, 1).cpu().numpy()       # (N, s, n)
+    ref = golden["c5_W"]
+    for r in range(4):
+        den = np.abs(ref[:, r]).max(axis=1)
+        assert (np.abs(W[:, r] - ref[:, r]).max(axis=1) / den).max() < W_TOL, r
+
+
+# ------------------------------------------------------------------ stepping
+def test_c1_run_linear_bitwise(lx, golden, orc):
+    from paper_2603_15964_b200 import configs
+    w = configs.c1()
+    m = orc.members_for(w.N, w.n, w.row, True)
+    W = np.tile(golden["c1_w"], (w.N, 1))
+    u = lx.kernels.run_linear(W, m, golden["c1_u0"], w.steps, False, 0.0, 0.0)
+    assert np.array_equal(u, golden["c1_u"])
+
+
+@pytest.mark.parametrize("tuning", [None, {"ring": 1}, {"tile": 256, "ksteps": 1},
+                                    {"tile": 300, "ksteps": 7}])
+def test_c1_launch_shapes_bitwise(lx, golden, orc, tuning):
+    from paper_2603_15964_b200 import configs
+    w = configs.c1()
+    m = orc.members_for(w.N, w.n, w.row, True)
+    W = np.tile(golden["c1_w"], (w.N, 1))
+    u = lx.kernels.run_linear(W, m, golden["c1_u0"], 123, tuning=tuning)
+    assert np.array_equal(u, orc.run_linear(W, m, golden["c1_u0"], 123))
+
+
+def test_c1_run_end_to_end(lx, golden):
+    from paper_2603_15964_b200 import configs
+    w = configs.c1()
+    g = lx.make_periodic_grid(w.N, w.x_min, w.x_max)
+    st = lx.select_stencils(g, w.n, lx.StencilPolicy.ONE_SIDED_UPWIND)
+    prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(w.terms), None, w.u0,
+                                lx.Boundary.periodic(), "none")
+    res = lx.run(g, st, prob, lx.SchemeConfig("linear"), w.delta_t, w.steps * w.delta_t,
+                 snapshot_stride=250 * w.delta_t)
+    assert res.snapshots.shape == (5, w.N)
+    assert rel_l2(res.u_final, golden["c1_u"]) < U_TOL
+    # Theorem 1 / exact transport: u(x - t)
+    x = g.nodes
+    k = np.arange(1, 9)
+    rng = np.random.default_rng(1)
+    a = rng.standard_normal(8) / k
+    th = rng.uniform(0, 2 * math.pi, 8)
+    T = w.steps * w.delta_t
+    exact = sum(a[i] * np.sin(k[i] * (x - T) + th[i]) for i in range(8))
+    assert np.abs(res.u_final - exact).max() < 1e-8
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_kdv_etdrk4(lx, golden, orc, exact):
+    N, n = 512, 11
+    rows = golden["kdv_rows"]
+    full = [np.tile(r, (N, 1)) for r in rows[:4]]
+    half = [np.tile(r, (N, 1)) for r in rows[4:6]]
+    d1 = np.tile(rows[6], (N, 1))
+    dt = float(golden["kdv_dt"])
+    w, al, be, ga, wh, p1h = orc.etdrk4_operators(full, half, dt)
+    m = orc.members_for(N, n, 5, True)
+    u = lx.kernels.run_etdrk4(w, al, be, ga, wh, p1h, 6.0 * d1, m, 1, golden["kdv_u0"],
+                              int(golden["kdv_steps"]), exact=exact)
+    if exact:
+        assert np.array_equal(u, golden["kdv_u"])
+    else:
+        assert rel_l2(u, golden["kdv_u"]) < U_TOL
+
+
+@pytest.mark.parametrize("tuning", [{"ring": 1}, {"tile": 64, "ksteps": 1}, {"tile": 128, "ksteps": 3}])
+def test_kdv_etdrk4_launch_shapes_bitwise(lx, golden, orc, tuning):
+    N, n = 512, 11
+    rows = golden["kdv_rows"]
+    full = [np.tile(r, (N, 1)) for r in rows[:4]]
+    half = [np.tile(r, (N, 1)) for r in rows[4:6]]
+    d1 = np.tile(rows[6], (N, 1))
+    dt = float(golden["kdv_dt"])
+    ops = orc.etdrk4_operators(full, half, dt)
+    m = orc.members_for(N, n, 5, True)
+    u = lx.kernels.run_etdrk4(*ops, 6.0 * d1, m, 1, golden["kdv_u0"], 37, tuning=tuning)
+    assert np.array_equal(u, orc.run_etdrk4(*ops, 6.0 * d1, m, 1, golden["kdv_u0"], 37))
+
+
+def test_burgers_etdrk4_and_etd2_run(lx, golden):
+    from paper_2603_15964_b200 import configs
+    w2 = configs.c2(N=256, steps=40)
+    g = lx.make_periodic_grid(w2.N, w2.x_min, w2.x_max)
+    st = lx.select_stencils(g, w2.n, lx.StencilPolicy.CENTERED)
+    prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(w2.terms), None, w2.u0,
+                                lx.Boundary.periodic(), "convective")
+    dt = float(golden["burg4_dt"])
+    T = int(golden["burg4_steps"]) * dt
+    r4 = lx.run(g, st, prob, lx.SchemeConfig("etdrk4"), dt, T)
+    assert rel_l2(r4.u_final, golden["burg4_u"]) < U_TOL
+    r2 = lx.run(g, st, prob, lx.SchemeConfig("etd-multistep", s=2), dt, T,
+                snapshot_stride=10 * dt)
+    assert rel_l2(r2.u_final, golden["burg2_u"]) < U_TOL
+
+
+def test_dirichlet_cubic_run(lx, golden):
+    N = 64
+    xg = np.linspace(-1.0, 1.0, N)
+    grid = lx.Grid(nodes=xg, x_min=-1.0, x_max=1.0, topology=lx.Topology.NON_PERIODIC)
+    st = lx.select_stencils(grid, 7, lx.StencilPolicy.CENTERED)
+    prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(((0, 1.0), (2, 1e-3))), None,
+                                golden["ac_u0"], lx.Boundary.dirichlet(-1.0, 1.0), "cubic")
+    dt = float(golden["ac_dt"])
+    res = lx.run(grid, st, prob, lx.SchemeConfig("etdrk4"), dt, 25 * dt)
+    assert rel_l2(res.u_final, golden["ac_u"]) < U_TOL
+    of = lx.assemble_global_phi(grid, st, lx.LinearOperatorSpec(((0, 1.0), (2, 1e-3))), dt, 4,
+                                frozen_nodes=(0, N - 1))
+    assert rel_inf(of[0].weights, golden["ac_wfull"]) < W_TOL
+    assert rel_inf(of[3].weights, golden["ac_p3"]) < W_TOL
+
+
+@pytest.mark.parametrize("tuning", [None, {"tile": 40, "ksteps": 1}, {"tile": 100, "ksteps": 4}])
+def test_c4_neumann_bitwise(lx, golden, orc, tuning):
+    W = golden["c4_weights"]
+    N, n = W.shape[1], W.shape[2]
+    m = orc.members_for(N, n, 3, False)
+    u0 = golden["c4_u0"].copy()
+    dl, dr = golden["c4_dl"], golden["c4_dr"]
+    acc = 0.0
+    for j in range(1, n):
+        acc += dl[j] * u0[j]
+    u0[0] = -acc / dl[0]
+    acc = 0.0
+    for j in range(n - 1):
+        acc += dr[j] * u0[N - n + j]
+    u0[N - 1] = -acc / dr[n - 1]
+    u = lx.kernels.run_etdrk4(*W, np.zeros((N, n)), m, 2, u0, 40, bc=("neumann", dl, dr),
+                              tuning=tuning)
+    assert np.array_equal(u, golden["c4_u"])
+
+
+def test_c4_family_run_neumann(lx, golden):
+    from paper_2603_15964_b200 import configs
+    w4 = configs.c4(N=256, steps=40)
+    g = lx.make_uniform_grid(w4.N, -1.0, 1.0)
+    st = lx.select_stencils(g, w4.n, lx.StencilPolicy.CENTERED)
+    prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(w4.terms), None, w4.u0,
+                                lx.Boundary.neumann(), "cubic")
+    res = lx.run(g, st, prob, lx.SchemeConfig("etdrk4"), w4.delta_t, 40 * w4.delta_t)
+    assert rel_l2(res.u_final, golden["c4_u"]) < U_TOL
+
+
+def test_c5_run_linear_per_node(lx, golden, orc):
+    from paper_2603_15964_b200 import configs
+    w5 = configs.c5(N=64, steps=20)
+    m = orc.members_for(w5.N, w5.n, w5.row, True)
+    W = np.ascontiguousarray(golden["c5_W"][:, 0])
+    u = lx.kernels.run_linear(W, m, w5.u0, w5.steps)
+    assert np.array_equal(u, golden["c5_u"])
+
+
+def test_c5_run_varcoef_end_to_end(lx, golden):
+    from paper_2603_15964_b200 import configs
+    w5 = configs.c5(N=64, steps=20)
+    c, nu = w5.coef
+    g = lx.make_periodic_grid(w5.N, 0.0, 1.0)
+    st = lx.select_stencils(g, w5.n, lx.StencilPolicy.CENTERED)
+    spec = lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1))
+    prob = lx.SemiLinearProblem(spec, None, w5.u0, lx.Boundary.periodic(), "none")
+    res = lx.run(g, st, prob, lx.SchemeConfig("linear"), w5.delta_t, 20 * w5.delta_t)
+    assert rel_l2(res.u_final, golden["c5_u"]) < U_TOL
+
+
+def test_nonfinite_run_raises_with_last_snapshot(lx):
+    # literal BASELINE C2 dt (mu ~ 209) blows up
+    N = 2048
+    g = lx.make_periodic_grid(N, 0.0, 2 * math.pi)
+    st = lx.select_stencils(g, 9, lx.StencilPolicy.CENTERED)
+    u0 = np.sin(g.nodes)
+    prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(((2, 0.01),)), None, u0,
+                                lx.Boundary.periodic(), "convective")
+    h = 2 * math.pi / N
+    dt = 2 * h
+    with pytest.raises(lx.NonFinite) as ei:
+        lx.run(g, st, prob, lx.SchemeConfig("etdrk4"), dt, 400 * dt, snapshot_stride=dt)
+    assert ei.value.state is not None and np.isfinite(ei.value.state).all()
+
+
+def test_apply_and_combine(lx, orc):
+    rng = np.random.default_rng(3)
+    N, n = 97, 5
+    g = lx.make_uniform_grid(N, -1.0, 1.0)
+    st = lx.select_stencils(g, n, lx.StencilPolicy.CENTERED)
+    m = st.members_array()
+    W = rng.standard_normal((N, n))
+    prop = lx.BandedPropagator(W, m, False, 0.1)
+    u = rng.standard_normal(N)
+    assert np.array_equal(lx.apply(prop, u), orc.banded_matvec(W, m, u))
+    uc = u + 1j * rng.standard_normal(N)
+    assert np.allclose(lx.apply(prop, uc), W @ np.zeros(n) + np.einsum("ij,ij->i", W, uc[m]))
+    P2 = lx.BandedPropagator(2 * W, m, False, 0.1)
+    cmb = lx.combine([prop, P2], [0.5, -0.25])
+    assert np.array_equal(cmb.weights, (np.zeros_like(W) + 0.5 * W) + (-0.25) * (2 * W))
+
+
+def test_scheme_consistency_zero_nonlinearity(lx):
+    """N = 0: ETDRK4, ETD2 and linear stepping agree."""
+    N = 300
+    g = lx.make_periodic_grid(N, 0.0, 1.0)
+    st = lx.select_stencils(g, 9, lx.StencilPolicy.CENTERED)
+    u0 = np.sin(2 * math.pi * g.nodes) + 0.3 * np.cos(6 * math.pi * g.nodes)
+    prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(((2, 1e-3), (1, -0.5))), None, u0,
+                                lx.Boundary.periodic(), "none")
+    dt = 0.4 / N
+    T = 30 * dt
+    ul = lx.run(g, st, prob, lx.SchemeConfig("linear"), dt, T).u_final
+    ue = lx.run(g, st, prob, lx.SchemeConfig("etdrk4"), dt, T).u_final
+    u2 = lx.run(g, st, prob, lx.SchemeConfig("etd-multistep", s=2), dt, T).u_final
+    assert rel_l2(ue, ul) < 1e-13 and rel_l2(u2, ul) < 1e-13

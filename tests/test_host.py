@@ -1,0 +1,106 @@
+"""Host-side logic: stencil geometry, member recognition, config validation."""
+
+import numpy as np
+import pytest
+
+import paper_2603_15964_b200 as lx
+from paper_2603_15964_b200 import _ops
+from paper_2603_15964_b200.grid import StencilSet
+
+
+def _ref_members(N, n, row, periodic):
+    # grid.py:136-175 restated with an explicit loop
+    out = []
+    rows = []
+    for t in range(N):
+        start = t - row
+        if periodic:
+            m = [(start + j) % N for j in range(n)]
+            r = row
+        else:
+            start = min(max(start, 0), N - n)
+            m = [start + j for j in range(n)]
+            r = t - start
+        out.append(m)
+        rows.append(r)
+    return np.array(out), np.array(rows)
+
+
+@pytest.mark.parametrize("N,n,policy,periodic", [(16, 5, "centered", True), (16, 5, "centered", False),
+                                                   (20, 7, "upwind", True), (20, 7, "upwind", False),
+                                                   (9, 9, "centered", True)])
+def test_stencil_set_matches_reference_windows(N, n, policy, periodic):
+    g = lx.make_periodic_grid(N, 0.0, 1.0) if periodic else lx.make_uniform_grid(N, -1.0, 1.0)
+    pol = lx.StencilPolicy.CENTERED if policy == "centered" else lx.StencilPolicy.ONE_SIDED_UPWIND
+    s = lx.select_stencils(g, n, pol)
+    m, r = _ref_members(N, n, s.row, periodic)
+    assert np.array_equal(s.members_array(), m)
+    assert np.array_equal(s.target_rows(), r)
+    for t in (0, N // 2, N - 1):
+        st = s[t]
+        assert np.array_equal(st.members, m[t]) and st.target_row == r[t]
+    assert _ops.validate_members(m, m.shape).__dict__ == s.__dict__
+
+
+def test_validate_members_rejects_scatter():
+    m = np.arange(40).reshape(8, 5) % 8
+    with pytest.raises(lx.InvalidConfig):
+        _ops.validate_members(m[::-1].copy(), m.shape)
+
+
+def test_select_stencils_errors():
+    g = lx.make_periodic_grid(8, 0.0, 1.0)
+    with pytest.raises(lx.StencilTooLarge):
+        lx.select_stencils(g, 9, lx.StencilPolicy.CENTERED)
+    with pytest.raises(lx.InvalidGrid):
+        lx.select_stencils(g, 4, lx.StencilPolicy.CENTERED)
+
+
+def test_grid_validation():
+    with pytest.raises(lx.InvalidGrid):
+        lx.Grid(nodes=[0.0, 0.0, 1.0], x_min=0.0, x_max=1.0, topology=lx.Topology.NON_PERIODIC)
+    with pytest.raises(lx.InvalidGrid):
+        lx.make_periodic_grid(2, 0.0, 1.0)
+
+
+def test_scheme_and_problem_validation():
+    with pytest.raises(lx.InvalidConfig):
+        lx.SchemeConfig("rk4")
+    with pytest.raises(lx.InvalidConfig):
+        lx.SchemeConfig("etd-multistep", s=0)
+    with pytest.raises(lx.InvalidConfig):
+        lx.SemiLinearProblem(lx.LinearOperatorSpec(((2, 1.0),)), None, np.zeros(5),
+                             lx.Boundary.periodic(), "quadratic")
+    with pytest.raises(lx.InvalidConfig):
+        lx.SemiLinearProblem(lx.LinearOperatorSpec(((2, 1.0),)), None, np.zeros(5),
+                             lx.Boundary.dirichlet(1.0, 0.0), "none")
+
+
+def test_operator_spec():
+    s = lx.LinearOperatorSpec(((0, 1.0), (2, 1e-4)))
+    assert s.max_order == 2 and s.reaction == 1.0
+    with pytest.raises(ValueError):
+        lx.LinearOperatorSpec(((1, 1.0), (1, 2.0)))
+    with pytest.raises(ValueError):
+        lx.LinearOperatorSpec(())
+
+
+def test_frozen_masks_and_class_plan():
+    from paper_2603_15964_b200.harvest import _frozen_masks
+    s = StencilSet(32, 7, 3, False)
+    t = np.arange(32)
+    masks = _frozen_masks(s, t, [0, 31])
+    m = s.members_array()
+    for i in range(32):
+        want = sum(1 << j for j in range(7) if m[i, j] in (0, 31))
+        assert int(masks[i]) == want
+
+
+def test_configs_are_seeded_and_shaped():
+    from paper_2603_15964_b200 import configs
+    a, b = configs.c1(), configs.c1()
+    assert np.array_equal(a.u0, b.u0) and a.N == 1024 and a.n == 7 and a.row == 6
+    c5 = configs.c5(N=256)
+    c, nu = c5.coef
+    assert abs(c.min() + 2) < 1e-12 and abs(c.max() - 2) < 1e-12
+    assert nu.min() >= 1e-4 * (1 - 1e-12) and nu.max() <= 1e-1 * (1 + 1e-12)
