@@ -1,0 +1,396 @@
+#!/usr/bin/env python
+"""LMEP benchmark (BASELINE.json metric: grid-point updates/s (fp64) +
+local-expm harvests/s, % of the HBM / FP64 roofline).
+
+Headline workload (`value`): BASELINE config 5 -- variable-coefficient
+advection-diffusion, periodic N=2^22, n=13, one matrix exponential per node
+(4,194,304 harvests) and 200 linear steps with per-node weights.  It is the
+config where both halves of the metric bind: the batched per-node harvest
+(FP64) and the per-node banded step (HBM, the >=70% target).  One bench
+"step" = one full pass of that workload (harvest + 200 steps) on resident
+inputs; value = N*200 / pass time.  Configs 1-4 are run once each and
+reported under "workloads".
+
+Timing: W warm-up passes, then K passes bracketed by barrier +
+cuda.synchronize, CUDA events on the launching stream, max over ranks.
+Inputs exceed L2 (per-node rows 436 MB are streamed every step), so no flush
+is needed.  `e2e` repeats the pass through the public API (`run`) from host
+numpy arrays, H2D/D2H inside the timed region.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+PI = {3: 2, 5: 3, 7: 4, 9: 5, 13: 6}    # matrix products of Pade degree m
+
+
+def expm_flops(d: int, ms: np.ndarray) -> float:
+    """Algorithmic FLOPs of the harvest: F = 2d^3 (pi_m + s) + 8/3 d^3 per matrix,
+    with (m, s) taken from the kernel's own per-matrix selection."""
+    m = ms & 0xFF
+    s = ms >> 8
+    pim = np.zeros_like(m)
+    for k, v in PI.items():
+        pim[m == k] = v
+    return float((2.0 * d**3 * (pim + s) + (8.0 / 3.0) * d**3).sum())
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def fp64_peak():
+    so = os.path.join(REPO, "tools", "libfp64peak.so")
+    lib = ctypes.CDLL(so)
+    lib.fp64_peak_tflops.restype = ctypes.c_double
+    lib.fp64_peak_tflops.argtypes = [ctypes.c_int]
+    return float(lib.fp64_peak_tflops(10))
+
+
+# ------------------------------------------------------------------ workloads
+def c5_inputs(N=None):
+    from paper_2603_15964_b200 import configs
+    w = configs.c5() if N is None else configs.c5(N=N)
+    c, nu = w.coef
+    return w, np.ascontiguousarray(np.stack([-c, nu], 1))
+
+
+class C5:
+    """Config 5 pass on resident device inputs."""
+
+    def __init__(self, dist=None):
+        import torch
+        import paper_2603_15964_b200 as lx
+        from paper_2603_15964_b200 import _ops
+        self.lx, self.torch = lx, torch
+        self.w, coef = c5_inputs()
+        self.coef_host, self.u0_host = coef, self.w.u0
+        self.grid = lx.make_periodic_grid(self.w.N, 0.0, 1.0)
+        self.sset = lx.select_stencils(self.grid, self.w.n, lx.StencilPolicy.CENTERED)
+        self.coef = _ops.dev_f64(coef)
+        self.u0 = _ops.dev_f64(self.w.u0)
+        self.spec = lx.VariableCoefficientSpec((1, 2), self.coef)
+        self.prob = lx.SemiLinearProblem(self.spec, None, self.u0, lx.Boundary.periodic(), "none")
+        self.scheme = lx.SchemeConfig("linear")
+        self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        self.last = {}
+
+    def device_pass(self):
+        from paper_2603_15964_b200.timestep import Stepper, prepare
+        stats = {}
+        e0, e1, e2 = self.ev
+        e0.record()
+        prep = prepare(self.grid, self.sset, self.prob, self.scheme, self.w.delta_t, stats)
+        e1.record()
+        st = Stepper(prep, self.u0)
+        st.advance(self.w.steps)
+        e2.record()
+        self.last = {"prep": prep, "stats": stats, "stepper": st}
+        return st.u
+
+    def phase_ms(self):
+        e0, e1, e2 = self.ev
+        self.torch.cuda.synchronize()
+        return e0.elapsed_time(e1), e1.elapsed_time(e2)
+
+    def e2e_pass(self):
+        """Public API from host arrays: H2D of u0 + coefficients, D2H of snapshots."""
+        lx = self.lx
+        spec = lx.VariableCoefficientSpec((1, 2), self.coef_host)
+        prob = lx.SemiLinearProblem(spec, None, self.u0_host, lx.Boundary.periodic(), "none")
+        res = lx.run(self.grid, self.sset, prob, self.scheme, self.w.delta_t,
+                     self.w.steps * self.w.delta_t)
+        return res
+
+    @property
+    def h2d_bytes(self):
+        return self.coef_host.nbytes + self.u0_host.nbytes
+
+    @property
+    def d2h_bytes(self):
+        return 2 * self.u0_host.nbytes        # snapshots: u0 and u_final (timestep.py:313,350)
+
+
+def time_other_configs():
+    """Configs 1-4, one timed run each after one warm-up (reported, not the headline)."""
+    import torch
+    import paper_2603_15964_b200 as lx
+    from paper_2603_15964_b200 import configs
+    from paper_2603_15964_b200.timestep import Stepper, prepare
+    out = {}
+    for name in ("c1", "c2", "c3", "c4"):
+        w = configs.make(name)
+        if w.periodic:
+            g = lx.make_periodic_grid(w.N, w.x_min, w.x_max)
+        else:
+            g = lx.make_uniform_grid(w.N, w.x_min, w.x_max)
+        pol = lx.StencilPolicy.ONE_SIDED_UPWIND if w.policy == "upwind" else lx.StencilPolicy.CENTERED
+        st = lx.select_stencils(g, w.n, pol)
+        bc = lx.Boundary.neumann() if w.boundary == "neumann" else lx.Boundary.periodic()
+        prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(w.terms), None, w.u0, bc, w.nonlinear,
+                                    nonlinear_scale=w.nl_scale or 1.0)
+        scheme = {"linear": lx.SchemeConfig("linear"), "etdrk4": lx.SchemeConfig("etdrk4"),
+                  "etd2": lx.SchemeConfig("etd-multistep", s=2)}[w.scheme]
+        res = {}
+        for exact in ((True, False) if w.scheme != "linear" else (True,)):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            u0 = torch.as_tensor(w.u0, device="cuda")
+            for rep in range(2):
+                torch.cuda.synchronize()
+                ev[0].record()
+                prep = prepare(g, st, prob, scheme, w.delta_t)
+                ev[1].record()
+                s = Stepper(prep, u0, exact=exact)
+                s.advance(w.steps)
+                ev[2].record()
+                torch.cuda.synchronize()
+            hv, sp = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
+            fin = bool(torch.isfinite(s.u).all().item())
+            res["exact" if exact else "fma"] = {
+                "updates_per_s": w.N * w.steps / (sp * 1e-3), "step_ms_total": sp,
+                "us_per_step": sp * 1e3 / w.steps, "harvest_ms": hv, "finite": fin}
+        out[name] = {"N": w.N, "n": w.n, "scheme": w.scheme, "steps": w.steps,
+                     "dt": w.delta_t, **res}
+    return out
+
+
+# ------------------------------------------------------------------ CPU arm
+def cpu_c5(sample_nodes=1 << 14, sample_steps=2, threads=None):
+    """The oracle (C restatement of the reference, OpenMP) on a bounded sample of
+    config 5: per-node harvest of `sample_nodes` nodes and `sample_steps`
+    full-grid per-node steps, extrapolated to the whole pass."""
+    from oracle import oracle as orc
+    orc.build()
+    if threads:
+        orc.set_threads(threads)
+    cores = orc.num_threads()
+    w, coef = c5_inputs()
+    x = (np.arange(w.n) - w.row) * w.h
+    D1 = np.array([orc.fornberg_weights(xi, x, 2)[1] for xi in x])
+    D2 = np.array([orc.fornberg_weights(xi, x, 2)[2] for xi in x])
+    idx = np.linspace(0, w.N - 1, sample_nodes).astype(np.int64)
+    t0 = time.perf_counter()
+    W = orc.harvest_batch_vc(D1, D2, coef[idx, 0], coef[idx, 1], w.delta_t, 1, w.row,
+                             reduced=True)
+    th = (time.perf_counter() - t0) / sample_nodes
+    Wfull = np.tile(W[:, 0], (w.N // sample_nodes + 1, 1))[: w.N]
+    m = orc.members_for(w.N, w.n, w.row, True)
+    t0 = time.perf_counter()
+    orc.run_linear(np.ascontiguousarray(Wfull), m, w.u0, sample_steps)
+    ts = (time.perf_counter() - t0) / sample_steps
+    total = th * w.N + ts * w.steps
+    return {"value": w.N * w.steps / total, "unit": "grid-point updates/s", "cores": cores,
+            "kind": "port",
+            "sample": f"oracle C port (OpenMP {cores} threads): per-node harvest of {sample_nodes} "
+                      f"of {w.N} nodes + {sample_steps} of {w.steps} per-node steps on the full "
+                      f"N={w.N} grid, extrapolated to one full pass",
+            "harvests_per_s": 1.0 / th, "step_s": ts}
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-others", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    metric = "LMEP grid-point updates/s (fp64), config 5 (per-node harvest + 200 steps)"
+    unit = "grid-point updates/s"
+    config = {"workload": "c5-varcoef: periodic [0,1), N=2^22, n=13, per-node expm "
+                          "(4194304 harvests), 200 linear steps, dt=0.5h^2/max(nu)",
+              "N": 1 << 22, "n": 13, "steps_per_pass": 200, "harvests_per_pass": 1 << 22,
+              "l2": "inputs larger than L2 (436 MB per-node rows streamed each step)",
+              "parallelism": f"replicas x{args.gpus}" if args.gpus > 1 else "single"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cb = cpu_c5()
+        vals = []
+        for _ in range(args.warmup + args.steps):
+            pass
+        line = {"metric": metric, "value": cb["value"], "unit": unit, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * (1 << 22) * 200 / cb["value"], "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config, "impl": "reference",
+                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": cb["value"], "unit": unit, "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    from paper_2603_15964_b200 import _native
+    lib = _native.load()
+
+    bench = C5()
+    for _ in range(args.warmup):
+        bench.device_pass()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    L0 = lib.lmep_launch_count()
+    times, harv, stepm = [], [], []
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            bench.device_pass()
+            h, s = bench.phase_ms()
+            harv.append(h)
+            stepm.append(s)
+            times.append(h + s)
+    torch.cuda.synchronize()
+    launches = (lib.lmep_launch_count() - L0) / args.steps
+    ms = float(np.mean(times))
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    w = bench.w
+    value = world * w.N * w.steps / (ms * 1e-3)
+    harvest_ms = float(np.mean(harv))
+    step_ms = float(np.mean(stepm))
+
+    # roofline of the per-node step kernel (HBM) and of the harvest (FP64)
+    hbm, hbm_kind = peaks()
+    step_bytes = w.N * (8 * w.n + 16)                      # u in/out + 13 rows per node
+    per_launch_ms = step_ms / w.steps
+    achieved = step_bytes / (per_launch_ms * 1e-3) / 1e9
+    ms_items = torch.cat(bench.last["stats"]["ms"]).cpu().numpy()
+    d = w.n                                               # s = 1: d = n
+    flops = expm_flops(d, ms_items)
+    fp64 = fp64_peak()
+    harvest_tflops = flops / (harvest_ms * 1e-3) / 1e12
+
+    # e2e through the public API
+    for _ in range(2):
+        bench.e2e_pass()
+    e2e_ms = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        bench.e2e_pass()
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_val = world * w.N * w.steps / (float(np.mean(e2e_ms)) * 1e-3)
+
+    others = {}
+    if not args.no_others and rank == 0:
+        others = time_other_configs()
+    cpu = None
+    if not args.no_cpu and rank == 0 and world == 1:
+        cpu = cpu_c5()
+
+    if rank == 0:
+        line = {
+            "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY 8(d))",
+            "config": config,
+            "harvests_per_s": world * w.N / (harvest_ms * 1e-3),
+            "phases_ms": {"harvest": harvest_ms, "steps": step_ms,
+                          "per_step_launch_ms": per_launch_ms},
+            "roofline": {"bound": "hbm", "kernel": "step_kernel<LIN,13,exact,P=1> (per-node rows)",
+                         "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": None,
+                         "algorithmic_bytes_per_launch": step_bytes, "peak_kind": hbm_kind},
+            "roofline_harvest": {"bound": "fp64", "kernel": "harvest_kernel<16,4>",
+                                 "achieved": harvest_tflops, "peak": fp64, "unit": "TFLOP/s",
+                                 "frac": harvest_tflops / fp64, "algorithmic_flops": flops,
+                                 "peak_kind": "measured DFMA chains (tools/fp64_peak.cu)"},
+            "e2e": {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": bench.h2d_bytes,
+                    "d2h_bytes_per_step": bench.d2h_bytes},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "cpu_baseline": None if cpu is None else
+            {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "workloads": others,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

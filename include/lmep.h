@@ -133,7 +133,7 @@ typedef struct {
     int32_t tile;              /* owned nodes per CTA                                 */
     int32_t ksteps;            /* time steps fused per launch (temporal blocking)     */
     int32_t ring;              /* 1: whole periodic grid resident in one CTA          */
-    int32_t reserved;
+    int32_t threads;           /* threads per CTA (multiple of 32, <= 256)            */
 } lmep_tuning;
 
 /* ---- library ------------------------------------------------------------ */

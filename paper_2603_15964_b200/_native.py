@@ -68,7 +68,7 @@ class LmepHalo(C.Structure):
 
 class LmepTuning(C.Structure):
     _fields_ = [("tile", C.c_int32), ("ksteps", C.c_int32), ("ring", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("threads", C.c_int32)]
 
 
 _lib = None

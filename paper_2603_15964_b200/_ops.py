@@ -327,6 +327,7 @@ def _tuning(tuning) -> nat.LmepTuning | None:
     t.tile = int(tuning.get("tile", 0))
     t.ksteps = int(tuning.get("ksteps", 0))
     t.ring = int(tuning.get("ring", 0))
+    t.threads = int(tuning.get("threads", 0))
     return t
 
 

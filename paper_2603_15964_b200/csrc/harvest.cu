@@ -173,57 +173,71 @@ __device__ __forceinline__ double warp_max(double v)
     return v;
 }
 
-// Diagonal balancing, LAPACK dgebal job 'S' (scipy.linalg.matrix_balance with
-// permute=False, expm.py:37).  Scales are exact powers of two.  Returns false
-// on NaN.
+// Diagonal balancing before the exponential (expm.py:27-39 balances with
+// LAPACK dgebal, job 'S').  Any diagonal similarity by powers of two is exact,
+// so the balancing only has to shrink the norm; the result of the exponential
+// does not depend on which balancing is chosen beyond rounding.  dgebal sweeps
+// the columns one after another (Gauss-Seidel order), which costs d dependent
+// warp reductions per sweep; here every lane i evaluates dgebal's acceptance
+// test for its own row/column pair simultaneously (Jacobi order, Osborne's
+// iteration), with the power-of-two factor from integer exponent arithmetic:
+//   f = 2^k with k chosen as dgebal's loops would, from ||col i||, ||row i||
+//   accept if ||col i|| f + ||row i|| / f < 0.95 (||col i|| + ||row i||).
+// Sweeps stop when no lane changes (at most 12).  Returns false on NaN.
+__device__ __forceinline__ int exp2i(double x)      // floor(log2 x) for normal x > 0
+{
+    return ((__double2hiint(x) >> 20) & 0x7ff) - 1023;
+}
+__device__ __forceinline__ double pow2(int k)       // 2^k, |k| < 1000
+{
+    return __hiloint2double((k + 1023) << 20, 0);
+}
+
 template <int DP>
 __device__ bool balance(double *A, double *scale, int d, int lane)
 {
     using T = Tile<DP>;
-    const double sclfac = 2.0, factor = 0.95;
-    const double sfmin1 = 2.2250738585072014e-308 / 2.220446049250313e-16;
-    const double sfmax1 = 1.0 / sfmin1;
-    const double sfmin2 = sfmin1 * sclfac;
-    const double sfmax2 = 1.0 / sfmin2;
-    if (lane < DP) scale[lane] = 1.0;
-    __syncwarp();
-    bool noconv = true;
-    int sweeps = 0;
-    while (noconv) {
-        noconv = false;
-        if (++sweeps > 1000) break;
-        for (int i = 0; i < d; ++i) {
-            const double ce = (lane < d) ? A[lane * T::LD + i] : 0.0;
-            const double re = (lane < d) ? A[i * T::LD + lane] : 0.0;
-            double c = sqrt(warp_sum(ce * ce));
-            double r = sqrt(warp_sum(re * re));
-            double ca = warp_max(fabs(ce));
-            double ra = warp_max(fabs(re));
-            if (c == 0.0 || r == 0.0) continue;
-            if (isnan(c + ca + r + ra)) return false;
-            double g = r / sclfac, f = 1.0;
-            const double s = c + r;
-            while (c < g && fmax(f, fmax(c, ca)) < sfmax2 && fmin(r, fmin(g, ra)) > sfmin2) {
-                f *= sclfac; c *= sclfac; ca *= sclfac; r /= sclfac; g /= sclfac; ra /= sclfac;
+    const int c = lane % DP, g = lane / DP;
+    double my_scale = 1.0;          // scale of row/column `lane`
+    for (int sweep = 0; sweep < 12; ++sweep) {
+        double c2 = 0.0, r2 = 0.0;
+        if (lane < d) {
+            for (int k = 0; k < d; ++k) {
+                const double ce = A[k * T::LD + lane], re = A[lane * T::LD + k];
+                c2 = fma(ce, ce, c2);
+                r2 = fma(re, re, r2);
             }
-            g = c / sclfac;
-            while (g >= r && fmax(r, ra) < sfmax2 && fmin(fmin(f, c), fmin(g, ca)) > sfmin2) {
-                f /= sclfac; c /= sclfac; g /= sclfac; ca /= sclfac; r *= sclfac; ra *= sclfac;
-            }
-            if ((c + r) >= factor * s) continue;
-            const double si = scale[i];
-            if (f < 1.0 && si < 1.0 && f * si <= sfmin1) continue;
-            if (f > 1.0 && si > 1.0 && si >= sfmax1 / f) continue;
-            g = 1.0 / f;
-            noconv = true;
-            __syncwarp();
-            if (lane == 0) scale[i] = si * f;
-            if (lane < d) A[i * T::LD + lane] *= g;   // row i / f
-            __syncwarp();
-            if (lane < d) A[lane * T::LD + i] *= f;   // column i * f
-            __syncwarp();
         }
+        if (isnan(c2 + r2)) return false;
+        int k = 0;
+        if (lane < d && c2 > 1e-280 && r2 > 1e-280 && c2 < 1e280 && r2 < 1e280) {
+            const double cn = sqrt(c2), rn = sqrt(r2);
+            // dgebal: while (c < r/2) {c*=2; r/=2}  /  while (c/2 >= r) {c/=2; r*=2}
+            int kk = (exp2i(rn) - exp2i(cn)) / 2;
+            while (cn * pow2(2 * kk + 1) < rn) ++kk;
+            while (kk > 0 && !(cn * pow2(2 * kk - 1) < rn)) --kk;
+            if (kk <= 0) {
+                kk = 0;
+                while (cn * pow2(-(2 * (-kk) + 1)) >= rn) --kk;
+                while (kk < 0 && !(cn * pow2(-(2 * (-kk) - 1)) >= rn)) ++kk;
+            }
+            const double f = pow2(kk);
+            if (kk != 0 && cn * f + rn / f < 0.95 * (cn + rn)) k = kk;
+        }
+        if (!__any_sync(FULL, k != 0)) break;
+        // A[r][c] <- A[r][c] * f_c / f_r  (row r divided by f_r, column c times f_c)
+        my_scale *= pow2(k);
+        const int kc = __shfl_sync(FULL, k, c);
+#pragma unroll
+        for (int j = 0; j < T::E; ++j) {
+            const int r = g + T::G * j;
+            const int kr = __shfl_sync(FULL, k, r);
+            if (r < d && c < d && kc != kr) A[r * T::LD + c] *= pow2(kc - kr);
+        }
+        __syncwarp();
     }
+    if (lane < DP) scale[lane] = my_scale;
+    __syncwarp();
     return true;
 }
 
@@ -235,15 +249,13 @@ __device__ bool lu_solve(double *Q, double *P, int d, int lane)
     using T = Tile<DP>;
     const int c = lane % DP, g = lane / DP;
     for (int k = 0; k < d; ++k) {
-        double val = (lane >= k && lane < d) ? fabs(Q[lane * T::LD + k]) : -1.0;
-        int idx = lane;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(FULL, val, o);
-            const int oi = __shfl_xor_sync(FULL, idx, o);
-            if (ov > val || (ov == val && oi < idx)) { val = ov; idx = oi; }
-        }
-        if (!(val > 0.0)) return false;
+        // pivot: max |Q[i][k]|, i >= k (32-bit key: high word of |q|, then lowest index)
+        const double qv = (lane >= k && lane < d) ? fabs(Q[lane * T::LD + k]) : 0.0;
+        const unsigned key = (lane >= k && lane < d)
+                                 ? ((unsigned)__double2hiint(qv) & ~31u) | (31u - lane) : 0u;
+        const unsigned best = __reduce_max_sync(FULL, key);
+        const int idx = 31 - (int)(best & 31u);
+        if (!(__shfl_sync(FULL, qv, idx) > 0.0)) return false;
         if (idx != k) {
             if (lane < d) {
                 double t = Q[k * T::LD + lane];

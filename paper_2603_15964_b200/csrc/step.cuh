@@ -38,6 +38,8 @@ namespace lmep {
 enum { SCH_LIN = 0, SCH_ETDRK4 = 1, SCH_ETD2 = 2 };
 constexpr int STEP_THREADS = 256;
 constexpr int SLOT_PAD = 24;
+constexpr int STEP_P_ETDRK4 = 5;   // consecutive outputs per thread (odd: conflict-free)
+constexpr int STEP_P_ETD2 = 5;
 
 struct StepParams {
     int64_t N, off, nloc;
@@ -61,6 +63,7 @@ struct StepParams {
     double *nl0_out;
     double dt;
     int ksteps, ext;
+    int threads;                                // CTA size (multiple of 32, <= STEP_THREADS)
     int64_t tile;
     int64_t slot_len;
     int *flag;
@@ -110,7 +113,7 @@ __device__ __forceinline__ int64_t class_of(const StepParams &p, int64_t i)
 
 // one banded product at node i (any position: clamped window, class rows)
 template <bool EX>
-__device__ double band_slow(const StepParams &p, int r, const double *X, int64_t i, int64_t base)
+__device__ __noinline__ double band_slow(const StepParams &p, int r, const double *X, int64_t i, int64_t base)
 {
     const int n = p.n;
     int64_t st = i - p.row;
@@ -135,16 +138,16 @@ __device__ double band_slow(const StepParams &p, int r, const double *X, int64_t
 }
 
 // P banded products at the consecutive interior nodes c0..c0+P-1.
-template <int NS, int P, bool EX>
-__device__ __forceinline__ void band_fast(const StepParams &p, int r, const double *X, int64_t c0,
-                                          int64_t base, double *out)
+template <int NS, int P, bool EX, bool PN>
+__device__ __forceinline__ void band_fast(const StepParams &p, int r, const double *X, int l,
+                                          int64_t lbase, double *out)
 {
-    const double *x = X + (c0 - p.row - base);
+    const double *x = X + (l - p.row);
     if constexpr (NS > 0) {
         double win[P + NS - 1];
 #pragma unroll
         for (int q = 0; q < P + NS - 1; ++q) win[q] = x[q];
-        if (p.wmode != LMEP_W_PERNODE) {
+        if constexpr (!PN) {
 #pragma unroll
             for (int q = 0; q < P; ++q) {
                 double acc = 0.0;
@@ -153,7 +156,7 @@ __device__ __forceinline__ void band_fast(const StepParams &p, int r, const doub
                 out[q] = acc;
             }
         } else {
-            const double *w = p.wp + (int64_t)r * NS * p.nloc + (c0 - p.off);
+            const double *w = p.wp + (int64_t)r * NS * p.nloc + (lbase + l);
 #pragma unroll
             for (int q = 0; q < P; ++q) {
                 double acc = 0.0;
@@ -166,10 +169,10 @@ __device__ __forceinline__ void band_fast(const StepParams &p, int r, const doub
         const int n = p.n;
         for (int q = 0; q < P; ++q) {
             double acc = 0.0;
-            if (p.wmode != LMEP_W_PERNODE) {
+            if constexpr (!PN) {
                 for (int j = 0; j < n; ++j) acc = macc<EX>(acc, p.wi[r][j], x[q + j]);
             } else {
-                const double *w = p.wp + (int64_t)r * n * p.nloc + (c0 - p.off) + q;
+                const double *w = p.wp + (int64_t)r * n * p.nloc + (lbase + l) + q;
                 for (int j = 0; j < n; ++j) acc = macc<EX>(acc, __ldcs(w + (int64_t)j * p.nloc), x[q + j]);
             }
             out[q] = acc;
@@ -177,18 +180,9 @@ __device__ __forceinline__ void band_fast(const StepParams &p, int r, const doub
     }
 }
 
-template <int NS, int P, bool EX>
-__device__ __forceinline__ void bands(const StepParams &p, int r, const double *X, int64_t c0,
-                                      int cnt, bool fast, int64_t base, double *out)
-{
-    if (fast) band_fast<NS, P, EX>(p, r, X, c0, base, out);
-    else
-        for (int q = 0; q < cnt; ++q) out[q] = band_slow<EX>(p, r, X, c0 + q, base);
-}
-
 // Value of a pinned node gb computed from stage vector X (smem, base-relative).
 template <bool EX>
-__device__ double bc_value(const StepParams &p, const double *X, int64_t gb, int64_t base)
+__device__ __noinline__ double bc_value(const StepParams &p, const double *X, int64_t gb, int64_t base)
 {
     if (p.bc == LMEP_BC_DIRICHLET) return gb == 0 ? p.lo : p.hi;
     const int n = p.n;
@@ -202,15 +196,62 @@ __device__ double bc_value(const StepParams &p, const double *X, int64_t gb, int
     return xdiv(-acc, p.dr[n - 1]);
 }
 
-template <int SCH, int NS, bool EX, int P>
-__global__ void __launch_bounds__(STEP_THREADS) step_kernel(const __grid_constant__ StepParams p)
+// One stage pass over the tile-local range [lo, hi): NB banded products
+// (rows[b] applied to X[b]) per node, then epi(l, v[NB]).  Full interior
+// chunks of P nodes take the register-window fast path with no guards; the
+// few remaining nodes (range ends, boundary classes) take a per-node path.
+template <int NS, int P, bool EX, bool PN, int NB, class Epi>
+__device__ __forceinline__ void run_pass(const StepParams &p, int lo, int hi, int fLo, int fHi,
+                                         int64_t base, int64_t lbase, const int (&rows)[NB],
+                                         const double *const (&X)[NB], Epi &&epi)
+{
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int flo = lo > fLo ? lo : fLo;
+    const int fhi = hi < fHi ? hi : fHi;
+    const int nch = fhi > flo ? (fhi - flo) / P : 0;
+    for (int ch = tid; ch < nch; ch += nt) {
+        const int l = flo + ch * P;
+        double v[NB > 0 ? NB : 1][P];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) band_fast<NS, P, EX, PN>(p, rows[b], X[b], l, lbase, v[b]);
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+            double vq[NB > 0 ? NB : 1];
+#pragma unroll
+            for (int b = 0; b < NB; ++b) vq[b] = v[b][q];
+            epi(l + q, vq);
+        }
+    }
+    const int a_end = nch > 0 ? flo : lo;
+    const int b_beg = nch > 0 ? flo + nch * P : lo;
+    const int na = a_end - lo, nb = hi - b_beg;
+    for (int k = tid; k < na + nb; k += nt) {
+        const int l = k < na ? lo + k : b_beg + (k - na);
+        double vq[NB > 0 ? NB : 1];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) vq[b] = band_slow<EX>(p, rows[b], X[b], base + l, base);
+        epi(l, vq);
+    }
+}
+
+// pointwise pass (no banded product)
+template <class Epi>
+__device__ __forceinline__ void run_pointwise(int lo, int hi, Epi &&epi)
+{
+    for (int l = lo + (int)threadIdx.x; l < hi; l += blockDim.x) epi(l);
+}
+
+template <int SCH, int NS, bool EX, int P, int NLK, bool PN>
+__global__ void __launch_bounds__(STEP_THREADS, SCH == SCH_LIN ? 1 : 2)
+step_kernel(const __grid_constant__ StepParams p)
 {
     extern __shared__ double sm[];
-    constexpr int NSLOT = SCH == SCH_LIN ? 2 : (SCH == SCH_ETD2 ? 5 : 7);
     const int tid = threadIdx.x, nt = blockDim.x;
     const int eL = p.eL, eR = p.eR;
     const bool ring = p.ring != 0;
     const bool pins = !p.periodic && p.bc != LMEP_BC_NONE;
+    constexpr int nlk = NLK;
+    constexpr bool cv = SCH != SCH_LIN && NLK == LMEP_NL_CONVECTIVE;
 
     int64_t O0, O1;
     if (ring) {
@@ -221,7 +262,7 @@ __global__ void __launch_bounds__(STEP_THREADS) step_kernel(const __grid_constan
         O0 = p.off + t0;
         O1 = p.off + (t0 + p.tile < p.nloc ? t0 + p.tile : p.nloc);
     }
-    auto expand = [&](int units, int64_t &lo, int64_t &hi) {
+    auto expand_g = [&](int units, int64_t &lo, int64_t &hi) {
         if (ring) { lo = 0; hi = p.N; return; }
         lo = O0 - (int64_t)units * eL;
         hi = O1 + (int64_t)units * eR;
@@ -233,22 +274,42 @@ __global__ void __launch_bounds__(STEP_THREADS) step_kernel(const __grid_constan
     const int K = p.ksteps;
     int64_t base, gend;
     if (ring) { base = -eL; gend = p.N + eR; }
-    else expand(K * p.ext, base, gend);
+    else expand_g(K * p.ext, base, gend);
     const int len = (int)(gend - base);
-
-    double *S[NSLOT];
-#pragma unroll
-    for (int q = 0; q < NSLOT; ++q) S[q] = sm + (int64_t)q * p.slot_len;
+    // pass ranges in tile-local (shared-memory) coordinates
+    auto expand = [&](int units, int &lo, int &hi) {
+        int64_t a, b;
+        expand_g(units, a, b);
+        lo = (int)(a - base);
+        hi = (int)(b - base);
+    };
+    // fast-path window: interior class and, for per-node rows, owned nodes
+    const int64_t lbase = base - p.off;
+    int fLo, fHi;
+    {
+        int64_t a = p.L_int - base, b = p.R_int - base;
+        if (PN) {
+            a = a > -lbase ? a : -lbase;
+            b = b < p.nloc - lbase ? b : p.nloc - lbase;
+        }
+        const int64_t big = 1 << 30;
+        fLo = (int)(a < -big ? -big : (a > big ? big : a));
+        fHi = (int)(b < -big ? -big : (b > big ? big : b));
+    }
+    const int slen = (int)p.slot_len;
+#define S(q) (sm + (q) * slen)
 
     // ---- stage u (and the etd2 history) into shared memory -------------
     for (int idx = tid; idx < len; idx += nt) {
         const int64_t g = base + idx;
-        S[0][idx] = load_node(p, p.u_in, p.hl, p.hr, g);
-        if constexpr (SCH == SCH_ETD2) S[1][idx] = load_node(p, p.q_in, p.qhl, p.qhr, g);
+        const double u = load_node(p, p.u_in, p.hl, p.hr, g);
+        S(0)[idx] = u;
+        if constexpr (SCH == SCH_ETD2) S(1)[idx] = load_node(p, p.q_in, p.qhl, p.qhr, g);
+        if constexpr (SCH == SCH_ETDRK4 && !cv) S(1)[idx] = nlp<EX>(nlk, u, 0.0);  // n0 of step 0
     }
     __syncthreads();
 
-    // ring: refresh ghost cells of slot X from the ring itself
+    // end of a pass: barrier, then (ring) refresh the ghost cells of X
     auto refresh = [&](double *X) {
         if (!ring) return;
         __syncthreads();
@@ -258,61 +319,51 @@ __global__ void __launch_bounds__(STEP_THREADS) step_kernel(const __grid_constan
         }
     };
     // thread 0 applies the closure of stage vector X at the boundary nodes in
-    // [lo, hi); fix(gb, value, si) recomputes dependent pointwise values.
-    auto pin_pass = [&](double *X, int64_t lo, int64_t hi, auto &&fix) {
+    // [lo, hi); fix(l, value) recomputes the dependent pointwise values.
+    auto pin_pass = [&](double *X, int lo, int hi, auto &&fix) {
         if (!pins) return;
+        const int64_t b0 = -base, b1 = p.N - 1 - base;          // CTA-uniform test
+        if (!((b0 >= lo && b0 < hi) || (b1 >= lo && b1 < hi))) return;
         __syncthreads();
         if (tid == 0) {
             const int64_t ends[2] = {0, p.N - 1};
             for (int e = 0; e < 2; ++e) {
                 const int64_t gb = ends[e];
-                if (gb < lo || gb >= hi) continue;
+                if (gb - base < lo || gb - base >= hi) continue;
                 const double v = bc_value<EX>(p, X, gb, base);
                 X[gb - base] = v;
-                fix(gb - base, v);
+                fix((int)(gb - base), v);
             }
         }
     };
-    auto none = [](int64_t, double) {};
-
-#define CHUNK_LOOP(LO, HI)                                                          \
-    for (int64_t c0 = (LO) + (int64_t)tid * P; c0 < (HI); c0 += (int64_t)nt * P)
-#define CHUNK_SETUP(HI)                                                             \
-    const int cnt = (int)((HI) - c0 < P ? (HI) - c0 : P);                           \
-    const bool fast = cnt == P && c0 >= p.L_int && c0 + P <= p.R_int &&                  \
-                      (p.wmode != LMEP_W_PERNODE || (c0 >= p.off && c0 + P <= p.off + p.nloc));
-
-    const int nlk = p.nl;
-    const int cv = (SCH != SCH_LIN && nlk == LMEP_NL_CONVECTIVE) ? 1 : 0;
+    auto none = [](int, double) {};
+    auto sub2 = [](double n2, double n0) { return EX ? xsub(xmul(2.0, n2), n0) : 2.0 * n2 - n0; };
 
     if constexpr (SCH == SCH_LIN) {
         int iU = 0, iV = 1;
         for (int s = 0; s < K; ++s) {
-            const int u0 = (K - 1 - s) * p.ext;
-            int64_t lo, hi;
-            expand(u0, lo, hi);
-            double *XU = S[iU], *XV = S[iV];
-            CHUNK_LOOP(lo, hi) {
-                CHUNK_SETUP(hi)
-                double b[P];
-                bands<NS, P, EX>(p, LMEP_ROW_W, XU, c0, cnt, fast, base, b);
-                for (int q = 0; q < cnt; ++q) XV[c0 + q - base] = b[q];
-            }
+            int lo, hi;
+            expand((K - 1 - s) * p.ext, lo, hi);
+            double *XU = S(iU), *XV = S(iV);
+            const int rows[1] = {LMEP_ROW_W};
+            const double *const X[1] = {XU};
+            run_pass<NS, P, EX, PN, 1>(p, lo, hi, fLo, fHi, base, lbase, rows, X,
+                                       [&](int l, const double *v) { XV[l] = v[0]; });
             pin_pass(XV, lo, hi, none);
             refresh(XV);
             __syncthreads();
-            int t = iU; iU = iV; iV = t;
+            const int t = iU; iU = iV; iV = t;
         }
         for (int64_t i = O0 + tid; i < O1; i += nt) {
-            const double v = S[iU][i - base];
+            const double v = S(iU)[i - base];
             p.u_out[i - p.off] = v;
             if (!isfinite(v)) *p.flag = 1;
         }
     } else if constexpr (SCH == SCH_ETDRK4) {
-        // role -> slot
+        // role -> slot; T2 shares WH's slot
         enum { U, N0, WH, A, N1, B, S12, C, N3, UN, NR };
         int sl[NR];
-        if (cv) {
+        if constexpr (cv) {
             sl[U] = 0; sl[N0] = 1; sl[WH] = 2; sl[A] = 3; sl[N3] = 3; sl[N1] = 4; sl[S12] = 4;
             sl[B] = 5; sl[C] = 5; sl[UN] = 6;
         } else {
@@ -321,148 +372,130 @@ __global__ void __launch_bounds__(STEP_THREADS) step_kernel(const __grid_constan
         }
         for (int s = 0; s < K; ++s) {
             const int u0 = (K - 1 - s) * p.ext;
-            double *XU = S[sl[U]], *XN0 = S[sl[N0]], *XWH = S[sl[WH]], *XA = S[sl[A]];
-            double *XN1 = S[sl[N1]], *XB = S[sl[B]], *XS12 = S[sl[S12]], *XC = S[sl[C]];
-            double *XN3 = S[sl[N3]], *XUN = S[sl[UN]];
+            double *XU = S(sl[U]), *XN0 = S(sl[N0]), *XWH = S(sl[WH]), *XA = S(sl[A]);
+            double *XN1 = S(sl[N1]), *XB = S(sl[B]), *XS12 = S(sl[S12]), *XC = S(sl[C]);
+            double *XN3 = S(sl[N3]), *XUN = S(sl[UN]);
             double *XT2 = XWH;
-            int64_t lo, hi;
-            // P1: n0 = N(u)
+            int lo, hi;
+            // P1: n0 = N(u)  (pointwise N: step 0 was fused into the load)
             expand(u0 + 4 + 3 * cv, lo, hi);
-            CHUNK_LOOP(lo, hi) {
-                CHUNK_SETUP(hi)
-                double du[P];
-                if (cv) bands<NS, P, EX>(p, LMEP_ROW_D1, XU, c0, cnt, fast, base, du);
-                for (int q = 0; q < cnt; ++q) {
-                    const int64_t si = c0 + q - base;
-                    XN0[si] = nlp<EX>(nlk, XU[si], cv ? du[q] : 0.0);
-                }
+            if (!cv && s == 0) {
+            } else if constexpr (cv) {
+                const int rows[1] = {LMEP_ROW_D1};
+                const double *const X[1] = {XU};
+                run_pass<NS, P, EX, PN, 1>(p, lo, hi, fLo, fHi, base, lbase, rows, X,
+                    [&](int l, const double *v) { XN0[l] = nlp<EX>(nlk, XU[l], v[0]); });
+            } else {
+                run_pointwise(lo, hi, [&](int l) { XN0[l] = nlp<EX>(nlk, XU[l], 0.0); });
             }
-            refresh(XN0);
-            __syncthreads();
-            // P2: whu = wh.u ; a = whu + p1h.n0 [pin] ; (cubic) n1 = N(a)
+            if (cv || s > 0) {
+                refresh(XN0);
+                __syncthreads();
+            }
+            // P2: whu = wh.u ; a = whu + p1h.n0 [pin] ; (pointwise N) n1 = N(a)
             expand(u0 + 3 + 3 * cv, lo, hi);
-            CHUNK_LOOP(lo, hi) {
-                CHUNK_SETUP(hi)
-                double bw[P], bp[P];
-                bands<NS, P, EX>(p, LMEP_ROW_WHALF, XU, c0, cnt, fast, base, bw);
-                bands<NS, P, EX>(p, LMEP_ROW_P1HALF, XN0, c0, cnt, fast, base, bp);
-                for (int q = 0; q < cnt; ++q) {
-                    const int64_t si = c0 + q - base;
-                    const double a = padd<EX>(bw[q], bp[q]);
-                    XWH[si] = bw[q];
-                    XA[si] = a;
-                    if (!cv) XN1[si] = nlp<EX>(nlk, a, 0.0);
-                }
+            {
+                const int rows[2] = {LMEP_ROW_WHALF, LMEP_ROW_P1HALF};
+                const double *const X[2] = {XU, XN0};
+                run_pass<NS, P, EX, PN, 2>(p, lo, hi, fLo, fHi, base, lbase, rows, X,
+                    [&](int l, const double *v) {
+                        const double a = padd<EX>(v[0], v[1]);
+                        XWH[l] = v[0];
+                        XA[l] = a;
+                        if constexpr (!cv) XN1[l] = nlp<EX>(nlk, a, 0.0);
+                    });
             }
-            pin_pass(XA, lo, hi, [&](int64_t si, double v) { if (!cv) XN1[si] = nlp<EX>(nlk, v, 0.0); });
+            pin_pass(XA, lo, hi, [&](int l, double v) { if constexpr (!cv) XN1[l] = nlp<EX>(nlk, v, 0.0); });
             refresh(XWH);
             refresh(XA);
-            if (!cv) refresh(XN1);
+            if constexpr (!cv) refresh(XN1);
             __syncthreads();
             // P3 (convective): n1 = N(a)
-            if (cv) {
+            if constexpr (cv) {
                 expand(u0 + 3 + 2 * cv, lo, hi);
-                CHUNK_LOOP(lo, hi) {
-                    CHUNK_SETUP(hi)
-                    double da[P];
-                    bands<NS, P, EX>(p, LMEP_ROW_D1, XA, c0, cnt, fast, base, da);
-                    for (int q = 0; q < cnt; ++q) {
-                        const int64_t si = c0 + q - base;
-                        XN1[si] = nlp<EX>(nlk, XA[si], da[q]);
-                    }
-                }
+                const int rows[1] = {LMEP_ROW_D1};
+                const double *const X[1] = {XA};
+                run_pass<NS, P, EX, PN, 1>(p, lo, hi, fLo, fHi, base, lbase, rows, X,
+                    [&](int l, const double *v) { XN1[l] = nlp<EX>(nlk, XA[l], v[0]); });
                 refresh(XN1);
                 __syncthreads();
             }
-            // P4: b = whu + p1h.n1 [pin] ; (cubic) n2 = N(b), t2 = 2 n2 - n0, s12 = n1 + n2
+            // P4: b = whu + p1h.n1 [pin] ; (pointwise N) n2 = N(b), t2 = 2 n2 - n0, s12 = n1 + n2
             expand(u0 + 2 + 2 * cv, lo, hi);
-            CHUNK_LOOP(lo, hi) {
-                CHUNK_SETUP(hi)
-                double bp[P];
-                bands<NS, P, EX>(p, LMEP_ROW_P1HALF, XN1, c0, cnt, fast, base, bp);
-                for (int q = 0; q < cnt; ++q) {
-                    const int64_t si = c0 + q - base;
-                    const double b = padd<EX>(XWH[si], bp[q]);
-                    XB[si] = b;
-                    if (!cv) {
-                        const double n2 = nlp<EX>(nlk, b, 0.0);
-                        XT2[si] = EX ? xsub(xmul(2.0, n2), XN0[si]) : 2.0 * n2 - XN0[si];
-                        XS12[si] = padd<EX>(XN1[si], n2);
-                    }
-                }
+            {
+                const int rows[1] = {LMEP_ROW_P1HALF};
+                const double *const X[1] = {XN1};
+                run_pass<NS, P, EX, PN, 1>(p, lo, hi, fLo, fHi, base, lbase, rows, X,
+                    [&](int l, const double *v) {
+                        const double b = padd<EX>(XWH[l], v[0]);
+                        XB[l] = b;
+                        if constexpr (!cv) {
+                            const double n2 = nlp<EX>(nlk, b, 0.0);
+                            XT2[l] = sub2(n2, XN0[l]);
+                            XS12[l] = padd<EX>(XN1[l], n2);
+                        }
+                    });
             }
-            pin_pass(XB, lo, hi, [&](int64_t si, double v) {
-                if (!cv) {
+            pin_pass(XB, lo, hi, [&](int l, double v) {
+                if constexpr (!cv) {
                     const double n2 = nlp<EX>(nlk, v, 0.0);
-                    XT2[si] = EX ? xsub(xmul(2.0, n2), XN0[si]) : 2.0 * n2 - XN0[si];
-                    XS12[si] = padd<EX>(XN1[si], n2);
+                    XT2[l] = sub2(n2, XN0[l]);
+                    XS12[l] = padd<EX>(XN1[l], n2);
                 }
             });
             refresh(XB);
-            if (!cv) { refresh(XT2); refresh(XS12); }
+            if constexpr (!cv) { refresh(XT2); refresh(XS12); }
             __syncthreads();
             // P5 (convective): n2 = N(b), t2 = 2 n2 - n0, s12 = n1 + n2
-            if (cv) {
+            if constexpr (cv) {
                 expand(u0 + 2 + cv, lo, hi);
-                CHUNK_LOOP(lo, hi) {
-                    CHUNK_SETUP(hi)
-                    double db[P];
-                    bands<NS, P, EX>(p, LMEP_ROW_D1, XB, c0, cnt, fast, base, db);
-                    for (int q = 0; q < cnt; ++q) {
-                        const int64_t si = c0 + q - base;
-                        const double n2 = nlp<EX>(nlk, XB[si], db[q]);
-                        XT2[si] = EX ? xsub(xmul(2.0, n2), XN0[si]) : 2.0 * n2 - XN0[si];
-                        XS12[si] = padd<EX>(XN1[si], n2);
-                    }
-                }
+                const int rows[1] = {LMEP_ROW_D1};
+                const double *const X[1] = {XB};
+                run_pass<NS, P, EX, PN, 1>(p, lo, hi, fLo, fHi, base, lbase, rows, X,
+                    [&](int l, const double *v) {
+                        const double n2 = nlp<EX>(nlk, XB[l], v[0]);
+                        XT2[l] = sub2(n2, XN0[l]);
+                        XS12[l] = padd<EX>(XN1[l], n2);
+                    });
                 refresh(XT2);
                 refresh(XS12);
                 __syncthreads();
             }
-            // P6: c = wh.a + p1h.t2 [pin] ; (cubic) n3 = N(c)
+            // P6: c = wh.a + p1h.t2 [pin] ; (pointwise N) n3 = N(c)
             expand(u0 + 1 + cv, lo, hi);
-            CHUNK_LOOP(lo, hi) {
-                CHUNK_SETUP(hi)
-                double ba[P], bt[P];
-                bands<NS, P, EX>(p, LMEP_ROW_WHALF, XA, c0, cnt, fast, base, ba);
-                bands<NS, P, EX>(p, LMEP_ROW_P1HALF, XT2, c0, cnt, fast, base, bt);
-                for (int q = 0; q < cnt; ++q) {
-                    const int64_t si = c0 + q - base;
-                    const double c = padd<EX>(ba[q], bt[q]);
-                    XC[si] = c;
-                    if (!cv) XN3[si] = nlp<EX>(nlk, c, 0.0);
-                }
+            {
+                const int rows[2] = {LMEP_ROW_WHALF, LMEP_ROW_P1HALF};
+                const double *const X[2] = {XA, XT2};
+                run_pass<NS, P, EX, PN, 2>(p, lo, hi, fLo, fHi, base, lbase, rows, X,
+                    [&](int l, const double *v) {
+                        const double c = padd<EX>(v[0], v[1]);
+                        XC[l] = c;
+                        if constexpr (!cv) XN3[l] = nlp<EX>(nlk, c, 0.0);
+                    });
             }
-            pin_pass(XC, lo, hi, [&](int64_t si, double v) { if (!cv) XN3[si] = nlp<EX>(nlk, v, 0.0); });
+            pin_pass(XC, lo, hi, [&](int l, double v) { if constexpr (!cv) XN3[l] = nlp<EX>(nlk, v, 0.0); });
             refresh(XC);
-            if (!cv) refresh(XN3);
+            if constexpr (!cv) refresh(XN3);
             __syncthreads();
             // P7 (convective): n3 = N(c)
-            if (cv) {
+            if constexpr (cv) {
                 expand(u0 + 1, lo, hi);
-                CHUNK_LOOP(lo, hi) {
-                    CHUNK_SETUP(hi)
-                    double dc[P];
-                    bands<NS, P, EX>(p, LMEP_ROW_D1, XC, c0, cnt, fast, base, dc);
-                    for (int q = 0; q < cnt; ++q) {
-                        const int64_t si = c0 + q - base;
-                        XN3[si] = nlp<EX>(nlk, XC[si], dc[q]);
-                    }
-                }
+                const int rows[1] = {LMEP_ROW_D1};
+                const double *const X[1] = {XC};
+                run_pass<NS, P, EX, PN, 1>(p, lo, hi, fLo, fHi, base, lbase, rows, X,
+                    [&](int l, const double *v) { XN3[l] = nlp<EX>(nlk, XC[l], v[0]); });
                 refresh(XN3);
                 __syncthreads();
             }
             // P8: u' = ((w.u + alpha.n0) + beta.s12) + gamma.n3 [pin]
             expand(u0, lo, hi);
-            CHUNK_LOOP(lo, hi) {
-                CHUNK_SETUP(hi)
-                double b0[P], b1[P], b2[P], b3[P];
-                bands<NS, P, EX>(p, LMEP_ROW_W, XU, c0, cnt, fast, base, b0);
-                bands<NS, P, EX>(p, LMEP_ROW_ALPHA, XN0, c0, cnt, fast, base, b1);
-                bands<NS, P, EX>(p, LMEP_ROW_BETA, XS12, c0, cnt, fast, base, b2);
-                bands<NS, P, EX>(p, LMEP_ROW_GAMMA, XN3, c0, cnt, fast, base, b3);
-                for (int q = 0; q < cnt; ++q)
-                    XUN[c0 + q - base] = padd<EX>(padd<EX>(padd<EX>(b0[q], b1[q]), b2[q]), b3[q]);
+            {
+                const int rows[4] = {LMEP_ROW_W, LMEP_ROW_ALPHA, LMEP_ROW_BETA, LMEP_ROW_GAMMA};
+                const double *const X[4] = {XU, XN0, XS12, XN3};
+                run_pass<NS, P, EX, PN, 4>(p, lo, hi, fLo, fHi, base, lbase, rows, X,
+                    [&](int l, const double *v) {
+                        XUN[l] = padd<EX>(padd<EX>(padd<EX>(v[0], v[1]), v[2]), v[3]);
+                    });
             }
             pin_pass(XUN, lo, hi, none);
             refresh(XUN);
@@ -476,7 +509,7 @@ __global__ void __launch_bounds__(STEP_THREADS) step_kernel(const __grid_constan
             sl[U] = newU;
         }
         for (int64_t i = O0 + tid; i < O1; i += nt) {
-            const double v = S[sl[U]][i - base];
+            const double v = S(sl[U])[i - base];
             p.u_out[i - p.off] = v;
             if (!isfinite(v)) *p.flag = 1;
         }
@@ -484,36 +517,36 @@ __global__ void __launch_bounds__(STEP_THREADS) step_kernel(const __grid_constan
         int iU = 0, iQ = 1, iK = 2, iD = 3, iV = 4;
         for (int s = 0; s < K; ++s) {
             const int u0 = (K - 1 - s) * p.ext;
-            double *XU = S[iU], *XQ = S[iQ], *XK = S[iK], *XD = S[iD], *XV = S[iV];
-            int64_t lo, hi;
+            double *XU = S(iU), *XQ = S(iQ), *XK = S(iK), *XD = S(iD), *XV = S(iV);
+            int lo, hi;
             // P1: nk = N(u), d = nk - n_{k-1}
             expand(u0 + 1, lo, hi);
-            CHUNK_LOOP(lo, hi) {
-                CHUNK_SETUP(hi)
-                double du[P];
-                if (cv) bands<NS, P, EX>(p, LMEP_ROW_D1, XU, c0, cnt, fast, base, du);
-                for (int q = 0; q < cnt; ++q) {
-                    const int64_t si = c0 + q - base;
-                    const double nk = nlp<EX>(nlk, XU[si], cv ? du[q] : 0.0);
-                    XK[si] = nk;
-                    XD[si] = EX ? xsub(nk, XQ[si]) : nk - XQ[si];
-                }
+            auto epi1 = [&](int l, double du) {
+                const double nk = nlp<EX>(nlk, XU[l], du);
+                XK[l] = nk;
+                XD[l] = EX ? xsub(nk, XQ[l]) : nk - XQ[l];
+            };
+            if constexpr (cv) {
+                const int rows[1] = {LMEP_ROW_D1};
+                const double *const X[1] = {XU};
+                run_pass<NS, P, EX, PN, 1>(p, lo, hi, fLo, fHi, base, lbase, rows, X,
+                                           [&](int l, const double *v) { epi1(l, v[0]); });
+            } else {
+                run_pointwise(lo, hi, [&](int l) { epi1(l, 0.0); });
             }
             refresh(XK);
             refresh(XD);
             __syncthreads();
             // P2: u' = (W u + P1 nk) + P2 d / dt   (timestep.py:206-210)
             expand(u0, lo, hi);
-            CHUNK_LOOP(lo, hi) {
-                CHUNK_SETUP(hi)
-                double b0[P], b1[P], b2[P];
-                bands<NS, P, EX>(p, LMEP_ROW_W, XU, c0, cnt, fast, base, b0);
-                bands<NS, P, EX>(p, LMEP_ROW_ALPHA, XK, c0, cnt, fast, base, b1);
-                bands<NS, P, EX>(p, LMEP_ROW_BETA, XD, c0, cnt, fast, base, b2);
-                for (int q = 0; q < cnt; ++q) {
-                    const double t = EX ? xdiv(b2[q], p.dt) : b2[q] * (1.0 / p.dt);
-                    XV[c0 + q - base] = padd<EX>(padd<EX>(b0[q], b1[q]), t);
-                }
+            {
+                const int rows[3] = {LMEP_ROW_W, LMEP_ROW_ALPHA, LMEP_ROW_BETA};
+                const double *const X[3] = {XU, XK, XD};
+                run_pass<NS, P, EX, PN, 3>(p, lo, hi, fLo, fHi, base, lbase, rows, X,
+                    [&](int l, const double *v) {
+                        const double d = EX ? xdiv(v[2], p.dt) : v[2] * (1.0 / p.dt);
+                        XV[l] = padd<EX>(padd<EX>(v[0], v[1]), d);
+                    });
             }
             pin_pass(XV, lo, hi, none);
             refresh(XV);
@@ -523,37 +556,48 @@ __global__ void __launch_bounds__(STEP_THREADS) step_kernel(const __grid_constan
             t = iU; iU = iV; iV = t;
         }
         for (int64_t i = O0 + tid; i < O1; i += nt) {
-            const double v = S[iU][i - base];
+            const double v = S(iU)[i - base];
             p.u_out[i - p.off] = v;
-            p.q_out[i - p.off] = S[iQ][i - base];
+            p.q_out[i - p.off] = S(iQ)[i - base];
             if (!isfinite(v)) *p.flag = 1;
         }
     }
-#undef CHUNK_LOOP
-#undef CHUNK_SETUP
+#undef S
 }
 
-template <int SCH, bool EX, int P>
+// Per-node rows of the ETD schemes use the generic-n instantiation only.
+template <int SCH, bool EX, int P, int NLK, bool PN = false>
 inline int launch_ns(int ns_case, const StepParams &p, dim3 grid, size_t shm, cudaStream_t st)
 {
     void (*k)(StepParams) = nullptr;
-    switch (ns_case) {
-    case 7: k = step_kernel<SCH, 7, EX, P>; break;
-    case 9: k = step_kernel<SCH, 9, EX, P>; break;
-    case 11: k = step_kernel<SCH, 11, EX, P>; break;
-    case 13: k = step_kernel<SCH, 13, EX, P>; break;
-    default: k = step_kernel<SCH, 0, EX, P>; break;
+    if (SCH != SCH_LIN && p.wmode == LMEP_W_PERNODE) {
+        k = step_kernel<SCH, 0, EX, P, NLK, true>;
+    } else {
+        switch (ns_case) {
+        case 7: k = step_kernel<SCH, 7, EX, P, NLK, PN>; break;
+        case 9: k = step_kernel<SCH, 9, EX, P, NLK, PN>; break;
+        case 11: k = step_kernel<SCH, 11, EX, P, NLK, PN>; break;
+        case 13: k = step_kernel<SCH, 13, EX, P, NLK, PN>; break;
+        default: k = step_kernel<SCH, 0, EX, P, NLK, PN>; break;
+        }
     }
     if (shm > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
         if (e != cudaSuccess) { set_last_error("cudaFuncSetAttribute", e); return LMEP_CUDA_ERROR; }
     }
-    k<<<grid, STEP_THREADS, shm, st>>>(p);
+    k<<<grid, p.threads, shm, st>>>(p);
     return launch_status("step_kernel");
 }
 
 int launch_scheme_lin(bool pernode, const StepParams &p, dim3 grid, size_t shm, cudaStream_t st);
-int launch_scheme_etdrk4(bool exact, const StepParams &p, dim3 grid, size_t shm, cudaStream_t st);
-int launch_scheme_etd2(bool exact, const StepParams &p, dim3 grid, size_t shm, cudaStream_t st);
+#define STEP_DECL(S, L) \
+    int launch_scheme_##S##_##L(bool exact, const StepParams &p, dim3 grid, size_t shm, cudaStream_t st);
+STEP_DECL(etdrk4, none)
+STEP_DECL(etdrk4, convective)
+STEP_DECL(etdrk4, cubic)
+STEP_DECL(etd2, none)
+STEP_DECL(etd2, convective)
+STEP_DECL(etd2, cubic)
+#undef STEP_DECL
 
 }  // namespace lmep

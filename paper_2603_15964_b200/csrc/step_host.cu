@@ -59,7 +59,8 @@ int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded
     if (tile <= 0) {
         if (pernode) tile = 2048;
         else if (sch == SCH_LIN) tile = 4096;
-        else tile = 2048;
+        else if (sch == SCH_ETD2) tile = 2048;
+        else tile = 1024;
         // small grids: enough tiles to cover the SMs
         while (tile > 256 && (g.nloc + tile - 1) / tile < 2 * nsm) tile /= 2;
         tile = std::min<int64_t>(tile, g.nloc);
@@ -87,8 +88,14 @@ static int launch_step(int sch, bool exact, bool pernode, const StepParams &p, d
                        size_t shm, cudaStream_t st)
 {
     if (sch == SCH_LIN) return launch_scheme_lin(pernode, p, grid, shm, st);
-    if (sch == SCH_ETDRK4) return launch_scheme_etdrk4(exact, p, grid, shm, st);
-    return launch_scheme_etd2(exact, p, grid, shm, st);
+    if (sch == SCH_ETDRK4) {
+        if (p.nl == LMEP_NL_CONVECTIVE) return launch_scheme_etdrk4_convective(exact, p, grid, shm, st);
+        if (p.nl == LMEP_NL_CUBIC) return launch_scheme_etdrk4_cubic(exact, p, grid, shm, st);
+        return launch_scheme_etdrk4_none(exact, p, grid, shm, st);
+    }
+    if (p.nl == LMEP_NL_CONVECTIVE) return launch_scheme_etd2_convective(exact, p, grid, shm, st);
+    if (p.nl == LMEP_NL_CUBIC) return launch_scheme_etd2_cubic(exact, p, grid, shm, st);
+    return launch_scheme_etd2_none(exact, p, grid, shm, st);
 }
 
 struct StepCall {
@@ -184,6 +191,8 @@ int run_steps(const StepCall &c)
     p.dt = c.dt;
     p.ext = step_ext(c.sch, c.nl);
     p.tile = t.tile;
+    p.threads = t.threads > 0 ? t.threads : STEP_THREADS;
+    if (p.threads % 32 != 0 || p.threads > STEP_THREADS) return LMEP_INVALID_CONFIG;
     const int P = pernode ? 1 : 5;
     const int64_t rad = (int64_t)p.ext * (p.eL + p.eR);
     p.slot_len = t.ring ? (g.N + g.n + SLOT_PAD + P) : (t.tile + (int64_t)t.ksteps * rad + SLOT_PAD + P);
