@@ -291,6 +291,17 @@ def combine_rows(parts: list[CompactRows], coeffs) -> CompactRows:
 # ---------------------------------------------------------------------------
 # stepping (K3-K5)
 # ---------------------------------------------------------------------------
+def c_halo(halo) -> nat.LmepHalo | None:
+    """halo = (left, right, hist_left, hist_right, width) device tensors (or None)."""
+    if halo is None:
+        return None
+    h = nat.LmepHalo()
+    h.left, h.right = nat.ptr(halo[0]), nat.ptr(halo[1])
+    h.hist_left, h.hist_right = nat.ptr(halo[2]), nat.ptr(halo[3])
+    h.width = int(halo[4])
+    return h
+
+
 def c_grid(layout: StencilSet, off: int = 0, nloc: int | None = None) -> nat.LmepGrid:
     g = nat.LmepGrid()
     g.N = layout.N
@@ -335,11 +346,15 @@ def step(scheme: int, rows: CompactRows, u: torch.Tensor, steps: int, *, bc: BC 
          nl: int = nat.NL_NONE, exact: bool = True, hist: torch.Tensor | None = None,
          delta_t: float = 0.0, nl0_out: torch.Tensor | None = None, tuning=None,
          flag: torch.Tensor | None = None, out: torch.Tensor | None = None,
-         hist_out: torch.Tensor | None = None, scratch: torch.Tensor | None = None):
-    """Run `steps` steps of a scheme on the whole grid (single shard).
+         hist_out: torch.Tensor | None = None, scratch: torch.Tensor | None = None,
+         off: int = 0, nloc: int | None = None, halo=None):
+    """Run `steps` steps of a scheme on the whole grid, or on the shard
+    [off, off+nloc) with ghost cells `halo` (see c_halo).
     Returns the new u (and the new history for ETD2)."""
     lay = rows.layout
-    g = c_grid(lay)
+    g = c_grid(lay, off, nloc)
+    hc = c_halo(halo)
+    hp = C.byref(hc) if hc is not None else None
     w = rows.c_weights()
     b = (bc or BC()).c()
     u = u.contiguous()
@@ -351,19 +366,19 @@ def step(scheme: int, rows: CompactRows, u: torch.Tensor, steps: int, *, bc: BC 
     s = nat.stream_handle()
     fp = nat.ptr(flag)
     if scheme == nat.SCH_LIN:
-        st = L.lmep_step_linear(C.byref(g), C.byref(w), C.byref(b), None, nat.ptr(u),
+        st = L.lmep_step_linear(C.byref(g), C.byref(w), C.byref(b), hp, nat.ptr(u),
                                 nat.ptr(out), nat.ptr(scratch), int(steps), flags, tp, fp, s)
         nat.check(st, "lmep_step_linear")
         return out
     if scheme == nat.SCH_ETDRK4:
-        st = L.lmep_step_etdrk4(C.byref(g), C.byref(w), C.byref(b), None, nl, nat.ptr(u),
+        st = L.lmep_step_etdrk4(C.byref(g), C.byref(w), C.byref(b), hp, nl, nat.ptr(u),
                                 nat.ptr(out), nat.ptr(scratch), int(steps), nat.ptr(nl0_out),
                                 flags, tp, fp, s)
         nat.check(st, "lmep_step_etdrk4")
         return out
     hist = hist.contiguous()
     hist_out = torch.empty_like(hist) if hist_out is None else hist_out
-    st = L.lmep_step_etd2(C.byref(g), C.byref(w), C.byref(b), None, nl, float(delta_t),
+    st = L.lmep_step_etd2(C.byref(g), C.byref(w), C.byref(b), hp, nl, float(delta_t),
                           nat.ptr(u), nat.ptr(hist), nat.ptr(out), nat.ptr(hist_out),
                           nat.ptr(scratch), int(steps), flags, tp, fp, s)
     nat.check(st, "lmep_step_etd2")

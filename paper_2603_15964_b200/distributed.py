@@ -1,0 +1,307 @@
+"""Slab-sharded stepping across GPUs.
+
+One process per GPU.  The grid is cut into contiguous slabs; every rank
+harvests what its slab needs without communication (the <= 2n+1 stencil
+classes redundantly, or its own nodes' per-node rows) and advances its slab
+with the fused step kernels.  The only data exchange is the halo: before a
+launch that fuses k steps, each rank sends its first and last
+G = k * ext * max(row, n-1-row) nodes to its neighbours (periodic ring or
+open chain) with NCCL point-to-point over NVLink.  A deep halo (k > 1)
+trades a little redundant edge compute for k times fewer exchanges.
+
+The exchange is an object with one method, ``exchange(u_local, ghosts)``,
+so the same driver runs with
+
+  * ``NcclHalo``   -- torch.distributed batch_isend_irecv (NCCL on GPUs,
+                      gloo on CPU for the host-side tests);
+  * ``LocalHalo``  -- P virtual shards inside one process (device copies),
+                      used to check sharded == unsharded on a single GPU.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _native as nat
+from . import _ops
+from .errors import InvalidConfig
+from .grid import Grid, as_stencil_set
+from .harvest import harvest_compact
+from .timestep import (Prepared, SchemeConfig, SemiLinearProblem, _bc_for, _etdrk4_bank,
+                       _nl_kind, _scaled, close_initial, derivative_compact)
+
+
+def partition(N: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous slab [off, off+nloc) of rank; sizes differ by at most one."""
+    base, rem = divmod(int(N), int(world))
+    off = rank * base + min(rank, rem)
+    return off, base + (1 if rank < rem else 0)
+
+
+def neighbours(rank: int, world: int, periodic: bool) -> tuple[int | None, int | None]:
+    if world == 1:
+        return (None, None)
+    left = (rank - 1) % world if (periodic or rank > 0) else None
+    right = (rank + 1) % world if (periodic or rank < world - 1) else None
+    return left, right
+
+
+class NcclHalo:
+    """Halo exchange over torch.distributed point-to-point (one group call).
+
+    Posting order per rank: send right edge -> right, recv left ghosts <- left,
+    send left edge -> left, recv right ghosts <- right.  Messages between a
+    pair match in posting order, which also makes the 2-rank periodic ring
+    (left == right) come out right.
+    """
+
+    def __init__(self, rank: int, world: int, periodic: bool, group=None):
+        self.rank, self.world, self.group = rank, world, group
+        self.left, self.right = neighbours(rank, world, periodic)
+
+    def exchange(self, u: torch.Tensor, gl: torch.Tensor, gr: torch.Tensor) -> None:
+        import torch.distributed as dist
+        G = gl.numel()
+        if u.numel() < G:
+            raise InvalidConfig(f"slab of {u.numel()} nodes is narrower than the halo {G}")
+        ops = []
+        if self.right is not None:
+            ops.append(dist.P2POp(dist.isend, u[u.numel() - G:].contiguous(), self.right, self.group))
+        if self.left is not None:
+            ops.append(dist.P2POp(dist.irecv, gl, self.left, self.group))
+            ops.append(dist.P2POp(dist.isend, u[:G].contiguous(), self.left, self.group))
+        if self.right is not None:
+            ops.append(dist.P2POp(dist.irecv, gr, self.right, self.group))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+
+
+class LocalHalo:
+    """P virtual shards of one process: ghosts are copied from the neighbour
+    shards' device buffers (registered in ``shards``)."""
+
+    def __init__(self, shards: list, rank: int, periodic: bool):
+        self.shards, self.rank = shards, rank
+        self.left, self.right = neighbours(rank, len(shards), periodic)
+        self.which = "u"
+
+    def exchange(self, u: torch.Tensor, gl: torch.Tensor, gr: torch.Tensor) -> None:
+        G = gl.numel()
+        if self.left is not None:
+            src = getattr(self.shards[self.left], self.which)
+            gl.copy_(src[src.numel() - G:])
+        if self.right is not None:
+            src = getattr(self.shards[self.right], self.which)
+            gr.copy_(src[:G])
+
+
+@dataclass
+class SlabPlan:
+    off: int
+    nloc: int
+    width: int          # ghost cells per side
+    ksteps: int         # steps per exchange
+
+
+def _ext(scheme: str, nl: int) -> int:
+    cv = 1 if nl == nat.NL_CONVECTIVE else 0
+    return {"linear": 1, "etdrk4": 4 + 4 * cv, "etd-multistep": 1 + cv}[scheme]
+
+
+class ShardedStepper:
+    """Advance one slab of a run (the sharded counterpart of timestep.Stepper)."""
+
+    def __init__(self, grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
+                 delta_t: float, rank: int, world: int, exchanger, *, exact: bool = True,
+                 ksteps: int | None = None, tuning=None):
+        sset = as_stencil_set(grid, stencils)
+        self.sset, self.rank, self.world = sset, rank, world
+        self.exact, self.tuning = exact, tuning
+        nl = _nl_kind(problem)
+        off, nloc = partition(sset.N, world, rank)
+        reach = max(sset.row, sset.n - 1 - sset.row)
+        ext = _ext(scheme.kind, nl)
+        per_node = _is_per_node(grid, problem)
+        if ksteps is None:
+            ksteps = 1 if per_node and scheme.kind == "linear" else \
+                max(1, min(16, nloc // (4 * ext * max(reach, 1))))
+        if per_node and scheme.kind == "linear":
+            ksteps = 1                      # per-node rows of halo nodes are not held
+        if per_node and scheme.kind != "linear" and world > 1:
+            raise InvalidConfig("sharded ETD schemes need shared or class rows")
+        width = ksteps * ext * reach
+        if world > 1 and width > nloc:
+            raise InvalidConfig(f"slab of {nloc} nodes narrower than the halo {width}")
+        self.plan = SlabPlan(off, nloc, width, ksteps)
+        self.prep = _prepare_shard(grid, sset, problem, scheme, delta_t, off, nloc)
+        self.ex = exchanger
+        dev = nat.device()
+        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        G = max(width, 1)
+        self.gl = torch.zeros(G, dtype=torch.float64, device=dev)
+        self.gr = torch.zeros(G, dtype=torch.float64, device=dev)
+        self.ql = torch.zeros(G, dtype=torch.float64, device=dev)
+        self.qr = torch.zeros(G, dtype=torch.float64, device=dev)
+        self.u = None
+        self.hist = None
+        self.done = 0
+
+    # ---------------------------------------------------------------------
+    def set_initial(self, u0_global) -> None:
+        """Slice the (closed) global initial data for this slab."""
+        u = _ops.dev_f64(u0_global)
+        u = close_initial(u, self.sset, self.prep.bc)
+        self.u = u[self.plan.off:self.plan.off + self.plan.nloc].contiguous()
+
+    def _halo(self, k):
+        w = k * _ext(self.prep.scheme, self.prep.nl) * max(self.sset.row, self.sset.n - 1 - self.sset.row)
+        if self.world == 1:
+            return None
+        return (self.gl[:w] if w else self.gl, self.gr[:w] if w else self.gr,
+                self.ql[:w] if w else self.ql, self.qr[:w] if w else self.qr, max(w, 1))
+
+    def _exchange(self, k, hist=False):
+        if self.world == 1:
+            return
+        h = self._halo(k)
+        if isinstance(self.ex, LocalHalo):
+            self.ex.which = "hist" if hist else "u"
+        if hist:
+            self.ex.exchange(self.hist, h[2], h[3])
+        else:
+            self.ex.exchange(self.u, h[0], h[1])
+
+    def step_chunk(self, k: int) -> None:
+        """k <= plan.ksteps steps with one halo exchange.  With LocalHalo the
+        caller must run exchange_phase on all shards before compute_phase."""
+        self.exchange_phase(k)
+        self.compute_phase(k)
+
+    def exchange_phase(self, k: int) -> None:
+        p = self.prep
+        self._exchange(k)
+        if p.scheme == "etd-multistep" and self.hist is not None:
+            self._exchange(k, hist=True)
+
+    def _tuning(self, k):
+        return {**(self.tuning or {}), "ksteps": k}
+
+    def compute_phase(self, k: int) -> None:
+        p = self.prep
+        kw = dict(bc=p.bc, nl=p.nl, exact=self.exact, tuning=self._tuning(k), flag=self.flag,
+                  off=self.plan.off, nloc=self.plan.nloc, halo=self._halo(k))
+        if p.scheme == "linear":
+            self.u = _ops.step(nat.SCH_LIN, p.bank, self.u, k, **kw)
+        elif p.scheme == "etdrk4":
+            self.u = _ops.step(nat.SCH_ETDRK4, p.bank, self.u, k, **kw)
+        else:
+            if self.hist is None:
+                raise InvalidConfig("call warm_up() before multistep chunks")
+            self.u, self.hist = _ops.step(nat.SCH_ETD2, p.bank, self.u, k, hist=self.hist,
+                                          delta_t=p.delta_t, **kw)
+        self.done += k
+
+    def warm_up_compute(self) -> None:
+        """ETD multistep: history N(u0) and one ETDRK4 warm-up step
+        (timestep.py:375-378); its halo must be exchanged first (k=1)."""
+        p = self.prep
+        self.hist = torch.zeros_like(self.u)
+        if p.s == 2:
+            kw = dict(bc=p.bc, nl=p.nl, exact=self.exact, tuning=self._tuning(1),
+                      flag=self.flag, off=self.plan.off, nloc=self.plan.nloc,
+                      halo=self._halo_etdrk4())
+            self.u = _ops.step(nat.SCH_ETDRK4, p.warm, self.u, 1, nl0_out=self.hist, **kw)
+            self.done += 1
+
+    def _halo_etdrk4(self):
+        if self.world == 1:
+            return None
+        w = _ext("etdrk4", self.prep.nl) * max(self.sset.row, self.sset.n - 1 - self.sset.row)
+        return (self.wl[:w], self.wr[:w], self.wl[:w], self.wr[:w], w)
+
+    def warm_up_exchange(self) -> None:
+        if self.world == 1 or self.prep.s != 2:
+            return
+        w = _ext("etdrk4", self.prep.nl) * max(self.sset.row, self.sset.n - 1 - self.sset.row)
+        dev = self.u.device
+        self.wl = torch.zeros(w, dtype=torch.float64, device=dev)
+        self.wr = torch.zeros(w, dtype=torch.float64, device=dev)
+        if isinstance(self.ex, LocalHalo):
+            self.ex.which = "u"
+        self.ex.exchange(self.u, self.wl, self.wr)
+
+    def nonfinite(self) -> bool:
+        return bool(self.flag.item())
+
+
+def _is_per_node(grid: Grid, problem: SemiLinearProblem) -> bool:
+    from .localop import VariableCoefficientSpec
+    return isinstance(problem.linear, VariableCoefficientSpec) or \
+        (not grid.periodic and grid.uniform_spacing is None)
+
+
+def _prepare_shard(grid, sset, problem, scheme, delta_t, off, nloc) -> Prepared:
+    """timestep.prepare restricted to one slab (per-node rows of the slab only)."""
+    nl = _nl_kind(problem)
+    bc = _bc_for(grid, sset, problem.boundary)
+    frozen = (0, grid.size - 1) if problem.boundary.closed and problem.boundary.freeze_rows else ()
+    d1 = None
+    if nl == nat.NL_CONVECTIVE:
+        d1 = _scaled(derivative_compact(grid, sset, 1), float(problem.nonlinear_scale))
+    rng = (off, nloc)
+    spec = problem.linear
+    warm = None
+    if scheme.kind == "linear":
+        bank = harvest_compact(grid, sset, spec, delta_t, 1, frozen, node_range=rng)
+    elif scheme.kind == "etdrk4":
+        full = harvest_compact(grid, sset, spec, delta_t, 4, frozen, node_range=rng)
+        half = harvest_compact(grid, sset, spec, delta_t / 2, 2, frozen, node_range=rng)
+        bank = _etdrk4_bank(full, half, delta_t, d1)
+    else:
+        s = scheme.s
+        if s > 2:
+            raise InvalidConfig("etd-multistep with s >= 3 has no device kernel yet")
+        ops = harvest_compact(grid, sset, spec, delta_t, s + 1, frozen, node_range=rng)
+        parts = {nat.ROW_W: ops.row(0), nat.ROW_ALPHA: ops.row(1)}
+        if s == 2:
+            parts[nat.ROW_BETA] = ops.row(2)
+            full = harvest_compact(grid, sset, spec, delta_t, 4, frozen, node_range=rng)
+            half = harvest_compact(grid, sset, spec, delta_t / 2, 2, frozen, node_range=rng)
+            warm = _etdrk4_bank(full, half, delta_t, d1)
+        if d1 is not None:
+            parts[nat.ROW_D1] = d1
+        bank = _ops.rows_bank_for(sset, parts, max(parts) + 1 if d1 is not None else 3)
+    return Prepared(sset, scheme.kind, nl, bc, bank, warm, float(delta_t), scheme.s)
+
+
+def run_virtual_shards(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
+                       delta_t: float, steps: int, P: int, *, exact: bool = True,
+                       ksteps: int | None = None) -> torch.Tensor:
+    """P slabs advanced in one process with device-copy halos; returns the
+    gathered global solution.  Used to check that sharding is exact."""
+    shards: list[ShardedStepper] = []
+    for r in range(P):
+        shards.append(ShardedStepper(grid, stencils, problem, scheme, delta_t, r, P, None,
+                                     exact=exact, ksteps=ksteps))
+    for r, s in enumerate(shards):
+        s.ex = LocalHalo(shards, r, grid.periodic)
+        s.set_initial(problem.initial)
+    done = 0
+    if scheme.kind == "etd-multistep":
+        for s in shards:
+            s.warm_up_exchange()
+        for s in shards:
+            s.warm_up_compute()
+        done = shards[0].done
+    k = shards[0].plan.ksteps
+    while done < steps:
+        kk = min(k, steps - done)
+        for s in shards:
+            s.exchange_phase(kk)
+        for s in shards:
+            s.compute_phase(kk)
+        done += kk
+    return torch.cat([s.u for s in shards])

@@ -170,6 +170,7 @@ class _Plan:
     masks: np.ndarray             # [T] frozen bitmasks (uint64)
     nleft: int = 0
     nright: int = 0
+    uniform_rows: bool = False    # every item has target row sset.row and no frozen rows
 
 
 def _frozen_masks(sset: StencilSet, t: np.ndarray, frozen: list[int]) -> np.ndarray:
@@ -212,6 +213,11 @@ def _plan(grid: Grid, sset: StencilSet, frozen_nodes=(), force_pernode=False) ->
         t = np.concatenate([np.arange(nl), [N // 2], np.arange(N - nr, N)]).astype(np.int64)
         return _Plan(nat.W_CLASS, _coords_for(grid, sset, t), sset.target_rows(t),
                      _frozen_masks(sset, t, frozen), nl, nr)
+    if grid.periodic and not frozen:
+        # variable coefficients on a periodic grid: one window geometry for all nodes
+        coords = _coords_for(grid, sset, np.array([0]))
+        return _Plan(nat.W_PERNODE, coords, np.array([row]), np.zeros(1, np.uint64),
+                     uniform_rows=True)
     t = np.arange(N, dtype=np.int64)
     coords = _coords_for(grid, sset, np.array([0]) if grid.periodic else t)
     return _Plan(nat.W_PERNODE, coords, sset.target_rows(t), _frozen_masks(sset, t, frozen))
@@ -228,8 +234,11 @@ def _rows_from(plan: _Plan, sset: StencilSet, out: torch.Tensor) -> _ops.Compact
 
 
 def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
-                    frozen_nodes=(), stats: dict | None = None) -> _ops.CompactRows:
-    """Harvest w_lin and the raw dt^j phi_j rows (R = s) for the whole grid."""
+                    frozen_nodes=(), stats: dict | None = None,
+                    node_range: tuple[int, int] | None = None) -> _ops.CompactRows:
+    """Harvest w_lin and the raw dt^j phi_j rows (R = s) for the whole grid.
+    node_range=(off, nloc): per-node rows only for the shard's nodes (the
+    shared / class modes are grid-wide by construction)."""
     if not 1 <= s <= 6:
         raise ValueError(f"augmentation depth must be in [1, 6], got {s}")
     n = sset.n
@@ -255,25 +264,44 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
         if stats is not None:
             stats.setdefault("ms", []).append(h.ms)
         return _rows_from(plan, sset, h.rows)
-    # per-node path: one item per node, chunked
-    N = sset.N
-    out = torch.empty((s, n, N), dtype=torch.float64, device=d)
+    # per-node path: one item per node (of the shard)
+    off, N = (0, sset.N) if node_range is None else (int(node_range[0]), int(node_range[1]))
+    sl = slice(off, off + N)
     shared_coords = plan.coords.shape[0] == 1
-    if shared_coords:
-        tables, cf, c0 = _ops.operator_tables(plan.coords, terms)
+    uniform_rows = plan.uniform_rows
     if varcoef:
-        coef_all = _ops.dev_f64(spec.coef)
-        react = None if spec.reaction is None else _ops.dev_f64(spec.reaction)
+        coef_all = _ops.dev_f64(spec.coef[sl])
+        react = None if spec.reaction is None else _ops.dev_f64(spec.reaction[sl])
+    if node_range is not None and not uniform_rows:
+        plan = _Plan(plan.mode, plan.coords if shared_coords else plan.coords[sl],
+                     plan.rows[sl], plan.masks[sl])
+    if shared_coords:
+        # one launch writes the SoA [s][n][N] table directly
+        tables, cf, c0 = _ops.operator_tables(plan.coords, terms)
+        if varcoef:
+            coef, cs = coef_all, len(spec.orders)
+            c0t, c0s = (None, 0) if react is None else (react, 1)
+        else:
+            coef, cs = _ops.dev_f64(cf or [0.0]), 0
+            c0t, c0s = _ops.dev_f64([c0]), 0
+        kw = dict(row_default=sset.row, frozen_default=0) if uniform_rows else \
+            dict(rows=_ops.dev_i32(plan.rows),
+                 frozen=torch.as_tensor(plan.masks.view(np.int64), device=d))
+        h = _ops.harvest(n, s, delta_t, N, tables=tables, coef=coef, coef_stride=cs, c0=c0t,
+                         c0_stride=c0s, layout=1, **kw)
+        _ops.raise_on_status(h)
+        if stats is not None:
+            stats.setdefault("ms", []).append(h.ms)
+        return _ops.CompactRows(sset, nat.W_PERNODE, pernode=h.rows)
+    # per-node coordinates (non-uniform grids): chunked to bound the table memory
+    out = torch.empty((s, n, N), dtype=torch.float64, device=d)
     rows_all = _ops.dev_i32(plan.rows)
     masks_all = torch.as_tensor(plan.masks.view(np.int64), device=d)
     for a in range(0, N, PERNODE_CHUNK):
         b = min(N, a + PERNODE_CHUNK)
         B = b - a
-        if not shared_coords:
-            tables, cf, c0 = _ops.operator_tables(plan.coords[a:b], terms)
-            tidx = _ops.dev_i32(np.arange(B))
-        else:
-            tidx = None
+        tables, cf, c0 = _ops.operator_tables(plan.coords[a:b], terms)
+        tidx = _ops.dev_i32(np.arange(B))
         if varcoef:
             coef, cs = coef_all[a:b].contiguous(), len(spec.orders)
             c0t, c0s = (None, 0) if react is None else (react[a:b].contiguous(), 1)

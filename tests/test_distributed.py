@@ -1,0 +1,130 @@
+"""Sharding: host-side halo exchange over a real 2-rank gloo group (CPU), and
+on the GPU, P virtual shards in one process against the unsharded kernels."""
+
+import math
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2603_15964_b200.distributed import NcclHalo, neighbours, partition
+
+
+def test_partition_covers_grid():
+    for N in (7, 64, 1000, 1 << 20):
+        for world in (1, 2, 3, 4, 8):
+            parts = [partition(N, world, r) for r in range(world)]
+            assert parts[0][0] == 0
+            for (o1, n1), (o2, _) in zip(parts, parts[1:]):
+                assert o1 + n1 == o2
+            assert sum(n for _, n in parts) == N
+            assert max(n for _, n in parts) - min(n for _, n in parts) <= 1
+
+
+def test_neighbours():
+    assert neighbours(0, 1, True) == (None, None)
+    assert neighbours(0, 4, True) == (3, 1)
+    assert neighbours(0, 4, False) == (None, 1)
+    assert neighbours(3, 4, False) == (2, None)
+    assert neighbours(1, 2, True) == (0, 0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, periodic, N, G, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        u_glob = torch.arange(N, dtype=torch.float64) * 1.5 + 0.25
+        off, nloc = partition(N, world, rank)
+        u = u_glob[off:off + nloc].clone()
+        gl = torch.full((G,), -1.0, dtype=torch.float64)
+        gr = torch.full((G,), -1.0, dtype=torch.float64)
+        NcclHalo(rank, world, periodic).exchange(u, gl, gr)
+        left, right = neighbours(rank, world, periodic)
+        idx_l = [(off - G + j) % N for j in range(G)]
+        idx_r = [(off + nloc + j) % N for j in range(G)]
+        ok_l = left is None or torch.equal(gl, u_glob[idx_l])
+        ok_r = right is None or torch.equal(gr, u_glob[idx_r])
+        out_q.put((rank, bool(ok_l), bool(ok_r), gl.tolist()[:2], gr.tolist()[:2]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,periodic", [(2, True), (2, False), (3, True), (4, False)])
+def test_halo_exchange_gloo(world, periodic):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, periodic, 37, 5, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ok_l, ok_r, a, b in res:
+        assert ok_l and ok_r, (rank, a, b)
+
+
+# ------------------------------------------------------------------ GPU
+def _cases():
+    import paper_2603_15964_b200 as lx
+    from paper_2603_15964_b200 import configs
+    out = []
+    w = configs.c1(N=1000)
+    g = lx.make_periodic_grid(w.N, w.x_min, w.x_max)
+    st = lx.select_stencils(g, w.n, lx.StencilPolicy.ONE_SIDED_UPWIND)
+    out.append(("c1-linear", g, st, lx.SemiLinearProblem(lx.LinearOperatorSpec(w.terms), None,
+                w.u0, lx.Boundary.periodic(), "none"), lx.SchemeConfig("linear"), w.delta_t, 40))
+    w = configs.c5(N=3000)
+    c, nu = w.coef
+    g = lx.make_periodic_grid(w.N, 0.0, 1.0)
+    st = lx.select_stencils(g, w.n, lx.StencilPolicy.CENTERED)
+    out.append(("c5-pernode", g, st, lx.SemiLinearProblem(
+        lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1)), None, w.u0,
+        lx.Boundary.periodic(), "none"), lx.SchemeConfig("linear"), w.delta_t, 15))
+    w = configs.c4(N=4000)
+    g = lx.make_uniform_grid(w.N, -1.0, 1.0)
+    st = lx.select_stencils(g, w.n, lx.StencilPolicy.CENTERED)
+    out.append(("c4-neumann", g, st, lx.SemiLinearProblem(lx.LinearOperatorSpec(w.terms), None,
+                w.u0, lx.Boundary.neumann(), "cubic"), lx.SchemeConfig("etdrk4"), w.delta_t, 9))
+    w = configs.c3(N=4096)
+    g = lx.make_periodic_grid(w.N, w.x_min, w.x_max)
+    st = lx.select_stencils(g, w.n, lx.StencilPolicy.CENTERED)
+    out.append(("c3-kdv", g, st, lx.SemiLinearProblem(lx.LinearOperatorSpec(w.terms), None,
+                w.u0, lx.Boundary.periodic(), "convective", nonlinear_scale=6.0),
+                lx.SchemeConfig("etdrk4"), w.delta_t, 7))
+    w = configs.c2(N=4096)
+    g = lx.make_periodic_grid(w.N, w.x_min, w.x_max)
+    st = lx.select_stencils(g, w.n, lx.StencilPolicy.CENTERED)
+    out.append(("c2-etd2", g, st, lx.SemiLinearProblem(lx.LinearOperatorSpec(w.terms), None,
+                w.u0, lx.Boundary.periodic(), "convective"),
+                lx.SchemeConfig("etd-multistep", s=2), w.delta_t, 11))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_virtual_shards_bitwise(P):
+    from paper_2603_15964_b200 import _ops
+    from paper_2603_15964_b200.distributed import run_virtual_shards
+    from paper_2603_15964_b200.timestep import Stepper, prepare
+    for name, g, st, prob, scheme, dt, steps in _cases():
+        ref = Stepper(prepare(g, st, prob, scheme, dt), _ops.dev_f64(prob.initial))
+        ref.advance(steps)
+        for k in (None, 1):
+            u = run_virtual_shards(g, st, prob, scheme, dt, steps, P, ksteps=k)
+            assert torch.equal(u, ref.u), (name, P, k, float((u - ref.u).abs().max()))
