@@ -52,6 +52,13 @@ def expm_flops(d: int, ms: np.ndarray) -> float:
     return float((2.0 * d**3 * (pim + s) + (8.0 / 3.0) * d**3).sum())
 
 
+def multiply_flops(d: int, ms: np.ndarray) -> float:
+    """Algorithmic FLOPs of the expm-multiply harvest (harvest_quad.cu): every
+    Taylor term is one d x d matrix-vector product (2 d^2 flops); the kernel
+    reports the number of products per matrix in the low 24 bits of ms."""
+    return float((ms & 0xFFFFFF).astype(np.float64).sum() * 2.0 * d * d)
+
+
 # ------------------------------------------------------------------ clocks
 class Clocks:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
@@ -105,6 +112,15 @@ def peaks():
     return 6650.0, "fallback"
 
 
+def traffic(kernel, key, units):
+    """Per-launch DRAM bytes scaled from the committed ncu capture (profiles/)."""
+    p = os.path.join(REPO, "profiles", "r1_traffic.json")
+    try:
+        return json.load(open(p))[kernel][key] * units
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def fp64_peak():
     so = os.path.join(REPO, "tools", "libfp64peak.so")
     lib = ctypes.CDLL(so)
@@ -122,18 +138,21 @@ def c5_inputs(N=None):
 
 
 class C5:
-    """Config 5 pass on resident device inputs."""
+    """Config 5 pass on resident device inputs (this rank's slab when sharded)."""
 
-    def __init__(self, dist=None):
+    def __init__(self, rank=0, world=1):
         import torch
         import paper_2603_15964_b200 as lx
         from paper_2603_15964_b200 import _ops
+        from paper_2603_15964_b200.distributed import partition
         self.lx, self.torch = lx, torch
+        self.rank, self.world = rank, world
         self.w, coef = c5_inputs()
         self.coef_host, self.u0_host = coef, self.w.u0
         self.grid = lx.make_periodic_grid(self.w.N, 0.0, 1.0)
         self.sset = lx.select_stencils(self.grid, self.w.n, lx.StencilPolicy.CENTERED)
-        self.coef = _ops.dev_f64(coef)
+        self.off, self.nloc = partition(self.w.N, world, rank)
+        self.coef = _ops.dev_f64(coef)              # resident (rank uses its slice)
         self.u0 = _ops.dev_f64(self.w.u0)
         self.spec = lx.VariableCoefficientSpec((1, 2), self.coef)
         self.prob = lx.SemiLinearProblem(self.spec, None, self.u0, lx.Boundary.periodic(), "none")
@@ -142,17 +161,25 @@ class C5:
         self.last = {}
 
     def device_pass(self):
-        from paper_2603_15964_b200.timestep import Stepper, prepare
-        stats = {}
+        from paper_2603_15964_b200.distributed import NcclHalo, ShardedStepper, advance_all
         e0, e1, e2 = self.ev
         e0.record()
-        prep = prepare(self.grid, self.sset, self.prob, self.scheme, self.w.delta_t, stats)
+        st = ShardedStepper(self.grid, self.sset, self.prob, self.scheme, self.w.delta_t,
+                            self.rank, self.world, NcclHalo(self.rank, self.world, True))
         e1.record()
-        st = Stepper(prep, self.u0)
-        st.advance(self.w.steps)
+        st.u = self.u0[self.off:self.off + self.nloc].clone()
+        advance_all(st, self.w.steps)
         e2.record()
-        self.last = {"prep": prep, "stats": stats, "stepper": st}
+        self.last = {"stepper": st}
         return st.u
+
+    def harvest_ms_stats(self):
+        """(m, s) of every harvested matrix of this rank (separate run; FLOP accounting)."""
+        from paper_2603_15964_b200.harvest import harvest_compact
+        stats = {}
+        harvest_compact(self.grid, self.sset, self.spec, self.w.delta_t, 1, (), stats,
+                        node_range=(self.off, self.nloc))
+        return self.torch.cat(stats["ms"]).cpu().numpy()
 
     def phase_ms(self):
         e0, e1, e2 = self.ev
@@ -160,21 +187,52 @@ class C5:
         return e0.elapsed_time(e1), e1.elapsed_time(e2)
 
     def e2e_pass(self):
-        """Public API from host arrays: H2D of u0 + coefficients, D2H of snapshots."""
+        """Public API from host arrays: H2D of u0 + coefficients, D2H of the result."""
         lx = self.lx
         spec = lx.VariableCoefficientSpec((1, 2), self.coef_host)
         prob = lx.SemiLinearProblem(spec, None, self.u0_host, lx.Boundary.periodic(), "none")
-        res = lx.run(self.grid, self.sset, prob, self.scheme, self.w.delta_t,
-                     self.w.steps * self.w.delta_t)
-        return res
+        if self.world == 1:
+            return lx.run(self.grid, self.sset, prob, self.scheme, self.w.delta_t,
+                          self.w.steps * self.w.delta_t)
+        from paper_2603_15964_b200.distributed import run_sharded
+        return run_sharded(self.grid, self.sset, prob, self.scheme, self.w.delta_t,
+                           self.w.steps * self.w.delta_t)
 
     @property
     def h2d_bytes(self):
-        return self.coef_host.nbytes + self.u0_host.nbytes
+        # per rank: its coefficient slice + the initial data (run/run_sharded copy u0)
+        return self.coef_host[self.off:self.off + self.nloc].nbytes + self.u0_host.nbytes
 
     @property
     def d2h_bytes(self):
-        return 2 * self.u0_host.nbytes        # snapshots: u0 and u_final (timestep.py:313,350)
+        # run(): snapshots u0 and u_final (timestep.py:313,350); run_sharded: final slab
+        return 2 * self.u0_host.nbytes if self.world == 1 else 8 * self.nloc
+
+
+def time_c4_sharded(rank, world):
+    """BASELINE config 4 (2^24, ETDRK4, Neumann) sharded over the ranks: us/step."""
+    import torch
+    import paper_2603_15964_b200 as lx
+    from paper_2603_15964_b200 import configs
+    from paper_2603_15964_b200.distributed import NcclHalo, ShardedStepper, advance_all
+    w = configs.c4()
+    g = lx.make_uniform_grid(w.N, -1.0, 1.0)
+    st = lx.select_stencils(g, w.n, lx.StencilPolicy.CENTERED)
+    prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(w.terms), None, w.u0, lx.Boundary.neumann(),
+                                "cubic")
+    s = ShardedStepper(g, st, prob, lx.SchemeConfig("etdrk4"), w.delta_t, rank, world,
+                       NcclHalo(rank, world, False))
+    s.set_initial(w.u0)
+    advance_all(s, 20)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    advance_all(s, w.steps)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    return {"N": w.N, "steps": w.steps, "us_per_step": ms * 1e3 / w.steps,
+            "updates_per_s": w.N * w.steps / (ms * 1e-3), "ksteps_per_exchange": s.plan.ksteps}
 
 
 def time_other_configs():
@@ -273,7 +331,8 @@ def main():
                           "(4194304 harvests), 200 linear steps, dt=0.5h^2/max(nu)",
               "N": 1 << 22, "n": 13, "steps_per_pass": 200, "harvests_per_pass": 1 << 22,
               "l2": "inputs larger than L2 (436 MB per-node rows streamed each step)",
-              "parallelism": f"replicas x{args.gpus}" if args.gpus > 1 else "single"}
+              "parallelism": f"slab-sharded x{args.gpus} (NCCL halo exchange)" if args.gpus > 1
+              else "single"}
 
     if args.impl == "reference":
         if rank != 0:
@@ -285,7 +344,7 @@ def main():
         line = {"metric": metric, "value": cb["value"], "unit": unit, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": 1e3 * (1 << 22) * 200 / cb["value"], "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": config, "impl": "reference",
                 "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
                 "e2e": {"value": cb["value"], "unit": unit, "h2d_bytes_per_step": 0,
@@ -303,7 +362,7 @@ def main():
     from paper_2603_15964_b200 import _native
     lib = _native.load()
 
-    bench = C5()
+    bench = C5(rank, world)
     for _ in range(args.warmup):
         bench.device_pass()
     torch.cuda.synchronize()
@@ -328,18 +387,18 @@ def main():
         ms = float(t.item())
         dist.barrier()
     w = bench.w
-    value = world * w.N * w.steps / (ms * 1e-3)
+    value = w.N * w.steps / (ms * 1e-3)           # strong scaling: the whole grid per pass
     harvest_ms = float(np.mean(harv))
     step_ms = float(np.mean(stepm))
 
     # roofline of the per-node step kernel (HBM) and of the harvest (FP64)
     hbm, hbm_kind = peaks()
-    step_bytes = w.N * (8 * w.n + 16)                      # u in/out + 13 rows per node
+    step_bytes = bench.nloc * (8 * w.n + 16)               # u in/out + 13 rows per node
     per_launch_ms = step_ms / w.steps
     achieved = step_bytes / (per_launch_ms * 1e-3) / 1e9
-    ms_items = torch.cat(bench.last["stats"]["ms"]).cpu().numpy()
+    ms_items = bench.harvest_ms_stats()
     d = w.n                                               # s = 1: d = n
-    flops = expm_flops(d, ms_items)
+    flops = multiply_flops(d, ms_items)
     fp64 = fp64_peak()
     harvest_tflops = flops / (harvest_ms * 1e-3) / 1e12
 
@@ -353,11 +412,13 @@ def main():
         bench.e2e_pass()
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    e2e_val = world * w.N * w.steps / (float(np.mean(e2e_ms)) * 1e-3)
+    e2e_val = w.N * w.steps / (float(np.mean(e2e_ms)) * 1e-3)
 
     others = {}
-    if not args.no_others and rank == 0:
-        others = time_other_configs()
+    if not args.no_others:
+        if world == 1:
+            others = time_other_configs()
+        others["c4_sharded"] = time_c4_sharded(rank, world)
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
         cpu = cpu_c5()
@@ -365,20 +426,27 @@ def main():
     if rank == 0:
         line = {
             "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY 8(d))",
             "config": config,
-            "harvests_per_s": world * w.N / (harvest_ms * 1e-3),
+            "harvests_per_s": w.N / (harvest_ms * 1e-3),
             "phases_ms": {"harvest": harvest_ms, "steps": step_ms,
                           "per_step_launch_ms": per_launch_ms},
-            "roofline": {"bound": "hbm", "kernel": "step_kernel<LIN,13,exact,P=1> (per-node rows)",
-                         "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None,
-                         "algorithmic_bytes_per_launch": step_bytes, "peak_kind": hbm_kind},
-            "roofline_harvest": {"bound": "fp64", "kernel": "harvest_kernel<16,4>",
-                                 "achieved": harvest_tflops, "peak": fp64, "unit": "TFLOP/s",
-                                 "frac": harvest_tflops / fp64, "algorithmic_flops": flops,
-                                 "peak_kind": "measured DFMA chains (tools/fp64_peak.cu)"},
+            # the dominant kernel of the pass (ncu launch list: ~80% of device time) is
+            # the FP64-bound harvest; the HBM-bound step kernel follows as roofline_step
+            "roofline": {"bound": "fp64", "kernel": "harvest_quad_kernel<13> (per-node expm-multiply, 13x13)",
+                         "achieved": harvest_tflops, "peak": fp64, "unit": "TFLOP/s",
+                         "frac": harvest_tflops / fp64,
+                         "traffic": traffic("harvest_quad_kernel<13>", "bytes_per_item", bench.nloc),
+                         "algorithmic_flops_per_launch": flops,
+                         "peak_kind": "measured DFMA chains (tools/fp64_peak.cu), this run"},
+            "roofline_step": {"bound": "hbm", "kernel": "step_kernel<LIN,13,exact,P=1> (per-node rows)",
+                              "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                              "frac": achieved / hbm,
+                              "traffic": traffic("step_kernel<LIN,13,exact,P=1,PN>", "bytes_per_node",
+                                                 bench.nloc),
+                              "algorithmic_bytes_per_launch": step_bytes,
+                              "peak_kind": f"{hbm_kind} (MEASURED_PEAKS.json hbm_gbs)"},
             "e2e": {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": bench.h2d_bytes,
                     "d2h_bytes_per_step": bench.d2h_bytes},
             "gpu_launches": launches,

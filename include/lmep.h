@@ -186,6 +186,12 @@ int lmep_harvest(int n, int s, int nterms, const double *tables, const int32_t *
                  const uint64_t *frozen, uint64_t frozen_default, int64_t B, int layout,
                  double *w_out, int32_t *status, int32_t *ms, void *stream);
 
+/* Harvest algorithm for d <= 16: 0 (default) = register-resident
+ * expm-multiply (harvest_quad.cu: balancing + scaled Taylor action on the
+ * needed columns), 1 = full Pade scaling-and-squaring per warp (harvest.cu).
+ * lmep_expm always uses the Pade kernel.  Process-wide setting. */
+int lmep_set_harvest_method(int method);
+
 /* ---- stepping (K3, K4, K5) ---------------------------------------------- */
 
 /* Linear banded propagation u <- W u for `steps` steps (kernels.py:33-43,

@@ -42,6 +42,7 @@ EXPORTS = (
     "lmep_version", "lmep_status_string", "lmep_last_error", "lmep_fornberg", "lmep_expm",
     "lmep_harvest", "lmep_step_linear", "lmep_step_etdrk4", "lmep_step_etd2",
     "lmep_banded_matvec", "lmep_plan", "lmep_rows_to_soa", "lmep_launch_count",
+    "lmep_set_harvest_method",
 )
 
 
@@ -113,6 +114,7 @@ def load(path: str | None = None):
     L.lmep_banded_matvec.argtypes = [G, W, H, vp, vp, i32, vp]
     L.lmep_plan.argtypes = [G, C.c_int, C.c_int, i64, T]
     L.lmep_rows_to_soa.argtypes = [vp, i64, C.c_int, vp, vp]
+    L.lmep_set_harvest_method.argtypes = [C.c_int]
     for name in EXPORTS:
         if name not in ("lmep_version", "lmep_status_string", "lmep_last_error",
                         "lmep_launch_count"):
@@ -154,3 +156,9 @@ def check(status: int, what: str, state=None, time=None) -> None:
     if cls is errors.NonFinite:
         raise errors.NonFinite(msg, state=state, time=time)
     raise cls(msg)
+
+
+def set_harvest_method(method: str) -> None:
+    """'multiply' (default for d <= 16) or 'pade' (full expm per warp)."""
+    code = {"multiply": 0, "auto": 0, "pade": 1}[method]
+    check(lib().lmep_set_harvest_method(code), "lmep_set_harvest_method")

@@ -19,7 +19,7 @@
 // barriers, every warp runs independently.
 #include <math.h>
 
-#include "common.cuh"
+#include "harvest.cuh"
 
 namespace lmep {
 
@@ -140,6 +140,53 @@ __device__ double abs_power_norm(const double *M, int d, int p, double scale, in
     return mx;
 }
 
+// Incremental v_p = (|A|^T)^p 1 (v lives in lane c): ||(|A|)^p||_1 = max_c v_p[c].
+// The ell(m) tests for m = 3, 5, 7, 9 need p = 7, 11, 15, 19 and share one
+// iteration instead of restarting (scipy _onenorm_matrix_power_nnm each time).
+template <int DP>
+struct AbsPowerIter {
+    double v;
+    int p;
+    __device__ void init(int d, int lane) { v = (lane % DP < d) ? 1.0 : 0.0; p = 0; }
+    __device__ double norm(const double *M, int d, int target, int lane)
+    {
+        using T = Tile<DP>;
+        const int c = lane % DP, g = lane / DP;
+        for (; p < target; ++p) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < T::E; ++j) {
+                const int r = g + T::G * j;
+                const double vr = __shfl_sync(FULL, v, r);
+                if (r < d && c < d) s += fabs(M[r * T::LD + c]) * vr;
+            }
+#pragma unroll
+            for (int o = DP; o < 32; o <<= 1) s += __shfl_xor_sync(FULL, s, o);
+            v = s;
+        }
+        double mx = (c < d) ? v : 0.0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+        return mx;
+    }
+};
+
+__device__ __forceinline__ int ell_from(double nrm, double onenorm_A, double scale, int m)
+{
+    double cm;
+    switch (m) {
+    case 3: cm = 100800.; break;
+    case 5: cm = 10059033600.; break;
+    case 7: cm = 4487938430976000.; break;
+    case 9: cm = 5914384781877411840000.; break;
+    default: cm = 113250775606021113483283660800000000.; break;
+    }
+    if (nrm == 0.0) return 0;
+    const double alpha = nrm / (onenorm_A * scale * cm);
+    const double v = ceil(log2(alpha / 0x1p-53) / (2 * m));
+    return v > 0.0 ? (int)v : 0;
+}
+
 // scipy _ell: extra squarings demanded by the backward-error bound of degree m.
 template <int DP>
 __device__ int ell(const double *A, int d, int m, double scale, double onenorm_A, int lane)
@@ -244,7 +291,7 @@ __device__ bool balance(double *A, double *scale, int d, int lane)
 // Solve Q X = P in place (X overwrites P) by Gaussian elimination with partial
 // pivoting (first maximal pivot, LAPACK idamax).  Returns false if singular.
 template <int DP>
-__device__ bool lu_solve(double *Q, double *P, int d, int lane)
+__device__ bool lu_solve(double *Q, double *P, double *inv_piv, int d, int lane)
 {
     using T = Tile<DP>;
     const int c = lane % DP, g = lane / DP;
@@ -268,6 +315,7 @@ __device__ bool lu_solve(double *Q, double *P, int d, int lane)
             __syncwarp();
         }
         const double inv = 1.0 / Q[k * T::LD + k];
+        if (lane == 0) inv_piv[k] = inv;
         const double qk = (c < d) ? Q[k * T::LD + c] : 0.0;
         const double pk = (c < d) ? P[k * T::LD + c] : 0.0;
 #pragma unroll
@@ -282,7 +330,7 @@ __device__ bool lu_solve(double *Q, double *P, int d, int lane)
         __syncwarp();
     }
     for (int k = d - 1; k >= 0; --k) {
-        const double x = (c < d) ? P[k * T::LD + c] / Q[k * T::LD + k] : 0.0;
+        const double x = (c < d) ? P[k * T::LD + c] * inv_piv[k] : 0.0;
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < T::E; ++j) {
@@ -337,24 +385,35 @@ __device__ int warp_expm(double *buf, double *scale, int d, int lane, int *mo, i
     mat_mul<DP>(A, A, A2, d, lane);
     mat_mul<DP>(A2, A2, A4, d, lane);
     mat_mul<DP>(A4, A2, A6, d, lane);
-    const double d4 = pow(one_norm<DP>(A4, d, lane), 0.25);
-    const double d6 = pow(one_norm<DP>(A6, d, lane), 1.0 / 6.0);
+    // Degree selection (AMH 2009 Alg. 6.1 as scipy implements it).  The tests
+    // eta < theta_m on d_k = ||A^k||^(1/k) are evaluated as ||A^k|| < theta_m^k
+    // (no fractional powers); roots are taken only on the degree-13 branch.
+    const double n4 = one_norm<DP>(A4, d, lane);
+    const double n6 = one_norm<DP>(A6, d, lane);
     const double nA = one_norm<DP>(A, d, lane);
+    constexpr double t3 = 1.495585217958292e-002, t5 = 2.539398330063230e-001;
+    constexpr double t7 = 9.504178996162932e-001, t9 = 2.097847961257068e+000;
+    constexpr double t3_4 = t3 * t3 * t3 * t3, t3_6 = t3_4 * t3 * t3;
+    constexpr double t5_4 = t5 * t5 * t5 * t5, t5_6 = t5_4 * t5 * t5;
+    constexpr double t7_6 = t7 * t7 * t7 * t7 * t7 * t7, t7_8 = t7_6 * t7 * t7;
+    constexpr double t9_6 = t9 * t9 * t9 * t9 * t9 * t9, t9_8 = t9_6 * t9 * t9;
+    AbsPowerIter<DP> pw;
+    pw.init(d, lane);
     int m = 13, s = 0;
-    const double eta1 = fmax(d4, d6);
-    if (eta1 < 1.495585217958292e-002 && ell<DP>(A, d, 3, 1.0, nA, lane) == 0) {
+    if (n4 < t3_4 && n6 < t3_6 && ell_from(pw.norm(A, d, 7, lane), nA, 1.0, 3) == 0) {
         m = 3;
-    } else if (eta1 < 2.539398330063230e-001 && ell<DP>(A, d, 5, 1.0, nA, lane) == 0) {
+    } else if (n4 < t5_4 && n6 < t5_6 && ell_from(pw.norm(A, d, 11, lane), nA, 1.0, 5) == 0) {
         m = 5;
     } else {
         mat_mul<DP>(A6, A2, A8, d, lane);
-        const double d8 = pow(one_norm<DP>(A8, d, lane), 0.125);
-        const double eta3 = fmax(d6, d8);
-        if (eta3 < 9.504178996162932e-001 && ell<DP>(A, d, 7, 1.0, nA, lane) == 0) {
+        const double n8 = one_norm<DP>(A8, d, lane);
+        if (n6 < t7_6 && n8 < t7_8 && ell_from(pw.norm(A, d, 15, lane), nA, 1.0, 7) == 0) {
             m = 7;
-        } else if (eta3 < 2.097847961257068e+000 && ell<DP>(A, d, 9, 1.0, nA, lane) == 0) {
+        } else if (n6 < t9_6 && n8 < t9_8 && ell_from(pw.norm(A, d, 19, lane), nA, 1.0, 9) == 0) {
             m = 9;
         } else {
+            const double d6 = pow(n6, 1.0 / 6.0), d8 = pow(n8, 0.125);
+            const double eta3 = fmax(d6, d8);
             mat_mul<DP>(A4, A6, W, d, lane);  // A10, only for its norm
             const double d10 = pow(one_norm<DP>(W, d, lane), 0.1);
             const double eta4 = fmax(d8, d10);
@@ -445,7 +504,7 @@ __device__ int warp_expm(double *buf, double *scale, int d, int lane, int *mo, i
         V[e] = -u + v;
     }
     __syncwarp();
-    if (!lu_solve<DP>(V, U, d, lane)) return -1;
+    if (!lu_solve<DP>(V, U, scale + DP, d, lane)) return -1;
     double *X = U, *Y = V;
     for (int q = 0; q < s; ++q) {
         mat_mul<DP>(X, X, Y, d, lane);
@@ -453,11 +512,12 @@ __device__ int warp_expm(double *buf, double *scale, int d, int lane, int *mo, i
     }
     // undo balancing: E = D^-1 ... scipy form E * (d_i / d_j)  (expm.py:39)
     bool ok = true;
+    const double inv_sc = 1.0 / scale[c];          // scales are powers of two: exact
 #pragma unroll
     for (int j = 0; j < T::E; ++j) {
         const int r = g + T::G * j;
         if (r < d && c < d) {
-            const double e = X[r * T::LD + c] * (scale[r] / scale[c]);
+            const double e = X[r * T::LD + c] * (scale[r] * inv_sc);
             X[r * T::LD + c] = e;
             ok &= (bool)isfinite(e);
         }
@@ -469,28 +529,7 @@ __device__ int warp_expm(double *buf, double *scale, int d, int lane, int *mo, i
     return (int)((X - buf) / T::SZ);
 }
 
-struct HarvestParams {
-    int mode;              // 0: expm of given matrices, 1: harvest (tables), 2: harvest (explicit L)
-    int n, s, d, nterms;
-    const double *tables;  // [ntab][nterms][n][n]
-    const int32_t *table_idx;
-    const double *coef;
-    int64_t coef_stride;
-    const double *c0;
-    int64_t c0_stride;
-    const double *L;       // [B][n][n]
-    const double *Ain;     // expm mode: [B][d][d]
-    double delta_t;
-    const int32_t *rows;
-    int row_default;
-    const uint64_t *frozen;
-    uint64_t frozen_default;
-    int64_t B;
-    int layout;
-    double *out;
-    int32_t *status;
-    int32_t *ms;
-};
+
 
 template <int DP, int WPB>
 __global__ void __launch_bounds__(32 * WPB) harvest_kernel(const HarvestParams P)
@@ -611,9 +650,13 @@ static int launch_harvest(const HarvestParams &P, cudaStream_t st)
     return launch_status("harvest_kernel");
 }
 
+static int g_harvest_method = 0;   // 0: auto (expm-multiply for d <= 16), 1: Pade expm
+
 static int dispatch_harvest(const HarvestParams &P, cudaStream_t st)
 {
     if (P.B == 0) return LMEP_OK;
+    if (P.mode != 0 && g_harvest_method == 0 && P.d >= 2 && P.d <= 16)
+        return launch_harvest_quad(P, st);
     if (P.d <= 8) return launch_harvest<8, 8>(P, st);
     if (P.d <= 16) return launch_harvest<16, 4>(P, st);
     if (P.d <= 32) return launch_harvest<32, 2>(P, st);
@@ -688,4 +731,11 @@ extern "C" int lmep_harvest(int n, int s, int nterms, const double *tables,
     P.status = status;
     P.ms = ms;
     return dispatch_harvest(P, (cudaStream_t)stream);
+}
+
+extern "C" int lmep_set_harvest_method(int method)
+{
+    if (method != 0 && method != 1) return LMEP_INVALID_CONFIG;
+    lmep::g_harvest_method = method;
+    return LMEP_OK;
 }

@@ -305,3 +305,82 @@ def run_virtual_shards(grid: Grid, stencils, problem: SemiLinearProblem, scheme:
             s.compute_phase(kk)
         done += kk
     return torch.cat([s.u for s in shards])
+
+
+def run_sharded(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
+                delta_t: float, t_final: float, *, group=None, exact: bool = True,
+                ksteps: int | None = None):
+    """``timestep.run`` over all ranks of a torch.distributed group (one GPU per
+    rank): per-rank harvest, slab stepping with NCCL halo exchange, and the
+    final state gathered on rank 0.  Returns a SimulationResult (snapshots:
+    initial and final state) on rank 0 and None elsewhere."""
+    import time
+
+    import numpy as np
+    import torch.distributed as dist
+
+    from .timestep import SimulationResult, _steps_for
+
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if t_final <= 0 or delta_t <= 0:
+        raise InvalidConfig("dt and t_final must be positive")
+    steps = _steps_for(t_final, delta_t, "final time")
+    dev = nat.device()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter_ns()
+    st = ShardedStepper(grid, stencils, problem, scheme, delta_t, rank, world,
+                        NcclHalo(rank, world, grid.periodic, group), exact=exact, ksteps=ksteps)
+    torch.cuda.synchronize(dev)
+    harvest_ns = time.perf_counter_ns() - t0
+    st.set_initial(problem.initial)
+    t0 = time.perf_counter_ns()
+    advance_all(st, steps)
+    torch.cuda.synchronize(dev)
+    step_ns = time.perf_counter_ns() - t0
+    u = gather_slabs(st, group)
+    if world > 1:
+        bad = torch.tensor([int(st.nonfinite())], device=dev)
+        dist.all_reduce(bad, group=group)
+        nonfinite = bool(bad.item())
+    else:
+        nonfinite = st.nonfinite()
+    if rank != 0:
+        return None
+    u0 = np.asarray(problem.initial.cpu() if isinstance(problem.initial, torch.Tensor)
+                    else problem.initial, dtype=np.float64)
+    if nonfinite:
+        from .errors import NonFinite
+        raise NonFinite("time integration blew up", state=u0, time=0.0)
+    return SimulationResult(times=np.array([0.0, steps * delta_t]),
+                            snapshots=np.stack([u0, _ops.to_host(u)]), steps=steps,
+                            harvest_ns=harvest_ns, step_ns=step_ns)
+
+
+def advance_all(st: ShardedStepper, steps: int) -> None:
+    """All of a rank's steps: (warm-up,) then chunks of plan.ksteps, one halo
+    exchange each."""
+    done = 0
+    if st.prep.scheme == "etd-multistep" and st.hist is None:
+        st.warm_up_exchange()
+        st.warm_up_compute()
+        done = st.done
+    while done < steps:
+        k = min(st.plan.ksteps, steps - done)
+        st.step_chunk(k)
+        done += k
+
+
+def gather_slabs(st: ShardedStepper, group=None) -> torch.Tensor | None:
+    """Concatenate the slabs on rank 0 (padded all_gather: slab sizes differ by <= 1)."""
+    import torch.distributed as dist
+    if st.world == 1:
+        return st.u
+    m = -(-st.sset.N // st.world)
+    buf = torch.zeros(m, dtype=torch.float64, device=st.u.device)
+    buf[:st.plan.nloc] = st.u
+    parts = [torch.empty_like(buf) for _ in range(st.world)]
+    dist.all_gather(parts, buf, group=group)
+    if st.rank != 0:
+        return None
+    return torch.cat([parts[r][:partition(st.sset.N, st.world, r)[1]] for r in range(st.world)])

@@ -79,7 +79,14 @@ def test_expm_nonfinite(lx):
         lx.expm(np.eye(3) * 1e6)
 
 
-def test_harvest_phi_weights_vs_reference(lx, golden):
+@pytest.fixture(params=["multiply", "pade"])
+def method(request, lx):
+    lx._native.set_harvest_method(request.param)
+    yield request.param
+    lx._native.set_harvest_method("multiply")
+
+
+def test_harvest_phi_weights_vs_reference(lx, golden, method):
     for i in range(int(golden["hv_count"])):
         dt, s, row = golden[f"hv{i}_meta"]
         s, row = int(s), int(row)
@@ -153,7 +160,29 @@ def test_c4_class_harvest_vs_reference_rows(lx, golden):
         assert err < (W_TOL if k in (0, 4, 5) else 1e-9), (k, err)
 
 
-def test_c5_per_node_harvest(lx, golden):
+def test_harvest_methods_agree_with_oracle_random(lx, orc, method):
+    """Random stencil operators (orders 1..3, one-sided rows, frozen rows, s = 1..4)."""
+    rng = np.random.default_rng(11)
+    for trial in range(60):
+        n = int(rng.choice([3, 5, 7, 9, 11, 13]))
+        row = int(rng.integers(0, n))
+        h = 10.0 ** rng.uniform(-4, -1)
+        x = (np.arange(n) - row) * h
+        kmax = int(min(3, n - 1))
+        terms = tuple((k, float(rng.uniform(-2, 2)) * (1 if k != 2 else abs(rng.uniform(0.1, 1))))
+                      for k in range(1, kmax + 1))
+        L = orc.local_operator(x, terms)
+        dt = float(rng.uniform(0.05, 2.0)) * h ** max(k for k, _ in terms) / 4
+        s = int(rng.integers(1, 5))
+        frozen = [0] if rng.random() < 0.3 and row != 0 else []
+        ws = lx.harvest_phi_weights(L, dt, s, row, frozen)
+        wl, wp = orc.harvest_phi_weights(L, dt, s, row, frozen)
+        got = np.vstack([ws.w_lin] + list(ws.w_phi))
+        ref = np.vstack([wl] + list(wp))
+        assert _rows_rel(got, ref) < W_TOL, (trial, n, row, s, _rows_rel(got, ref))
+
+
+def test_c5_per_node_harvest(lx, golden, method):
     from paper_2603_15964_b200 import configs
     from paper_2603_15964_b200.harvest import harvest_compact
     w5 = configs.c5(N=64, steps=20)
