@@ -655,7 +655,8 @@ static int g_harvest_method = 0;   // 0: auto (expm-multiply for d <= 16), 1: Pa
 static int dispatch_harvest(const HarvestParams &P, cudaStream_t st)
 {
     if (P.B == 0) return LMEP_OK;
-    if (P.mode != 0 && g_harvest_method == 0 && P.d >= 2 && P.d <= 16)
+    if (P.mode != 0 && g_harvest_method == 0 && P.d >= 2 && P.d <= 16 &&
+        (P.mode == 2 || P.nterms <= 4))
         return launch_harvest_quad(P, st);
     if (P.d <= 8) return launch_harvest<8, 8>(P, st);
     if (P.d <= 16) return launch_harvest<16, 4>(P, st);

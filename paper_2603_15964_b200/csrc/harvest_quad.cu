@@ -61,12 +61,25 @@ __global__ void __launch_bounds__(128) harvest_quad_kernel(const HarvestParams P
     const double dt = P.delta_t;
 
     // ---- own rows of A = [[dt L'^T, dt e_row, 0], [0, 0, dt J]] -------------
-    const double *tab = nullptr, *cf = nullptr;
+    // A table shared by every item (table_idx == null) is staged once per CTA
+    // in shared memory; per-item coefficients go to registers.
+    extern __shared__ double stab[];
+    const double *tab = nullptr;
+    double cfr[4] = {0.0, 0.0, 0.0, 0.0};
     double cz = 0.0;
+    const bool shared_tab = P.mode == 1 && P.table_idx == nullptr;
+    if (shared_tab) {
+        const int tn = P.nterms * n * n;
+        for (int i = threadIdx.x; i < tn; i += blockDim.x) stab[i] = P.tables[i];
+        __syncthreads();
+        tab = stab;
+    }
     if (P.mode == 1) {
-        const int ti = P.table_idx ? P.table_idx[b] : 0;
-        tab = P.tables + (size_t)ti * P.nterms * n * n;
-        cf = P.coef + b * P.coef_stride;
+        if (!shared_tab) tab = P.tables + (size_t)P.table_idx[b] * P.nterms * n * n;
+        const double *cf = P.coef + b * P.coef_stride;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            if (t < P.nterms) cfr[t] = cf[t];
         cz = P.c0 ? P.c0[b * P.c0_stride] : 0.0;
     }
     double a[R][D];
@@ -83,8 +96,9 @@ __global__ void __launch_bounds__(128) harvest_quad_kernel(const HarvestParams P
                     if (P.mode == 1) {
                         // localop.py:120-127: term order, then the reaction on the diagonal
                         l = 0.0;
-                        for (int t = 0; t < P.nterms; ++t)
-                            l = xadd(l, xmul(cf[t], tab[(t * n + c) * n + j]));
+#pragma unroll
+                        for (int t = 0; t < 4; ++t)
+                            if (t < P.nterms) l = xadd(l, xmul(cfr[t], tab[(t * n + c) * n + j]));
                         if (c == j && cz != 0.0) l = xadd(l, cz);
                     } else {
                         l = P.L[(b * n + c) * n + j];
@@ -254,12 +268,14 @@ static int launch_quad(const HarvestParams &P, cudaStream_t st)
     const int64_t threads = P.B * 4;
     const int64_t blocks = (threads + 127) / 128;
     if (blocks > 0x7fffffffLL) return LMEP_INVALID_CONFIG;
-    harvest_quad_kernel<D><<<(unsigned)blocks, 128, 0, st>>>(P);
+    const size_t shm = (P.mode == 1 && P.table_idx == nullptr) ? (size_t)P.nterms * P.n * P.n * 8 : 0;
+    harvest_quad_kernel<D><<<(unsigned)blocks, 128, shm, st>>>(P);
     return launch_status("harvest_quad_kernel");
 }
 
 int launch_harvest_quad(const HarvestParams &P, cudaStream_t st)
 {
+    if (P.mode == 1 && P.nterms > 4) return LMEP_INVALID_CONFIG;   // caller falls back to Pade
     switch (P.d) {
     case 2: return launch_quad<2>(P, st);
     case 3: return launch_quad<3>(P, st);

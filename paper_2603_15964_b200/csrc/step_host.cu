@@ -247,7 +247,10 @@ int run_steps(const StepCall &c)
             p.qhl = c.halo->hist_left; p.qhr = c.halo->hist_right;
             p.G = c.halo->width;
         }
-        rc = launch_step(c.sch, (c.flags & LMEP_FLAG_EXACT) != 0, pernode, p, grid, shm, c.stream);
+        if (c.sch == SCH_LIN && pernode && p.bc == LMEP_BC_NONE && k == 1 && !t.ring)
+            rc = launch_lin_pernode(p, c.stream);          // lean streaming kernel (C5)
+        else
+            rc = launch_step(c.sch, (c.flags & LMEP_FLAG_EXACT) != 0, pernode, p, grid, shm, c.stream);
         if (rc) break;
         src = dst;
         qsrc = qdst;
