@@ -8,6 +8,7 @@ combination of harvested rows that ``harvest.combine`` defines).
 from __future__ import annotations
 
 import ctypes as C
+import warnings
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -21,14 +22,20 @@ F64 = torch.float64
 
 
 def dev_f64(a) -> torch.Tensor:
-    """Contiguous float64 tensor on the product device (host arrays are copied)."""
+    """Contiguous float64 tensor on the product device.  Host data is copied
+    once (asynchronously from pinned torch tensors); read-only numpy arrays
+    are wrapped without a host-side copy (the wrapper is never written)."""
     d = nat.device()
     if isinstance(a, torch.Tensor):
+        if a.device.type == "cpu":
+            a = a.to(dtype=F64).contiguous()
+            return a.to(device=d, non_blocking=a.is_pinned())
         return a.to(device=d, dtype=F64).contiguous()
     h = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
-    if not h.flags.writeable:
-        h = h.copy()
-    return torch.as_tensor(h, device=d)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)     # read-only source, copied to device
+        t = torch.from_numpy(h)
+    return t.to(device=d)
 
 
 def dev_i32(a) -> torch.Tensor:
@@ -37,6 +44,14 @@ def dev_i32(a) -> torch.Tensor:
 
 def to_host(t: torch.Tensor) -> np.ndarray:
     return t.detach().cpu().numpy()
+
+
+def to_host_pinned(t: torch.Tensor) -> np.ndarray:
+    """D2H through a page-locked buffer (torch caches pinned blocks), then a numpy view."""
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return h.numpy()
 
 
 # ---------------------------------------------------------------------------

@@ -208,24 +208,31 @@ __device__ __forceinline__ void run_pass(const StepParams &p, int lo, int hi, in
     const int tid = threadIdx.x, nt = blockDim.x;
     const int flo = lo > fLo ? lo : fLo;
     const int fhi = hi < fHi ? hi : fHi;
-    const int nch = fhi > flo ? (fhi - flo) / P : 0;
+    // interior chunks, the last one possibly partial: the fast path computes
+    // all P outputs (the window may run into the slot padding) and stores cnt
+    const int nch = fhi > flo ? (fhi - flo + P - 1) / P : 0;
     for (int ch = tid; ch < nch; ch += nt) {
         const int l = flo + ch * P;
+        const int cnt = fhi - l < P ? fhi - l : P;
         double v[NB > 0 ? NB : 1][P];
 #pragma unroll
         for (int b = 0; b < NB; ++b) band_fast<NS, P, EX, PN>(p, rows[b], X[b], l, lbase, v[b]);
 #pragma unroll
         for (int q = 0; q < P; ++q) {
-            double vq[NB > 0 ? NB : 1];
+            if (q < cnt) {
+                double vq[NB > 0 ? NB : 1];
 #pragma unroll
-            for (int b = 0; b < NB; ++b) vq[b] = v[b][q];
-            epi(l + q, vq);
+                for (int b = 0; b < NB; ++b) vq[b] = v[b][q];
+                epi(l + q, vq);
+            }
         }
     }
-    const int a_end = nch > 0 ? flo : lo;
-    const int b_beg = nch > 0 ? flo + nch * P : lo;
+    // boundary-class nodes of non-periodic grids (or the whole range if it has
+    // no interior part): per-node path, handed to the threads with fewest chunks
+    const int a_end = nch > 0 ? flo : hi;
+    const int b_beg = nch > 0 ? fhi : hi;
     const int na = a_end - lo, nb = hi - b_beg;
-    for (int k = tid; k < na + nb; k += nt) {
+    for (int k = nt - 1 - tid; k < na + nb; k += nt) {
         const int l = k < na ? lo + k : b_beg + (k - na);
         double vq[NB > 0 ? NB : 1];
 #pragma unroll

@@ -60,7 +60,7 @@ int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded
         if (pernode) tile = 2048;
         else if (sch == SCH_LIN) tile = 4096;
         else if (sch == SCH_ETD2) tile = 2048;
-        else tile = 1024;
+        else tile = 1200;                                      // ETDRK4: + halo ~ 256 chunks of 5
         // small grids: enough tiles to cover the SMs
         while (tile > 256 && (g.nloc + tile - 1) / tile < 2 * nsm) tile /= 2;
         tile = std::min<int64_t>(tile, g.nloc);
@@ -81,6 +81,13 @@ int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded
     t.tile = (int32_t)tile;
     t.ksteps = (int32_t)k;
     t.ring = 0;
+    if (t.threads <= 0 && sch != SCH_LIN) {
+        // one chunk of P nodes per thread for the widest pass of a step:
+        // a pass is a single round, nobody waits for a second one at the barrier
+        const int64_t widest = tile + (int64_t)ext * (eL + eR);
+        int64_t th = ((widest + P - 1) / P + 31) / 32 * 32;
+        t.threads = (int32_t)std::max<int64_t>(32, std::min<int64_t>(256, th));
+    }
     return LMEP_OK;
 }
 

@@ -366,7 +366,7 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
 
     st = Stepper(prep, _ops.dev_f64(u0), exact=exact, tuning=tuning)
     times = [0.0]
-    snaps = [_ops.to_host(st.u)]
+    snaps = [_ops.to_host_pinned(st.u)]
     step_ns = 0
     done = 0
     while done < steps_total:
@@ -380,7 +380,7 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
         if st.nonfinite():
             raise NonFinite("time integration blew up", state=snaps[-1], time=times[-1])
         times.append(done * delta_t)
-        snaps.append(_ops.to_host(st.u))
+        snaps.append(_ops.to_host_pinned(st.u))
     return SimulationResult(times=np.array(times), snapshots=np.array(snaps), steps=steps_total,
                             harvest_ns=harvest_ns, step_ns=step_ns)
 
