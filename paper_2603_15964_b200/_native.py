@@ -87,7 +87,7 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = path or LIB_PATH
+    p = path or os.environ.get("LMEP_LIB") or LIB_PATH
     if not os.path.exists(p):
         raise errors.LocalExpError(
             f"liblmep.so not found at {p}; run __graft_entry__.build() (no CPU fallback exists)")
@@ -159,6 +159,7 @@ def check(status: int, what: str, state=None, time=None) -> None:
 
 
 def set_harvest_method(method: str) -> None:
-    """'multiply' (default for d <= 16) or 'pade' (full expm per warp)."""
-    code = {"multiply": 0, "auto": 0, "pade": 1}[method]
+    """'multiply' (default for d <= 16: expm-multiply, 8 lanes per item when
+    d > 8), 'multiply4' (4 lanes per item) or 'pade' (full expm per warp)."""
+    code = {"multiply": 0, "auto": 0, "pade": 1, "multiply4": 2}[method]
     check(lib().lmep_set_harvest_method(code), "lmep_set_harvest_method")

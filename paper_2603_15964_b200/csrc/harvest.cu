@@ -736,7 +736,8 @@ extern "C" int lmep_harvest(int n, int s, int nterms, const double *tables,
 
 extern "C" int lmep_set_harvest_method(int method)
 {
-    if (method != 0 && method != 1) return LMEP_INVALID_CONFIG;
-    lmep::g_harvest_method = method;
+    if (method < 0 || method > 2) return LMEP_INVALID_CONFIG;
+    lmep::g_harvest_method = method == 1 ? 1 : 0;
+    lmep::set_lanes_per_item(method == 2 ? 4 : 8);
     return LMEP_OK;
 }

@@ -29,5 +29,6 @@ struct HarvestParams {
 
 // expm-multiply harvest for d <= 16 (harvest_quad.cu)
 int launch_harvest_quad(const HarvestParams &P, cudaStream_t st);
+void set_lanes_per_item(int lpi);
 
 }  // namespace lmep

@@ -31,28 +31,36 @@ __constant__ double kInvK[48] = {
     1.0 / 38, 1.0 / 39, 1.0 / 40, 1.0 / 41, 1.0 / 42, 1.0 / 43, 1.0 / 44, 1.0 / 45, 1.0 / 46,
     1.0 / 47};
 constexpr int TAYLOR_MAX = 47;
+#ifndef HARVEST_THETA
+#define HARVEST_THETA 2.0
+#endif
 
 __device__ __forceinline__ int q_exp2i(double x) { return ((__double2hiint(x) >> 20) & 0x7ff) - 1023; }
 __device__ __forceinline__ double q_pow2(int k) { return __hiloint2double((k + 1023) << 20, 0); }
+template <int LPI>
 __device__ __forceinline__ double q_sum(double v, unsigned m)
 {
-    v += __shfl_xor_sync(m, v, 1);
-    return v + __shfl_xor_sync(m, v, 2);
+#pragma unroll
+    for (int o = 1; o < LPI; o <<= 1) v += __shfl_xor_sync(m, v, o);
+    return v;
 }
+template <int LPI>
 __device__ __forceinline__ double q_max(double v, unsigned m)
 {
-    v = fmax(v, __shfl_xor_sync(m, v, 1));
-    return fmax(v, __shfl_xor_sync(m, v, 2));
+#pragma unroll
+    for (int o = 1; o < LPI; o <<= 1) v = fmax(v, __shfl_xor_sync(m, v, o));
+    return v;
 }
 
-template <int D>
+template <int D, int LPI>
 __global__ void __launch_bounds__(128) harvest_quad_kernel(const HarvestParams P)
 {
-    constexpr int R = (D + 3) / 4;            // rows per lane
+    constexpr int R = (D + LPI - 1) / LPI;    // rows per lane
+    constexpr int SH = LPI == 4 ? 2 : 3;
     const int lane = threadIdx.x & 31;
-    const int q = lane & 3, qb = lane & ~3;
-    const unsigned qm = 0xFu << qb;
-    const int64_t braw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 2;
+    const int q = lane & (LPI - 1), qb = lane & ~(LPI - 1);
+    const unsigned qm = ((1u << LPI) - 1u) << qb;
+    const int64_t braw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> SH;
     const bool live = braw < P.B;
     const int64_t b = live ? braw : P.B - 1;   // idle quads mirror the last item, never store
     const int n = P.n, sd = P.s;
@@ -86,7 +94,7 @@ __global__ void __launch_bounds__(128) harvest_quad_kernel(const HarvestParams P
     bool fin = true;
 #pragma unroll
     for (int m = 0; m < R; ++m) {
-        const int j = q + 4 * m;
+        const int j = q + LPI * m;
 #pragma unroll
         for (int c = 0; c < D; ++c) {
             double v = 0.0;
@@ -130,8 +138,8 @@ __global__ void __launch_bounds__(128) harvest_quad_kernel(const HarvestParams P
             double p = 0.0;
 #pragma unroll
             for (int m = 0; m < R; ++m) p = fma(a[m][c], a[m][c], p);
-            p = q_sum(p, qm);
-            if ((c & 3) == q) myc2[c >> 2] = p;
+            p = q_sum<LPI>(p, qm);
+            if ((c & (LPI - 1)) == q) myc2[c >> SH] = p;
         }
         int k[R];
         bool chg = false;
@@ -142,7 +150,7 @@ __global__ void __launch_bounds__(128) harvest_quad_kernel(const HarvestParams P
 #pragma unroll
             for (int c = 0; c < D; ++c) r2 = fma(a[m][c], a[m][c], r2);
             const double c2 = myc2[m];
-            if (q + 4 * m < D && c2 > 1e-280 && r2 > 1e-280 && c2 < 1e280 && r2 < 1e280) {
+            if (q + LPI * m < D && c2 > 1e-280 && r2 > 1e-280 && c2 < 1e280 && r2 < 1e280) {
                 const double cn = sqrt(c2), rn = sqrt(r2);
                 int kk = (q_exp2i(rn) - q_exp2i(cn)) / 2;
                 while (cn * q_pow2(2 * kk + 1) < rn) ++kk;
@@ -159,7 +167,7 @@ __global__ void __launch_bounds__(128) harvest_quad_kernel(const HarvestParams P
         if (!__any_sync(qm, chg)) break;
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-            const int kc = __shfl_sync(qm, k[c >> 2], qb + (c & 3));
+            const int kc = __shfl_sync(qm, k[c >> SH], qb + (c & (LPI - 1)));
 #pragma unroll
             for (int m = 0; m < R; ++m)
                 if (kc != k[m]) a[m][c] *= q_pow2(kc - k[m]);
@@ -168,23 +176,23 @@ __global__ void __launch_bounds__(128) harvest_quad_kernel(const HarvestParams P
         for (int m = 0; m < R; ++m) e[m] += k[m];
     }
 
-    // ---- scaling: ||B / 2^s||_1 <= 1 ------------------------------------------
+    // ---- scaling: ||B / reps||_1 <= THETA ---------------------------------------
     double nrm = 0.0;
 #pragma unroll
     for (int c = 0; c < D; ++c) {
         double p = 0.0;
 #pragma unroll
         for (int m = 0; m < R; ++m) p += fabs(a[m][c]);
-        nrm = fmax(nrm, q_sum(p, qm));
+        nrm = fmax(nrm, q_sum<LPI>(p, qm));
     }
-    int s = 0;
-    if (nrm > 1.0) {
-        s = q_exp2i(nrm);
-        if (nrm > q_pow2(s)) ++s;
-        if (s > 30) status = LMEP_NONFINITE;    // ||B|| > 2^30: not a stencil operator
-    }
-    if (s > 0) {
-        const double sc = q_pow2(-s);
+    // THETA = 2: Taylor terms of a norm-2 step peak at 2 (loss < 4 bits
+    // against the decay of the exponential) and fewer steps beat shorter series
+    constexpr double THETA = HARVEST_THETA;
+    int s = 0;                                  // number of steps `reps`
+    if (!(nrm <= 1e9)) status = LMEP_NONFINITE; // also NaN: not a stencil operator
+    else s = nrm > THETA ? (int)ceil(nrm / THETA) : 1;
+    if (s > 1) {
+        const double sc = 1.0 / (double)s;
 #pragma unroll
         for (int m = 0; m < R; ++m)
 #pragma unroll
@@ -193,14 +201,14 @@ __global__ void __launch_bounds__(128) harvest_quad_kernel(const HarvestParams P
 
     // ---- exp(A) e_idx for every wanted column -----------------------------------
     int nmv = 0;
-    const int reps = status == LMEP_OK ? (1 << s) : 0;
+    const int reps = status == LMEP_OK ? s : 0;
     for (int qo = 0; qo < sd; ++qo) {
         const int idx = qo == 0 ? row : n + qo - 1;
         double t[D], acc[R];
 #pragma unroll
         for (int c = 0; c < D; ++c) t[c] = (c == idx) ? 1.0 : 0.0;
 #pragma unroll
-        for (int m = 0; m < R; ++m) acc[m] = (q + 4 * m == idx) ? 1.0 : 0.0;
+        for (int m = 0; m < R; ++m) acc[m] = (q + LPI * m == idx) ? 1.0 : 0.0;
         for (int rep = 0; rep < reps; ++rep) {
             double wprev = INFINITY;
             for (int kt = 1; kt <= TAYLOR_MAX; ++kt) {
@@ -219,33 +227,33 @@ __global__ void __launch_bounds__(128) harvest_quad_kernel(const HarvestParams P
                     acc[m] += w[m];
                     // convergence is judged on the extracted rows only: the
                     // augmentation chain (rows >= n) is O(1) while dt^j phi_j is tiny
-                    if (q + 4 * m < n) {
+                    if (q + LPI * m < n) {
                         wn = fmax(wn, fabs(w[m]));
                         an = fmax(an, fabs(acc[m]));
                     }
                 }
                 ++nmv;
-                wn = q_max(wn, qm);
-                an = q_max(an, qm);
+                wn = q_max<LPI>(wn, qm);
+                an = q_max<LPI>(an, qm);
 #pragma unroll
-                for (int c = 0; c < D; ++c) t[c] = __shfl_sync(qm, w[c >> 2], qb + (c & 3));
+                for (int c = 0; c < D; ++c) t[c] = __shfl_sync(qm, w[c >> SH], qb + (c & (LPI - 1)));
                 // the chain needs qo products to reach the extracted rows
                 if (kt > qo && an > 0.0 && wn + wprev <= 0x1p-53 * an) break;
                 wprev = wn;
             }
 #pragma unroll
-            for (int c = 0; c < D; ++c) t[c] = __shfl_sync(qm, acc[c >> 2], qb + (c & 3));
+            for (int c = 0; c < D; ++c) t[c] = __shfl_sync(qm, acc[c >> SH], qb + (c & (LPI - 1)));
         }
         // back to A's coordinates: exp(A) e_idx = 2^-e_idx D exp(B) e_idx
         int eo = 0;
 #pragma unroll
         for (int m = 0; m < R; ++m)
-            if ((idx >> 2) == m) eo = e[m];
-        const int eidx = __shfl_sync(qm, eo, qb + (idx & 3));
+            if ((idx >> SH) == m) eo = e[m];
+        const int eidx = __shfl_sync(qm, eo, qb + (idx & (LPI - 1)));
         bool okv = true;
 #pragma unroll
         for (int m = 0; m < R; ++m) {
-            const int j = q + 4 * m;
+            const int j = q + LPI * m;
             double w = acc[m] * q_pow2(e[m] - eidx);
             okv &= (bool)isfinite(w);
             if (qo > 0 && ((fz >> j) & 1ull)) w = 0.0;
@@ -258,20 +266,26 @@ __global__ void __launch_bounds__(128) harvest_quad_kernel(const HarvestParams P
     }
     if (live && q == 0) {
         if (P.status) P.status[b] = status;
-        if (P.ms) P.ms[b] = nmv | (s << 24);
+        if (P.ms) P.ms[b] = nmv | (min(s, 255) << 24);
     }
 }
+
+static int g_lanes_per_item = 8;     // d > 8: 8 lanes per item (lower registers, 2x warps)
 
 template <int D>
 static int launch_quad(const HarvestParams &P, cudaStream_t st)
 {
-    const int64_t threads = P.B * 4;
+    const int lpi = (D > 8 && g_lanes_per_item == 8) ? 8 : 4;
+    const int64_t threads = P.B * lpi;
     const int64_t blocks = (threads + 127) / 128;
     if (blocks > 0x7fffffffLL) return LMEP_INVALID_CONFIG;
     const size_t shm = (P.mode == 1 && P.table_idx == nullptr) ? (size_t)P.nterms * P.n * P.n * 8 : 0;
-    harvest_quad_kernel<D><<<(unsigned)blocks, 128, shm, st>>>(P);
+    if (lpi == 8) harvest_quad_kernel<D, 8><<<(unsigned)blocks, 128, shm, st>>>(P);
+    else harvest_quad_kernel<D, 4><<<(unsigned)blocks, 128, shm, st>>>(P);
     return launch_status("harvest_quad_kernel");
 }
+
+void set_lanes_per_item(int lpi) { g_lanes_per_item = lpi; }
 
 int launch_harvest_quad(const HarvestParams &P, cudaStream_t st)
 {
