@@ -397,8 +397,27 @@ def main():
 
     # roofline of the per-node step kernel (HBM) and of the harvest (FP64)
     hbm, hbm_kind = peaks()
-    step_bytes = bench.nloc * (8 * w.n + 16)               # u in/out + 13 rows per node
-    per_launch_ms = step_ms / w.steps
+    # Step traffic of the algorithm that runs.  One step per launch (the
+    # reference schedule) moves 16 + 8n bytes per node; the temporally blocked
+    # kernel (rows in registers for k steps, lin_pernode_tb_kernel) moves, per
+    # launch of k steps, the rows + u of its staged range (tile + k(n-1)) once
+    # and the tile's u once.  achieved = those bytes / the per-launch time.
+    from paper_2603_15964_b200 import _native as nat, _ops
+    pl = _ops.plan(bench.sset, nat.SCH_LIN, nat.NL_NONE, nat.W_PERNODE, w.steps) \
+        if world == 1 else {"tile": 0, "ksteps": 1}
+    kb = max(1, pl["ksteps"])
+    if world == 1 and pl["tile"] > 0 and kb > 1:
+        launches_steps = -(-w.steps // kb)
+        ks = [min(kb, w.steps - i * kb) for i in range(launches_steps)]
+        step_bytes_total = sum(bench.nloc * (8 * w.n + 8) * (pl["tile"] + k * (w.n - 1)) /
+                               pl["tile"] + bench.nloc * 8 for k in ks)
+        step_kernel = f"lin_pernode_tb_kernel<13,3> (rows in registers, k={kb} steps/launch)"
+        per_launch_ms = step_ms / launches_steps
+        step_bytes = step_bytes_total / launches_steps
+    else:
+        step_bytes = bench.nloc * (8 * w.n + 16)           # u in/out + 13 rows per node
+        step_kernel = "lin_pernode_kernel<13,4> (per-node rows, one step per launch)"
+        per_launch_ms = step_ms / w.steps
     achieved = step_bytes / (per_launch_ms * 1e-3) / 1e9
     ms_items = bench.harvest_ms_stats()
     d = w.n                                               # s = 1: d = n
@@ -444,10 +463,10 @@ def main():
                          "traffic": traffic("harvest_quad_kernel<13>", "bytes_per_item", bench.nloc),
                          "algorithmic_flops_per_launch": flops,
                          "peak_kind": "measured DFMA chains (tools/fp64_peak.cu), this run"},
-            "roofline_step": {"bound": "hbm", "kernel": "lin_pernode_kernel<13,4> (per-node rows, exact)",
+            "roofline_step": {"bound": "hbm", "kernel": step_kernel,
                               "achieved": achieved, "peak": hbm, "unit": "GB/s",
                               "frac": achieved / hbm,
-                              "traffic": traffic("lin_pernode_kernel<13,4>", "bytes_per_node",
+                              "traffic": traffic(step_kernel.split(" ")[0], "bytes_per_node",
                                                  bench.nloc),
                               "algorithmic_bytes_per_launch": step_bytes,
                               "peak_kind": f"{hbm_kind} (MEASURED_PEAKS.json hbm_gbs)"},

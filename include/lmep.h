@@ -229,8 +229,9 @@ int lmep_step_etd2(const lmep_grid *grid, const lmep_weights *w, const lmep_bc *
 int lmep_banded_matvec(const lmep_grid *grid, const lmep_weights *w, const lmep_halo *halo,
                        const double *u, double *out, int32_t flags, void *stream);
 
-/* Chooses the launch shape the library would use (for reporting/tests). */
-int lmep_plan(const lmep_grid *grid, int scheme, int nl_kind, int64_t steps,
+/* Chooses the launch shape the library would use (for reporting/tests).
+ * scheme: 0 linear, 1 etdrk4, 2 etd2; weight_mode: LMEP_W_*. */
+int lmep_plan(const lmep_grid *grid, int scheme, int nl_kind, int weight_mode, int64_t steps,
               lmep_tuning *out);
 
 /* Transpose (N, n) row-major per-node rows into the SoA [n][N] layout. */

@@ -112,7 +112,7 @@ def load(path: str | None = None):
     L.lmep_step_etd2.argtypes = [G, W, B, H, C.c_int, dbl, vp, vp, vp, vp, vp, i64, i32, T, vp,
                                  vp]
     L.lmep_banded_matvec.argtypes = [G, W, H, vp, vp, i32, vp]
-    L.lmep_plan.argtypes = [G, C.c_int, C.c_int, i64, T]
+    L.lmep_plan.argtypes = [G, C.c_int, C.c_int, C.c_int, i64, T]
     L.lmep_rows_to_soa.argtypes = [vp, i64, C.c_int, vp, vp]
     L.lmep_set_harvest_method.argtypes = [C.c_int]
     for name in EXPORTS:

@@ -438,3 +438,12 @@ def validate_members(members, weights_shape) -> StencilSet:
         if np.array_equal(cand.members_array(), m):
             return cand
     raise InvalidConfig("members are not contiguous select_stencils windows; no device path")
+
+
+def plan(layout: StencilSet, scheme: int, nl: int, weight_mode: int, steps: int) -> dict:
+    """The launch shape liblmep picks (lmep_plan): tile, ksteps, ring, threads."""
+    g = c_grid(layout)
+    t = nat.LmepTuning()
+    st = nat.lib().lmep_plan(C.byref(g), scheme, nl, weight_mode, int(steps), C.byref(t))
+    nat.check(st, "lmep_plan")
+    return {"tile": t.tile, "ksteps": t.ksteps, "ring": t.ring, "threads": t.threads}

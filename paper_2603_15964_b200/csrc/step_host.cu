@@ -54,6 +54,18 @@ int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded
         return LMEP_OK;
     }
     int64_t tile = t.tile, k = t.ksteps;
+    if (pernode && sch == SCH_LIN && g.periodic && !sharded && tb_nodes_per_cta(n) > 0 &&
+        steps > 1 && t.tile == 0) {
+        // per-node rows held in registers for k steps (lin_pernode_tb_kernel)
+        k = t.ksteps > 0 ? t.ksteps : std::min<int64_t>(16, steps);
+        const int64_t span = tb_nodes_per_cta(n);
+        while (k > 1 && span - k * (n - 1) < span / 2) --k;
+        t.tile = (int32_t)(span - k * (n - 1));
+        t.ksteps = (int32_t)k;
+        t.ring = 0;
+        t.threads = 256;
+        return LMEP_OK;
+    }
     if (pernode && (sch == SCH_LIN || sharded)) k = 1;
     const int64_t nsm = num_sms();
     if (tile <= 0) {
@@ -206,6 +218,19 @@ int run_steps(const StepCall &c)
     p.slot_len = (p.slot_len + 3) & ~int64_t(3);
     const size_t shm = (size_t)nslots(c.sch) * p.slot_len * 8;
 
+    // Keep freed stream-ordered allocations in the device pool: with the
+    // default release threshold (0) every synchronize returns them to the OS
+    // and the next cudaMallocAsync maps fresh pages (milliseconds per call).
+    static bool pool_tuned = false;
+    if (!pool_tuned) {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool_tuned = true;
+    }
     // finiteness flag
     int *flag = c.nonfinite;
     int *own_flag = nullptr;
@@ -254,8 +279,11 @@ int run_steps(const StepCall &c)
             p.qhl = c.halo->hist_left; p.qhr = c.halo->hist_right;
             p.G = c.halo->width;
         }
-        if (c.sch == SCH_LIN && pernode && p.bc == LMEP_BC_NONE && k == 1 && !t.ring)
-            rc = launch_lin_pernode(p, c.stream);          // lean streaming kernel (C5)
+        if (c.sch == SCH_LIN && pernode && p.bc == LMEP_BC_NONE && !sharded && g.periodic &&
+            t.threads == 256 && t.tile + (int64_t)t.ksteps * (g.n - 1) == tb_nodes_per_cta(g.n))
+            rc = launch_lin_pernode_tb(p, c.stream);       // rows in registers, k steps (C5)
+        else if (c.sch == SCH_LIN && pernode && p.bc == LMEP_BC_NONE && k == 1 && !t.ring)
+            rc = launch_lin_pernode(p, c.stream);          // lean streaming kernel
         else
             rc = launch_step(c.sch, (c.flags & LMEP_FLAG_EXACT) != 0, pernode, p, grid, shm, c.stream);
         if (rc) break;
@@ -336,13 +364,14 @@ extern "C" int lmep_banded_matvec(const lmep_grid *grid, const lmep_weights *w,
     return run_steps(c);
 }
 
-extern "C" int lmep_plan(const lmep_grid *grid, int scheme, int nl_kind, int64_t steps,
-                         lmep_tuning *out)
+extern "C" int lmep_plan(const lmep_grid *grid, int scheme, int nl_kind, int weight_mode,
+                         int64_t steps, lmep_tuning *out)
 {
     if (!grid || !out) return LMEP_INVALID_CONFIG;
     if (scheme < 0 || scheme > 2) return LMEP_INVALID_CONFIG;
     lmep_tuning t = *out;
-    int st = plan_launch(*grid, scheme, nl_kind, steps, grid->nloc != grid->N, false, t);
+    int st = plan_launch(*grid, scheme, nl_kind, steps, grid->nloc != grid->N,
+                         weight_mode == LMEP_W_PERNODE, t);
     *out = t;
     return st;
 }

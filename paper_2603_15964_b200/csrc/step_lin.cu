@@ -67,3 +67,77 @@ int launch_lin_pernode(const StepParams &p, cudaStream_t st)
 }
 
 }  // namespace lmep
+
+namespace lmep {
+
+// Per-node linear steps with temporal blocking (periodic, single shard, no
+// closure): a CTA stages u over its tile plus k*(n-1) halo nodes in shared
+// memory and holds the per-node rows of every node it computes in REGISTERS
+// (thread t owns nodes t, t+nt, ..., t+(J-1)nt of the staged range), then
+// advances k steps on chip.  The 8n bytes of rows per node cross HBM once per
+// k steps instead of once per step.  Same ascending unfused arithmetic as
+// kernels.py:23-29 (bit-identical to the one-step kernels).
+template <int NS, int J>
+__global__ void __launch_bounds__(256, 2) lin_pernode_tb_kernel(const __grid_constant__ StepParams p)
+{
+    extern __shared__ double sm[];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int K = p.ksteps;
+    const int eL = p.row, eR = NS - 1 - p.row;
+    const int64_t t0 = (int64_t)blockIdx.x * p.tile;
+    const int64_t t1 = t0 + p.tile < p.N ? t0 + p.tile : p.N;
+    const int64_t base = t0 - (int64_t)K * eL;
+    const int len = (int)(t1 - t0) + K * (eL + eR);
+    double *U0 = sm, *U1 = sm + p.slot_len;
+    for (int i = tid; i < len; i += nt) U0[i] = p.u_in[wrap(base + i, p.N)];
+    double w[J][NS];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        const int l = tid + j * nt;
+        const int64_t g = wrap(base + (l < len ? l : 0), p.N);
+#pragma unroll
+        for (int c = 0; c < NS; ++c) w[j][c] = __ldcs(p.wp + (int64_t)c * p.nloc + g);
+    }
+    __syncthreads();
+    for (int s = 0; s < K; ++s) {
+        const int lo = (s + 1) * eL, hi = len - (s + 1) * eR;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int l = tid + j * nt;
+            if (l >= lo && l < hi) {
+                const double *x = U0 + (l - eL);
+                double acc = 0.0;
+#pragma unroll
+                for (int c = 0; c < NS; ++c) acc = xadd(acc, xmul(w[j][c], x[c]));
+                U1[l] = acc;
+            }
+        }
+        __syncthreads();
+        double *t = U0; U0 = U1; U1 = t;
+    }
+    for (int64_t i = t0 + tid; i < t1; i += nt) {
+        const double v = U0[(int)(i - base)];
+        p.u_out[i] = v;
+        if (!isfinite(v)) *p.flag = 1;
+    }
+}
+
+// nodes per CTA staged range = J * 256; returns 0 if not applicable
+int tb_nodes_per_cta(int n) { return n == 13 || n == 11 || n == 9 || n == 7 ? 3 * 256 : 0; }
+
+int launch_lin_pernode_tb(const StepParams &p, cudaStream_t st)
+{
+    constexpr int J = 3, TPB = 256;
+    const int64_t blocks = (p.N + p.tile - 1) / p.tile;
+    const size_t shm = 2 * (size_t)p.slot_len * 8;
+    switch (p.n) {
+    case 13: lin_pernode_tb_kernel<13, J><<<(unsigned)blocks, TPB, shm, st>>>(p); break;
+    case 11: lin_pernode_tb_kernel<11, J><<<(unsigned)blocks, TPB, shm, st>>>(p); break;
+    case 9: lin_pernode_tb_kernel<9, J><<<(unsigned)blocks, TPB, shm, st>>>(p); break;
+    case 7: lin_pernode_tb_kernel<7, J><<<(unsigned)blocks, TPB, shm, st>>>(p); break;
+    default: return LMEP_INVALID_CONFIG;
+    }
+    return launch_status("lin_pernode_tb_kernel");
+}
+
+}  // namespace lmep

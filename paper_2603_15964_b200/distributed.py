@@ -128,11 +128,13 @@ class ShardedStepper:
         if ksteps is None:
             ksteps = 1 if per_node and scheme.kind == "linear" else \
                 max(1, min(16, nloc // (4 * ext * max(reach, 1))))
-        if per_node and scheme.kind == "linear":
+        if per_node and scheme.kind == "linear" and world > 1:
             ksteps = 1                      # per-node rows of halo nodes are not held
+        if world == 1:
+            ksteps = 1 << 30                # no halo: the library plans the launches
         if per_node and scheme.kind != "linear" and world > 1:
             raise InvalidConfig("sharded ETD schemes need shared or class rows")
-        width = ksteps * ext * reach
+        width = ksteps * ext * reach if world > 1 else 0
         if world > 1 and width > nloc:
             raise InvalidConfig(f"slab of {nloc} nodes narrower than the halo {width}")
         self.plan = SlabPlan(off, nloc, width, ksteps)
@@ -148,6 +150,8 @@ class ShardedStepper:
         self.u = None
         self.hist = None
         self.done = 0
+        # ping-pong scratch for multi-launch calls (u and the etd2 history)
+        self.scratch = torch.empty(2 * nloc, dtype=torch.float64, device=dev)
 
     # ---------------------------------------------------------------------
     def set_initial(self, u0_global) -> None:
@@ -187,12 +191,15 @@ class ShardedStepper:
             self._exchange(k, hist=True)
 
     def _tuning(self, k):
+        if self.world == 1:
+            return self.tuning              # single shard: library heuristics
         return {**(self.tuning or {}), "ksteps": k}
 
     def compute_phase(self, k: int) -> None:
         p = self.prep
         kw = dict(bc=p.bc, nl=p.nl, exact=self.exact, tuning=self._tuning(k), flag=self.flag,
-                  off=self.plan.off, nloc=self.plan.nloc, halo=self._halo(k))
+                  off=self.plan.off, nloc=self.plan.nloc, halo=self._halo(k),
+                  scratch=self.scratch)
         if p.scheme == "linear":
             self.u = _ops.step(nat.SCH_LIN, p.bank, self.u, k, **kw)
         elif p.scheme == "etdrk4":
