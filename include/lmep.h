@@ -92,7 +92,9 @@ typedef struct {
  * every interior node (mode SHARED and CLASS).  CLASS: `classes` is a device
  * [nleft+1+nright][nrows][n] table; node t uses class t for t < nleft,
  * nleft+1+(t-(N-nright)) for t >= N-nright, and the interior set otherwise.
- * PERNODE: `pernode` is a device SoA [nrows][n][nloc] table of this shard. */
+ * PERNODE: `pernode` is a device SoA [nrows][n][nloc + 2*pernode_pad] table of
+ * this shard: local node i at column i + pernode_pad, the pad columns holding
+ * the rows of the halo nodes (needed to fuse several steps per exchange). */
 typedef struct {
     int32_t mode;
     int32_t nrows;
@@ -101,6 +103,7 @@ typedef struct {
     const double *interior;    /* host   */
     const double *classes;     /* device */
     const double *pernode;     /* device */
+    int64_t pernode_pad;
 } lmep_weights;
 
 /* Boundary closure (non-periodic grids).  DIRICHLET pins u[0]=lo, u[N-1]=hi

@@ -54,7 +54,7 @@ class LmepGrid(C.Structure):
 class LmepWeights(C.Structure):
     _fields_ = [("mode", C.c_int32), ("nrows", C.c_int32), ("nleft", C.c_int32),
                 ("nright", C.c_int32), ("interior", C.c_void_p), ("classes", C.c_void_p),
-                ("pernode", C.c_void_p)]
+                ("pernode", C.c_void_p), ("pernode_pad", C.c_int64)]
 
 
 class LmepBC(C.Structure):

@@ -171,6 +171,7 @@ class CompactRows:
     nleft: int = 0
     nright: int = 0
     pernode: torch.Tensor | None = None
+    pernode_pad: int = 0                 # halo-node columns on each side of a shard's table
     _host_interior: np.ndarray | None = field(default=None, repr=False)
 
     @property
@@ -191,7 +192,8 @@ class CompactRows:
     def row(self, r: int) -> "CompactRows":
         """The single-operator view of row r."""
         if self.mode == nat.W_PERNODE:
-            return CompactRows(self.layout, self.mode, pernode=self.pernode[r:r + 1].contiguous())
+            return CompactRows(self.layout, self.mode, pernode=self.pernode[r:r + 1].contiguous(),
+                               pernode_pad=self.pernode_pad)
         cl = None if self.classes is None else self.classes[:, r:r + 1].contiguous()
         return CompactRows(self.layout, self.mode, self.interior[r:r + 1].contiguous(), cl,
                            self.nleft, self.nright)
@@ -239,6 +241,7 @@ class CompactRows:
             w.interior = self.host_interior().ctypes.data
         w.classes = nat.ptr(self.classes) if self.classes is not None else None
         w.pernode = nat.ptr(self.pernode) if self.pernode is not None else None
+        w.pernode_pad = int(self.pernode_pad)
         return w
 
 
@@ -246,8 +249,12 @@ def stack_rows(parts: list[CompactRows]) -> CompactRows:
     """Concatenate single/multi-row CompactRows (same layout) into one bank."""
     lay = parts[0].layout
     if any(p.mode == nat.W_PERNODE for p in parts):
+        pads = {p.pernode_pad for p in parts if p.mode == nat.W_PERNODE}
+        if len(pads) > 1 or (pads != {0} and any(p.mode != nat.W_PERNODE for p in parts)):
+            raise InvalidConfig("cannot stack per-node tables with different halo padding")
         pn = [p.to_pernode().pernode for p in parts]
-        return CompactRows(lay, nat.W_PERNODE, pernode=torch.cat(pn, 0).contiguous())
+        return CompactRows(lay, nat.W_PERNODE, pernode=torch.cat(pn, 0).contiguous(),
+                           pernode_pad=pads.pop())
     if any(p.mode == nat.W_CLASS for p in parts):
         nl = max(p.nleft for p in parts)
         nr = max(p.nright for p in parts)
@@ -298,7 +305,8 @@ def combine_rows(parts: list[CompactRows], coeffs) -> CompactRows:
                 t2 = bank.classes[:, sl] * c
                 acc_c = torch.zeros_like(t2) + t2 if acc_c is None else acc_c + t2
     if bank.mode == nat.W_PERNODE:
-        return CompactRows(bank.layout, nat.W_PERNODE, pernode=acc_p.contiguous())
+        return CompactRows(bank.layout, nat.W_PERNODE, pernode=acc_p.contiguous(),
+                           pernode_pad=bank.pernode_pad)
     return CompactRows(bank.layout, bank.mode, acc_i.contiguous(),
                        None if acc_c is None else acc_c.contiguous(), bank.nleft, bank.nright)
 

@@ -49,7 +49,8 @@ struct StepParams {
     int64_t L_int, R_int;                       // fast-path interior [L_int, R_int)
     double wi[LMEP_MAX_ROWS][LMEP_MAX_N];       // interior / shared rows
     const double *wc;                           // class rows [C][nrows][n]
-    const double *wp;                           // per-node SoA [nrows][n][nloc]
+    const double *wp;                           // per-node SoA [nrows][n][wld]
+    int64_t wld, wpad;                          // per-node table: leading dim, local node 0 at wpad
     int nl;
     int bc;
     double lo, hi;
@@ -123,8 +124,8 @@ __device__ __noinline__ double band_slow(const StepParams &p, int r, const doubl
     if (p.wmode == LMEP_W_PERNODE) {
         // single shard: halo nodes of a periodic tile wrap onto their owners
         const int64_t li = (p.periodic && p.hl == nullptr) ? wrap(i, p.N) : i - p.off;
-        wr = p.wp + (int64_t)r * n * p.nloc + li;
-        ws = p.nloc;
+        wr = p.wp + (int64_t)r * n * p.wld + li + p.wpad;
+        ws = p.wld;
     } else if (p.wmode == LMEP_W_CLASS) {
         const int64_t cl = class_of(p, i);
         wr = cl < 0 ? p.wi[r] : p.wc + (cl * p.nrows + r) * n;
@@ -156,12 +157,12 @@ __device__ __forceinline__ void band_fast(const StepParams &p, int r, const doub
                 out[q] = acc;
             }
         } else {
-            const double *w = p.wp + (int64_t)r * NS * p.nloc + (lbase + l);
+            const double *w = p.wp + (int64_t)r * NS * p.wld + (lbase + l + p.wpad);
 #pragma unroll
             for (int q = 0; q < P; ++q) {
                 double acc = 0.0;
 #pragma unroll
-                for (int j = 0; j < NS; ++j) acc = macc<EX>(acc, __ldcs(w + (int64_t)j * p.nloc + q), win[q + j]);
+                for (int j = 0; j < NS; ++j) acc = macc<EX>(acc, __ldcs(w + (int64_t)j * p.wld + q), win[q + j]);
                 out[q] = acc;
             }
         }
@@ -172,8 +173,8 @@ __device__ __forceinline__ void band_fast(const StepParams &p, int r, const doub
             if constexpr (!PN) {
                 for (int j = 0; j < n; ++j) acc = macc<EX>(acc, p.wi[r][j], x[q + j]);
             } else {
-                const double *w = p.wp + (int64_t)r * n * p.nloc + (lbase + l) + q;
-                for (int j = 0; j < n; ++j) acc = macc<EX>(acc, __ldcs(w + (int64_t)j * p.nloc), x[q + j]);
+                const double *w = p.wp + (int64_t)r * n * p.wld + (lbase + l + p.wpad) + q;
+                for (int j = 0; j < n; ++j) acc = macc<EX>(acc, __ldcs(w + (int64_t)j * p.wld), x[q + j]);
             }
             out[q] = acc;
         }

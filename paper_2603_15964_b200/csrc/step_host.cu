@@ -34,7 +34,7 @@ static int num_sms()
 static const int64_t kSmemBudget = 200 * 1024;  // bytes per CTA we allow ourselves
 
 int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded, bool pernode,
-                lmep_tuning &t)
+                lmep_tuning &t, int64_t pernode_pad)
 {
     const int n = g.n, eL = g.row, eR = n - 1 - g.row;
     const int ext = step_ext(sch, nl);
@@ -54,10 +54,11 @@ int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded
         return LMEP_OK;
     }
     int64_t tile = t.tile, k = t.ksteps;
-    if (pernode && sch == SCH_LIN && g.periodic && !sharded && tb_nodes_per_cta(n) > 0 &&
-        steps > 1 && t.tile == 0) {
-        // per-node rows held in registers for k steps (lin_pernode_tb_kernel)
-        k = t.ksteps > 0 ? t.ksteps : std::min<int64_t>(16, steps);
+    if (pernode && sch == SCH_LIN && g.periodic && tb_nodes_per_cta(n) > 0 && steps > 1 &&
+        t.tile == 0 && (!sharded || pernode_pad >= steps * std::max(eL, eR))) {
+        // per-node rows held in registers for k steps (lin_pernode_tb_kernel);
+        // sharded: the caller fuses `steps` steps per halo exchange
+        k = sharded ? steps : (t.ksteps > 0 ? t.ksteps : std::min<int64_t>(16, steps));
         const int64_t span = tb_nodes_per_cta(n);
         while (k > 1 && span - k * (n - 1) < span / 2) --k;
         t.tile = (int32_t)(span - k * (n - 1));
@@ -150,7 +151,7 @@ int run_steps(const StepCall &c)
     const int need_rows = c.nl == LMEP_NL_CONVECTIVE ? LMEP_ROW_D1 + 1 : need;
     if (w.nrows < need_rows || w.nrows > LMEP_MAX_ROWS) return LMEP_DIMENSION;
     if (!pernode && !w.interior) return LMEP_INVALID_CONFIG;
-    if (pernode && !w.pernode) return LMEP_INVALID_CONFIG;
+    if (pernode && (!w.pernode || w.pernode_pad < 0)) return LMEP_INVALID_CONFIG;
     if (w.mode == LMEP_W_CLASS) {
         if (!w.classes || w.nleft < 0 || w.nright < 0 || w.nleft + w.nright >= g.N)
             return LMEP_INVALID_CONFIG;
@@ -174,7 +175,7 @@ int run_steps(const StepCall &c)
     lmep_tuning t{};
     if (c.tuning) t = *c.tuning;
     if (sharded) { t.ring = 0; }
-    int st = plan_launch(g, c.sch, c.nl, c.steps, sharded, pernode, t);
+    int st = plan_launch(g, c.sch, c.nl, c.steps, sharded, pernode, t, pernode ? w.pernode_pad : 0);
     if (st) return st;
 
     static StepParams p;  // host staging (the struct is large); calls are serialised per process
@@ -188,6 +189,8 @@ int run_steps(const StepCall &c)
             for (int j = 0; j < g.n; ++j) p.wi[r][j] = w.interior[r * g.n + j];
     p.wc = w.classes;
     p.wp = w.pernode;
+    p.wpad = pernode ? w.pernode_pad : 0;
+    p.wld = g.nloc + 2 * p.wpad;
     if (g.periodic) {
         p.L_int = INT64_MIN / 4;
         p.R_int = INT64_MAX / 4;
@@ -279,7 +282,7 @@ int run_steps(const StepCall &c)
             p.qhl = c.halo->hist_left; p.qhr = c.halo->hist_right;
             p.G = c.halo->width;
         }
-        if (c.sch == SCH_LIN && pernode && p.bc == LMEP_BC_NONE && !sharded && g.periodic &&
+        if (c.sch == SCH_LIN && pernode && p.bc == LMEP_BC_NONE && g.periodic &&
             t.threads == 256 && t.tile + (int64_t)t.ksteps * (g.n - 1) == tb_nodes_per_cta(g.n))
             rc = launch_lin_pernode_tb(p, c.stream);       // rows in registers, k steps (C5)
         else if (c.sch == SCH_LIN && pernode && p.bc == LMEP_BC_NONE && k == 1 && !t.ring)
@@ -371,7 +374,7 @@ extern "C" int lmep_plan(const lmep_grid *grid, int scheme, int nl_kind, int wei
     if (scheme < 0 || scheme > 2) return LMEP_INVALID_CONFIG;
     lmep_tuning t = *out;
     int st = plan_launch(*grid, scheme, nl_kind, steps, grid->nloc != grid->N,
-                         weight_mode == LMEP_W_PERNODE, t);
+                         weight_mode == LMEP_W_PERNODE, t, 0);
     *out = t;
     return st;
 }

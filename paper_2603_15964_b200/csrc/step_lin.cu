@@ -32,21 +32,21 @@ __global__ void __launch_bounds__(256) lin_pernode_kernel(const __grid_constant_
         const int64_t g = p.off + li;
         int64_t st = g - p.row;
         if (!p.periodic) st = st < 0 ? 0 : (st > p.N - n ? p.N - n : st);
-        const double *w = p.wp + li;
+        const double *w = p.wp + li + p.wpad;
         double acc = 0.0;
         if (single && p.periodic && st >= 0 && st + n <= p.N) {
             const double *u = p.u_in + st;
 #pragma unroll
             for (int j = 0; j < (NS > 0 ? NS : 1); ++j) {
                 if (NS == 0) break;
-                acc = xadd(acc, xmul(__ldcs(w + (int64_t)j * p.nloc), __ldg(u + j)));
+                acc = xadd(acc, xmul(__ldcs(w + (int64_t)j * p.wld), __ldg(u + j)));
             }
             if (NS == 0)
                 for (int j = 0; j < n; ++j)
-                    acc = xadd(acc, xmul(__ldcs(w + (int64_t)j * p.nloc), __ldg(u + j)));
+                    acc = xadd(acc, xmul(__ldcs(w + (int64_t)j * p.wld), __ldg(u + j)));
         } else {
             for (int j = 0; j < n; ++j)
-                acc = xadd(acc, xmul(__ldcs(w + (int64_t)j * p.nloc),
+                acc = xadd(acc, xmul(__ldcs(w + (int64_t)j * p.wld),
                                      load_node(p, p.u_in, p.hl, p.hr, st + j)));
         }
         p.u_out[li] = acc;
@@ -84,19 +84,24 @@ __global__ void __launch_bounds__(256, 2) lin_pernode_tb_kernel(const __grid_con
     const int tid = threadIdx.x, nt = blockDim.x;
     const int K = p.ksteps;
     const int eL = p.row, eR = NS - 1 - p.row;
+    // tile of this shard (local indices), staged range in global indices
     const int64_t t0 = (int64_t)blockIdx.x * p.tile;
-    const int64_t t1 = t0 + p.tile < p.N ? t0 + p.tile : p.N;
-    const int64_t base = t0 - (int64_t)K * eL;
+    const int64_t t1 = t0 + p.tile < p.nloc ? t0 + p.tile : p.nloc;
+    const int64_t base = p.off + t0 - (int64_t)K * eL;
     const int len = (int)(t1 - t0) + K * (eL + eR);
+    const bool single = p.hl == nullptr && p.hr == nullptr;
     double *U0 = sm, *U1 = sm + p.slot_len;
-    for (int i = tid; i < len; i += nt) U0[i] = p.u_in[wrap(base + i, p.N)];
+    for (int i = tid; i < len; i += nt) U0[i] = load_node(p, p.u_in, p.hl, p.hr, base + i);
+    // rows: single shard -> the periodic grid's own table (wrap); sharded ->
+    // this shard's table, padded with the rows of wpad halo nodes per side
     double w[J][NS];
 #pragma unroll
     for (int j = 0; j < J; ++j) {
         const int l = tid + j * nt;
-        const int64_t g = wrap(base + (l < len ? l : 0), p.N);
+        const int64_t g = base + (l < len ? l : (int64_t)K * eL);
+        const int64_t wi = single ? wrap(g, p.N) : g - p.off + p.wpad;
 #pragma unroll
-        for (int c = 0; c < NS; ++c) w[j][c] = __ldcs(p.wp + (int64_t)c * p.nloc + g);
+        for (int c = 0; c < NS; ++c) w[j][c] = __ldcs(p.wp + (int64_t)c * p.wld + wi);
     }
     __syncthreads();
     for (int s = 0; s < K; ++s) {
@@ -115,11 +120,13 @@ __global__ void __launch_bounds__(256, 2) lin_pernode_tb_kernel(const __grid_con
         __syncthreads();
         double *t = U0; U0 = U1; U1 = t;
     }
+    bool bad = false;
     for (int64_t i = t0 + tid; i < t1; i += nt) {
-        const double v = U0[(int)(i - base)];
+        const double v = U0[(int)(i + K * eL - t0)];
         p.u_out[i] = v;
-        if (!isfinite(v)) *p.flag = 1;
+        bad |= !isfinite(v);
     }
+    if (bad) *p.flag = 1;
 }
 
 // nodes per CTA staged range = J * 256; returns 0 if not applicable
@@ -128,7 +135,7 @@ int tb_nodes_per_cta(int n) { return n == 13 || n == 11 || n == 9 || n == 7 ? 3 
 int launch_lin_pernode_tb(const StepParams &p, cudaStream_t st)
 {
     constexpr int J = 3, TPB = 256;
-    const int64_t blocks = (p.N + p.tile - 1) / p.tile;
+    const int64_t blocks = (p.nloc + p.tile - 1) / p.tile;
     const size_t shm = 2 * (size_t)p.slot_len * 8;
     switch (p.n) {
     case 13: lin_pernode_tb_kernel<13, J><<<(unsigned)blocks, TPB, shm, st>>>(p); break;

@@ -125,11 +125,13 @@ class ShardedStepper:
         reach = max(sset.row, sset.n - 1 - sset.row)
         ext = _ext(scheme.kind, nl)
         per_node = _is_per_node(grid, problem)
+        # periodic per-node linear rows: the shard also harvests its halo
+        # nodes' rows (no communication), so k steps fuse per exchange
+        pad_ok = per_node and scheme.kind == "linear" and grid.periodic
         if ksteps is None:
-            ksteps = 1 if per_node and scheme.kind == "linear" else \
-                max(1, min(16, nloc // (4 * ext * max(reach, 1))))
-        if per_node and scheme.kind == "linear" and world > 1:
-            ksteps = 1                      # per-node rows of halo nodes are not held
+            ksteps = max(1, min(16, nloc // (4 * ext * max(reach, 1))))
+        if per_node and scheme.kind == "linear" and world > 1 and not pad_ok:
+            ksteps = 1                      # non-periodic per-node rows: one step per exchange
         if world == 1:
             ksteps = 1 << 30                # no halo: the library plans the launches
         if per_node and scheme.kind != "linear" and world > 1:
@@ -138,7 +140,8 @@ class ShardedStepper:
         if world > 1 and width > nloc:
             raise InvalidConfig(f"slab of {nloc} nodes narrower than the halo {width}")
         self.plan = SlabPlan(off, nloc, width, ksteps)
-        self.prep = _prepare_shard(grid, sset, problem, scheme, delta_t, off, nloc)
+        pad = ksteps * reach if (pad_ok and world > 1 and ksteps > 1) else 0
+        self.prep = _prepare_shard(grid, sset, problem, scheme, delta_t, off, nloc, pad)
         self.ex = exchanger
         dev = nat.device()
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -250,7 +253,7 @@ def _is_per_node(grid: Grid, problem: SemiLinearProblem) -> bool:
         (not grid.periodic and grid.uniform_spacing is None)
 
 
-def _prepare_shard(grid, sset, problem, scheme, delta_t, off, nloc) -> Prepared:
+def _prepare_shard(grid, sset, problem, scheme, delta_t, off, nloc, pad=0) -> Prepared:
     """timestep.prepare restricted to one slab (per-node rows of the slab only)."""
     nl = _nl_kind(problem)
     bc = _bc_for(grid, sset, problem.boundary)
@@ -262,7 +265,7 @@ def _prepare_shard(grid, sset, problem, scheme, delta_t, off, nloc) -> Prepared:
     spec = problem.linear
     warm = None
     if scheme.kind == "linear":
-        bank = harvest_compact(grid, sset, spec, delta_t, 1, frozen, node_range=rng)
+        bank = harvest_compact(grid, sset, spec, delta_t, 1, frozen, node_range=rng, pad=pad)
     elif scheme.kind == "etdrk4":
         full = harvest_compact(grid, sset, spec, delta_t, 4, frozen, node_range=rng)
         half = harvest_compact(grid, sset, spec, delta_t / 2, 2, frozen, node_range=rng)

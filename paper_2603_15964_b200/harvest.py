@@ -235,10 +235,13 @@ def _rows_from(plan: _Plan, sset: StencilSet, out: torch.Tensor) -> _ops.Compact
 
 def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
                     frozen_nodes=(), stats: dict | None = None,
-                    node_range: tuple[int, int] | None = None) -> _ops.CompactRows:
+                    node_range: tuple[int, int] | None = None,
+                    pad: int = 0) -> _ops.CompactRows:
     """Harvest w_lin and the raw dt^j phi_j rows (R = s) for the whole grid.
     node_range=(off, nloc): per-node rows only for the shard's nodes (the
-    shared / class modes are grid-wide by construction)."""
+    shared / class modes are grid-wide by construction); pad > 0 (periodic
+    per-node only) also harvests the `pad` halo nodes on each side, so a shard
+    can fuse several steps per halo exchange."""
     if not 1 <= s <= 6:
         raise ValueError(f"augmentation depth must be in [1, 6], got {s}")
     n = sset.n
@@ -264,14 +267,26 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
         if stats is not None:
             stats.setdefault("ms", []).append(h.ms)
         return _rows_from(plan, sset, h.rows)
-    # per-node path: one item per node (of the shard)
+    # per-node path: one item per node (of the shard, plus its halo nodes)
     off, N = (0, sset.N) if node_range is None else (int(node_range[0]), int(node_range[1]))
-    sl = slice(off, off + N)
+    if pad and not (grid.periodic and plan.uniform_rows):
+        raise InvalidConfig("padded per-node tables are supported on periodic grids only")
     shared_coords = plan.coords.shape[0] == 1
     uniform_rows = plan.uniform_rows
+    if pad:
+        idx = torch.remainder(torch.arange(off - pad, off + N + pad, device=d), sset.N)
+        N += 2 * pad
+    else:
+        idx = None
+    sl = slice(off, off + N)
     if varcoef:
-        coef_all = _ops.dev_f64(spec.coef[sl])
-        react = None if spec.reaction is None else _ops.dev_f64(spec.reaction[sl])
+        if idx is not None:
+            coef_all = _ops.dev_f64(spec.coef).index_select(0, idx).contiguous()
+            react = None if spec.reaction is None else \
+                _ops.dev_f64(spec.reaction).index_select(0, idx).contiguous()
+        else:
+            coef_all = _ops.dev_f64(spec.coef[sl])
+            react = None if spec.reaction is None else _ops.dev_f64(spec.reaction[sl])
     if node_range is not None and not uniform_rows:
         plan = _Plan(plan.mode, plan.coords if shared_coords else plan.coords[sl],
                      plan.rows[sl], plan.masks[sl])
@@ -292,7 +307,7 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
         _ops.raise_on_status(h)
         if stats is not None:
             stats.setdefault("ms", []).append(h.ms)
-        return _ops.CompactRows(sset, nat.W_PERNODE, pernode=h.rows)
+        return _ops.CompactRows(sset, nat.W_PERNODE, pernode=h.rows, pernode_pad=int(pad))
     # per-node coordinates (non-uniform grids): chunked to bound the table memory
     out = torch.empty((s, n, N), dtype=torch.float64, device=d)
     rows_all = _ops.dev_i32(plan.rows)
