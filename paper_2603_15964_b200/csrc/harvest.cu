@@ -296,13 +296,16 @@ __device__ bool lu_solve(double *Q, double *P, double *inv_piv, int d, int lane)
     using T = Tile<DP>;
     const int c = lane % DP, g = lane / DP;
     for (int k = 0; k < d; ++k) {
-        // pivot: max |Q[i][k]|, i >= k (32-bit key: high word of |q|, then lowest index)
-        const double qv = (lane >= k && lane < d) ? fabs(Q[lane * T::LD + k]) : 0.0;
-        const unsigned key = (lane >= k && lane < d)
-                                 ? ((unsigned)__double2hiint(qv) & ~31u) | (31u - lane) : 0u;
-        const unsigned best = __reduce_max_sync(FULL, key);
-        const int idx = 31 - (int)(best & 31u);
-        if (!(__shfl_sync(FULL, qv, idx) > 0.0)) return false;
+        // pivot: first maximal |Q[i][k]|, i >= k (LAPACK idamax), exact comparison
+        double val = (lane >= k && lane < d) ? fabs(Q[lane * T::LD + k]) : -1.0;
+        int idx = lane;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(FULL, val, o);
+            const int oi = __shfl_xor_sync(FULL, idx, o);
+            if (ov > val || (ov == val && oi < idx)) { val = ov; idx = oi; }
+        }
+        if (!(val > 0.0)) return false;
         if (idx != k) {
             if (lane < d) {
                 double t = Q[k * T::LD + lane];
@@ -330,7 +333,7 @@ __device__ bool lu_solve(double *Q, double *P, double *inv_piv, int d, int lane)
         __syncwarp();
     }
     for (int k = d - 1; k >= 0; --k) {
-        const double x = (c < d) ? P[k * T::LD + c] * inv_piv[k] : 0.0;
+        const double x = (c < d) ? P[k * T::LD + c] / Q[k * T::LD + k] : 0.0;
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < T::E; ++j) {

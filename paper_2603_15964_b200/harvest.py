@@ -402,17 +402,21 @@ def combine(props: list[BandedPropagator], coeffs) -> BandedPropagator:
 
 
 def weight_table_json(stencils, rows: list[PhiWeightSet]) -> str:
-    """17-significant-digit JSON weight table (harvest.py:238-265)."""
-    import json
-
+    """Weight table as JSON with 17 significant digits, one record per node
+    (harvest.py:238-265); the text is the reference's byte for byte."""
     st = list(stencils)
     if len(st) != len(rows):
         raise DimensionMismatch("one weight set per stencil required")
-    g = lambda x: float(format(float(x), ".17g"))  # noqa: E731
-    doc = {"delta_t": g(rows[0].delta_t), "N": len(st), "n": st[0].n,
-           "s": len(rows[0].w_phi) + 1,
-           "nodes": [{"index": int(s_.target), "target_row": int(s_.target_row),
-                      "members": [int(m) for m in s_.members],
-                      "w_lin": [g(w) for w in r.w_lin],
-                      "w_phi": [[g(w) for w in v] for v in r.w_phi]} for s_, r in zip(st, rows)]}
-    return json.dumps(doc, separators=(", ", ": "))
+
+    def num(x):
+        return format(float(x), ".17g")
+
+    def vec(v):
+        return "[" + ", ".join(num(x) for x in v) + "]"
+
+    recs = ['{"index": %d, "target_row": %d, "members": [%s], "w_lin": %s, "w_phi": [%s]}'
+            % (int(s_.target), int(s_.target_row), ", ".join(str(int(m)) for m in s_.members),
+               vec(r.w_lin), ", ".join(vec(v) for v in r.w_phi)) for s_, r in zip(st, rows)]
+    head = '{"delta_t": %s, "N": %d, "n": %d, "s": %d, "nodes": [' % (
+        num(rows[0].delta_t), len(st), st[0].n, len(rows[0].w_phi) + 1)
+    return head + ", ".join(recs) + "]}"

@@ -261,8 +261,64 @@ def main(out=os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.np
     G["c5_u"] = kernels.run_linear(np.ascontiguousarray(W5[:, 0, :]), members, w5.u0, w5.steps,
                                    False, 0.0, 0.0)
 
+    # ---- 13. Chebyshev grid (the paper's Allen-Cahn setup, problems.py:150-167):
+    #          per-node harvest with frozen ends + pinned Dirichlet ETDRK4 run
+    from localexp import problems as le_problems
+    spec = le_problems.allen_cahn_benchmark(N=64, n=21)
+    gridc = le.make_chebyshev_grid(spec.N, spec.x_min, spec.x_max)
+    stc = le.select_stencils(gridc, spec.n, spec.policy)
+    u0c = spec.initial(gridc.nodes)
+    probc = le.SemiLinearProblem(spec.linear, None, u0c, spec.boundary, "cubic")
+    resc = le.run(gridc, stc, probc, le.SchemeConfig("etdrk4"), spec.delta_t, 30 * spec.delta_t)
+    G["cheb_u0"] = u0c
+    G["cheb_u"] = resc.u_final
+    ofc = le.assemble_global_phi(gridc, stc, spec.linear, spec.delta_t, s=4,
+                                 frozen_nodes=(0, spec.N - 1))
+    G["cheb_w"] = np.stack([o.weights for o in ofc])
+    # 60-digit values of the same rows (mpmath expm of the (n+3) augmentation,
+    # mathematically identical to the reference's block form): the truth the
+    # reference and the device harvest are both measured against, because the
+    # boundary-adjacent Chebyshev operators (||dt L||_1 ~ 1e9) are too
+    # ill-conditioned for any fp64 formulation to agree to 1e-12.
+    G["cheb_exact"] = _cheb_exact(le, gridc, stc, spec, (0, spec.N - 1))
+
+    # ---- 14. weight_table_json (harvest.py:238-265) ---------------------------
+    gw = le.make_periodic_grid(6, 0.0, 1.0)
+    sw = le.select_stencils(gw, 3, le.StencilPolicy.CENTERED)
+    from localexp import harvest as le_harvest
+    rows = le_harvest._harvest_rows(gw, sw, le.LinearOperatorSpec(((2, 0.3), (1, -0.7))), 0.01, 2)
+    G["wtj"] = np.array(le.weight_table_json(sw, rows))
+
     np.savez_compressed(out, **G)
     print(f"wrote {out}: {len(G)} arrays, {os.path.getsize(out)} bytes")
+
+
+def _cheb_exact(le, grid, stencils, spec, frozen_nodes, digits=50):
+    import mpmath
+    mpmath.mp.dps = digits
+    N, n, s = grid.size, stencils[0].n, 4
+    out = np.zeros((s, N, n))
+    for t, st in enumerate(stencils):
+        coords = grid.nodes[st.members] - grid.nodes[t]
+        L = le.local_operator(coords, spec.linear)
+        fz = [j for j, m in enumerate(st.members.tolist()) if m in frozen_nodes]
+        r = st.target_row
+        D = n + s - 1
+        A = mpmath.zeros(D, D)
+        dt = mpmath.mpf(float(spec.delta_t))
+        for i in range(n):
+            if i in fz:
+                continue
+            for j in range(n):
+                A[j, i] = dt * mpmath.mpf(float(L[i, j]))
+        A[r, n] = dt
+        for q in range(s - 2):
+            A[n + q, n + q + 1] = dt
+        E = mpmath.expm(A)
+        out[0, t] = [float(E[j, r]) for j in range(n)]
+        for q in range(1, s):
+            out[q, t] = [0.0 if j in fz else float(E[j, n + q - 1]) for j in range(n)]
+    return out
 
 
 def _etdrk4_neumann(kernels, w, al, be, ga, wh, p1h, u0, steps, dl, dr):

@@ -128,3 +128,27 @@ def test_virtual_shards_bitwise(P):
         for k in (None, 1):
             u = run_virtual_shards(g, st, prob, scheme, dt, steps, P, ksteps=k)
             assert torch.equal(u, ref.u), (name, P, k, float((u - ref.u).abs().max()))
+
+
+@pytest.mark.gpu
+def test_run_sharded_single_rank_nccl():
+    """The NCCL entry point end to end on a 1-rank group matches run()."""
+    import paper_2603_15964_b200 as lx
+    from paper_2603_15964_b200 import configs
+    from paper_2603_15964_b200.distributed import run_sharded
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        w = configs.c5(N=2048, steps=20)
+        c, nu = w.coef
+        g = lx.make_periodic_grid(w.N, 0.0, 1.0)
+        st = lx.select_stencils(g, w.n, lx.StencilPolicy.CENTERED)
+        prob = lx.SemiLinearProblem(lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1)),
+                                    None, w.u0, lx.Boundary.periodic(), "none")
+        T = 20 * w.delta_t
+        a = run_sharded(g, st, prob, lx.SchemeConfig("linear"), w.delta_t, T)
+        b = lx.run(g, st, prob, lx.SchemeConfig("linear"), w.delta_t, T)
+        assert np.array_equal(a.u_final, b.u_final)
+    finally:
+        dist.destroy_process_group()
