@@ -289,6 +289,27 @@ def main(out=os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.np
     rows = le_harvest._harvest_rows(gw, sw, le.LinearOperatorSpec(((2, 0.3), (1, -0.7))), 0.01, 2)
     G["wtj"] = np.array(le.weight_table_json(sw, rows))
 
+    # ---- 15. analysis (analysis.py:42-193): stability scan, footprint, quadrature
+    from localexp import analysis as le_an
+    ga = le.make_periodic_grid(256, 0.0, 2 * math.pi)
+    sa = le.select_stencils(ga, 7, le.StencilPolicy.ONE_SIDED_UPWIND)
+    ha = ga.spacing
+    dts = [c * ha for c in (0.5, 1.5, 3.5, 5.0, 6.5, 8.0, 9.5)]
+    sb = le_an.scan_stability(ga, sa, le.LinearOperatorSpec(((1, -1.0),)), dts, steps=300)
+    G["scan_dt"] = np.array(sb.dt_grid)
+    G["scan_stable"] = np.array(sb.stable[0])
+    G["scan_dt_star"] = np.array(sb.dt_star[0])
+    row = le.assemble_global(ga, sa, le.LinearOperatorSpec(((1, -1.0),)), 3.5 * ha).weights[0]
+    fp = le_an.spectral_footprint(row, np.arange(7) - 6, ha, 33, shift=3.5 * ha)
+    G["fp_row"], G["fp_G"], G["fp_disp"] = row, fp.amplification, fp.dispersion
+    G["cc_w"] = le_an.clenshaw_curtis_weights(17)
+    G["cc_w_odd"] = le_an.clenshaw_curtis_weights(18)
+    gc = le.make_chebyshev_grid(17, -1.0, 1.0)
+    uq = np.sin(3 * gc.nodes) + 0.2
+    cq = le_an.conserved_quantities(uq, gc)
+    G["cq"] = np.array([cq["mass_l1"], cq["energy_l2"]])
+    G["cq_u"] = uq
+
     np.savez_compressed(out, **G)
     print(f"wrote {out}: {len(G)} arrays, {os.path.getsize(out)} bytes")
 

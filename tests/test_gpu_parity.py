@@ -454,3 +454,31 @@ def test_weight_table_json(lx, golden):
         assert a["members"] == b["members"] and a["target_row"] == b["target_row"]
         assert rel_inf(a["w_lin"], b["w_lin"]) < W_TOL
         assert rel_inf(a["w_phi"][0], b["w_phi"][0]) < W_TOL
+
+
+def test_scan_stability_and_footprint(lx, golden):
+    """analysis.scan_stability / spectral_footprint (analysis.py:42-97) vs the reference."""
+    g = lx.make_periodic_grid(256, 0.0, 2 * math.pi)
+    st = lx.select_stencils(g, 7, lx.StencilPolicy.ONE_SIDED_UPWIND)
+    spec = lx.LinearOperatorSpec(((1, -1.0),))
+    sb = lx.scan_stability(g, st, spec, golden["scan_dt"], steps=300)
+    assert sb.stable[0] == tuple(bool(x) for x in golden["scan_stable"])
+    assert sb.dt_star[0] == float(golden["scan_dt_star"])
+    m = lx.merge_boundaries([sb, sb])
+    assert m.n_values == (7, 7) and len(m.stable) == 2
+    h = g.spacing
+    fp = lx.spectral_footprint(golden["fp_row"], np.arange(7) - 6, h, 33, shift=3.5 * h)
+    assert np.abs(fp.amplification - golden["fp_G"]).max() < 1e-13
+    assert np.abs(fp.dispersion - golden["fp_disp"]).max() < 1e-12
+
+
+def test_quadrature_and_norms(lx, golden):
+    assert np.allclose(lx.analysis.clenshaw_curtis_weights(17), golden["cc_w"], rtol=0, atol=1e-15)
+    assert np.allclose(lx.analysis.clenshaw_curtis_weights(18), golden["cc_w_odd"], rtol=0,
+                       atol=1e-15)
+    gc = lx.make_chebyshev_grid(17, -1.0, 1.0)
+    cq = lx.conserved_quantities(golden["cq_u"], gc)
+    assert abs(cq["mass_l1"] - golden["cq"][0]) < 1e-14
+    assert abs(cq["energy_l2"] - golden["cq"][1]) < 1e-14
+    nr = lx.norms(np.array([1.0, 2.0, 3.0]), np.array([1.0, 2.5, 2.0]))
+    assert nr["l_inf"] == 1.0 and abs(nr["l_2"] - math.sqrt(1.25)) < 1e-15
