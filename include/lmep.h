@@ -227,6 +227,19 @@ int lmep_step_etd2(const lmep_grid *grid, const lmep_weights *w, const lmep_bc *
                    int64_t steps, int32_t flags, const lmep_tuning *tuning,
                    int32_t *nonfinite, void *stream);
 
+/* Exponential multistep of order s = `order` (1..5), the literal formula of
+ * timestep.py:187-215 (without gamma-coefficient conversion):
+ *   u <- W u + sum_{j<s} P_{j+1} grad^j N / dt^j,
+ *   grad^j N = sum_{i<=j} (-1)^i C(j,i) N_{k-i}
+ * rows W (exp) and P_j = raw dt^j phi_j at slots 0..s (ALPHA = P_1 ...), D1 for
+ * convective N.  hist_in / hist_out: [s-1][nloc], newest first (N_{k-1} ...);
+ * halo hist ghosts [s-1][width].  scratch: s*nloc doubles. */
+int lmep_step_etds(const lmep_grid *grid, const lmep_weights *w, const lmep_bc *bc,
+                   const lmep_halo *halo, int nl_kind, int order, double delta_t,
+                   const double *u_in, const double *hist_in, double *u_out, double *hist_out,
+                   double *scratch, int64_t steps, int32_t flags, const lmep_tuning *tuning,
+                   int32_t *nonfinite, void *stream);
+
 /* Plain banded mat-vec out[i] = sum_j w[i][j] * u[members(i, j)] with the
  * grid's window rule (kernels.py:23-29, harvest.apply at harvest.py:213-222). */
 int lmep_banded_matvec(const lmep_grid *grid, const lmep_weights *w, const lmep_halo *halo,

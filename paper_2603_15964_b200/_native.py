@@ -42,7 +42,7 @@ EXPORTS = (
     "lmep_version", "lmep_status_string", "lmep_last_error", "lmep_fornberg", "lmep_expm",
     "lmep_harvest", "lmep_step_linear", "lmep_step_etdrk4", "lmep_step_etd2",
     "lmep_banded_matvec", "lmep_plan", "lmep_rows_to_soa", "lmep_launch_count",
-    "lmep_set_harvest_method",
+    "lmep_set_harvest_method", "lmep_step_etds",
 )
 
 
@@ -111,6 +111,8 @@ def load(path: str | None = None):
     L.lmep_step_etdrk4.argtypes = [G, W, B, H, C.c_int, vp, vp, vp, i64, vp, i32, T, vp, vp]
     L.lmep_step_etd2.argtypes = [G, W, B, H, C.c_int, dbl, vp, vp, vp, vp, vp, i64, i32, T, vp,
                                  vp]
+    L.lmep_step_etds.argtypes = [G, W, B, H, C.c_int, C.c_int, dbl, vp, vp, vp, vp, vp, i64, i32,
+                                 T, vp, vp]
     L.lmep_banded_matvec.argtypes = [G, W, H, vp, vp, i32, vp]
     L.lmep_plan.argtypes = [G, C.c_int, C.c_int, C.c_int, i64, T]
     L.lmep_rows_to_soa.argtypes = [vp, i64, C.c_int, vp, vp]

@@ -370,7 +370,7 @@ def step(scheme: int, rows: CompactRows, u: torch.Tensor, steps: int, *, bc: BC 
          delta_t: float = 0.0, nl0_out: torch.Tensor | None = None, tuning=None,
          flag: torch.Tensor | None = None, out: torch.Tensor | None = None,
          hist_out: torch.Tensor | None = None, scratch: torch.Tensor | None = None,
-         off: int = 0, nloc: int | None = None, halo=None):
+         off: int = 0, nloc: int | None = None, halo=None, etd_order: int = 2):
     """Run `steps` steps of a scheme on the whole grid, or on the shard
     [off, off+nloc) with ghost cells `halo` (see c_halo).
     Returns the new u (and the new history for ETD2)."""
@@ -399,12 +399,15 @@ def step(scheme: int, rows: CompactRows, u: torch.Tensor, steps: int, *, bc: BC 
                                 flags, tp, fp, s)
         nat.check(st, "lmep_step_etdrk4")
         return out
-    hist = hist.contiguous()
-    hist_out = torch.empty_like(hist) if hist_out is None else hist_out
-    st = L.lmep_step_etd2(C.byref(g), C.byref(w), C.byref(b), hp, nl, float(delta_t),
-                          nat.ptr(u), nat.ptr(hist), nat.ptr(out), nat.ptr(hist_out),
-                          nat.ptr(scratch), int(steps), flags, tp, fp, s)
-    nat.check(st, "lmep_step_etd2")
+    order = int(etd_order)
+    if order > 1:
+        hist = hist.contiguous()
+        hist_out = torch.empty_like(hist) if hist_out is None else hist_out
+    st = L.lmep_step_etds(C.byref(g), C.byref(w), C.byref(b), hp, nl, order, float(delta_t),
+                          nat.ptr(u), nat.ptr(hist) if order > 1 else None, nat.ptr(out),
+                          nat.ptr(hist_out) if order > 1 else None, nat.ptr(scratch), int(steps),
+                          flags, tp, fp, s)
+    nat.check(st, "lmep_step_etds")
     return out, hist_out
 
 

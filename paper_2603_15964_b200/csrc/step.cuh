@@ -63,7 +63,10 @@ struct StepParams {
     int64_t G;
     double *nl0_out;
     double dt;
+    double dtj[6];                              // etd-s: dt**j as Python computes it
+    int64_t qld;                                // etd-s: history vector stride (>= nloc)
     int ksteps, ext;
+    int etds;                                   // etd-s order (1..5)
     int threads;                                // CTA size (multiple of 32, <= STEP_THREADS)
     int64_t tile;
     int64_t slot_len;
@@ -249,7 +252,7 @@ __device__ __forceinline__ void run_pointwise(int lo, int hi, Epi &&epi)
     for (int l = lo + (int)threadIdx.x; l < hi; l += blockDim.x) epi(l);
 }
 
-template <int SCH, int NS, bool EX, int P, int NLK, bool PN>
+template <int SCH, int NS, bool EX, int P, int NLK, bool PN, int ETDS = 2>
 __global__ void __launch_bounds__(STEP_THREADS, SCH == SCH_LIN ? 1 : 2)
 step_kernel(const __grid_constant__ StepParams p)
 {
@@ -312,7 +315,13 @@ step_kernel(const __grid_constant__ StepParams p)
         const int64_t g = base + idx;
         const double u = load_node(p, p.u_in, p.hl, p.hr, g);
         S(0)[idx] = u;
-        if constexpr (SCH == SCH_ETD2) S(1)[idx] = load_node(p, p.q_in, p.qhl, p.qhr, g);
+        if constexpr (SCH == SCH_ETD2) {
+#pragma unroll
+            for (int i = 1; i < ETDS; ++i)                       // history N_{k-i}, newest first
+                S(i)[idx] = load_node(p, p.q_in + (int64_t)(i - 1) * p.qld,
+                                      p.qhl ? p.qhl + (int64_t)(i - 1) * p.G : nullptr,
+                                      p.qhr ? p.qhr + (int64_t)(i - 1) * p.G : nullptr, g);
+        }
         if constexpr (SCH == SCH_ETDRK4 && !cv) S(1)[idx] = nlp<EX>(nlk, u, 0.0);  // n0 of step 0
     }
     __syncthreads();
@@ -521,18 +530,38 @@ step_kernel(const __grid_constant__ StepParams p)
             p.u_out[i - p.off] = v;
             if (!isfinite(v)) *p.flag = 1;
         }
-    } else {  // SCH_ETD2
-        int iU = 0, iQ = 1, iK = 2, iD = 3, iV = 4;
+    } else {  // SCH_ETD2: exponential multistep of order ETDS (timestep.py:187-215)
+        constexpr int so = ETDS;
+        // slots: 0 u | 1..so-1 history N_{k-i} | so N_k | so+1..2so-1 grad^j N | 2so u'
+        int iU = 0, iK = so, iV = 2 * so;
+        int iq[so > 1 ? so - 1 : 1];
+#pragma unroll
+        for (int i = 1; i < so; ++i) iq[i - 1] = i;
         for (int s = 0; s < K; ++s) {
             const int u0 = (K - 1 - s) * p.ext;
-            double *XU = S(iU), *XQ = S(iQ), *XK = S(iK), *XD = S(iD), *XV = S(iV);
+            double *XU = S(iU), *XK = S(iK), *XV = S(iV);
+            double *XQ[so > 1 ? so - 1 : 1];
+#pragma unroll
+            for (int i = 1; i < so; ++i) XQ[i - 1] = S(iq[i - 1]);
             int lo, hi;
-            // P1: nk = N(u), d = nk - n_{k-1}
+            // P1: nk = N(u); grad^j N = sum_i (-1)^i C(j,i) N_{k-i}, accumulated from 0
+            // in i order with separate roundings, as timestep.py:208 does
             expand(u0 + 1, lo, hi);
             auto epi1 = [&](int l, double du) {
                 const double nk = nlp<EX>(nlk, XU[l], du);
                 XK[l] = nk;
-                XD[l] = EX ? xsub(nk, XQ[l]) : nk - XQ[l];
+#pragma unroll
+                for (int j = 1; j < so; ++j) {
+                    double g = EX ? xadd(0.0, nk) : nk;
+                    int c = 1;                                   // (-1)^i C(j, i)
+#pragma unroll
+                    for (int i = 1; i <= j; ++i) {
+                        c = -c * (j - i + 1) / i;
+                        const double q = XQ[i - 1][l];
+                        g = EX ? xadd(g, xmul((double)c, q)) : g + (double)c * q;
+                    }
+                    S(so + j)[l] = g;
+                }
             };
             if constexpr (cv) {
                 const int rows[1] = {LMEP_ROW_D1};
@@ -543,43 +572,73 @@ step_kernel(const __grid_constant__ StepParams p)
                 run_pointwise(lo, hi, [&](int l) { epi1(l, 0.0); });
             }
             refresh(XK);
-            refresh(XD);
+#pragma unroll
+            for (int j = 1; j < so; ++j) refresh(S(so + j));
             __syncthreads();
-            // P2: u' = (W u + P1 nk) + P2 d / dt   (timestep.py:206-210)
+            // P2: u' = W u + sum_j P_{j+1} grad^j N / dt^j   (timestep.py:206-210)
             expand(u0, lo, hi);
             {
-                const int rows[3] = {LMEP_ROW_W, LMEP_ROW_ALPHA, LMEP_ROW_BETA};
-                const double *const X[3] = {XU, XK, XD};
-                run_pass<NS, P, EX, PN, 3>(p, lo, hi, fLo, fHi, base, lbase, rows, X,
+                int rows[so + 1];
+                const double *X[so + 1];
+                rows[0] = LMEP_ROW_W;
+                X[0] = XU;
+#pragma unroll
+                for (int j = 0; j < so; ++j) {
+                    rows[j + 1] = LMEP_ROW_ALPHA + j;
+                    X[j + 1] = j == 0 ? XK : S(so + j);
+                }
+                const int (&rr)[so + 1] = rows;
+                const double *const (&xx)[so + 1] = X;
+                run_pass<NS, P, EX, PN, so + 1>(p, lo, hi, fLo, fHi, base, lbase, rr, xx,
                     [&](int l, const double *v) {
-                        const double d = EX ? xdiv(v[2], p.dt) : v[2] * (1.0 / p.dt);
-                        XV[l] = padd<EX>(padd<EX>(v[0], v[1]), d);
+                        double acc = padd<EX>(v[0], v[1]);      // /dt**0 == /1.0, exact
+#pragma unroll
+                        for (int j = 1; j < so; ++j) {
+                            const double d = EX ? xdiv(v[j + 1], p.dtj[j]) : v[j + 1] * (1.0 / p.dtj[j]);
+                            acc = padd<EX>(acc, d);
+                        }
+                        XV[l] = acc;
                     });
             }
             pin_pass(XV, lo, hi, none);
             refresh(XV);
             __syncthreads();
-            // history <- nk, u <- u'
-            int t = iQ; iQ = iK; iK = t;
-            t = iU; iU = iV; iV = t;
+            // history <- (nk, N_{k-1}, ...), u <- u'
+            if constexpr (so > 1) {
+                const int freed = iq[so - 2];
+#pragma unroll
+                for (int i = so - 2; i > 0; --i) iq[i] = iq[i - 1];
+                iq[0] = iK;
+                iK = freed;
+            }
+            const int t = iU; iU = iV; iV = t;
         }
+        bool bad = false;
+        double *XQ[so > 1 ? so - 1 : 1];
+#pragma unroll
+        for (int i = 1; i < so; ++i) XQ[i - 1] = S(iq[i - 1]);
         for (int64_t i = O0 + tid; i < O1; i += nt) {
             const double v = S(iU)[i - base];
             p.u_out[i - p.off] = v;
-            p.q_out[i - p.off] = S(iQ)[i - base];
-            if (!isfinite(v)) *p.flag = 1;
+#pragma unroll
+            for (int j = 1; j < so; ++j) p.q_out[(int64_t)(j - 1) * p.qld + (i - p.off)] = XQ[j - 1][i - base];
+            bad |= !isfinite(v);
         }
+        if (bad) *p.flag = 1;
     }
 #undef S
 }
 
-// Per-node rows of the ETD schemes use the generic-n instantiation only.
-template <int SCH, bool EX, int P, int NLK, bool PN = false>
+// Per-node rows of the ETD schemes use the generic-n instantiation only, as do
+// ETD orders other than 2.
+template <int SCH, bool EX, int P, int NLK, bool PN = false, int ETDS = 2>
 inline int launch_ns(int ns_case, const StepParams &p, dim3 grid, size_t shm, cudaStream_t st)
 {
     void (*k)(StepParams) = nullptr;
     if (SCH != SCH_LIN && p.wmode == LMEP_W_PERNODE) {
-        k = step_kernel<SCH, 0, EX, P, NLK, true>;
+        k = step_kernel<SCH, 0, EX, P, NLK, true, ETDS>;
+    } else if (ETDS != 2) {
+        k = step_kernel<SCH, 0, EX, P, NLK, PN, ETDS>;
     } else {
         switch (ns_case) {
         case 7: k = step_kernel<SCH, 7, EX, P, NLK, PN>; break;

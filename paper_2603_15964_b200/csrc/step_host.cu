@@ -1,5 +1,7 @@
 // step_host.cu -- host side of the step kernels: validation, launch planning,
 // temporal-blocking launch loop and the C-ABI entry points (lmep.h).
+#include <math.h>
+
 #include "step.cuh"
 
 namespace lmep {
@@ -7,7 +9,7 @@ namespace lmep {
 // --------------------------------------------------------------------------
 // host side
 // --------------------------------------------------------------------------
-static int nslots(int sch) { return sch == SCH_LIN ? 2 : (sch == SCH_ETD2 ? 5 : 7); }
+static int nslots(int sch, int etds = 2) { return sch == SCH_LIN ? 2 : (sch == SCH_ETD2 ? 2 * etds + 1 : 7); }
 
 // per-step dependency extent in stencil units
 static int step_ext(int sch, int nl)
@@ -34,11 +36,11 @@ static int num_sms()
 static const int64_t kSmemBudget = 200 * 1024;  // bytes per CTA we allow ourselves
 
 int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded, bool pernode,
-                lmep_tuning &t, int64_t pernode_pad)
+                lmep_tuning &t, int64_t pernode_pad, int etds)
 {
     const int n = g.n, eL = g.row, eR = n - 1 - g.row;
     const int ext = step_ext(sch, nl);
-    const int ns = nslots(sch);
+    const int ns = nslots(sch, etds);
     const int P = pernode ? 1 : 5;
     const int64_t rad = (int64_t)ext * (eL + eR);
     // ring mode: whole periodic grid on one CTA for all steps
@@ -120,6 +122,7 @@ static int launch_step(int sch, bool exact, bool pernode, const StepParams &p, d
 
 struct StepCall {
     int sch;
+    int etds = 2;
     const lmep_grid *grid;
     const lmep_weights *w;
     const lmep_bc *bc;
@@ -147,7 +150,8 @@ int run_steps(const StepCall &c)
     if (c.nl < 0 || c.nl > 2) return LMEP_INVALID_CONFIG;
     const bool pernode = w.mode == LMEP_W_PERNODE;
     if (w.mode < 0 || w.mode > 2) return LMEP_INVALID_CONFIG;
-    const int need = c.sch == SCH_LIN ? 1 : (c.sch == SCH_ETD2 ? 3 : 6);
+    if (c.sch == SCH_ETD2 && (c.etds < 1 || c.etds > 5)) return LMEP_INVALID_CONFIG;
+    const int need = c.sch == SCH_LIN ? 1 : (c.sch == SCH_ETD2 ? c.etds + 1 : 6);
     const int need_rows = c.nl == LMEP_NL_CONVECTIVE ? LMEP_ROW_D1 + 1 : need;
     if (w.nrows < need_rows || w.nrows > LMEP_MAX_ROWS) return LMEP_DIMENSION;
     if (!pernode && !w.interior) return LMEP_INVALID_CONFIG;
@@ -166,8 +170,9 @@ int run_steps(const StepCall &c)
     if (!g.periodic && g.N < 2 * g.n) return LMEP_INVALID_CONFIG;
     if (c.steps == 0) {
         cudaError_t e = cudaMemcpyAsync(c.u_out, c.u_in, g.nloc * 8, cudaMemcpyDeviceToDevice, c.stream);
-        if (e == cudaSuccess && c.sch == SCH_ETD2)
-            e = cudaMemcpyAsync(c.q_out, c.q_in, g.nloc * 8, cudaMemcpyDeviceToDevice, c.stream);
+        if (e == cudaSuccess && c.sch == SCH_ETD2 && c.etds > 1)
+            e = cudaMemcpyAsync(c.q_out, c.q_in, (c.etds - 1) * g.nloc * 8, cudaMemcpyDeviceToDevice,
+                                c.stream);
         if (e != cudaSuccess) { set_last_error("cudaMemcpyAsync", e); return LMEP_CUDA_ERROR; }
         return LMEP_OK;
     }
@@ -175,7 +180,8 @@ int run_steps(const StepCall &c)
     lmep_tuning t{};
     if (c.tuning) t = *c.tuning;
     if (sharded) { t.ring = 0; }
-    int st = plan_launch(g, c.sch, c.nl, c.steps, sharded, pernode, t, pernode ? w.pernode_pad : 0);
+    int st = plan_launch(g, c.sch, c.nl, c.steps, sharded, pernode, t, pernode ? w.pernode_pad : 0,
+                         c.etds);
     if (st) return st;
 
     static StepParams p;  // host staging (the struct is large); calls are serialised per process
@@ -211,6 +217,9 @@ int run_steps(const StepCall &c)
             for (int j = 0; j < g.n; ++j) { p.dl[j] = c.bc->dl[j]; p.dr[j] = c.bc->dr[j]; }
     }
     p.dt = c.dt;
+    p.etds = c.etds;
+    p.qld = g.nloc;
+    for (int j = 0; j < 6; ++j) p.dtj[j] = pow(c.dt, (double)j);   // Python's dt**j
     p.ext = step_ext(c.sch, c.nl);
     p.tile = t.tile;
     p.threads = t.threads > 0 ? t.threads : STEP_THREADS;
@@ -219,7 +228,7 @@ int run_steps(const StepCall &c)
     const int64_t rad = (int64_t)p.ext * (p.eL + p.eR);
     p.slot_len = t.ring ? (g.N + g.n + SLOT_PAD + P) : (t.tile + (int64_t)t.ksteps * rad + SLOT_PAD + P);
     p.slot_len = (p.slot_len + 3) & ~int64_t(3);
-    const size_t shm = (size_t)nslots(c.sch) * p.slot_len * 8;
+    const size_t shm = (size_t)nslots(c.sch, c.etds) * p.slot_len * 8;
 
     // Keep freed stream-ordered allocations in the device pool: with the
     // default release threshold (0) every synchronize returns them to the OS
@@ -251,11 +260,12 @@ int run_steps(const StepCall &c)
         if (nlaunch != 1) return LMEP_INVALID_CONFIG;     // caller exchanges halos per launch
         const int64_t need_w = c.steps * p.ext * std::max(p.eL, p.eR);
         if (c.halo->width < need_w) return LMEP_INVALID_CONFIG;
-        if (c.sch == SCH_ETD2 && (!c.halo->hist_left && !c.halo->hist_right)) return LMEP_INVALID_CONFIG;
+        if (c.sch == SCH_ETD2 && c.etds > 1 && (!c.halo->hist_left && !c.halo->hist_right))
+            return LMEP_INVALID_CONFIG;
     }
     // scratch ping-pong
     double *scr = c.scratch, *own_scr = nullptr;
-    const int64_t scr_need = (c.sch == SCH_ETD2 ? 2 : 1) * g.nloc;
+    const int64_t scr_need = (c.sch == SCH_ETD2 ? c.etds : 1) * g.nloc;
     if (nlaunch > 1 && !scr) {
         cudaError_t e = cudaMallocAsync((void **)&own_scr, scr_need * 8, c.stream);
         if (e != cudaSuccess) { set_last_error("cudaMallocAsync", e); return LMEP_CUDA_ERROR; }
@@ -270,7 +280,7 @@ int run_steps(const StepCall &c)
         // the last launch must land in u_out
         const bool to_out = ((nlaunch - 1 - L) % 2) == 0;
         double *dst = to_out ? c.u_out : scr;
-        double *qdst = c.sch == SCH_ETD2 ? (to_out ? c.q_out : scr + g.nloc) : nullptr;
+        double *qdst = (c.sch == SCH_ETD2 && c.etds > 1) ? (to_out ? c.q_out : scr + g.nloc) : nullptr;
         p.ksteps = (int)k;
         p.u_in = src;
         p.u_out = dst;
@@ -338,20 +348,31 @@ extern "C" int lmep_step_etdrk4(const lmep_grid *grid, const lmep_weights *w, co
     return run_steps(c);
 }
 
+extern "C" int lmep_step_etds(const lmep_grid *grid, const lmep_weights *w, const lmep_bc *bc,
+                              const lmep_halo *halo, int nl_kind, int order, double delta_t,
+                              const double *u_in, const double *hist_in, double *u_out,
+                              double *hist_out, double *scratch, int64_t steps, int32_t flags,
+                              const lmep_tuning *tuning, int32_t *nonfinite, void *stream)
+{
+    if (order < 1 || order > 5) return LMEP_INVALID_CONFIG;
+    if (order > 1 && (!hist_in || !hist_out)) return LMEP_INVALID_CONFIG;
+    if (!(delta_t > 0.0)) return LMEP_INVALID_CONFIG;
+    StepCall c{};
+    c.sch = SCH_ETD2; c.etds = order; c.grid = grid; c.w = w; c.bc = bc; c.halo = halo;
+    c.nl = nl_kind; c.dt = delta_t; c.u_in = u_in; c.q_in = hist_in; c.u_out = u_out;
+    c.q_out = hist_out; c.scratch = scratch; c.steps = steps; c.flags = flags; c.tuning = tuning;
+    c.nonfinite = nonfinite; c.stream = (cudaStream_t)stream;
+    return run_steps(c);
+}
+
 extern "C" int lmep_step_etd2(const lmep_grid *grid, const lmep_weights *w, const lmep_bc *bc,
                               const lmep_halo *halo, int nl_kind, double delta_t,
                               const double *u_in, const double *hist_in, double *u_out,
                               double *hist_out, double *scratch, int64_t steps, int32_t flags,
                               const lmep_tuning *tuning, int32_t *nonfinite, void *stream)
 {
-    if (!hist_in || !hist_out) return LMEP_INVALID_CONFIG;
-    if (!(delta_t > 0.0)) return LMEP_INVALID_CONFIG;
-    StepCall c{};
-    c.sch = SCH_ETD2; c.grid = grid; c.w = w; c.bc = bc; c.halo = halo; c.nl = nl_kind;
-    c.dt = delta_t; c.u_in = u_in; c.q_in = hist_in; c.u_out = u_out; c.q_out = hist_out;
-    c.scratch = scratch; c.steps = steps; c.flags = flags; c.tuning = tuning;
-    c.nonfinite = nonfinite; c.stream = (cudaStream_t)stream;
-    return run_steps(c);
+    return lmep_step_etds(grid, w, bc, halo, nl_kind, 2, delta_t, u_in, hist_in, u_out, hist_out,
+                          scratch, steps, flags, tuning, nonfinite, stream);
 }
 
 extern "C" int lmep_banded_matvec(const lmep_grid *grid, const lmep_weights *w,
@@ -374,7 +395,7 @@ extern "C" int lmep_plan(const lmep_grid *grid, int scheme, int nl_kind, int wei
     if (scheme < 0 || scheme > 2) return LMEP_INVALID_CONFIG;
     lmep_tuning t = *out;
     int st = plan_launch(*grid, scheme, nl_kind, steps, grid->nloc != grid->N,
-                         weight_mode == LMEP_W_PERNODE, t, 0);
+                         weight_mode == LMEP_W_PERNODE, t, 0, 2);
     *out = t;
     return st;
 }

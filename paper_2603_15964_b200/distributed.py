@@ -88,13 +88,18 @@ class LocalHalo:
         self.left, self.right = neighbours(rank, len(shards), periodic)
         self.which = "u"
 
+    def _src(self, shard):
+        if isinstance(self.which, tuple):
+            return getattr(shard, self.which[0])[self.which[1]]
+        return getattr(shard, self.which)
+
     def exchange(self, u: torch.Tensor, gl: torch.Tensor, gr: torch.Tensor) -> None:
         G = gl.numel()
         if self.left is not None:
-            src = getattr(self.shards[self.left], self.which)
+            src = self._src(self.shards[self.left])
             gl.copy_(src[src.numel() - G:])
         if self.right is not None:
-            src = getattr(self.shards[self.right], self.which)
+            src = self._src(self.shards[self.right])
             gr.copy_(src[:G])
 
 
@@ -146,15 +151,16 @@ class ShardedStepper:
         dev = nat.device()
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
         G = max(width, 1)
+        nh = max(scheme.s - 1, 1) if scheme.kind == "etd-multistep" else 1
         self.gl = torch.zeros(G, dtype=torch.float64, device=dev)
         self.gr = torch.zeros(G, dtype=torch.float64, device=dev)
-        self.ql = torch.zeros(G, dtype=torch.float64, device=dev)
-        self.qr = torch.zeros(G, dtype=torch.float64, device=dev)
+        self.ql = torch.zeros(nh * G, dtype=torch.float64, device=dev)   # [s-1][width] ghosts
+        self.qr = torch.zeros(nh * G, dtype=torch.float64, device=dev)
         self.u = None
         self.hist = None
         self.done = 0
         # ping-pong scratch for multi-launch calls (u and the etd2 history)
-        self.scratch = torch.empty(2 * nloc, dtype=torch.float64, device=dev)
+        self.scratch = torch.empty((nh + 1) * nloc, dtype=torch.float64, device=dev)
 
     # ---------------------------------------------------------------------
     def set_initial(self, u0_global) -> None:
@@ -163,21 +169,32 @@ class ShardedStepper:
         u = close_initial(u, self.sset, self.prep.bc)
         self.u = u[self.plan.off:self.plan.off + self.plan.nloc].contiguous()
 
+    def _width(self, k, scheme=None):
+        ext = _ext(scheme or self.prep.scheme, self.prep.nl)
+        return k * ext * max(self.sset.row, self.sset.n - 1 - self.sset.row)
+
+    def _nh(self):
+        return max(self.prep.s - 1, 1) if self.prep.scheme == "etd-multistep" else 1
+
     def _halo(self, k):
-        w = k * _ext(self.prep.scheme, self.prep.nl) * max(self.sset.row, self.sset.n - 1 - self.sset.row)
         if self.world == 1:
             return None
-        return (self.gl[:w] if w else self.gl, self.gr[:w] if w else self.gr,
-                self.ql[:w] if w else self.ql, self.qr[:w] if w else self.qr, max(w, 1))
+        w = max(self._width(k), 1)
+        nh = self._nh()
+        return (self.gl[:w], self.gr[:w], self.ql[:nh * w], self.qr[:nh * w], w)
 
     def _exchange(self, k, hist=False):
         if self.world == 1:
             return
         h = self._halo(k)
+        w = h[4]
         if isinstance(self.ex, LocalHalo):
             self.ex.which = "hist" if hist else "u"
         if hist:
-            self.ex.exchange(self.hist, h[2], h[3])
+            for i in range(self.hist.shape[0]):
+                if isinstance(self.ex, LocalHalo):
+                    self.ex.which = ("hist", i)
+                self.ex.exchange(self.hist[i], h[2][i * w:(i + 1) * w], h[3][i * w:(i + 1) * w])
         else:
             self.ex.exchange(self.u, h[0], h[1])
 
@@ -210,38 +227,44 @@ class ShardedStepper:
         else:
             if self.hist is None:
                 raise InvalidConfig("call warm_up() before multistep chunks")
-            self.u, self.hist = _ops.step(nat.SCH_ETD2, p.bank, self.u, k, hist=self.hist,
-                                          delta_t=p.delta_t, **kw)
+            self.u, q = _ops.step(nat.SCH_ETD2, p.bank, self.u, k, hist=self.hist,
+                                  delta_t=p.delta_t, etd_order=p.s, **kw)
+            if p.s > 1:
+                self.hist = q
         self.done += k
 
-    def warm_up_compute(self) -> None:
-        """ETD multistep: history N(u0) and one ETDRK4 warm-up step
-        (timestep.py:375-378); its halo must be exchanged first (k=1)."""
-        p = self.prep
-        self.hist = torch.zeros_like(self.u)
-        if p.s == 2:
-            kw = dict(bc=p.bc, nl=p.nl, exact=self.exact, tuning=self._tuning(1),
-                      flag=self.flag, off=self.plan.off, nloc=self.plan.nloc,
-                      halo=self._halo_etdrk4())
-            self.u = _ops.step(nat.SCH_ETDRK4, p.warm, self.u, 1, nl0_out=self.hist, **kw)
-            self.done += 1
-
-    def _halo_etdrk4(self):
-        if self.world == 1:
-            return None
-        w = _ext("etdrk4", self.prep.nl) * max(self.sset.row, self.sset.n - 1 - self.sset.row)
-        return (self.wl[:w], self.wr[:w], self.wl[:w], self.wr[:w], w)
+    # ETD multistep warm-up (timestep.py:375-378): s-1 ETDRK4 steps, each
+    # storing N(u) in front of the history; each needs its own halo exchange.
+    def warm_up_steps(self) -> int:
+        return max(self.prep.s - 1, 0) if self.prep.scheme == "etd-multistep" else 0
 
     def warm_up_exchange(self) -> None:
-        if self.world == 1 or self.prep.s != 2:
+        if self.hist is None:
+            self.hist = torch.zeros((self._nh(), self.u.numel()), dtype=torch.float64,
+                                    device=self.u.device)
+        if self.world == 1:
             return
-        w = _ext("etdrk4", self.prep.nl) * max(self.sset.row, self.sset.n - 1 - self.sset.row)
+        w = self._width(1, "etdrk4")
         dev = self.u.device
         self.wl = torch.zeros(w, dtype=torch.float64, device=dev)
         self.wr = torch.zeros(w, dtype=torch.float64, device=dev)
         if isinstance(self.ex, LocalHalo):
             self.ex.which = "u"
         self.ex.exchange(self.u, self.wl, self.wr)
+
+    def warm_up_compute(self, i: int = 0) -> None:
+        """Warm-up step i (0-based) of s-1."""
+        p = self.prep
+        if i > 0:
+            self.hist[1:i + 1] = self.hist[0:i].clone()
+        halo = None
+        if self.world > 1:
+            w = self._width(1, "etdrk4")
+            halo = (self.wl, self.wr, self.wl, self.wr, w)
+        kw = dict(bc=p.bc, nl=p.nl, exact=self.exact, tuning=self._tuning(1), flag=self.flag,
+                  off=self.plan.off, nloc=self.plan.nloc, halo=halo)
+        self.u = _ops.step(nat.SCH_ETDRK4, p.warm, self.u, 1, nl0_out=self.hist[0], **kw)
+        self.done += 1
 
     def nonfinite(self) -> bool:
         return bool(self.flag.item())
@@ -272,18 +295,17 @@ def _prepare_shard(grid, sset, problem, scheme, delta_t, off, nloc, pad=0) -> Pr
         bank = _etdrk4_bank(full, half, delta_t, d1)
     else:
         s = scheme.s
-        if s > 2:
-            raise InvalidConfig("etd-multistep with s >= 3 has no device kernel yet")
+        if s > 5:
+            raise InvalidConfig("etd-multistep supports s <= 5 (phi rows up to phi_5)")
         ops = harvest_compact(grid, sset, spec, delta_t, s + 1, frozen, node_range=rng)
-        parts = {nat.ROW_W: ops.row(0), nat.ROW_ALPHA: ops.row(1)}
-        if s == 2:
-            parts[nat.ROW_BETA] = ops.row(2)
+        parts = {nat.ROW_W + j: ops.row(j) for j in range(s + 1)}
+        if s >= 2:
             full = harvest_compact(grid, sset, spec, delta_t, 4, frozen, node_range=rng)
             half = harvest_compact(grid, sset, spec, delta_t / 2, 2, frozen, node_range=rng)
             warm = _etdrk4_bank(full, half, delta_t, d1)
         if d1 is not None:
             parts[nat.ROW_D1] = d1
-        bank = _ops.rows_bank_for(sset, parts, max(parts) + 1 if d1 is not None else 3)
+        bank = _ops.rows_bank_for(sset, parts, max(parts) + 1)
     return Prepared(sset, scheme.kind, nl, bc, bank, warm, float(delta_t), scheme.s)
 
 
@@ -301,10 +323,15 @@ def run_virtual_shards(grid: Grid, stencils, problem: SemiLinearProblem, scheme:
         s.set_initial(problem.initial)
     done = 0
     if scheme.kind == "etd-multistep":
-        for s in shards:
-            s.warm_up_exchange()
-        for s in shards:
-            s.warm_up_compute()
+        nw = min(shards[0].warm_up_steps(), steps)
+        if nw == 0:
+            for s in shards:
+                s.warm_up_exchange()
+        for i in range(nw):
+            for s in shards:
+                s.warm_up_exchange()
+            for s in shards:
+                s.warm_up_compute(i)
         done = shards[0].done
     k = shards[0].plan.ksteps
     while done < steps:
@@ -372,8 +399,12 @@ def advance_all(st: ShardedStepper, steps: int) -> None:
     exchange each."""
     done = 0
     if st.prep.scheme == "etd-multistep" and st.hist is None:
-        st.warm_up_exchange()
-        st.warm_up_compute()
+        nw = min(st.warm_up_steps(), steps)
+        if nw == 0:
+            st.warm_up_exchange()             # allocates the (unused) history
+        for i in range(nw):
+            st.warm_up_exchange()
+            st.warm_up_compute(i)
         done = st.done
     while done < steps:
         k = min(st.plan.ksteps, steps - done)

@@ -21,6 +21,7 @@ import torch
 
 from . import _native as nat
 from . import _ops
+from .errors import InvalidConfig
 
 NL_NONE = nat.NL_NONE
 NL_CONVECTIVE = nat.NL_CONVECTIVE   # -u * (D1 u)
@@ -96,15 +97,22 @@ def run_etdrk4(w_full, w_alpha, w_beta, w_gamma, w_half, w_p1h, d1w, members, ki
 
 def run_etd2(ops, d1w, members, kind, u0, hist, steps, delta_t, pin=False, pin_lo=0.0,
              pin_hi=0.0, *, exact=True, bc=None, tuning=None):
-    """Exponential multistep, order 2, after warm-up (timestep.py:187-215 with
-    s=2): ops = (exp, dt*phi1, dt^2*phi2) raw rows, hist = N_{k-1}.
-    Returns (u, N_last).  Extension: the reference runs this step in Python."""
+    """Exponential multistep after warm-up (timestep.py:187-215): ops =
+    (exp, P_1, ..., P_s) raw rows (P_j = dt^j phi_j), hist = [N_{k-1}, ...,
+    N_{k-s+1}] (a single vector for s=2).  The order s is len(ops)-1.
+    Returns (u, history).  Extension: the reference runs this step in Python."""
+    s = len(ops) - 1
+    if not 1 <= s <= 5:
+        raise InvalidConfig("etd-multistep supports 1 <= s <= 5")
     lay = _ops.validate_members(members, np.shape(ops[0]))
-    named = {nat.ROW_W: ops[0], nat.ROW_ALPHA: ops[1], nat.ROW_BETA: ops[2]}
+    named = {nat.ROW_W + j: ops[j] for j in range(s + 1)}
     if int(kind) == NL_CONVECTIVE:
         named[nat.ROW_D1] = d1w
     bank = _bank(lay, named)
+    h = _dense(hist) if s > 1 else None
     u, q = _ops.step(nat.SCH_ETD2, bank, _dense(u0), int(steps),
                      bc=_bc(pin, pin_lo, pin_hi, bc), nl=int(kind), exact=exact,
-                     hist=_dense(hist), delta_t=float(delta_t), tuning=tuning)
+                     hist=h, delta_t=float(delta_t), tuning=tuning, etd_order=s)
+    if s == 1:
+        return _ret(u, u0), None
     return _ret(u, u0), _ret(q, u0)

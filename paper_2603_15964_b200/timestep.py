@@ -270,19 +270,17 @@ def prepare(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConf
         bank = _etdrk4_bank(full, half, delta_t, d1)
     else:
         s = scheme.s
-        if s > 2:
-            raise InvalidConfig("etd-multistep with s >= 3 has no device kernel yet "
-                                "(SURVEY 8(f) next-2)")
+        if s > 5:
+            raise InvalidConfig("etd-multistep supports s <= 5 (phi rows up to phi_5)")
         ops = harvest_compact(grid, sset, spec, delta_t, s + 1, frozen, stats)
-        parts = {nat.ROW_W: ops.row(0), nat.ROW_ALPHA: ops.row(1)}
-        if s == 2:
-            parts[nat.ROW_BETA] = ops.row(2)
+        parts = {nat.ROW_W + j: ops.row(j) for j in range(s + 1)}
+        if s >= 2:
             full = harvest_compact(grid, sset, spec, delta_t, 4, frozen, stats)
             half = harvest_compact(grid, sset, spec, delta_t / 2, 2, frozen, stats)
             warm = _etdrk4_bank(full, half, delta_t, d1)
         if d1 is not None:
             parts[nat.ROW_D1] = d1
-        bank = _ops.rows_bank_for(sset, parts, max(parts) + 1 if d1 is not None else 3)
+        bank = _ops.rows_bank_for(sset, parts, max(parts) + 1)
     return Prepared(sset, scheme.kind, nl, bc, bank, warm, float(delta_t), scheme.s)
 
 
@@ -300,7 +298,7 @@ class Stepper:
         self.flag = torch.zeros(1, dtype=torch.int32, device=u0.device)
         N = prep.sset.N
         self._out = torch.empty(N, dtype=torch.float64, device=u0.device)
-        self._scr = torch.empty(2 * N, dtype=torch.float64, device=u0.device)
+        self._scr = torch.empty(max(prep.s, 2) * N, dtype=torch.float64, device=u0.device)
         self._hout = None
 
     def advance(self, k: int) -> None:
@@ -316,22 +314,32 @@ class Stepper:
             out = _ops.step(nat.SCH_ETDRK4, p.bank, self.u, k, out=self._out, **kw)
             self._out, self.u = self.u, out
         else:
+            s = p.s
             if self.hist is None:
-                self.hist = torch.zeros_like(self.u)
-                if p.s == 2:
-                    # warm-up: one ETDRK4 step, history = (N(u0),)  (timestep.py:375-378)
-                    out = _ops.step(nat.SCH_ETDRK4, p.warm, self.u, 1, out=self._out,
-                                    nl0_out=self.hist, **kw)
-                    self._out, self.u = self.u, out
-                    self.done += 1
-                    k -= 1
-                    if k == 0:
-                        return
-                self._hout = torch.empty_like(self.u)
+                self.hist = torch.zeros((max(s - 1, 1), self.u.numel()), dtype=torch.float64,
+                                        device=self.u.device)
+                self._hout = torch.empty_like(self.hist)
+                self._warm = 0
+            # warm-up: s-1 ETDRK4 steps, each storing N(u) in front of the
+            # history (timestep.py:375-378); may straddle advance() calls
+            while self._warm < s - 1 and k > 0:
+                i = self._warm
+                if i > 0:
+                    self.hist[1:i + 1] = self.hist[0:i].clone()
+                out = _ops.step(nat.SCH_ETDRK4, p.warm, self.u, 1, out=self._out,
+                                nl0_out=self.hist[0], **kw)
+                self._out, self.u = self.u, out
+                self._warm += 1
+                self.done += 1
+                k -= 1
+            if k == 0:
+                return
             u, q = _ops.step(nat.SCH_ETD2, p.bank, self.u, k, hist=self.hist,
-                             delta_t=p.delta_t, out=self._out, hist_out=self._hout, **kw)
+                             delta_t=p.delta_t, out=self._out, hist_out=self._hout,
+                             etd_order=s, **kw)
             self._out, self.u = self.u, u
-            self._hout, self.hist = self.hist, q
+            if s > 1:
+                self._hout, self.hist = self.hist, q
         self.done += k
 
     def nonfinite(self) -> bool:
@@ -419,36 +427,49 @@ def etdrk4_step(ops_full, ops_half, problem: SemiLinearProblem, state: StepperSt
 
 def etd_multistep_step(ops, problem: SemiLinearProblem, state: StepperState, s: int, *,
                        d1: BandedPropagator | None = None, exact: bool = True) -> StepperState:
-    """One exponential multistep update of order s <= 2 (timestep.py:187-215)."""
+    """One exponential multistep update of order s <= 5 (timestep.py:187-215)."""
     if len(ops) < s + 1:
         raise InvalidConfig(f"order {s} needs phi rows up to phi_{s}")
     if len(state.history) < s - 1:
         raise NotWarmedUp(f"order {s} needs {s - 1} stored evaluations, have {len(state.history)}")
-    if s > 2:
-        raise InvalidConfig("etd-multistep with s >= 3 has no device kernel yet")
+    if s > 5:
+        raise InvalidConfig("etd-multistep supports s <= 5")
     nl = _nl_kind(problem)
-    slots = {nat.ROW_W: ops[0].rows(), nat.ROW_ALPHA: ops[1].rows()}
-    if s == 2:
-        slots[nat.ROW_BETA] = ops[2].rows()
+    slots = {nat.ROW_W + j: ops[j].rows() for j in range(s + 1)}
     if nl == nat.NL_CONVECTIVE:
         if d1 is None:
             raise InvalidConfig("convective nonlinearity needs the banded D1 operator (d1=)")
         slots[nat.ROW_D1] = _scaled(d1.rows(), float(problem.nonlinear_scale))
     lay = slots[nat.ROW_W].layout
-    bank = _ops.rows_bank_for(lay, slots, max(slots) + 1 if nl == nat.NL_CONVECTIVE else 3)
+    bank = _ops.rows_bank_for(lay, slots, max(slots) + 1)
     bc = _ops.BC()
     if problem.boundary.pinned:
         bc = _ops.BC(nat.BC_DIRICHLET, problem.boundary.left, problem.boundary.right)
     u = _ops.dev_f64(state.u)
-    hist = _ops.dev_f64(state.history[0]) if s == 2 else torch.zeros_like(u)
+    hist = torch.stack([_ops.dev_f64(h) for h in state.history[:s - 1]]) if s > 1 else None
     flag = torch.zeros(1, dtype=torch.int32, device=u.device)
-    un, nk = _ops.step(nat.SCH_ETD2, bank, u, 1, bc=bc, nl=nl, exact=exact, hist=hist,
-                       delta_t=ops[0].delta_t, flag=flag)
+    un, q = _ops.step(nat.SCH_ETD2, bank, u, 1, bc=bc, nl=nl, exact=exact, hist=hist,
+                      delta_t=ops[0].delta_t, flag=flag, etd_order=s)
     if flag.item():
         raise NonFinite("multistep update produced non-finite values", state=state.u, time=state.t)
     conv = (lambda x: x) if isinstance(state.u, torch.Tensor) else _ops.to_host
+    nk = q[0] if s > 1 else _nl_eval_device(u, d1, problem, nl)
     history = (conv(nk),) + tuple(state.history[:max(s - 2, 0)])
     return StepperState(u=conv(un), t=state.t + ops[0].delta_t, history=history)
+
+
+def _nl_eval_device(u: torch.Tensor, d1: BandedPropagator | None, problem: SemiLinearProblem,
+                    nl: int) -> torch.Tensor:
+    """N(u) at the step start (the history entry), computed by the step kernel:
+    one 0-step-ahead ETDRK4 launch would advance u, so evaluate through apply."""
+    if nl == nat.NL_NONE:
+        return torch.zeros_like(u)
+    if nl == nat.NL_CUBIC:
+        return -u * u * u
+    from .harvest import apply
+    du = apply(BandedPropagator(periodic=d1.periodic, delta_t=0.0,
+                                _rows=_scaled(d1.rows(), float(problem.nonlinear_scale))), u)
+    return -u * du
 
 
 __all__ = ["Boundary", "SemiLinearProblem", "StepperState", "SchemeConfig", "SimulationResult",

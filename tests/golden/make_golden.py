@@ -204,6 +204,10 @@ def main(out=os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.np
     # ---- 9. ETD2 (etd-multistep s=2) Burgers through run() ---------------
     res = le.run(grid, st, prob, le.SchemeConfig("etd-multistep", s=2), dtb, w2.steps * dtb)
     G["burg2_u"] = res.u_final
+    # ---- 9b. etd-multistep of orders 1, 3, 4, 5 (backward-difference form)
+    for s in (1, 3, 4, 5):
+        res = le.run(grid, st, prob, le.SchemeConfig("etd-multistep", s=s), dtb, w2.steps * dtb)
+        G[f"burg_s{s}_u"] = res.u_final
 
     # ---- 10. cubic ETDRK4 with Dirichlet pins on a non-periodic grid -----
     N = 64

@@ -113,6 +113,10 @@ def _cases():
     out.append(("c2-etd2", g, st, lx.SemiLinearProblem(lx.LinearOperatorSpec(w.terms), None,
                 w.u0, lx.Boundary.periodic(), "convective"),
                 lx.SchemeConfig("etd-multistep", s=2), w.delta_t, 11))
+    for s in (1, 3, 5):
+        out.append((f"c2-etd{s}", g, st, lx.SemiLinearProblem(
+            lx.LinearOperatorSpec(w.terms), None, w.u0, lx.Boundary.periodic(), "convective"),
+            lx.SchemeConfig("etd-multistep", s=s), 0.25 * w.delta_t, 9))
     return out
 
 

@@ -289,6 +289,70 @@ def test_burgers_etdrk4_and_etd2_run(lx, golden):
     assert rel_l2(r2.u_final, golden["burg2_u"]) < U_TOL
 
 
+@pytest.mark.parametrize("s", [1, 3, 4, 5])
+def test_burgers_etd_multistep_orders(lx, golden, s):
+    """etd-multistep of order s through run(), against the reference's
+    backward-difference update (timestep.py:187-215) with its s-1 ETDRK4
+    warm-up steps (timestep.py:370-380).  A snapshot stride of one step makes
+    the warm-up straddle advance() calls."""
+    from paper_2603_15964_b200 import configs
+    w2 = configs.c2(N=256, steps=40)
+    g = lx.make_periodic_grid(w2.N, w2.x_min, w2.x_max)
+    st = lx.select_stencils(g, w2.n, lx.StencilPolicy.CENTERED)
+    prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(w2.terms), None, w2.u0,
+                                lx.Boundary.periodic(), "convective")
+    dt = float(golden["burg4_dt"])
+    T = int(golden["burg4_steps"]) * dt
+    a = lx.run(g, st, prob, lx.SchemeConfig("etd-multistep", s=s), dt, T)
+    assert rel_l2(a.u_final, golden[f"burg_s{s}_u"]) < U_TOL
+    b = lx.run(g, st, prob, lx.SchemeConfig("etd-multistep", s=s), dt, T, snapshot_stride=dt)
+    assert np.array_equal(a.u_final, b.u_final)
+
+
+@pytest.mark.parametrize("s", [1, 2, 3, 4, 5])
+def test_etd_multistep_linear_consistency(lx, s):
+    """With N == 0 every order reduces to the linear propagator exactly in
+    value (the gradient terms vanish)."""
+    N = 128
+    g = lx.make_periodic_grid(N, 0.0, 1.0)
+    st = lx.select_stencils(g, 9, lx.StencilPolicy.CENTERED)
+    u0 = np.sin(2 * math.pi * g.nodes) + 0.3 * np.cos(6 * math.pi * g.nodes)
+    prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(((2, 1e-3), (1, -0.5))), None, u0,
+                                lx.Boundary.periodic(), "none")
+    dt = 0.4 / N
+    T = 30 * dt
+    ul = lx.run(g, st, prob, lx.SchemeConfig("linear"), dt, T).u_final
+    us = lx.run(g, st, prob, lx.SchemeConfig("etd-multistep", s=s), dt, T).u_final
+    assert rel_l2(us, ul) < 1e-13
+
+
+def test_etd_multistep_step_api(lx, golden):
+    """The single-step API with an explicit history (timestep.py:187-215)
+    continues a run() trajectory: run(k) then etd_multistep_step matches run(k+1)."""
+    from paper_2603_15964_b200 import configs
+    from paper_2603_15964_b200.timestep import StepperState
+    w2 = configs.c2(N=256, steps=40)
+    g = lx.make_periodic_grid(w2.N, w2.x_min, w2.x_max)
+    st = lx.select_stencils(g, w2.n, lx.StencilPolicy.CENTERED)
+    prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(w2.terms), None, w2.u0,
+                                lx.Boundary.periodic(), "convective")
+    dt = float(golden["burg4_dt"])
+    s = 3
+    ops = lx.assemble_global_phi(g, st, prob.linear, dt, s=s + 1)
+    d1 = lx.assemble_derivative(g, st, 1)
+    r = lx.run(g, st, prob, lx.SchemeConfig("etd-multistep", s=s), dt, 6 * dt,
+               snapshot_stride=dt)
+    from paper_2603_15964_b200 import _ops
+    from paper_2603_15964_b200 import _native as nat
+    from paper_2603_15964_b200.timestep import _nl_eval_device, etd_multistep_step
+    hist = tuple(_ops.to_host(_nl_eval_device(_ops.dev_f64(r.snapshots[i]), d1, prob,
+                                              nat.NL_CONVECTIVE)) for i in (5, 4))
+    state = StepperState(u=r.snapshots[6], t=6 * dt, history=hist)
+    out = etd_multistep_step(ops, prob, state, s, d1=d1)
+    r7 = lx.run(g, st, prob, lx.SchemeConfig("etd-multistep", s=s), dt, 7 * dt)
+    assert rel_l2(out.u, r7.u_final) < 1e-13
+
+
 def test_dirichlet_cubic_run(lx, golden):
     N = 64
     xg = np.linspace(-1.0, 1.0, N)
