@@ -189,6 +189,27 @@ int lmep_harvest(int n, int s, int nterms, const double *tables, const int32_t *
                  const uint64_t *frozen, uint64_t frozen_default, int64_t B, int layout,
                  double *w_out, int32_t *status, int32_t *ms, void *stream);
 
+/* Row-scaled variable coefficients: with a map, local
+ * row i of item b takes coef[m * coef_stride + t] and c0[m * c0_stride] of
+ * node m = node0 + b - row_b + i (mod nnodes when periodic) -- the operator
+ * sum_t diag(c_t) D^(k_t) + diag(c0) restricted to the stencil, instead of
+ * the coefficients frozen at the target node.  coef / c0 then index the
+ * whole grid (nnodes rows), items are the consecutive nodes node0, node0+1, ...
+ * Table mode only (L == NULL). */
+typedef struct lmep_coef_map {
+    int64_t node0;
+    int64_t nnodes;
+    int32_t periodic;
+    int32_t reserved;
+} lmep_coef_map;
+
+int lmep_harvest_mapped(int n, int s, int nterms, const double *tables, const int32_t *table_idx,
+                        const double *coef, int64_t coef_stride, const double *c0,
+                        int64_t c0_stride, const double *L, double delta_t,
+                        const int32_t *target_row, int row_default, const uint64_t *frozen,
+                        uint64_t frozen_default, int64_t B, int layout, double *w_out,
+                        int32_t *status, int32_t *ms, const lmep_coef_map *map, void *stream);
+
 /* Harvest algorithm for d <= 16: 0 (default) = register-resident
  * expm-multiply (harvest_quad.cu: balancing + scaled Taylor action on the
  * needed columns), 1 = full Pade scaling-and-squaring per warp (harvest.cu).

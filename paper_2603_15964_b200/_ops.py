@@ -118,17 +118,23 @@ class HarvestOut:
 
 def harvest(n: int, s: int, delta_t: float, B: int, *, tables=None, table_idx=None, coef=None,
             coef_stride=0, c0=None, c0_stride=0, L=None, rows=None, row_default=0,
-            frozen=None, frozen_default=0, layout=0) -> HarvestOut:
+            frozen=None, frozen_default=0, layout=0, coef_map=None) -> HarvestOut:
+    """coef_map = (node0, nnodes, periodic): row-scaled coefficients
+    (lmep_harvest_mapped); coef / c0 then index the whole grid."""
     d = nat.device()
     out = torch.empty((B, s, n) if layout == 0 else (s, n, B), dtype=F64, device=d)
     ms = torch.empty(B, dtype=torch.int32, device=d)
     status = torch.empty(B, dtype=torch.int32, device=d)
     nterms = 0 if tables is None else int(tables.shape[1])
-    st = nat.lib().lmep_harvest(
-        n, s, nterms, nat.ptr(tables), nat.ptr(table_idx), nat.ptr(coef), int(coef_stride),
-        nat.ptr(c0), int(c0_stride), nat.ptr(L), float(delta_t), nat.ptr(rows), int(row_default),
-        nat.ptr(frozen), C.c_uint64(int(frozen_default)), B, layout, nat.ptr(out), nat.ptr(status),
-        nat.ptr(ms), nat.stream_handle())
+    args = (n, s, nterms, nat.ptr(tables), nat.ptr(table_idx), nat.ptr(coef), int(coef_stride),
+            nat.ptr(c0), int(c0_stride), nat.ptr(L), float(delta_t), nat.ptr(rows),
+            int(row_default), nat.ptr(frozen), C.c_uint64(int(frozen_default)), B, layout,
+            nat.ptr(out), nat.ptr(status), nat.ptr(ms))
+    if coef_map is None:
+        st = nat.lib().lmep_harvest(*args, nat.stream_handle())
+    else:
+        m = nat.LmepCoefMap(int(coef_map[0]), int(coef_map[1]), int(bool(coef_map[2])), 0)
+        st = nat.lib().lmep_harvest_mapped(*args, C.byref(m), nat.stream_handle())
     nat.check(st, "lmep_harvest")
     return HarvestOut(out, ms, status)
 

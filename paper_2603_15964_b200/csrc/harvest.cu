@@ -580,10 +580,17 @@ __global__ void __launch_bounds__(32 * WPB) harvest_kernel(const HarvestParams P
                 double l;
                 if (P.mode == 1) {
                     // localop.py:120-127: L[i] += c_k * table[k] in term order, then c0*I
+                    const double *cfi = cf;
+                    double czi = cz;
+                    if (P.map_on) {          // row-scaled: row i reads node m_i
+                        const int64_t mi = coef_node(P, b, row, i);
+                        cfi = P.coef + mi * P.coef_stride;
+                        czi = P.c0 ? P.c0[mi * P.c0_stride] : 0.0;
+                    }
                     l = 0.0;
                     for (int t = 0; t < P.nterms; ++t)
-                        l = xadd(l, xmul(cf[t], tab[(t * n + i) * n + jj]));
-                    if (i == jj && cz != 0.0) l = xadd(l, cz);
+                        l = xadd(l, xmul(cfi[t], tab[(t * n + i) * n + jj]));
+                    if (i == jj && czi != 0.0) l = xadd(l, czi);
                 } else {
                     l = P.L[(b * n + i) * n + jj];
                 }
@@ -698,12 +705,13 @@ extern "C" int lmep_expm(const double *A, int d, int64_t B, double *E, int32_t *
     return dispatch_harvest(P, (cudaStream_t)stream);
 }
 
-extern "C" int lmep_harvest(int n, int s, int nterms, const double *tables,
+extern "C" int lmep_harvest_mapped(int n, int s, int nterms, const double *tables,
                             const int32_t *table_idx, const double *coef, int64_t coef_stride,
                             const double *c0, int64_t c0_stride, const double *L, double delta_t,
                             const int32_t *target_row, int row_default, const uint64_t *frozen,
                             uint64_t frozen_default, int64_t B, int layout, double *w_out,
-                            int32_t *status, int32_t *ms, void *stream)
+                            int32_t *status, int32_t *ms, const lmep_coef_map *map,
+                            void *stream)
 {
     if (s < 1 || s > 6) return LMEP_INVALID_CONFIG;                 // harvest.py:85-86
     if (n < 1 || n > LMEP_MAX_N || n + s - 1 > LMEP_MAX_DIM) return LMEP_DIMENSION;
@@ -734,7 +742,26 @@ extern "C" int lmep_harvest(int n, int s, int nterms, const double *tables,
     P.out = w_out;
     P.status = status;
     P.ms = ms;
+    if (map) {
+        if (L || !coef || map->nnodes < 1) return LMEP_INVALID_CONFIG;
+        P.map_on = 1;
+        P.map_periodic = map->periodic ? 1 : 0;
+        P.map_node0 = map->node0;
+        P.map_nnodes = map->nnodes;
+    }
     return dispatch_harvest(P, (cudaStream_t)stream);
+}
+
+extern "C" int lmep_harvest(int n, int s, int nterms, const double *tables,
+                            const int32_t *table_idx, const double *coef, int64_t coef_stride,
+                            const double *c0, int64_t c0_stride, const double *L, double delta_t,
+                            const int32_t *target_row, int row_default, const uint64_t *frozen,
+                            uint64_t frozen_default, int64_t B, int layout, double *w_out,
+                            int32_t *status, int32_t *ms, void *stream)
+{
+    return lmep_harvest_mapped(n, s, nterms, tables, table_idx, coef, coef_stride, c0, c0_stride,
+                               L, delta_t, target_row, row_default, frozen, frozen_default, B,
+                               layout, w_out, status, ms, nullptr, stream);
 }
 
 extern "C" int lmep_set_harvest_method(int method)

@@ -25,7 +25,21 @@ struct HarvestParams {
     double *out;
     int32_t *status;
     int32_t *ms;
+    // row-scaled coefficients (lmep_harvest_mapped): local row i of item b
+    // reads coef/c0 of node  map_node0 + b - row_b + i  (mod map_nnodes)
+    int map_on, map_periodic;
+    int64_t map_node0, map_nnodes;
 };
+
+__device__ __forceinline__ int64_t coef_node(const HarvestParams &P, int64_t b, int row, int i)
+{
+    int64_t m = P.map_node0 + b - row + i;
+    if (P.map_periodic) {
+        m %= P.map_nnodes;
+        if (m < 0) m += P.map_nnodes;
+    }
+    return m;
+}
 
 // expm-multiply harvest for d <= 16 (harvest_quad.cu)
 int launch_harvest_quad(const HarvestParams &P, cudaStream_t st);

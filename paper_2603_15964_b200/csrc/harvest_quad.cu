@@ -101,7 +101,17 @@ __global__ void __launch_bounds__(128) harvest_quad_kernel(const HarvestParams P
             if (j < D) {
                 if (j < n && c < n) {
                     double l;
-                    if (P.mode == 1) {
+                    if (P.mode == 1 && P.map_on) {
+                        // row-scaled: local row c takes node m_c's coefficients
+                        const int64_t mc = coef_node(P, b, row, c);
+                        const double *cfc = P.coef + mc * P.coef_stride;
+                        l = 0.0;
+#pragma unroll
+                        for (int t = 0; t < 4; ++t)
+                            if (t < P.nterms) l = xadd(l, xmul(cfc[t], tab[(t * n + c) * n + j]));
+                        const double czc = P.c0 ? P.c0[mc * P.c0_stride] : 0.0;
+                        if (c == j && czc != 0.0) l = xadd(l, czc);
+                    } else if (P.mode == 1) {
                         // localop.py:120-127: term order, then the reaction on the diagonal
                         l = 0.0;
 #pragma unroll

@@ -279,7 +279,14 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
     else:
         idx = None
     sl = slice(off, off + N)
-    if varcoef:
+    rs = varcoef and spec.row_scaled
+    if rs:
+        # row-scaled: the kernel reads member nodes' coefficients from the
+        # whole-grid arrays (lmep_harvest_mapped); item b is node node0 + b
+        coef_all = _ops.dev_f64(spec.coef).contiguous()
+        react = None if spec.reaction is None else _ops.dev_f64(spec.reaction).contiguous()
+        node0 = off - pad
+    elif varcoef:
         if idx is not None:
             coef_all = _ops.dev_f64(spec.coef).index_select(0, idx).contiguous()
             react = None if spec.reaction is None else \
@@ -302,6 +309,8 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
         kw = dict(row_default=sset.row, frozen_default=0) if uniform_rows else \
             dict(rows=_ops.dev_i32(plan.rows),
                  frozen=torch.as_tensor(plan.masks.view(np.int64), device=d))
+        if rs:
+            kw["coef_map"] = (node0, sset.N, grid.periodic)
         h = _ops.harvest(n, s, delta_t, N, tables=tables, coef=coef, coef_stride=cs, c0=c0t,
                          c0_stride=c0s, layout=1, **kw)
         _ops.raise_on_status(h)
@@ -317,7 +326,12 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
         B = b - a
         tables, cf, c0 = _ops.operator_tables(plan.coords[a:b], terms)
         tidx = _ops.dev_i32(np.arange(B))
-        if varcoef:
+        cmap = None
+        if rs:
+            coef, cs = coef_all, len(spec.orders)
+            c0t, c0s = (None, 0) if react is None else (react, 1)
+            cmap = (node0 + a, sset.N, grid.periodic)
+        elif varcoef:
             coef, cs = coef_all[a:b].contiguous(), len(spec.orders)
             c0t, c0s = (None, 0) if react is None else (react[a:b].contiguous(), 1)
         else:
@@ -325,7 +339,7 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
             c0t, c0s = _ops.dev_f64([c0]), 0
         h = _ops.harvest(n, s, delta_t, B, tables=tables, table_idx=tidx, coef=coef,
                          coef_stride=cs, c0=c0t, c0_stride=c0s, rows=rows_all[a:b].contiguous(),
-                         frozen=masks_all[a:b].contiguous(), layout=1)
+                         frozen=masks_all[a:b].contiguous(), layout=1, coef_map=cmap)
         _ops.raise_on_status(h)
         if stats is not None:
             stats.setdefault("ms", []).append(h.ms)

@@ -45,15 +45,19 @@ class LinearOperatorSpec:
 
 @dataclass(frozen=True)
 class VariableCoefficientSpec:
-    """Per-node coefficients: node i's local operator is
-    sum_t coef[i, t] * D^(orders[t]) (+ reaction[i] * I), frozen at the target
-    node.  Node i's operator equals
-    ``LinearOperatorSpec(tuple(zip(orders, coef[i])))`` bit for bit (M12).
+    """Per-node coefficients.  Default (frozen at the target node, SURVEY
+    Appendix B.3): node i's local operator is sum_t coef[i, t] * D^(orders[t])
+    (+ reaction[i] * I), equal to ``LinearOperatorSpec(tuple(zip(orders,
+    coef[i])))`` bit for bit (M12).  row_scaled=True: the stencil restriction
+    of sum_t diag(coef[:, t]) D^(orders[t]) + diag(reaction), i.e. local row j
+    of node i's operator uses the coefficients of the stencil member m_j
+     -- a different discretisation.
     Extension of the reference API for BASELINE config 5."""
 
     orders: tuple[int, ...]
     coef: np.ndarray            # (N, len(orders))
     reaction: np.ndarray | None = None
+    row_scaled: bool = False
 
     def __post_init__(self):
         orders = tuple(int(k) for k in self.orders)

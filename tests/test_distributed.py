@@ -96,6 +96,9 @@ def _cases():
     out.append(("c5-pernode", g, st, lx.SemiLinearProblem(
         lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1)), None, w.u0,
         lx.Boundary.periodic(), "none"), lx.SchemeConfig("linear"), w.delta_t, 15))
+    out.append(("c5-rowscaled", g, st, lx.SemiLinearProblem(
+        lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1), row_scaled=True), None, w.u0,
+        lx.Boundary.periodic(), "none"), lx.SchemeConfig("linear"), w.delta_t, 15))
     w = configs.c4(N=4000)
     g = lx.make_uniform_grid(w.N, -1.0, 1.0)
     st = lx.select_stencils(g, w.n, lx.StencilPolicy.CENTERED)

@@ -198,6 +198,42 @@ def test_c5_per_node_harvest(lx, golden, method):
         assert (np.abs(W[:, r] - ref[:, r]).max(axis=1) / den).max() < W_TOL, r
 
 
+@pytest.mark.parametrize("periodic", [True, False])
+def test_row_scaled_varcoef_harvest(lx, orc, method, periodic):
+    """Row-scaled variable coefficients: local row j of
+    node i's operator is (0 + c1[m_j] D1[j]) + c2[m_j] D2[j] (localop.py:120-127
+    accumulation order with member coefficients), harvested per node and
+    checked against the oracle's harvest of that explicit L."""
+    from paper_2603_15964_b200 import configs
+    from paper_2603_15964_b200.harvest import harvest_compact
+    N, n = 48, 13
+    w5 = configs.c5(N=N, steps=1)
+    c, nu = w5.coef
+    if periodic:
+        g = lx.make_periodic_grid(N, 0.0, 1.0)
+    else:
+        g = lx.make_uniform_grid(N, 0.0, 1.0)
+    st = lx.select_stencils(g, n, lx.StencilPolicy.CENTERED)
+    spec = lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1), row_scaled=True)
+    dt = w5.delta_t * 8
+    rows = harvest_compact(g, st, spec, dt, 3)
+    W = rows.pernode.permute(2, 0, 1).cpu().numpy()           # (N, s, n)
+    m = orc.members_for(N, n, (n - 1) // 2, periodic)
+    trows = orc.target_rows_for(N, n, (n - 1) // 2, periodic)
+    h = 1.0 / N if periodic else 1.0 / (N - 1)
+    for i in range(N):
+        x = (np.arange(n) - trows[i]) * h if periodic else g.nodes[m[i]] - g.nodes[i]
+        D1 = np.stack([orc.fornberg_weights(x[j], x, 2)[1] for j in range(n)])
+        D2 = np.stack([orc.fornberg_weights(x[j], x, 2)[2] for j in range(n)])
+        L = (0.0 + (-c[m[i]])[:, None] * D1) + nu[m[i]][:, None] * D2
+        wl, wp = orc.harvest_phi_weights(L, dt, 3, int(trows[i]), reduced=True)
+        ref = np.vstack([wl] + list(wp))
+        assert _rows_rel(W[i], ref) < W_TOL, (i, _rows_rel(W[i], ref))
+    # differs from the frozen-at-target discretisation
+    frz = harvest_compact(g, st, lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1)), dt, 3)
+    assert not torch.equal(frz.pernode, rows.pernode)
+
+
 # ------------------------------------------------------------------ stepping
 def test_c1_run_linear_bitwise(lx, golden, orc):
     from paper_2603_15964_b200 import configs
