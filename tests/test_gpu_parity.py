@@ -582,3 +582,26 @@ def test_quadrature_and_norms(lx, golden):
     assert abs(cq["energy_l2"] - golden["cq"][1]) < 1e-14
     nr = lx.norms(np.array([1.0, 2.0, 3.0]), np.array([1.0, 2.5, 2.0]))
     assert nr["l_inf"] == 1.0 and abs(nr["l_2"] - math.sqrt(1.25)) < 1e-15
+
+
+def test_weight_table_binary_device_roundtrip(lx, tmp_path):
+    """A harvested per-node table saved and reloaded into HBM steps bit-identically."""
+    import torch
+    from paper_2603_15964_b200 import _native as nat
+    from paper_2603_15964_b200 import _ops, configs
+    from paper_2603_15964_b200.harvest import harvest_compact
+    w5 = configs.c5(N=4096, steps=10)
+    c, nu = w5.coef
+    g = lx.make_periodic_grid(w5.N, 0.0, 1.0)
+    from paper_2603_15964_b200.grid import as_stencil_set
+    st = as_stencil_set(g, lx.select_stencils(g, w5.n, lx.StencilPolicy.CENTERED))
+    rows = harvest_compact(g, st, lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1)),
+                           w5.delta_t, 1)
+    p = tmp_path / "c5.lmwt"
+    lx.save_weight_table(p, rows, w5.delta_t)
+    back, dt = lx.load_weight_table(p)
+    assert dt == w5.delta_t and back.pernode.is_cuda
+    u0 = _ops.dev_f64(w5.u0)
+    a = _ops.step(nat.SCH_LIN, rows, u0, 10)
+    b = _ops.step(nat.SCH_LIN, back, u0, 10)
+    assert torch.equal(a, b)

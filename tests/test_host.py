@@ -104,3 +104,54 @@ def test_configs_are_seeded_and_shaped():
     c, nu = c5.coef
     assert abs(c.min() + 2) < 1e-12 and abs(c.max() - 2) < 1e-12
     assert nu.min() >= 1e-4 * (1 - 1e-12) and nu.max() <= 1e-1 * (1 + 1e-12)
+
+
+# ---------------------------------------------------------------- table I/O
+@pytest.mark.parametrize("mode", ["shared", "class", "pernode"])
+def test_weight_table_binary_roundtrip(tmp_path, mode):
+    import torch
+    from paper_2603_15964_b200 import _native as nat
+    from paper_2603_15964_b200 import _ops
+    from paper_2603_15964_b200.grid import StencilSet
+    from paper_2603_15964_b200.tableio import load_weight_table, save_weight_table
+    rng = np.random.default_rng(3)
+    R, n = 3, 7
+    if mode == "shared":
+        rows = _ops.CompactRows(StencilSet(64, n, 3, True), nat.W_SHARED,
+                                torch.from_numpy(rng.standard_normal((R, n))))
+    elif mode == "class":
+        rows = _ops.CompactRows(StencilSet(64, n, 3, False), nat.W_CLASS,
+                                torch.from_numpy(rng.standard_normal((R, n))),
+                                torch.from_numpy(rng.standard_normal((7, R, n))), 3, 3)
+    else:
+        rows = _ops.CompactRows(StencilSet(64, n, 3, True), nat.W_PERNODE,
+                                pernode=torch.from_numpy(rng.standard_normal((R, n, 64 + 8))),
+                                pernode_pad=4)
+    p = tmp_path / "t.lmwt"
+    nbytes = save_weight_table(p, rows, 1.25e-3)
+    assert nbytes == p.stat().st_size
+    back, dt = load_weight_table(p, device="cpu")
+    assert dt == 1.25e-3 and back.mode == rows.mode and back.pernode_pad == rows.pernode_pad
+    assert (back.layout.N, back.layout.n, back.layout.row, back.layout.periodic) == \
+        (rows.layout.N, rows.layout.n, rows.layout.row, rows.layout.periodic)
+    for a in ("interior", "classes", "pernode"):
+        x, y = getattr(rows, a), getattr(back, a)
+        assert (x is None and y is None) or torch.equal(x, y)
+
+
+def test_weight_table_json_parse(golden):
+    """The reference's JSON table (harvest.py:238-265) parses back exactly."""
+    import json
+    from paper_2603_15964_b200.tableio import parse_weight_table_json
+    text = str(golden["wtj"])
+    rows, dt = parse_weight_table_json(text, device="cpu")
+    ref = json.loads(text)
+    assert dt == ref["delta_t"] and rows.layout.periodic and rows.layout.N == ref["N"]
+    W = rows.pernode.numpy()
+    for i, r in enumerate(ref["nodes"]):
+        assert np.array_equal(W[0, :, i], r["w_lin"])
+        assert np.array_equal(W[1, :, i], r["w_phi"][0])
+    with pytest.raises(Exception):
+        bad = json.loads(text)
+        bad["nodes"][0]["members"] = [5, 3, 1]
+        parse_weight_table_json(json.dumps(bad), device="cpu")
