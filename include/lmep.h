@@ -211,9 +211,11 @@ int lmep_harvest_mapped(int n, int s, int nterms, const double *tables, const in
                         int32_t *status, int32_t *ms, const lmep_coef_map *map, void *stream);
 
 /* Harvest algorithm for d <= 16: 0 (default) = register-resident
- * expm-multiply (harvest_quad.cu: balancing + scaled Taylor action on the
- * needed columns), 1 = full Pade scaling-and-squaring per warp (harvest.cu).
- * lmep_expm always uses the Pade kernel.  Process-wide setting. */
+ * expm-multiply, warp-uniform (harvest_mv.cuh: balancing + scaled Taylor
+ * action on the needed columns), 1 = full Pade scaling-and-squaring per warp
+ * (harvest.cu), 2 / 3 = the first-generation expm-multiply kernel with 4 / 8
+ * lanes per item (harvest_quad.cu).  lmep_expm always uses the Pade kernel.
+ * Process-wide setting. */
 int lmep_set_harvest_method(int method);
 
 /* ---- stepping (K3, K4, K5) ---------------------------------------------- */

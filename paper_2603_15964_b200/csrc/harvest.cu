@@ -665,9 +665,9 @@ static int g_harvest_method = 0;   // 0: auto (expm-multiply for d <= 16), 1: Pa
 static int dispatch_harvest(const HarvestParams &P, cudaStream_t st)
 {
     if (P.B == 0) return LMEP_OK;
-    if (P.mode != 0 && g_harvest_method == 0 && P.d >= 2 && P.d <= 16 &&
+    if (P.mode != 0 && g_harvest_method != 1 && P.d >= 2 && P.d <= 16 &&
         (P.mode == 2 || P.nterms <= 4))
-        return launch_harvest_quad(P, st);
+        return g_harvest_method == 0 ? launch_harvest_mv(P, st) : launch_harvest_quad(P, st);
     if (P.d <= 8) return launch_harvest<8, 8>(P, st);
     if (P.d <= 16) return launch_harvest<16, 4>(P, st);
     if (P.d <= 32) return launch_harvest<32, 2>(P, st);
@@ -766,8 +766,8 @@ extern "C" int lmep_harvest(int n, int s, int nterms, const double *tables,
 
 extern "C" int lmep_set_harvest_method(int method)
 {
-    if (method < 0 || method > 2) return LMEP_INVALID_CONFIG;
-    lmep::g_harvest_method = method == 1 ? 1 : 0;
+    if (method < 0 || method > 3) return LMEP_INVALID_CONFIG;
+    lmep::g_harvest_method = method;            // 0 mv, 1 pade, 2/3 quad (4 / 8 lanes)
     lmep::set_lanes_per_item(method == 2 ? 4 : 8);
     return LMEP_OK;
 }

@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--method", default="multiply")
     ap.add_argument("--N", type=int, default=None)
+    ap.add_argument("--s", type=int, default=1, help="harvest: phi rows (1 = w_lin only)")
     a = ap.parse_args()
     torch.cuda.set_device(0)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -55,16 +56,22 @@ def main():
         c, nu = w.coef                      # resident coefficients: time the device path only
         spec = lx.VariableCoefficientSpec((1, 2), _ops.dev_f64(np.stack([-c, nu], 1)))
         prob = lx.SemiLinearProblem(spec, None, w.u0, lx.Boundary.periodic(), "none")
+        from paper_2603_15964_b200.grid import as_stencil_set
+        from paper_2603_15964_b200.harvest import harvest_compact
+        sset = as_stencil_set(g, st)
+
+        def once():
+            return harvest_compact(g, sset, spec, w.delta_t, a.s)
         for _ in range(2):
-            prepare(g, st, prob, scheme, w.delta_t)
+            once()
         torch.cuda.synchronize()
         ev0.record()
         for _ in range(a.reps):
-            prepare(g, st, prob, scheme, w.delta_t)
+            once()
         ev1.record()
         torch.cuda.synchronize()
         ms = ev0.elapsed_time(ev1) / a.reps
-        print(json.dumps({"case": "harvest", "method": a.method, "N": w.N, "ms": ms,
+        print(json.dumps({"case": "harvest", "method": a.method, "N": w.N, "s": a.s, "ms": ms,
                           "harvests_per_s": w.N / ms * 1e3}))
         return
     name = {"c3": "c3", "c4": "c4", "c5step": "c5", "c1": "c1", "c2": "c2"}[a.case]
