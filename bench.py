@@ -53,7 +53,7 @@ def expm_flops(d: int, ms: np.ndarray) -> float:
 
 
 def multiply_flops(d: int, ms: np.ndarray) -> float:
-    """Algorithmic FLOPs of the expm-multiply harvest (harvest_quad.cu): every
+    """Algorithmic FLOPs of the expm-multiply harvest (harvest_mv.cuh): every
     Taylor term is one d x d matrix-vector product (2 d^2 flops); the kernel
     reports the number of products per matrix in the low 24 bits of ms."""
     return float((ms & 0xFFFFFF).astype(np.float64).sum() * 2.0 * d * d)
@@ -457,10 +457,10 @@ def main():
                           "per_step_launch_ms": per_launch_ms},
             # the dominant kernel of the pass (ncu launch list: ~80% of device time) is
             # the FP64-bound harvest; the HBM-bound step kernel follows as roofline_step
-            "roofline": {"bound": "fp64", "kernel": "harvest_quad_kernel<13> (per-node expm-multiply, 13x13)",
+            "roofline": {"bound": "fp64", "kernel": "harvest_mv_kernel<13> (per-node expm-multiply, 13x13)",
                          "achieved": harvest_tflops, "peak": fp64, "unit": "TFLOP/s",
                          "frac": harvest_tflops / fp64,
-                         "traffic": traffic("harvest_quad_kernel<13>", "bytes_per_item", bench.nloc),
+                         "traffic": traffic("harvest_mv_kernel<13>", "bytes_per_item", bench.nloc),
                          "algorithmic_flops_per_launch": flops,
                          "peak_kind": "measured DFMA chains (tools/fp64_peak.cu), this run"},
             "roofline_step": {"bound": "hbm", "kernel": step_kernel,

@@ -210,6 +210,21 @@ int lmep_harvest_mapped(int n, int s, int nterms, const double *tables, const in
                         uint64_t frozen_default, int64_t B, int layout, double *w_out,
                         int32_t *status, int32_t *ms, const lmep_coef_map *map, void *stream);
 
+/* One slice of a larger per-node harvest (host-pipelined uploads): as
+ * lmep_harvest_mapped, but the layout-1 output [s][n][out_ld] has leading
+ * dimension out_ld >= B.  To harvest items [a, a+B) of a table of out_ld
+ * items, offset coef / c0 by a rows, target_row / frozen / status / ms by a,
+ * w_out by a, and map->node0 by a.  Layout 0 ignores out_ld.
+ * Replaces the per-node loop of harvest._harvest_rows (harvest.py:135-159)
+ * for one contiguous node range. */
+int lmep_harvest_chunk(int n, int s, int nterms, const double *tables, const int32_t *table_idx,
+                       const double *coef, int64_t coef_stride, const double *c0,
+                       int64_t c0_stride, const double *L, double delta_t,
+                       const int32_t *target_row, int row_default, const uint64_t *frozen,
+                       uint64_t frozen_default, int64_t B, int layout, double *w_out,
+                       int32_t *status, int32_t *ms, const lmep_coef_map *map, int64_t out_ld,
+                       void *stream);
+
 /* Harvest algorithm for d <= 16: 0 (default) = register-resident
  * expm-multiply, warp-uniform (harvest_mv.cuh: balancing + scaled Taylor
  * action on the needed columns), 1 = full Pade scaling-and-squaring per warp

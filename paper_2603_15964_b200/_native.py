@@ -42,7 +42,7 @@ EXPORTS = (
     "lmep_version", "lmep_status_string", "lmep_last_error", "lmep_fornberg", "lmep_expm",
     "lmep_harvest", "lmep_step_linear", "lmep_step_etdrk4", "lmep_step_etd2",
     "lmep_banded_matvec", "lmep_plan", "lmep_rows_to_soa", "lmep_launch_count",
-    "lmep_set_harvest_method", "lmep_step_etds", "lmep_harvest_mapped",
+    "lmep_set_harvest_method", "lmep_step_etds", "lmep_harvest_mapped", "lmep_harvest_chunk",
 )
 
 
@@ -111,6 +111,8 @@ def load(path: str | None = None):
     L.lmep_harvest.argtypes = [C.c_int, C.c_int, C.c_int, vp, vp, vp, i64, vp, i64, vp, dbl, vp,
                                C.c_int, vp, C.c_uint64, i64, C.c_int, vp, vp, vp, vp]
     L.lmep_harvest_mapped.argtypes = L.lmep_harvest.argtypes[:-1] + [C.POINTER(LmepCoefMap), vp]
+    L.lmep_harvest_chunk.argtypes = L.lmep_harvest.argtypes[:-1] + [C.POINTER(LmepCoefMap), i64,
+                                                                     vp]
     G, W, B, H, T = (C.POINTER(LmepGrid), C.POINTER(LmepWeights), C.POINTER(LmepBC),
                      C.POINTER(LmepHalo), C.POINTER(LmepTuning))
     L.lmep_step_linear.argtypes = [G, W, B, H, vp, vp, vp, i64, i32, T, vp, vp]

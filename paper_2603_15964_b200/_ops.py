@@ -42,6 +42,34 @@ def dev_i32(a) -> torch.Tensor:
     return torch.as_tensor(np.ascontiguousarray(np.asarray(a, dtype=np.int32)), device=nat.device())
 
 
+_COPY_STREAMS: dict = {}
+
+
+def copy_stream(which: int = 0) -> torch.cuda.Stream:
+    """Side streams host<->device transfers overlap on (per device): 0 carries
+    harvest inputs and snapshots, 1 the initial state."""
+    d = nat.device()
+    key = (d.index if d.index is not None else torch.cuda.current_device(), which)
+    if key not in _COPY_STREAMS:
+        _COPY_STREAMS[key] = torch.cuda.Stream(device=d)
+    return _COPY_STREAMS[key]
+
+
+def is_host(a) -> bool:
+    """True for data that lives in host memory (numpy / CPU tensors)."""
+    return not (isinstance(a, torch.Tensor) and a.device.type == "cuda")
+
+
+def host_f64(a) -> torch.Tensor:
+    """Contiguous float64 CPU tensor view of host data (no copy when possible;
+    pinned tensors stay pinned)."""
+    if isinstance(a, torch.Tensor):
+        return a.to(dtype=F64).contiguous()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64)))
+
+
 def to_host(t: torch.Tensor) -> np.ndarray:
     return t.detach().cpu().numpy()
 
@@ -118,25 +146,41 @@ class HarvestOut:
 
 def harvest(n: int, s: int, delta_t: float, B: int, *, tables=None, table_idx=None, coef=None,
             coef_stride=0, c0=None, c0_stride=0, L=None, rows=None, row_default=0,
-            frozen=None, frozen_default=0, layout=0, coef_map=None) -> HarvestOut:
+            frozen=None, frozen_default=0, layout=0, coef_map=None,
+            into: HarvestOut | None = None, item0: int = 0) -> HarvestOut:
     """coef_map = (node0, nnodes, periodic): row-scaled coefficients
-    (lmep_harvest_mapped); coef / c0 then index the whole grid."""
+    (lmep_harvest_mapped); coef / c0 then index the whole grid.
+    into / item0 (layout 1): write items [item0, item0 + B) of a larger
+    HarvestOut (lmep_harvest_chunk); coef / c0 / rows / frozen are then the
+    slice's own (already offset) arrays."""
     d = nat.device()
-    out = torch.empty((B, s, n) if layout == 0 else (s, n, B), dtype=F64, device=d)
-    ms = torch.empty(B, dtype=torch.int32, device=d)
-    status = torch.empty(B, dtype=torch.int32, device=d)
+    if into is None:
+        out = torch.empty((B, s, n) if layout == 0 else (s, n, B), dtype=F64, device=d)
+        ms = torch.empty(B, dtype=torch.int32, device=d)
+        status = torch.empty(B, dtype=torch.int32, device=d)
+        res, ld, optr = HarvestOut(out, ms, status), B, nat.ptr(out)
+    else:
+        if layout != 1:
+            raise InvalidConfig("chunked harvests write the SoA layout")
+        res, ld = into, int(into.rows.shape[2])
+        optr = into.rows.data_ptr() + 8 * int(item0)
+        ms, status = into.ms[item0:item0 + B], into.status[item0:item0 + B]
     nterms = 0 if tables is None else int(tables.shape[1])
     args = (n, s, nterms, nat.ptr(tables), nat.ptr(table_idx), nat.ptr(coef), int(coef_stride),
             nat.ptr(c0), int(c0_stride), nat.ptr(L), float(delta_t), nat.ptr(rows),
             int(row_default), nat.ptr(frozen), C.c_uint64(int(frozen_default)), B, layout,
-            nat.ptr(out), nat.ptr(status), nat.ptr(ms))
-    if coef_map is None:
+            optr, nat.ptr(status), nat.ptr(ms))
+    if into is not None:
+        m = None if coef_map is None else \
+            C.byref(nat.LmepCoefMap(int(coef_map[0]), int(coef_map[1]), int(bool(coef_map[2])), 0))
+        st = nat.lib().lmep_harvest_chunk(*args, m, ld, nat.stream_handle())
+    elif coef_map is None:
         st = nat.lib().lmep_harvest(*args, nat.stream_handle())
     else:
         m = nat.LmepCoefMap(int(coef_map[0]), int(coef_map[1]), int(bool(coef_map[2])), 0)
         st = nat.lib().lmep_harvest_mapped(*args, C.byref(m), nat.stream_handle())
     nat.check(st, "lmep_harvest")
-    return HarvestOut(out, ms, status)
+    return res
 
 
 def raise_on_status(h: HarvestOut, what="matrix exponential overflowed") -> None:

@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(32 * WPB) harvest_kernel(const HarvestParams P
         if (q == 0) w = E[i * T::LD + row];
         else w = ((fz >> i) & 1ull) ? 0.0 : E[i * T::LD + n + q - 1];
         if (P.layout == 0) P.out[(b * sd + q) * n + i] = w;
-        else P.out[((int64_t)q * n + i) * P.B + b] = w;
+        else P.out[((int64_t)q * n + i) * P.out_ld + b] = w;
     }
 }
 
@@ -699,20 +699,23 @@ extern "C" int lmep_expm(const double *A, int d, int64_t B, double *E, int32_t *
     P.d = d;
     P.Ain = A;
     P.B = B;
+    P.out_ld = B;
     P.out = E;
     P.status = status;
     P.ms = ms;
     return dispatch_harvest(P, (cudaStream_t)stream);
 }
 
-extern "C" int lmep_harvest_mapped(int n, int s, int nterms, const double *tables,
-                            const int32_t *table_idx, const double *coef, int64_t coef_stride,
-                            const double *c0, int64_t c0_stride, const double *L, double delta_t,
-                            const int32_t *target_row, int row_default, const uint64_t *frozen,
-                            uint64_t frozen_default, int64_t B, int layout, double *w_out,
-                            int32_t *status, int32_t *ms, const lmep_coef_map *map,
-                            void *stream)
+extern "C" int lmep_harvest_chunk(int n, int s, int nterms, const double *tables,
+                                  const int32_t *table_idx, const double *coef,
+                                  int64_t coef_stride, const double *c0, int64_t c0_stride,
+                                  const double *L, double delta_t, const int32_t *target_row,
+                                  int row_default, const uint64_t *frozen,
+                                  uint64_t frozen_default, int64_t B, int layout, double *w_out,
+                                  int32_t *status, int32_t *ms, const lmep_coef_map *map,
+                                  int64_t out_ld, void *stream)
 {
+    if (layout == 1 && out_ld < B) return LMEP_DIMENSION;
     if (s < 1 || s > 6) return LMEP_INVALID_CONFIG;                 // harvest.py:85-86
     if (n < 1 || n > LMEP_MAX_N || n + s - 1 > LMEP_MAX_DIM) return LMEP_DIMENSION;
     if (!target_row && (row_default < 0 || row_default >= n)) return LMEP_DIMENSION;
@@ -738,6 +741,7 @@ extern "C" int lmep_harvest_mapped(int n, int s, int nterms, const double *table
     P.frozen = frozen;
     P.frozen_default = frozen_default;
     P.B = B;
+    P.out_ld = layout == 1 ? out_ld : B;
     P.layout = layout;
     P.out = w_out;
     P.status = status;
@@ -750,6 +754,20 @@ extern "C" int lmep_harvest_mapped(int n, int s, int nterms, const double *table
         P.map_nnodes = map->nnodes;
     }
     return dispatch_harvest(P, (cudaStream_t)stream);
+}
+
+extern "C" int lmep_harvest_mapped(int n, int s, int nterms, const double *tables,
+                                   const int32_t *table_idx, const double *coef,
+                                   int64_t coef_stride, const double *c0, int64_t c0_stride,
+                                   const double *L, double delta_t, const int32_t *target_row,
+                                   int row_default, const uint64_t *frozen,
+                                   uint64_t frozen_default, int64_t B, int layout, double *w_out,
+                                   int32_t *status, int32_t *ms, const lmep_coef_map *map,
+                                   void *stream)
+{
+    return lmep_harvest_chunk(n, s, nterms, tables, table_idx, coef, coef_stride, c0, c0_stride,
+                              L, delta_t, target_row, row_default, frozen, frozen_default, B,
+                              layout, w_out, status, ms, map, B, stream);
 }
 
 extern "C" int lmep_harvest(int n, int s, int nterms, const double *tables,

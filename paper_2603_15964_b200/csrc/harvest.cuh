@@ -21,6 +21,7 @@ struct HarvestParams {
     const uint64_t *frozen;
     uint64_t frozen_default;
     int64_t B;
+    int64_t out_ld;        // layout 1: leading dimension of out [s][n][out_ld] (>= B)
     int layout;
     double *out;
     int32_t *status;

@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(128) harvest_mv_kernel(const HarvestParams P)
                         if (qo > 0 && ((fz >> j) & 1ull)) o = 0.0;
                         if (live && j < n) {
                             if (P.layout == 0) P.out[(b * sd + qo) * n + j] = o;
-                            else P.out[((int64_t)qo * n + j) * P.B + b] = o;
+                            else P.out[((int64_t)qo * n + j) * P.out_ld + b] = o;
                         }
                     }
                     ++qo;
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(128) harvest_mv_kernel(const HarvestParams P)
                 const int j = q + LPI * m;
                 if (j < n) {
                     if (P.layout == 0) P.out[(b * sd + qq) * n + j] = __longlong_as_double(0x7ff8000000000000LL);
-                    else P.out[((int64_t)qq * n + j) * P.B + b] = __longlong_as_double(0x7ff8000000000000LL);
+                    else P.out[((int64_t)qq * n + j) * P.out_ld + b] = __longlong_as_double(0x7ff8000000000000LL);
                 }
             }
     }

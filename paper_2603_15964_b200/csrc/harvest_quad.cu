@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(128) harvest_quad_kernel(const HarvestParams P
             if (qo > 0 && ((fz >> j) & 1ull)) w = 0.0;
             if (live && j < n) {
                 if (P.layout == 0) P.out[(b * sd + qo) * n + j] = w;
-                else P.out[((int64_t)qo * n + j) * P.B + b] = w;
+                else P.out[((int64_t)qo * n + j) * P.out_ld + b] = w;
             }
         }
         if (!__all_sync(qm, okv)) status = LMEP_NONFINITE;

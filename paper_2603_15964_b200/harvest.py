@@ -286,6 +286,16 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
         coef_all = _ops.dev_f64(spec.coef).contiguous()
         react = None if spec.reaction is None else _ops.dev_f64(spec.reaction).contiguous()
         node0 = off - pad
+    elif varcoef and idx is None and shared_coords and uniform_rows and \
+            _ops.is_host(spec.coef) and N >= PIPELINE_MIN:
+        # host coefficients: upload in chunks on the copy stream, each chunk's
+        # harvest starting as soon as its slice has landed
+        tables, _, _ = _ops.operator_tables(plan.coords, terms)
+        h = _harvest_pipelined(spec, sl, N, n, s, delta_t, tables, sset.row)
+        _ops.raise_on_status(h)
+        if stats is not None:
+            stats.setdefault("ms", []).append(h.ms)
+        return _ops.CompactRows(sset, nat.W_PERNODE, pernode=h.rows)
     elif varcoef:
         if idx is not None:
             coef_all = _ops.dev_f64(spec.coef).index_select(0, idx).contiguous()
@@ -345,6 +355,46 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
             stats.setdefault("ms", []).append(h.ms)
         out[:, :, a:b] = h.rows
     return _ops.CompactRows(sset, nat.W_PERNODE, pernode=out)
+
+
+PIPELINE_MIN = 1 << 18      # nodes; smaller host tables go up in one copy
+PIPELINE_CHUNKS = 8
+
+
+def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
+                       tables: torch.Tensor, row: int) -> _ops.HarvestOut:
+    """Per-node harvest (one shared window geometry) from HOST coefficients:
+    the [N, K] coefficient table goes up in PIPELINE_CHUNKS slices on the copy
+    stream, and the harvest of slice i (lmep_harvest_chunk into the shared SoA
+    output) overlaps the upload of slice i+1."""
+    d = nat.device()
+    cur = torch.cuda.current_stream(d)
+    cp = _ops.copy_stream()
+    K = len(spec.orders)
+    hc = _ops.host_f64(spec.coef)[sl]
+    hr = None if spec.reaction is None else _ops.host_f64(spec.reaction)[sl]
+    dc = torch.empty((N, K), dtype=torch.float64, device=d)
+    dr = None if hr is None else torch.empty(N, dtype=torch.float64, device=d)
+    out = _ops.HarvestOut(torch.empty((s, n, N), dtype=torch.float64, device=d),
+                          torch.empty(N, dtype=torch.int32, device=d),
+                          torch.empty(N, dtype=torch.int32, device=d))
+    cp.wait_stream(cur)                      # dc / dr were allocated on cur
+    step = -(-N // PIPELINE_CHUNKS)
+    step = -(-step // 128) * 128
+    for a in range(0, N, step):
+        b = min(N, a + step)
+        with torch.cuda.stream(cp):
+            dc[a:b].copy_(hc[a:b], non_blocking=True)
+            if dr is not None:
+                dr[a:b].copy_(hr[a:b], non_blocking=True)
+        cur.wait_event(cp.record_event())
+        _ops.harvest(n, s, delta_t, b - a, tables=tables, coef=dc[a:b], coef_stride=K,
+                     c0=None if dr is None else dr[a:b], c0_stride=0 if dr is None else 1,
+                     row_default=row, frozen_default=0, layout=1, into=out, item0=a)
+    dc.record_stream(cp)
+    if dr is not None:
+        dr.record_stream(cp)
+    return out
 
 
 def derivative_compact(grid: Grid, sset: StencilSet, k: int) -> _ops.CompactRows:

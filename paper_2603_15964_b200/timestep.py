@@ -365,31 +365,64 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
     u0 = problem.initial
     if tuple(u0.shape) != (grid.size,):
         raise DimensionMismatch(f"initial data must have shape ({grid.size},)")
+    N = grid.size
+    cur = torch.cuda.current_stream(dev)
+    cp, cp1 = _ops.copy_stream(0), _ops.copy_stream(1)
 
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter_ns()
+    # the initial data goes up on its own copy stream while the harvest runs
+    # (the harvest's own host inputs use copy stream 0)
+    with torch.cuda.stream(cp1):
+        u0d = _ops.dev_f64(u0)
+    ev_u0 = cp1.record_event()
     prep = prepare(grid, stencils, problem, scheme, delta_t, stats)
     torch.cuda.synchronize(dev)
     harvest_ns = time.perf_counter_ns() - t0
 
-    st = Stepper(prep, _ops.dev_f64(u0), exact=exact, tuning=tuning)
+    cur.wait_event(ev_u0)
+    u0d.record_stream(cur)
+    st = Stepper(prep, u0d, exact=exact, tuning=tuning)
+    nsnap = 1 + -(-steps_total // snap_every)
+    # snapshots land straight in one page-locked [S, N] block (returned as is)
+    snaps = torch.empty((nsnap, N), dtype=torch.float64, pin_memory=True)
+    snap_ev = None
+
+    def snapshot(i):
+        # D2H on the copy stream, overlapping the next chunk of steps; the
+        # next advance() waits for it before it may reuse st.u's buffer
+        cp.wait_stream(cur)
+        with torch.cuda.stream(cp):
+            snaps[i].copy_(st.u, non_blocking=True)
+        st.u.record_stream(cp)
+        return cp.record_event()
+
     times = [0.0]
-    snaps = [_ops.to_host_pinned(st.u)]
+    snap_ev, prev_ev = snapshot(0), None
     step_ns = 0
     done = 0
     while done < steps_total:
         k = min(snap_every, steps_total - done)
-        torch.cuda.synchronize(dev)
+        cur.synchronize()
         t0 = time.perf_counter_ns()
+        # a linear / ETDRK4 advance() reads st.u and writes the other buffers:
+        # it may overwrite the buffer the PREVIOUS snapshot was read from, never
+        # the latest.  Multistep warm-up swaps buffers between single steps.
+        wait = prev_ev if prep.scheme in ("linear", "etdrk4") else snap_ev
+        if wait is not None:
+            cur.wait_event(wait)
         st.advance(k)
-        torch.cuda.synchronize(dev)
+        cur.synchronize()
         step_ns += time.perf_counter_ns() - t0
         done += k
         if st.nonfinite():
-            raise NonFinite("time integration blew up", state=snaps[-1], time=times[-1])
+            cp.synchronize()
+            raise NonFinite("time integration blew up", state=snaps[len(times) - 1].numpy().copy(),
+                            time=times[-1])
         times.append(done * delta_t)
-        snaps.append(_ops.to_host_pinned(st.u))
-    return SimulationResult(times=np.array(times), snapshots=np.array(snaps), steps=steps_total,
+        prev_ev, snap_ev = snap_ev, snapshot(len(times) - 1)
+    cp.synchronize()
+    return SimulationResult(times=np.array(times), snapshots=snaps.numpy(), steps=steps_total,
                             harvest_ns=harvest_ns, step_ns=step_ns)
 
 

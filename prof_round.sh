@@ -1,9 +1,22 @@
-mkdir -p gpurun_out/r1e
-python bench.py --steps 5 --warmup 3 > gpurun_out/r1e/bench.json 2> gpurun_out/r1e/bench.err; echo bench rc=$?
-python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/r1e/bench_ref.json 2> gpurun_out/r1e/bench_ref.err; echo ref rc=$?
-python bench.py --steps 1 --warmup 1 --no-others --no-cpu > gpurun_out/r1e/b_small.json 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r1e/launches.csv python bench.py --steps 1 --warmup 1 --no-others --no-cpu > gpurun_out/r1e/ncu_launch.log 2>&1
-python tools/prof_cases.py harvest --reps 1 --N 1048576 && ncu --set full --clock-control none --import-source on -k regex:harvest_quad -s 1 -c 1 -o gpurun_out/r1e/harvest python tools/prof_cases.py harvest --reps 1 --N 1048576 > gpurun_out/r1e/ncu_h.log 2>&1
-python tools/prof_cases.py c5step --reps 32 && ncu --set full --clock-control none --import-source on -k regex:lin_pernode_tb -s 2 -c 1 -o gpurun_out/r1e/c5step python tools/prof_cases.py c5step --reps 32 > gpurun_out/r1e/ncu_c5s.log 2>&1
-python tools/prof_cases.py c4 --reps 2 --N 4194304 && ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 3 -c 1 -o gpurun_out/r1e/c4 python tools/prof_cases.py c4 --reps 2 --N 4194304 > gpurun_out/r1e/ncu_c4.log 2>&1
-python tools/prof_cases.py c3 --reps 2 && ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 3 -c 1 -o gpurun_out/r1e/c3 python tools/prof_cases.py c3 --reps 2 > gpurun_out/r1e/ncu_c3.log 2>&1
-ls gpurun_out/r1e
+#!/bin/bash
+# One GPU profiling round: tests, bench (ours + reference arm), launch list, ncu --set full
+# of the top kernels.  Usage: bash prof_round.sh <tag>   (outputs in gpurun_out/<tag>/)
+T=${1:-r1}
+O=gpurun_out/$T
+mkdir -p $O
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > $O/smi.txt 2>&1
+timeout 1200 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?"
+tail -3 $O/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"
+timeout 900 python bench.py --steps 5 --warmup 3 > $O/bench.json 2> $O/bench.err; echo "bench rc=$?"
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref.json 2> $O/bench_ref.err; echo "ref rc=$?"
+timeout 600 python bench.py --steps 1 --warmup 1 --no-others --no-cpu > $O/b_small.json 2>&1 && \
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
+  python bench.py --steps 1 --warmup 1 --no-others --no-cpu > $O/ncu_launch.log 2>&1; echo "launches rc=$?"
+timeout 300 python tools/prof_cases.py harvest --reps 1 --N 1048576 > $O/h_plain.json 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:harvest_mv -s 1 -c 1 -o $O/harvest \
+  python tools/prof_cases.py harvest --reps 1 --N 1048576 > $O/ncu_h.log 2>&1; echo "ncu harvest rc=$?"
+timeout 300 python tools/prof_cases.py c5step --reps 32 > $O/c5s_plain.json 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:lin_pernode_tb -s 2 -c 1 -o $O/c5step \
+  python tools/prof_cases.py c5step --reps 32 > $O/ncu_c5s.log 2>&1; echo "ncu c5step rc=$?"
+ls $O

@@ -457,6 +457,57 @@ def test_c5_run_varcoef_end_to_end(lx, golden):
     assert rel_l2(res.u_final, golden["c5_u"]) < U_TOL
 
 
+@pytest.mark.parametrize("src", ["numpy", "pinned"])
+def test_pipelined_host_harvest_bitwise(lx, src):
+    """Host coefficient tables above PIPELINE_MIN go up in chunks on the copy
+    stream (lmep_harvest_chunk into one SoA table): bit-identical to the
+    single-launch harvest from device-resident coefficients."""
+    from paper_2603_15964_b200 import configs, harvest as hv
+    N = 1 << 19
+    w5 = configs.c5(N=N, steps=1)
+    c, nu = w5.coef
+    g = lx.make_periodic_grid(N, 0.0, 1.0)
+    st = lx.select_stencils(g, w5.n, lx.StencilPolicy.CENTERED)
+    coef = np.stack([-c, nu], 1)
+    react = 0.25 * np.cos(g.nodes)
+    host = (torch.from_numpy(coef).pin_memory(), torch.from_numpy(react).pin_memory()) \
+        if src == "pinned" else (coef, react)
+    for s in (1, 3):
+        for r_h, r_d in ((None, None), (host[1], torch.as_tensor(react, device="cuda"))):
+            a = hv.harvest_compact(g, st, lx.VariableCoefficientSpec((1, 2), host[0], r_h),
+                                   w5.delta_t, s)
+            b = hv.harvest_compact(g, st, lx.VariableCoefficientSpec(
+                (1, 2), torch.as_tensor(coef, device="cuda"), r_d), w5.delta_t, s)
+            assert torch.equal(a.pernode, b.pernode), (s, r_h is None)
+
+
+@pytest.mark.parametrize("scheme", ["linear", "etd2"])
+def test_run_overlapped_snapshots_bitwise(lx, scheme):
+    """run() uploads u0 and downloads snapshots on copy streams that overlap
+    the harvest / steps: the snapshots equal a Stepper advanced chunk by
+    chunk from device-resident inputs."""
+    from paper_2603_15964_b200.timestep import Stepper, prepare
+    N = 1 << 16
+    g = lx.make_periodic_grid(N, 0.0, 2 * math.pi)
+    st = lx.select_stencils(g, 9, lx.StencilPolicy.CENTERED)
+    u0 = np.sin(g.nodes) + 0.1 * np.cos(3 * g.nodes)
+    h = 2 * math.pi / N
+    dt = 0.5 * h * h / 0.01
+    sc = lx.SchemeConfig("linear") if scheme == "linear" else lx.SchemeConfig("etd-multistep", s=2)
+    kind = "none" if scheme == "linear" else "convective"
+    for init in (u0, torch.from_numpy(u0).pin_memory()):
+        prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(((2, 0.01),)), None, init,
+                                    lx.Boundary.periodic(), kind)
+        res = lx.run(g, st, prob, sc, dt, 12 * dt, snapshot_stride=4 * dt)
+        assert res.snapshots.shape == (4, N)
+        prep = prepare(g, st, prob, sc, dt)
+        ref = Stepper(prep, torch.as_tensor(u0, device="cuda"))
+        assert np.array_equal(res.snapshots[0], u0)
+        for i in range(1, 4):
+            ref.advance(4)
+            assert np.array_equal(res.snapshots[i], ref.u.cpu().numpy()), i
+
+
 def test_nonfinite_run_raises_with_last_snapshot(lx):
     # literal BASELINE C2 dt (mu ~ 209) blows up (SURVEY M5/M6)
     N = 2048
