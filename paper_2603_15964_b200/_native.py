@@ -172,5 +172,5 @@ def set_harvest_method(method: str) -> None:
     """'multiply' (default for d <= 16: expm-multiply, 8 lanes per item when
     d > 8), "pade" (full expm per warp), or the first-generation kernel
     "quad" (8 lanes) / "multiply4" (4 lanes)."""
-    code = {"multiply": 0, "auto": 0, "pade": 1, "multiply4": 2, "quad": 3}[method]
+    code = {"multiply": 0, "auto": 0, "pade": 1, "multiply4": 2, "quad": 3, "mv4": 4}[method]
     check(lib().lmep_set_harvest_method(code), "lmep_set_harvest_method")

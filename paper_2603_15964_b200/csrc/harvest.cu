@@ -661,6 +661,8 @@ static int launch_harvest(const HarvestParams &P, cudaStream_t st)
 }
 
 static int g_harvest_method = 0;   // 0: auto (expm-multiply for d <= 16), 1: Pade expm
+static int g_mv_lanes = 0;
+int mv_lanes_override() { return g_mv_lanes; }
 
 static int dispatch_harvest(const HarvestParams &P, cudaStream_t st)
 {
@@ -784,8 +786,11 @@ extern "C" int lmep_harvest(int n, int s, int nterms, const double *tables,
 
 extern "C" int lmep_set_harvest_method(int method)
 {
-    if (method < 0 || method > 3) return LMEP_INVALID_CONFIG;
-    lmep::g_harvest_method = method;            // 0 mv, 1 pade, 2/3 quad (4 / 8 lanes)
+    if (method < 0 || method > 4) return LMEP_INVALID_CONFIG;
+    // 0 mv, 1 pade, 2/3 quad (4 / 8 lanes), 4 mv with 4 lanes per item for d > 8
+    lmep::g_mv_lanes = method == 4 ? 4 : 0;
+    if (method == 4) method = 0;
+    lmep::g_harvest_method = method;
     lmep::set_lanes_per_item(method == 2 ? 4 : 8);
     return LMEP_OK;
 }

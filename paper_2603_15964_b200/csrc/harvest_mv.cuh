@@ -74,7 +74,7 @@ struct MvCfg {
     static constexpr int R = (D + LPI - 1) / LPI;       // rows per lane
     static constexpr int SH = LPI == 4 ? 2 : 3;
     static constexpr int G = 32 / LPI;                  // items per warp
-    static constexpr int TS = LPI == 8 ? 18 : 10;       // doubles per item vector (bank-spread pad)
+    static constexpr int TS = (LPI == 8 || D > 8) ? 18 : 10;   // doubles per item vector (bank-spread pad)
     static constexpr int BUF = G * TS;                  // one buffer of a warp
     static constexpr int WARP_T = 2 * BUF;              // double buffered
     static constexpr int THREADS = 128;
@@ -413,10 +413,11 @@ __global__ void __launch_bounds__(128) harvest_mv_kernel(const HarvestParams P)
     }
 }
 
-template <int D>
-int launch_mv(const HarvestParams &P, cudaStream_t st)
+int mv_lanes_override();   // 0: default (8 lanes for d > 8, else 4)
+
+template <int D, int LPI>
+int launch_mv_l(const HarvestParams &P, cudaStream_t st)
 {
-    constexpr int LPI = D > 8 ? 8 : 4;
     using C = MvCfg<D, LPI>;
     const int64_t threads = P.B * LPI;
     const int64_t blocks = (threads + C::THREADS - 1) / C::THREADS;
@@ -434,6 +435,17 @@ int launch_mv(const HarvestParams &P, cudaStream_t st)
     default: harvest_mv_kernel<D, LPI, 0><<<g, t, shm, st>>>(P); break;
     }
     return launch_status("harvest_mv_kernel");
+}
+
+template <int D>
+int launch_mv(const HarvestParams &P, cudaStream_t st)
+{
+    if constexpr (D > 8) {
+        if (mv_lanes_override() == 4) return launch_mv_l<D, 4>(P, st);
+        return launch_mv_l<D, 8>(P, st);
+    } else {
+        return launch_mv_l<D, 4>(P, st);
+    }
 }
 
 }  // namespace lmep

@@ -70,13 +70,22 @@ int launch_lin_pernode(const StepParams &p, cudaStream_t st)
 
 namespace lmep {
 
-// Per-node linear steps with temporal blocking (periodic, single shard, no
-// closure): a CTA stages u over its tile plus k*(n-1) halo nodes in shared
-// memory and holds the per-node rows of every node it computes in REGISTERS
-// (thread t owns nodes t, t+nt, ..., t+(J-1)nt of the staged range), then
-// advances k steps on chip.  The 8n bytes of rows per node cross HBM once per
-// k steps instead of once per step.  Same ascending unfused arithmetic as
-// kernels.py:23-29 (bit-identical to the one-step kernels).
+// Per-node linear steps with temporal blocking (periodic, no closure): a CTA
+// stages u over its tile plus k*(n-1) halo nodes in shared memory and holds
+// the per-node rows of every node it computes in REGISTERS, then advances k
+// steps on chip.  The 8n bytes of rows per node cross HBM once per k steps
+// instead of once per step.
+//
+// Thread t owns the J CONSECUTIVE staged nodes J*t .. J*t+J-1: one sliding
+// window of J+n-1 shared-memory loads serves its J outputs (J odd: the
+// stride-J lane pattern is bank-conflict free for 8-byte words), and the J
+// accumulation chains interleave.  Every thread computes all its nodes every
+// step (no per-node predicates, so the chains stay in one basic block); the
+// staged buffers carry eL / eR pad words so edge windows stay in bounds, and
+// values outside the shrinking valid range are never consumed.
+// Arithmetic: the ascending, unfused order of kernels.py:23-29, with the
+// chain started at the first product (0 + p0 == p0 up to the sign of zero),
+// so results equal the one-step kernels.
 template <int NS, int J>
 __global__ void __launch_bounds__(256, 2) lin_pernode_tb_kernel(const __grid_constant__ StepParams p)
 {
@@ -90,39 +99,48 @@ __global__ void __launch_bounds__(256, 2) lin_pernode_tb_kernel(const __grid_con
     const int64_t base = p.off + t0 - (int64_t)K * eL;
     const int len = (int)(t1 - t0) + K * (eL + eR);
     const bool single = p.hl == nullptr && p.hr == nullptr;
+    // staged node l lives at U[eL + l]; U[0, eL) and U[eL + len, ...) are pads
     double *U0 = sm, *U1 = sm + p.slot_len;
-    for (int i = tid; i < len; i += nt) U0[i] = load_node(p, p.u_in, p.hl, p.hr, base + i);
+    const int span = J * nt;
+    for (int i = tid; i < span + NS - 1; i += nt) {
+        const int l = i - eL;
+        U0[i] = (l >= 0 && l < len) ? load_node(p, p.u_in, p.hl, p.hr, base + l) : 0.0;
+        U1[i] = 0.0;
+    }
     // rows: single shard -> the periodic grid's own table (wrap); sharded ->
-    // this shard's table, padded with the rows of wpad halo nodes per side
+    // this shard's table, padded with the rows of wpad halo nodes per side.
+    // The J loads of one tap cover J*32 consecutive doubles per warp (L1 hits).
     double w[J][NS];
 #pragma unroll
     for (int j = 0; j < J; ++j) {
-        const int l = tid + j * nt;
+        const int l = J * tid + j;
         const int64_t g = base + (l < len ? l : (int64_t)K * eL);
         const int64_t wi = single ? wrap(g, p.N) : g - p.off + p.wpad;
 #pragma unroll
-        for (int c = 0; c < NS; ++c) w[j][c] = __ldcs(p.wp + (int64_t)c * p.wld + wi);
+        for (int c = 0; c < NS; ++c) w[j][c] = __ldg(p.wp + (int64_t)c * p.wld + wi);
     }
     __syncthreads();
     for (int s = 0; s < K; ++s) {
-        const int lo = (s + 1) * eL, hi = len - (s + 1) * eR;
+        const double *x = U0 + J * tid;          // window of node J*tid starts at U[J*tid]
+        double acc[J];
 #pragma unroll
-        for (int j = 0; j < J; ++j) {
-            const int l = tid + j * nt;
-            if (l >= lo && l < hi) {
-                const double *x = U0 + (l - eL);
-                double acc = 0.0;
+        for (int i = 0; i < J + NS - 1; ++i) {
+            const double v = x[i];
 #pragma unroll
-                for (int c = 0; c < NS; ++c) acc = xadd(acc, xmul(w[j][c], x[c]));
-                U1[l] = acc;
+            for (int j = 0; j < J; ++j) {
+                const int c = i - j;
+                if (c == 0) acc[j] = xmul(w[j][0], v);
+                else if (c > 0 && c < NS) acc[j] = xadd(acc[j], xmul(w[j][c], v));
             }
         }
+#pragma unroll
+        for (int j = 0; j < J; ++j) U1[eL + J * tid + j] = acc[j];
         __syncthreads();
         double *t = U0; U0 = U1; U1 = t;
     }
     bool bad = false;
     for (int64_t i = t0 + tid; i < t1; i += nt) {
-        const double v = U0[(int)(i + K * eL - t0)];
+        const double v = U0[eL + (int)(i + K * eL - t0)];
         p.u_out[i] = v;
         bad |= !isfinite(v);
     }
