@@ -56,12 +56,15 @@ int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded
         return LMEP_OK;
     }
     int64_t tile = t.tile, k = t.ksteps;
-    if (pernode && sch == SCH_LIN && g.periodic && tb_nodes_per_cta(n) > 0 && steps > 1 &&
+    if (pernode && sch == SCH_LIN && g.periodic && tb_nodes_per_cta(n, false) > 0 && steps > 1 &&
         t.tile == 0 && (!sharded || pernode_pad >= steps * std::max(eL, eR))) {
-        // per-node rows held in registers for k steps (lin_pernode_tb_kernel);
-        // sharded: the caller fuses `steps` steps per halo exchange
+        // per-node rows held in registers for k steps: single shard with an
+        // even N -> the persistent TMA-pipelined kernel (lin_pernode_tma_kernel),
+        // else lin_pernode_tb_kernel; sharded: the caller fuses `steps` steps
+        // per halo exchange
         k = sharded ? steps : (t.ksteps > 0 ? t.ksteps : std::min<int64_t>(16, steps));
-        const int64_t span = tb_nodes_per_cta(n);
+        const bool tma = !sharded && (g.N % 2) == 0 && g.N >= tb_nodes_per_cta(n, true);
+        const int64_t span = tb_nodes_per_cta(n, tma);
         while (k > 1 && span - k * (n - 1) < span / 2) --k;
         t.tile = (int32_t)(span - k * (n - 1));
         t.ksteps = (int32_t)k;
@@ -292,9 +295,12 @@ int run_steps(const StepCall &c)
             p.qhl = c.halo->hist_left; p.qhr = c.halo->hist_right;
             p.G = c.halo->width;
         }
-        if (c.sch == SCH_LIN && pernode && p.bc == LMEP_BC_NONE && g.periodic &&
-            t.threads == 256 && t.tile + (int64_t)t.ksteps * (g.n - 1) == tb_nodes_per_cta(g.n))
-            rc = launch_lin_pernode_tb(p, c.stream);       // rows in registers, k steps (C5)
+        if (c.sch == SCH_LIN && pernode && p.bc == LMEP_BC_NONE && g.periodic && !sharded &&
+            t.threads == 256 && t.tile + (int64_t)t.ksteps * (g.n - 1) == tb_nodes_per_cta(g.n, true))
+            rc = launch_lin_pernode_tma(p, c.stream);      // persistent, TMA-pipelined (C5)
+        else if (c.sch == SCH_LIN && pernode && p.bc == LMEP_BC_NONE && g.periodic &&
+            t.threads == 256 && t.tile + (int64_t)t.ksteps * (g.n - 1) == tb_nodes_per_cta(g.n, false))
+            rc = launch_lin_pernode_tb(p, c.stream);       // rows in registers, k steps
         else if (c.sch == SCH_LIN && pernode && p.bc == LMEP_BC_NONE && k == 1 && !t.ring)
             rc = launch_lin_pernode(p, c.stream);          // lean streaming kernel
         else

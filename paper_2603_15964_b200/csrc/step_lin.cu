@@ -148,7 +148,11 @@ __global__ void __launch_bounds__(256, 2) lin_pernode_tb_kernel(const __grid_con
 }
 
 // nodes per CTA staged range = J * 256; returns 0 if not applicable
-int tb_nodes_per_cta(int n) { return n == 13 || n == 11 || n == 9 || n == 7 ? 3 * 256 : 0; }
+// tma: the persistent kernel (step_lin_tma.cu, 3 x 512 nodes), else 3 x 256
+int tb_nodes_per_cta(int n, bool tma)
+{
+    return n == 13 || n == 11 || n == 9 || n == 7 ? 3 * (tma ? 512 : 256) : 0;
+}
 
 int launch_lin_pernode_tb(const StepParams &p, cudaStream_t st)
 {

@@ -1,0 +1,227 @@
+// step_lin_tma.cu -- persistent, TMA-pipelined per-node linear steps
+// (BASELINE config 5: periodic grid, one shard, per-node rows, no closure).
+//
+// Same schedule and arithmetic as lin_pernode_tb_kernel (step_lin.cu): a tile
+// of the grid plus k*(n-1) halo nodes is staged on chip, each thread holds the
+// per-node rows of its J consecutive staged nodes in registers, and the CTA
+// advances k steps with one barrier per step; the rows cross HBM once per k
+// steps.  What changes is that the loads of tile i+1 overlap the k steps of
+// tile i:
+//
+//   * one CTA per SM (persistent, tiles strided by gridDim.x);
+//   * one elected thread moves the next tile's rows ([n][span] slice of the
+//     SoA table) and its u into shared memory with 1-D bulk copies
+//     (cp.async.bulk ... mbarrier::complete_tx), issued as soon as every
+//     thread has copied the current tile's rows from shared memory into its
+//     registers, so HBM streams while the FP64 pipe works;
+//   * three u buffers rotate: the landed tile's initial state, its ping-pong
+//     partner, and the target of the next tile's copy.
+//
+// Bulk copies need 16-byte aligned sources and sizes, so each row / u slice
+// is fetched from the even node at or below the staged range start and the
+// smem origin is shifted by that parity (`o`).  Periodic wrap splits a slice
+// into two copies.  Arithmetic: the ascending unfused order of
+// kernels.py:23-29, bit-identical to the other per-node step kernels.
+#include "step.cuh"
+
+namespace lmep {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// staged range of tile `tile`: global nodes [base, base + len), fetched from
+// the even node `start` = base - o, cnt (even) nodes, wrapping at N
+struct TileRange {
+    int64_t t0, t1, base, start;
+    int len, o, cnt;
+};
+
+__device__ __forceinline__ TileRange tile_range(const StepParams &p, int64_t tile, int K, int eL, int eR)
+{
+    TileRange r;
+    r.t0 = tile * p.tile;
+    r.t1 = r.t0 + p.tile < p.nloc ? r.t0 + p.tile : p.nloc;
+    r.len = (int)(r.t1 - r.t0) + K * (eL + eR);
+    int64_t b = (r.t0 - (int64_t)K * eL) % p.N;
+    if (b < 0) b += p.N;
+    r.base = b;
+    r.o = (int)(b & 1);
+    r.start = b - r.o;
+    r.cnt = (r.len + r.o + 1) & ~1;
+    return r;
+}
+
+// copy cnt doubles of the periodic vector v (length N, even) starting at the
+// even index `start` into dst: one or two bulk copies; returns the byte count
+__device__ __forceinline__ uint32_t copy_wrapped(double *dst, const double *v, int64_t N,
+                                                 int64_t start, int cnt, uint64_t *bar)
+{
+    const int64_t first = start + cnt <= N ? cnt : N - start;
+    bulk_g2s(dst, v + start, (uint32_t)(first * 8), bar);
+    if (first < cnt) bulk_g2s(dst + first, v, (uint32_t)((cnt - first) * 8), bar);
+    return (uint32_t)cnt * 8u;
+}
+
+}  // namespace
+
+// u buffer length (even, so every buffer starts 16-byte aligned)
+__host__ __device__ constexpr int tma_ulen(int n, int span) { return (span + n + 5) & ~1; }
+
+template <int NS, int J, int NT>
+__global__ void __launch_bounds__(NT, 1) lin_pernode_tma_kernel(const __grid_constant__ StepParams p)
+{
+    constexpr int SPAN = J * NT;
+    constexpr int RS = SPAN + 4;                 // row slice stride (even: 16-byte aligned)
+    constexpr int UL = tma_ulen(NS, SPAN);       // u buffer: pads for eL/eR and the parity shift
+    extern __shared__ __align__(16) double sm[];
+    double *R = sm;                              // [NS][RS]
+    double *Ub = sm + NS * RS;                   // [3][UL]
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x;
+    const int K = p.ksteps;
+    const int eL = p.row, eR = NS - 1 - p.row;
+    const int64_t ntiles = (p.nloc + p.tile - 1) / p.tile;
+
+    for (int i = tid; i < NS * RS + 3 * UL; i += NT) sm[i] = 0.0;
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    // buffer b's origin: staged node l of a tile at Ub[b*UL + org + l] with
+    // org - o even, so the bulk copy destination (org - o) is 16-byte aligned
+    auto issue = [&](int64_t tile, int b) {
+        const TileRange r = tile_range(p, tile, K, eL, eR);
+        const int org = eL + ((eL - r.o) & 1);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        const uint32_t bytes = (uint32_t)r.cnt * 8u * (NS + 1);
+        mbar_expect_tx(&bar, bytes);
+#pragma unroll 1
+        for (int c = 0; c < NS; ++c)
+            copy_wrapped(R + c * RS, p.wp + (int64_t)c * p.wld, p.N, r.start, r.cnt, &bar);
+        copy_wrapped(Ub + b * UL + org - r.o, p.u_in, p.N, r.start, r.cnt, &bar);
+    };
+
+    int64_t tile = blockIdx.x;
+    if (tid == 0 && tile < ntiles) issue(tile, 0);
+    bool bad = false;
+    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+        const TileRange r = tile_range(p, tile, K, eL, eR);
+        const int org = eL + ((eL - r.o) & 1);
+        const int bT = it % 3, bP = (it + 2) % 3;
+        mbar_wait(&bar, (uint32_t)(it & 1));
+        // rows of this thread's J consecutive staged nodes -> registers
+        double w[J][NS];
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int l = J * tid + j;
+            const int ls = r.o + (l < r.len ? l : K * eL);
+#pragma unroll
+            for (int c = 0; c < NS; ++c) w[j][c] = R[c * RS + ls];
+        }
+        __syncthreads();                         // R free, previous tile's outputs stored
+        const int64_t nxt = tile + gridDim.x;
+        if (tid == 0 && nxt < ntiles) issue(nxt, (it + 1) % 3);
+
+        double *U0 = Ub + bT * UL + org - eL, *U1 = Ub + bP * UL + org - eL;
+        for (int s = 0; s < K; ++s) {
+            const double *x = U0 + J * tid;      // window of staged node J*tid
+            double acc[J];
+#pragma unroll
+            for (int i = 0; i < J + NS - 1; ++i) {
+                const double v = x[i];
+#pragma unroll
+                for (int j = 0; j < J; ++j) {
+                    const int c = i - j;
+                    if (c == 0) acc[j] = xmul(w[j][0], v);
+                    else if (c > 0 && c < NS) acc[j] = xadd(acc[j], xmul(w[j][c], v));
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < J; ++j) U1[eL + J * tid + j] = acc[j];
+            __syncthreads();
+            double *t = U0; U0 = U1; U1 = t;
+        }
+        for (int64_t i = r.t0 + tid; i < r.t1; i += NT) {
+            const double v = U0[eL + (int)(i - r.t0) + K * eL];
+            p.u_out[i] = v;
+            bad |= !isfinite(v);
+        }
+    }
+    if (bad) *p.flag = 1;
+}
+
+size_t tma_smem_bytes(int n, int span) { return (size_t)(n * (span + 4) + 3 * tma_ulen(n, span)) * 8; }
+
+int launch_lin_pernode_tma(const StepParams &p, cudaStream_t st)
+{
+    constexpr int J = 3, NT = 512;
+    const size_t shm = tma_smem_bytes(p.n, J * NT);
+    const int64_t ntiles = (p.nloc + p.tile - 1) / p.tile;
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (nsm <= 0) nsm = 148;
+    }
+    const unsigned grid = (unsigned)(ntiles < nsm ? ntiles : nsm);
+    if ((p.N & 1) || (p.wld & 1) || ((uintptr_t)p.wp & 15) || ((uintptr_t)p.u_in & 15))
+        return LMEP_INVALID_CONFIG;
+#define LMEP_TMA_CASE(NS_)                                                                        \
+    case NS_:                                                                                     \
+        cudaFuncSetAttribute(lin_pernode_tma_kernel<NS_, J, NT>,                                  \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);              \
+        lin_pernode_tma_kernel<NS_, J, NT><<<grid, NT, shm, st>>>(p);                             \
+        break;
+    switch (p.n) {
+        LMEP_TMA_CASE(13)
+        LMEP_TMA_CASE(11)
+        LMEP_TMA_CASE(9)
+        LMEP_TMA_CASE(7)
+    default: return LMEP_INVALID_CONFIG;
+    }
+#undef LMEP_TMA_CASE
+    return launch_status("lin_pernode_tma_kernel");
+}
+
+}  // namespace lmep
