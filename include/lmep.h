@@ -226,10 +226,12 @@ int lmep_harvest_chunk(int n, int s, int nterms, const double *tables, const int
                        void *stream);
 
 /* Harvest algorithm for d <= 16: 0 (default) = register-resident
- * expm-multiply, warp-uniform (harvest_mv.cuh: balancing + scaled Taylor
- * action on the needed columns), 1 = full Pade scaling-and-squaring per warp
- * (harvest.cu), 2 / 3 = the first-generation expm-multiply kernel with 4 / 8
- * lanes per item (harvest_quad.cu).  lmep_expm always uses the Pade kernel.
+ * expm-multiply, warp-uniform, 4 lanes per item (harvest_mv.cuh: balancing +
+ * scaled Taylor action on the needed columns), 1 = full Pade
+ * scaling-and-squaring per warp (harvest.cu), 2 / 3 = the first-generation
+ * expm-multiply kernel with 4 / 8 lanes per item (harvest_quad.cu), 4 = the
+ * warp-uniform kernel with 8 lanes per item for d > 8.  lmep_expm always uses
+ * the Pade kernel.
  * Process-wide setting. */
 int lmep_set_harvest_method(int method);
 

@@ -787,8 +787,8 @@ extern "C" int lmep_harvest(int n, int s, int nterms, const double *tables,
 extern "C" int lmep_set_harvest_method(int method)
 {
     if (method < 0 || method > 4) return LMEP_INVALID_CONFIG;
-    // 0 mv, 1 pade, 2/3 quad (4 / 8 lanes), 4 mv with 4 lanes per item for d > 8
-    lmep::g_mv_lanes = method == 4 ? 4 : 0;
+    // 0 mv (4 lanes per item), 1 pade, 2/3 quad (4 / 8 lanes), 4 mv with 8 lanes for d > 8
+    lmep::g_mv_lanes = method == 4 ? 8 : 0;
     if (method == 4) method = 0;
     lmep::g_harvest_method = method;
     lmep::set_lanes_per_item(method == 2 ? 4 : 8);

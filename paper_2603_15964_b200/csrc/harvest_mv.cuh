@@ -78,7 +78,8 @@ struct MvCfg {
     static constexpr int BUF = G * TS;                  // one buffer of a warp
     static constexpr int WARP_T = 2 * BUF;              // double buffered
     static constexpr int THREADS = 128;
-    static constexpr int INV = 48;                      // 1/k table
+    static constexpr int INV = 48;                      // 1/k! table
+    static constexpr int EXPW = (THREADS / LPI) * 16 / 2;   // per-group balancing exponents (int)
     static_assert(TS >= D + (D & 1), "item vector too short");
 };
 
@@ -86,7 +87,7 @@ template <int D, int LPI>
 constexpr size_t mv_smem_bytes(int nt)
 {
     using C = MvCfg<D, LPI>;
-    return (size_t)(C::INV + (C::THREADS / 32) * C::WARP_T + nt * D * D) * sizeof(double);
+    return (size_t)(C::INV + C::EXPW + (C::THREADS / 32) * C::WARP_T + nt * D * D) * sizeof(double);
 }
 
 // A's rows owned by this lane from a CTA-shared table sT[t][j][c] = D_t[c][j]
@@ -176,14 +177,19 @@ __global__ void __launch_bounds__(128) harvest_mv_kernel(const HarvestParams P)
     using C = MvCfg<D, LPI>;
     constexpr int R = C::R, SH = C::SH;
     extern __shared__ __align__(16) double mv_sm[];
-    double *sInv = mv_sm;
-    double *sT = mv_sm + C::INV + (threadIdx.x >> 5) * C::WARP_T;
-    double *sTab = mv_sm + C::INV + (C::THREADS / 32) * C::WARP_T;
+    double *sFact = mv_sm;                                     // 1/k!
+    int *sE = reinterpret_cast<int *>(mv_sm + C::INV);        // [group][16] exponents
+    double *sT = mv_sm + C::INV + C::EXPW + (threadIdx.x >> 5) * C::WARP_T;
+    double *sTab = mv_sm + C::INV + C::EXPW + (C::THREADS / 32) * C::WARP_T;
     const int lane = threadIdx.x & 31;
     const int q = lane & (LPI - 1), qb = lane & ~(LPI - 1), grp = lane >> SH;
     const int n = P.n, sd = P.s;
 
-    for (int i = threadIdx.x; i < C::INV; i += blockDim.x) sInv[i] = i ? 1.0 / (double)i : 0.0;
+    for (int i = threadIdx.x; i < C::INV; i += blockDim.x) {
+        double f = 1.0;
+        for (int j = 2; j <= i; ++j) f *= (double)j;
+        sFact[i] = 1.0 / f;
+    }
     if (NT > 0) {
         for (int i = threadIdx.x; i < NT * D * D; i += blockDim.x) {
             const int t = i / (D * D), r = i - t * D * D, j = r / D, c = r - j * D;
@@ -216,6 +222,11 @@ __global__ void __launch_bounds__(128) harvest_mv_kernel(const HarvestParams P)
     int status = (mv_gmax<LPI>(finite ^ 1u) == 0u) ? LMEP_OK : LMEP_NONFINITE;
 
     // ---- balancing: parallel Osborne sweeps with exact powers of two --------
+    // Any power-of-two diagonal similarity leaves exp(A) unchanged up to
+    // rounding (expm.py:27-30 balances for the norm and for overflow); the
+    // step per row comes straight from the exponents of the squared row and
+    // column 2-norms, which avoids the square roots and search loops of
+    // dgebal's acceptance test.
     int e[R];
 #pragma unroll
     for (int m = 0; m < R; ++m) e[m] = 0;
@@ -242,16 +253,12 @@ __global__ void __launch_bounds__(128) harvest_mv_kernel(const HarvestParams P)
             const double c2 = myc2[m];
             if (status == LMEP_OK && q + LPI * m < D && c2 > 1e-280 && r2 > 1e-280 &&
                 c2 < 1e280 && r2 < 1e280) {
-                const double cn = sqrt(c2), rn = sqrt(r2);
-                int kk = (mv_exp2i(rn) - mv_exp2i(cn)) / 2;
-                while (cn * mv_pow2(2 * kk + 1) < rn) ++kk;
-                while (kk > 0 && !(cn * mv_pow2(2 * kk - 1) < rn)) --kk;
-                if (kk <= 0) {
-                    kk = 0;
-                    while (cn * mv_pow2(-(2 * (-kk) + 1)) >= rn) --kk;
-                }
-                const double f = mv_pow2(kk);
-                if (kk != 0 && cn * f + rn / f < 0.95 * (cn + rn)) k[m] = kk;
+                // 2^kk ~ sqrt(rn / cn) minimises cn 2^kk + rn 2^-kk; ex = log2(r2 / c2)
+                // to +-1, so |ex| >= 4 (rn / cn >= 2^1.5) guarantees kk = +-1 or
+                // more strictly reduces the row + column norm (no oscillation)
+                const int ex = mv_exp2i(r2) - mv_exp2i(c2);
+                if (ex >= 4) k[m] = (ex + 2) >> 2;
+                else if (ex <= -4) k[m] = -((2 - ex) >> 2);
             }
             chg |= k[m] != 0;
         }
@@ -290,6 +297,12 @@ __global__ void __launch_bounds__(128) harvest_mv_kernel(const HarvestParams P)
     const int reps = status == LMEP_OK ? s : 0;
 
     // ---- flattened Taylor iteration: state (column qo, rep, term kt) per group
+    // The iterate is the unscaled power u_k = B^k v (||B|| <= THETA keeps it
+    // bounded) and the partial sum takes u_k / k! with one FMA per row.
+    int *eg = sE + (threadIdx.x >> SH) * 16;                  // this group's exponents
+#pragma unroll
+    for (int m = 0; m < R; ++m)
+        if (q + LPI * m < D) eg[q + LPI * m] = e[m];
     int qo = 0, rep = 0, kt = 1, nmv = 0, idx = row;
     bool done = reps == 0;
     unsigned bad = 0u;
@@ -305,49 +318,63 @@ __global__ void __launch_bounds__(128) harvest_mv_kernel(const HarvestParams P)
     __syncwarp();
     while (__any_sync(MV_FULL, !done)) {
         const double *tv = tg + buf * C::BUF;
-        double s0[R], s1[R];
+        double u[R];
+        if constexpr (R >= 4) {                  // R independent chains already
 #pragma unroll
-        for (int m = 0; m < R; ++m) s0[m] = s1[m] = 0.0;
+            for (int m = 0; m < R; ++m) u[m] = 0.0;
 #pragma unroll
-        for (int c = 0; c < D; c += 2) {
-            if (c + 1 < D) {
-                const double2 tt = *reinterpret_cast<const double2 *>(tv + c);
+            for (int c = 0; c < D; c += 2) {
+                if (c + 1 < D) {
+                    const double2 tt = *reinterpret_cast<const double2 *>(tv + c);
 #pragma unroll
-                for (int m = 0; m < R; ++m) {
-                    s0[m] = fma(a[m][c], tt.x, s0[m]);
-                    s1[m] = fma(a[m][c + 1], tt.y, s1[m]);
+                    for (int m = 0; m < R; ++m) u[m] = fma(a[m][c + 1], tt.y, fma(a[m][c], tt.x, u[m]));
+                } else {
+                    const double t0 = tv[c];
+#pragma unroll
+                    for (int m = 0; m < R; ++m) u[m] = fma(a[m][c], t0, u[m]);
                 }
-            } else {
-                const double t0 = tv[c];
-#pragma unroll
-                for (int m = 0; m < R; ++m) s0[m] = fma(a[m][c], t0, s0[m]);
             }
+        } else {
+            double s0[R], s1[R];
+#pragma unroll
+            for (int m = 0; m < R; ++m) s0[m] = s1[m] = 0.0;
+#pragma unroll
+            for (int c = 0; c < D; c += 2) {
+                if (c + 1 < D) {
+                    const double2 tt = *reinterpret_cast<const double2 *>(tv + c);
+#pragma unroll
+                    for (int m = 0; m < R; ++m) {
+                        s0[m] = fma(a[m][c], tt.x, s0[m]);
+                        s1[m] = fma(a[m][c + 1], tt.y, s1[m]);
+                    }
+                } else {
+                    const double t0 = tv[c];
+#pragma unroll
+                    for (int m = 0; m < R; ++m) s0[m] = fma(a[m][c], t0, s0[m]);
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < R; ++m) u[m] = s0[m] + s1[m];
         }
-        const double ik = sInv[kt];
-        double w[R];
+        const double fk = sFact[kt];
+        const double fa = done ? 0.0 : fk;
         unsigned wh = 0u, ah = 0u;
 #pragma unroll
         for (int m = 0; m < R; ++m) {
-            w[m] = (s0[m] + s1[m]) * ik;
-            if (!done) acc[m] += w[m];
+            acc[m] = fma(u[m], fa, acc[m]);
             // convergence is judged on the extracted rows only: the augmentation
             // chain (rows >= n) is O(1) while dt^j phi_j is tiny
             if (q + LPI * m < n) {
-                wh = max(wh, mv_hiabs(w[m]));
+                wh = max(wh, mv_hiabs(u[m]));
                 ah = max(ah, mv_hiabs(acc[m]));
             }
         }
         wh = mv_gmax<LPI>(wh);
         ah = mv_gmax<LPI>(ah);
-        const double wn = __hiloint2double((int)wh, -1);   // >= max |w|
-        const double an = __hiloint2double((int)ah, 0);    // <= max |acc|
+        const double wn = __hiloint2double((int)wh, -1) * fk;  // >= max |u_k / k!| (to rounding)
+        const double an = __hiloint2double((int)ah, 0);         // <= max |acc|
         // the chain needs qo products to reach the extracted rows
         const bool conv = (kt > qo && an > 0.0 && wn + wprev <= 0x1p-53 * an) || kt >= MV_TMAX;
-        int eo = 0;
-#pragma unroll
-        for (int m = 0; m < R; ++m)
-            if ((idx >> SH) == m) eo = e[m];
-        const int eidx = __shfl_sync(MV_FULL, eo, qb + (idx & (LPI - 1)));
         if (!done) {
             ++nmv;
             double nt[R];
@@ -357,6 +384,7 @@ __global__ void __launch_bounds__(128) harvest_mv_kernel(const HarvestParams P)
                 wprev = INFINITY;
                 if (rep >= reps) {
                     // back to A's coordinates: exp(A) e_idx = 2^-e_idx D exp(B) e_idx
+                    const int eidx = eg[idx];
 #pragma unroll
                     for (int m = 0; m < R; ++m) {
                         const int j = q + LPI * m;
@@ -384,7 +412,7 @@ __global__ void __launch_bounds__(128) harvest_mv_kernel(const HarvestParams P)
                 ++kt;
                 wprev = wn;
 #pragma unroll
-                for (int m = 0; m < R; ++m) nt[m] = w[m];
+                for (int m = 0; m < R; ++m) nt[m] = u[m];
             }
             buf ^= 1;
             double *to = tg + buf * C::BUF;
@@ -413,7 +441,7 @@ __global__ void __launch_bounds__(128) harvest_mv_kernel(const HarvestParams P)
     }
 }
 
-int mv_lanes_override();   // 0: default (8 lanes for d > 8, else 4)
+int mv_lanes_override();   // 0: default (4 lanes per item), 8: 8 lanes for d > 8
 
 template <int D, int LPI>
 int launch_mv_l(const HarvestParams &P, cudaStream_t st)
@@ -441,8 +469,8 @@ template <int D>
 int launch_mv(const HarvestParams &P, cudaStream_t st)
 {
     if constexpr (D > 8) {
-        if (mv_lanes_override() == 4) return launch_mv_l<D, 4>(P, st);
-        return launch_mv_l<D, 8>(P, st);
+        if (mv_lanes_override() == 8) return launch_mv_l<D, 8>(P, st);
+        return launch_mv_l<D, 4>(P, st);
     } else {
         return launch_mv_l<D, 4>(P, st);
     }

@@ -17,6 +17,6 @@ timeout 300 python tools/prof_cases.py harvest --reps 1 --N 1048576 > $O/h_plain
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:harvest_mv -s 1 -c 1 -o $O/harvest \
   python tools/prof_cases.py harvest --reps 1 --N 1048576 > $O/ncu_h.log 2>&1; echo "ncu harvest rc=$?"
 timeout 300 python tools/prof_cases.py c5step --reps 32 > $O/c5s_plain.json 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:lin_pernode_tb -s 2 -c 1 -o $O/c5step \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:lin_pernode_t -s 2 -c 1 -o $O/c5step \
   python tools/prof_cases.py c5step --reps 32 > $O/ncu_c5s.log 2>&1; echo "ncu c5step rc=$?"
 ls $O
