@@ -669,7 +669,11 @@ static int dispatch_harvest(const HarvestParams &P, cudaStream_t st)
     if (P.B == 0) return LMEP_OK;
     if (P.mode != 0 && g_harvest_method != 1 && P.d >= 2 && P.d <= 16 &&
         (P.mode == 2 || P.nterms <= 4))
-        return g_harvest_method == 0 ? launch_harvest_mv(P, st) : launch_harvest_quad(P, st);
+    {
+        if (g_harvest_method == 0 && harvest_mvb_eligible(P)) return launch_harvest_mvb(P, st);
+        if (g_harvest_method == 0 || g_harvest_method == 5) return launch_harvest_mv(P, st);
+        return launch_harvest_quad(P, st);
+    }
     if (P.d <= 8) return launch_harvest<8, 8>(P, st);
     if (P.d <= 16) return launch_harvest<16, 4>(P, st);
     if (P.d <= 32) return launch_harvest<32, 2>(P, st);
@@ -786,10 +790,12 @@ extern "C" int lmep_harvest(int n, int s, int nterms, const double *tables,
 
 extern "C" int lmep_set_harvest_method(int method)
 {
-    if (method < 0 || method > 4) return LMEP_INVALID_CONFIG;
-    // 0 mv (4 lanes per item), 1 pade, 2/3 quad (4 / 8 lanes), 4 mv with 8 lanes for d > 8
+    if (method < 0 || method > 5) return LMEP_INVALID_CONFIG;
+    // 0 auto: block-balanced mv for large single-geometry batches, else mv (4 lanes per
+    // item); 1 pade; 2/3 quad (4 / 8 lanes); 4 per-item mv with 8 lanes for d > 8;
+    // 5 per-item mv (4 lanes) only
     lmep::g_mv_lanes = method == 4 ? 8 : 0;
-    if (method == 4) method = 0;
+    if (method == 4) method = 5;
     lmep::g_harvest_method = method;
     lmep::set_lanes_per_item(method == 2 ? 4 : 8);
     return LMEP_OK;

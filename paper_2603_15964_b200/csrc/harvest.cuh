@@ -56,4 +56,24 @@ inline int launch_harvest_mv(const HarvestParams &P, cudaStream_t st)
 }
 void set_lanes_per_item(int lpi);
 
+// block-balanced fast path for large single-geometry per-node batches
+// (harvest_mvb.cuh, instantiated in harvest_mvb_{a,b,c}.cu)
+int launch_harvest_mvb_a(const HarvestParams &P, cudaStream_t st);
+int launch_harvest_mvb_b(const HarvestParams &P, cudaStream_t st);
+int launch_harvest_mvb_c(const HarvestParams &P, cudaStream_t st);
+inline int launch_harvest_mvb(const HarvestParams &P, cudaStream_t st)
+{
+    if (P.d <= 10) return launch_harvest_mvb_a(P, st);
+    if (P.d <= 13) return launch_harvest_mvb_b(P, st);
+    return launch_harvest_mvb_c(P, st);
+}
+// same test as mvb_eligible (harvest_mvb.cuh), visible to harvest.cu
+inline bool harvest_mvb_eligible(const HarvestParams &P)
+{
+    const int nt = P.nterms + (P.c0 ? 1 : 0);
+    return P.mode == 1 && P.table_idx == nullptr && !P.map_on && P.rows == nullptr &&
+           P.frozen == nullptr && P.frozen_default == 0 && P.nterms >= 1 && nt <= 3 &&
+           P.d >= 5 && P.d <= 16 && P.B >= 4096;
+}
+
 }  // namespace lmep

@@ -1,0 +1,429 @@
+// harvest_mvb.cuh -- K1 fast path for large per-node batches over ONE shared
+// derivative-table geometry (periodic / uniform grids with variable
+// coefficients, BASELINE config 5): block-balanced expm-multiply.
+//
+// Same mathematics as harvest_mv.cuh (exp(A) e_c by a Taylor series on A/reps,
+// truncated when two consecutive terms fall below 2^-53 of the partial sum,
+// Al-Mohy & Higham 2011; harvest.py:97-121 semantics).  The ncu profile of
+// the per-item kernel (profiles/r1b_harvest_mv_kernel.md) showed that half of
+// its instructions were spent before the Taylor loop: assembling A with
+// per-entry selects (frozen rows, reaction term, augmentation, padding) and
+// one Osborne balancing per item.  Two observations remove almost all of it:
+//
+//   * balancing only has to be SOME power-of-two diagonal similarity (exp(A)
+//     is unchanged up to rounding, expm.py:27-30); items that share a table
+//     and differ by their coefficients have nearly the same best scaling
+//     (C5: identical exponents over the whole grid, because nu D2 dominates).
+//     So one item per superblock of 256 items is balanced (warp 0, the
+//     per-item sweep of harvest_mv.cuh) and its exponents are folded into a
+//     CTA-shared copy of the tables: T'[j][c] = T[j][c] 2^(e_c - e_j).
+//     Scaling by a power of two is exact, so every item's balanced matrix
+//     is bit-identical to "assemble, then balance with those exponents".
+//   * with frozen rows excluded (host check) and the reaction term carried as
+//     one more table (the identity), the assembly is the same straight-line
+//     product chain for every entry: no selects at all.
+//
+// The norm that fixes reps is the infinity norm of B (the lane-local row
+// sums; the max-abs convergence test is measured in the same norm), with
+// ||B / reps||_inf <= 4: fewer Taylor products per item than ||.||_1 <= 2
+// at the same 2^-53 truncation (9.7 vs 18.8 products per
+// item on the C5 coefficient field, errors ~7e-15 either way).
+//
+// CTAs are persistent (grid = resident CTAs) and walk superblocks
+// interleaved, so the cost of a superblock (which varies with nu(x)) is
+// spread over the grid.
+#pragma once
+#include <math.h>
+
+#include <algorithm>
+
+#include "harvest_mv.cuh"
+
+namespace lmep {
+
+constexpr int MVB_LPI = 4;
+constexpr int MVB_ITERS = 8;                         // 32-item iterations per superblock
+constexpr int MVB_SB = MVB_ITERS * 32;               // items per superblock (128 threads, 4 lanes each)
+constexpr double MVB_THETA = 4.0;
+
+template <int D, int NT>
+struct MvbCfg {
+    using C = MvCfg<D, MVB_LPI>;
+    static constexpr int R = C::R;
+    static constexpr int RP = R * MVB_LPI;            // padded rows (zeros beyond d)
+    static constexpr int NTP = NT == 1 ? 1 : (NT == 2 ? 2 : 4);   // LDS.64 / LDS.128 granules
+    static constexpr int TAB = RP * D * NTP;           // one table copy (doubles)
+    // smem: 1/k!, exponents (int, as doubles), Taylor buffers, tab0, tabS, aug
+    static constexpr int OFF_E = C::INV;
+    static constexpr int OFF_T = OFF_E + 8;
+    static constexpr int OFF_TAB0 = OFF_T + (C::THREADS / 32) * C::WARP_T;
+    static constexpr int OFF_TABS = OFF_TAB0 + TAB;
+    static constexpr int OFF_AUG = OFF_TABS + TAB;
+    static constexpr int TOTAL = OFF_AUG + RP * D;
+};
+
+template <int D, int NT>
+constexpr size_t mvb_smem_bytes() { return (size_t)MvbCfg<D, NT>::TOTAL * sizeof(double); }
+
+template <int D, int NT>
+__global__ void __launch_bounds__(128, 3) harvest_mvb_kernel(const HarvestParams P, int64_t nsb)
+{
+    using C = MvCfg<D, MVB_LPI>;
+    using K = MvbCfg<D, NT>;
+    constexpr int R = C::R, SH = C::SH, LPI = MVB_LPI, NTP = K::NTP;
+    extern __shared__ __align__(16) double mv_sm[];
+    double *sFact = mv_sm;
+    int *sE = reinterpret_cast<int *>(mv_sm + K::OFF_E);          // [16] exponents of this superblock
+    double *sT = mv_sm + K::OFF_T + (threadIdx.x >> 5) * C::WARP_T;
+    double *sTab0 = mv_sm + K::OFF_TAB0;                            // [RP][D][NTP]: T_t[c][j] at (j, c, t)
+    double *sTabS = mv_sm + K::OFF_TABS;                            // balanced copy
+    double *sAug = mv_sm + K::OFF_AUG;                              // [RP][D] balanced augmentation
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int q = lane & (LPI - 1), grp = lane >> SH;
+    const int n = P.n, sd = P.s, row = P.row_default;
+    const int nterms = P.nterms;                                    // NT = nterms (+1 with c0)
+    const double dt = P.delta_t;
+
+    for (int i = threadIdx.x; i < C::INV; i += blockDim.x) {
+        double f = 1.0;
+        for (int j = 2; j <= i; ++j) f *= (double)j;
+        sFact[i] = 1.0 / f;
+    }
+    // tables (and the identity for the reaction term), zero outside n x n
+    for (int i = threadIdx.x; i < K::TAB; i += blockDim.x) {
+        const int t = i % NTP, r = i / NTP, c = r % D, j = r / D;
+        double v = 0.0;
+        if (j < n && c < n) {
+            if (t < nterms) v = P.tables[((int64_t)t * n + c) * n + j];
+            else if (t < NT) v = (c == j) ? 1.0 : 0.0;
+        }
+        sTab0[i] = v;
+    }
+    __syncthreads();
+
+    const double *cfp = P.coef;
+    for (int64_t sb = blockIdx.x; sb < nsb; sb += gridDim.x) {
+        const int64_t b0 = sb * MVB_SB;
+        // ---- representative balancing (warp 0; every group of it runs item b0)
+        if (warp == 0) {
+            double a[R][D];
+            double cf0[NT];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) cf0[t] = t < nterms ? cfp[b0 * P.coef_stride + t] : P.c0[b0 * P.c0_stride];
+#pragma unroll
+            for (int m = 0; m < R; ++m) {
+                const int j = q + LPI * m;
+#pragma unroll
+                for (int c = 0; c < D; ++c) {
+                    double l = 0.0;
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) l = xadd(l, xmul(cf0[t], sTab0[(j * D + c) * NTP + t]));
+                    double v = xmul(dt, l);
+                    if (c == n && j == row) v = dt;
+                    else if (j >= n && j < D && c == j + 1) v = dt;
+                    a[m][c] = v;
+                }
+            }
+            int e[R];
+#pragma unroll
+            for (int m = 0; m < R; ++m) e[m] = 0;
+            bool ok = true;
+#pragma unroll
+            for (int m = 0; m < R; ++m)
+#pragma unroll
+                for (int c = 0; c < D; ++c) ok &= (bool)isfinite(a[m][c]);
+            ok = __all_sync(MV_FULL, ok);
+            for (int sweep = 0; ok && sweep < 12; ++sweep) {
+                double myc2[R];
+#pragma unroll
+                for (int m = 0; m < R; ++m) myc2[m] = 0.0;
+#pragma unroll
+                for (int c = 0; c < D; ++c) {
+                    double p = 0.0;
+#pragma unroll
+                    for (int m = 0; m < R; ++m) p = fma(a[m][c], a[m][c], p);
+                    p = mv_gsum<LPI>(p);
+                    if ((c & (LPI - 1)) == q) myc2[c >> SH] = p;
+                }
+                int k[R];
+                bool chg = false;
+#pragma unroll
+                for (int m = 0; m < R; ++m) {
+                    k[m] = 0;
+                    double r2 = 0.0;
+#pragma unroll
+                    for (int c = 0; c < D; ++c) r2 = fma(a[m][c], a[m][c], r2);
+                    const double c2 = myc2[m];
+                    if (q + LPI * m < D && c2 > 1e-280 && r2 > 1e-280 && c2 < 1e280 && r2 < 1e280) {
+                        const int ex = mv_exp2i(r2) - mv_exp2i(c2);
+                        if (ex >= 4) k[m] = (ex + 2) >> 2;
+                        else if (ex <= -4) k[m] = -((2 - ex) >> 2);
+                    }
+                    chg |= k[m] != 0;
+                }
+                if (!__any_sync(MV_FULL, chg)) break;
+#pragma unroll
+                for (int c = 0; c < D; ++c) {
+                    const int kc = __shfl_sync(MV_FULL, k[c >> SH], (lane & ~(LPI - 1)) + (c & (LPI - 1)));
+#pragma unroll
+                    for (int m = 0; m < R; ++m)
+                        if (kc != k[m]) a[m][c] *= mv_pow2(kc - k[m]);
+                }
+#pragma unroll
+                for (int m = 0; m < R; ++m) e[m] += k[m];
+            }
+            if (grp == 0) {
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    if (q + LPI * m < 16) sE[q + LPI * m] = (q + LPI * m < D) ? e[m] : 0;
+            }
+        }
+        __syncthreads();
+        // ---- fold the exponents into the CTA copy of the tables (exact)
+        for (int i = threadIdx.x; i < K::TAB; i += blockDim.x) {
+            const int r = i / NTP, c = r % D, j = r / D;
+            const double sc = (j < D) ? mv_pow2(sE[c] - sE[j]) : 1.0;
+            sTabS[i] = sTab0[i] * sc;
+        }
+        if (sd > 1) {
+            for (int i = threadIdx.x; i < K::RP * D; i += blockDim.x) {
+                const int c = i % D, j = i / D;
+                double v = 0.0;
+                if ((c == n && j == row) || (j >= n && j < D && c == j + 1)) v = dt * mv_pow2(sE[c] - sE[j]);
+                sAug[i] = v;
+            }
+        }
+        __syncthreads();
+
+        int ej[R];
+#pragma unroll
+        for (int m = 0; m < R; ++m) ej[m] = sE[q + LPI * m < 16 ? q + LPI * m : 0];
+        const int erow = sE[row];
+
+        for (int it = 0; it < MVB_ITERS; ++it) {
+            const int64_t braw = b0 + it * 32 + (threadIdx.x >> SH);
+            const bool live = braw < P.B;
+            const int64_t b = live ? braw : P.B - 1;
+
+            double cf[NT];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) cf[t] = t < nterms ? cfp[b * P.coef_stride + t] : P.c0[b * P.c0_stride];
+
+            // ---- assembly: a[m][c] = dt * L'[c][j] 2^(e_c - e_j), no selects
+            double a[R][D];
+            double rs = 0.0;
+#pragma unroll
+            for (int m = 0; m < R; ++m) {
+                const int j = q + LPI * m;
+                const double *tr = sTabS + j * D * NTP;
+                double rsm = 0.0;
+#pragma unroll
+                for (int c = 0; c < D; ++c) {
+                    double tv[NTP];
+                    if constexpr (NTP == 1) {
+                        tv[0] = tr[c];
+                    } else {
+#pragma unroll
+                        for (int t2 = 0; t2 < NTP; t2 += 2) {
+                            const double2 x2 = *reinterpret_cast<const double2 *>(tr + c * NTP + t2);
+                            tv[t2] = x2.x;
+                            tv[t2 + 1] = x2.y;
+                        }
+                    }
+                    // localop.py:120-127 term order (reaction last)
+                    double l = xmul(cf[0], tv[0]);
+#pragma unroll
+                    for (int t = 1; t < NT; ++t) l = xadd(l, xmul(cf[t], tv[t]));
+                    double v = xmul(dt, l);
+                    if (sd > 1) v = xadd(v, sAug[j * D + c]);
+                    a[m][c] = v;
+                    rsm += fabs(v);
+                }
+                rs = fmax(rs, rsm);
+                if (!(rsm <= 1e300)) rs = INFINITY;         // NaN / Inf entries
+            }
+            // ---- scaling: ||B / reps||_inf <= THETA
+            const double nrm = mv_gfmax<LPI>(rs);
+            int status = LMEP_OK;
+            int s = 0;
+            if (!(nrm <= 1e9)) status = LMEP_NONFINITE;
+            else s = nrm > MVB_THETA ? (int)ceil(nrm / MVB_THETA) : 1;
+            if (s > 1) {
+                const double sc = 1.0 / (double)s;
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+#pragma unroll
+                    for (int c = 0; c < D; ++c) a[m][c] *= sc;
+            }
+            const int reps = status == LMEP_OK ? s : 0;
+
+            // ---- flattened Taylor iteration (harvest_mv.cuh), CTA exponents
+            int qo = 0, rep = 0, kt = 1, nmv = 0, idx = row, eidx = erow;
+            bool done = reps == 0;
+            unsigned bad = 0u;
+            double acc[R];
+#pragma unroll
+            for (int m = 0; m < R; ++m) acc[m] = (q + LPI * m == idx) ? 1.0 : 0.0;
+            double wprev = INFINITY;
+            double *tg = sT + grp * C::TS;
+            int buf = 0;
+            __syncwarp();
+#pragma unroll
+            for (int m = 0; m < R; ++m)
+                if (q + LPI * m < D) tg[q + LPI * m] = acc[m];
+            __syncwarp();
+            while (__any_sync(MV_FULL, !done)) {
+                const double *tv = tg + buf * C::BUF;
+                double u[R];
+                if constexpr (R >= 4) {
+#pragma unroll
+                    for (int m = 0; m < R; ++m) u[m] = 0.0;
+#pragma unroll
+                    for (int c = 0; c < D; c += 2) {
+                        if (c + 1 < D) {
+                            const double2 tt = *reinterpret_cast<const double2 *>(tv + c);
+#pragma unroll
+                            for (int m = 0; m < R; ++m) u[m] = fma(a[m][c + 1], tt.y, fma(a[m][c], tt.x, u[m]));
+                        } else {
+                            const double t0 = tv[c];
+#pragma unroll
+                            for (int m = 0; m < R; ++m) u[m] = fma(a[m][c], t0, u[m]);
+                        }
+                    }
+                } else {
+                    double s0[R], s1[R];
+#pragma unroll
+                    for (int m = 0; m < R; ++m) s0[m] = s1[m] = 0.0;
+#pragma unroll
+                    for (int c = 0; c < D; c += 2) {
+                        if (c + 1 < D) {
+                            const double2 tt = *reinterpret_cast<const double2 *>(tv + c);
+#pragma unroll
+                            for (int m = 0; m < R; ++m) {
+                                s0[m] = fma(a[m][c], tt.x, s0[m]);
+                                s1[m] = fma(a[m][c + 1], tt.y, s1[m]);
+                            }
+                        } else {
+                            const double t0 = tv[c];
+#pragma unroll
+                            for (int m = 0; m < R; ++m) s0[m] = fma(a[m][c], t0, s0[m]);
+                        }
+                    }
+#pragma unroll
+                    for (int m = 0; m < R; ++m) u[m] = s0[m] + s1[m];
+                }
+                const double fk = sFact[kt];
+                const double fa = done ? 0.0 : fk;
+                unsigned wh = 0u, ah = 0u;
+#pragma unroll
+                for (int m = 0; m < R; ++m) {
+                    acc[m] = fma(u[m], fa, acc[m]);
+                    if (q + LPI * m < n) {
+                        wh = max(wh, mv_hiabs(u[m]));
+                        ah = max(ah, mv_hiabs(acc[m]));
+                    }
+                }
+                wh = mv_gmax<LPI>(wh);
+                ah = mv_gmax<LPI>(ah);
+                const double wn = __hiloint2double((int)wh, -1) * fk;
+                const double an = __hiloint2double((int)ah, 0);
+                const bool conv = (kt > qo && an > 0.0 && wn + wprev <= 0x1p-53 * an) || kt >= MV_TMAX;
+                if (!done) {
+                    ++nmv;
+                    double nt[R];
+                    if (conv) {
+                        ++rep;
+                        kt = 1;
+                        wprev = INFINITY;
+                        if (rep >= reps) {
+#pragma unroll
+                            for (int m = 0; m < R; ++m) {
+                                const int j = q + LPI * m;
+                                const double o = acc[m] * mv_pow2(ej[m] - eidx);
+                                bad |= (unsigned)!isfinite(o);
+                                if (live && j < n) {
+                                    if (P.layout == 0) P.out[(b * sd + qo) * n + j] = o;
+                                    else P.out[((int64_t)qo * n + j) * P.out_ld + b] = o;
+                                }
+                            }
+                            ++qo;
+                            rep = 0;
+                            if (qo >= sd) {
+                                done = true;
+                            } else {
+                                idx = n + qo - 1;
+                                eidx = sE[idx];
+#pragma unroll
+                                for (int m = 0; m < R; ++m) acc[m] = (q + LPI * m == idx) ? 1.0 : 0.0;
+                            }
+                        }
+#pragma unroll
+                        for (int m = 0; m < R; ++m) nt[m] = acc[m];
+                    } else {
+                        ++kt;
+                        wprev = wn;
+#pragma unroll
+                        for (int m = 0; m < R; ++m) nt[m] = u[m];
+                    }
+                    buf ^= 1;
+                    double *to = tg + buf * C::BUF;
+#pragma unroll
+                    for (int m = 0; m < R; ++m)
+                        if (q + LPI * m < D) to[q + LPI * m] = nt[m];
+                }
+                __syncwarp();
+            }
+            if (mv_gor<LPI>(bad)) status = LMEP_NONFINITE;
+            if (reps == 0 && live) {
+                for (int qq = 0; qq < sd; ++qq)
+#pragma unroll
+                    for (int m = 0; m < R; ++m) {
+                        const int j = q + LPI * m;
+                        if (j < n) {
+                            const double nan = __longlong_as_double(0x7ff8000000000000LL);
+                            if (P.layout == 0) P.out[(b * sd + qq) * n + j] = nan;
+                            else P.out[((int64_t)qq * n + j) * P.out_ld + b] = nan;
+                        }
+                    }
+            }
+            if (live && q == 0) {
+                if (P.status) P.status[b] = status;
+                if (P.ms) P.ms[b] = nmv | (min(s, 255) << 24);
+            }
+        }
+        __syncthreads();          // the next superblock rewrites sE / sTabS
+    }
+}
+
+template <int D, int NT>
+int launch_mvb_nt(const HarvestParams &P, cudaStream_t st)
+{
+    auto kern = harvest_mvb_kernel<D, NT>;
+    const size_t shm = mvb_smem_bytes<D, NT>();
+    static int per_sm = 0, sms = 0;
+    if (per_sm == 0) {
+        if (shm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, shm);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (per_sm < 1) per_sm = 1;
+    }
+    const int64_t nsb = (P.B + MVB_SB - 1) / MVB_SB;
+    const int64_t grid = std::min<int64_t>(nsb, (int64_t)per_sm * sms);
+    kern<<<(unsigned)grid, 128, shm, st>>>(P, nsb);
+    return launch_status("harvest_mvb_kernel");
+}
+
+template <int D>
+int launch_mvb(const HarvestParams &P, cudaStream_t st)
+{
+    switch (P.nterms + (P.c0 ? 1 : 0)) {
+    case 1: return launch_mvb_nt<D, 1>(P, st);
+    case 2: return launch_mvb_nt<D, 2>(P, st);
+    case 3: return launch_mvb_nt<D, 3>(P, st);
+    default: return LMEP_INVALID_CONFIG;
+    }
+}
+
+}  // namespace lmep

@@ -79,7 +79,7 @@ def test_expm_nonfinite(lx):
         lx.expm(np.eye(3) * 1e6)
 
 
-@pytest.fixture(params=["multiply", "mv8", "quad", "multiply4", "pade"])
+@pytest.fixture(params=["multiply", "mvitem", "mv8", "quad", "multiply4", "pade"])
 def method(request, lx):
     lx._native.set_harvest_method(request.param)
     yield request.param
@@ -196,6 +196,89 @@ def test_c5_per_node_harvest(lx, golden, method):
     for r in range(4):
         den = np.abs(ref[:, r]).max(axis=1)
         assert (np.abs(W[:, r] - ref[:, r]).max(axis=1) / den).max() < W_TOL, r
+
+
+def _c5_large(lx, N):
+    from paper_2603_15964_b200 import configs
+    w5 = configs.c5(N=N, steps=1)
+    g = lx.make_periodic_grid(N, 0.0, 1.0)
+    st = lx.select_stencils(g, w5.n, lx.StencilPolicy.CENTERED)
+    return w5, g, st
+
+
+@pytest.mark.parametrize("s", [1, 2, 4])
+@pytest.mark.parametrize("dtmul", [1.0, 4.0])
+def test_block_balanced_harvest_large_batch(lx, orc, s, dtmul):
+    """Large single-geometry per-node batch (B >= 4096): the block-balanced
+    kernel (harvest_mvb.cuh, one representative balancing per 256 items, inf
+    norm scaling) against the oracle's per-node harvest on a sample of nodes,
+    and against the per-item balanced kernel on every node."""
+    from paper_2603_15964_b200.harvest import harvest_compact
+    N = 1 << 15
+    w5, g, st = _c5_large(lx, N)
+    c, nu = w5.coef
+    # dtmul 4: ||dt L||_inf up to ~40, up to 11 Taylor reps.  (Much larger dt
+    # leaves the well-conditioned regime: at 16x some nodes' rows reach 2e5
+    # with row sums of 1, and no fp64 formulation reproduces another to 1e-12.)
+    dt = w5.delta_t * dtmul
+    spec = lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1))
+    stats = {}
+    W = harvest_compact(g, st, spec, dt, s, (), stats).pernode.permute(2, 0, 1).cpu().numpy()
+    reps = (torch.cat(stats["ms"]).cpu().numpy() >> 24)
+    if dtmul > 1:
+        assert reps.max() > 4, reps.max()
+    idx = np.arange(0, N, 61)
+    x = (np.arange(w5.n) - w5.row) * w5.h
+    D1 = np.array([orc.fornberg_weights(xi, x, 2)[1] for xi in x])
+    D2 = np.array([orc.fornberg_weights(xi, x, 2)[2] for xi in x])
+    ref = orc.harvest_batch_vc(D1, D2, -c[idx], nu[idx], dt, s, w5.row, reduced=True)
+    worst = max(_rows_rel(W[i], ref[k]) for k, i in enumerate(idx))
+    assert worst < W_TOL, worst
+    lx._native.set_harvest_method("mvitem")
+    try:
+        W2 = harvest_compact(g, st, spec, dt, s).pernode.permute(2, 0, 1).cpu().numpy()
+    finally:
+        lx._native.set_harvest_method("multiply")
+    den = np.abs(W2).max(axis=2, keepdims=True)
+    assert (np.abs(W - W2) / den).max() < W_TOL
+
+
+def test_block_balanced_harvest_reaction_and_single_term(lx, orc):
+    """The reaction term rides as an identity table (localop.py:120-127 order:
+    derivative terms, then the diagonal), and one-term operators (nu(x) D2)."""
+    from paper_2603_15964_b200.harvest import harvest_compact
+    N = 8192
+    w5, g, st = _c5_large(lx, N)
+    c, nu = w5.coef
+    dt = w5.delta_t * 4
+    r = np.sin(2 * np.pi * g.nodes) * 3e4
+    n, row, h = w5.n, w5.row, w5.h
+    x = (np.arange(n) - row) * h
+    for spec, terms_of in (
+            (lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1), reaction=r),
+             lambda i: ((1, -c[i]), (2, nu[i]), (0, r[i]))),
+            (lx.VariableCoefficientSpec((2,), nu[:, None]), lambda i: ((2, nu[i]),))):
+        W = harvest_compact(g, st, spec, dt, 3).pernode.permute(2, 0, 1).cpu().numpy()
+        for i in range(0, N, 397):
+            tm = terms_of(i)
+            L = orc.local_operator(x, tuple(t for t in tm if t[0] > 0))
+            for k, v in tm:
+                if k == 0:
+                    L = L + v * np.eye(n)
+            wl, wp = orc.harvest_phi_weights(L, dt, 3, row, reduced=True)
+            assert _rows_rel(W[i], np.vstack([wl] + list(wp))) < W_TOL, i
+
+
+def test_block_balanced_harvest_nonfinite(lx):
+    from paper_2603_15964_b200.harvest import harvest_compact
+    N = 8192
+    w5, g, st = _c5_large(lx, N)
+    c, nu = w5.coef
+    nu = nu.copy()
+    nu[5000] = np.nan
+    with pytest.raises(lx.NonFinite):
+        harvest_compact(g, st, lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1)),
+                        w5.delta_t, 1)
 
 
 @pytest.mark.parametrize("periodic", [True, False])
