@@ -119,7 +119,7 @@ def peaks():
 
 def traffic(kernel, key, units):
     """Per-launch DRAM bytes scaled from the committed ncu capture (profiles/)."""
-    p = os.path.join(REPO, "profiles", "r1_traffic.json")
+    p = os.path.join(REPO, "profiles", "traffic.json")
     try:
         return json.load(open(p))[kernel][key] * units
     except (OSError, KeyError, ValueError):
@@ -416,7 +416,8 @@ def main():
         ks = [min(kb, w.steps - i * kb) for i in range(launches_steps)]
         step_bytes_total = sum(bench.nloc * (8 * w.n + 8) * (pl["tile"] + k * (w.n - 1)) /
                                pl["tile"] + bench.nloc * 8 for k in ks)
-        step_kernel = f"lin_pernode_tb_kernel<13,3> (rows in registers, k={kb} steps/launch)"
+        step_kernel = (f"lin_pernode_tma_kernel<13,3> (persistent, TMA-pipelined; rows in registers, "
+                       f"k={kb} steps/launch)")
         per_launch_ms = step_ms / launches_steps
         step_bytes = step_bytes_total / launches_steps
     else:
@@ -462,10 +463,11 @@ def main():
                           "per_step_launch_ms": per_launch_ms},
             # the dominant kernel of the pass (ncu launch list: ~80% of device time) is
             # the FP64-bound harvest; the HBM-bound step kernel follows as roofline_step
-            "roofline": {"bound": "fp64", "kernel": "harvest_mv_kernel<13> (per-node expm-multiply, 13x13)",
+            "roofline": {"bound": "fp64",
+                         "kernel": "harvest_mvb_kernel<13,2,4> (block-balanced per-node expm-multiply, 13x13)",
                          "achieved": harvest_tflops, "peak": fp64, "unit": "TFLOP/s",
                          "frac": harvest_tflops / fp64,
-                         "traffic": traffic("harvest_mv_kernel<13>", "bytes_per_item", bench.nloc),
+                         "traffic": traffic("harvest_mvb_kernel<13,2,4>", "bytes_per_item", bench.nloc),
                          "algorithmic_flops_per_launch": flops,
                          "peak_kind": "measured DFMA chains (tools/fp64_peak.cu), this run"},
             "roofline_step": {"bound": "hbm", "kernel": step_kernel,
@@ -475,6 +477,13 @@ def main():
                                                  bench.nloc),
                               "algorithmic_bytes_per_launch": step_bytes,
                               "peak_kind": f"{hbm_kind} (MEASURED_PEAKS.json hbm_gbs)"},
+            # the blocked step kernel is no longer HBM-bound: it issues the reference's
+            # unfused multiply + add per tap (2n flops per point-step, kernels.py:23-29),
+            # so its ceiling is the FP64 pipe at one op per lane per issue = fp64 / 2
+            "roofline_step_fp64": {"bound": "fp64 (unfused mul+add)", "kernel": step_kernel,
+                                   "achieved": 2 * w.n * w.N * w.steps / (step_ms * 1e-3) / 1e12,
+                                   "peak": fp64 / 2, "unit": "TFLOP/s",
+                                   "frac": 2 * w.n * w.N * w.steps / (step_ms * 1e-3) / 1e12 / (fp64 / 2)},
             "e2e": {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": bench.h2d_bytes,
                     "d2h_bytes_per_step": bench.d2h_bytes},
             "gpu_launches": launches,

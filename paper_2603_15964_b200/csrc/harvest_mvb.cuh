@@ -41,16 +41,19 @@
 
 namespace lmep {
 
-constexpr int MVB_LPI = 4;
-constexpr int MVB_ITERS = 8;                         // 32-item iterations per superblock
-constexpr int MVB_SB = MVB_ITERS * 32;               // items per superblock (128 threads, 4 lanes each)
+constexpr int MVB_ITERS = 8;                         // CTA iterations per superblock
+template <int LPI>
+constexpr int mvb_sb() { return MVB_ITERS * (128 / LPI); }   // items per superblock
 constexpr double MVB_THETA = 4.0;
+#ifndef MVB_MINB
+#define MVB_MINB 3
+#endif
 
-template <int D, int NT>
+template <int D, int NT, int LPI>
 struct MvbCfg {
-    using C = MvCfg<D, MVB_LPI>;
+    using C = MvCfg<D, LPI>;
     static constexpr int R = C::R;
-    static constexpr int RP = R * MVB_LPI;            // padded rows (zeros beyond d)
+    static constexpr int RP = R * LPI;                // padded rows (zeros beyond d)
     static constexpr int NTP = NT == 1 ? 1 : (NT == 2 ? 2 : 4);   // LDS.64 / LDS.128 granules
     static constexpr int TAB = RP * D * NTP;           // one table copy (doubles)
     // smem: 1/k!, exponents (int, as doubles), Taylor buffers, tab0, tabS, aug
@@ -59,18 +62,20 @@ struct MvbCfg {
     static constexpr int OFF_TAB0 = OFF_T + (C::THREADS / 32) * C::WARP_T;
     static constexpr int OFF_TABS = OFF_TAB0 + TAB;
     static constexpr int OFF_AUG = OFF_TABS + TAB;
-    static constexpr int TOTAL = OFF_AUG + RP * D;
+    static constexpr int OFF_RS = OFF_AUG + RP * D;     // [NT][RP] row |.|-sums of tabS, [RP] of aug
+    static constexpr int TOTAL = OFF_RS + (NT + 1) * RP;
 };
 
-template <int D, int NT>
-constexpr size_t mvb_smem_bytes() { return (size_t)MvbCfg<D, NT>::TOTAL * sizeof(double); }
+template <int D, int NT, int LPI>
+constexpr size_t mvb_smem_bytes() { return (size_t)MvbCfg<D, NT, LPI>::TOTAL * sizeof(double); }
 
-template <int D, int NT>
-__global__ void __launch_bounds__(128, 3) harvest_mvb_kernel(const HarvestParams P, int64_t nsb)
+template <int D, int NT, int LPI>
+__global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : 4) harvest_mvb_kernel(const HarvestParams P, int64_t nsb)
 {
-    using C = MvCfg<D, MVB_LPI>;
-    using K = MvbCfg<D, NT>;
-    constexpr int R = C::R, SH = C::SH, LPI = MVB_LPI, NTP = K::NTP;
+    using C = MvCfg<D, LPI>;
+    using K = MvbCfg<D, NT, LPI>;
+    constexpr int R = C::R, SH = C::SH, NTP = K::NTP;
+    constexpr int GC = 128 / LPI;                                   // items per CTA iteration
     extern __shared__ __align__(16) double mv_sm[];
     double *sFact = mv_sm;
     int *sE = reinterpret_cast<int *>(mv_sm + K::OFF_E);          // [16] exponents of this superblock
@@ -78,6 +83,7 @@ __global__ void __launch_bounds__(128, 3) harvest_mvb_kernel(const HarvestParams
     double *sTab0 = mv_sm + K::OFF_TAB0;                            // [RP][D][NTP]: T_t[c][j] at (j, c, t)
     double *sTabS = mv_sm + K::OFF_TABS;                            // balanced copy
     double *sAug = mv_sm + K::OFF_AUG;                              // [RP][D] balanced augmentation
+    double *sRS = mv_sm + K::OFF_RS;                                // row abs-sum bounds
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int q = lane & (LPI - 1), grp = lane >> SH;
     const int n = P.n, sd = P.s, row = P.row_default;
@@ -103,7 +109,7 @@ __global__ void __launch_bounds__(128, 3) harvest_mvb_kernel(const HarvestParams
 
     const double *cfp = P.coef;
     for (int64_t sb = blockIdx.x; sb < nsb; sb += gridDim.x) {
-        const int64_t b0 = sb * MVB_SB;
+        const int64_t b0 = sb * mvb_sb<LPI>();
         // ---- representative balancing (warp 0; every group of it runs item b0)
         if (warp == 0) {
             double a[R][D];
@@ -185,6 +191,21 @@ __global__ void __launch_bounds__(128, 3) harvest_mvb_kernel(const HarvestParams
             const double sc = (j < D) ? mv_pow2(sE[c] - sE[j]) : 1.0;
             sTabS[i] = sTab0[i] * sc;
         }
+        // per-row abs sums of every balanced table and of the augmentation:
+        // ||B||_inf <= dt max_j sum_t |cf_t| RS_t[j] + RA[j] (triangle inequality)
+        for (int i = threadIdx.x; i < (NT + 1) * K::RP; i += blockDim.x) {
+            const int t = i / K::RP, j = i % K::RP;
+            double sum = 0.0;
+            if (j < D) {
+#pragma unroll 1
+                for (int c = 0; c < D; ++c) {
+                    const double sc = mv_pow2(sE[c] - sE[j]);
+                    if (t < NT) sum += fabs(sTab0[(j * D + c) * NTP + t]) * sc;
+                    else if (sd > 1 && ((c == n && j == row) || (j >= n && c == j + 1))) sum += fabs(dt) * sc;
+                }
+            }
+            sRS[i] = sum;
+        }
         if (sd > 1) {
             for (int i = threadIdx.x; i < K::RP * D; i += blockDim.x) {
                 const int c = i % D, j = i / D;
@@ -201,7 +222,7 @@ __global__ void __launch_bounds__(128, 3) harvest_mvb_kernel(const HarvestParams
         const int erow = sE[row];
 
         for (int it = 0; it < MVB_ITERS; ++it) {
-            const int64_t braw = b0 + it * 32 + (threadIdx.x >> SH);
+            const int64_t braw = b0 + it * GC + (threadIdx.x >> SH);
             const bool live = braw < P.B;
             const int64_t b = live ? braw : P.B - 1;
 
@@ -209,14 +230,31 @@ __global__ void __launch_bounds__(128, 3) harvest_mvb_kernel(const HarvestParams
 #pragma unroll
             for (int t = 0; t < NT; ++t) cf[t] = t < nterms ? cfp[b * P.coef_stride + t] : P.c0[b * P.c0_stride];
 
-            // ---- assembly: a[m][c] = dt * L'[c][j] 2^(e_c - e_j), no selects
+            // ---- scaling: ||B / reps||_inf <= THETA, from the row-sum bounds.  A
+            // NaN coefficient, or entries that overflow, make the bound non-finite.
+            double rb = 0.0;
+#pragma unroll
+            for (int m = 0; m < R; ++m) {
+                const int j = q + LPI * m;
+                double r = 0.0;
+#pragma unroll
+                for (int t = 0; t < NT; ++t) r = fma(fabs(cf[t]), sRS[t * K::RP + j], r);
+                r = fma(fabs(dt), r, sRS[NT * K::RP + j]);
+                rb = (r > rb || r != r) ? r : rb;
+            }
+            const double nrm = mv_gfmax<LPI>(rb != rb ? INFINITY : rb);
+            int status = LMEP_OK;
+            int s = 0;
+            if (!(nrm <= 1e9)) status = LMEP_NONFINITE;
+            else s = nrm > MVB_THETA ? (int)ceil(nrm / MVB_THETA) : 1;
+            const double sc = 1.0 / (double)max(s, 1);
+
+            // ---- assembly: a[m][c] = dt * L'[c][j] 2^(e_c - e_j) (/ reps), no selects
             double a[R][D];
-            double rs = 0.0;
 #pragma unroll
             for (int m = 0; m < R; ++m) {
                 const int j = q + LPI * m;
                 const double *tr = sTabS + j * D * NTP;
-                double rsm = 0.0;
 #pragma unroll
                 for (int c = 0; c < D; ++c) {
                     double tv[NTP];
@@ -236,24 +274,9 @@ __global__ void __launch_bounds__(128, 3) harvest_mvb_kernel(const HarvestParams
                     for (int t = 1; t < NT; ++t) l = xadd(l, xmul(cf[t], tv[t]));
                     double v = xmul(dt, l);
                     if (sd > 1) v = xadd(v, sAug[j * D + c]);
+                    if (s > 1) v *= sc;
                     a[m][c] = v;
-                    rsm += fabs(v);
                 }
-                rs = fmax(rs, rsm);
-                if (!(rsm <= 1e300)) rs = INFINITY;         // NaN / Inf entries
-            }
-            // ---- scaling: ||B / reps||_inf <= THETA
-            const double nrm = mv_gfmax<LPI>(rs);
-            int status = LMEP_OK;
-            int s = 0;
-            if (!(nrm <= 1e9)) status = LMEP_NONFINITE;
-            else s = nrm > MVB_THETA ? (int)ceil(nrm / MVB_THETA) : 1;
-            if (s > 1) {
-                const double sc = 1.0 / (double)s;
-#pragma unroll
-                for (int m = 0; m < R; ++m)
-#pragma unroll
-                    for (int c = 0; c < D; ++c) a[m][c] *= sc;
             }
             const int reps = status == LMEP_OK ? s : 0;
 
@@ -273,24 +296,16 @@ __global__ void __launch_bounds__(128, 3) harvest_mvb_kernel(const HarvestParams
                 if (q + LPI * m < D) tg[q + LPI * m] = acc[m];
             __syncwarp();
             while (__any_sync(MV_FULL, !done)) {
+                // group max of |acc| before this term: its shuffles overlap the products
+                unsigned ah = 0u;
+#pragma unroll
+                for (int m = 0; m < R; ++m)
+                    if (q + LPI * m < n) ah = max(ah, mv_hiabs(acc[m]));
+                ah = mv_gmax<LPI>(ah);
                 const double *tv = tg + buf * C::BUF;
                 double u[R];
-                if constexpr (R >= 4) {
-#pragma unroll
-                    for (int m = 0; m < R; ++m) u[m] = 0.0;
-#pragma unroll
-                    for (int c = 0; c < D; c += 2) {
-                        if (c + 1 < D) {
-                            const double2 tt = *reinterpret_cast<const double2 *>(tv + c);
-#pragma unroll
-                            for (int m = 0; m < R; ++m) u[m] = fma(a[m][c + 1], tt.y, fma(a[m][c], tt.x, u[m]));
-                        } else {
-                            const double t0 = tv[c];
-#pragma unroll
-                            for (int m = 0; m < R; ++m) u[m] = fma(a[m][c], t0, u[m]);
-                        }
-                    }
-                } else {
+                {
+                    // two chains per row (even / odd columns): 2R independent DFMA chains
                     double s0[R], s1[R];
 #pragma unroll
                     for (int m = 0; m < R; ++m) s0[m] = s1[m] = 0.0;
@@ -314,20 +329,21 @@ __global__ void __launch_bounds__(128, 3) harvest_mvb_kernel(const HarvestParams
                 }
                 const double fk = sFact[kt];
                 const double fa = done ? 0.0 : fk;
-                unsigned wh = 0u, ah = 0u;
+                unsigned wh = 0u;
 #pragma unroll
                 for (int m = 0; m < R; ++m) {
                     acc[m] = fma(u[m], fa, acc[m]);
-                    if (q + LPI * m < n) {
-                        wh = max(wh, mv_hiabs(u[m]));
-                        ah = max(ah, mv_hiabs(acc[m]));
-                    }
+                    if (q + LPI * m < n) wh = max(wh, mv_hiabs(u[m]));
                 }
-                wh = mv_gmax<LPI>(wh);
-                ah = mv_gmax<LPI>(ah);
-                const double wn = __hiloint2double((int)wh, -1) * fk;
-                const double an = __hiloint2double((int)ah, 0);
-                const bool conv = (kt > qo && an > 0.0 && wn + wprev <= 0x1p-53 * an) || kt >= MV_TMAX;
+                // every lane tests its own rows against the group scale; the group
+                // converges when all its lanes pass (one ballot instead of a
+                // shuffle reduction on the critical path)
+                const double wn = __hiloint2double((int)wh, -1) * fk;   // >= max |u_k / k!| of this lane
+                const double an = __hiloint2double((int)ah, 0);          // <= group max |acc_{k-1}|
+                const bool pass = kt > qo && an > 0.0 && wn + wprev <= 0x1p-53 * an;
+                const unsigned bal = __ballot_sync(MV_FULL, pass);
+                const bool conv = ((bal >> (grp * LPI)) & ((1u << LPI) - 1u)) == ((1u << LPI) - 1u) ||
+                                  kt >= MV_TMAX;
                 if (!done) {
                     ++nmv;
                     double nt[R];
@@ -395,11 +411,11 @@ __global__ void __launch_bounds__(128, 3) harvest_mvb_kernel(const HarvestParams
     }
 }
 
-template <int D, int NT>
+template <int D, int NT, int LPI>
 int launch_mvb_nt(const HarvestParams &P, cudaStream_t st)
 {
-    auto kern = harvest_mvb_kernel<D, NT>;
-    const size_t shm = mvb_smem_bytes<D, NT>();
+    auto kern = harvest_mvb_kernel<D, NT, LPI>;
+    const size_t shm = mvb_smem_bytes<D, NT, LPI>();
     static int per_sm = 0, sms = 0;
     if (per_sm == 0) {
         if (shm > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
@@ -409,7 +425,7 @@ int launch_mvb_nt(const HarvestParams &P, cudaStream_t st)
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (per_sm < 1) per_sm = 1;
     }
-    const int64_t nsb = (P.B + MVB_SB - 1) / MVB_SB;
+    const int64_t nsb = (P.B + mvb_sb<LPI>() - 1) / mvb_sb<LPI>();
     const int64_t grid = std::min<int64_t>(nsb, (int64_t)per_sm * sms);
     kern<<<(unsigned)grid, 128, shm, st>>>(P, nsb);
     return launch_status("harvest_mvb_kernel");
@@ -419,9 +435,10 @@ template <int D>
 int launch_mvb(const HarvestParams &P, cudaStream_t st)
 {
     switch (P.nterms + (P.c0 ? 1 : 0)) {
-    case 1: return launch_mvb_nt<D, 1>(P, st);
-    case 2: return launch_mvb_nt<D, 2>(P, st);
-    case 3: return launch_mvb_nt<D, 3>(P, st);
+    case 1: return launch_mvb_nt<D, 1, 4>(P, st);
+    case 2: if (D == 13 && mv_lanes_override() == 8) return launch_mvb_nt<D, 2, 8>(P, st);
+            return launch_mvb_nt<D, 2, 4>(P, st);
+    case 3: return launch_mvb_nt<D, 3, 4>(P, st);
     default: return LMEP_INVALID_CONFIG;
     }
 }

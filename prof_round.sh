@@ -13,9 +13,9 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $O/bench_ref
 timeout 600 python bench.py --steps 1 --warmup 1 --no-others --no-cpu > $O/b_small.json 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
   python bench.py --steps 1 --warmup 1 --no-others --no-cpu > $O/ncu_launch.log 2>&1; echo "launches rc=$?"
-timeout 300 python tools/prof_cases.py harvest --reps 1 --N 1048576 > $O/h_plain.json 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:harvest_mv -s 1 -c 1 -o $O/harvest \
-  python tools/prof_cases.py harvest --reps 1 --N 1048576 > $O/ncu_h.log 2>&1; echo "ncu harvest rc=$?"
+timeout 300 python tools/prof_cases.py harvest --reps 1 --N 4194304 > $O/h_plain.json 2>&1 && \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:harvest_mvb -s 1 -c 1 -o $O/harvest \
+  python tools/prof_cases.py harvest --reps 1 --N 4194304 > $O/ncu_h.log 2>&1; echo "ncu harvest rc=$?"
 timeout 300 python tools/prof_cases.py c5step --reps 32 > $O/c5s_plain.json 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:lin_pernode_t -s 2 -c 1 -o $O/c5step \
   python tools/prof_cases.py c5step --reps 32 > $O/ncu_c5s.log 2>&1; echo "ncu c5step rc=$?"
