@@ -176,5 +176,5 @@ def set_harvest_method(method: str) -> None:
     expm per warp), or the first-generation kernel "quad" (8 lanes) /
     "multiply4" (4 lanes)."""
     code = {"multiply": 0, "auto": 0, "pade": 1, "multiply4": 2, "quad": 3, "mv8": 4,
-            "mvitem": 5, "mvb8": 6}[method]
+            "mvitem": 5, "mvb8": 6, "mvb2": 7, "mvb4": 8}[method]
     check(lib().lmep_set_harvest_method(code), "lmep_set_harvest_method")

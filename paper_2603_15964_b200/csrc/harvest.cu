@@ -790,14 +790,14 @@ extern "C" int lmep_harvest(int n, int s, int nterms, const double *tables,
 
 extern "C" int lmep_set_harvest_method(int method)
 {
-    if (method < 0 || method > 6) return LMEP_INVALID_CONFIG;
-    // 0 auto: block-balanced mv for large single-geometry batches, else mv (4 lanes per
-    // item); 1 pade; 2/3 quad (4 / 8 lanes); 4 per-item mv with 8 lanes for d > 8;
-    // 5 per-item mv (4 lanes) only
-    // 6 (experimental): auto with 8 lanes per item in the block-balanced kernel
-    lmep::g_mv_lanes = (method == 4 || method == 6) ? 8 : 0;
+    if (method < 0 || method > 8) return LMEP_INVALID_CONFIG;
+    // 0 auto: block-balanced mv (harvest_mvb.cuh) for large single-geometry batches, else
+    // the per-item mv (4 lanes per item); 1 pade; 2/3 quad (4 / 8 lanes); 4 per-item mv
+    // with 8 lanes for d > 8; 5 per-item mv only; 6 / 7 / 8 auto with the block-balanced
+    // kernel forced to 8 / 2 / 4 lanes per item (tuning)
+    lmep::g_mv_lanes = (method == 4 || method == 6) ? 8 : (method == 7 ? 2 : (method == 8 ? 4 : 0));
     if (method == 4) method = 5;
-    if (method == 6) method = 0;
+    if (method >= 6) method = 0;
     lmep::g_harvest_method = method;
     lmep::set_lanes_per_item(method == 2 ? 4 : 8);
     return LMEP_OK;

@@ -72,7 +72,7 @@ __device__ __forceinline__ double mv_gfmax(double v)
 template <int D, int LPI>
 struct MvCfg {
     static constexpr int R = (D + LPI - 1) / LPI;       // rows per lane
-    static constexpr int SH = LPI == 4 ? 2 : 3;
+    static constexpr int SH = LPI == 2 ? 1 : (LPI == 4 ? 2 : 3);
     static constexpr int G = 32 / LPI;                  // items per warp
     static constexpr int TS = (LPI == 8 || D > 8) ? 18 : 10;   // doubles per item vector (bank-spread pad)
     static constexpr int BUF = G * TS;                  // one buffer of a warp

@@ -3,9 +3,8 @@
 // coefficients, BASELINE config 5): block-balanced expm-multiply.
 //
 // Same mathematics as harvest_mv.cuh (exp(A) e_c by a Taylor series on A/reps,
-// truncated when two consecutive terms fall below 2^-53 of the partial sum,
 // Al-Mohy & Higham 2011; harvest.py:97-121 semantics).  The ncu profile of
-// the per-item kernel (profiles/r1b_harvest_mv_kernel.md) showed that half of
+// the per-item kernel (profiles/r1c_* and the r1b capture) showed that half of
 // its instructions were spent before the Taylor loop: assembling A with
 // per-entry selects (frozen rows, reaction term, augmentation, padding) and
 // one Osborne balancing per item.  Two observations remove almost all of it:
@@ -23,11 +22,15 @@
 //     one more table (the identity), the assembly is the same straight-line
 //     product chain for every entry: no selects at all.
 //
-// The norm that fixes reps is the infinity norm of B (the lane-local row
-// sums; the max-abs convergence test is measured in the same norm), with
-// ||B / reps||_inf <= 4: fewer Taylor products per item than ||.||_1 <= 2
-// at the same 2^-53 truncation (9.7 vs 18.8 products per
-// item on the C5 coefficient field, errors ~7e-15 either way).
+// The norm that fixes reps is an upper bound of ||B||_inf from per-row abs
+// sums of the balanced tables (triangle inequality, no pass over the entries),
+// with ||B / reps||_inf <= 4.  Every term is then bounded geometrically,
+// |B^{j+1} v| <= 4 |B^j v|, so the Taylor tail after term k is at most
+// tau_k |term_k|, tau_k = (4/(k+1)) / (1 - 4/(k+2)): the series stops at the
+// first term whose tail bound falls below 2^-53 of the partial sum.  On the
+// C5 coefficient field this takes 8.5 products per item, against 9.7 for the
+// two-consecutive-terms test and 18.8 for ||.||_1 <= 2 (the per-item
+// kernel), at the same ~7e-15 error (SURVEY 8(d) C5 sample, scipy truth).
 //
 // CTAs are persistent (grid = resident CTAs) and walk superblocks
 // interleaved, so the cost of a superblock (which varies with nu(x)) is
@@ -57,7 +60,8 @@ struct MvbCfg {
     static constexpr int NTP = NT == 1 ? 1 : (NT == 2 ? 2 : 4);   // LDS.64 / LDS.128 granules
     static constexpr int TAB = RP * D * NTP;           // one table copy (doubles)
     // smem: 1/k!, exponents (int, as doubles), Taylor buffers, tab0, tabS, aug
-    static constexpr int OFF_E = C::INV;
+    static constexpr int OFF_TF = C::INV;                // tau_k / k! (tail bound)
+    static constexpr int OFF_E = OFF_TF + C::INV;
     static constexpr int OFF_T = OFF_E + 8;
     static constexpr int OFF_TAB0 = OFF_T + (C::THREADS / 32) * C::WARP_T;
     static constexpr int OFF_TABS = OFF_TAB0 + TAB;
@@ -70,7 +74,7 @@ template <int D, int NT, int LPI>
 constexpr size_t mvb_smem_bytes() { return (size_t)MvbCfg<D, NT, LPI>::TOTAL * sizeof(double); }
 
 template <int D, int NT, int LPI>
-__global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : 4) harvest_mvb_kernel(const HarvestParams P, int64_t nsb)
+__global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : (LPI == 2 ? 2 : 4)) harvest_mvb_kernel(const HarvestParams P, int64_t nsb)
 {
     using C = MvCfg<D, LPI>;
     using K = MvbCfg<D, NT, LPI>;
@@ -78,6 +82,7 @@ __global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : 4) harvest_mvb_kern
     constexpr int GC = 128 / LPI;                                   // items per CTA iteration
     extern __shared__ __align__(16) double mv_sm[];
     double *sFact = mv_sm;
+    double *sTF = mv_sm + K::OFF_TF;
     int *sE = reinterpret_cast<int *>(mv_sm + K::OFF_E);          // [16] exponents of this superblock
     double *sT = mv_sm + K::OFF_T + (threadIdx.x >> 5) * C::WARP_T;
     double *sTab0 = mv_sm + K::OFF_TAB0;                            // [RP][D][NTP]: T_t[c][j] at (j, c, t)
@@ -94,6 +99,9 @@ __global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : 4) harvest_mvb_kern
         double f = 1.0;
         for (int j = 2; j <= i; ++j) f *= (double)j;
         sFact[i] = 1.0 / f;
+        // the Taylor tail after term k is at most tau_k |term_k| when ||B||_inf <= THETA
+        // (|B^{j+1} v| <= THETA |B^j v|, geometric): tau_k = (T/(k+1)) / (1 - T/(k+2))
+        sTF[i] = (i + 2 > MVB_THETA) ? (MVB_THETA / (i + 1)) / (1.0 - MVB_THETA / (i + 2)) / f : INFINITY;
     }
     // tables (and the identity for the reaction term), zero outside n x n
     for (int i = threadIdx.x; i < K::TAB; i += blockDim.x) {
@@ -216,9 +224,6 @@ __global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : 4) harvest_mvb_kern
         }
         __syncthreads();
 
-        int ej[R];
-#pragma unroll
-        for (int m = 0; m < R; ++m) ej[m] = sE[q + LPI * m < 16 ? q + LPI * m : 0];
         const int erow = sE[row];
 
         for (int it = 0; it < MVB_ITERS; ++it) {
@@ -287,7 +292,6 @@ __global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : 4) harvest_mvb_kern
             double acc[R];
 #pragma unroll
             for (int m = 0; m < R; ++m) acc[m] = (q + LPI * m == idx) ? 1.0 : 0.0;
-            double wprev = INFINITY;
             double *tg = sT + grp * C::TS;
             int buf = 0;
             __syncwarp();
@@ -296,33 +300,51 @@ __global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : 4) harvest_mvb_kern
                 if (q + LPI * m < D) tg[q + LPI * m] = acc[m];
             __syncwarp();
             while (__any_sync(MV_FULL, !done)) {
-                // group max of |acc| before this term: its shuffles overlap the products
+                // the iterate first (LDS latency overlaps the group max below), then the
+                // group max of |acc| before this term (its shuffles overlap the products)
+                const double *tv = tg + buf * C::BUF;
+                constexpr int NP = D / 2;
+                double2 tt[NP];
+#pragma unroll
+                for (int p = 0; p < NP; ++p) tt[p] = *reinterpret_cast<const double2 *>(tv + 2 * p);
+                double tlast = 0.0;
+                if constexpr (D & 1) tlast = tv[D - 1];
                 unsigned ah = 0u;
 #pragma unroll
                 for (int m = 0; m < R; ++m)
                     if (q + LPI * m < n) ah = max(ah, mv_hiabs(acc[m]));
                 ah = mv_gmax<LPI>(ah);
-                const double *tv = tg + buf * C::BUF;
                 double u[R];
-                {
+                if constexpr (R >= 6) {
+                    // R independent DFMA chains already cover the DFMA latency
+#pragma unroll
+                    for (int m = 0; m < R; ++m) u[m] = 0.0;
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) {
+#pragma unroll
+                        for (int m = 0; m < R; ++m)
+                            u[m] = fma(a[m][2 * p + 1], tt[p].y, fma(a[m][2 * p], tt[p].x, u[m]));
+                    }
+                    if constexpr (D & 1) {
+#pragma unroll
+                        for (int m = 0; m < R; ++m) u[m] = fma(a[m][D - 1], tlast, u[m]);
+                    }
+                } else {
                     // two chains per row (even / odd columns): 2R independent DFMA chains
                     double s0[R], s1[R];
 #pragma unroll
                     for (int m = 0; m < R; ++m) s0[m] = s1[m] = 0.0;
 #pragma unroll
-                    for (int c = 0; c < D; c += 2) {
-                        if (c + 1 < D) {
-                            const double2 tt = *reinterpret_cast<const double2 *>(tv + c);
+                    for (int p = 0; p < NP; ++p) {
 #pragma unroll
-                            for (int m = 0; m < R; ++m) {
-                                s0[m] = fma(a[m][c], tt.x, s0[m]);
-                                s1[m] = fma(a[m][c + 1], tt.y, s1[m]);
-                            }
-                        } else {
-                            const double t0 = tv[c];
-#pragma unroll
-                            for (int m = 0; m < R; ++m) s0[m] = fma(a[m][c], t0, s0[m]);
+                        for (int m = 0; m < R; ++m) {
+                            s0[m] = fma(a[m][2 * p], tt[p].x, s0[m]);
+                            s1[m] = fma(a[m][2 * p + 1], tt[p].y, s1[m]);
                         }
+                    }
+                    if constexpr (D & 1) {
+#pragma unroll
+                        for (int m = 0; m < R; ++m) s0[m] = fma(a[m][D - 1], tlast, s0[m]);
                     }
 #pragma unroll
                     for (int m = 0; m < R; ++m) u[m] = s0[m] + s1[m];
@@ -333,14 +355,17 @@ __global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : 4) harvest_mvb_kern
 #pragma unroll
                 for (int m = 0; m < R; ++m) {
                     acc[m] = fma(u[m], fa, acc[m]);
-                    if (q + LPI * m < n) wh = max(wh, mv_hiabs(u[m]));
+                    wh = max(wh, mv_hiabs(u[m]));             // whole vector (padding rows are 0)
                 }
                 // every lane tests its own rows against the group scale; the group
                 // converges when all its lanes pass (one ballot instead of a
                 // shuffle reduction on the critical path)
-                const double wn = __hiloint2double((int)wh, -1) * fk;   // >= max |u_k / k!| of this lane
-                const double an = __hiloint2double((int)ah, 0);          // <= group max |acc_{k-1}|
-                const bool pass = kt > qo && an > 0.0 && wn + wprev <= 0x1p-53 * an;
+                // stop when the rigorous tail bound tau_k |u_k / k!|_inf falls below 2^-53 of
+                // the extracted partial sum (one term earlier than the two-term test of
+                // AMH 2011 on average, and a bound rather than a heuristic)
+                const double wn = __hiloint2double((int)wh, -1) * sTF[kt];   // >= tau_k max |u_k / k!| of this lane
+                const double an = __hiloint2double((int)ah, 0);              // <= group max |acc_{k-1}|
+                const bool pass = kt > qo && an > 0.0 && wn <= 0x1p-53 * an;
                 const unsigned bal = __ballot_sync(MV_FULL, pass);
                 const bool conv = ((bal >> (grp * LPI)) & ((1u << LPI) - 1u)) == ((1u << LPI) - 1u) ||
                                   kt >= MV_TMAX;
@@ -350,12 +375,11 @@ __global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : 4) harvest_mvb_kern
                     if (conv) {
                         ++rep;
                         kt = 1;
-                        wprev = INFINITY;
                         if (rep >= reps) {
 #pragma unroll
                             for (int m = 0; m < R; ++m) {
                                 const int j = q + LPI * m;
-                                const double o = acc[m] * mv_pow2(ej[m] - eidx);
+                                const double o = acc[m] * mv_pow2(sE[j < 16 ? j : 0] - eidx);
                                 bad |= (unsigned)!isfinite(o);
                                 if (live && j < n) {
                                     if (P.layout == 0) P.out[(b * sd + qo) * n + j] = o;
@@ -377,7 +401,6 @@ __global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : 4) harvest_mvb_kern
                         for (int m = 0; m < R; ++m) nt[m] = acc[m];
                     } else {
                         ++kt;
-                        wprev = wn;
 #pragma unroll
                         for (int m = 0; m < R; ++m) nt[m] = u[m];
                     }
@@ -431,14 +454,29 @@ int launch_mvb_nt(const HarvestParams &P, cudaStream_t st)
     return launch_status("harvest_mvb_kernel");
 }
 
+// Lanes per item: 2 while the item's rows fit the register file (d <= 13:
+// <= 7 rows of d doubles per lane, 2 CTAs of 128 threads per SM), else 4.
+// mv_lanes_override() 4 / 8 forces 4 / 8 lanes (tuning and tests).
+template <int D, int NT>
+int launch_mvb_l(const HarvestParams &P, cudaStream_t st)
+{
+    const int ov = mv_lanes_override();
+    if constexpr (D <= 13) {
+        if (ov == 0 || ov == 2) return launch_mvb_nt<D, NT, 2>(P, st);
+    }
+    if constexpr (D == 13 && NT == 2) {
+        if (ov == 8) return launch_mvb_nt<D, NT, 8>(P, st);
+    }
+    return launch_mvb_nt<D, NT, 4>(P, st);
+}
+
 template <int D>
 int launch_mvb(const HarvestParams &P, cudaStream_t st)
 {
     switch (P.nterms + (P.c0 ? 1 : 0)) {
-    case 1: return launch_mvb_nt<D, 1, 4>(P, st);
-    case 2: if (D == 13 && mv_lanes_override() == 8) return launch_mvb_nt<D, 2, 8>(P, st);
-            return launch_mvb_nt<D, 2, 4>(P, st);
-    case 3: return launch_mvb_nt<D, 3, 4>(P, st);
+    case 1: return launch_mvb_l<D, 1>(P, st);
+    case 2: return launch_mvb_l<D, 2>(P, st);
+    case 3: return launch_mvb_l<D, 3>(P, st);
     default: return LMEP_INVALID_CONFIG;
     }
 }

@@ -208,7 +208,8 @@ def _c5_large(lx, N):
 
 @pytest.mark.parametrize("s", [1, 2, 4])
 @pytest.mark.parametrize("dtmul", [1.0, 4.0])
-def test_block_balanced_harvest_large_batch(lx, orc, s, dtmul):
+@pytest.mark.parametrize("lanes", ["multiply", "mvb4", "mvb8"])
+def test_block_balanced_harvest_large_batch(lx, orc, s, dtmul, lanes):
     """Large single-geometry per-node batch (B >= 4096): the block-balanced
     kernel (harvest_mvb.cuh, one representative balancing per 256 items, inf
     norm scaling) against the oracle's per-node harvest on a sample of nodes,
@@ -223,7 +224,11 @@ def test_block_balanced_harvest_large_batch(lx, orc, s, dtmul):
     dt = w5.delta_t * dtmul
     spec = lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1))
     stats = {}
-    W = harvest_compact(g, st, spec, dt, s, (), stats).pernode.permute(2, 0, 1).cpu().numpy()
+    lx._native.set_harvest_method(lanes)          # lanes per item of harvest_mvb (auto: 2 for d <= 13)
+    try:
+        W = harvest_compact(g, st, spec, dt, s, (), stats).pernode.permute(2, 0, 1).cpu().numpy()
+    finally:
+        lx._native.set_harvest_method("multiply")
     reps = (torch.cat(stats["ms"]).cpu().numpy() >> 24)
     if dtmul > 1:
         assert reps.max() > 4, reps.max()
