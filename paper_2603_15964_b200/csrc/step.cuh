@@ -215,6 +215,7 @@ __device__ __forceinline__ void run_pass(const StepParams &p, int lo, int hi, in
     // interior chunks, the last one possibly partial: the fast path computes
     // all P outputs (the window may run into the slot padding) and stores cnt
     const int nch = fhi > flo ? (fhi - flo + P - 1) / P : 0;
+#pragma unroll 1
     for (int ch = tid; ch < nch; ch += nt) {
         const int l = flo + ch * P;
         const int cnt = fhi - l < P ? fhi - l : P;
@@ -236,6 +237,7 @@ __device__ __forceinline__ void run_pass(const StepParams &p, int lo, int hi, in
     const int a_end = nch > 0 ? flo : hi;
     const int b_beg = nch > 0 ? fhi : hi;
     const int na = a_end - lo, nb = hi - b_beg;
+#pragma unroll 1
     for (int k = nt - 1 - tid; k < na + nb; k += nt) {
         const int l = k < na ? lo + k : b_beg + (k - na);
         double vq[NB > 0 ? NB : 1];
@@ -249,6 +251,7 @@ __device__ __forceinline__ void run_pass(const StepParams &p, int lo, int hi, in
 template <class Epi>
 __device__ __forceinline__ void run_pointwise(int lo, int hi, Epi &&epi)
 {
+#pragma unroll 1
     for (int l = lo + (int)threadIdx.x; l < hi; l += blockDim.x) epi(l);
 }
 
@@ -287,12 +290,20 @@ step_kernel(const __grid_constant__ StepParams p)
     if (ring) { base = -eL; gend = p.N + eR; }
     else expand_g(K * p.ext, base, gend);
     const int len = (int)(gend - base);
-    // pass ranges in tile-local (shared-memory) coordinates
+    // pass ranges in tile-local (shared-memory) coordinates, 32-bit: the owned
+    // range [o0, o1) grows by units*(eL, eR), clamped to the grid for
+    // non-periodic grids (ring mode: the whole staged ring)
+    const int64_t big = 1 << 30;
+    auto clampi = [&](int64_t v) { return (int)(v < -big ? -big : (v > big ? big : v)); };
+    const int o0 = ring ? 0 : clampi(O0 - base), o1 = ring ? (int)p.N : clampi(O1 - base);
+    const int cLo = (ring || p.periodic) ? -(1 << 30) : clampi(-base);
+    const int cHi = (ring || p.periodic) ? (1 << 30) : clampi(p.N - base);
     auto expand = [&](int units, int &lo, int &hi) {
-        int64_t a, b;
-        expand_g(units, a, b);
-        lo = (int)(a - base);
-        hi = (int)(b - base);
+        if (ring) { lo = eL; hi = eL + (int)p.N; return; }          // global [0, N)
+        lo = o0 - units * eL;
+        hi = o1 + units * eR;
+        lo = lo > cLo ? lo : cLo;
+        hi = hi < cHi ? hi : cHi;
     };
     // fast-path window: interior class and, for per-node rows, owned nodes
     const int64_t lbase = base - p.off;
@@ -303,9 +314,8 @@ step_kernel(const __grid_constant__ StepParams p)
             a = a > -lbase ? a : -lbase;
             b = b < p.nloc - lbase ? b : p.nloc - lbase;
         }
-        const int64_t big = 1 << 30;
-        fLo = (int)(a < -big ? -big : (a > big ? big : a));
-        fHi = (int)(b < -big ? -big : (b > big ? big : b));
+        fLo = clampi(a);
+        fHi = clampi(b);
     }
     const int slen = (int)p.slot_len;
 #define S(q) (sm + (q) * slen)
@@ -337,10 +347,10 @@ step_kernel(const __grid_constant__ StepParams p)
     };
     // thread 0 applies the closure of stage vector X at the boundary nodes in
     // [lo, hi); fix(l, value) recomputes the dependent pointwise values.
+    const int pb0 = clampi(-base), pb1 = clampi(p.N - 1 - base);   // boundary nodes, tile-local
     auto pin_pass = [&](double *X, int lo, int hi, auto &&fix) {
         if (!pins) return;
-        const int64_t b0 = -base, b1 = p.N - 1 - base;          // CTA-uniform test
-        if (!((b0 >= lo && b0 < hi) || (b1 >= lo && b1 < hi))) return;
+        if (!((pb0 >= lo && pb0 < hi) || (pb1 >= lo && pb1 < hi))) return;   // CTA-uniform
         __syncthreads();
         if (tid == 0) {
             const int64_t ends[2] = {0, p.N - 1};

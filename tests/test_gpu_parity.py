@@ -248,6 +248,30 @@ def test_block_balanced_harvest_large_batch(lx, orc, s, dtmul, lanes):
     assert (np.abs(W - W2) / den).max() < W_TOL
 
 
+@pytest.mark.parametrize("n,s", [(5, 1), (7, 1), (7, 4), (9, 2), (11, 1), (11, 3), (13, 3)])
+def test_block_balanced_harvest_other_widths(lx, orc, n, s):
+    """Every (d = n + s - 1) instantiation family of the block kernel on a
+    large per-node batch (C5 coefficient field, centred n-point stencils)."""
+    from paper_2603_15964_b200 import configs
+    from paper_2603_15964_b200.harvest import harvest_compact
+    N = 1 << 13
+    w5 = configs.c5(N=N, steps=1)
+    c, nu = w5.coef
+    g = lx.make_periodic_grid(N, 0.0, 1.0)
+    st = lx.select_stencils(g, n, lx.StencilPolicy.CENTERED)
+    row = (n - 1) // 2
+    dt = w5.delta_t * 2
+    spec = lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1))
+    W = harvest_compact(g, st, spec, dt, s).pernode.permute(2, 0, 1).cpu().numpy()
+    idx = np.arange(0, N, 37)
+    x = (np.arange(n) - row) * w5.h
+    D1 = np.array([orc.fornberg_weights(xi, x, 2)[1] for xi in x])
+    D2 = np.array([orc.fornberg_weights(xi, x, 2)[2] for xi in x])
+    ref = orc.harvest_batch_vc(D1, D2, -c[idx], nu[idx], dt, s, row, reduced=True)
+    worst = max(_rows_rel(W[i], ref[k]) for k, i in enumerate(idx))
+    assert worst < W_TOL, worst
+
+
 def test_block_balanced_harvest_reaction_and_single_term(lx, orc):
     """The reaction term rides as an identity table (localop.py:120-127 order:
     derivative terms, then the diagonal), and one-term operators (nu(x) D2)."""
