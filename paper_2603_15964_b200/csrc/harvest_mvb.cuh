@@ -252,7 +252,10 @@ __global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : (LPI == 2 ? 2 : 4))
             int s = 0;
             if (!(nrm <= 1e9)) status = LMEP_NONFINITE;
             else s = nrm > MVB_THETA ? (int)ceil(nrm / MVB_THETA) : 1;
-            const double sc = 1.0 / (double)max(s, 1);
+            // B = A / reps: the 1/reps scale rides on dt (dt itself when reps == 1, so
+            // the entries are then bit-identical to dt * local_operator)
+            const double rinv = s > 1 ? 1.0 / (double)s : 1.0;
+            const double dts = dt * rinv;
 
             // ---- assembly: a[m][c] = dt * L'[c][j] 2^(e_c - e_j) (/ reps), no selects
             double a[R][D];
@@ -277,9 +280,8 @@ __global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : (LPI == 2 ? 2 : 4))
                     double l = xmul(cf[0], tv[0]);
 #pragma unroll
                     for (int t = 1; t < NT; ++t) l = xadd(l, xmul(cf[t], tv[t]));
-                    double v = xmul(dt, l);
-                    if (sd > 1) v = xadd(v, sAug[j * D + c]);
-                    if (s > 1) v *= sc;
+                    double v = xmul(dts, l);
+                    if (sd > 1) v = fma(sAug[j * D + c], rinv, v);   // v = +-0 at augmentation entries
                     a[m][c] = v;
                 }
             }
