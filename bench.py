@@ -464,10 +464,10 @@ def main():
             # the dominant kernel of the pass (ncu launch list: ~80% of device time) is
             # the FP64-bound harvest; the HBM-bound step kernel follows as roofline_step
             "roofline": {"bound": "fp64",
-                         "kernel": "harvest_mvb_kernel<13,2,4> (block-balanced per-node expm-multiply, 13x13)",
+                         "kernel": "harvest_mvb_kernel<13,2,2> (block-balanced per-node expm-multiply, 13x13, 2 lanes per item)",
                          "achieved": harvest_tflops, "peak": fp64, "unit": "TFLOP/s",
                          "frac": harvest_tflops / fp64,
-                         "traffic": traffic("harvest_mvb_kernel<13,2,4>", "bytes_per_item", bench.nloc),
+                         "traffic": traffic("harvest_mvb_kernel<13,2,2>", "bytes_per_item", bench.nloc),
                          "algorithmic_flops_per_launch": flops,
                          "peak_kind": "measured DFMA chains (tools/fp64_peak.cu), this run"},
             "roofline_step": {"bound": "hbm", "kernel": step_kernel,
