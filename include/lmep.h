@@ -225,14 +225,22 @@ int lmep_harvest_chunk(int n, int s, int nterms, const double *tables, const int
                        int32_t *status, int32_t *ms, const lmep_coef_map *map, int64_t out_ld,
                        void *stream);
 
-/* Harvest algorithm for d <= 16: 0 (default) = register-resident
- * expm-multiply, warp-uniform, 4 lanes per item (harvest_mv.cuh: balancing +
- * scaled Taylor action on the needed columns), 1 = full Pade
- * scaling-and-squaring per warp (harvest.cu), 2 / 3 = the first-generation
- * expm-multiply kernel with 4 / 8 lanes per item (harvest_quad.cu), 4 = the
- * warp-uniform kernel with 8 lanes per item for d > 8.  lmep_expm always uses
- * the Pade kernel.
- * Process-wide setting. */
+/* Harvest algorithm for d <= 16:
+ *   0 (default) = expm-multiply: large single-geometry batches (B >= 4096, one
+ *     shared table, one target row, no frozen rows) take the block-balanced
+ *     kernel (harvest_mvb.cuh: one balancing per 256 items folded into the
+ *     tables, inf-norm bound scaling, rigorous Taylor tail stop, 2 lanes per
+ *     item for d <= 13, else 4); everything else the per-item kernel
+ *     (harvest_mv.cuh: per-item balancing, 4 lanes per item);
+ *   1 = full Pade scaling-and-squaring per warp (harvest.cu);
+ *   2 / 3 = the first-generation expm-multiply kernel, 4 / 8 lanes per item
+ *     (harvest_quad.cu);
+ *   4 = the per-item kernel with 8 lanes per item for d > 8;
+ *   5 = the per-item kernel only (no block-balanced path);
+ *   6 / 7 / 8 = as 0 with the block-balanced kernel forced to 8 / 2 / 4 lanes
+ *     per item (tuning, tests).
+ * lmep_expm always uses the Pade kernel.  Process-wide setting; returns
+ * LMEP_INVALID_CONFIG for other codes. */
 int lmep_set_harvest_method(int method);
 
 /* ---- stepping (K3, K4, K5) ---------------------------------------------- */
