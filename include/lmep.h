@@ -228,7 +228,7 @@ int lmep_harvest_chunk(int n, int s, int nterms, const double *tables, const int
 /* Harvest algorithm for d <= 16:
  *   0 (default) = expm-multiply: large single-geometry batches (B >= 4096, one
  *     shared table, one target row, no frozen rows) take the block-balanced
- *     kernel (harvest_mvb.cuh: one balancing per 256 items folded into the
+ *     kernel (harvest_mvb.cuh: one balancing per superblock of 1024 items folded into the
  *     tables, inf-norm bound scaling, rigorous Taylor tail stop, 2 lanes per
  *     item for d <= 13, else 4); everything else the per-item kernel
  *     (harvest_mv.cuh: per-item balancing, 4 lanes per item);

@@ -13,7 +13,8 @@
 //     is unchanged up to rounding, expm.py:27-30); items that share a table
 //     and differ by their coefficients have nearly the same best scaling
 //     (C5: identical exponents over the whole grid, because nu D2 dominates).
-//     So one item per superblock of 256 items is balanced (warp 0, the
+//     So one item per superblock (16 CTA iterations: 1024 items at 2 lanes
+//     per item) is balanced (warp 0, the
 //     per-item sweep of harvest_mv.cuh) and its exponents are folded into a
 //     CTA-shared copy of the tables: T'[j][c] = T[j][c] 2^(e_c - e_j).
 //     Scaling by a power of two is exact, so every item's balanced matrix
@@ -44,7 +45,7 @@
 
 namespace lmep {
 
-constexpr int MVB_ITERS = 8;                         // CTA iterations per superblock
+constexpr int MVB_ITERS = 16;                        // CTA iterations per superblock
 template <int LPI>
 constexpr int mvb_sb() { return MVB_ITERS * (128 / LPI); }   // items per superblock
 constexpr double MVB_THETA = 4.0;

@@ -358,13 +358,32 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
 
 
 PIPELINE_MIN = 1 << 18      # nodes; smaller host tables go up in one copy
-PIPELINE_CHUNKS = 8
+# growing slices (fractions of N): only the first, small upload is exposed, each
+# upload is hidden behind the previous slice's harvest (the harvest runs ~1.8x
+# slower than PCIe per item), and few launches keep the persistent harvest
+# kernel's per-launch tail small
+PIPELINE_FRACTIONS = (1 / 16, 1 / 8, 3 / 16, 1 / 4, 3 / 8)
+
+
+def _pipeline_bounds(N: int):
+    if N < 1 << 16:
+        return [(0, N)] if N > 0 else []
+    out, a, acc = [], 0, 0.0
+    for f in PIPELINE_FRACTIONS:
+        acc += f
+        b = N if f is PIPELINE_FRACTIONS[-1] else min(N, -(-int(acc * N) // 1024) * 1024)
+        if b > a:
+            out.append((a, b))
+            a = b
+    return out
 
 
 def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
                        tables: torch.Tensor, row: int) -> _ops.HarvestOut:
     """Per-node harvest (one shared window geometry) from HOST coefficients:
-    the [N, K] coefficient table goes up in PIPELINE_CHUNKS slices on the copy
+    the [N, K] coefficient table goes up in growing slices (_pipeline_bounds;
+    multiples of 1024 items, so the block-balanced kernel's superblocks and
+    their representative balancing are those of a resident harvest) on the copy
     stream, and the harvest of slice i (lmep_harvest_chunk into the shared SoA
     output) overlaps the upload of slice i+1."""
     d = nat.device()
@@ -379,10 +398,7 @@ def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
                           torch.empty(N, dtype=torch.int32, device=d),
                           torch.empty(N, dtype=torch.int32, device=d))
     cp.wait_stream(cur)                      # dc / dr were allocated on cur
-    step = -(-N // PIPELINE_CHUNKS)
-    step = -(-step // 128) * 128
-    for a in range(0, N, step):
-        b = min(N, a + step)
+    for a, b in _pipeline_bounds(N):
         with torch.cuda.stream(cp):
             dc[a:b].copy_(hc[a:b], non_blocking=True)
             if dr is not None:
