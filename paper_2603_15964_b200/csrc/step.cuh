@@ -408,6 +408,38 @@ step_kernel(const __grid_constant__ StepParams p)
 
     if constexpr (SCH == SCH_LIN) {
         int iU = 0, iV = 1;
+        if constexpr (!PN && NS > 0) {
+            // Ring mode (a periodic grid resident in one CTA, C1): one barrier per
+            // step.  The threads that write nodes mirrored by the ghost cells also
+            // write the mirror, so no separate ghost refresh (and its barrier) is
+            // needed: staged position eL + i holds node i, ghosts [0, eL) mirror
+            // nodes N - eL .. N - 1 and [eL + N, eL + N + eR) mirror nodes 0 .. eR - 1.
+            if (ring) {
+                const int NN = (int)p.N;
+                for (int s = 0; s < K; ++s) {
+                    double *XU = S(iU), *XV = S(iV);
+                    const int rows[1] = {LMEP_ROW_W};
+                    const double *const X[1] = {XU};
+                    fast_pass<NS, P, EX, 1>(p, eL, eL + NN, rows, X, [&](int l, const double *v) {
+                        if (l < eL + NN) {
+                            XV[l] = v[0];
+                            if (l >= NN) XV[l - NN] = v[0];
+                            if (l < eL + eR) XV[l + NN] = v[0];
+                        }
+                    });
+                    __syncthreads();
+                    const int t = iU; iU = iV; iV = t;
+                }
+                bool bad = false;
+                for (int64_t i = O0 + tid; i < O1; i += nt) {
+                    const double v = S(iU)[i - base];
+                    p.u_out[i - p.off] = v;
+                    bad |= !isfinite(v);
+                }
+                if (bad) *p.flag = 1;
+                return;
+            }
+        }
         for (int s = 0; s < K; ++s) {
             int lo, hi;
             expand((K - 1 - s) * p.ext, lo, hi);
