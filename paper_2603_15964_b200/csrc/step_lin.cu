@@ -1,11 +1,85 @@
 // step_lin.cu -- instantiations of the linear step kernel.
+#include <algorithm>
+
 #include "step.cuh"
 
 namespace lmep {
 
+// Ring mode for the linear scheme (a periodic grid resident in one CTA, C1:
+// N = 1024, 1000 steps in one launch).  The whole run is one SM, so the
+// per-step latency chain and the SM's shared-memory bandwidth are the cost:
+// each thread owns P consecutive nodes and loads one register window of
+// P + n - 1 values (odd P: the lane stride hits distinct bank pairs), then
+// runs P interleaved chains of the reference's ascending unfused
+// multiply-adds (kernels.py:23-29).  Ghost mirrors are written by their
+// producers, so there is one barrier per step.
+template <int NS, int P>
+__global__ void __launch_bounds__(1024) ring_lin_kernel(const __grid_constant__ StepParams p)
+{
+    extern __shared__ double rsm[];
+    const int N = (int)p.N, eL = p.eL, eR = p.eR;
+    const int span = N + eL + eR;
+    const int slot = span + P + NS;               // overhang of the last window / chunk
+    double *X0 = rsm, *X1 = rsm + slot;
+    for (int i = threadIdx.x; i < span; i += blockDim.x) {
+        int64_t g = (int64_t)i - eL;
+        g = g < 0 ? g + N : (g >= N ? g - N : g);
+        X0[i] = p.u_in[g];
+    }
+    __syncthreads();
+    double w[NS];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) w[j] = p.wi[LMEP_ROW_W][j];
+    const int K = p.ksteps;
+    for (int s = 0; s < K; ++s) {
+#pragma unroll 1
+        for (int i0 = P * threadIdx.x; i0 < N; i0 += P * blockDim.x) {
+            const double *x = X0 + i0;                // window of node i0: staged i0 .. i0 + n - 1
+            double win[P + NS - 1];
+#pragma unroll
+            for (int q = 0; q < P + NS - 1; ++q) win[q] = x[q];
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                const int i = i0 + q;
+                double acc = xmul(w[0], win[q]);
+#pragma unroll
+                for (int j = 1; j < NS; ++j) acc = xadd(acc, xmul(w[j], win[q + j]));
+                if (i < N) {
+                    X1[eL + i] = acc;
+                    if (i >= N - eL) X1[i - (N - eL)] = acc;  // left ghosts mirror nodes N - eL ..
+                    if (i < eR) X1[eL + N + i] = acc;         // right ghosts mirror nodes 0 .. eR - 1
+                }
+            }
+        }
+        __syncthreads();
+        double *t = X0; X0 = X1; X1 = t;
+    }
+    bool bad = false;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        const double v = X0[eL + i];
+        p.u_out[i] = v;
+        bad |= !isfinite(v);
+    }
+    if (bad) *p.flag = 1;
+}
+
 int launch_scheme_lin(bool pernode, const StepParams &p, dim3 grid, size_t shm, cudaStream_t st)
 {
     if (pernode) return launch_ns<SCH_LIN, true, 1, LMEP_NL_NONE, true>(p.n, p, grid, shm, st);
+    if (p.ring && p.off == 0 && p.hl == nullptr && p.hr == nullptr && p.wmode == LMEP_W_SHARED &&
+        (p.n == 7 || p.n == 9 || p.n == 11 || p.n == 13)) {
+        constexpr int RP = 3;
+        const int threads = (int)std::min<int64_t>(1024, ((p.N + RP - 1) / RP + 31) / 32 * 32);
+        const size_t rshm = (size_t)2 * (p.N + p.eL + p.eR + RP + p.n) * sizeof(double);
+        void (*k)(StepParams) = p.n == 7 ? ring_lin_kernel<7, RP> : p.n == 9 ? ring_lin_kernel<9, RP>
+                                : p.n == 11 ? ring_lin_kernel<11, RP> : ring_lin_kernel<13, RP>;
+        if (rshm > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rshm);
+            if (e != cudaSuccess) { set_last_error("cudaFuncSetAttribute", e); return LMEP_CUDA_ERROR; }
+        }
+        k<<<1, threads, rshm, st>>>(p);
+        return launch_status("ring_lin_kernel");
+    }
     return launch_ns<SCH_LIN, true, 5, LMEP_NL_NONE>(p.n, p, grid, shm, st);
 }
 
