@@ -81,6 +81,14 @@ __global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : (LPI == 2 ? 2 : 4))
     using K = MvbCfg<D, NT, LPI>;
     constexpr int R = C::R, SH = C::SH, NTP = K::NTP;
     constexpr int GC = 128 / LPI;                                   // items per CTA iteration
+    // 2 lanes per item with odd d: the last row is split by columns (lane q holds
+    // columns q, q+2, ...; one shuffle sums the halves) instead of padding lane 1
+    // with a d-th row of zeros -- d doubles of registers back, which lets the
+    // iterate loads run ahead of the products.
+    constexpr bool SPLIT = LPI == 2 && (D & 1) && D >= 5;
+    constexpr int RM = SPLIT ? (D - 1) / 2 : R;                     // whole rows per lane
+    constexpr int H = (D + 1) / 2;                                  // split-row slots per lane
+    constexpr int J1 = D - 1;
     extern __shared__ __align__(16) double mv_sm[];
     double *sFact = mv_sm;
     double *sTF = mv_sm + K::OFF_TF;
@@ -240,8 +248,8 @@ __global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : (LPI == 2 ? 2 : 4))
             // NaN coefficient, or entries that overflow, make the bound non-finite.
             double rb = 0.0;
 #pragma unroll
-            for (int m = 0; m < R; ++m) {
-                const int j = q + LPI * m;
+            for (int m = 0; m < RM + (SPLIT ? 1 : 0); ++m) {
+                const int j = m < RM ? q + LPI * m : J1;
                 double r = 0.0;
 #pragma unroll
                 for (int t = 0; t < NT; ++t) r = fma(fabs(cf[t]), sRS[t * K::RP + j], r);
@@ -259,9 +267,26 @@ __global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : (LPI == 2 ? 2 : 4))
             const double dts = dt * rinv;
 
             // ---- assembly: a[m][c] = dt * L'[c][j] 2^(e_c - e_j) (/ reps), no selects
-            double a[R][D];
+            double a[RM][D];
+            double a12[SPLIT ? H : 1];
+            if constexpr (SPLIT) {
+                const double *tr = sTabS + J1 * D * NTP;
 #pragma unroll
-            for (int m = 0; m < R; ++m) {
+                for (int i = 0; i < H; ++i) {
+                    const int c = q + 2 * i;
+                    double v = 0.0;
+                    if (c < D) {
+                        double l = xmul(cf[0], tr[c * NTP]);
+#pragma unroll
+                        for (int t = 1; t < NT; ++t) l = xadd(l, xmul(cf[t], tr[c * NTP + t]));
+                        v = xmul(dts, l);
+                        if (sd > 1) v = fma(sAug[J1 * D + c], rinv, v);
+                    }
+                    a12[i] = v;
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < RM; ++m) {
                 const int j = q + LPI * m;
                 const double *tr = sTabS + j * D * NTP;
 #pragma unroll
@@ -292,15 +317,17 @@ __global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : (LPI == 2 ? 2 : 4))
             int qo = 0, rep = 0, kt = 1, nmv = 0, idx = row, eidx = erow;
             bool done = reps == 0;
             unsigned bad = 0u;
-            double acc[R];
+            double acc[RM];
 #pragma unroll
-            for (int m = 0; m < R; ++m) acc[m] = (q + LPI * m == idx) ? 1.0 : 0.0;
+            for (int m = 0; m < RM; ++m) acc[m] = (q + LPI * m == idx) ? 1.0 : 0.0;
+            double acc12 = (SPLIT && J1 == idx) ? 1.0 : 0.0;
             double *tg = sT + grp * C::TS;
             int buf = 0;
             __syncwarp();
 #pragma unroll
-            for (int m = 0; m < R; ++m)
+            for (int m = 0; m < RM; ++m)
                 if (q + LPI * m < D) tg[q + LPI * m] = acc[m];
+            if (SPLIT && q == 0) tg[J1] = acc12;
             __syncwarp();
             while (__any_sync(MV_FULL, !done)) {
                 // the iterate first (LDS latency overlaps the group max below), then the
@@ -314,51 +341,64 @@ __global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : (LPI == 2 ? 2 : 4))
                 if constexpr (D & 1) tlast = tv[D - 1];
                 unsigned ah = 0u;
 #pragma unroll
-                for (int m = 0; m < R; ++m)
+                for (int m = 0; m < RM; ++m)
                     if (q + LPI * m < n) ah = max(ah, mv_hiabs(acc[m]));
+                if (SPLIT && J1 < n) ah = max(ah, mv_hiabs(acc12));
                 ah = mv_gmax<LPI>(ah);
-                double u[R];
-                if constexpr (R >= 6) {
+                double u[RM];
+                double u12 = 0.0;
+                if constexpr (SPLIT) {
+                    double p12 = 0.0;
+#pragma unroll
+                    for (int i = 0; i < D / 2; ++i) p12 = fma(a12[i], q ? tt[i].y : tt[i].x, p12);
+                    p12 = fma(a12[D / 2], tlast, p12);       // lane 1: a12 = 0 (column d)
+                    u12 = p12 + __shfl_xor_sync(MV_FULL, p12, 1);
+                }
+                if constexpr (RM >= 6) {
                     // R independent DFMA chains already cover the DFMA latency
 #pragma unroll
-                    for (int m = 0; m < R; ++m) u[m] = 0.0;
+                    for (int m = 0; m < RM; ++m) u[m] = 0.0;
 #pragma unroll
                     for (int p = 0; p < NP; ++p) {
 #pragma unroll
-                        for (int m = 0; m < R; ++m)
+                        for (int m = 0; m < RM; ++m)
                             u[m] = fma(a[m][2 * p + 1], tt[p].y, fma(a[m][2 * p], tt[p].x, u[m]));
                     }
                     if constexpr (D & 1) {
 #pragma unroll
-                        for (int m = 0; m < R; ++m) u[m] = fma(a[m][D - 1], tlast, u[m]);
+                        for (int m = 0; m < RM; ++m) u[m] = fma(a[m][D - 1], tlast, u[m]);
                     }
                 } else {
                     // two chains per row (even / odd columns): 2R independent DFMA chains
-                    double s0[R], s1[R];
+                    double s0[RM], s1[RM];
 #pragma unroll
-                    for (int m = 0; m < R; ++m) s0[m] = s1[m] = 0.0;
+                    for (int m = 0; m < RM; ++m) s0[m] = s1[m] = 0.0;
 #pragma unroll
                     for (int p = 0; p < NP; ++p) {
 #pragma unroll
-                        for (int m = 0; m < R; ++m) {
+                        for (int m = 0; m < RM; ++m) {
                             s0[m] = fma(a[m][2 * p], tt[p].x, s0[m]);
                             s1[m] = fma(a[m][2 * p + 1], tt[p].y, s1[m]);
                         }
                     }
                     if constexpr (D & 1) {
 #pragma unroll
-                        for (int m = 0; m < R; ++m) s0[m] = fma(a[m][D - 1], tlast, s0[m]);
+                        for (int m = 0; m < RM; ++m) s0[m] = fma(a[m][D - 1], tlast, s0[m]);
                     }
 #pragma unroll
-                    for (int m = 0; m < R; ++m) u[m] = s0[m] + s1[m];
+                    for (int m = 0; m < RM; ++m) u[m] = s0[m] + s1[m];
                 }
                 const double fk = sFact[kt];
                 const double fa = done ? 0.0 : fk;
                 unsigned wh = 0u;
 #pragma unroll
-                for (int m = 0; m < R; ++m) {
+                for (int m = 0; m < RM; ++m) {
                     acc[m] = fma(u[m], fa, acc[m]);
                     wh = max(wh, mv_hiabs(u[m]));             // whole vector (padding rows are 0)
+                }
+                if constexpr (SPLIT) {
+                    acc12 = fma(u12, fa, acc12);
+                    wh = max(wh, mv_hiabs(u12));
                 }
                 // every lane tests its own rows against the group scale; the group
                 // converges when all its lanes pass (one ballot instead of a
@@ -374,13 +414,22 @@ __global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : (LPI == 2 ? 2 : 4))
                                   kt >= MV_TMAX;
                 if (!done) {
                     ++nmv;
-                    double nt[R];
+                    double nt[RM];
+                    double nt12 = 0.0;
                     if (conv) {
                         ++rep;
                         kt = 1;
                         if (rep >= reps) {
+                            if constexpr (SPLIT) {
+                                const double o = acc12 * mv_pow2(sE[J1] - eidx);
+                                bad |= (unsigned)!isfinite(o);
+                                if (live && J1 < n && q == 0) {
+                                    if (P.layout == 0) P.out[(b * sd + qo) * n + J1] = o;
+                                    else P.out[((int64_t)qo * n + J1) * P.out_ld + b] = o;
+                                }
+                            }
 #pragma unroll
-                            for (int m = 0; m < R; ++m) {
+                            for (int m = 0; m < RM; ++m) {
                                 const int j = q + LPI * m;
                                 const double o = acc[m] * mv_pow2(sE[j < 16 ? j : 0] - eidx);
                                 bad |= (unsigned)!isfinite(o);
@@ -397,21 +446,25 @@ __global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : (LPI == 2 ? 2 : 4))
                                 idx = n + qo - 1;
                                 eidx = sE[idx];
 #pragma unroll
-                                for (int m = 0; m < R; ++m) acc[m] = (q + LPI * m == idx) ? 1.0 : 0.0;
+                                for (int m = 0; m < RM; ++m) acc[m] = (q + LPI * m == idx) ? 1.0 : 0.0;
+                                acc12 = (SPLIT && J1 == idx) ? 1.0 : 0.0;
                             }
                         }
 #pragma unroll
-                        for (int m = 0; m < R; ++m) nt[m] = acc[m];
+                        for (int m = 0; m < RM; ++m) nt[m] = acc[m];
+                        nt12 = acc12;
                     } else {
                         ++kt;
 #pragma unroll
-                        for (int m = 0; m < R; ++m) nt[m] = u[m];
+                        for (int m = 0; m < RM; ++m) nt[m] = u[m];
+                        nt12 = u12;
                     }
                     buf ^= 1;
                     double *to = tg + buf * C::BUF;
 #pragma unroll
-                    for (int m = 0; m < R; ++m)
+                    for (int m = 0; m < RM; ++m)
                         if (q + LPI * m < D) to[q + LPI * m] = nt[m];
+                    if (SPLIT && q == 0) to[J1] = nt12;
                 }
                 __syncwarp();
             }
@@ -419,8 +472,8 @@ __global__ void __launch_bounds__(128, LPI == 4 ? MVB_MINB : (LPI == 2 ? 2 : 4))
             if (reps == 0 && live) {
                 for (int qq = 0; qq < sd; ++qq)
 #pragma unroll
-                    for (int m = 0; m < R; ++m) {
-                        const int j = q + LPI * m;
+                    for (int m = 0; m < RM + (SPLIT ? 1 : 0); ++m) {
+                        const int j = m < RM ? q + LPI * m : (q == 0 ? J1 : D);
                         if (j < n) {
                             const double nan = __longlong_as_double(0x7ff8000000000000LL);
                             if (P.layout == 0) P.out[(b * sd + qq) * n + j] = nan;
