@@ -39,7 +39,7 @@ enum { SCH_LIN = 0, SCH_ETDRK4 = 1, SCH_ETD2 = 2 };
 constexpr int STEP_THREADS = 256;
 constexpr int SLOT_PAD = 24;
 constexpr int STEP_P_ETDRK4 = 5;   // consecutive outputs per thread (odd: conflict-free)
-constexpr int STEP_P_ETD2 = 5;
+constexpr int STEP_P_ETD2 = 1;
 
 struct StepParams {
     int64_t N, off, nloc;
