@@ -55,6 +55,38 @@ def copy_stream(which: int = 0) -> torch.cuda.Stream:
     return _COPY_STREAMS[key]
 
 
+class DeferredUpload:
+    """A host->device copy that a pipelined harvest queues on copy stream 0
+    right after its coefficient slices (timestep.run's initial state): both
+    directions of PCIe then serve the harvest inputs first.  ``event`` is set
+    once the copy is queued."""
+
+    def __init__(self, src: torch.Tensor, dst: torch.Tensor):
+        self.src, self.dst, self.event = src, dst, None
+
+    def issue(self, stream: torch.cuda.Stream) -> None:
+        with torch.cuda.stream(stream):
+            self.dst.copy_(self.src, non_blocking=self.src.is_pinned())
+        self.event = stream.record_event()
+
+
+_DEFERRED: list[DeferredUpload] = []
+
+
+def defer_upload(up: DeferredUpload) -> None:
+    _DEFERRED.append(up)
+
+
+def issue_deferred(stream: torch.cuda.Stream) -> None:
+    while _DEFERRED:
+        _DEFERRED.pop(0).issue(stream)
+
+
+def drop_deferred(up: DeferredUpload) -> None:
+    if up in _DEFERRED:
+        _DEFERRED.remove(up)
+
+
 def is_host(a) -> bool:
     """True for data that lives in host memory (numpy / CPU tensors)."""
     return not (isinstance(a, torch.Tensor) and a.device.type == "cuda")

@@ -410,6 +410,7 @@ def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
     dc.record_stream(cp)
     if dr is not None:
         dr.record_stream(cp)
+    _ops.issue_deferred(cp)                  # e.g. run()'s initial state, behind the slices
     return out
 
 

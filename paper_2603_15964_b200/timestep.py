@@ -30,7 +30,7 @@ from . import _ops
 from .errors import DimensionMismatch, InvalidConfig, NonFinite, NotWarmedUp
 from .grid import Grid, StencilSet, as_stencil_set
 from .harvest import BandedPropagator, combine, derivative_compact, harvest_compact
-from .localop import LinearOperatorSpec, fornberg_weights
+from .localop import LinearOperatorSpec, VariableCoefficientSpec, fornberg_weights
 
 
 @dataclass(frozen=True)
@@ -371,12 +371,29 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
 
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter_ns()
-    # the initial data goes up on its own copy stream while the harvest runs
-    # (the harvest's own host inputs use copy stream 0)
-    with torch.cuda.stream(cp1):
-        u0d = _ops.dev_f64(u0)
-    ev_u0 = cp1.record_event()
-    prep = prepare(grid, stencils, problem, scheme, delta_t, stats)
+    # The initial data goes up while the harvest runs.  When the harvest
+    # streams host coefficients (copy stream 0), u0 is queued behind them so
+    # the slices the harvest waits on get the PCIe bandwidth first; otherwise
+    # it goes up at once on its own copy stream.
+    lin = problem.linear
+    deferred = None
+    if isinstance(lin, VariableCoefficientSpec) and _ops.is_host(lin.coef) and _ops.is_host(u0):
+        src = _ops.host_f64(u0)
+        deferred = _ops.DeferredUpload(src, torch.empty(N, dtype=torch.float64, device=dev))
+        _ops.defer_upload(deferred)
+    else:
+        with torch.cuda.stream(cp1):
+            u0d = _ops.dev_f64(u0)
+        ev_u0 = cp1.record_event()
+    try:
+        prep = prepare(grid, stencils, problem, scheme, delta_t, stats)
+    finally:
+        if deferred is not None:
+            _ops.drop_deferred(deferred)
+    if deferred is not None:
+        if deferred.event is None:           # the harvest did not pipeline: upload now
+            deferred.issue(cp1)
+        u0d, ev_u0 = deferred.dst, deferred.event
     torch.cuda.synchronize(dev)
     harvest_ns = time.perf_counter_ns() - t0
 
