@@ -585,6 +585,38 @@ def test_c5_run_varcoef_end_to_end(lx, golden):
 
 
 @pytest.mark.parametrize("src", ["numpy", "pinned"])
+def test_run_host_coefficients_pipelined_bitwise(lx, src):
+    """run() from host coefficients at a size that pipelines the harvest (the
+    initial state is queued behind the coefficient slices) is bit-identical to
+    run() from device-resident coefficients and initial state."""
+    from paper_2603_15964_b200 import configs
+    N = 1 << 19
+    w5 = configs.c5(N=N, steps=1)
+    c, nu = w5.coef
+    g = lx.make_periodic_grid(N, 0.0, 1.0)
+    st = lx.select_stencils(g, w5.n, lx.StencilPolicy.CENTERED)
+    coef = np.stack([-c, nu], 1)
+    u0 = np.array(w5.u0)
+    if src == "pinned":
+        hc, hu = torch.from_numpy(coef).pin_memory(), torch.from_numpy(u0).pin_memory()
+    else:
+        hc, hu = coef, u0
+    sch = lx.SchemeConfig("linear")
+    a = lx.run(g, st, lx.SemiLinearProblem(lx.VariableCoefficientSpec((1, 2), hc), None, hu,
+                                           lx.Boundary.periodic(), "none"), sch, w5.delta_t,
+               37 * w5.delta_t, 12 * w5.delta_t)
+    b = lx.run(g, st, lx.SemiLinearProblem(
+        lx.VariableCoefficientSpec((1, 2), torch.as_tensor(coef, device="cuda")), None,
+        torch.as_tensor(u0, device="cuda"), lx.Boundary.periodic(), "none"), sch, w5.delta_t,
+        37 * w5.delta_t, 12 * w5.delta_t)
+    sa = np.asarray(a.snapshots)
+    sb = np.asarray(b.snapshots.cpu() if isinstance(b.snapshots, torch.Tensor) else b.snapshots)
+    assert sa.shape == sb.shape and np.array_equal(sa, sb)
+    assert np.array_equal(np.asarray(a.u_final), np.asarray(b.u_final.cpu() if isinstance(
+        b.u_final, torch.Tensor) else b.u_final))
+
+
+@pytest.mark.parametrize("src", ["numpy", "pinned"])
 def test_pipelined_host_harvest_bitwise(lx, src):
     """Host coefficient tables above PIPELINE_MIN go up in chunks on the copy
     stream (lmep_harvest_chunk into one SoA table): bit-identical to the
