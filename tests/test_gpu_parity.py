@@ -367,6 +367,20 @@ def test_c1_launch_shapes_bitwise(lx, golden, orc, tuning):
     assert np.array_equal(u, orc.run_linear(W, m, golden["c1_u0"], 123))
 
 
+@pytest.mark.parametrize("n,row,N", [(9, 4, 777), (11, 10, 1000), (13, 6, 2048), (7, 0, 96)])
+def test_ring_linear_widths_bitwise(lx, orc, n, row, N):
+    """The single-CTA ring kernel (ring_lin_kernel) over stencil widths, rows
+    (upwind, centred, downwind ghosts) and sizes that are not multiples of its
+    3-node windows: bit-identical to the reference loop (kernels.py:33-43)."""
+    rng = np.random.default_rng(n * 1000 + N)
+    w = rng.standard_normal(n) / n
+    m = orc.members_for(N, n, row, True)
+    W = np.tile(w, (N, 1))
+    u0 = rng.standard_normal(N)
+    u = lx.kernels.run_linear(W, m, u0, 57, tuning={"ring": 1})
+    assert np.array_equal(u, orc.run_linear(W, m, u0, 57))
+
+
 def test_c1_run_end_to_end(lx, golden):
     from paper_2603_15964_b200 import configs
     w = configs.c1()
