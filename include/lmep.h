@@ -243,6 +243,13 @@ int lmep_harvest_chunk(int n, int s, int nterms, const double *tables, const int
  * LMEP_INVALID_CONFIG for other codes. */
 int lmep_set_harvest_method(int method);
 
+/* Ring mode of the linear scheme (a periodic grid resident on chip for all
+ * steps, BASELINE config 1): 1 (default) = one thread-block cluster of 8 CTAs
+ * exchanging halos through distributed shared memory every kb steps when
+ * N % 8 == 0 (ring_lin_cluster_kernel), 0 = one CTA (ring_lin_kernel).
+ * Process-wide setting; results are bit-identical either way. */
+int lmep_set_ring_cluster(int on);
+
 /* ---- stepping (K3, K4, K5) ---------------------------------------------- */
 
 /* Linear banded propagation u <- W u for `steps` steps (kernels.py:33-43,

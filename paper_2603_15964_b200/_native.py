@@ -42,7 +42,7 @@ EXPORTS = (
     "lmep_version", "lmep_status_string", "lmep_last_error", "lmep_fornberg", "lmep_expm",
     "lmep_harvest", "lmep_step_linear", "lmep_step_etdrk4", "lmep_step_etd2",
     "lmep_banded_matvec", "lmep_plan", "lmep_rows_to_soa", "lmep_launch_count",
-    "lmep_set_harvest_method", "lmep_step_etds", "lmep_harvest_mapped", "lmep_harvest_chunk",
+    "lmep_set_harvest_method", "lmep_set_ring_cluster", "lmep_step_etds", "lmep_harvest_mapped", "lmep_harvest_chunk",
 )
 
 
@@ -125,6 +125,7 @@ def load(path: str | None = None):
     L.lmep_plan.argtypes = [G, C.c_int, C.c_int, C.c_int, i64, T]
     L.lmep_rows_to_soa.argtypes = [vp, i64, C.c_int, vp, vp]
     L.lmep_set_harvest_method.argtypes = [C.c_int]
+    L.lmep_set_ring_cluster.argtypes = [C.c_int]
     for name in EXPORTS:
         if name not in ("lmep_version", "lmep_status_string", "lmep_last_error",
                         "lmep_launch_count"):
@@ -178,3 +179,8 @@ def set_harvest_method(method: str) -> None:
     code = {"multiply": 0, "auto": 0, "pade": 1, "multiply4": 2, "quad": 3, "mv8": 4,
             "mvitem": 5, "mvb8": 6, "mvb2": 7, "mvb4": 8}[method]
     check(lib().lmep_set_harvest_method(code), "lmep_set_harvest_method")
+
+
+def set_ring_cluster(on: bool) -> None:
+    """Linear ring mode on one thread-block cluster (default) or one CTA."""
+    check(lib().lmep_set_ring_cluster(1 if on else 0), "lmep_set_ring_cluster")

@@ -1,9 +1,16 @@
 // step_lin.cu -- instantiations of the linear step kernel.
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "step.cuh"
 
+namespace cg = cooperative_groups;
+
 namespace lmep {
+
+// set by lmep_set_ring_cluster (capi.cu): 1 = cluster ring kernel when eligible
+int g_ring_cluster = 1;
 
 // Ring mode for the linear scheme (a periodic grid resident in one CTA, C1:
 // N = 1024, 1000 steps in one launch).  The whole run is one SM, so the
@@ -63,11 +70,107 @@ __global__ void __launch_bounds__(1024) ring_lin_kernel(const __grid_constant__ 
     if (bad) *p.flag = 1;
 }
 
+// Ring mode over a thread-block CLUSTER: the periodic grid is split into C
+// slabs of M = N / C nodes, one per CTA of one cluster (C SMs instead of one).
+// Each block of kb steps starts by gathering eL*kb / eR*kb halo nodes from the
+// neighbouring CTAs' shared memory (DSMEM, cluster.map_shared_rank), then the
+// CTA advances kb steps on its extended range with CTA-local barriers
+// (temporal blocking: the stale halo edges move inward by eL / eR per step and
+// never reach the owned nodes), and publishes its owned nodes back.  Two
+// cluster barriers per kb steps replace kb whole-grid barriers; the arithmetic
+// is the reference's ascending unfused order, bit-identical.
+template <int NS>
+__global__ void __launch_bounds__(1024) ring_lin_cluster_kernel(const __grid_constant__ StepParams p, int kb)
+{
+    cg::cluster_group cl = cg::this_cluster();
+    const int C = (int)cl.num_blocks(), r = (int)cl.block_rank();
+    const int N = (int)p.N, M = N / C, eL = p.eL, eR = p.eR;
+    const int HL = eL * kb, HR = eR * kb, span = HL + M + HR;
+    extern __shared__ double csm[];
+    double *own = csm;                            // [M] this slab's state at block boundaries
+    double *A = csm + M, *B = A + span;           // ping-pong over the extended range
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int i = tid; i < M; i += nt) own[i] = p.u_in[(int64_t)r * M + i];
+    double w[NS];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) w[j] = p.wi[LMEP_ROW_W][j];
+    cl.sync();
+    const double *lown = cl.map_shared_rank(own, (r + C - 1) % C);
+    const double *rown = cl.map_shared_rank(own, (r + 1) % C);
+    const int K = p.ksteps;
+    for (int s0 = 0; s0 < K; s0 += kb) {
+        const int ks = K - s0 < kb ? K - s0 : kb;
+        for (int i = tid; i < span; i += nt)
+            A[i] = i < HL ? lown[M - HL + i] : (i < HL + M ? own[i - HL] : rown[i - HL - M]);
+        cl.sync();                                // neighbours' own[] read: it may be rewritten
+        for (int j = 0; j < ks; ++j) {
+            for (int i = eL + tid; i < span - eR; i += nt) {
+                const double *x = A + i - eL;
+                double acc = xmul(w[0], x[0]);
+#pragma unroll
+                for (int c = 1; c < NS; ++c) acc = xadd(acc, xmul(w[c], x[c]));
+                B[i] = acc;
+            }
+            __syncthreads();
+            double *t = A; A = B; B = t;
+        }
+        for (int i = tid; i < M; i += nt) own[i] = A[HL + i];
+        cl.sync();                                // own[] complete before the next gather
+    }
+    bool bad = false;
+    for (int i = tid; i < M; i += nt) {
+        const double v = own[i];
+        p.u_out[(int64_t)r * M + i] = v;
+        bad |= !isfinite(v);
+    }
+    if (bad) *p.flag = 1;
+}
+
+static int launch_ring_cluster(const StepParams &p, cudaStream_t st)
+{
+    constexpr int C = 8;
+    const int reach = std::max(p.eL, p.eR);
+    if (p.N % C != 0 || reach == 0) return -1;
+    const int M = (int)(p.N / C);
+    // a cluster barrier costs ~0.4 us, a local step ~0.25 us: take the deepest
+    // halo that still comes from the adjacent slabs only (eL*kb, eR*kb <= M)
+    const int kb = std::min(32, M / reach);
+    if (kb < 2) return -1;
+    const int span = p.eL * kb + M + p.eR * kb;
+    const int threads = std::min(1024, (span + 31) / 32 * 32);
+    const size_t shm = (size_t)(M + 2 * span) * sizeof(double);
+    void (*k)(StepParams, int) = p.n == 7 ? ring_lin_cluster_kernel<7> : p.n == 9 ? ring_lin_cluster_kernel<9>
+                                 : p.n == 11 ? ring_lin_cluster_kernel<11> : ring_lin_cluster_kernel<13>;
+    if (shm > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        if (e != cudaSuccess) return -1;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = shm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k, p, kb);
+    if (e != cudaSuccess) { set_last_error("cudaLaunchKernelEx(ring_lin_cluster_kernel)", e); return LMEP_CUDA_ERROR; }
+    return launch_status("ring_lin_cluster_kernel");
+}
+
 int launch_scheme_lin(bool pernode, const StepParams &p, dim3 grid, size_t shm, cudaStream_t st)
 {
     if (pernode) return launch_ns<SCH_LIN, true, 1, LMEP_NL_NONE, true>(p.n, p, grid, shm, st);
     if (p.ring && p.off == 0 && p.hl == nullptr && p.hr == nullptr && p.wmode == LMEP_W_SHARED &&
         (p.n == 7 || p.n == 9 || p.n == 11 || p.n == 13)) {
+        if (g_ring_cluster) {
+            const int rc = launch_ring_cluster(p, st);
+            if (rc >= 0) return rc;                  // else: shape not eligible, one-CTA kernel
+        }
         constexpr int RP = 3;
         const int threads = (int)std::min<int64_t>(1024, ((p.N + RP - 1) / RP + 31) / 32 * 32);
         const size_t rshm = (size_t)2 * (p.N + p.eL + p.eR + RP + p.n) * sizeof(double);
@@ -244,3 +347,10 @@ int launch_lin_pernode_tb(const StepParams &p, cudaStream_t st)
 }
 
 }  // namespace lmep
+
+extern "C" int lmep_set_ring_cluster(int on)
+{
+    if (on != 0 && on != 1) return LMEP_INVALID_CONFIG;
+    lmep::g_ring_cluster = on;
+    return LMEP_OK;
+}

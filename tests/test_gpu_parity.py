@@ -367,8 +367,10 @@ def test_c1_launch_shapes_bitwise(lx, golden, orc, tuning):
     assert np.array_equal(u, orc.run_linear(W, m, golden["c1_u0"], 123))
 
 
-@pytest.mark.parametrize("n,row,N", [(9, 4, 777), (11, 10, 1000), (13, 6, 2048), (7, 0, 96)])
-def test_ring_linear_widths_bitwise(lx, orc, n, row, N):
+@pytest.mark.parametrize("cluster", [True, False])
+@pytest.mark.parametrize("n,row,N", [(9, 4, 777), (11, 10, 1000), (13, 6, 2048), (7, 0, 96),
+                                     (7, 6, 1024), (9, 8, 4096)])
+def test_ring_linear_widths_bitwise(lx, orc, n, row, N, cluster):
     """The single-CTA ring kernel (ring_lin_kernel) over stencil widths, rows
     (upwind, centred, downwind ghosts) and sizes that are not multiples of its
     3-node windows: bit-identical to the reference loop (kernels.py:33-43)."""
@@ -377,7 +379,11 @@ def test_ring_linear_widths_bitwise(lx, orc, n, row, N):
     m = orc.members_for(N, n, row, True)
     W = np.tile(w, (N, 1))
     u0 = rng.standard_normal(N)
-    u = lx.kernels.run_linear(W, m, u0, 57, tuning={"ring": 1})
+    lx._native.set_ring_cluster(cluster)
+    try:
+        u = lx.kernels.run_linear(W, m, u0, 57, tuning={"ring": 1})
+    finally:
+        lx._native.set_ring_cluster(True)
     assert np.array_equal(u, orc.run_linear(W, m, u0, 57))
 
 
