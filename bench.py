@@ -218,6 +218,35 @@ class C5:
         return 2 * self.u0_host.nbytes if self.world == 1 else 8 * self.nloc
 
 
+def time_c5_onestep(steps=20):
+    """The reference's schedule for config 5 -- one banded per-node step per
+    launch, every row and u crossing HBM each step (lin_pernode_kernel, the
+    kernel sharded / clamped per-node grids use): its HBM roofline fraction on
+    16 + 8n bytes per point-step."""
+    import torch
+    import paper_2603_15964_b200 as lx
+    from paper_2603_15964_b200 import _ops
+    from paper_2603_15964_b200.timestep import Stepper, prepare
+    w, coef = c5_inputs()
+    g = lx.make_periodic_grid(w.N, 0.0, 1.0)
+    st = lx.select_stencils(g, w.n, lx.StencilPolicy.CENTERED)
+    prob = lx.SemiLinearProblem(lx.VariableCoefficientSpec((1, 2), _ops.dev_f64(coef)), None,
+                                w.u0, lx.Boundary.periodic(), "none")
+    prep = prepare(g, st, prob, lx.SchemeConfig("linear"), w.delta_t)
+    s = Stepper(prep, _ops.dev_f64(w.u0), exact=True, tuning={"tile": 4096, "ksteps": 1})
+    s.advance(3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    s.advance(steps)
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / steps
+    nbytes = w.N * (8 * w.n + 16)
+    return {"kernel": "lin_pernode_kernel<13,4> (one step per launch)", "us_per_step": us,
+            "algorithmic_bytes_per_launch": nbytes, "achieved_gbs": nbytes / (us * 1e-6) / 1e9}
+
+
 def time_c4_sharded(rank, world):
     """BASELINE config 4 (2^24, ETDRK4, Neumann) sharded over the ranks: us/step."""
     import torch
@@ -435,6 +464,8 @@ def main():
     fp64 = fp64_peak()
     harvest_tflops = flops / (harvest_ms * 1e-3) / 1e12
 
+    onestep = time_c5_onestep() if world == 1 else None
+
     # e2e through the public API
     for _ in range(2):
         bench.e2e_pass()
@@ -484,6 +515,15 @@ def main():
             # the blocked step kernel is no longer HBM-bound: it issues the reference's
             # unfused multiply + add per tap (2n flops per point-step, kernels.py:23-29),
             # so its ceiling is the FP64 pipe at one op per lane per issue = fp64 / 2
+            # the reference's one-step-per-launch schedule on the same rows: the HBM-bound
+            # kernel the north star's >= 70% target is about; the blocked kernel above
+            # beats this roofline by the ratio of the two step times
+            "roofline_step_onestep": None if onestep is None else {
+                "bound": "hbm", "kernel": onestep["kernel"], "achieved": onestep["achieved_gbs"],
+                "peak": hbm, "unit": "GB/s", "frac": onestep["achieved_gbs"] / hbm,
+                "us_per_step": onestep["us_per_step"],
+                "algorithmic_bytes_per_launch": onestep["algorithmic_bytes_per_launch"],
+                "blocked_speedup": onestep["us_per_step"] / (step_ms * 1e3 / w.steps)},
             "roofline_step_fp64": {"bound": "fp64 (unfused mul+add)", "kernel": step_kernel,
                                    "achieved": 2 * w.n * w.N * w.steps / (step_ms * 1e-3) / 1e12,
                                    "peak": fp64 / 2, "unit": "TFLOP/s",
