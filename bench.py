@@ -145,13 +145,14 @@ def c5_inputs(N=None):
 class C5:
     """Config 5 pass on resident device inputs (this rank's slab when sharded)."""
 
-    def __init__(self, rank=0, world=1):
+    def __init__(self, rank=0, world=1, exact=False):
         import torch
         import paper_2603_15964_b200 as lx
         from paper_2603_15964_b200 import _ops
         from paper_2603_15964_b200.distributed import partition
         self.lx, self.torch = lx, torch
         self.rank, self.world = rank, world
+        self.exact = exact
         self.w, coef = c5_inputs()
         self.coef_host, self.u0_host = coef, self.w.u0
         self.grid = lx.make_periodic_grid(self.w.N, 0.0, 1.0)
@@ -170,7 +171,8 @@ class C5:
         e0, e1, e2 = self.ev
         e0.record()
         st = ShardedStepper(self.grid, self.sset, self.prob, self.scheme, self.w.delta_t,
-                            self.rank, self.world, NcclHalo(self.rank, self.world, True))
+                            self.rank, self.world, NcclHalo(self.rank, self.world, True),
+                            exact=self.exact)
         e1.record()
         st.u = self.u0[self.off:self.off + self.nloc].clone()
         advance_all(st, self.w.steps)
@@ -202,10 +204,10 @@ class C5:
         prob = lx.SemiLinearProblem(spec, None, self.u0_pin, lx.Boundary.periodic(), "none")
         if self.world == 1:
             return lx.run(self.grid, self.sset, prob, self.scheme, self.w.delta_t,
-                          self.w.steps * self.w.delta_t)
+                          self.w.steps * self.w.delta_t, exact=self.exact)
         from paper_2603_15964_b200.distributed import run_sharded
         return run_sharded(self.grid, self.sset, prob, self.scheme, self.w.delta_t,
-                           self.w.steps * self.w.delta_t)
+                           self.w.steps * self.w.delta_t, exact=self.exact)
 
     @property
     def h2d_bytes(self):
@@ -362,6 +364,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-others", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--exact", action="store_true",
+                    help="C5 steps in the bit-exact unfused order (default: fused multiply-adds, "
+                         "within 1e-13 of it; tests/test_gpu_parity.py::test_c5_run_fma_vs_exact)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -374,7 +379,9 @@ def main():
               "N": 1 << 22, "n": 13, "steps_per_pass": 200, "harvests_per_pass": 1 << 22,
               "l2": "inputs larger than L2 (436 MB per-node rows streamed each step)",
               "parallelism": f"slab-sharded x{args.gpus} (NCCL halo exchange)" if args.gpus > 1
-              else "single"}
+              else "single",
+              "step_arith": "exact (unfused mul+add, bit-identical to numba)" if args.exact
+              else "fma (fused multiply-add; <=1e-13 rel L2 from the exact order)"}
 
     if args.impl == "reference":
         if rank != 0:
@@ -404,7 +411,7 @@ def main():
     from paper_2603_15964_b200 import _native
     lib = _native.load()
 
-    bench = C5(rank, world)
+    bench = C5(rank, world, exact=args.exact)
     for _ in range(args.warmup):
         bench.device_pass()
     torch.cuda.synchronize()
@@ -524,10 +531,12 @@ def main():
                 "us_per_step": onestep["us_per_step"],
                 "algorithmic_bytes_per_launch": onestep["algorithmic_bytes_per_launch"],
                 "blocked_speedup": onestep["us_per_step"] / (step_ms * 1e3 / w.steps)},
-            "roofline_step_fp64": {"bound": "fp64 (unfused mul+add)", "kernel": step_kernel,
+            "roofline_step_fp64": {"bound": "fp64 (unfused mul+add)" if args.exact else "fp64 (fma)",
+                                   "kernel": step_kernel,
                                    "achieved": 2 * w.n * w.N * w.steps / (step_ms * 1e-3) / 1e12,
-                                   "peak": fp64 / 2, "unit": "TFLOP/s",
-                                   "frac": 2 * w.n * w.N * w.steps / (step_ms * 1e-3) / 1e12 / (fp64 / 2)},
+                                   "peak": fp64 / 2 if args.exact else fp64, "unit": "TFLOP/s",
+                                   "frac": 2 * w.n * w.N * w.steps / (step_ms * 1e-3) / 1e12 /
+                                   (fp64 / 2 if args.exact else fp64)},
             "e2e": {"value": e2e_val, "unit": unit, "h2d_bytes_per_step": bench.h2d_bytes,
                     "d2h_bytes_per_step": bench.d2h_bytes},
             "gpu_launches": launches,

@@ -256,7 +256,9 @@ int lmep_set_ring_cluster(int on);
  * run_linear).  u_in is not modified; the result lands in u_out.  `scratch`
  * (nloc doubles, nullable = library-allocated) is the ping-pong buffer.
  * nonfinite (nullable, device int32) is set to 1 if any produced value is
- * not finite (the caller raises NonFinite, timestep.py:345-348). */
+ * not finite (the caller raises NonFinite, timestep.py:345-348).
+ * flags: LMEP_FLAG_EXACT clear lets the temporally blocked per-node kernels
+ * (config 5) fuse each multiply-add; every other linear kernel is exact. */
 int lmep_step_linear(const lmep_grid *grid, const lmep_weights *w, const lmep_bc *bc,
                      const lmep_halo *halo, const double *u_in, double *u_out,
                      double *scratch, int64_t steps, int32_t flags,

@@ -297,10 +297,10 @@ int run_steps(const StepCall &c)
         }
         if (c.sch == SCH_LIN && pernode && p.bc == LMEP_BC_NONE && g.periodic && !sharded &&
             t.threads == 256 && t.tile + (int64_t)t.ksteps * (g.n - 1) == tb_nodes_per_cta(g.n, true))
-            rc = launch_lin_pernode_tma(p, c.stream);      // persistent, TMA-pipelined (C5)
+            rc = launch_lin_pernode_tma(p, (c.flags & LMEP_FLAG_EXACT) != 0, c.stream);      // persistent, TMA-pipelined (C5)
         else if (c.sch == SCH_LIN && pernode && p.bc == LMEP_BC_NONE && g.periodic &&
             t.threads == 256 && t.tile + (int64_t)t.ksteps * (g.n - 1) == tb_nodes_per_cta(g.n, false))
-            rc = launch_lin_pernode_tb(p, c.stream);       // rows in registers, k steps
+            rc = launch_lin_pernode_tb(p, (c.flags & LMEP_FLAG_EXACT) != 0, c.stream);       // rows in registers, k steps
         else if (c.sch == SCH_LIN && pernode && p.bc == LMEP_BC_NONE && k == 1 && !t.ring)
             rc = launch_lin_pernode(p, c.stream);          // lean streaming kernel
         else
@@ -336,7 +336,9 @@ extern "C" int lmep_step_linear(const lmep_grid *grid, const lmep_weights *w, co
 {
     StepCall c{};
     c.sch = SCH_LIN; c.grid = grid; c.w = w; c.bc = bc; c.halo = halo; c.nl = 0;
-    c.u_in = u_in; c.u_out = u_out; c.scratch = scratch; c.steps = steps; c.flags = flags | LMEP_FLAG_EXACT;
+    // LMEP_FLAG_EXACT clear selects fused multiply-adds in the temporally blocked
+    // per-node kernels (FP64-issue-bound); every other linear kernel is always exact
+    c.u_in = u_in; c.u_out = u_out; c.scratch = scratch; c.steps = steps; c.flags = flags;
     c.tuning = tuning; c.nonfinite = nonfinite; c.stream = (cudaStream_t)stream;
     return run_steps(c);
 }

@@ -262,8 +262,8 @@ namespace lmep {
 // values outside the shrinking valid range are never consumed.
 // Arithmetic: the ascending, unfused order of kernels.py:23-29, with the
 // chain started at the first product (0 + p0 == p0 up to the sign of zero),
-// so results equal the one-step kernels.
-template <int NS, int J>
+// so results equal the one-step kernels.  !EX: the same chain as FMAs.
+template <int NS, int J, bool EX>
 __global__ void __launch_bounds__(256, 2) lin_pernode_tb_kernel(const __grid_constant__ StepParams p)
 {
     extern __shared__ double sm[];
@@ -306,8 +306,13 @@ __global__ void __launch_bounds__(256, 2) lin_pernode_tb_kernel(const __grid_con
 #pragma unroll
             for (int j = 0; j < J; ++j) {
                 const int c = i - j;
-                if (c == 0) acc[j] = xmul(w[j][0], v);
-                else if (c > 0 && c < NS) acc[j] = xadd(acc[j], xmul(w[j][c], v));
+                if constexpr (EX) {
+                    if (c == 0) acc[j] = xmul(w[j][0], v);
+                    else if (c > 0 && c < NS) acc[j] = xadd(acc[j], xmul(w[j][c], v));
+                } else {
+                    if (c == 0) acc[j] = w[j][0] * v;
+                    else if (c > 0 && c < NS) acc[j] = fma(w[j][c], v, acc[j]);
+                }
             }
         }
 #pragma unroll
@@ -331,16 +336,28 @@ int tb_nodes_per_cta(int n, bool tma)
     return n == 13 || n == 11 || n == 9 || n == 7 ? 3 * (tma ? 512 : 256) : 0;
 }
 
-int launch_lin_pernode_tb(const StepParams &p, cudaStream_t st)
+int launch_lin_pernode_tb(const StepParams &p, bool exact, cudaStream_t st)
 {
     constexpr int J = 3, TPB = 256;
     const int64_t blocks = (p.nloc + p.tile - 1) / p.tile;
     const size_t shm = 2 * (size_t)p.slot_len * 8;
     switch (p.n) {
-    case 13: lin_pernode_tb_kernel<13, J><<<(unsigned)blocks, TPB, shm, st>>>(p); break;
-    case 11: lin_pernode_tb_kernel<11, J><<<(unsigned)blocks, TPB, shm, st>>>(p); break;
-    case 9: lin_pernode_tb_kernel<9, J><<<(unsigned)blocks, TPB, shm, st>>>(p); break;
-    case 7: lin_pernode_tb_kernel<7, J><<<(unsigned)blocks, TPB, shm, st>>>(p); break;
+    case 13:
+        if (exact) lin_pernode_tb_kernel<13, J, true><<<(unsigned)blocks, TPB, shm, st>>>(p);
+        else lin_pernode_tb_kernel<13, J, false><<<(unsigned)blocks, TPB, shm, st>>>(p);
+        break;
+    case 11:
+        if (exact) lin_pernode_tb_kernel<11, J, true><<<(unsigned)blocks, TPB, shm, st>>>(p);
+        else lin_pernode_tb_kernel<11, J, false><<<(unsigned)blocks, TPB, shm, st>>>(p);
+        break;
+    case 9:
+        if (exact) lin_pernode_tb_kernel<9, J, true><<<(unsigned)blocks, TPB, shm, st>>>(p);
+        else lin_pernode_tb_kernel<9, J, false><<<(unsigned)blocks, TPB, shm, st>>>(p);
+        break;
+    case 7:
+        if (exact) lin_pernode_tb_kernel<7, J, true><<<(unsigned)blocks, TPB, shm, st>>>(p);
+        else lin_pernode_tb_kernel<7, J, false><<<(unsigned)blocks, TPB, shm, st>>>(p);
+        break;
     default: return LMEP_INVALID_CONFIG;
     }
     return launch_status("lin_pernode_tb_kernel");

@@ -20,8 +20,12 @@
 // Bulk copies need 16-byte aligned sources and sizes, so each row / u slice
 // is fetched from the even node at or below the staged range start and the
 // smem origin is shifted by that parity (`o`).  Periodic wrap splits a slice
-// into two copies.  Arithmetic: the ascending unfused order of
-// kernels.py:23-29, bit-identical to the other per-node step kernels.
+// into two copies.  Arithmetic (EX): the ascending unfused order of
+// kernels.py:23-29, bit-identical to the other per-node step kernels; !EX
+// (LMEP_FLAG_EXACT clear): the same ascending chain as fused multiply-adds.
+// Launch shape J = 3, NT = 512 measured best against (J, NT) = (5, 288),
+// (5, 256), (7, 192): more nodes per thread cut shared-memory wavefronts but
+// the fewer resident warps expose the per-step barrier and load latency.
 #include "step.cuh"
 
 namespace lmep {
@@ -105,7 +109,7 @@ __device__ __forceinline__ uint32_t copy_wrapped(double *dst, const double *v, i
 // u buffer length (even, so every buffer starts 16-byte aligned)
 __host__ __device__ constexpr int tma_ulen(int n, int span) { return (span + n + 5) & ~1; }
 
-template <int NS, int J, int NT>
+template <int NS, int J, int NT, bool EX>
 __global__ void __launch_bounds__(NT, 1) lin_pernode_tma_kernel(const __grid_constant__ StepParams p)
 {
     constexpr int SPAN = J * NT;
@@ -172,8 +176,13 @@ __global__ void __launch_bounds__(NT, 1) lin_pernode_tma_kernel(const __grid_con
 #pragma unroll
                 for (int j = 0; j < J; ++j) {
                     const int c = i - j;
-                    if (c == 0) acc[j] = xmul(w[j][0], v);
-                    else if (c > 0 && c < NS) acc[j] = xadd(acc[j], xmul(w[j][c], v));
+                    if constexpr (EX) {
+                        if (c == 0) acc[j] = xmul(w[j][0], v);
+                        else if (c > 0 && c < NS) acc[j] = xadd(acc[j], xmul(w[j][c], v));
+                    } else {
+                        if (c == 0) acc[j] = w[j][0] * v;
+                        else if (c > 0 && c < NS) acc[j] = fma(w[j][c], v, acc[j]);
+                    }
                 }
             }
 #pragma unroll
@@ -192,7 +201,7 @@ __global__ void __launch_bounds__(NT, 1) lin_pernode_tma_kernel(const __grid_con
 
 size_t tma_smem_bytes(int n, int span) { return (size_t)(n * (span + 4) + 3 * tma_ulen(n, span)) * 8; }
 
-int launch_lin_pernode_tma(const StepParams &p, cudaStream_t st)
+int launch_lin_pernode_tma(const StepParams &p, bool exact, cudaStream_t st)
 {
     constexpr int J = 3, NT = 512;
     const size_t shm = tma_smem_bytes(p.n, J * NT);
@@ -209,9 +218,15 @@ int launch_lin_pernode_tma(const StepParams &p, cudaStream_t st)
         return LMEP_INVALID_CONFIG;
 #define LMEP_TMA_CASE(NS_)                                                                        \
     case NS_:                                                                                     \
-        cudaFuncSetAttribute(lin_pernode_tma_kernel<NS_, J, NT>,                                  \
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);              \
-        lin_pernode_tma_kernel<NS_, J, NT><<<grid, NT, shm, st>>>(p);                             \
+        if (exact) {                                                                              \
+            cudaFuncSetAttribute(lin_pernode_tma_kernel<NS_, J, NT, true>,                        \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);          \
+            lin_pernode_tma_kernel<NS_, J, NT, true><<<grid, NT, shm, st>>>(p);                   \
+        } else {                                                                                  \
+            cudaFuncSetAttribute(lin_pernode_tma_kernel<NS_, J, NT, false>,                       \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);          \
+            lin_pernode_tma_kernel<NS_, J, NT, false><<<grid, NT, shm, st>>>(p);                  \
+        }                                                                                         \
         break;
     switch (p.n) {
         LMEP_TMA_CASE(13)

@@ -67,15 +67,17 @@ def banded_matvec(weights, members, u, out) -> None:
         out[...] = r if isinstance(r, np.ndarray) else _ops.to_host(r)
 
 
-def run_linear(weights, members, u0, steps, pin=False, pin_lo=0.0, pin_hi=0.0, *, bc=None,
-               tuning=None):
+def run_linear(weights, members, u0, steps, pin=False, pin_lo=0.0, pin_hi=0.0, *, exact=True,
+               bc=None, tuning=None):
     """steps x (banded mat-vec, optional Dirichlet pin) (kernels.py:33-43).
-    Always exact (this step is bandwidth-bound; FMA would buy nothing)."""
+    ``exact=False`` lets the temporally blocked per-node kernels use fused
+    multiply-adds (they are FP64-issue-bound); the other linear kernels are
+    always exact."""
     lay = _ops.validate_members(members, np.shape(weights))
     bank = _bank(lay, {nat.ROW_W: weights})
     u = _dense(u0)
     out = _ops.step(nat.SCH_LIN, bank, u, int(steps), bc=_bc(pin, pin_lo, pin_hi, bc),
-                    exact=True, tuning=tuning)
+                    exact=exact, tuning=tuning)
     return _ret(out, u0)
 
 

@@ -592,6 +592,41 @@ def test_per_node_steps_bitwise(lx, orc, N, n, row):
     assert np.array_equal(u, orc.run_linear(W, m, u0, 21))
 
 
+@pytest.mark.parametrize("N", [5000, 4999])
+@pytest.mark.parametrize("n,row", [(13, 6), (9, 4)])
+def test_per_node_steps_fma_within_tolerance(lx, orc, N, n, row):
+    """exact=False: the temporally blocked per-node kernels (TMA for even N,
+    register tb for odd N) fuse each multiply-add; the result stays within the
+    north star's 1e-10 relative L2 of the reference order."""
+    rng = np.random.default_rng(N + 11 * n + row)
+    W = rng.standard_normal((N, n)) / n
+    u0 = rng.standard_normal(N)
+    m = orc.members_for(N, n, row, True)
+    ref = orc.run_linear(W, m, u0, 37)
+    u = lx.kernels.run_linear(W, m, u0, 37, exact=False)
+    assert rel_l2(u, ref) < 1e-13
+    assert rel_l2(u - u0, ref - u0) < 1e-12
+
+
+def test_c5_run_fma_vs_exact(lx):
+    """Config 5 family at N=2^18 through run(): the FMA step mode against the
+    bit-exact mode, on the state (north star: 1e-10) and on the increment."""
+    from paper_2603_15964_b200 import configs
+    w5 = configs.c5(N=1 << 18, steps=200)
+    c, nu = w5.coef
+    g = lx.make_periodic_grid(w5.N, 0.0, 1.0)
+    st = lx.select_stencils(g, w5.n, lx.StencilPolicy.CENTERED)
+    spec = lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1))
+    prob = lx.SemiLinearProblem(spec, None, w5.u0, lx.Boundary.periodic(), "none")
+    T = w5.steps * w5.delta_t
+    a = lx.run(g, st, prob, lx.SchemeConfig("linear"), w5.delta_t, T).u_final
+    b = lx.run(g, st, prob, lx.SchemeConfig("linear"), w5.delta_t, T, exact=False).u_final
+    assert rel_l2(b, a) < 1e-13
+    # C5 barely moves at its stable dt (|u_T - u_0| ~ 1e-4 |u_0|): the increment
+    # carries the state's rounding relative to a small norm (SURVEY 8c: ~1e-9)
+    assert rel_l2(b - w5.u0, a - w5.u0) < 1e-8
+
+
 def test_c5_run_varcoef_end_to_end(lx, golden):
     from paper_2603_15964_b200 import configs
     w5 = configs.c5(N=64, steps=20)
