@@ -226,7 +226,11 @@ int lmep_harvest_chunk(int n, int s, int nterms, const double *tables, const int
                        void *stream);
 
 /* Harvest algorithm for d <= 16:
- *   0 (default) = expm-multiply: large single-geometry batches (B >= 4096, one
+ *   0 (default) = expm-multiply: large single-geometry w_lin batches (s = 1,
+ *     n in {7, 9, 11, 13}, <= 2 tables, B >= 4096) take the constant-table
+ *     kernel (harvest_mvc.cu: one item per lane, launch-uniform balancing,
+ *     tables as constant-bank operands); other large single-geometry
+ *     batches (B >= 4096, one
  *     shared table, one target row, no frozen rows) take the block-balanced
  *     kernel (harvest_mvb.cuh: one balancing per superblock of 1024 items folded into the
  *     tables, inf-norm bound scaling, rigorous Taylor tail stop, 2 lanes per
@@ -238,7 +242,8 @@ int lmep_harvest_chunk(int n, int s, int nterms, const double *tables, const int
  *   4 = the per-item kernel with 8 lanes per item for d > 8;
  *   5 = the per-item kernel only (no block-balanced path);
  *   6 / 7 / 8 = as 0 with the block-balanced kernel forced to 8 / 2 / 4 lanes
- *     per item (tuning, tests).
+ *     per item (tuning, tests), no constant-table kernel;
+ *   9 = as 0 without the constant-table kernel.
  * lmep_expm always uses the Pade kernel.  Process-wide setting; returns
  * LMEP_INVALID_CONFIG for other codes. */
 int lmep_set_harvest_method(int method);

@@ -662,6 +662,7 @@ static int launch_harvest(const HarvestParams &P, cudaStream_t st)
 
 static int g_harvest_method = 0;   // 0: auto (expm-multiply for d <= 16), 1: Pade expm
 static int g_mv_lanes = 0;
+static bool g_mvc = true;          // constant-table kernel (harvest_mvc.cu) when eligible
 int mv_lanes_override() { return g_mv_lanes; }
 
 static int dispatch_harvest(const HarvestParams &P, cudaStream_t st)
@@ -670,6 +671,8 @@ static int dispatch_harvest(const HarvestParams &P, cudaStream_t st)
     if (P.mode != 0 && g_harvest_method != 1 && P.d >= 2 && P.d <= 16 &&
         (P.mode == 2 || P.nterms <= 4))
     {
+        if (g_harvest_method == 0 && g_mv_lanes == 0 && g_mvc && harvest_mvc_eligible(P))
+            return launch_harvest_mvc(P, st);
         if (g_harvest_method == 0 && harvest_mvb_eligible(P)) return launch_harvest_mvb(P, st);
         if (g_harvest_method == 0 || g_harvest_method == 5) return launch_harvest_mv(P, st);
         return launch_harvest_quad(P, st);
@@ -790,14 +793,16 @@ extern "C" int lmep_harvest(int n, int s, int nterms, const double *tables,
 
 extern "C" int lmep_set_harvest_method(int method)
 {
-    if (method < 0 || method > 8) return LMEP_INVALID_CONFIG;
+    if (method < 0 || method > 9) return LMEP_INVALID_CONFIG;
     // 0 auto: block-balanced mv (harvest_mvb.cuh) for large single-geometry batches, else
     // the per-item mv (4 lanes per item); 1 pade; 2/3 quad (4 / 8 lanes); 4 per-item mv
     // with 8 lanes for d > 8; 5 per-item mv only; 6 / 7 / 8 auto with the block-balanced
-    // kernel forced to 8 / 2 / 4 lanes per item (tuning)
+    // kernel forced to 8 / 2 / 4 lanes per item (tuning); 9 auto without the
+    // constant-table kernel (harvest_mvc.cu)
+    lmep::g_mvc = method == 0;
     lmep::g_mv_lanes = (method == 4 || method == 6) ? 8 : (method == 7 ? 2 : (method == 8 ? 4 : 0));
     if (method == 4) method = 5;
-    if (method >= 6) method = 0;
+    if (method >= 6) method = 0;   // 6..9
     lmep::g_harvest_method = method;
     lmep::set_lanes_per_item(method == 2 ? 4 : 8);
     return LMEP_OK;

@@ -76,4 +76,9 @@ inline bool harvest_mvb_eligible(const HarvestParams &P)
            P.d >= 5 && P.d <= 16 && P.B >= 4096;
 }
 
+// constant-table kernel for the largest single-geometry w_lin batches
+// (harvest_mvc.cu: one item per lane, tables as constant-bank DFMA operands)
+bool harvest_mvc_eligible(const HarvestParams &P);
+int launch_harvest_mvc(const HarvestParams &P, cudaStream_t st);
+
 }  // namespace lmep

@@ -1,0 +1,299 @@
+// harvest_mvc.cu -- K1 for the largest per-node batches: one item per lane,
+// the shared derivative tables as constant-bank operands.
+//
+// Scope: the w_lin harvest (s = 1, harvest.py:73-79 / harvest_propagator) of
+// a single table geometry with per-item coefficients (periodic / uniform grids
+// with variable coefficients, BASELINE config 5), n in {7, 9, 11, 13}, one or
+// two derivative tables plus an optional reaction term.  Same mathematics as
+// harvest_mvb.cuh: row r of exp(dt L_b) is exp(B^T)^reps e_r with
+// B = S^-1 (dt L_b / reps) S, S a power-of-two balancing (expm.py:27-30), the
+// Taylor series stopped by the rigorous tail bound (||B||_inf <= 4).
+//
+// What changes is where the operator lives.  L_b = sum_t cf_bt T_t (+ c0_b I)
+// with the SAME tables T_t for every item, so
+//     B^T v = sum_t (dt cf_bt / reps) (T'_t^T v) (+ dt c0_b / reps v)
+// needs no per-item matrix at all: each lane keeps only its iterate, its
+// partial sum and two table products (4 x 13 doubles), and the table entries
+// are DFMA operands read straight from the constant bank (a warp-uniform
+// address: no load instruction, no shared-memory traffic, no cross-lane
+// exchange).  The price is one product per table instead of one with the
+// assembled matrix (2 x 169 instead of 169 DFMA per term at n = 13), paid in
+// exchange for the block kernel's per-item assembly, group broadcasts,
+// ballots and 255-register footprint (profiles/r1h_harvest_mvb_kernel.md:
+// 39% FP64 pipe, 12% occupancy, 41% of instructions FP64).
+//
+// The balancing exponents are launch-uniform: a one-warp prep kernel runs the
+// block kernel's sweep on item 0, folds the exponents into the tables
+// (T'_t[c][j] = T_t[c][j] 2^(e_c - e_j), exact) with their row abs-sum bounds,
+// and the host copies that block into the constant bank (stream-ordered
+// device-to-device copy).  Any diagonal similarity leaves exp(A) unchanged up
+// to rounding; on single-geometry batches the per-superblock exponents of the
+// block kernel are identical over the grid (C5), so nothing is lost.
+#include <math.h>
+
+#include <mutex>
+
+#include "harvest.cuh"
+#include "harvest_mv.cuh"
+
+namespace lmep {
+
+namespace {
+
+constexpr int MVC_D = 16;
+constexpr int MVC_NT = 2;
+constexpr double MVC_THETA = 4.0;
+
+struct MvcConst {
+    double tt[MVC_NT][MVC_D][MVC_D];   // tt[t][j][c] = T_t[c][j] 2^(e_c - e_j)  (row j of T'^T)
+    double rs[MVC_NT + 1][MVC_D];      // row abs sums of tt[t]; rs[NT] = 1 (reaction: identity)
+    double inv[48];                    // 1 / k
+    double tf[48];                     // tail factor tau_k (scaled terms), inf while k + 2 <= theta
+    int e[MVC_D];
+};
+
+__constant__ MvcConst c_mvc;
+
+// one warp: balance the representative item 0 (harvest_mvb.cuh sweep rule),
+// fold the exponents into the tables, row sums, 1/k and tail factors
+__global__ void mvc_prep_kernel(const HarvestParams P, MvcConst *out)
+{
+    __shared__ double M[MVC_D][MVC_D + 1];
+    __shared__ int kk[MVC_D];
+    __shared__ int ee[MVC_D];
+    const int j = threadIdx.x, n = P.n, nt = P.nterms;
+    const bool c0 = P.c0 != nullptr;
+    for (int k = j; k < 48; k += 32) {
+        out->inv[k] = k > 0 ? 1.0 / (double)k : 0.0;
+        out->tf[k] = (k + 2 > MVC_THETA) ? (MVC_THETA / (k + 1)) / (1.0 - MVC_THETA / (k + 2)) : INFINITY;
+    }
+    bool ok = true;
+    if (j < n) {
+        // M[j][c] = dt * L_0[c][j] (row j of A^T), localop.py:120-127 term order
+        for (int c = 0; c < n; ++c) {
+            double l = 0.0;
+            for (int t = 0; t < nt; ++t)
+                l = xadd(l, xmul(P.coef[t], P.tables[((int64_t)t * n + c) * n + j]));
+            if (c0 && c == j) l = xadd(l, P.c0[0]);
+            M[j][c] = xmul(P.delta_t, l);
+            ok &= (bool)isfinite(M[j][c]);
+        }
+        ee[j] = 0;
+    }
+    ok = __all_sync(FULL, ok);
+    __syncwarp();
+    for (int sweep = 0; ok && sweep < 12; ++sweep) {
+        int k = 0;
+        if (j < n) {
+            double r2 = 0.0, c2 = 0.0;
+            for (int c = 0; c < n; ++c) {
+                r2 = fma(M[j][c], M[j][c], r2);
+                c2 = fma(M[c][j], M[c][j], c2);
+            }
+            if (c2 > 1e-280 && r2 > 1e-280 && c2 < 1e280 && r2 < 1e280) {
+                const int ex = mv_exp2i(r2) - mv_exp2i(c2);
+                if (ex >= 4) k = (ex + 2) >> 2;
+                else if (ex <= -4) k = -((2 - ex) >> 2);
+            }
+            kk[j] = k;
+        }
+        if (!__any_sync(FULL, k != 0)) break;
+        __syncwarp();
+        if (j < n) {
+            for (int c = 0; c < n; ++c)
+                if (kk[c] != k) M[j][c] *= mv_pow2(kk[c] - k);
+            ee[j] += k;
+        }
+        __syncwarp();
+    }
+    __syncwarp();
+    if (j < MVC_D) {
+        out->e[j] = j < n ? ee[j] : 0;
+        for (int t = 0; t < MVC_NT; ++t) {
+            double sum = 0.0;
+            for (int c = 0; c < MVC_D; ++c) {
+                double v = 0.0;
+                if (t < nt && j < n && c < n)
+                    v = P.tables[((int64_t)t * n + c) * n + j] * mv_pow2(ee[c] - ee[j]);
+                out->tt[t][j][c] = v;
+                sum += fabs(v);
+            }
+            out->rs[t][j] = sum;
+        }
+        out->rs[MVC_NT][j] = (c0 && j < n) ? 1.0 : 0.0;
+    }
+}
+
+template <int D, int NT, bool C0>
+__global__ void __launch_bounds__(128) harvest_mvc_kernel(const HarvestParams P)
+{
+    const int64_t braw = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = braw < P.B;
+    const int64_t b = live ? braw : P.B - 1;
+    const int row = P.row_default;
+    const double dt = P.delta_t;
+
+    double cf[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) cf[t] = P.coef[b * P.coef_stride + t];
+    const double cz = C0 ? P.c0[b * P.c0_stride] : 0.0;
+
+    // scaling: ||B / reps||_inf <= THETA from the balanced row-sum bounds
+    double rb = 0.0;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        double r = C0 ? fabs(cz) * c_mvc.rs[MVC_NT][j] : 0.0;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) r = fma(fabs(cf[t]), c_mvc.rs[t][j], r);
+        rb = (r > rb || r != r) ? r : rb;
+    }
+    const double nrm = fabs(dt) * rb;
+    int status = LMEP_OK, s = 0;
+    if (!(nrm <= 1e9)) status = LMEP_NONFINITE;
+    else s = nrm > MVC_THETA ? (int)ceil(nrm / MVC_THETA) : 1;
+    const double dts = dt * (s > 1 ? 1.0 / (double)s : 1.0);
+    double al[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) al[t] = dts * cf[t];
+    const double alz = dts * cz;
+
+    double acc[D], v[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) acc[j] = v[j] = (j == row) ? 1.0 : 0.0;
+    int kt = 1, rep = 0, nmv = 0;
+    bool done = status != LMEP_OK;
+    while (__any_sync(FULL, !done)) {
+        // term k of the series restarted at acc: w = B^T v / k (1/k rides on the scalars)
+        const double ik = c_mvc.inv[kt];
+        double a[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) a[t] = al[t] * ik;
+        const double az = alz * ik;
+        double w[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            double y[NT];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                double p = c_mvc.tt[t][j][0] * v[0];
+#pragma unroll
+                for (int c = 1; c < D; ++c) p = fma(c_mvc.tt[t][j][c], v[c], p);
+                y[t] = p;
+            }
+            double o = a[0] * y[0];
+#pragma unroll
+            for (int t = 1; t < NT; ++t) o = fma(a[t], y[t], o);
+            if constexpr (C0) o = fma(az, v[j], o);
+            w[j] = o;
+        }
+        // rigorous stop: tau_k |w|_inf <= 2^-53 |acc_{k-1}|_inf (harvest_mvb.cuh)
+        unsigned ah = 0u, wh = 0u;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            ah = max(ah, mv_hiabs(acc[j]));
+            wh = max(wh, mv_hiabs(w[j]));
+        }
+        const double an = __hiloint2double((int)ah, 0);
+        const double wn = __hiloint2double((int)wh, -1) * c_mvc.tf[kt];
+        const bool conv = (an > 0.0 && wn <= 0x1p-53 * an) || kt >= MV_TMAX;
+        if (!done) {
+            ++nmv;
+#pragma unroll
+            for (int j = 0; j < D; ++j) acc[j] += w[j];
+            if (conv) {
+                kt = 1;
+                if (++rep >= s) done = true;
+#pragma unroll
+                for (int j = 0; j < D; ++j) v[j] = acc[j];
+            } else {
+                ++kt;
+#pragma unroll
+                for (int j = 0; j < D; ++j) v[j] = w[j];
+            }
+        }
+    }
+    if (!live) return;
+    const int n = P.n;
+    const int er = c_mvc.e[row];
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        const double o = status == LMEP_OK ? acc[j] * mv_pow2(c_mvc.e[j] - er)
+                                           : __longlong_as_double(0x7ff8000000000000LL);
+        bad |= !isfinite(o);
+        if (j < n) {
+            if (P.layout == 0) P.out[b * n + j] = o;
+            else P.out[(int64_t)j * P.out_ld + b] = o;
+        }
+    }
+    if (bad) status = LMEP_NONFINITE;
+    if (P.status) P.status[b] = status;
+    if (P.ms) P.ms[b] = nmv | (min(s, 255) << 24);
+}
+
+MvcConst *g_mvc_scratch = nullptr;
+cudaEvent_t g_mvc_done = nullptr;
+cudaStream_t g_mvc_last = nullptr;
+std::mutex g_mvc_mu;
+
+template <int D, int NT, bool C0>
+void launch_mvc_kernel(const HarvestParams &P, cudaStream_t st)
+{
+    const int64_t blocks = (P.B + 127) / 128;
+    harvest_mvc_kernel<D, NT, C0><<<(unsigned)blocks, 128, 0, st>>>(P);
+}
+
+template <int D>
+void launch_mvc_d(const HarvestParams &P, cudaStream_t st)
+{
+    const bool c0 = P.c0 != nullptr;
+    if (P.nterms == 1) {
+        if (c0) launch_mvc_kernel<D, 1, true>(P, st);
+        else launch_mvc_kernel<D, 1, false>(P, st);
+    } else {
+        if (c0) launch_mvc_kernel<D, 2, true>(P, st);
+        else launch_mvc_kernel<D, 2, false>(P, st);
+    }
+}
+
+}  // namespace
+
+bool harvest_mvc_eligible(const HarvestParams &P)
+{
+    return harvest_mvb_eligible(P) && P.s == 1 && P.d == P.n &&
+           (P.n == 7 || P.n == 9 || P.n == 11 || P.n == 13) && P.nterms >= 1 &&
+           P.nterms <= MVC_NT && P.row_default >= 0 && P.row_default < P.n &&
+           P.B < ((int64_t)1 << 31) * 128;
+}
+
+// The constant block is process-wide: calls are serialised in stream order,
+// and a call on another stream than the previous one first waits for the
+// previous call's kernel (event), so a later copy cannot overwrite tables an
+// earlier kernel still reads.
+int launch_harvest_mvc(const HarvestParams &P, cudaStream_t st)
+{
+    std::lock_guard<std::mutex> lock(g_mvc_mu);
+    cudaError_t e = cudaSuccess;
+    if (!g_mvc_scratch) {
+        e = cudaMalloc((void **)&g_mvc_scratch, sizeof(MvcConst));
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_mvc_done, cudaEventDisableTiming);
+        if (e != cudaSuccess) { set_last_error("harvest_mvc setup", e); return LMEP_CUDA_ERROR; }
+    } else if (st != g_mvc_last) {
+        e = cudaStreamWaitEvent(st, g_mvc_done, 0);
+        if (e != cudaSuccess) { set_last_error("cudaStreamWaitEvent", e); return LMEP_CUDA_ERROR; }
+    }
+    mvc_prep_kernel<<<1, 32, 0, st>>>(P, g_mvc_scratch);
+    e = cudaMemcpyToSymbolAsync(c_mvc, g_mvc_scratch, sizeof(MvcConst), 0, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) { set_last_error("cudaMemcpyToSymbolAsync", e); return LMEP_CUDA_ERROR; }
+    switch (P.n) {
+    case 7: launch_mvc_d<7>(P, st); break;
+    case 9: launch_mvc_d<9>(P, st); break;
+    case 11: launch_mvc_d<11>(P, st); break;
+    default: launch_mvc_d<13>(P, st); break;
+    }
+    cudaEventRecord(g_mvc_done, st);
+    g_mvc_last = st;
+    return launch_status("harvest_mvc_kernel");
+}
+
+}  // namespace lmep

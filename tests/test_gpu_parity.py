@@ -298,6 +298,82 @@ def test_block_balanced_harvest_reaction_and_single_term(lx, orc):
             assert _rows_rel(W[i], np.vstack([wl] + list(wp))) < W_TOL, i
 
 
+@pytest.mark.parametrize("n", [7, 9, 11, 13])
+@pytest.mark.parametrize("dtmul", [1.0, 4.0])
+@pytest.mark.parametrize("form", ["advdiff", "diffusion", "reaction"])
+def test_constant_table_harvest(lx, orc, n, dtmul, form):
+    """w_lin harvest of a large single-geometry per-node batch through the
+    constant-table kernel (harvest_mvc.cu: one item per lane, launch-uniform
+    balancing): against the oracle's per-node harvest on a sample of nodes and
+    against the block-balanced kernel (method "mvb") on every node."""
+    from paper_2603_15964_b200.harvest import harvest_compact
+    from paper_2603_15964_b200 import configs
+    N = 1 << 14
+    w5 = configs.c5(N=N, steps=1)
+    c, nu = w5.coef
+    g = lx.make_periodic_grid(N, 0.0, 1.0)
+    st = lx.select_stencils(g, n, lx.StencilPolicy.CENTERED)
+    row = (n - 1) // 2
+    dt = w5.delta_t * dtmul
+    r = np.sin(2 * np.pi * g.nodes) * 3e4
+    if form == "advdiff":
+        spec = lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1))
+        terms_of = lambda i: ((1, -c[i]), (2, nu[i]))
+    elif form == "diffusion":
+        spec = lx.VariableCoefficientSpec((2,), nu[:, None])
+        terms_of = lambda i: ((2, nu[i]),)
+    else:
+        spec = lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1), reaction=r)
+        terms_of = lambda i: ((1, -c[i]), (2, nu[i]), (0, r[i]))
+    stats = {}
+    W = harvest_compact(g, st, spec, dt, 1, (), stats).pernode.permute(2, 0, 1).cpu().numpy()
+    reps = torch.cat(stats["ms"]).cpu().numpy() >> 24
+    if dtmul > 1 and n >= 11:
+        assert reps.max() > 1, reps.max()
+    x = (np.arange(n) - row) * w5.h
+    for i in range(0, N, 331):
+        tm = terms_of(i)
+        L = orc.local_operator(x, tuple(t for t in tm if t[0] > 0))
+        for k, v in tm:
+            if k == 0:
+                L = L + v * np.eye(n)
+        wl, _ = orc.harvest_phi_weights(L, dt, 1, row, reduced=True)
+        assert _rows_rel(W[i], wl[None]) < W_TOL, i
+    lx._native.set_harvest_method("mvb")
+    try:
+        W2 = harvest_compact(g, st, spec, dt, 1).pernode.permute(2, 0, 1).cpu().numpy()
+    finally:
+        lx._native.set_harvest_method("multiply")
+    den = np.abs(W2).max(axis=2, keepdims=True)
+    assert (np.abs(W - W2) / den).max() < W_TOL
+
+
+def test_constant_table_harvest_streams(lx):
+    """The constant block is process-wide: back-to-back harvests of different
+    geometries on two streams still each see their own tables."""
+    from paper_2603_15964_b200.harvest import harvest_compact
+    from paper_2603_15964_b200 import configs
+    N = 1 << 13
+    w5 = configs.c5(N=N, steps=1)
+    c, nu = w5.coef
+    g = lx.make_periodic_grid(N, 0.0, 1.0)
+    spec = lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1))
+    ref = {}
+    for n in (9, 13):
+        st = lx.select_stencils(g, n, lx.StencilPolicy.CENTERED)
+        ref[n] = harvest_compact(g, st, spec, w5.delta_t, 1).pernode.clone()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = {}
+    for _ in range(3):
+        for n, strm in ((9, s1), (13, s2)):
+            with torch.cuda.stream(strm):
+                st = lx.select_stencils(g, n, lx.StencilPolicy.CENTERED)
+                outs[n] = harvest_compact(g, st, spec, w5.delta_t, 1).pernode
+    torch.cuda.synchronize()
+    for n in (9, 13):
+        assert torch.equal(outs[n], ref[n])
+
+
 def test_block_balanced_harvest_nonfinite(lx):
     from paper_2603_15964_b200.harvest import harvest_compact
     N = 8192
