@@ -199,6 +199,16 @@ def _coords_for(grid: Grid, sset: StencilSet, t: np.ndarray) -> torch.Tensor:
     return (nodes[m] - nodes[tt][:, None]).contiguous()
 
 
+def _coords0_host(grid: Grid, sset: StencilSet, plan) -> np.ndarray:
+    """The first window's local coordinates on the host (for the node checks):
+    computed directly on uniform / periodic grids (the same values _coords_for
+    uploads), else read back."""
+    if grid.periodic or grid.uniform_spacing is not None:
+        h = grid.spacing if grid.periodic else grid.uniform_spacing
+        return (np.arange(sset.n, dtype=np.int64) - int(plan.rows[0])).astype(np.float64) * h
+    return _ops.to_host(plan.coords[0])
+
+
 def _plan(grid: Grid, sset: StencilSet, frozen_nodes=(), force_pernode=False) -> _Plan:
     N, n, row = sset.N, sset.n, sset.row
     frozen = sorted({int(i) for i in frozen_nodes})
@@ -253,7 +263,7 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
     if max(k for k, _ in terms) > n - 1:
         from .errors import OrderTooHigh
         raise OrderTooHigh(f"operator order {max(k for k, _ in terms)} not representable on {n} nodes")
-    _ops.check_nodes(_ops.to_host(plan.coords[0]), max(k for k, _ in terms))
+    _ops.check_nodes(_coords0_host(grid, sset, plan), max(k for k, _ in terms))
     d = nat.device()
     if plan.mode != nat.W_PERNODE:
         tables, cf, c0 = _ops.operator_tables(plan.coords, terms)
