@@ -188,6 +188,33 @@ class C5:
                         node_range=(self.off, self.nloc))
         return self.torch.cat(stats["ms"]).cpu().numpy()
 
+    def harvest_launch_ms(self, reps=5):
+        """The harvest launch alone (lmep_harvest: prep + constant copy + kernel on
+        the current stream), CUDA events around `reps` launches on resident
+        tables and coefficients, for the roofline of the kernel itself."""
+        from paper_2603_15964_b200 import _ops
+        from paper_2603_15964_b200.harvest import _plan
+        torch = self.torch
+        plan = _plan(self.grid, self.sset, (), force_pernode=True)
+        tables, _, _ = _ops.operator_tables(plan.coords, ((1, 1.0), (2, 1.0)))
+        coef = self.coef[self.off:self.off + self.nloc]
+
+        def once():
+            return _ops.harvest(self.w.n, 1, self.w.delta_t, self.nloc, tables=tables, coef=coef,
+                                coef_stride=2, c0=None, c0_stride=0, row_default=self.sset.row,
+                                frozen_default=0, layout=1)
+        once()
+        e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            h = once()
+        e1.record()
+        torch.cuda.synchronize()
+        if int(h.status.abs().max().item()) != 0:
+            raise RuntimeError("harvest launch failed")
+        return e0.elapsed_time(e1) / reps
+
     def phase_ms(self):
         e0, e1, e2 = self.ev
         self.torch.cuda.synchronize()
@@ -469,7 +496,8 @@ def main():
     d = w.n                                               # s = 1: d = n
     flops = multiply_flops(d, ms_items)
     fp64 = fp64_peak()
-    harvest_tflops = flops / (harvest_ms * 1e-3) / 1e12
+    harvest_launch_ms = bench.harvest_launch_ms()
+    harvest_tflops = flops / (harvest_launch_ms * 1e-3) / 1e12
 
     onestep = time_c5_onestep() if world == 1 else None
 
@@ -506,11 +534,16 @@ def main():
             # the dominant kernel of the pass (ncu launch list: ~80% of device time) is
             # the FP64-bound harvest; the HBM-bound step kernel follows as roofline_step
             "roofline": {"bound": "fp64",
-                         "kernel": "harvest_mvb_kernel<13,2,2> (block-balanced per-node expm-multiply, 13x13, 2 lanes per item)",
+                         "kernel": "harvest_mvc_kernel<13,2,0> (per-node expm-multiply, one item per lane, "
+                                   "derivative tables as constant-bank DFMA operands)",
                          "achieved": harvest_tflops, "peak": fp64, "unit": "TFLOP/s",
                          "frac": harvest_tflops / fp64,
-                         "traffic": traffic("harvest_mvb_kernel<13,2,2>", "bytes_per_item", bench.nloc),
+                         "traffic": traffic("harvest_mvc_kernel<13,2,0>", "bytes_per_item", bench.nloc),
                          "algorithmic_flops_per_launch": flops,
+                         "launch_ms": harvest_launch_ms,
+                         "flops_note": "algorithmic = Taylor products x 2d^2 (one assembled d x d "
+                                       "mat-vec per term); the kernel issues one product per "
+                                       "derivative table (2x that) to keep no per-item matrix",
                          "peak_kind": "measured DFMA chains (tools/fp64_peak.cu), this run"},
             "roofline_step": {"bound": "hbm", "kernel": step_kernel,
                               "achieved": achieved, "peak": hbm, "unit": "GB/s",
