@@ -169,16 +169,27 @@ class C5:
     def device_pass(self):
         from paper_2603_15964_b200.distributed import NcclHalo, ShardedStepper, advance_all
         e0, e1, e2 = self.ev
+        from paper_2603_15964_b200 import _ops
         e0.record()
-        st = ShardedStepper(self.grid, self.sset, self.prob, self.scheme, self.w.delta_t,
-                            self.rank, self.world, NcclHalo(self.rank, self.world, True),
-                            exact=self.exact)
+        # the harvest status is checked after the pass (no sync between the
+        # harvest and the steps: the host enqueues the steps while it runs)
+        with _ops.deferred_status_checks() as pending:
+            st = ShardedStepper(self.grid, self.sset, self.prob, self.scheme, self.w.delta_t,
+                                self.rank, self.world, NcclHalo(self.rank, self.world, True),
+                                exact=self.exact)
         e1.record()
         st.u = self.u0[self.off:self.off + self.nloc].clone()
         advance_all(st, self.w.steps)
         e2.record()
-        self.last = {"stepper": st}
+        self.last = {"stepper": st, "pending": pending}
         return st.u
+
+    def check(self):
+        """The deferred harvest status and the finiteness of the last pass."""
+        from paper_2603_15964_b200 import _ops
+        _ops.check_deferred(self.last["pending"])
+        if not bool(self.torch.isfinite(self.last["stepper"].u).all().item()):
+            raise RuntimeError("config-5 pass produced non-finite values")
 
     def harvest_ms_stats(self):
         """(m, s) of every harvested matrix of this rank (separate run; FLOP accounting)."""
@@ -455,6 +466,7 @@ def main():
             stepm.append(s)
             times.append(h + s)
     torch.cuda.synchronize()
+    bench.check()
     launches = (lib.lmep_launch_count() - L0) / args.steps
     ms = float(np.mean(times))
     if world > 1:

@@ -7,6 +7,8 @@ combination of harvested rows that ``harvest.combine`` defines).
 
 from __future__ import annotations
 
+from contextlib import contextmanager
+
 import ctypes as C
 import warnings
 from dataclasses import dataclass, field
@@ -215,7 +217,33 @@ def harvest(n: int, s: int, delta_t: float, B: int, *, tables=None, table_idx=No
     return res
 
 
+_PENDING_STATUS: list | None = None
+
+
+@contextmanager
+def deferred_status_checks():
+    """Within the block, harvests queue their per-item status instead of
+    synchronising on it; the caller runs check_deferred(list) at its own sync
+    point (a pipeline that enqueues harvest + steps back to back)."""
+    global _PENDING_STATUS
+    prev, _PENDING_STATUS = _PENDING_STATUS, []
+    try:
+        yield _PENDING_STATUS
+    finally:
+        _PENDING_STATUS = prev
+
+
+def check_deferred(pending: list) -> None:
+    for status, what in pending:
+        if status.numel() and int(status.abs().max().item()) != 0:
+            nat.check(nat.LMEP_NONFINITE, what)
+    pending.clear()
+
+
 def raise_on_status(h: HarvestOut, what="matrix exponential overflowed") -> None:
+    if _PENDING_STATUS is not None:
+        _PENDING_STATUS.append((h.status, what))
+        return
     if int(h.status.abs().max().item() if h.status.numel() else 0) != 0:
         nat.check(nat.LMEP_NONFINITE, what)
 

@@ -43,6 +43,24 @@ def test_fornberg_bitwise(lx, golden):
         assert np.array_equal(c, golden[f"forn{i}_c"]), i
 
 
+@pytest.mark.parametrize("n,m", [(7, 2), (13, 3), (21, 20)])
+def test_fornberg_warp_and_thread_kernels_bitwise(lx, orc, n, m):
+    """Batches up to 4096 items take the warp-per-item kernel, larger ones the
+    thread-per-item kernel: both bit-identical to each other and to the oracle."""
+    from paper_2603_15964_b200 import _ops
+    rng = np.random.default_rng(n * 100 + m)
+    B = 5000
+    x = np.sort(rng.uniform(-1, 1, (B, n)), axis=1)
+    z = x[np.arange(B), rng.integers(0, n, B)]
+    xd, zd = _ops.dev_f64(x), _ops.dev_f64(z)
+    big = _ops.fornberg_dev(zd, xd, m).cpu().numpy()                  # thread kernel
+    small = np.concatenate([_ops.fornberg_dev(zd[a:a + 1000].contiguous(), xd[a:a + 1000].contiguous(), m)
+                            .cpu().numpy() for a in range(0, B, 1000)])   # warp kernel
+    assert np.array_equal(big, small)
+    for i in range(0, B, 701):
+        assert np.array_equal(small[i], orc.fornberg_weights(z[i], x[i], m))
+
+
 def test_local_operator_bitwise(lx, golden):
     for i in range(int(golden["lop_count"])):
         terms = tuple(zip(golden[f"lop{i}_k"].tolist(), golden[f"lop{i}_c"].tolist()))
@@ -384,6 +402,25 @@ def test_block_balanced_harvest_nonfinite(lx):
     with pytest.raises(lx.NonFinite):
         harvest_compact(g, st, lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1)),
                         w5.delta_t, 1)
+
+
+def test_deferred_harvest_status(lx):
+    """Inside deferred_status_checks() a failed harvest does not synchronise or
+    raise; check_deferred() raises NonFinite at the caller's sync point."""
+    from paper_2603_15964_b200 import _ops
+    from paper_2603_15964_b200.harvest import harvest_compact
+    N = 8192
+    w5, g, st = _c5_large(lx, N)
+    c, nu = w5.coef
+    nu = nu.copy()
+    nu[77] = np.inf
+    spec = lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1))
+    with _ops.deferred_status_checks() as pending:
+        rows = harvest_compact(g, st, spec, w5.delta_t, 1)
+    assert len(pending) == 1
+    assert torch.isnan(rows.pernode[:, :, 77]).all()
+    with pytest.raises(lx.NonFinite):
+        _ops.check_deferred(pending)
 
 
 @pytest.mark.parametrize("periodic", [True, False])
