@@ -50,6 +50,13 @@ struct MvcConst {
     double rs[MVC_NT + 1][MVC_D];      // row abs sums of tt[t]; rs[NT] = 1 (reaction: identity)
     double inv[52];                    // 1 / k
     double tf[52];                     // tail factor tau_k (||B||_inf <= THETA), inf while k + 2 <= THETA
+    // reflection-symmetric tables (centred stencils on uniform grids): with R the
+    // reversal j -> n-1-j, R T_t R = sg_t T_t, so T^T v follows from the halves
+    // u = v + Rv, m = v - Rv on rows 0..M (M = (n-1)/2); fp / fm fold the columns
+    double fp[MVC_NT][8][8];           // fp[t][i][j] = tt[i][j] + tt[i][n-1-j] (j < M), 2 tt[i][M]
+    double fm[MVC_NT][8][8];           // fm[t][i][j] = tt[i][j] - tt[i][n-1-j] (j < M)
+    double sg[MVC_NT];                 // reflection sign of table t
+    int sym;                           // 1: every table (anti)symmetric, exponents symmetric
     int e[MVC_D];
 };
 
@@ -82,6 +89,29 @@ __global__ void mvc_prep_kernel(const HarvestParams P, MvcConst *out)
         ee[j] = 0;
     }
     ok = __all_sync(FULL, ok);
+    // reflection (anti)symmetry of each raw table, within 1e-13 of its largest entry
+    __shared__ double sgs[MVC_NT];
+    bool sym = (n & 1) == 1;
+    for (int t = 0; t < nt; ++t) {
+        double amax = 0.0, dp = 0.0, dm = 0.0;
+        if (j < n)
+            for (int c = 0; c < n; ++c) {
+                const double a = P.tables[((int64_t)t * n + c) * n + j];
+                const double r = P.tables[((int64_t)t * n + (n - 1 - c)) * n + (n - 1 - j)];
+                amax = fmax(amax, fabs(a));
+                dp = fmax(dp, fabs(a - r));
+                dm = fmax(dm, fabs(a + r));
+            }
+        for (int o = 16; o > 0; o >>= 1) {
+            amax = fmax(amax, __shfl_xor_sync(FULL, amax, o));
+            dp = fmax(dp, __shfl_xor_sync(FULL, dp, o));
+            dm = fmax(dm, __shfl_xor_sync(FULL, dm, o));
+        }
+        const double tol = 1e-13 * amax;
+        if (dp <= tol) { if (j == 0) sgs[t] = 1.0; }
+        else if (dm <= tol) { if (j == 0) sgs[t] = -1.0; }
+        else sym = false;
+    }
     __syncwarp();
     for (int sweep = 0; ok && sweep < 12; ++sweep) {
         int k = 0;
@@ -108,6 +138,15 @@ __global__ void mvc_prep_kernel(const HarvestParams P, MvcConst *out)
         __syncwarp();
     }
     __syncwarp();
+    if (sym) {
+        // a symmetric similarity keeps the balanced tables (anti)symmetric
+        const int es = j < n ? (ee[j] + ee[n - 1 - j]) >> 1 : 0;
+        __syncwarp();
+        if (j < n) ee[j] = es;
+        __syncwarp();
+    }
+    if (j == 0) out->sym = sym ? 1 : 0;
+    if (j < MVC_NT) out->sg[j] = (sym && j < nt) ? sgs[j] : 1.0;
     if (j < MVC_D) {
         out->e[j] = j < n ? ee[j] : 0;
         for (int t = 0; t < MVC_NT; ++t) {
@@ -122,6 +161,23 @@ __global__ void mvc_prep_kernel(const HarvestParams P, MvcConst *out)
             out->rs[t][j] = sum;
         }
         out->rs[MVC_NT][j] = (c0 && j < n) ? 1.0 : 0.0;
+    }
+    // folded halves (rows i <= M) from the balanced tables
+    const int Mh = (n - 1) / 2;
+    if (j < 8) {
+        for (int t = 0; t < MVC_NT; ++t)
+            for (int c = 0; c < 8; ++c) {
+                double a = 0.0, b = 0.0;
+                if (sym && t < nt && j <= Mh && c <= Mh) {
+                    const double lo = P.tables[((int64_t)t * n + c) * n + j] * mv_pow2(ee[c] - ee[j]);
+                    const int c2 = n - 1 - c;
+                    const double hi = P.tables[((int64_t)t * n + c2) * n + j] * mv_pow2(ee[c2] - ee[j]);
+                    if (c < Mh) { a = lo + hi; b = lo - hi; }
+                    else a = 2.0 * lo;
+                }
+                out->fp[t][j][c] = a;
+                out->fm[t][j][c] = b;
+            }
     }
 }
 
@@ -213,21 +269,58 @@ __global__ void __launch_bounds__(128, 3) harvest_mvc_kernel(const HarvestParams
 #pragma unroll
         for (int t = 0; t < NT; ++t) a[t] = al[t] * ik;
         const double az = alz * ik;
+        if (c_mvc.sym) {
+            // T^T v = (T^T u + T^T m) / 2 with u = v + Rv, m = v - Rv: rows 0..M from
+            // the folded tables, rows n-1-i by the reflection signs (about 0.54 of
+            // the full products)
+            constexpr int M = (D - 1) / 2;
+            double u[M + 1], m[M];
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
-            double y[NT];
+            for (int c = 0; c < M; ++c) {
+                u[c] = v[c] + v[D - 1 - c];
+                m[c] = v[c] - v[D - 1 - c];
+            }
+            u[M] = v[M];
+            double h[NT], hs[NT];
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
-                double p = c_mvc.tt[t][j][0] * v[0];
-#pragma unroll
-                for (int c = 1; c < D; ++c) p = fma(c_mvc.tt[t][j][c], v[c], p);
-                y[t] = p;
+                h[t] = 0.5 * a[t];
+                hs[t] = h[t] * c_mvc.sg[t];
             }
-            double o = a[0] * y[0];
 #pragma unroll
-            for (int t = 1; t < NT; ++t) o = fma(a[t], y[t], o);
-            if constexpr (C0) o = fma(az, v[j], o);
-            w[j] = o;
+            for (int i = 0; i <= M; ++i) {
+                double lo = C0 ? az * v[i] : 0.0, hi = C0 ? az * v[D - 1 - i] : 0.0;
+#pragma unroll
+                for (int t = 0; t < NT; ++t) {
+                    double pu = c_mvc.fp[t][i][0] * u[0];
+#pragma unroll
+                    for (int c = 1; c <= M; ++c) pu = fma(c_mvc.fp[t][i][c], u[c], pu);
+                    double qm = c_mvc.fm[t][i][0] * m[0];
+#pragma unroll
+                    for (int c = 1; c < M; ++c) qm = fma(c_mvc.fm[t][i][c], m[c], qm);
+                    lo = fma(h[t], pu + qm, lo);
+                    hi = fma(hs[t], pu - qm, hi);
+                }
+                w[i] = lo;
+                if (i < M) w[D - 1 - i] = hi;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                double y[NT];
+#pragma unroll
+                for (int t = 0; t < NT; ++t) {
+                    double p = c_mvc.tt[t][j][0] * v[0];
+#pragma unroll
+                    for (int c = 1; c < D; ++c) p = fma(c_mvc.tt[t][j][c], v[c], p);
+                    y[t] = p;
+                }
+                double o = a[0] * y[0];
+#pragma unroll
+                for (int t = 1; t < NT; ++t) o = fma(a[t], y[t], o);
+                if constexpr (C0) o = fma(az, v[j], o);
+                w[j] = o;
+            }
         }
         advance();
     }

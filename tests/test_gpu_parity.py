@@ -366,6 +366,28 @@ def test_constant_table_harvest(lx, orc, n, dtmul, form):
     assert (np.abs(W - W2) / den).max() < W_TOL
 
 
+@pytest.mark.parametrize("n", [7, 13])
+def test_constant_table_harvest_upwind(lx, orc, n):
+    """One-sided upwind windows (row n-1): tables without reflection symmetry
+    take the kernel's full-product branch; oracle on a sample of nodes."""
+    from paper_2603_15964_b200.harvest import harvest_compact
+    from paper_2603_15964_b200 import configs
+    N = 1 << 13
+    w5 = configs.c5(N=N, steps=1)
+    c, nu = w5.coef
+    g = lx.make_periodic_grid(N, 0.0, 1.0)
+    st = lx.select_stencils(g, n, lx.StencilPolicy.ONE_SIDED_UPWIND)
+    row = n - 1
+    dt = w5.delta_t * 0.05
+    spec = lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1))
+    W = harvest_compact(g, st, spec, dt, 1).pernode.permute(2, 0, 1).cpu().numpy()
+    x = (np.arange(n) - row) * w5.h
+    for i in range(0, N, 293):
+        L = orc.local_operator(x, ((1, -c[i]), (2, nu[i])))
+        wl, _ = orc.harvest_phi_weights(L, dt, 1, row, reduced=True)
+        assert _rows_rel(W[i], wl[None]) < W_TOL, i
+
+
 def test_constant_table_harvest_streams(lx):
     """The constant block is process-wide: back-to-back harvests of different
     geometries on two streams still each see their own tables."""
