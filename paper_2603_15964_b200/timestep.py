@@ -386,7 +386,10 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
             u0d = _ops.dev_f64(u0)
         ev_u0 = cp1.record_event()
     try:
-        prep = prepare(grid, stencils, problem, scheme, delta_t, stats)
+        # the harvest's status is checked once it has finished (below), so the
+        # host runs ahead and prepares the stepping while the device harvests
+        with _ops.deferred_status_checks() as pending:
+            prep = prepare(grid, stencils, problem, scheme, delta_t, stats)
     finally:
         if deferred is not None:
             _ops.drop_deferred(deferred)
@@ -394,15 +397,16 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
         if deferred.event is None:           # the harvest did not pipeline: upload now
             deferred.issue(cp1)
         u0d, ev_u0 = deferred.dst, deferred.event
+    nsnap = 1 + -(-steps_total // snap_every)
+    # snapshots land straight in one page-locked [S, N] block (returned as is)
+    snaps = torch.empty((nsnap, N), dtype=torch.float64, pin_memory=True)
     torch.cuda.synchronize(dev)
     harvest_ns = time.perf_counter_ns() - t0
+    _ops.check_deferred(pending)
 
     cur.wait_event(ev_u0)
     u0d.record_stream(cur)
     st = Stepper(prep, u0d, exact=exact, tuning=tuning)
-    nsnap = 1 + -(-steps_total // snap_every)
-    # snapshots land straight in one page-locked [S, N] block (returned as is)
-    snaps = torch.empty((nsnap, N), dtype=torch.float64, pin_memory=True)
     snap_ev = None
 
     def snapshot(i):

@@ -2,7 +2,7 @@
 torch profiler: every kernel / copy with its start offset and duration, so the
 gaps between the harvest and the steps show up.  Diagnostic only.
 
-  python tools/timeline.py [--exact]
+  python tools/timeline.py [--exact] [--e2e]   (--e2e: the run() pass from host arrays)
 """
 import json
 import os
@@ -16,11 +16,12 @@ def main():
     from torch.profiler import ProfilerActivity, profile
     import bench
     b = bench.C5(0, 1, exact="--exact" in sys.argv)
+    fn = b.e2e_pass if "--e2e" in sys.argv else b.device_pass
     for _ in range(3):
-        b.device_pass()
+        fn()
     torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
-        b.device_pass()
+        fn()
         torch.cuda.synchronize()
     path = "/tmp/c5_trace.json"
     prof.export_chrome_trace(path)
@@ -31,7 +32,7 @@ def main():
     prev_end = t0
     for e in ev:
         gap = e["ts"] - prev_end
-        print(f"{e['ts'] - t0:9.1f} us  +gap {gap:7.1f}  dur {e['dur']:8.1f}  {e['name'][:90]}")
+        print(f"{e['ts'] - t0:9.1f} us  +gap {gap:7.1f}  dur {e['dur']:8.1f}  s{e.get('args', {}).get('stream', '?')}  {e['name'][:80]}")
         prev_end = max(prev_end, e["ts"] + e["dur"])
     print(f"span {prev_end - t0:.1f} us, busy {sum(e['dur'] for e in ev):.1f} us")
 
