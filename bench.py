@@ -226,6 +226,28 @@ class C5:
             raise RuntimeError("harvest launch failed")
         return e0.elapsed_time(e1) / reps
 
+    def phi_harvest(self, s=4, reps=3):
+        """SURVEY 8(d) C5 harvest benchmark: the per-node phi_0..phi_{s-1} rows
+        (reduced (n+s-1)^2 augmentation, 16 x 16 at s = 4) of every node, on
+        resident coefficients; returns (ms per harvest call, Taylor products)."""
+        from paper_2603_15964_b200.harvest import harvest_compact
+        torch = self.torch
+
+        def once(stats=None):
+            return harvest_compact(self.grid, self.sset, self.spec, self.w.delta_t, s, (), stats,
+                                   node_range=(self.off, self.nloc))
+        once()
+        e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            once()
+        e1.record()
+        torch.cuda.synchronize()
+        stats = {}
+        once(stats)
+        return e0.elapsed_time(e1) / reps, torch.cat(stats["ms"]).cpu().numpy()
+
     def phase_ms(self):
         e0, e1, e2 = self.ev
         self.torch.cuda.synchronize()
@@ -512,6 +534,8 @@ def main():
     harvest_tflops = flops / (harvest_launch_ms * 1e-3) / 1e12
 
     onestep = time_c5_onestep() if world == 1 else None
+    phi_ms, phi_items = bench.phi_harvest(4)
+    phi_flops = multiply_flops(w.n + 3, phi_items)
 
     # e2e through the public API
     for _ in range(2):
@@ -541,6 +565,11 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY 8(d))",
             "config": config,
             "harvests_per_s": w.N / (harvest_ms * 1e-3),
+            # the per-node phi_0..phi_3 harvest (reduced 16 x 16), timed
+            # alone through harvest_compact (constant-table kernel, harvest_mvc.cu)
+            "harvest_phi4": {"harvests_per_s": bench.nloc / (phi_ms * 1e-3), "ms": phi_ms,
+                             "d": w.n + 3, "algorithmic_tflops": phi_flops / (phi_ms * 1e-3) / 1e12,
+                             "fp64_frac": phi_flops / (phi_ms * 1e-3) / 1e12 / fp64},
             "phases_ms": {"harvest": harvest_ms, "steps": step_ms,
                           "per_step_launch_ms": per_launch_ms},
             # the dominant kernel of the pass (ncu launch list: ~80% of device time) is

@@ -226,8 +226,9 @@ int lmep_harvest_chunk(int n, int s, int nterms, const double *tables, const int
                        void *stream);
 
 /* Harvest algorithm for d <= 16:
- *   0 (default) = expm-multiply: large single-geometry w_lin batches (s = 1,
- *     n in {7, 9, 11, 13}, <= 2 tables, B >= 4096) take the constant-table
+ *   0 (default) = expm-multiply: large single-geometry batches (n in
+ *     {7, 9, 11, 13}, B >= 4096; s = 1 with <= 2 tables, or s <= 4 with two
+ *     tables and no reaction) take the constant-table
  *     kernel (harvest_mvc.cu: one item per lane, launch-uniform balancing,
  *     tables as constant-bank operands); other large single-geometry
  *     batches (B >= 4096, one

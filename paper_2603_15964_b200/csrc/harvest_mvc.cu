@@ -1,10 +1,12 @@
 // harvest_mvc.cu -- K1 for the largest per-node batches: one item per lane,
 // the shared derivative tables as constant-bank operands.
 //
-// Scope: the w_lin harvest (s = 1, harvest.py:73-79 / harvest_propagator) of
-// a single table geometry with per-item coefficients (periodic / uniform grids
-// with variable coefficients, BASELINE config 5), n in {7, 9, 11, 13}, one or
-// two derivative tables plus an optional reaction term.  Same mathematics as
+// Scope: per-item harvests of a single table geometry with per-item
+// coefficients (periodic / uniform grids with variable coefficients, BASELINE
+// config 5), n in {7, 9, 11, 13}: the w_lin row (s = 1, harvest.py:73-79) with
+// one or two derivative tables plus an optional reaction term, and the raw
+// dt^j phi_j rows (s = 2..4, harvest.py:97-121) of two-table operators through
+// the reduced (n + s - 1) augmentation.  Same mathematics as
 // harvest_mvb.cuh: row r of exp(dt L_b) is exp(B^T)^reps e_r with
 // B = S^-1 (dt L_b / reps) S, S a power-of-two balancing (expm.py:27-30), the
 // Taylor series stopped by the rigorous tail bound (||B||_inf <= 4), the
@@ -57,6 +59,11 @@ struct MvcConst {
     double fm[MVC_NT][8][8];           // fm[t][i][j] = tt[i][j] - tt[i][n-1-j] (j < M)
     double sg[MVC_NT];                 // reflection sign of table t
     int sym;                           // 1: every table (anti)symmetric, exponents symmetric
+    // phi rows (s > 1): the reduced augmentation's entries A^T[row][n] and
+    // A^T[j][j+1] (n <= j < d-1) are dt; ax[k] their balancing scales, rsa[j]
+    // their |dt|-scaled row abs sums
+    double ax[4];
+    double rsa[MVC_D];
     int e[MVC_D];
 };
 
@@ -69,7 +76,7 @@ __global__ void mvc_prep_kernel(const HarvestParams P, MvcConst *out)
     __shared__ double M[MVC_D][MVC_D + 1];
     __shared__ int kk[MVC_D];
     __shared__ int ee[MVC_D];
-    const int j = threadIdx.x, n = P.n, nt = P.nterms;
+    const int j = threadIdx.x, n = P.n, nt = P.nterms, d = P.d, row = P.row_default;
     const bool c0 = P.c0 != nullptr;
     for (int k = j; k < 52; k += 32) {
         out->inv[k] = k > 0 ? 1.0 / (double)k : 0.0;
@@ -86,6 +93,10 @@ __global__ void mvc_prep_kernel(const HarvestParams P, MvcConst *out)
             M[j][c] = xmul(P.delta_t, l);
             ok &= (bool)isfinite(M[j][c]);
         }
+    }
+    if (j < d) {
+        for (int c = (j < n ? n : 0); c < d; ++c)
+            M[j][c] = ((c == n && j == row) || (j >= n && c == j + 1)) ? P.delta_t : 0.0;
         ee[j] = 0;
     }
     ok = __all_sync(FULL, ok);
@@ -115,9 +126,9 @@ __global__ void mvc_prep_kernel(const HarvestParams P, MvcConst *out)
     __syncwarp();
     for (int sweep = 0; ok && sweep < 12; ++sweep) {
         int k = 0;
-        if (j < n) {
+        if (j < d) {
             double r2 = 0.0, c2 = 0.0;
-            for (int c = 0; c < n; ++c) {
+            for (int c = 0; c < d; ++c) {
                 r2 = fma(M[j][c], M[j][c], r2);
                 c2 = fma(M[c][j], M[c][j], c2);
             }
@@ -130,8 +141,8 @@ __global__ void mvc_prep_kernel(const HarvestParams P, MvcConst *out)
         }
         if (!__any_sync(FULL, k != 0)) break;
         __syncwarp();
-        if (j < n) {
-            for (int c = 0; c < n; ++c)
+        if (j < d) {
+            for (int c = 0; c < d; ++c)
                 if (kk[c] != k) M[j][c] *= mv_pow2(kk[c] - k);
             ee[j] += k;
         }
@@ -146,9 +157,19 @@ __global__ void mvc_prep_kernel(const HarvestParams P, MvcConst *out)
         __syncwarp();
     }
     if (j == 0) out->sym = sym ? 1 : 0;
+    if (j < 4) {
+        const int r0 = j == 0 ? row : n + j - 1, c1 = n + j;
+        out->ax[j] = c1 < d ? mv_pow2(ee[c1] - ee[r0]) : 0.0;
+    }
+    if (j < MVC_D) {
+        double ra = 0.0;
+        if (j == row && d > n) ra += fabs(P.delta_t) * mv_pow2(ee[n] - ee[row]);
+        if (j >= n && j + 1 < d) ra += fabs(P.delta_t) * mv_pow2(ee[j + 1] - ee[j]);
+        out->rsa[j] = ra;
+    }
     if (j < MVC_NT) out->sg[j] = (sym && j < nt) ? sgs[j] : 1.0;
     if (j < MVC_D) {
-        out->e[j] = j < n ? ee[j] : 0;
+        out->e[j] = j < d ? ee[j] : 0;
         for (int t = 0; t < MVC_NT; ++t) {
             double sum = 0.0;
             for (int c = 0; c < MVC_D; ++c) {
@@ -182,10 +203,12 @@ __global__ void mvc_prep_kernel(const HarvestParams P, MvcConst *out)
 }
 
 // 3 CTAs per SM (<= 168 registers): 12 warps hide the DFMA and constant-load
-// latency better than 8 warps at the unbounded 174 (measured 1.01 vs 1.09 ms)
-template <int D, int NT, bool C0>
+// latency better than 8 warps at the unbounded 174 (measured 1.01 vs 1.09 ms).
+// N = n (the operator block), PA = s - 1 augmentation columns (phi rows).
+template <int N, int NT, bool C0, int PA>
 __global__ void __launch_bounds__(128, 3) harvest_mvc_kernel(const HarvestParams P)
 {
+    constexpr int D = N + PA;
     const int64_t braw = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const bool live = braw < P.B;
     const int64_t b = live ? braw : P.B - 1;
@@ -198,15 +221,18 @@ __global__ void __launch_bounds__(128, 3) harvest_mvc_kernel(const HarvestParams
     const double cz = C0 ? P.c0[b * P.c0_stride] : 0.0;
 
     // scaling: ||B / reps||_inf <= THETA from the balanced row-sum bounds
-    double rb = 0.0;
+    double nrm = 0.0;
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-        double r = C0 ? fabs(cz) * c_mvc.rs[MVC_NT][j] : 0.0;
+        double r = 0.0;
+        if (j < N) {
+            r = C0 ? fabs(cz) * c_mvc.rs[MVC_NT][j] : 0.0;
 #pragma unroll
-        for (int t = 0; t < NT; ++t) r = fma(fabs(cf[t]), c_mvc.rs[t][j], r);
-        rb = (r > rb || r != r) ? r : rb;
+            for (int t = 0; t < NT; ++t) r = fma(fabs(cf[t]), c_mvc.rs[t][j], r);
+        }
+        r = fma(fabs(dt), r, PA > 0 ? c_mvc.rsa[j] : 0.0);
+        nrm = (r > nrm || r != r) ? r : nrm;
     }
-    const double nrm = fabs(dt) * rb;
     int status = LMEP_OK, s = 0;
     if (!(nrm <= 1e9)) status = LMEP_NONFINITE;
     else s = nrm > MVC_THETA ? (int)ceil(nrm / MVC_THETA) : 1;
@@ -218,14 +244,16 @@ __global__ void __launch_bounds__(128, 3) harvest_mvc_kernel(const HarvestParams
 
     double acc[D], v[D], w[D];
     int kt = 1, rep = 0, nmv = 0;
-    bool done = status != LMEP_OK;
+    bool done = true, bad = false;
     // update after term kt (in w): rigorous stop tau_k |w|_inf <= 2^-53 |acc_{k-1}|_inf,
     // then the next iterate (w, or acc when a repetition of the series restarts)
     auto advance = [&]() {
+        // scale: the extracted rows only (the augmentation entries of a phi
+        // series are O(1) while its extracted rows are O(dt^j), harvest_mvb.cuh)
         unsigned ah = 0u, wh = 0u;
 #pragma unroll
         for (int j = 0; j < D; ++j) {
-            ah = max(ah, mv_hiabs(acc[j]));
+            if (j < N) ah = max(ah, mv_hiabs(acc[j]));
             wh = max(wh, mv_hiabs(w[j]));
         }
         const double an = __hiloint2double((int)ah, 0);
@@ -247,97 +275,121 @@ __global__ void __launch_bounds__(128, 3) harvest_mvc_kernel(const HarvestParams
             }
         }
     };
+    const int n = P.n;
+#pragma unroll 1
+    for (int qo = 0; qo <= PA; ++qo) {
+        // w_lin: row `row` of exp(A); raw dt^j phi_j rows: rows n + j - 1 (harvest.py:119-120)
+        const int idx = qo == 0 ? row : N + qo - 1;
 #pragma unroll
-    for (int j = 0; j < D; ++j) acc[j] = (j == row) ? 1.0 : 0.0;
-    // term 1 on e_r is column r of the scaled tables (no product)
-    {
-        const double *t0 = &c_mvc.tt[0][0][0] + row;
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-            double o = al[0] * t0[j * MVC_D];
-#pragma unroll
-            for (int t = 1; t < NT; ++t) o = fma(al[t], t0[(t * MVC_D + j) * MVC_D], o);
-            if constexpr (C0) o = fma(alz, acc[j], o);
-            w[j] = o;
-        }
-    }
-    advance();
-    while (__any_sync(FULL, !done)) {
-        // term k of the series restarted at acc: w = B^T v / k (1/k rides on the scalars)
-        const double ik = c_mvc.inv[kt];
-        double a[NT];
-#pragma unroll
-        for (int t = 0; t < NT; ++t) a[t] = al[t] * ik;
-        const double az = alz * ik;
-        if (c_mvc.sym) {
-            // T^T v = (T^T u + T^T m) / 2 with u = v + Rv, m = v - Rv: rows 0..M from
-            // the folded tables, rows n-1-i by the reflection signs (about 0.54 of
-            // the full products)
-            constexpr int M = (D - 1) / 2;
-            double u[M + 1], m[M];
-#pragma unroll
-            for (int c = 0; c < M; ++c) {
-                u[c] = v[c] + v[D - 1 - c];
-                m[c] = v[c] - v[D - 1 - c];
-            }
-            u[M] = v[M];
-            double h[NT], hs[NT];
-#pragma unroll
-            for (int t = 0; t < NT; ++t) {
-                h[t] = 0.5 * a[t];
-                hs[t] = h[t] * c_mvc.sg[t];
-            }
-#pragma unroll
-            for (int i = 0; i <= M; ++i) {
-                double lo = C0 ? az * v[i] : 0.0, hi = C0 ? az * v[D - 1 - i] : 0.0;
-#pragma unroll
-                for (int t = 0; t < NT; ++t) {
-                    double pu = c_mvc.fp[t][i][0] * u[0];
-#pragma unroll
-                    for (int c = 1; c <= M; ++c) pu = fma(c_mvc.fp[t][i][c], u[c], pu);
-                    double qm = c_mvc.fm[t][i][0] * m[0];
-#pragma unroll
-                    for (int c = 1; c < M; ++c) qm = fma(c_mvc.fm[t][i][c], m[c], qm);
-                    lo = fma(h[t], pu + qm, lo);
-                    hi = fma(hs[t], pu - qm, hi);
-                }
-                w[i] = lo;
-                if (i < M) w[D - 1 - i] = hi;
-            }
-        } else {
+        for (int j = 0; j < D; ++j) acc[j] = v[j] = (j == idx) ? 1.0 : 0.0;
+        kt = 1;
+        rep = 0;
+        done = status != LMEP_OK;
+        if (qo == 0) {
+            // term 1 on e_r is column r of the scaled tables (no product); the
+            // augmentation rows see no top-block entry
+            const double *t0 = &c_mvc.tt[0][0][0] + row;
 #pragma unroll
             for (int j = 0; j < D; ++j) {
-                double y[NT];
+                double o = 0.0;
+                if (j < N) {
+                    o = al[0] * t0[j * MVC_D];
 #pragma unroll
-                for (int t = 0; t < NT; ++t) {
-                    double p = c_mvc.tt[t][j][0] * v[0];
-#pragma unroll
-                    for (int c = 1; c < D; ++c) p = fma(c_mvc.tt[t][j][c], v[c], p);
-                    y[t] = p;
+                    for (int t = 1; t < NT; ++t) o = fma(al[t], t0[(t * MVC_D + j) * MVC_D], o);
+                    if constexpr (C0) o = fma(alz, acc[j], o);
                 }
-                double o = a[0] * y[0];
-#pragma unroll
-                for (int t = 1; t < NT; ++t) o = fma(a[t], y[t], o);
-                if constexpr (C0) o = fma(az, v[j], o);
                 w[j] = o;
             }
+            advance();
         }
-        advance();
+        while (__any_sync(FULL, !done)) {
+            // term k of the series restarted at acc: w = B^T v / k (1/k rides on the scalars)
+            const double ik = c_mvc.inv[kt];
+            double a[NT];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) a[t] = al[t] * ik;
+            const double az = alz * ik;
+            if (c_mvc.sym) {
+                // T^T v = (T^T u + T^T m) / 2 with u = v + Rv, m = v - Rv: rows 0..M from
+                // the folded tables, rows n-1-i by the reflection signs (about 0.54 of
+                // the full products)
+                constexpr int M = (N - 1) / 2;
+                double u[M + 1], m[M];
+#pragma unroll
+                for (int c = 0; c < M; ++c) {
+                    u[c] = v[c] + v[N - 1 - c];
+                    m[c] = v[c] - v[N - 1 - c];
+                }
+                u[M] = v[M];
+                double h[NT], hs[NT];
+#pragma unroll
+                for (int t = 0; t < NT; ++t) {
+                    h[t] = 0.5 * a[t];
+                    hs[t] = h[t] * c_mvc.sg[t];
+                }
+#pragma unroll
+                for (int i = 0; i <= M; ++i) {
+                    double lo = C0 ? az * v[i] : 0.0, hi = C0 ? az * v[N - 1 - i] : 0.0;
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) {
+                        double pu = c_mvc.fp[t][i][0] * u[0];
+#pragma unroll
+                        for (int c = 1; c <= M; ++c) pu = fma(c_mvc.fp[t][i][c], u[c], pu);
+                        double qm = c_mvc.fm[t][i][0] * m[0];
+#pragma unroll
+                        for (int c = 1; c < M; ++c) qm = fma(c_mvc.fm[t][i][c], m[c], qm);
+                        lo = fma(h[t], pu + qm, lo);
+                        hi = fma(hs[t], pu - qm, hi);
+                    }
+                    w[i] = lo;
+                    if (i < M) w[N - 1 - i] = hi;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < N; ++j) {
+                    double y[NT];
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) {
+                        double p = c_mvc.tt[t][j][0] * v[0];
+#pragma unroll
+                        for (int c = 1; c < N; ++c) p = fma(c_mvc.tt[t][j][c], v[c], p);
+                        y[t] = p;
+                    }
+                    double o = a[0] * y[0];
+#pragma unroll
+                    for (int t = 1; t < NT; ++t) o = fma(a[t], y[t], o);
+                    if constexpr (C0) o = fma(az, v[j], o);
+                    w[j] = o;
+                }
+            }
+            if constexpr (PA > 0) {
+                // augmentation: (B^T v)[row] += dt' v[n], (B^T v)[j] = dt' v[j+1] (n <= j < d-1)
+                const double g = dts * ik;
+                const double g0 = g * c_mvc.ax[0] * v[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i)
+                    if (i == row) w[i] += g0;
+#pragma unroll
+                for (int k = 0; k + 1 < PA; ++k) w[N + k] = (g * c_mvc.ax[k + 1]) * v[N + k + 1];
+                w[D - 1] = 0.0;
+            }
+            advance();
+        }
+        if (live) {
+            const int ei = c_mvc.e[idx];
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                const double o = status == LMEP_OK ? acc[j] * mv_pow2(c_mvc.e[j] - ei)
+                                                   : __longlong_as_double(0x7ff8000000000000LL);
+                bad |= !isfinite(o);
+                if (j < n) {
+                    if (P.layout == 0) P.out[(b * (PA + 1) + qo) * n + j] = o;
+                    else P.out[((int64_t)qo * n + j) * P.out_ld + b] = o;
+                }
+            }
+        }
     }
     if (!live) return;
-    const int n = P.n;
-    const int er = c_mvc.e[row];
-    bool bad = false;
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-        const double o = status == LMEP_OK ? acc[j] * mv_pow2(c_mvc.e[j] - er)
-                                           : __longlong_as_double(0x7ff8000000000000LL);
-        bad |= !isfinite(o);
-        if (j < n) {
-            if (P.layout == 0) P.out[b * n + j] = o;
-            else P.out[(int64_t)j * P.out_ld + b] = o;
-        }
-    }
     if (bad) status = LMEP_NONFINITE;
     if (P.status) P.status[b] = status;
     if (P.ms) P.ms[b] = nmv | (min(s, 255) << 24);
@@ -348,23 +400,27 @@ cudaEvent_t g_mvc_done = nullptr;
 cudaStream_t g_mvc_last = nullptr;
 std::mutex g_mvc_mu;
 
-template <int D, int NT, bool C0>
+template <int N, int NT, bool C0, int PA>
 void launch_mvc_kernel(const HarvestParams &P, cudaStream_t st)
 {
     const int64_t blocks = (P.B + 127) / 128;
-    harvest_mvc_kernel<D, NT, C0><<<(unsigned)blocks, 128, 0, st>>>(P);
+    harvest_mvc_kernel<N, NT, C0, PA><<<(unsigned)blocks, 128, 0, st>>>(P);
 }
 
-template <int D>
+template <int N>
 void launch_mvc_d(const HarvestParams &P, cudaStream_t st)
 {
     const bool c0 = P.c0 != nullptr;
-    if (P.nterms == 1) {
-        if (c0) launch_mvc_kernel<D, 1, true>(P, st);
-        else launch_mvc_kernel<D, 1, false>(P, st);
+    if (P.s > 1) {                       // phi rows: two tables, no reaction (eligibility)
+        if (P.s == 2) launch_mvc_kernel<N, 2, false, 1>(P, st);
+        else if (P.s == 3) launch_mvc_kernel<N, 2, false, 2>(P, st);
+        else launch_mvc_kernel<N, 2, false, 3>(P, st);
+    } else if (P.nterms == 1) {
+        if (c0) launch_mvc_kernel<N, 1, true, 0>(P, st);
+        else launch_mvc_kernel<N, 1, false, 0>(P, st);
     } else {
-        if (c0) launch_mvc_kernel<D, 2, true>(P, st);
-        else launch_mvc_kernel<D, 2, false>(P, st);
+        if (c0) launch_mvc_kernel<N, 2, true, 0>(P, st);
+        else launch_mvc_kernel<N, 2, false, 0>(P, st);
     }
 }
 
@@ -372,7 +428,8 @@ void launch_mvc_d(const HarvestParams &P, cudaStream_t st)
 
 bool harvest_mvc_eligible(const HarvestParams &P)
 {
-    return harvest_mvb_eligible(P) && P.s == 1 && P.d == P.n &&
+    return harvest_mvb_eligible(P) && P.s >= 1 && P.s <= 4 && P.d == P.n + P.s - 1 &&
+           (P.s == 1 || (P.nterms == 2 && P.c0 == nullptr)) &&
            (P.n == 7 || P.n == 9 || P.n == 11 || P.n == 13) && P.nterms >= 1 &&
            P.nterms <= MVC_NT && P.row_default >= 0 && P.row_default < P.n &&
            P.B < ((int64_t)1 << 31) * 128;

@@ -367,9 +367,11 @@ def test_constant_table_harvest(lx, orc, n, dtmul, form):
 
 
 @pytest.mark.parametrize("n", [7, 13])
-def test_constant_table_harvest_upwind(lx, orc, n):
+@pytest.mark.parametrize("s", [1, 3])
+def test_constant_table_harvest_upwind(lx, orc, n, s):
     """One-sided upwind windows (row n-1): tables without reflection symmetry
-    take the kernel's full-product branch; oracle on a sample of nodes."""
+    take the kernel's full-product branch (w_lin and phi rows); oracle on a
+    sample of nodes."""
     from paper_2603_15964_b200.harvest import harvest_compact
     from paper_2603_15964_b200 import configs
     N = 1 << 13
@@ -380,12 +382,12 @@ def test_constant_table_harvest_upwind(lx, orc, n):
     row = n - 1
     dt = w5.delta_t * 0.05
     spec = lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1))
-    W = harvest_compact(g, st, spec, dt, 1).pernode.permute(2, 0, 1).cpu().numpy()
+    W = harvest_compact(g, st, spec, dt, s).pernode.permute(2, 0, 1).cpu().numpy()
     x = (np.arange(n) - row) * w5.h
     for i in range(0, N, 293):
         L = orc.local_operator(x, ((1, -c[i]), (2, nu[i])))
-        wl, _ = orc.harvest_phi_weights(L, dt, 1, row, reduced=True)
-        assert _rows_rel(W[i], wl[None]) < W_TOL, i
+        wl, wp = orc.harvest_phi_weights(L, dt, s, row, reduced=True)
+        assert _rows_rel(W[i], np.vstack([wl] + list(wp))) < W_TOL, i
 
 
 def test_constant_table_harvest_streams(lx):
