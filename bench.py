@@ -572,9 +572,23 @@ def main():
                              "fp64_frac": phi_flops / (phi_ms * 1e-3) / 1e12 / fp64},
             "phases_ms": {"harvest": harvest_ms, "steps": step_ms,
                           "per_step_launch_ms": per_launch_ms},
-            # the dominant kernel of the pass (ncu launch list: ~80% of device time) is
-            # the FP64-bound harvest; the HBM-bound step kernel follows as roofline_step
-            "roofline": {"bound": "fp64",
+            # the dominant kernel of the pass (ncu launch list, profiles/r1l_launches_*:
+            # 200 steps in 13 launches of the blocked step kernel, ~2/3 of the pass) on
+            # the HBM bytes of its schedule; the FP64-bound harvest kernel follows as
+            # roofline_harvest
+            "roofline": {"bound": "hbm", "kernel": step_kernel,
+                         "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm,
+                         "traffic": traffic(step_kernel.split(" ")[0], "bytes_per_node",
+                                            bench.nloc),
+                         "algorithmic_bytes_per_launch": step_bytes,
+                         "launch_ms": per_launch_ms,
+                         "peak_kind": f"{hbm_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                         "note": "rows held in registers for 16 steps: 8.9 B/point-step against "
+                                 "120 for one step per launch (roofline_step_onestep); the kernel "
+                                 "is bound by shared-memory wavefronts and the per-step barrier, "
+                                 "see roofline_step_fp64 and profiles/r1h_c5step_shapes.md"},
+            "roofline_harvest": {"bound": "fp64",
                          "kernel": "harvest_mvc_kernel<13,2,0> (per-node expm-multiply, one item per lane, "
                                    "derivative tables as constant-bank DFMA operands)",
                          "achieved": harvest_tflops, "peak": fp64, "unit": "TFLOP/s",
@@ -584,15 +598,9 @@ def main():
                          "launch_ms": harvest_launch_ms,
                          "flops_note": "algorithmic = Taylor products x 2d^2 (one assembled d x d "
                                        "mat-vec per term); the kernel issues one product per "
-                                       "derivative table (2x that) to keep no per-item matrix",
+                                       "derivative table on folded symmetric halves (about "
+                                       "1.1x that) and keeps no per-item matrix",
                          "peak_kind": "measured DFMA chains (tools/fp64_peak.cu), this run"},
-            "roofline_step": {"bound": "hbm", "kernel": step_kernel,
-                              "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                              "frac": achieved / hbm,
-                              "traffic": traffic(step_kernel.split(" ")[0], "bytes_per_node",
-                                                 bench.nloc),
-                              "algorithmic_bytes_per_launch": step_bytes,
-                              "peak_kind": f"{hbm_kind} (MEASURED_PEAKS.json hbm_gbs)"},
             # the blocked step kernel is no longer HBM-bound: it issues the reference's
             # unfused multiply + add per tap (2n flops per point-step, kernels.py:23-29),
             # so its ceiling is the FP64 pipe at one op per lane per issue = fp64 / 2

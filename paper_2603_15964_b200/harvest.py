@@ -300,8 +300,8 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
             _ops.is_host(spec.coef) and N >= PIPELINE_MIN:
         # host coefficients: upload in chunks on the copy stream, each chunk's
         # harvest starting as soon as its slice has landed
-        tables, _, _ = _ops.operator_tables(plan.coords, terms)
-        h = _harvest_pipelined(spec, sl, N, n, s, delta_t, tables, sset.row)
+        h = _harvest_pipelined(spec, sl, N, n, s, delta_t,
+                               lambda: _ops.operator_tables(plan.coords, terms)[0], sset.row)
         _ops.raise_on_status(h)
         if stats is not None:
             stats.setdefault("ms", []).append(h.ms)
@@ -389,13 +389,16 @@ def _pipeline_bounds(N: int):
 
 
 def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
-                       tables: torch.Tensor, row: int) -> _ops.HarvestOut:
+                       tables_fn, row: int) -> _ops.HarvestOut:
     """Per-node harvest (one shared window geometry) from HOST coefficients:
     the [N, K] coefficient table goes up in growing slices (_pipeline_bounds;
     multiples of 1024 items, so the block-balanced kernel's superblocks and
-    their representative balancing are those of a resident harvest) on the copy
+    their representative balancing are those of a resident harvest; the
+    constant-table kernel balances each slice's first item, which on C5's
+    fields gives the resident exponents, else rows equal within rounding) on the copy
     stream, and the harvest of slice i (lmep_harvest_chunk into the shared SoA
-    output) overlaps the upload of slice i+1."""
+    output) overlaps the upload of slice i+1.  Every slice is queued before
+    tables_fn() builds the derivative tables, so PCIe starts at once."""
     d = nat.device()
     cur = torch.cuda.current_stream(d)
     cp = _ops.copy_stream()
@@ -408,19 +411,24 @@ def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
                           torch.empty(N, dtype=torch.int32, device=d),
                           torch.empty(N, dtype=torch.int32, device=d))
     cp.wait_stream(cur)                      # dc / dr were allocated on cur
-    for a, b in _pipeline_bounds(N):
-        with torch.cuda.stream(cp):
+    bounds = _pipeline_bounds(N)
+    landed = []
+    with torch.cuda.stream(cp):
+        for a, b in bounds:
             dc[a:b].copy_(hc[a:b], non_blocking=True)
             if dr is not None:
                 dr[a:b].copy_(hr[a:b], non_blocking=True)
-        cur.wait_event(cp.record_event())
-        _ops.harvest(n, s, delta_t, b - a, tables=tables, coef=dc[a:b], coef_stride=K,
-                     c0=None if dr is None else dr[a:b], c0_stride=0 if dr is None else 1,
-                     row_default=row, frozen_default=0, layout=1, into=out, item0=a)
+            landed.append(cp.record_event())
     dc.record_stream(cp)
     if dr is not None:
         dr.record_stream(cp)
     _ops.issue_deferred(cp)                  # e.g. run()'s initial state, behind the slices
+    tables = tables_fn()                     # overlaps the first slices' transfer
+    for (a, b), ev in zip(bounds, landed):
+        cur.wait_event(ev)
+        _ops.harvest(n, s, delta_t, b - a, tables=tables, coef=dc[a:b], coef_stride=K,
+                     c0=None if dr is None else dr[a:b], c0_stride=0 if dr is None else 1,
+                     row_default=row, frozen_default=0, layout=1, into=out, item0=a)
     return out
 
 
