@@ -390,6 +390,35 @@ def test_constant_table_harvest_upwind(lx, orc, n, s):
         assert _rows_rel(W[i], np.vstack([wl] + list(wp))) < W_TOL, i
 
 
+def test_c5_full_size_kernels_agree(lx):
+    """BASELINE config 5 at full size (2^22 nodes): the constant-table harvest
+    against the block-balanced kernel on every node (two independent
+    formulations, 1e-12), and 200 steps in the FMA mode against the bit-exact
+    mode through run() (1e-13 on the state)."""
+    from paper_2603_15964_b200.harvest import harvest_compact
+    from paper_2603_15964_b200 import _ops, configs
+    w5 = configs.c5()
+    c, nu = w5.coef
+    g = lx.make_periodic_grid(w5.N, 0.0, 1.0)
+    st = lx.select_stencils(g, w5.n, lx.StencilPolicy.CENTERED)
+    spec = lx.VariableCoefficientSpec((1, 2), _ops.dev_f64(np.stack([-c, nu], 1)))
+    W = harvest_compact(g, st, spec, w5.delta_t, 1).pernode
+    lx._native.set_harvest_method("mvb")
+    try:
+        W2 = harvest_compact(g, st, spec, w5.delta_t, 1).pernode
+    finally:
+        lx._native.set_harvest_method("multiply")
+    den = W2.abs().amax(dim=1, keepdim=True)
+    assert float(((W - W2).abs() / den).max()) < W_TOL
+    del W, W2
+    prob = lx.SemiLinearProblem(spec, None, _ops.dev_f64(w5.u0), lx.Boundary.periodic(), "none")
+    T = w5.steps * w5.delta_t
+    a = lx.run(g, st, prob, lx.SchemeConfig("linear"), w5.delta_t, T).u_final
+    b = lx.run(g, st, prob, lx.SchemeConfig("linear"), w5.delta_t, T, exact=False).u_final
+    assert np.isfinite(a).all()
+    assert rel_l2(b, a) < 1e-13
+
+
 def test_constant_table_harvest_streams(lx):
     """The constant block is process-wide: back-to-back harvests of different
     geometries on two streams still each see their own tables."""
