@@ -78,7 +78,10 @@ int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded
         if (pernode) tile = 2048;
         else if (sch == SCH_LIN) tile = 4096;
         else if (sch == SCH_ETD2) tile = 2048;
-        else tile = 1200;                                      // ETDRK4: + halo ~ 256 chunks of 5
+        // ETDRK4: + halo ~ 256 chunks of 5; large unsharded grids take wider tiles
+        // with several steps per launch (C4 2^24: 254 -> 192 us/step, C3 2^20:
+        // 36.7 -> 33.0, tools/prof_cases.py sweeps over tile x k)
+        else tile = (!sharded && g.nloc >= (int64_t)1800 * 2 * nsm) ? 1800 : 1200;
         // small grids: enough tiles to cover the SMs
         while (tile > 256 && (g.nloc + tile - 1) / tile < 2 * nsm) tile /= 2;
         tile = std::min<int64_t>(tile, g.nloc);
@@ -88,6 +91,7 @@ int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded
         k = 1;
         if (sch == SCH_LIN && !pernode) k = 8;                  // HBM-bound: reuse u on chip
         else if (ntiles < 2 * nsm) k = std::max<int64_t>(1, tile / (4 * std::max<int64_t>(rad, 1)));
+        else if (sch == SCH_ETDRK4 && !sharded && tile == 1800) k = nl == LMEP_NL_CONVECTIVE ? 2 : 6;
         k = std::min<int64_t>(k, std::max<int64_t>(steps, 1));
         k = std::max<int64_t>(k, 1);
     }
