@@ -20,9 +20,11 @@ def main():
     pr.enable()
     for _ in range(5):
         b.device_pass()
+        torch.cuda.synchronize()          # each pass starts on an idle device, as in bench.py
     pr.disable()
     torch.cuda.synchronize()
-    pstats.Stats(pr).sort_stats("cumulative").print_stats(40)
+    pstats.Stats(pr).sort_stats("cumulative").print_stats(45)
+    pstats.Stats(pr).sort_stats("tottime").print_stats(15)
 
 
 if __name__ == "__main__":
