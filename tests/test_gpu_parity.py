@@ -419,6 +419,36 @@ def test_c5_full_size_kernels_agree(lx):
     assert rel_l2(b, a) < 1e-13
 
 
+@pytest.mark.parametrize("N", [4097, 6001])
+@pytest.mark.parametrize("s", [1, 3])
+def test_constant_table_harvest_ragged_and_layouts(lx, N, s):
+    """Batch sizes off the 128-item CTA grain (tail lanes idle), both output
+    layouts of lmep_harvest ([B][s][n] and [s][n][B]) and the per-item kernel
+    ("mvitem") as the independent check on every item."""
+    from paper_2603_15964_b200 import _ops, configs
+    from paper_2603_15964_b200.harvest import _plan
+    w5 = configs.c5(N=N, steps=1)
+    c, nu = w5.coef
+    g = lx.make_periodic_grid(N, 0.0, 1.0)
+    st = lx.select_stencils(g, w5.n, lx.StencilPolicy.CENTERED)
+    plan = _plan(g, st, (), force_pernode=True)
+    tables, _, _ = _ops.operator_tables(plan.coords, ((1, 1.0), (2, 1.0)))
+    coef = _ops.dev_f64(np.stack([-c, nu], 1))
+    kw = dict(tables=tables, coef=coef, coef_stride=2, c0=None, c0_stride=0,
+              row_default=st.row, frozen_default=0)
+    h0 = _ops.harvest(w5.n, s, w5.delta_t, N, layout=0, **kw)
+    h1 = _ops.harvest(w5.n, s, w5.delta_t, N, layout=1, **kw)
+    assert int(h0.status.abs().max()) == 0 and int(h1.status.abs().max()) == 0
+    assert torch.equal(h0.rows, h1.rows.permute(2, 0, 1))
+    lx._native.set_harvest_method("mvitem")
+    try:
+        h2 = _ops.harvest(w5.n, s, w5.delta_t, N, layout=0, **kw)
+    finally:
+        lx._native.set_harvest_method("multiply")
+    den = h2.rows.abs().amax(dim=2, keepdim=True)
+    assert float(((h0.rows - h2.rows).abs() / den).max()) < W_TOL
+
+
 def test_constant_table_harvest_streams(lx):
     """The constant block is process-wide: back-to-back harvests of different
     geometries on two streams still each see their own tables."""
