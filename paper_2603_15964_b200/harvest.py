@@ -185,12 +185,59 @@ def _frozen_masks(sset: StencilSet, t: np.ndarray, frozen: list[int]) -> np.ndar
     return masks
 
 
+# Stencil-geometry constants of uniform / periodic grids (window coordinates and
+# their derivative tables, a few n x n doubles per geometry), keyed by exactly what
+# determines them (spacing, n, target rows, operator terms) -- the analogue of the
+# reference's exact-match cache (harvest.py:135-159), which keys whole harvested rows.
+# Harvested weights themselves are never cached.
+_GEOMETRY: dict = {}
+
+
+def _geometry(key, make):
+    """The memoised value; a later use waits (on the device, stream order) for
+    the kernels that produced it."""
+    hit = _GEOMETRY.get(key)
+    if hit is None:
+        if len(_GEOMETRY) >= 64:
+            _GEOMETRY.clear()
+        v = make()
+        _GEOMETRY[key] = (v, torch.cuda.current_stream().record_event())
+        return v
+    v, ev = hit
+    cur = torch.cuda.current_stream()
+    cur.wait_event(ev)
+    t = v[0] if isinstance(v, tuple) else v
+    if t.numel():
+        t.record_stream(cur)               # stays allocated for this stream's readers
+    return v
+
+
+def _uniform_h(grid: Grid):
+    if grid.periodic:
+        return grid.spacing
+    return grid.uniform_spacing
+
+
+def _tables_for(grid: Grid, sset: StencilSet, plan, terms):
+    """operator_tables of the plan's windows; memoised for uniform / periodic
+    geometries with few windows (shared and class plans, periodic per-node)."""
+    h = _uniform_h(grid)
+    if h is None or plan.coords.shape[0] > 64:
+        return _ops.operator_tables(plan.coords, terms)
+    key = ("tables", str(plan.coords.device), sset.n, float(h), np.asarray(plan.rows).tobytes(),
+           tuple((int(k), float(c)) for k, c in terms))
+    return _geometry(key, lambda: _ops.operator_tables(plan.coords, terms))
+
+
 def _coords_for(grid: Grid, sset: StencilSet, t: np.ndarray) -> torch.Tensor:
     """Local coordinates of the windows of nodes t (harvest.py:124-132)."""
     trow = sset.target_rows(t)
     off = np.arange(sset.n, dtype=np.int64)[None, :] - trow[:, None]
     if grid.periodic or grid.uniform_spacing is not None:
         h = grid.spacing if grid.periodic else grid.uniform_spacing
+        if trow.size <= 64:
+            key = ("coords", str(nat.device()), sset.n, float(h), trow.tobytes())
+            return _geometry(key, lambda: _ops.dev_f64(off.astype(np.float64) * h))
         return _ops.dev_f64(off.astype(np.float64) * h)
     nodes = _ops.dev_f64(grid.nodes)
     tt = torch.as_tensor(t, device=nodes.device)
@@ -266,7 +313,7 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
     _ops.check_nodes(_coords0_host(grid, sset, plan), max(k for k, _ in terms))
     d = nat.device()
     if plan.mode != nat.W_PERNODE:
-        tables, cf, c0 = _ops.operator_tables(plan.coords, terms)
+        tables, cf, c0 = _tables_for(grid, sset, plan, terms)
         T = plan.coords.shape[0]
         h = _ops.harvest(n, s, delta_t, T, tables=tables,
                          table_idx=_ops.dev_i32(np.arange(T)), coef=_ops.dev_f64(cf or [0.0]),
@@ -301,7 +348,7 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
         # host coefficients: upload in chunks on the copy stream, each chunk's
         # harvest starting as soon as its slice has landed
         h = _harvest_pipelined(spec, sl, N, n, s, delta_t,
-                               lambda: _ops.operator_tables(plan.coords, terms)[0], sset.row)
+                               lambda: _tables_for(grid, sset, plan, terms)[0], sset.row)
         _ops.raise_on_status(h)
         if stats is not None:
             stats.setdefault("ms", []).append(h.ms)
@@ -319,7 +366,7 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
                      plan.rows[sl], plan.masks[sl])
     if shared_coords:
         # one launch writes the SoA [s][n][N] table directly
-        tables, cf, c0 = _ops.operator_tables(plan.coords, terms)
+        tables, cf, c0 = _tables_for(grid, sset, plan, terms)
         if varcoef:
             coef, cs = coef_all, len(spec.orders)
             c0t, c0s = (None, 0) if react is None else (react, 1)
