@@ -199,10 +199,11 @@ class C5:
                         node_range=(self.off, self.nloc))
         return self.torch.cat(stats["ms"]).cpu().numpy()
 
-    def harvest_launch_ms(self, reps=5):
+    def harvest_launch_ms(self, reps=11):
         """The harvest launch alone (lmep_harvest: prep + constant copy + kernel on
-        the current stream), CUDA events around `reps` launches on resident
-        tables and coefficients, for the roofline of the kernel itself."""
+        the current stream): median over `reps` back-to-back launches, each
+        between its own CUDA events, on resident tables and coefficients (the
+        roofline of the kernel itself)."""
         from paper_2603_15964_b200 import _ops
         from paper_2603_15964_b200.harvest import _plan
         torch = self.torch
@@ -214,17 +215,19 @@ class C5:
             return _ops.harvest(self.w.n, 1, self.w.delta_t, self.nloc, tables=tables, coef=coef,
                                 coef_stride=2, c0=None, c0_stride=0, row_default=self.sset.row,
                                 frozen_default=0, layout=1)
-        once()
-        e0, e1 = (torch.cuda.Event(enable_timing=True) for _ in range(2))
+        for _ in range(3):
+            once()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(reps)]
         torch.cuda.synchronize()
-        e0.record()
-        for _ in range(reps):
+        for a, b in ev:                      # back to back, one event pair per launch
+            a.record()
             h = once()
-        e1.record()
+            b.record()
         torch.cuda.synchronize()
         if int(h.status.abs().max().item()) != 0:
             raise RuntimeError("harvest launch failed")
-        return e0.elapsed_time(e1) / reps
+        return float(np.median([a.elapsed_time(b) for a, b in ev]))
 
     def phi_harvest(self, s=4, reps=3):
         """SURVEY 8(d) C5 harvest benchmark: the per-node phi_0..phi_{s-1} rows
