@@ -78,6 +78,13 @@ __global__ void mvc_prep_kernel(const HarvestParams P, MvcConst *out)
     __shared__ int ee[MVC_D];
     const int j = threadIdx.x, n = P.n, nt = P.nterms, d = P.d, row = P.row_default;
     const bool c0 = P.c0 != nullptr;
+    // the tables once into shared memory (coalesced); every pass below reads them there
+    __shared__ double Tsm[MVC_NT][MVC_D][MVC_D];
+    for (int i = j; i < nt * n * n; i += 32) {
+        const int t = i / (n * n), r = i % (n * n);
+        Tsm[t][r / n][r % n] = P.tables[i];
+    }
+    __syncwarp();
     for (int k = j; k < 52; k += 32) {
         out->inv[k] = k > 0 ? 1.0 / (double)k : 0.0;
         out->tf[k] = (k + 2 > MVC_THETA) ? (MVC_THETA / (k + 1)) / (1.0 - MVC_THETA / (k + 2)) : INFINITY;
@@ -88,7 +95,7 @@ __global__ void mvc_prep_kernel(const HarvestParams P, MvcConst *out)
         for (int c = 0; c < n; ++c) {
             double l = 0.0;
             for (int t = 0; t < nt; ++t)
-                l = xadd(l, xmul(P.coef[t], P.tables[((int64_t)t * n + c) * n + j]));
+                l = xadd(l, xmul(P.coef[t], Tsm[t][c][j]));
             if (c0 && c == j) l = xadd(l, P.c0[0]);
             M[j][c] = xmul(P.delta_t, l);
             ok &= (bool)isfinite(M[j][c]);
@@ -107,8 +114,8 @@ __global__ void mvc_prep_kernel(const HarvestParams P, MvcConst *out)
         double amax = 0.0, dp = 0.0, dm = 0.0;
         if (j < n)
             for (int c = 0; c < n; ++c) {
-                const double a = P.tables[((int64_t)t * n + c) * n + j];
-                const double r = P.tables[((int64_t)t * n + (n - 1 - c)) * n + (n - 1 - j)];
+                const double a = Tsm[t][c][j];
+                const double r = Tsm[t][n - 1 - c][n - 1 - j];
                 amax = fmax(amax, fabs(a));
                 dp = fmax(dp, fabs(a - r));
                 dm = fmax(dm, fabs(a + r));
@@ -175,7 +182,7 @@ __global__ void mvc_prep_kernel(const HarvestParams P, MvcConst *out)
             for (int c = 0; c < MVC_D; ++c) {
                 double v = 0.0;
                 if (t < nt && j < n && c < n)
-                    v = P.tables[((int64_t)t * n + c) * n + j] * mv_pow2(ee[c] - ee[j]);
+                    v = Tsm[t][c][j] * mv_pow2(ee[c] - ee[j]);
                 out->tt[t][j][c] = v;
                 sum += fabs(v);
             }
@@ -190,9 +197,9 @@ __global__ void mvc_prep_kernel(const HarvestParams P, MvcConst *out)
             for (int c = 0; c < 8; ++c) {
                 double a = 0.0, b = 0.0;
                 if (sym && t < nt && j <= Mh && c <= Mh) {
-                    const double lo = P.tables[((int64_t)t * n + c) * n + j] * mv_pow2(ee[c] - ee[j]);
+                    const double lo = Tsm[t][c][j] * mv_pow2(ee[c] - ee[j]);
                     const int c2 = n - 1 - c;
-                    const double hi = P.tables[((int64_t)t * n + c2) * n + j] * mv_pow2(ee[c2] - ee[j]);
+                    const double hi = Tsm[t][c2][j] * mv_pow2(ee[c2] - ee[j]);
                     if (c < Mh) { a = lo + hi; b = lo - hi; }
                     else a = 2.0 * lo;
                 }
