@@ -733,6 +733,29 @@ def test_dirichlet_cubic_run(lx, golden):
     assert rel_inf(of[3].weights, golden["ac_p3"]) < W_TOL
 
 
+@pytest.mark.parametrize("name,N", [("c4", 1 << 20), ("c3", 1 << 20)])
+def test_large_grid_etdrk4_plan_bitwise(lx, name, N):
+    """Large unsharded ETDRK4 grids take 1800-node tiles with 6 (cubic) or 2
+    (convective) steps per launch by default; in the exact mode the result is
+    bit-identical to one step per launch on 1200-node tiles (the shape the
+    oracle tests pin at small sizes), Neumann closure included (C4)."""
+    from paper_2603_15964_b200 import _ops, configs
+    from paper_2603_15964_b200.timestep import Stepper, prepare
+    w = configs.make(name, N=N, steps=13)
+    g = (lx.make_periodic_grid if w.periodic else lx.make_uniform_grid)(w.N, w.x_min, w.x_max)
+    st = lx.select_stencils(g, w.n, lx.StencilPolicy.CENTERED)
+    bc = lx.Boundary.neumann() if w.boundary == "neumann" else lx.Boundary.periodic()
+    prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(w.terms), None, w.u0, bc, w.nonlinear,
+                                nonlinear_scale=w.nl_scale or 1.0)
+    prep = prepare(g, st, prob, lx.SchemeConfig("etdrk4"), w.delta_t)
+    a = Stepper(prep, _ops.dev_f64(w.u0), exact=True)
+    a.advance(13)
+    b = Stepper(prep, _ops.dev_f64(w.u0), exact=True, tuning={"tile": 1200, "ksteps": 1})
+    b.advance(13)
+    assert torch.equal(a.u, b.u)
+    assert bool(torch.isfinite(a.u).all())
+
+
 @pytest.mark.parametrize("tuning", [None, {"tile": 40, "ksteps": 1}, {"tile": 100, "ksteps": 4}])
 def test_c4_neumann_bitwise(lx, golden, orc, tuning):
     W = golden["c4_weights"]
