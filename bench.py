@@ -517,11 +517,17 @@ def main():
     kb = max(1, pl["ksteps"])
     if world == 1 and pl["tile"] > 0 and kb > 1:
         launches_steps = -(-w.steps // kb)
-        ks = [min(kb, w.steps - i * kb) for i in range(launches_steps)]
-        step_bytes_total = sum(bench.nloc * (8 * w.n + 8) * (pl["tile"] + k * (w.n - 1)) /
-                               pl["tile"] + bench.nloc * 8 for k in ks)
+        # the library spreads the steps evenly over the launches, each launch's tile
+        # widened to what its k leaves of the 1536-node span (step_host.cu)
+        span = pl["tile"] + kb * (w.n - 1)
+        ks, left = [], w.steps
+        for i in range(launches_steps):
+            ks.append(-(-left // (launches_steps - i)))
+            left -= ks[-1]
+        step_bytes_total = sum(bench.nloc * (8 * w.n + 8) * span / (span - k * (w.n - 1)) +
+                               bench.nloc * 8 for k in ks)
         step_kernel = (f"lin_pernode_tma_kernel<13,3> (persistent, TMA-pipelined; rows in registers, "
-                       f"k={kb} steps/launch)")
+                       f"{min(ks)}-{max(ks)} steps/launch)")
         per_launch_ms = step_ms / launches_steps
         step_bytes = step_bytes_total / launches_steps
     else:

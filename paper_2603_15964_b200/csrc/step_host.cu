@@ -285,8 +285,18 @@ int run_steps(const StepCall &c)
     const double *src = c.u_in, *qsrc = c.q_in;
     int rc = LMEP_OK;
     int64_t done = 0;
+    // persistent TMA per-node kernel: the steps spread evenly over the launches, each
+    // launch's tile widened to the span its k leaves (tile + k (n-1) = span): C5's
+    // 200 steps run as 8 x 15 + 5 x 16 instead of 12 x 16 + 8
+    const bool tma_path = c.sch == SCH_LIN && pernode && p.bc == LMEP_BC_NONE && g.periodic &&
+                          !sharded && t.threads == 256 &&
+                          t.tile + (int64_t)t.ksteps * (g.n - 1) == tb_nodes_per_cta(g.n, true);
     for (int64_t L = 0; L < nlaunch; ++L) {
-        const int64_t k = std::min<int64_t>(kmax, c.steps - done);
+        int64_t k = std::min<int64_t>(kmax, c.steps - done);
+        if (tma_path) {
+            k = (c.steps - done + (nlaunch - L) - 1) / (nlaunch - L);
+            p.tile = tb_nodes_per_cta(g.n, true) - k * (g.n - 1);
+        }
         // the last launch must land in u_out
         const bool to_out = ((nlaunch - 1 - L) % 2) == 0;
         double *dst = to_out ? c.u_out : scr;
@@ -302,8 +312,7 @@ int run_steps(const StepCall &c)
             p.qhl = c.halo->hist_left; p.qhr = c.halo->hist_right;
             p.G = c.halo->width;
         }
-        if (c.sch == SCH_LIN && pernode && p.bc == LMEP_BC_NONE && g.periodic && !sharded &&
-            t.threads == 256 && t.tile + (int64_t)t.ksteps * (g.n - 1) == tb_nodes_per_cta(g.n, true))
+        if (tma_path)
             rc = launch_lin_pernode_tma(p, (c.flags & LMEP_FLAG_EXACT) != 0, c.stream);      // persistent, TMA-pipelined (C5)
         else if (c.sch == SCH_LIN && pernode && p.bc == LMEP_BC_NONE && g.periodic &&
             t.threads == 256 && t.tile + (int64_t)t.ksteps * (g.n - 1) == tb_nodes_per_cta(g.n, false))
