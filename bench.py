@@ -60,9 +60,10 @@ def multiply_flops(d: int, ms: np.ndarray) -> float:
 
 # ------------------------------------------------------------------ clocks
 class Clocks:
-    """nvidia-smi sampling (SM clock, max clock, throttle reasons) in its own
-    PROCESS (`-lms 100`), so the sampler never competes for the GIL with the
-    timed launches."""
+    """SM clock, max clock and clock-event reasons during the timed region: one
+    NVML reading per timed pass, taken while that pass runs on the device (the
+    pass is timed by CUDA events, so the host-side call costs it nothing);
+    without NVML, nvidia-smi sampling (`-lms 100`) in its own process."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
@@ -71,8 +72,36 @@ class Clocks:
         self.index = index
         self.samples = []
         self._p = None
+        self._nvml = None
+
+    def sample(self):
+        """One NVML reading (SM clock, max SM clock, clock-event reasons), taken by
+        the caller while its kernels run; the nvidia-smi process below is the
+        fallback when NVML is unavailable."""
+        if self._nvml is None:
+            return
+        nv, h = self._nvml
+        try:
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            return
+        act = lambda bit: "Active" if r & bit else "Not Active"
+        self.samples.append([str(sm), str(mx), "",
+                             act(nv.nvmlClocksEventReasonHwSlowdown),
+                             act(nv.nvmlClocksEventReasonHwThermalSlowdown),
+                             act(nv.nvmlClocksEventReasonSwThermalSlowdown),
+                             act(nv.nvmlClocksEventReasonSwPowerCap)])
 
     def __enter__(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self._nvml = (nv, nv.nvmlDeviceGetHandleByIndex(self.index))
+            return self
+        except Exception:
+            self._nvml = None
         try:
             self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
                                         "--format=csv,noheader,nounits", "-lms", "100"],
@@ -83,6 +112,12 @@ class Clocks:
         return self
 
     def __exit__(self, *a):
+        if self._nvml is not None:
+            try:
+                self._nvml[0].nvmlShutdown()
+            except Exception:
+                pass
+            return
         if self._p is None:
             return
         time.sleep(0.12)                         # at least one more sample under load
@@ -486,6 +521,7 @@ def main():
         for _ in range(args.steps):
             torch.cuda.synchronize()
             bench.device_pass()
+            clk.sample()                          # while the pass runs on the device
             h, s = bench.phase_ms()
             harv.append(h)
             stepm.append(s)
