@@ -18,7 +18,6 @@ Extensions beyond the reference API (each documented where it is used):
 from __future__ import annotations
 
 import math
-import time
 from dataclasses import dataclass
 from typing import Callable
 
@@ -370,7 +369,11 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
     cp, cp1 = _ops.copy_stream(0), _ops.copy_stream(1)
 
     torch.cuda.synchronize(dev)
-    t0 = time.perf_counter_ns()
+    # harvest_ns / step_ns are device intervals between CUDA events on the compute
+    # stream, so the host never waits between the harvest and the steps: it
+    # enqueues the steps while the coefficients stream up and the harvest runs
+    ev_start = torch.cuda.Event(enable_timing=True)
+    ev_start.record(cur)
     # The initial data goes up while the harvest runs.  When the harvest
     # streams host coefficients (copy stream 0), u0 is queued behind them so
     # the slices the harvest waits on get the PCIe bandwidth first; otherwise
@@ -400,9 +403,9 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
     nsnap = 1 + -(-steps_total // snap_every)
     # snapshots land straight in one page-locked [S, N] block (returned as is)
     snaps = torch.empty((nsnap, N), dtype=torch.float64, pin_memory=True)
-    torch.cuda.synchronize(dev)
-    harvest_ns = time.perf_counter_ns() - t0
-    _ops.check_deferred(pending)
+    ev_harvest = torch.cuda.Event(enable_timing=True)
+    ev_harvest.record(cur)
+    harvest_ns = None
 
     cur.wait_event(ev_u0)
     u0d.record_stream(cur)
@@ -422,10 +425,10 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
     snap_ev, prev_ev = snapshot(0), None
     step_ns = 0
     done = 0
+    ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     while done < steps_total:
         k = min(snap_every, steps_total - done)
-        cur.synchronize()
-        t0 = time.perf_counter_ns()
+        ev_a.record(cur)
         # a linear / ETDRK4 advance() reads st.u and writes the other buffers:
         # it may overwrite the buffer the PREVIOUS snapshot was read from, never
         # the latest.  Multistep warm-up swaps buffers between single steps.
@@ -433,8 +436,14 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
         if wait is not None:
             cur.wait_event(wait)
         st.advance(k)
+        ev_b.record(cur)
         cur.synchronize()
-        step_ns += time.perf_counter_ns() - t0
+        if harvest_ns is None:
+            # the harvest's status first: a failed exponential surfaces as the
+            # harvest's NonFinite (timestep.py:284-308), not as a blown-up step
+            harvest_ns = int(ev_start.elapsed_time(ev_harvest) * 1e6)
+            _ops.check_deferred(pending)
+        step_ns += int(ev_a.elapsed_time(ev_b) * 1e6)
         done += k
         if st.nonfinite():
             cp.synchronize()
