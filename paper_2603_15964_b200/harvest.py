@@ -229,6 +229,22 @@ def _tables_for(grid: Grid, sset: StencilSet, plan, terms):
     return _geometry(key, lambda: _ops.operator_tables(plan.coords, terms))
 
 
+_CHECKED: set = set()
+
+
+def _checked_nodes(grid: Grid, sset: StencilSet, plan, kmax: int) -> None:
+    """localop.py:69-74 node checks on the first window; a uniform / periodic
+    geometry that passed once is not re-checked (the check raises, it never
+    changes anything)."""
+    h = _uniform_h(grid)
+    key = None if h is None else (sset.n, float(h), int(plan.rows[0]), int(kmax))
+    if key is not None and key in _CHECKED:
+        return
+    _ops.check_nodes(_coords0_host(grid, sset, plan), kmax)
+    if key is not None:
+        _CHECKED.add(key)
+
+
 def _coords_for(grid: Grid, sset: StencilSet, t: np.ndarray) -> torch.Tensor:
     """Local coordinates of the windows of nodes t (harvest.py:124-132)."""
     trow = sset.target_rows(t)
@@ -310,7 +326,7 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
     if max(k for k, _ in terms) > n - 1:
         from .errors import OrderTooHigh
         raise OrderTooHigh(f"operator order {max(k for k, _ in terms)} not representable on {n} nodes")
-    _ops.check_nodes(_coords0_host(grid, sset, plan), max(k for k, _ in terms))
+    _checked_nodes(grid, sset, plan, max(k for k, _ in terms))
     d = nat.device()
     if plan.mode != nat.W_PERNODE:
         tables, cf, c0 = _tables_for(grid, sset, plan, terms)
