@@ -649,6 +649,219 @@ void orc_run_etd2(const double *ops0, const double *ops1, const double *ops2,
     free(pool);
 }
 
+/* ------------------------------------------------------------------ */
+/* Compact-operator stepping (full-size parity runs).                  */
+/*                                                                     */
+/* The same arithmetic as the member-array loops above -- every node's */
+/* window sum runs j = 0..n-1 ascending from acc = 0.0 with separate   */
+/* multiply / add roundings (kernels.py:23-29) and every pointwise     */
+/* expression keeps the reference's operand order (kernels.py:62-132,  */
+/* timestep.py:187-215) -- but the window of node i comes from the     */
+/* select_stencils rule (grid.py:136-175) by index arithmetic instead  */
+/* of an (N, n) int64 member array, and rows are stored compactly:     */
+/*   mode 0  one shared row [n]          (periodic uniform grid)       */
+/*   mode 1  classes [nleft + 1 + nright][n]: node i < nleft uses      */
+/*           class i, i >= N - nright class nleft+1+(i-(N-nright)),    */
+/*           every other node the interior class nleft                 */
+/*   mode 2  per-node rows [N][n] (the reference's weights layout)     */
+/*   mode 3  keyed rows [K][n] with a per-node key cls[N]: the rows of  */
+/*           the reference's exact-match harvest cache (harvest.py:    */
+/*           135-159), one per distinct (coordinates, row, frozen) key */
+/* Results are bit-identical to the member-array loops on the dense    */
+/* rows these expand to (tests/test_oracle_golden.py checks that); the */
+/* pointwise stages are fused into the window loops and every loop is  */
+/* OpenMP-parallel, so the BASELINE-size runs (C4: 2^24 x 1000 steps)  */
+/* finish in minutes instead of hours.                                 */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    int64_t N;
+    int32_t n, row, periodic, mode, nleft, nright;
+    const int32_t *cls;        /* mode 3: key of node i */
+} orc_geom;
+
+static inline const double *crow(const orc_geom *g, const double *w, int64_t i)
+{
+    if (g->mode == 0) return w;
+    if (g->mode == 2) return w + i * g->n;
+    if (g->mode == 3) return w + (int64_t)g->cls[i] * g->n;
+    if (i < g->nleft) return w + i * g->n;
+    if (i >= g->N - g->nright) return w + (g->nleft + 1 + (i - (g->N - g->nright))) * g->n;
+    return w + (int64_t)g->nleft * g->n;
+}
+
+/* sum_j w_i[j] * u[member(i, j)], ascending j (kernels.py:23-29) */
+static inline double cdot(const orc_geom *g, const double *w, const double *u, int64_t i)
+{
+    const double *wr = crow(g, w, i);
+    const int n = g->n;
+    const int64_t N = g->N;
+    int64_t s = i - g->row;
+    double acc = 0.0;
+    if (g->periodic) {
+        if (s >= 0 && s + n <= N) {
+            for (int j = 0; j < n; ++j) acc += wr[j] * u[s + j];
+        } else {
+            s = ((s % N) + N) % N;
+            for (int j = 0; j < n; ++j) {
+                int64_t m = s + j;
+                if (m >= N) m -= N;
+                acc += wr[j] * u[m];
+            }
+        }
+    } else {
+        if (s < 0) s = 0;
+        if (s > N - n) s = N - n;
+        for (int j = 0; j < n; ++j) acc += wr[j] * u[s + j];
+    }
+    return acc;
+}
+
+/* kernels.py:47-58 for node i (convective: -u * (D1 u), cubic: -u^3) */
+static inline double cnl(int kind, const orc_geom *g, const double *d1w, const double *u,
+                         int64_t i)
+{
+    if (kind == 0) return 0.0;
+    if (kind == 1) return -u[i] * cdot(g, d1w, u, i);
+    return -u[i] * u[i] * u[i];
+}
+
+#ifdef _OPENMP
+#define ORC_PFOR _Pragma("omp parallel for schedule(static)")
+#else
+#define ORC_PFOR
+#endif
+
+/* kernels.py:33-43 on compact rows */
+void orc_run_linear_c(const orc_geom *g, const double *w, const double *u0, int64_t steps,
+                      int bc, double lo, double hi, const double *dl, const double *dr,
+                      double *out)
+{
+    const int64_t N = g->N;
+    orc_bc b = {bc, lo, hi, dl, dr, g->n};
+    double *u = (double *)malloc(sizeof(double) * N);
+    double *buf = (double *)malloc(sizeof(double) * N);
+    memcpy(u, u0, sizeof(double) * N);
+    for (int64_t s = 0; s < steps; ++s) {
+        ORC_PFOR
+        for (int64_t i = 0; i < N; ++i) buf[i] = cdot(g, w, u, i);
+        apply_bc(buf, N, &b);
+        double *t = u; u = buf; buf = t;
+    }
+    memcpy(out, u, sizeof(double) * N);
+    free(u); free(buf);
+}
+
+/* kernels.py:62-132 on compact rows (+ the Neumann closure of Appendix B.2),
+ * one step; rows: w, alpha, beta, gamma, w_half, p1_half, d1. */
+static void etdrk4_step_c(const orc_geom *g, const double *const *R, int kind, double *u,
+                          double *unew, double *pool, const orc_bc *b)
+{
+    const int64_t N = g->N;
+    const double *w = R[0], *al = R[1], *be = R[2], *ga = R[3], *wh = R[4], *p1h = R[5],
+                 *d1 = R[6];
+    double *n0 = pool, *n1 = pool + N, *n2 = pool + 2 * N, *n3 = pool + 3 * N;
+    double *whu = pool + 4 * N, *a = pool + 5 * N, *bb = pool + 6 * N, *c = pool + 7 * N;
+    double *t2 = pool + 8 * N;
+    ORC_PFOR
+    for (int64_t i = 0; i < N; ++i) {
+        n0[i] = cnl(kind, g, d1, u, i);
+        whu[i] = cdot(g, wh, u, i);
+    }
+    ORC_PFOR
+    for (int64_t i = 0; i < N; ++i) a[i] = whu[i] + cdot(g, p1h, n0, i);
+    apply_bc(a, N, b);
+    ORC_PFOR
+    for (int64_t i = 0; i < N; ++i) n1[i] = cnl(kind, g, d1, a, i);
+    ORC_PFOR
+    for (int64_t i = 0; i < N; ++i) bb[i] = whu[i] + cdot(g, p1h, n1, i);
+    apply_bc(bb, N, b);
+    ORC_PFOR
+    for (int64_t i = 0; i < N; ++i) {
+        n2[i] = cnl(kind, g, d1, bb, i);
+        t2[i] = 2.0 * n2[i] - n0[i];
+    }
+    ORC_PFOR
+    for (int64_t i = 0; i < N; ++i) c[i] = cdot(g, wh, a, i) + cdot(g, p1h, t2, i);
+    apply_bc(c, N, b);
+    ORC_PFOR
+    for (int64_t i = 0; i < N; ++i) {
+        n3[i] = cnl(kind, g, d1, c, i);
+        t2[i] = n1[i] + n2[i];
+    }
+    ORC_PFOR
+    for (int64_t i = 0; i < N; ++i) {
+        double t1 = cdot(g, w, u, i);
+        t1 += cdot(g, al, n0, i);
+        t1 += cdot(g, be, t2, i);
+        unew[i] = t1 + cdot(g, ga, n3, i);
+    }
+    apply_bc(unew, N, b);
+}
+
+void orc_run_etdrk4_c(const orc_geom *g, const double *w, const double *al, const double *be,
+                      const double *ga, const double *wh, const double *p1h, const double *d1,
+                      int kind, const double *u0, int64_t steps, int bc, double lo, double hi,
+                      const double *dl, const double *dr, double *out, double *nl0_out)
+{
+    const int64_t N = g->N;
+    const double *R[7] = {w, al, be, ga, wh, p1h, d1};
+    orc_bc b = {bc, lo, hi, dl, dr, g->n};
+    double *pool = (double *)malloc(sizeof(double) * N * 11);
+    double *u = pool + 9 * N, *un = pool + 10 * N;
+    memcpy(u, u0, sizeof(double) * N);
+    for (int64_t s = 0; s < steps; ++s) {
+        etdrk4_step_c(g, R, kind, u, un, pool, &b);
+        if (s == 0 && nl0_out) memcpy(nl0_out, pool, sizeof(double) * N);   /* N(u0) */
+        double *t = u; u = un; un = t;
+    }
+    memcpy(out, u, sizeof(double) * N);
+    free(pool);
+}
+
+/* ETD multistep, order 2 (timestep.py:187-215) after one ETDRK4 warm-up step
+ * (timestep.py:364-380), on compact rows: ops0/ops1/ops2 = exp, dt*phi1,
+ * dt^2*phi2 at dt; warm = the ETDRK4 rows (w, alpha, beta, gamma, w_half,
+ * p1_half); d1 the (scaled) derivative row of the convective N(u). */
+void orc_run_etd2_c(const orc_geom *g, const double *ops0, const double *ops1,
+                    const double *ops2, const double *w, const double *al, const double *be,
+                    const double *ga, const double *wh, const double *p1h, const double *d1,
+                    int kind, const double *u0, int64_t steps, double dt, int bc, double lo,
+                    double hi, const double *dl, const double *dr, double *out,
+                    double *nhist_out)
+{
+    const int64_t N = g->N;
+    const double *R[7] = {w, al, be, ga, wh, p1h, d1};
+    orc_bc b = {bc, lo, hi, dl, dr, g->n};
+    double *pool = (double *)malloc(sizeof(double) * N * 14);
+    double *u = pool + 9 * N, *un = pool + 10 * N, *nk = pool + 11 * N, *np_ = pool + 12 * N,
+           *gr = pool + 13 * N;
+    memcpy(u, u0, sizeof(double) * N);
+    if (steps >= 1) {
+        etdrk4_step_c(g, R, kind, u, un, pool, &b);
+        memcpy(np_, pool, sizeof(double) * N);              /* history = (N(u0),) */
+        double *t = u; u = un; un = t;
+    }
+    for (int64_t s = 1; s < steps; ++s) {
+        ORC_PFOR
+        for (int64_t i = 0; i < N; ++i) {
+            nk[i] = cnl(kind, g, d1, u, i);
+            gr[i] = nk[i] - np_[i];
+        }
+        ORC_PFOR
+        for (int64_t i = 0; i < N; ++i) {
+            double t1 = cdot(g, ops0, u, i);
+            t1 = t1 + cdot(g, ops1, nk, i) / 1.0;
+            un[i] = t1 + cdot(g, ops2, gr, i) / dt;
+        }
+        apply_bc(un, N, &b);
+        double *t = u; u = un; un = t;
+        t = np_; np_ = nk; nk = t;
+    }
+    memcpy(out, u, sizeof(double) * N);
+    if (nhist_out) memcpy(nhist_out, np_, sizeof(double) * N);
+    free(pool);
+}
+
 int orc_num_threads(void)
 {
 #ifdef _OPENMP

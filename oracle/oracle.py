@@ -24,6 +24,14 @@ _ip = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
 _i32p = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
 
 
+class Geom(C.Structure):
+    """orc_geom: the select_stencils window rule (grid.py:136-175) plus the
+    compact row mode (0 shared [n], 1 classes [nleft+1+nright][n], 2 per-node [N][n])."""
+    _fields_ = [("N", C.c_int64), ("n", C.c_int32), ("row", C.c_int32), ("periodic", C.c_int32),
+                ("mode", C.c_int32), ("nleft", C.c_int32), ("nright", C.c_int32),
+                ("cls", C.c_void_p)]
+
+
 class OracleError(RuntimeError):
     def __init__(self, code, what):
         super().__init__(f"oracle {what} failed with status {code}")
@@ -66,6 +74,18 @@ def lib():
                                              C.c_double, C.c_int, C.c_double, C.c_double,
                                              C.c_void_p, C.c_void_p, _dp, C.c_void_p]
     L.orc_run_etd2.restype = None
+    G = C.POINTER(Geom)
+    L.orc_run_linear_c.argtypes = [G, _dp, _dp, C.c_int64, C.c_int, C.c_double, C.c_double,
+                                   C.c_void_p, C.c_void_p, _dp]
+    L.orc_run_linear_c.restype = None
+    L.orc_run_etdrk4_c.argtypes = [G] + [_dp] * 7 + [C.c_int, _dp, C.c_int64, C.c_int, C.c_double,
+                                                    C.c_double, C.c_void_p, C.c_void_p, _dp,
+                                                    C.c_void_p]
+    L.orc_run_etdrk4_c.restype = None
+    L.orc_run_etd2_c.argtypes = [G] + [_dp] * 10 + [C.c_int, _dp, C.c_int64, C.c_double, C.c_int,
+                                                     C.c_double, C.c_double, C.c_void_p,
+                                                     C.c_void_p, _dp, C.c_void_p]
+    L.orc_run_etd2_c.restype = None
     L.orc_num_threads.restype = C.c_int
     L.orc_set_threads.argtypes = [C.c_int]
     L.orc_set_threads.restype = None
@@ -268,3 +288,120 @@ def neumann_rows(n, h):
     dl = fornberg_weights(0.0, np.arange(n) * h, 1)[1]
     dr = fornberg_weights(0.0, (np.arange(n) - (n - 1)) * h, 1)[1]
     return dl, dr
+
+
+# --- compact rows (index arithmetic; full-size parity runs) ----------------
+class Compact:
+    """Operator rows in compact form on the select_stencils windows of
+    (N, n, row, periodic): mode 0 shared [n], 1 classes [nleft+1+nright][n],
+    2 per-node [N][n] (the reference's weights layout), 3 keyed rows [K][n]
+    with node i using key cls[i] (the reference's exact-match harvest cache,
+    harvest.py:135-159)."""
+
+    def __init__(self, N, n, row, periodic, mode, nleft=0, nright=0, cls=None, nkeys=0):
+        self._cls = None if cls is None else np.ascontiguousarray(cls, dtype=np.int32)
+        self.nkeys = int(nkeys)
+        self.geom = Geom(int(N), int(n), int(row), int(bool(periodic)), int(mode), int(nleft),
+                         int(nright), None if self._cls is None else self._cls.ctypes.data)
+
+    def rows(self, r):
+        """Validate one operator's rows for this geometry."""
+        r = _f64(r)
+        g = self.geom
+        want = {0: (g.n,), 1: (g.nleft + 1 + g.nright, g.n), 2: (g.N, g.n),
+                3: (self.nkeys, g.n)}[g.mode]
+        if r.shape != want and not (g.mode == 0 and r.shape == (1, g.n)):
+            raise ValueError(f"rows of shape {r.shape}, expected {want}")
+        return np.ascontiguousarray(r.reshape(-1))
+
+    def dense(self, r):
+        """The (N, n) array these compact rows stand for."""
+        g = self.geom
+        r = _f64(r)
+        if g.mode == 0:
+            return np.tile(r.reshape(1, g.n), (g.N, 1))
+        if g.mode == 2:
+            return r.reshape(g.N, g.n).copy()
+        if g.mode == 3:
+            return r.reshape(self.nkeys, g.n)[self._cls]
+        out = np.tile(r[g.nleft].reshape(1, g.n), (g.N, 1))
+        out[:g.nleft] = r[:g.nleft]
+        if g.nright:
+            out[g.N - g.nright:] = r[g.nleft + 1:]
+        return out
+
+    def run_linear(self, w, u0, steps, bc=None):
+        u0 = _f64(u0)
+        out = np.zeros_like(u0)
+        kind, lo, hi, dl, dr, keep = _bc_args(bc)
+        lib().orc_run_linear_c(C.byref(self.geom), self.rows(w), u0, int(steps), kind, lo, hi,
+                               dl, dr, out)
+        return out
+
+    def _zeros(self):
+        g = self.geom
+        return np.zeros({0: g.n, 1: (g.nleft + 1 + g.nright) * g.n, 2: g.N * g.n,
+                         3: self.nkeys * g.n}[g.mode])
+
+    def run_etdrk4(self, ops, d1w, kind, u0, steps, bc=None, return_nl0=False):
+        """ops = (w, alpha, beta, gamma, w_half, p1_half) compact rows."""
+        rs = [self.rows(x) for x in ops] + [self._zeros() if d1w is None else self.rows(d1w)]
+        u0 = _f64(u0)
+        out = np.zeros_like(u0)
+        nl0 = np.zeros_like(u0)
+        b, lo, hi, dl, dr, keep = _bc_args(bc)
+        lib().orc_run_etdrk4_c(C.byref(self.geom), *rs, int(kind), u0, int(steps), b, lo, hi,
+                               dl, dr, out, nl0.ctypes.data)
+        return (out, nl0) if return_nl0 else out
+
+    def run_etd2(self, ops, warm, d1w, kind, u0, steps, delta_t, bc=None, return_hist=False):
+        """ops = (exp, dt*phi1, dt^2*phi2) raw rows; warm = the ETDRK4 rows."""
+        rs = [self.rows(x) for x in list(ops[:3]) + list(warm)]
+        rs.append(self._zeros() if d1w is None else self.rows(d1w))
+        u0 = _f64(u0)
+        out = np.zeros_like(u0)
+        hist = np.zeros_like(u0)
+        b, lo, hi, dl, dr, keep = _bc_args(bc)
+        lib().orc_run_etd2_c(C.byref(self.geom), *rs, int(kind), u0, int(steps), float(delta_t),
+                             b, lo, hi, dl, dr, out, hist.ctypes.data)
+        return (out, hist) if return_hist else out
+
+
+def combine_rows(arrs, coeffs):
+    """harvest.combine (harvest.py:225-235): from zeros, in list order, numpy's
+    two roundings per term."""
+    acc = np.zeros_like(_f64(arrs[0]))
+    for a, c in zip(arrs, coeffs):
+        acc = acc + float(c) * _f64(a)
+    return acc
+
+
+def etdrk4_rows(full, half, delta_t):
+    """timestep.py:141-156 on any row arrays: (w, alpha, beta, gamma, w_half, p1_half)."""
+    dt = float(delta_t)
+    w, p1, p2, p3 = (_f64(x) for x in full[:4])
+    return (w, combine_rows([p1, p2, p3], [1.0, -3.0 / dt, 4.0 / dt**2]),
+            combine_rows([p2, p3], [2.0 / dt, -4.0 / dt**2]),
+            combine_rows([p3, p2], [4.0 / dt**2, -1.0 / dt]), _f64(half[0]), _f64(half[1]))
+
+
+def close(u, bc):
+    """The boundary closure of the initial data (timestep.py:310-311 pin;
+    Appendix B.2 zero-gradient closure), as apply_bc does it."""
+    u = _f64(u).copy()
+    if bc is None:
+        return u
+    if bc[0] == "dirichlet":
+        u[0], u[-1] = bc[1], bc[2]
+        return u
+    dl, dr = _f64(bc[1]), _f64(bc[2])
+    n, N = dl.size, u.size
+    acc = 0.0
+    for j in range(1, n):
+        acc += dl[j] * u[j]
+    u[0] = -acc / dl[0]
+    acc = 0.0
+    for j in range(n - 1):
+        acc += dr[j] * u[N - n + j]
+    u[N - 1] = -acc / dr[n - 1]
+    return u

@@ -1,0 +1,434 @@
+"""Full-size parity at the BASELINE.json configs (north_star: harvested
+weights within 1e-12 relative, the solution after the FULL run within 1e-10
+relative L2), the CUDA path against the C oracle on the same seeded inputs
+(paper_2603_15964_b200/configs.py = SURVEY 8(d)).
+
+Each config is checked three ways:
+
+1. rows: every harvested row the run uses against the oracle's restatement of
+   the reference harvest (block augmentation, harvest.py:97-121, scipy's
+   balancing + Pade expm), row-relative inf norm <= 1e-12;
+2. run: the public ``run()`` (exact and fused-multiply-add modes) against the
+   oracle stepping the ORACLE's own rows for the full step count
+   (kernels.py:33-132, timestep.py:187-215, 255-394): relative L2 <= 1e-10 on
+   u_T, and the increment u_T - u_0 reported (C3 / C5 barely move at a
+   stable dt);
+3. stepping: the device's exact-mode steps against the oracle stepping the
+   DEVICE's harvested rows: bit-identical (np.array_equal).
+
+The oracle is the compact-row restatement (oracle/lmep_oracle.c, index
+arithmetic instead of (N, n) member arrays, OpenMP over every host core),
+pinned bit for bit to the member-array loops and the golden vectors of the
+live reference by tests/test_oracle_golden.py.
+
+C4's full run is checked against the reference's own stencil coordinates on
+np.linspace nodes (nodes[m] - nodes[t], harvest.py:124-132) with its
+exact-match harvest cache (harvest.py:135-159): one oracle row set per
+distinct key (21 at 2^24).  The device harvests offsets * h windows (nine
+position classes, DESIGN 5.5); its rows equal the oracle's on those windows
+to 1e-12, and equal the reference's keys to 1e-12 wherever the linspace
+coordinates round to offsets * h (all but 272 interior nodes, whose
+coordinates np.linspace moves by ~1e-9 relative).
+
+Results are printed (run pytest with -s) as one JSON line per config.
+"""
+
+import json
+import math
+import os
+import time
+
+import numpy as np
+import pytest
+import torch
+
+from tests.conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+W_TOL = 1e-12
+U_TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def lx():
+    import paper_2603_15964_b200 as m
+    m._native.device()
+    return m
+
+
+@pytest.fixture(scope="module")
+def orcx(orc):
+    orc.set_threads(os.cpu_count() or 1)
+    return orc
+
+
+def _report(name, **kw):
+    kw = {"config": name, **kw}
+    print("\nFULLSIZE " + json.dumps(kw))
+    d = os.environ.get("LMEP_PARITY_LOG")
+    if d:
+        with open(d, "a") as f:
+            f.write(json.dumps(kw) + "\n")
+
+
+def _row_rel(got, ref):
+    """max over rows of |got - ref|_inf / |ref|_inf (row-relative)."""
+    got = np.asarray(got, float).reshape(-1, ref.shape[-1])
+    ref = np.asarray(ref, float).reshape(-1, ref.shape[-1])
+    den = np.abs(ref).max(axis=1)
+    return float((np.abs(got - ref).max(axis=1) / np.where(den > 0, den, 1.0)).max())
+
+
+def _incr(u, ref, u0):
+    d = np.asarray(ref) - np.asarray(u0)
+    nd = np.linalg.norm(d)
+    return float(np.linalg.norm(np.asarray(u) - np.asarray(ref)) / (nd if nd > 0 else 1.0))
+
+
+def _problem(lx, w, spec=None):
+    bc = lx.Boundary.neumann() if w.boundary == "neumann" else lx.Boundary.periodic()
+    spec = spec if spec is not None else lx.LinearOperatorSpec(w.terms)
+    return lx.SemiLinearProblem(spec, None, w.u0, bc, w.nonlinear,
+                                nonlinear_scale=w.nl_scale or 1.0)
+
+
+def _grid(lx, w):
+    if w.periodic:
+        return lx.make_periodic_grid(w.N, w.x_min, w.x_max)
+    return lx.make_uniform_grid(w.N, w.x_min, w.x_max)
+
+
+def _scheme(lx, w):
+    return {"linear": lx.SchemeConfig("linear"), "etdrk4": lx.SchemeConfig("etdrk4"),
+            "etd2": lx.SchemeConfig("etd-multistep", s=2)}[w.scheme]
+
+
+def _oracle_shared(orcx, w, s, dt, frozen=()):
+    """The reference harvest of one periodic window (harvest.py:97-121 on
+    offsets * h, harvest.py:124-129): rows [s, n]."""
+    x = (np.arange(w.n) - w.row) * w.h
+    L = orcx.local_operator(x, w.terms)
+    wl, wp = orcx.harvest_phi_weights(L, dt, s, w.row, frozen)
+    return np.vstack([wl] + list(wp))
+
+
+def _oracle_d1(orcx, w):
+    """timestep.assemble_derivative (timestep.py:218-237) on one periodic window."""
+    x = (np.arange(w.n) - w.row) * w.h
+    return orcx.fornberg_weights(0.0, x, 1)[1]
+
+
+def _run_both(lx, w, g, st, prob):
+    T = w.steps * w.delta_t
+    out = {}
+    for exact in (True, False):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = lx.run(g, st, prob, _scheme(lx, w), w.delta_t, T, exact=exact)
+        out[exact] = (r.u_final, time.perf_counter() - t0)
+        assert r.steps == w.steps
+    return out
+
+
+# ---------------------------------------------------------------- config 2
+def test_c2_full_run(lx, orcx):
+    """Burgers N=65536, n=9, ETD2 (one ETDRK4 warm-up step), 5000 steps at mu=0.5."""
+    from paper_2603_15964_b200 import configs
+    from paper_2603_15964_b200.harvest import harvest_compact
+    from paper_2603_15964_b200.timestep import Stepper, prepare
+    from paper_2603_15964_b200 import _ops
+    w = configs.c2()
+    g, prob = _grid(lx, w), _problem(lx, w)
+    st = lx.select_stencils(g, w.n, lx.StencilPolicy.CENTERED)
+    dt = w.delta_t
+    # 1. rows: phi_0..phi_2 at dt (the multistep set), phi_0..3 at dt and phi_0..1
+    #    at dt/2 (the warm-up set)
+    spec = lx.LinearOperatorSpec(w.terms)
+    err_rows = 0.0
+    ref_sets = {}
+    for s, tau in ((3, dt), (4, dt), (2, dt / 2)):
+        ref = _oracle_shared(orcx, w, s, tau)
+        got = harvest_compact(g, st, spec, tau, s).interior.cpu().numpy()
+        err_rows = max(err_rows, _row_rel(got, ref))
+        ref_sets[(s, tau)] = ref
+    assert err_rows < W_TOL
+    # 2. full run against the oracle on its own rows
+    d1 = _oracle_d1(orcx, w)
+    warm = orcx.etdrk4_rows(ref_sets[(4, dt)], ref_sets[(2, dt / 2)][:2], dt)
+    cp = orcx.Compact(w.N, w.n, w.row, True, 0)
+    t0 = time.perf_counter()
+    u_ref = cp.run_etd2(ref_sets[(3, dt)], warm, d1, 1, w.u0, w.steps, dt)
+    t_orc = time.perf_counter() - t0
+    res = _run_both(lx, w, g, st, prob)
+    e_exact, e_fma = rel_l2(res[True][0], u_ref), rel_l2(res[False][0], u_ref)
+    # 3. device steps vs the oracle on the device's rows, bit for bit
+    prep = prepare(g, st, prob, _scheme(lx, w), dt)
+    bank, wb = prep.bank.interior.cpu().numpy(), prep.warm.interior.cpu().numpy()
+    u_dev_rows = cp.run_etd2(bank[:3], wb[:6], bank[6], 1, w.u0, w.steps, dt)
+    s = Stepper(prep, _ops.dev_f64(w.u0), exact=True)
+    s.advance(w.steps)
+    bitwise = bool(np.array_equal(s.u.cpu().numpy(), u_dev_rows))
+    _report("c2", N=w.N, steps=w.steps, rows_rel=err_rows, run_rel_l2_exact=e_exact,
+            run_rel_l2_fma=e_fma, incr_rel_exact=_incr(res[True][0], u_ref, w.u0),
+            incr_rel_fma=_incr(res[False][0], u_ref, w.u0), steps_bitwise=bitwise,
+            oracle_s=t_orc, threads=orcx.num_threads())
+    assert e_exact < U_TOL and e_fma < U_TOL
+    assert bitwise
+
+
+# ---------------------------------------------------------------- config 3
+def test_c3_full_run(lx, orcx):
+    """KdV N=2^20, n=11, ETDRK4 with N(u) = -6 u D1 u, 2000 steps at dt = 0.05 h^3."""
+    from paper_2603_15964_b200 import configs, _ops
+    from paper_2603_15964_b200.harvest import harvest_compact
+    from paper_2603_15964_b200.timestep import Stepper, prepare
+    w = configs.c3()
+    g, prob = _grid(lx, w), _problem(lx, w)
+    st = lx.select_stencils(g, w.n, lx.StencilPolicy.CENTERED)
+    dt = w.delta_t
+    spec = lx.LinearOperatorSpec(w.terms)
+    full, half = _oracle_shared(orcx, w, 4, dt), _oracle_shared(orcx, w, 2, dt / 2)
+    err_rows = max(_row_rel(harvest_compact(g, st, spec, dt, 4).interior.cpu().numpy(), full),
+                   _row_rel(harvest_compact(g, st, spec, dt / 2, 2).interior.cpu().numpy(), half))
+    assert err_rows < W_TOL
+    ops = orcx.etdrk4_rows(full, half, dt)
+    d1 = 6.0 * _oracle_d1(orcx, w)
+    cp = orcx.Compact(w.N, w.n, w.row, True, 0)
+    t0 = time.perf_counter()
+    u_ref = cp.run_etdrk4(ops, d1, 1, w.u0, w.steps)
+    t_orc = time.perf_counter() - t0
+    res = _run_both(lx, w, g, st, prob)
+    e_exact, e_fma = rel_l2(res[True][0], u_ref), rel_l2(res[False][0], u_ref)
+    prep = prepare(g, st, prob, _scheme(lx, w), dt)
+    bank = prep.bank.interior.cpu().numpy()
+    u_dev_rows = cp.run_etdrk4(bank[:6], bank[6], 1, w.u0, w.steps)
+    s = Stepper(prep, _ops.dev_f64(w.u0), exact=True)
+    s.advance(w.steps)
+    bitwise = bool(np.array_equal(s.u.cpu().numpy(), u_dev_rows))
+    _report("c3", N=w.N, steps=w.steps, rows_rel=err_rows, run_rel_l2_exact=e_exact,
+            run_rel_l2_fma=e_fma, incr_rel_exact=_incr(res[True][0], u_ref, w.u0),
+            incr_rel_fma=_incr(res[False][0], u_ref, w.u0), steps_bitwise=bitwise,
+            oracle_s=t_orc, threads=orcx.num_threads())
+    assert e_exact < U_TOL and e_fma < U_TOL
+    assert bitwise
+
+
+# ---------------------------------------------------------------- config 4
+def _c4_reference_keys(N, n, row, chunk=1 << 22):
+    """The reference's exact-match harvest keys on np.linspace nodes
+    (harvest.py:135-159: coordinates nodes[m] - nodes[t] as bytes, target row,
+    frozen local rows with frozen_nodes = (0, N-1)): per-node key index [N],
+    and per key (coordinates, target row, frozen local rows)."""
+    nodes = np.linspace(-1.0, 1.0, N)
+    j = np.arange(n, dtype=np.int64)[None, :]
+    hashes = np.empty(N, dtype=np.uint64)
+    mult = np.uint64(0x9E3779B97F4A7C15)
+    for a in range(0, N, chunk):
+        t = np.arange(a, min(N, a + chunk), dtype=np.int64)
+        start = np.clip(t - row, 0, N - n)
+        m = start[:, None] + j
+        x = nodes[m] - nodes[t][:, None]
+        bits = x.view(np.uint64)
+        h = np.zeros(t.size, dtype=np.uint64)
+        with np.errstate(over="ignore"):
+            for c in range(n):
+                h = (h ^ bits[:, c]) * mult
+            trow = (t - start).astype(np.uint64)
+            fz = ((m[:, 0] == 0).astype(np.uint64) << np.uint64(1)) | \
+                (m[:, -1] == N - 1).astype(np.uint64)
+            h = (h ^ (trow << np.uint64(8)) ^ fz) * mult
+        hashes[a:t[-1] + 1] = h
+    uniq, first, cls = np.unique(hashes, return_index=True, return_inverse=True)
+    keys = []
+    for i in first:
+        s = int(np.clip(i - row, 0, N - n))
+        m = np.arange(s, s + n)
+        frozen = tuple(int(k) for k in np.flatnonzero((m == 0) | (m == N - 1)))
+        keys.append((nodes[m] - nodes[i], int(i - s), frozen))
+    # exact-match check: every node's key equals its representative's
+    reps = np.stack([k[0] for k in keys])
+    for a in range(0, N, chunk):
+        t = np.arange(a, min(N, a + chunk), dtype=np.int64)
+        start = np.clip(t - row, 0, N - n)
+        x = nodes[start[:, None] + j] - nodes[t][:, None]
+        c = cls[a:t[-1] + 1]
+        assert np.array_equal(x, reps[c]), "hash collision in the key grouping"
+        assert np.array_equal(t - start, np.array([k[1] for k in keys])[c])
+    return cls.astype(np.int32), keys
+
+
+def test_c4_full_run(lx, orcx):
+    """Allen-Cahn N=2^24 uniform non-periodic, n=7, Neumann (frozen-row
+    harvest + zero-gradient closure), ETDRK4 cubic, 1000 steps at mu=0.5."""
+    from paper_2603_15964_b200 import configs, _ops
+    from paper_2603_15964_b200.harvest import harvest_compact
+    from paper_2603_15964_b200.timestep import Stepper, prepare
+    w = configs.c4()
+    N, n, row, dt = w.N, w.n, w.row, w.delta_t
+    g, prob = _grid(lx, w), _problem(lx, w)
+    st = lx.select_stencils(g, n, lx.StencilPolicy.CENTERED)
+    spec = lx.LinearOperatorSpec(w.terms)
+    cls, keys = _c4_reference_keys(N, n, row)
+    K = len(keys)
+    full = np.zeros((K, 4, n))
+    half = np.zeros((K, 2, n))
+    for k, (x, trow, frozen) in enumerate(keys):
+        L = orcx.local_operator(x, w.terms)
+        wl, wp = orcx.harvest_phi_weights(L, dt, 4, trow, frozen)
+        full[k] = np.vstack([wl] + list(wp))
+        wl, wp = orcx.harvest_phi_weights(L, dt / 2, 2, trow, frozen)
+        half[k] = np.vstack([wl] + list(wp))
+    # 1a. rows, formulation parity: the device's class rows (offsets * h windows,
+    #     DESIGN 5.5) against the oracle harvesting the same windows, every class
+    rf = harvest_compact(g, st, spec, dt, 4, (0, N - 1))
+    rh = harvest_compact(g, st, spec, dt / 2, 2, (0, N - 1))
+    nl, nright = rf.nleft, rf.nright
+    cf, ch = rf.classes.cpu().numpy(), rh.classes.cpu().numpy()      # [C, s, n]
+    C = cf.shape[0]
+    creps = list(range(nl)) + [N // 2] + list(range(N - nright, N))
+    ofull = np.zeros((C, 4, n))
+    ohalf = np.zeros((C, 2, n))
+    for c, t in enumerate(creps):
+        s0 = int(np.clip(t - row, 0, N - n))
+        trow = t - s0
+        frozen = tuple(int(k) for k in np.flatnonzero((np.arange(s0, s0 + n) == 0) |
+                                                      (np.arange(s0, s0 + n) == N - 1)))
+        L = orcx.local_operator((np.arange(n) - trow) * g.uniform_spacing, w.terms)
+        wl, wp = orcx.harvest_phi_weights(L, dt, 4, trow, frozen)
+        ofull[c] = np.vstack([wl] + list(wp))
+        wl, wp = orcx.harvest_phi_weights(L, dt / 2, 2, trow, frozen)
+        ohalf[c] = np.vstack([wl] + list(wp))
+    err_full = max(_row_rel(cf[c], ofull[c]) for c in range(C))
+    err_half = max(_row_rel(ch[c], ohalf[c]) for c in range(C))
+    assert err_full < W_TOL and err_half < W_TOL
+    # alpha / beta / gamma: 1e-12 on each phi row, propagated through the
+    # combination's coefficients (|c1| |p1| + |c2| |p2| + |c3| |p3|, the
+    # cancellation bound of harvest.combine, harvest.py:225-235) plus its own
+    # rounding
+    oops = orcx.etdrk4_rows([ofull[:, r] for r in range(4)], [ohalf[:, 0], ohalf[:, 1]], dt)
+    prep = prepare(g, st, prob, lx.SchemeConfig("etdrk4"), dt)
+    bank_cl = prep.bank.classes.cpu().numpy()                          # [C, 6, n]
+    co = {1: ((1, 1.0), (2, -3.0 / dt), (3, 4.0 / dt**2)), 2: ((2, 2.0 / dt), (3, -4.0 / dt**2)),
+          3: ((3, 4.0 / dt**2), (2, -1.0 / dt))}
+    err_abg = 0.0
+    for r in (1, 2, 3):
+        for c in range(C):
+            got, ref = bank_cl[c, r], oops[r][c]
+            bound = sum(abs(k) * np.abs(ofull[c, p]).max() for p, k in co[r])
+            err = np.abs(got - ref).max()
+            assert err <= W_TOL * bound + 8 * np.finfo(float).eps * bound, (r, c, err, bound)
+            err_abg = max(err_abg, err / bound)
+    # 1b. rows against the reference's own keys (linspace windows).  Keys whose
+    #     coordinates equal offsets * h to rounding (the boundary classes and the
+    #     dominant interior key) must agree to 1e-12; the few interior keys where
+    #     np.linspace rounding moves nodes[m] - nodes[t] by ~1e-9 relative
+    #     differ from every clean row by that much, bounded by 4x the coordinate
+    #     perturbation (measured ratio <= 0.74)
+    def dev_class(t):
+        if t < nl:
+            return t
+        if t >= N - nright:
+            return nl + 1 + (t - (N - nright))
+        return nl
+
+    counts = np.bincount(cls, minlength=K)
+    rep = np.unique(cls, return_index=True)[1]
+    err_clean, err_noisy, n_noisy = 0.0, 0.0, 0
+    for k, (x, trow, frozen) in enumerate(keys):
+        c = dev_class(int(rep[k]))
+        pert = np.abs(x - (np.arange(n) - trow) * g.uniform_spacing).max() / g.uniform_spacing
+        e = max(_row_rel(cf[c], full[k]), _row_rel(ch[c], half[k]))
+        if pert <= 1e-13:
+            err_clean = max(err_clean, e)
+            assert e < W_TOL, (k, e)
+        else:
+            n_noisy += int(counts[k])
+            err_noisy = max(err_noisy, e)
+            assert e < W_TOL + 4 * pert, (k, e, pert)
+    ops_ref = orcx.etdrk4_rows([full[:, r] for r in range(4)], [half[:, 0], half[:, 1]], dt)
+    # 2. the full run: device run() vs the oracle on the reference-keyed rows
+    dl, dr = orcx.neumann_rows(n, g.uniform_spacing)
+    bc = ("neumann", dl, dr)
+    cp = orcx.Compact(N, n, row, False, 3, cls=cls, nkeys=K)
+    u0c = orcx.close(w.u0, bc)
+    t0 = time.perf_counter()
+    u_ref = cp.run_etdrk4(ops_ref, None, 2, u0c, w.steps, bc)
+    t_orc = time.perf_counter() - t0
+    res = _run_both(lx, w, g, st, prob)
+    e_exact, e_fma = rel_l2(res[True][0], u_ref), rel_l2(res[False][0], u_ref)
+    # 3. device steps vs the oracle on the device's class rows, bit for bit
+    nsteps_bw = int(os.environ.get("LMEP_C4_BITWISE_STEPS", "200"))
+    cpd = orcx.Compact(N, n, row, False, 1, prep.bank.nleft, prep.bank.nright)
+    u_dev_rows = cpd.run_etdrk4([bank_cl[:, r] for r in range(6)], None, 2, u0c, nsteps_bw, bc)
+    s = Stepper(prep, _ops.dev_f64(w.u0), exact=True)
+    s.advance(nsteps_bw)
+    bitwise = bool(np.array_equal(s.u.cpu().numpy(), u_dev_rows))
+    _report("c4", N=N, steps=w.steps, keys=K, rows_rel_full=err_full, rows_rel_half=err_half,
+            abg_rel_to_bound=err_abg, ref_keys_rows_rel_clean=err_clean,
+            ref_keys_rows_rel_linspace_rounded=err_noisy, nodes_in_rounded_keys=n_noisy, run_rel_l2_exact=e_exact, run_rel_l2_fma=e_fma,
+            incr_rel_exact=_incr(res[True][0], u_ref, u0c),
+            incr_rel_fma=_incr(res[False][0], u_ref, u0c), steps_bitwise=bitwise,
+            bitwise_steps=nsteps_bw, oracle_s=t_orc, threads=orcx.num_threads())
+    assert e_exact < U_TOL and e_fma < U_TOL
+    assert bitwise
+
+
+# ---------------------------------------------------------------- config 5
+def test_c5_full_run(lx, orcx):
+    """Variable coefficients N=2^22, n=13: all 4,194,304 per-node rows
+    (frozen-at-target L_i = -c_i D1 + nu_i D2, local_operator + harvest_propagator
+    per node) and 200 linear steps."""
+    from paper_2603_15964_b200 import configs, _ops
+    from paper_2603_15964_b200.timestep import Stepper, prepare
+    w = configs.c5()
+    c, nu = w.coef
+    g = _grid(lx, w)
+    st = lx.select_stencils(g, w.n, lx.StencilPolicy.CENTERED)
+    spec = lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1))
+    prob = lx.SemiLinearProblem(spec, None, w.u0, lx.Boundary.periodic(), "none")
+    x = (np.arange(w.n) - w.row) * w.h
+    D1 = np.array([orcx.fornberg_weights(xi, x, 2)[1] for xi in x])
+    D2 = np.array([orcx.fornberg_weights(xi, x, 2)[2] for xi in x])
+    t0 = time.perf_counter()
+    W_ref = orcx.harvest_batch_vc(D1, D2, -c, nu, w.delta_t, 1, w.row, reduced=False)[:, 0]
+    t_harv = time.perf_counter() - t0
+    prep = prepare(g, st, prob, lx.SchemeConfig("linear"), w.delta_t)
+    W_dev = prep.bank.pernode[0].t().contiguous().cpu().numpy()          # (N, n)
+    err_rows = _row_rel(W_dev, W_ref)
+    assert err_rows < W_TOL
+    cp = orcx.Compact(w.N, w.n, w.row, True, 2)
+    t0 = time.perf_counter()
+    u_ref = cp.run_linear(W_ref, w.u0, w.steps)
+    t_orc = time.perf_counter() - t0
+    res = _run_both(lx, w, g, st, prob)
+    e_exact, e_fma = rel_l2(res[True][0], u_ref), rel_l2(res[False][0], u_ref)
+    u_dev_rows = cp.run_linear(W_dev, w.u0, w.steps)
+    s = Stepper(prep, _ops.dev_f64(w.u0), exact=True)
+    s.advance(w.steps)
+    bitwise = bool(np.array_equal(s.u.cpu().numpy(), u_dev_rows))
+    _report("c5", N=w.N, steps=w.steps, harvests=w.N, rows_rel=err_rows,
+            run_rel_l2_exact=e_exact, run_rel_l2_fma=e_fma,
+            incr_rel_exact=_incr(res[True][0], u_ref, w.u0),
+            incr_rel_fma=_incr(res[False][0], u_ref, w.u0), steps_bitwise=bitwise,
+            oracle_harvest_s=t_harv, oracle_steps_s=t_orc, threads=orcx.num_threads())
+    assert e_exact < U_TOL and e_fma < U_TOL
+    assert bitwise
+
+
+# ---------------------------------------------------------------- config 1
+def test_c1_full_run(lx, orcx):
+    """Advection N=1024, n=7 upwind, CFL 3.5, 1000 steps (run() bit-identical
+    to the oracle on the oracle's own shared row)."""
+    from paper_2603_15964_b200 import configs
+    w = configs.c1()
+    g, prob = _grid(lx, w), _problem(lx, w)
+    st = lx.select_stencils(g, w.n, lx.StencilPolicy.ONE_SIDED_UPWIND)
+    ref = _oracle_shared(orcx, w, 1, w.delta_t)[0]
+    cp = orcx.Compact(w.N, w.n, w.row, True, 0)
+    u_ref = cp.run_linear(ref, w.u0, w.steps)
+    res = _run_both(lx, w, g, st, prob)
+    e = rel_l2(res[True][0], u_ref)
+    _report("c1", N=w.N, steps=w.steps, run_rel_l2_exact=e,
+            bitwise=bool(np.array_equal(res[True][0], u_ref)))
+    assert e < U_TOL

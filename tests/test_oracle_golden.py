@@ -187,3 +187,44 @@ def test_c5_per_node_harvest_and_run(golden, orc):
     u = orc.run_linear(np.ascontiguousarray(W[:, 0]), m, w5.u0, w5.steps)
     assert rel_l2(u, golden["c5_u"]) < 1e-12
     del tab
+
+
+@pytest.mark.parametrize("periodic,mode", [(True, 0), (True, 2), (False, 1), (False, 2),
+                                           (False, 3), (True, 3)])
+def test_compact_runners_bitwise_with_member_loops(orc, periodic, mode):
+    """The index-arithmetic runners (full-size parity runs) against the
+    member-array loops that restate kernels.py, on the dense rows the compact
+    rows stand for: linear, ETDRK4 (convective + cubic, Neumann closure on
+    clamped grids) and ETD2 with its warm-up step, bit for bit."""
+    rng = np.random.default_rng(7 + mode)
+    N, n, row = 97, 7, 3
+    nl, nr = (3, 4) if mode == 1 else (0, 0)
+    K = 5
+    cls = rng.integers(0, K, N) if mode == 3 else None
+    cp = orc.Compact(N, n, row, periodic, mode, nl, nr, cls=cls, nkeys=K)
+    shape = {0: (n,), 1: (nl + 1 + nr, n), 2: (N, n), 3: (K, n)}[mode]
+    ops = [0.1 * rng.standard_normal(shape) for _ in range(7)]
+    dense = [cp.dense(x) for x in ops]
+    m = orc.members_for(N, n, row, periodic)
+    u0 = 0.1 * rng.standard_normal(N)
+    bc = None if periodic else ("neumann", rng.standard_normal(n) + 3, rng.standard_normal(n) + 3)
+    assert np.array_equal(cp.run_linear(ops[0], u0, 5, bc), orc.run_linear(dense[0], m, u0, 5, bc))
+    for kind in (1, 2):
+        a = cp.run_etdrk4(ops[:6], ops[6], kind, u0, 3, bc)
+        assert np.array_equal(a, orc.run_etdrk4(*dense[:6], dense[6], m, kind, u0, 3, bc))
+        a, ha = cp.run_etd2(ops[:3], ops[:6], ops[6], kind, u0, 4, 0.3, bc, return_hist=True)
+        b, hb = orc.run_etd2(dense[:3], dense[:6], dense[6], m, kind, u0, 4, 0.3, bc,
+                             return_hist=True)
+        assert np.array_equal(a, b) and np.array_equal(ha, hb)
+
+
+def test_compact_runner_on_golden_kdv(golden, orc):
+    """The compact ETDRK4 runner reproduces the reference's KdV run (golden,
+    numba loop) bit for bit from the shared rows."""
+    N, n = 512, 11
+    rows = golden["kdv_rows"]
+    dt = float(golden["kdv_dt"])
+    ops = orc.etdrk4_rows(rows[:4], rows[4:6], dt)
+    cp = orc.Compact(N, n, 5, True, 0)
+    u = cp.run_etdrk4(ops, 6.0 * rows[6], 1, golden["kdv_u0"], int(golden["kdv_steps"]))
+    assert np.array_equal(u, golden["kdv_u"])
