@@ -421,36 +421,89 @@ def time_other_configs():
 
 
 # ------------------------------------------------------------------ CPU arm
-def cpu_c5(sample_nodes=1 << 14, sample_steps=2, threads=None):
-    """The oracle (C restatement of the reference, OpenMP) on a bounded sample of
-    config 5: per-node harvest of `sample_nodes` nodes and `sample_steps`
-    full-grid per-node steps, extrapolated to the whole pass."""
-    from oracle import oracle as orc
-    orc.build()
-    if threads:
-        orc.set_threads(threads)
-    cores = orc.num_threads()
-    w, coef = c5_inputs()
-    x = (np.arange(w.n) - w.row) * w.h
-    D1 = np.array([orc.fornberg_weights(xi, x, 2)[1] for xi in x])
-    D2 = np.array([orc.fornberg_weights(xi, x, 2)[2] for xi in x])
-    idx = np.linspace(0, w.N - 1, sample_nodes).astype(np.int64)
-    t0 = time.perf_counter()
-    W = orc.harvest_batch_vc(D1, D2, coef[idx, 0], coef[idx, 1], w.delta_t, 1, w.row,
-                             reduced=True)
-    th = (time.perf_counter() - t0) / sample_nodes
-    Wfull = np.tile(W[:, 0], (w.N // sample_nodes + 1, 1))[: w.N]
-    m = orc.members_for(w.N, w.n, w.row, True)
-    t0 = time.perf_counter()
-    orc.run_linear(np.ascontiguousarray(Wfull), m, w.u0, sample_steps)
-    ts = (time.perf_counter() - t0) / sample_steps
-    total = th * w.N + ts * w.steps
-    return {"value": w.N * w.steps / total, "unit": "grid-point updates/s", "cores": cores,
+class CpuC5:
+    """The reference's config-5 pass restated in C (oracle/, test infrastructure):
+    every node's L_i = -c_i D1 + nu_i D2 from one Fornberg table (bit-identical
+    to local_operator) exponentiated by the scipy restatement
+    (balancing + Pade scaling-and-squaring, harvest_propagator,
+    harvest.py:73-79) -- all 4,194,304 of them -- then the reference's stencil
+    member array (harvest.py:172) and its 200 steps of kernels.run_linear
+    (kernels.py:33-43, member-array banded mat-vec).  Nothing is sampled or
+    extrapolated: one call is one whole pass.  harvest_s / step_s follow
+    SimulationResult.harvest_ns / step_ns (timestep.py:284,308,341-343)."""
+
+    def __init__(self):
+        from oracle import oracle as orc
+        orc.build()
+        self.orc = orc
+        self.w, self.coef = c5_inputs()
+        w = self.w
+        x = (np.arange(w.n) - w.row) * w.h
+        self.D1 = np.array([orc.fornberg_weights(xi, x, 2)[1] for xi in x])
+        self.D2 = np.array([orc.fornberg_weights(xi, x, 2)[2] for xi in x])
+
+    def set_threads(self, threads):
+        self.orc.set_threads(int(threads))
+        return self.orc.num_threads()
+
+    def full_pass(self):
+        orc, w = self.orc, self.w
+        t0 = time.perf_counter()
+        W = orc.harvest_batch_vc(self.D1, self.D2, self.coef[:, 0], self.coef[:, 1], w.delta_t, 1,
+                                 w.row, reduced=False)[:, 0]
+        m = orc.members_for(w.N, w.n, w.row, True)
+        t1 = time.perf_counter()
+        u = orc.run_linear(np.ascontiguousarray(W), m, w.u0, w.steps)
+        t2 = time.perf_counter()
+        if not np.isfinite(u).all():
+            raise RuntimeError("reference C5 pass produced non-finite values")
+        return t1 - t0, t2 - t1
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_one_core(cpu: CpuC5) -> dict:
+    """the reference is single-threaded -- one full pass on
+    one core (affinity pinned to the first allowed CPU, like taskset -c, and one
+    OpenMP thread)."""
+    allowed = os.sched_getaffinity(0)
+    first = min(allowed)
+    threads = cpu.orc.num_threads()
+    try:
+        os.sched_setaffinity(0, {first})
+        cpu.set_threads(1)
+        hs, ss = cpu.full_pass()
+    finally:
+        os.sched_setaffinity(0, allowed)
+        cpu.set_threads(threads)
+    w = cpu.w
+    return {"value": w.N * w.steps / (hs + ss), "unit": "grid-point updates/s", "cores": 1,
+            "pinned_cpu": first, "harvest_ns": int(hs * 1e9), "step_ns": int(ss * 1e9),
+            "harvests_per_s": w.N / hs, "sample": "one whole config-5 pass (all 4194304 "
+            "harvests + 200 steps), one thread pinned to one core"}
+
+
+def cpu_c5(passes=1):
+    """All host cores, whole passes (no sampling): the cpu_baseline leg."""
+    cpu = CpuC5()
+    cores = cpu.set_threads(host_cores())
+    hs = ss = 0.0
+    for _ in range(passes):
+        h, s_ = cpu.full_pass()
+        hs += h
+        ss += s_
+    w = cpu.w
+    hs, ss = hs / passes, ss / passes
+    return {"value": w.N * w.steps / (hs + ss), "unit": "grid-point updates/s", "cores": cores,
             "kind": "port",
-            "sample": f"oracle C port (OpenMP {cores} threads): per-node harvest of {sample_nodes} "
-                      f"of {w.N} nodes + {sample_steps} of {w.steps} per-node steps on the full "
-                      f"N={w.N} grid, extrapolated to one full pass",
-            "harvests_per_s": 1.0 / th, "step_s": ts}
+            "sample": f"oracle C port (OpenMP {cores} threads), {passes} whole config-5 pass(es): "
+                      f"all {w.N} per-node harvests + {w.steps} member-array steps, timed",
+            "harvest_ns": int(hs * 1e9), "step_ns": int(ss * 1e9), "harvests_per_s": w.N / hs}
 
 
 # ------------------------------------------------------------------ main
@@ -484,17 +537,33 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        cb = cpu_c5()
-        vals = []
-        for _ in range(args.warmup + args.steps):
-            pass
-        line = {"metric": metric, "value": cb["value"], "unit": unit, "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": 1e3 * (1 << 22) * 200 / cb["value"], "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": config, "impl": "reference",
-                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
-                "e2e": {"value": cb["value"], "unit": unit, "h2d_bytes_per_step": 0,
+        cpu = CpuC5()
+        cores = cpu.set_threads(host_cores())
+        for _ in range(args.warmup):
+            cpu.full_pass()
+        hs, ss = [], []
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            h, s_ = cpu.full_pass()
+            hs.append(h)
+            ss.append(s_)
+        wall = time.perf_counter() - t0
+        ms = 1e3 * wall / args.steps
+        w = cpu.w
+        value = w.N * w.steps / (ms * 1e-3)
+        one = None if args.no_cpu else cpu_one_core(cpu)
+        line = {"metric": metric, "value": value, "unit": unit, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic", "config": config, "impl": "reference",
+                "harvest_ns": int(1e9 * float(np.mean(hs))), "step_ns": int(1e9 * float(np.mean(ss))),
+                "harvests_per_s": w.N / float(np.mean(hs)),
+                "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "port",
+                                 "sample": f"each step one whole config-5 pass (all {w.N} per-node "
+                                           f"harvests + {w.steps} member-array steps) in the oracle "
+                                           f"C port, OpenMP {cores} threads; nothing extrapolated"},
+                "cpu_1core": one,
+                "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
@@ -669,7 +738,8 @@ def main():
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": None if cpu is None else
-            {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "harvest_ns",
+                                 "step_ns")},
             "workloads": others,
         }
         print(json.dumps(line))

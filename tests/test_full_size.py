@@ -358,7 +358,7 @@ def test_c4_full_run(lx, orcx):
     res = _run_both(lx, w, g, st, prob)
     e_exact, e_fma = rel_l2(res[True][0], u_ref), rel_l2(res[False][0], u_ref)
     # 3. device steps vs the oracle on the device's class rows, bit for bit
-    nsteps_bw = int(os.environ.get("LMEP_C4_BITWISE_STEPS", "200"))
+    nsteps_bw = int(os.environ.get("LMEP_C4_BITWISE_STEPS", str(w.steps)))
     cpd = orcx.Compact(N, n, row, False, 1, prep.bank.nleft, prep.bank.nright)
     u_dev_rows = cpd.run_etdrk4([bank_cl[:, r] for r in range(6)], None, 2, u0c, nsteps_bw, bc)
     s = Stepper(prep, _ops.dev_f64(w.u0), exact=True)
