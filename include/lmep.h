@@ -238,22 +238,21 @@ int lmep_harvest_chunk(int n, int s, int nterms, const double *tables, const int
  *     item for d <= 13, else 4); everything else the per-item kernel
  *     (harvest_mv.cuh: per-item balancing, 4 lanes per item);
  *   1 = full Pade scaling-and-squaring per warp (harvest.cu);
- *   2 / 3 = the first-generation expm-multiply kernel, 4 / 8 lanes per item
- *     (harvest_quad.cu);
+ *   2 / 3 = retired (the first-generation kernel): LMEP_INVALID_CONFIG;
  *   4 = the per-item kernel with 8 lanes per item for d > 8;
  *   5 = the per-item kernel only (no block-balanced path);
  *   6 / 7 / 8 = as 0 with the block-balanced kernel forced to 8 / 2 / 4 lanes
  *     per item (tuning, tests), no constant-table kernel;
  *   9 = as 0 without the constant-table kernel.
- * lmep_expm always uses the Pade kernel.  Process-wide setting; returns
- * LMEP_INVALID_CONFIG for other codes. */
+ * lmep_expm always uses the Pade kernel.  The setting belongs to the calling
+ * thread's current CUDA device; returns LMEP_INVALID_CONFIG for other codes. */
 int lmep_set_harvest_method(int method);
 
 /* Ring mode of the linear scheme (a periodic grid resident on chip for all
  * steps, BASELINE config 1): 1 (default) = one thread-block cluster of 8 CTAs
  * exchanging halos through distributed shared memory every kb steps when
  * N % 8 == 0 (ring_lin_cluster_kernel), 0 = one CTA (ring_lin_kernel).
- * Process-wide setting; results are bit-identical either way. */
+ * Per-device setting (the current device); results are bit-identical either way. */
 int lmep_set_ring_cluster(int on);
 
 /* ---- stepping (K3, K4, K5) ---------------------------------------------- */

@@ -170,15 +170,15 @@ def check(status: int, what: str, state=None, time=None) -> None:
 
 
 def set_harvest_method(method: str) -> None:
-    """'multiply' (default for d <= 16: warp-uniform expm-multiply; large
-    single-geometry per-node batches take the block-balanced kernel
-    the constant-table kernel harvest_mvc for s = 1, else harvest_mvb),
-    "mvb" (auto without harvest_mvc), "mvitem" (per-item balanced expm-multiply only, 4 lanes per
-    item), "mv8" (the same with 8 lanes per item for d > 8), "pade" (full
-    expm per warp), or the first-generation kernel "quad" (8 lanes) /
-    "multiply4" (4 lanes)."""
-    code = {"multiply": 0, "auto": 0, "pade": 1, "multiply4": 2, "quad": 3, "mv8": 4,
-            "mvitem": 5, "mvb8": 6, "mvb2": 7, "mvb4": 8, "mvb": 9}[method]
+    """'multiply' (default for d <= 16: expm-multiply; large single-geometry
+    per-node batches take the constant-table kernel harvest_mvc, or the
+    block-balanced kernel harvest_mvb), "mvb" (auto without harvest_mvc),
+    "mvitem" (per-item balanced expm-multiply only, 4 lanes per item), "mv8"
+    (the same with 8 lanes per item for d > 8), "mvb2" / "mvb4" / "mvb8" (the
+    block kernel at 2 / 4 / 8 lanes per item) or "pade" (full expm per warp).
+    Applies to the current CUDA device."""
+    code = {"multiply": 0, "auto": 0, "pade": 1, "mv8": 4, "mvitem": 5, "mvb8": 6, "mvb2": 7,
+            "mvb4": 8, "mvb": 9}[method]
     check(lib().lmep_set_harvest_method(code), "lmep_set_harvest_method")
 
 

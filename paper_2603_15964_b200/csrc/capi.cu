@@ -6,17 +6,42 @@
 
 namespace lmep {
 
-static char g_last_error[512] = "";
-static int64_t g_launches = 0;
+static thread_local char g_last_error[512] = "";
+static std::atomic<int64_t> g_launches{0};
 
 void set_last_error(const char *what, cudaError_t e)
 {
     snprintf(g_last_error, sizeof(g_last_error), "%s: %s", what, cudaGetErrorString(e));
 }
 
+int current_device()
+{
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) dev = 0;
+    return dev < kMaxDevices ? dev : kMaxDevices - 1;
+}
+
+static std::atomic<int> g_sms[kMaxDevices];
+
+int device_sm_count()
+{
+    const int dev = current_device();
+    int v = g_sms[dev].load(std::memory_order_relaxed);
+    if (v <= 0) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+            v = 148;
+        g_sms[dev].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+
+static DeviceSettings g_settings[kMaxDevices];
+
+DeviceSettings &device_settings() { return g_settings[current_device()]; }
+
 int launch_status(const char *what)
 {
-    ++g_launches;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         set_last_error(what, e);
@@ -45,4 +70,4 @@ extern "C" const char *lmep_status_string(int status)
 
 extern "C" const char *lmep_last_error(void) { return lmep::g_last_error; }
 
-extern "C" int64_t lmep_launch_count(void) { return lmep::g_launches; }
+extern "C" int64_t lmep_launch_count(void) { return lmep::g_launches.load(); }

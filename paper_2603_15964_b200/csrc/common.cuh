@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "lmep.h"
 
 namespace lmep {
@@ -24,8 +26,37 @@ __device__ __forceinline__ double macc(double acc, double w, double v)
     else return fma(w, v, acc);
 }
 
-// Host-side error bookkeeping (capi.cu).
+// Host-side error bookkeeping (capi.cu).  The last error is per host thread.
 void set_last_error(const char *what, cudaError_t e);
 int launch_status(const char *what);
+
+// Per-device library state (capi.cu).  One process may drive several GPUs
+// (and several host threads may call in concurrently): nothing device-specific
+// is cached process-wide.
+constexpr int kMaxDevices = 64;
+int current_device();                 // cudaGetDevice, clamped to [0, kMaxDevices)
+int device_sm_count();                // SM count of the current device (cached per device)
+
+// Method switches of lmep_set_harvest_method / lmep_set_ring_cluster, one set
+// per device (the setter applies to the calling thread's current device).
+struct DeviceSettings {
+    std::atomic<int> harvest_method{0};   // 0 auto (expm-multiply for d <= 16), 1 Pade
+    std::atomic<int> mv_lanes{0};         // block / per-item lanes override (0 = heuristic)
+    std::atomic<int> mvc{1};              // constant-table kernel when eligible
+    std::atomic<int> ring_cluster{1};     // linear ring mode on a thread-block cluster
+};
+DeviceSettings &device_settings();
+
+// "Done on this device" bitmask for one-time per-device setup (function
+// attributes, pool thresholds).  The setup runs before the bit is published;
+// two threads racing both run it, which is harmless for those idempotent calls.
+inline bool done_on_device(const std::atomic<uint64_t> &mask, int dev)
+{
+    return (mask.load(std::memory_order_acquire) >> dev) & 1ull;
+}
+inline void mark_device(std::atomic<uint64_t> &mask, int dev)
+{
+    mask.fetch_or(1ull << dev, std::memory_order_release);
+}
 
 }  // namespace lmep

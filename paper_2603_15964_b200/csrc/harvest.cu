@@ -710,10 +710,11 @@ static int launch_harvest(const HarvestParams &P, cudaStream_t st)
     using T = Tile<DP>;
     const size_t shm = (size_t)WPB * T::WARP_DOUBLES * sizeof(double);
     auto kern = harvest_kernel<DP, WPB>;
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    const int dev = current_device();
+    if (!done_on_device(attr, dev)) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
-        attr = true;
+        mark_device(attr, dev);
     }
     const int64_t blocks = (P.B + WPB - 1) / WPB;
     if (blocks > 0x7fffffffLL) return LMEP_INVALID_CONFIG;
@@ -721,22 +722,18 @@ static int launch_harvest(const HarvestParams &P, cudaStream_t st)
     return launch_status("harvest_kernel");
 }
 
-static int g_harvest_method = 0;   // 0: auto (expm-multiply for d <= 16), 1: Pade expm
-static int g_mv_lanes = 0;
-static bool g_mvc = true;          // constant-table kernel (harvest_mvc.cu) when eligible
-int mv_lanes_override() { return g_mv_lanes; }
+int mv_lanes_override() { return device_settings().mv_lanes.load(); }
 
 static int dispatch_harvest(const HarvestParams &P, cudaStream_t st)
 {
     if (P.B == 0) return LMEP_OK;
-    if (P.mode != 0 && g_harvest_method != 1 && P.d >= 2 && P.d <= 16 &&
-        (P.mode == 2 || P.nterms <= 4))
-    {
-        if (g_harvest_method == 0 && g_mv_lanes == 0 && g_mvc && harvest_mvc_eligible(P))
+    const DeviceSettings &ds = device_settings();
+    const int method = ds.harvest_method.load();
+    if (P.mode != 0 && method != 1 && P.d >= 2 && P.d <= 16 && (P.mode == 2 || P.nterms <= 4)) {
+        if (method == 0 && ds.mv_lanes.load() == 0 && ds.mvc.load() && harvest_mvc_eligible(P))
             return launch_harvest_mvc(P, st);
-        if (g_harvest_method == 0 && harvest_mvb_eligible(P)) return launch_harvest_mvb(P, st);
-        if (g_harvest_method == 0 || g_harvest_method == 5) return launch_harvest_mv(P, st);
-        return launch_harvest_quad(P, st);
+        if (method == 0 && harvest_mvb_eligible(P)) return launch_harvest_mvb(P, st);
+        return launch_harvest_mv(P, st);
     }
     if (P.d <= 8) return launch_harvest<8, 8>(P, st);
     if (P.d <= 16) return launch_harvest<16, 4>(P, st);
@@ -863,17 +860,19 @@ extern "C" int lmep_harvest(int n, int s, int nterms, const double *tables,
 
 extern "C" int lmep_set_harvest_method(int method)
 {
-    if (method < 0 || method > 9) return LMEP_INVALID_CONFIG;
-    // 0 auto: block-balanced mv (harvest_mvb.cuh) for large single-geometry batches, else
-    // the per-item mv (4 lanes per item); 1 pade; 2/3 quad (4 / 8 lanes); 4 per-item mv
-    // with 8 lanes for d > 8; 5 per-item mv only; 6 / 7 / 8 auto with the block-balanced
-    // kernel forced to 8 / 2 / 4 lanes per item (tuning); 9 auto without the
-    // constant-table kernel (harvest_mvc.cu)
-    lmep::g_mvc = method == 0;
-    lmep::g_mv_lanes = (method == 4 || method == 6) ? 8 : (method == 7 ? 2 : (method == 8 ? 4 : 0));
+    // 0 auto: constant-table kernel (harvest_mvc.cu) / block-balanced mv
+    // (harvest_mvb.cuh) for large single-geometry batches, else the per-item mv
+    // (4 lanes per item); 1 pade; 4 per-item mv with 8 lanes for d > 8; 5
+    // per-item mv only; 6 / 7 / 8 auto with the block-balanced kernel forced to
+    // 8 / 2 / 4 lanes per item (tuning); 9 auto without the constant-table
+    // kernel.  (2 / 3 named the retired first-generation kernel.)  Applies to
+    // the calling thread's current device.
+    if (method < 0 || method > 9 || method == 2 || method == 3) return LMEP_INVALID_CONFIG;
+    lmep::DeviceSettings &ds = lmep::device_settings();
+    ds.mvc.store(method == 0 ? 1 : 0);
+    ds.mv_lanes.store((method == 4 || method == 6) ? 8 : (method == 7 ? 2 : (method == 8 ? 4 : 0)));
     if (method == 4) method = 5;
     if (method >= 6) method = 0;   // 6..9
-    lmep::g_harvest_method = method;
-    lmep::set_lanes_per_item(method == 2 ? 4 : 8);
+    ds.harvest_method.store(method);
     return LMEP_OK;
 }

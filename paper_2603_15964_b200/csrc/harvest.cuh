@@ -42,9 +42,8 @@ __device__ __forceinline__ int64_t coef_node(const HarvestParams &P, int64_t b, 
     return m;
 }
 
-// expm-multiply harvest for d <= 16: quad kernel (harvest_quad.cu) and the
-// warp-uniform kernel (harvest_mv.cuh, instantiated in harvest_mv_{a,b,c}.cu)
-int launch_harvest_quad(const HarvestParams &P, cudaStream_t st);
+// expm-multiply harvest for d <= 16: the per-item kernel (harvest_mv.cuh,
+// instantiated in harvest_mv_{a,b,c}.cu)
 int launch_harvest_mv_a(const HarvestParams &P, cudaStream_t st);
 int launch_harvest_mv_b(const HarvestParams &P, cudaStream_t st);
 int launch_harvest_mv_c(const HarvestParams &P, cudaStream_t st);
@@ -54,7 +53,6 @@ inline int launch_harvest_mv(const HarvestParams &P, cudaStream_t st)
     if (P.d <= 12) return launch_harvest_mv_b(P, st);
     return launch_harvest_mv_c(P, st);
 }
-void set_lanes_per_item(int lpi);
 
 // block-balanced fast path for large single-geometry per-node batches
 // (harvest_mvb.cuh, instantiated in harvest_mvb_{a,b,c}.cu)

@@ -402,9 +402,14 @@ __global__ void __launch_bounds__(128, 3) harvest_mvc_kernel(const HarvestParams
     if (P.ms) P.ms[b] = nmv | (min(s, 255) << 24);
 }
 
-MvcConst *g_mvc_scratch = nullptr;
-cudaEvent_t g_mvc_done = nullptr;
-cudaStream_t g_mvc_last = nullptr;
+// Per-device state: the prep kernel's output block and the event of the
+// device's last constant-table launch.  (__constant__ c_mvc itself is a
+// per-device copy of the module's constant bank.)
+struct MvcDevice {
+    MvcConst *scratch = nullptr;
+    cudaEvent_t done = nullptr;
+};
+MvcDevice g_mvc_dev[kMaxDevices];
 std::mutex g_mvc_mu;
 
 template <int N, int NT, bool C0, int PA>
@@ -442,24 +447,25 @@ bool harvest_mvc_eligible(const HarvestParams &P)
            P.B < ((int64_t)1 << 31) * 128;
 }
 
-// The constant block is process-wide: calls are serialised in stream order,
-// and a call on another stream than the previous one first waits for the
-// previous call's kernel (event), so a later copy cannot overwrite tables an
-// earlier kernel still reads.
+// The constant block is per device and shared by every stream on it: each call
+// first waits for the device's previous constant-table kernel (event; a no-op
+// on the same stream), so a later copy can never overwrite tables an earlier
+// kernel still reads.  The host mutex orders the enqueues of concurrent threads.
 int launch_harvest_mvc(const HarvestParams &P, cudaStream_t st)
 {
     std::lock_guard<std::mutex> lock(g_mvc_mu);
+    MvcDevice &D = g_mvc_dev[current_device()];
     cudaError_t e = cudaSuccess;
-    if (!g_mvc_scratch) {
-        e = cudaMalloc((void **)&g_mvc_scratch, sizeof(MvcConst));
-        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g_mvc_done, cudaEventDisableTiming);
+    if (!D.scratch) {
+        e = cudaMalloc((void **)&D.scratch, sizeof(MvcConst));
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&D.done, cudaEventDisableTiming);
         if (e != cudaSuccess) { set_last_error("harvest_mvc setup", e); return LMEP_CUDA_ERROR; }
-    } else if (st != g_mvc_last) {
-        e = cudaStreamWaitEvent(st, g_mvc_done, 0);
+    } else {
+        e = cudaStreamWaitEvent(st, D.done, 0);
         if (e != cudaSuccess) { set_last_error("cudaStreamWaitEvent", e); return LMEP_CUDA_ERROR; }
     }
-    mvc_prep_kernel<<<1, 32, 0, st>>>(P, g_mvc_scratch);
-    e = cudaMemcpyToSymbolAsync(c_mvc, g_mvc_scratch, sizeof(MvcConst), 0, cudaMemcpyDeviceToDevice, st);
+    mvc_prep_kernel<<<1, 32, 0, st>>>(P, D.scratch);
+    e = cudaMemcpyToSymbolAsync(c_mvc, D.scratch, sizeof(MvcConst), 0, cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) { set_last_error("cudaMemcpyToSymbolAsync", e); return LMEP_CUDA_ERROR; }
     switch (P.n) {
     case 7: launch_mvc_d<7>(P, st); break;
@@ -467,8 +473,7 @@ int launch_harvest_mvc(const HarvestParams &P, cudaStream_t st)
     case 11: launch_mvc_d<11>(P, st); break;
     default: launch_mvc_d<13>(P, st); break;
     }
-    cudaEventRecord(g_mvc_done, st);
-    g_mvc_last = st;
+    cudaEventRecord(D.done, st);
     return launch_status("harvest_mvc_kernel");
 }
 

@@ -20,23 +20,12 @@ static int step_ext(int sch, int nl)
     return 4 + 4 * cv;
 }
 
-static int g_num_sms = 0;
-static int num_sms()
-{
-    if (g_num_sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
-            g_num_sms <= 0)
-            g_num_sms = 148;
-    }
-    return g_num_sms;
-}
+static int num_sms() { return device_sm_count(); }
 
 static const int64_t kSmemBudget = 200 * 1024;  // bytes per CTA we allow ourselves
 
 int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded, bool pernode,
-                lmep_tuning &t, int64_t pernode_pad, int etds)
+                lmep_tuning &t, int64_t pernode_pad, int etds, bool tma_ok)
 {
     const int n = g.n, eL = g.row, eR = n - 1 - g.row;
     const int ext = step_ext(sch, nl);
@@ -63,7 +52,7 @@ int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded
         // else lin_pernode_tb_kernel; sharded: the caller fuses `steps` steps
         // per halo exchange
         k = sharded ? steps : (t.ksteps > 0 ? t.ksteps : std::min<int64_t>(16, steps));
-        const bool tma = !sharded && (g.N % 2) == 0 && g.N >= tb_nodes_per_cta(n, true);
+        const bool tma = tma_ok && !sharded && (g.N % 2) == 0 && g.N >= tb_nodes_per_cta(n, true);
         const int64_t span = tb_nodes_per_cta(n, tma);
         while (k > 1 && span - k * (n - 1) < span / 2) --k;
         t.tile = (int32_t)(span - k * (n - 1));
@@ -190,11 +179,16 @@ int run_steps(const StepCall &c)
     lmep_tuning t{};
     if (c.tuning) t = *c.tuning;
     if (sharded) { t.ring = 0; }
+    // the TMA kernel bulk-copies u_in and the rows: both 16-byte aligned (a
+    // contiguous view at an odd element offset takes the register-blocked kernel)
+    const bool tma_ok = ((uintptr_t)c.u_in & 15) == 0 && ((uintptr_t)w.pernode & 15) == 0;
     int st = plan_launch(g, c.sch, c.nl, c.steps, sharded, pernode, t, pernode ? w.pernode_pad : 0,
-                         c.etds);
+                         c.etds, tma_ok);
     if (st) return st;
 
-    static StepParams p;  // host staging (the struct is large); calls are serialised per process
+    // host staging of the (large) parameter block, one per calling thread: the
+    // launches copy it, so concurrent callers on other streams never share it
+    static thread_local StepParams p;
     p = StepParams{};
     p.N = g.N; p.off = g.off; p.nloc = g.nloc;
     p.n = g.n; p.row = g.row; p.periodic = g.periodic ? 1 : 0; p.ring = t.ring;
@@ -243,15 +237,15 @@ int run_steps(const StepCall &c)
     // Keep freed stream-ordered allocations in the device pool: with the
     // default release threshold (0) every synchronize returns them to the OS
     // and the next cudaMallocAsync maps fresh pages (milliseconds per call).
-    static bool pool_tuned = false;
-    if (!pool_tuned) {
-        int dev = 0;
+    static std::atomic<uint64_t> pool_tuned{0};
+    const int dev = current_device();
+    if (!done_on_device(pool_tuned, dev)) {
         cudaMemPool_t pool;
-        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
             uint64_t thr = UINT64_MAX;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
-        pool_tuned = true;
+        mark_device(pool_tuned, dev);
     }
     // finiteness flag
     int *flag = c.nonfinite;
@@ -419,7 +413,7 @@ extern "C" int lmep_plan(const lmep_grid *grid, int scheme, int nl_kind, int wei
     if (scheme < 0 || scheme > 2) return LMEP_INVALID_CONFIG;
     lmep_tuning t = *out;
     int st = plan_launch(*grid, scheme, nl_kind, steps, grid->nloc != grid->N,
-                         weight_mode == LMEP_W_PERNODE, t, 0, 2);
+                         weight_mode == LMEP_W_PERNODE, t, 0, 2, true);
     *out = t;
     return st;
 }

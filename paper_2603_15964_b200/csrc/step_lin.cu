@@ -10,7 +10,6 @@ namespace cg = cooperative_groups;
 namespace lmep {
 
 // set by lmep_set_ring_cluster (capi.cu): 1 = cluster ring kernel when eligible
-int g_ring_cluster = 1;
 
 // Ring mode for the linear scheme (a periodic grid resident in one CTA, C1:
 // N = 1024, 1000 steps in one launch).  The whole run is one SM, so the
@@ -167,7 +166,7 @@ int launch_scheme_lin(bool pernode, const StepParams &p, dim3 grid, size_t shm, 
     if (pernode) return launch_ns<SCH_LIN, true, 1, LMEP_NL_NONE, true>(p.n, p, grid, shm, st);
     if (p.ring && p.off == 0 && p.hl == nullptr && p.hr == nullptr && p.wmode == LMEP_W_SHARED &&
         (p.n == 7 || p.n == 9 || p.n == 11 || p.n == 13)) {
-        if (g_ring_cluster) {
+        if (device_settings().ring_cluster.load()) {
             const int rc = launch_ring_cluster(p, st);
             if (rc >= 0) return rc;                  // else: shape not eligible, one-CTA kernel
         }
@@ -368,6 +367,6 @@ int launch_lin_pernode_tb(const StepParams &p, bool exact, cudaStream_t st)
 extern "C" int lmep_set_ring_cluster(int on)
 {
     if (on != 0 && on != 1) return LMEP_INVALID_CONFIG;
-    lmep::g_ring_cluster = on;
+    lmep::device_settings().ring_cluster.store(on);
     return LMEP_OK;
 }

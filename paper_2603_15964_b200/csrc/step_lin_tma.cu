@@ -206,13 +206,7 @@ int launch_lin_pernode_tma(const StepParams &p, bool exact, cudaStream_t st)
     constexpr int J = 3, NT = 512;
     const size_t shm = tma_smem_bytes(p.n, J * NT);
     const int64_t ntiles = (p.nloc + p.tile - 1) / p.tile;
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        if (nsm <= 0) nsm = 148;
-    }
+    const int nsm = device_sm_count();
     const unsigned grid = (unsigned)(ntiles < nsm ? ntiles : nsm);
     if ((p.N & 1) || (p.wld & 1) || ((uintptr_t)p.wp & 15) || ((uintptr_t)p.u_in & 15))
         return LMEP_INVALID_CONFIG;

@@ -400,7 +400,7 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
         if deferred.event is None:           # the harvest did not pipeline: upload now
             deferred.issue(cp1)
         u0d, ev_u0 = deferred.dst, deferred.event
-    nsnap = 1 + -(-steps_total // snap_every)
+    nsnap = 1 + (-(-steps_total // snap_every) if snap_every else 0)
     # snapshots land straight in one page-locked [S, N] block (returned as is)
     snaps = torch.empty((nsnap, N), dtype=torch.float64, pin_memory=True)
     ev_harvest = torch.cuda.Event(enable_timing=True)
@@ -451,6 +451,12 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
                             time=times[-1])
         times.append(done * delta_t)
         prev_ev, snap_ev = snap_ev, snapshot(len(times) - 1)
+    if harvest_ns is None:
+        # zero steps (t_final below the dt rounding tolerance, _steps_for): the
+        # harvest still ran and its status and time are reported (timestep.py:284)
+        cur.synchronize()
+        harvest_ns = int(ev_start.elapsed_time(ev_harvest) * 1e6)
+        _ops.check_deferred(pending)
     cp.synchronize()
     return SimulationResult(times=np.array(times), snapshots=snaps.numpy(), steps=steps_total,
                             harvest_ns=harvest_ns, step_ns=step_ns)

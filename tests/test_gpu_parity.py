@@ -97,7 +97,7 @@ def test_expm_nonfinite(lx):
         lx.expm(np.eye(3) * 1e6)
 
 
-@pytest.fixture(params=["multiply", "mvitem", "mv8", "quad", "multiply4", "pade"])
+@pytest.fixture(params=["multiply", "mvitem", "mv8", "pade"])
 def method(request, lx):
     lx._native.set_harvest_method(request.param)
     yield request.param
