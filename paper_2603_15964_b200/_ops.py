@@ -10,6 +10,7 @@ from __future__ import annotations
 from contextlib import contextmanager
 
 import ctypes as C
+import threading
 import warnings
 from dataclasses import dataclass, field
 
@@ -72,21 +73,31 @@ class DeferredUpload:
         self.event = stream.record_event()
 
 
-_DEFERRED: list[DeferredUpload] = []
+# per host thread: uploads waiting for a pipelined harvest, and the harvest
+# status checks a pipeline defers to its own sync point
+_TLS = threading.local()
+
+
+def _deferred() -> list:
+    if not hasattr(_TLS, "deferred"):
+        _TLS.deferred = []
+    return _TLS.deferred
 
 
 def defer_upload(up: DeferredUpload) -> None:
-    _DEFERRED.append(up)
+    _deferred().append(up)
 
 
 def issue_deferred(stream: torch.cuda.Stream) -> None:
-    while _DEFERRED:
-        _DEFERRED.pop(0).issue(stream)
+    q = _deferred()
+    while q:
+        q.pop(0).issue(stream)
 
 
 def drop_deferred(up: DeferredUpload) -> None:
-    if up in _DEFERRED:
-        _DEFERRED.remove(up)
+    q = _deferred()
+    if up in q:
+        q.remove(up)
 
 
 def is_host(a) -> bool:
@@ -217,20 +228,17 @@ def harvest(n: int, s: int, delta_t: float, B: int, *, tables=None, table_idx=No
     return res
 
 
-_PENDING_STATUS: list | None = None
-
-
 @contextmanager
 def deferred_status_checks():
-    """Within the block, harvests queue their per-item status instead of
-    synchronising on it; the caller runs check_deferred(list) at its own sync
-    point (a pipeline that enqueues harvest + steps back to back)."""
-    global _PENDING_STATUS
-    prev, _PENDING_STATUS = _PENDING_STATUS, []
+    """Within the block (this host thread), harvests queue their per-item
+    status instead of synchronising on it; the caller runs check_deferred(list)
+    at its own sync point (a pipeline that enqueues harvest + steps back to back)."""
+    prev = getattr(_TLS, "pending", None)
+    _TLS.pending = []
     try:
-        yield _PENDING_STATUS
+        yield _TLS.pending
     finally:
-        _PENDING_STATUS = prev
+        _TLS.pending = prev
 
 
 def check_deferred(pending: list) -> None:
@@ -241,8 +249,9 @@ def check_deferred(pending: list) -> None:
 
 
 def raise_on_status(h: HarvestOut, what="matrix exponential overflowed") -> None:
-    if _PENDING_STATUS is not None:
-        _PENDING_STATUS.append((h.status, what))
+    pending = getattr(_TLS, "pending", None)
+    if pending is not None:
+        pending.append((h.status, what))
         return
     if int(h.status.abs().max().item() if h.status.numel() else 0) != 0:
         nat.check(nat.LMEP_NONFINITE, what)
