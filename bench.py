@@ -631,14 +631,23 @@ def main():
             left -= ks[-1]
         step_bytes_total = sum(bench.nloc * (8 * w.n + 8) * span / (span - k * (w.n - 1)) +
                                bench.nloc * 8 for k in ks)
-        step_kernel = (f"lin_pernode_tma_kernel<13,3> (persistent, TMA-pipelined; rows in registers, "
-                       f"{min(ks)}-{max(ks)} steps/launch)")
+        step_kernel = ("lin_pernode_tma_kernel<13,3,512> (persistent, TMA-pipelined; rows in "
+                       "registers, shared-memory windows, " if args.exact else
+                       "lin_pernode_tmx_kernel<13,6,6,256> (persistent, TMA-pipelined; rows and "
+                       "values in registers, slot-major halo exchange, ") + \
+            f"{min(ks)}-{max(ks)} steps/launch)"
         per_launch_ms = step_ms / launches_steps
         step_bytes = step_bytes_total / launches_steps
+        step_note = (f"rows held in registers for {min(ks)}-{max(ks)} steps per launch: "
+                     f"{step_bytes_total / (bench.nloc * w.steps):.1f} B/point-step against 120 for "
+                     "one step per launch (roofline_step_onestep); after blocking the kernel is "
+                     "bound by the per-step halo exchange + barrier and the FP64 pipe, see "
+                     "roofline_step_fp64")
     else:
         step_bytes = bench.nloc * (8 * w.n + 16)           # u in/out + 13 rows per node
         step_kernel = "lin_pernode_kernel<13,4> (per-node rows, one step per launch)"
         per_launch_ms = step_ms / w.steps
+        step_note = "one step per launch: 16 + 8n bytes per point-step"
     achieved = step_bytes / (per_launch_ms * 1e-3) / 1e9
     ms_items = bench.harvest_ms_stats()
     d = w.n                                               # s = 1: d = n
@@ -698,10 +707,7 @@ def main():
                          "algorithmic_bytes_per_launch": step_bytes,
                          "launch_ms": per_launch_ms,
                          "peak_kind": f"{hbm_kind} (MEASURED_PEAKS.json hbm_gbs)",
-                         "note": "rows held in registers for 16 steps: 8.9 B/point-step against "
-                                 "120 for one step per launch (roofline_step_onestep); the kernel "
-                                 "is bound by shared-memory wavefronts and the per-step barrier, "
-                                 "see roofline_step_fp64 and profiles/r1h_c5step_shapes.md"},
+                         "note": step_note},
             "roofline_harvest": {"bound": "fp64",
                          "kernel": "harvest_mvc_kernel<13,2,0> (per-node expm-multiply, one item per lane, "
                                    "derivative tables as constant-bank DFMA operands)",

@@ -255,6 +255,14 @@ int lmep_set_harvest_method(int method);
  * Per-device setting (the current device); results are bit-identical either way. */
 int lmep_set_ring_cluster(int on);
 
+/* Kernel of the persistent TMA-pipelined per-node linear steps (BASELINE
+ * config 5): 1 = register-resident values with a slot-major halo exchange
+ * (lin_pernode_tmx_kernel; centred n <= 13 and n = 7 one-sided), 0 = the
+ * shared-memory window kernel (lin_pernode_tma_kernel), 2 (default) = the
+ * register kernel for fused multiply-adds, the window kernel for the exact
+ * order.  Per-device setting; results are bit-identical in the exact mode. */
+int lmep_set_pernode_kernel(int variant);
+
 /* ---- stepping (K3, K4, K5) ---------------------------------------------- */
 
 /* Linear banded propagation u <- W u for `steps` steps (kernels.py:33-43,

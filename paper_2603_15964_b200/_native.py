@@ -43,6 +43,7 @@ EXPORTS = (
     "lmep_harvest", "lmep_step_linear", "lmep_step_etdrk4", "lmep_step_etd2",
     "lmep_banded_matvec", "lmep_plan", "lmep_rows_to_soa", "lmep_launch_count",
     "lmep_set_harvest_method", "lmep_set_ring_cluster", "lmep_step_etds", "lmep_harvest_mapped", "lmep_harvest_chunk",
+    "lmep_set_pernode_kernel",
 )
 
 
@@ -126,6 +127,7 @@ def load(path: str | None = None):
     L.lmep_rows_to_soa.argtypes = [vp, i64, C.c_int, vp, vp]
     L.lmep_set_harvest_method.argtypes = [C.c_int]
     L.lmep_set_ring_cluster.argtypes = [C.c_int]
+    L.lmep_set_pernode_kernel.argtypes = [C.c_int]
     for name in EXPORTS:
         if name not in ("lmep_version", "lmep_status_string", "lmep_last_error",
                         "lmep_launch_count"):
@@ -180,6 +182,14 @@ def set_harvest_method(method: str) -> None:
     code = {"multiply": 0, "auto": 0, "pade": 1, "mv8": 4, "mvitem": 5, "mvb8": 6, "mvb2": 7,
             "mvb4": 8, "mvb": 9}[method]
     check(lib().lmep_set_harvest_method(code), "lmep_set_harvest_method")
+
+
+def set_pernode_kernel(variant: str) -> None:
+    """Persistent per-node linear step kernel: "auto" (default: registers for
+    fused multiply-adds, window for the exact order), "registers" (values in
+    registers, slot-major halo exchange) or "window" (shared-memory windows)."""
+    check(lib().lmep_set_pernode_kernel({"registers": 1, "window": 0, "auto": 2}[variant]),
+          "lmep_set_pernode_kernel")
 
 
 def set_ring_cluster(on: bool) -> None:

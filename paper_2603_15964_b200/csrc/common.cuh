@@ -44,6 +44,7 @@ struct DeviceSettings {
     std::atomic<int> mv_lanes{0};         // block / per-item lanes override (0 = heuristic)
     std::atomic<int> mvc{1};              // constant-table kernel when eligible
     std::atomic<int> ring_cluster{1};     // linear ring mode on a thread-block cluster
+    std::atomic<int> pernode_kernel{2};   // TMA per-node steps: 1 registers, 0 window, 2 auto
 };
 DeviceSettings &device_settings();
 

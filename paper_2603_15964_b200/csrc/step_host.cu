@@ -51,7 +51,11 @@ int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded
         // even N -> the persistent TMA-pipelined kernel (lin_pernode_tma_kernel),
         // else lin_pernode_tb_kernel; sharded: the caller fuses `steps` steps
         // per halo exchange
-        k = sharded ? steps : (t.ksteps > 0 ? t.ksteps : std::min<int64_t>(16, steps));
+        // steps per launch: the rows cross HBM once per launch; past ~25 steps the
+        // halo recompute (k (n-1) of the 1536-node span) outweighs it (C5 sweep
+        // tools/c5_ksweep2.py: k = 16 11.1, 25 10.2, 40 10.6 us/step)
+        const int64_t kdef = (!sharded && (g.N % 2) == 0 && g.N >= tb_nodes_per_cta(n, true)) ? 25 : 16;
+        k = sharded ? steps : (t.ksteps > 0 ? t.ksteps : std::min<int64_t>(kdef, steps));
         const bool tma = tma_ok && !sharded && (g.N % 2) == 0 && g.N >= tb_nodes_per_cta(n, true);
         const int64_t span = tb_nodes_per_cta(n, tma);
         while (k > 1 && span - k * (n - 1) < span / 2) --k;

@@ -199,6 +199,169 @@ __global__ void __launch_bounds__(NT, 1) lin_pernode_tma_kernel(const __grid_con
     if (bad) *p.flag = 1;
 }
 
+// ---------------------------------------------------------------------------
+// Register-resident variant (lin_pernode_tmx_kernel): the same tiles, TMA
+// pipeline, launch plan and arithmetic, but each thread keeps its J = 6
+// consecutive staged nodes' VALUES in registers across the k steps, not just
+// their rows.  Per step a thread publishes its J values into a structure-of-
+// arrays exchange buffer Q[slot j][thread] and reads back only the halo it
+// needs -- the last EL values of thread t-1 and the first ER values of thread
+// t+1 (EL, ER <= J) -- so the window of J + n - 1 values costs n - 1 shared
+// loads and J stores per thread instead of J + n - 1 loads and J stores: for
+// n = 13 (J = 6, 256 threads) 24 B of shared-memory traffic per output instead
+// of 40 (the J = 3 kernel above was bound by those wavefronts, ncu
+// profiles/r1s_c5_lin_pernode_tma_kernel.md).  Slot-major Q makes every load /
+// store of a warp hit consecutive 8-byte words (conflict-free); Q is double
+// buffered, so one barrier per step suffices.  Rows and the initial values
+// are read from the TMA-staged natural layout with 16-byte loads (conflict-
+// free at a 48-byte lane stride).  The accumulation order is the same
+// ascending chain as every other per-node kernel (bit-identical in EX).
+// ---------------------------------------------------------------------------
+template <int NS, int EL, int J, int NT, bool EX>
+__global__ void __launch_bounds__(NT, 1) lin_pernode_tmx_kernel(const __grid_constant__ StepParams p)
+{
+    constexpr int ER = NS - 1 - EL;
+    static_assert(EL <= J && ER <= J && J % 2 == 0, "halo must come from the adjacent threads");
+    constexpr int SPAN = J * NT;
+    constexpr int RS = SPAN + 4;                 // row slice stride (even: 16-byte aligned)
+    constexpr int UL = tma_ulen(NS, SPAN);
+    constexpr int QS = NT + 2;                   // exchange slot stride (thread t at 1 + t)
+    constexpr int W = EL + J + ER;               // window
+    extern __shared__ __align__(16) double sm[];
+    double *R = sm;                              // [NS][RS]
+    double *Ub = sm + NS * RS;                   // [UL] landed initial values
+    double *Q = Ub + UL;                         // [2][J][QS]
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x;
+    const int K = p.ksteps;
+    const int eL = EL, eR = ER;
+    const int64_t ntiles = (p.nloc + p.tile - 1) / p.tile;
+
+    for (int i = tid; i < NS * RS + UL + 2 * J * QS; i += NT) sm[i] = 0.0;
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    auto issue = [&](int64_t tile) {
+        const TileRange r = tile_range(p, tile, K, eL, eR);
+        const int org = eL + ((eL - r.o) & 1);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        const uint32_t bytes = (uint32_t)r.cnt * 8u * (NS + 1);
+        mbar_expect_tx(&bar, bytes);
+#pragma unroll 1
+        for (int c = 0; c < NS; ++c)
+            copy_wrapped(R + c * RS, p.wp + (int64_t)c * p.wld, p.N, r.start, r.cnt, &bar);
+        copy_wrapped(Ub + org - r.o, p.u_in, p.N, r.start, r.cnt, &bar);
+    };
+
+    int64_t tile = blockIdx.x;
+    if (tid == 0 && tile < ntiles) issue(tile);
+    bool bad = false;
+    for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+        const TileRange r = tile_range(p, tile, K, eL, eR);
+        const int org = eL + ((eL - r.o) & 1);
+        mbar_wait(&bar, (uint32_t)(it & 1));
+        // rows and initial values of this thread's J staged nodes -> registers
+        // (nodes past the staged range keep finite placeholders; their results
+        // only reach nodes that are never stored)
+        double w[J][NS], x[J];
+        const int l0 = J * tid;
+        if (r.o == 0 && l0 + J <= r.len) {
+#pragma unroll
+            for (int c = 0; c < NS; ++c) {
+#pragma unroll
+                for (int j = 0; j < J; j += 2) {
+                    const double2 v = *reinterpret_cast<const double2 *>(R + c * RS + l0 + j);
+                    w[j][c] = v.x;
+                    w[j + 1][c] = v.y;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                const int ls = r.o + (l0 + j < r.len ? l0 + j : K * eL);
+#pragma unroll
+                for (int c = 0; c < NS; ++c) w[j][c] = R[c * RS + ls];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < J; ++j) x[j] = Ub[org + (l0 + j < r.len ? l0 + j : K * eL)];
+        __syncthreads();                         // R and Ub free for the next tile's copies
+        const int64_t nxt = tile + gridDim.x;
+        if (tid == 0 && nxt < ntiles) issue(nxt);
+
+        for (int s = 0; s < K; ++s) {
+            double *Qb = Q + (s & 1) * (J * QS);
+#pragma unroll
+            for (int j = 0; j < J; ++j) Qb[j * QS + 1 + tid] = x[j];
+            __syncthreads();
+            double win[W];
+#pragma unroll
+            for (int m = 0; m < EL; ++m) win[m] = Qb[(J - EL + m) * QS + tid];          // t-1
+#pragma unroll
+            for (int j = 0; j < J; ++j) win[EL + j] = x[j];
+#pragma unroll
+            for (int m = 0; m < ER; ++m) win[EL + J + m] = Qb[m * QS + 2 + tid];        // t+1
+            // the J chains interleaved tap by tap: J independent FMAs per tap
+            // hide the FP64 latency.  EX keeps each node's ascending chain (the
+            // reference order); the fused mode splits it into two half chains
+            // (taps [0, H) and [H, n)) joined by one add: 2J independent chains
+            double acc[J], acc2[J];
+            constexpr int H = EX ? NS : (NS + 1) / 2;
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                acc[j] = EX ? xmul(w[j][0], win[j]) : w[j][0] * win[j];
+                if constexpr (!EX) acc2[j] = w[j][H] * win[j + H];
+            }
+#pragma unroll
+            for (int c = 1; c < H; ++c) {
+#pragma unroll
+                for (int j = 0; j < J; ++j) {
+                    if constexpr (EX) acc[j] = xadd(acc[j], xmul(w[j][c], win[j + c]));
+                    else {
+                        acc[j] = fma(w[j][c], win[j + c], acc[j]);
+                        if (H + c < NS) acc2[j] = fma(w[j][H + c], win[j + H + c], acc2[j]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < J; ++j) x[j] = EX ? acc[j] : acc[j] + acc2[j];
+        }
+        // outputs: staged nodes [K eL, K eL + (t1 - t0)) -> u_out[t0 ...]
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int64_t i = r.t0 + (int64_t)(l0 + j - K * eL);
+            if (i >= r.t0 && i < r.t1) {
+                p.u_out[i] = x[j];
+                bad |= !isfinite(x[j]);
+            }
+        }
+    }
+    if (bad) *p.flag = 1;
+}
+
+// (n, row) pairs with both halo widths <= 6 that the register-resident kernel
+// is instantiated for: the centred stencils and the n = 7 one-sided ones
+template <bool EX>
+static int launch_tmx(const StepParams &p, unsigned grid, cudaStream_t st)
+{
+    constexpr int J = 6, NT = 256;
+    const size_t shm = (size_t)(p.n * (J * NT + 4) + tma_ulen(p.n, J * NT) + 2 * J * (NT + 2)) * 8;
+    void (*k)(StepParams) = nullptr;
+    if (p.n == 13 && p.row == 6) k = lin_pernode_tmx_kernel<13, 6, J, NT, EX>;
+    else if (p.n == 11 && p.row == 5) k = lin_pernode_tmx_kernel<11, 5, J, NT, EX>;
+    else if (p.n == 9 && p.row == 4) k = lin_pernode_tmx_kernel<9, 4, J, NT, EX>;
+    else if (p.n == 7 && p.row == 3) k = lin_pernode_tmx_kernel<7, 3, J, NT, EX>;
+    else if (p.n == 7 && p.row == 6) k = lin_pernode_tmx_kernel<7, 6, J, NT, EX>;
+    else if (p.n == 7 && p.row == 0) k = lin_pernode_tmx_kernel<7, 0, J, NT, EX>;
+    if (!k) return -1;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+    k<<<grid, NT, shm, st>>>(p);
+    return launch_status("lin_pernode_tmx_kernel");
+}
+
 size_t tma_smem_bytes(int n, int span) { return (size_t)(n * (span + 4) + 3 * tma_ulen(n, span)) * 8; }
 
 int launch_lin_pernode_tma(const StepParams &p, bool exact, cudaStream_t st)
@@ -210,6 +373,15 @@ int launch_lin_pernode_tma(const StepParams &p, bool exact, cudaStream_t st)
     const unsigned grid = (unsigned)(ntiles < nsm ? ntiles : nsm);
     if ((p.N & 1) || (p.wld & 1) || ((uintptr_t)p.wp & 15) || ((uintptr_t)p.u_in & 15))
         return LMEP_INVALID_CONFIG;
+    // auto: the register-resident kernel for the fused mode (C5 200 steps,
+    // 25 per launch: 10.2 vs 10.6 us/step), the window kernel for the exact
+    // order (11.7 vs 12.3: two roundings per tap double its FP64 work and the
+    // window kernel's 16 warps hide that latency better)
+    const int pk = device_settings().pernode_kernel.load();
+    if (pk == 1 || (pk == 2 && !exact)) {
+        const int rc = exact ? launch_tmx<true>(p, grid, st) : launch_tmx<false>(p, grid, st);
+        if (rc >= 0) return rc;                  // else: (n, row) not instantiated
+    }
 #define LMEP_TMA_CASE(NS_)                                                                        \
     case NS_:                                                                                     \
         if (exact) {                                                                              \
@@ -234,3 +406,10 @@ int launch_lin_pernode_tma(const StepParams &p, bool exact, cudaStream_t st)
 }
 
 }  // namespace lmep
+
+extern "C" int lmep_set_pernode_kernel(int variant)
+{
+    if (variant < 0 || variant > 2) return LMEP_INVALID_CONFIG;
+    lmep::device_settings().pernode_kernel.store(variant);
+    return LMEP_OK;
+}

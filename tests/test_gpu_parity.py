@@ -796,19 +796,27 @@ def test_c5_run_linear_per_node(lx, golden, orc):
     assert np.array_equal(u, golden["c5_u"])
 
 
-@pytest.mark.parametrize("N", [5000, 4999, 1536])
-@pytest.mark.parametrize("n,row", [(13, 6), (11, 5), (7, 3), (7, 6)])
-def test_per_node_steps_bitwise(lx, orc, N, n, row):
-    """Per-node rows on a periodic grid: the persistent TMA kernel (even N >=
-    its 1536-node span; staged-range parities both ways, periodic wrap of the
-    bulk copies, a partial last tile, k = 16 then 5 steps) and the register
-    tb kernel (odd N) are bit-identical to the oracle's run_linear."""
+@pytest.mark.parametrize("kernel", ["registers", "window"])
+@pytest.mark.parametrize("N", [5000, 4999, 1536, 3074])
+@pytest.mark.parametrize("n,row", [(13, 6), (11, 5), (9, 4), (7, 3), (7, 6), (7, 0), (9, 8)])
+def test_per_node_steps_bitwise(lx, orc, N, n, row, kernel):
+    """Per-node rows on a periodic grid: the persistent TMA kernels (even N >=
+    their 1536-node span; staged-range parities both ways, periodic wrap of the
+    bulk copies, a partial last tile, k = 16 then 5 steps; register-resident
+    values with a slot-major halo exchange, or shared-memory windows) and the
+    register tb kernel (odd N) are bit-identical to the oracle's run_linear."""
     rng = np.random.default_rng(N + 7 * n + row)
     W = rng.standard_normal((N, n)) / n
     u0 = rng.standard_normal(N)
     m = orc.members_for(N, n, row, True)
-    u = lx.kernels.run_linear(W, m, u0, 21)
+    lx._native.set_pernode_kernel(kernel)
+    try:
+        u = lx.kernels.run_linear(W, m, u0, 21)
+        u1 = lx.kernels.run_linear(W, m, u0, 1)
+    finally:
+        lx._native.set_pernode_kernel("auto")
     assert np.array_equal(u, orc.run_linear(W, m, u0, 21))
+    assert np.array_equal(u1, orc.run_linear(W, m, u0, 1))
 
 
 @pytest.mark.parametrize("N", [5000, 4999])
