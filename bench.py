@@ -161,12 +161,54 @@ def traffic(kernel, key, units):
         return None
 
 
-def fp64_peak():
+def _peaklib():
     so = os.path.join(REPO, "tools", "libfp64peak.so")
     lib = ctypes.CDLL(so)
     lib.fp64_peak_tflops.restype = ctypes.c_double
     lib.fp64_peak_tflops.argtypes = [ctypes.c_int]
-    return float(lib.fp64_peak_tflops(10))
+    lib.fp64_latency_clk.restype = ctypes.c_double
+    lib.barrier_trip_clk.restype = ctypes.c_double
+    lib.barrier_trip_clk.argtypes = [ctypes.c_int]
+    return lib
+
+
+def fp64_peak():
+    return float(_peaklib().fp64_peak_tflops(10))
+
+
+def latency_constants():
+    """Measured on this GPU: clocks per dependent FP64 op, and per shared-memory
+    store + __syncthreads + neighbour load with 8 warps per CTA."""
+    lib = _peaklib()
+    return {"fp64_dep_clk": float(lib.fp64_latency_clk()),
+            "bar_trip_clk_8w": float(lib.barrier_trip_clk(8))}
+
+
+# SURVEY 8(d): algorithmic flops per point-step of the FP64-bound configs
+FLOPS_PER_POINT_STEP = {"c3": 299, "c4": 143}
+
+
+def config_roofline(name, w, us_per_step, fp64, hbm, lat, sm_mhz):
+    """The roofline of one config's step kernel.  C3 / C4: FP64 on
+    the algorithmic flops; C1 / C2: a latency floor built from measured
+    constants -- per dependent pass of a step, one n-tap dependent chain plus
+    one store/barrier/load round trip (C1: one pass per step in the cluster
+    ring kernel; C2 ETD2 convective: two passes, N(u) then the three-product
+    update) -- against the measured time per step."""
+    if name in FLOPS_PER_POINT_STEP:
+        tf = FLOPS_PER_POINT_STEP[name] * w.N / (us_per_step * 1e-6) / 1e12
+        gbs = 16 * w.N / (us_per_step * 1e-6) / 1e9
+        return {"bound": "fp64", "achieved": tf, "peak": fp64, "unit": "TFLOP/s", "frac": tf / fp64,
+                "algorithmic_flops_per_point_step": FLOPS_PER_POINT_STEP[name],
+                "peak_kind": "measured DFMA chains (tools/fp64_peak.cu), this run",
+                "hbm_view": {"achieved_gbs": gbs, "frac": gbs / hbm, "bytes_per_point_step": 16}}
+    passes = 1 if name == "c1" else 2
+    clk = passes * (w.n * lat["fp64_dep_clk"] + lat["bar_trip_clk_8w"])
+    floor_us = clk / sm_mhz
+    return {"bound": "latency", "achieved": us_per_step, "peak": floor_us, "unit": "us/step",
+            "frac": floor_us / us_per_step, "floor_clk_per_step": clk, "passes_per_step": passes,
+            "constants": lat, "sm_mhz": sm_mhz,
+            "note": "frac = latency floor / measured time per step (lower is further from the floor)"}
 
 
 # ------------------------------------------------------------------ workloads
@@ -373,8 +415,9 @@ def time_c4_sharded(rank, world):
             "updates_per_s": w.N * w.steps / (ms * 1e-3), "ksteps_per_exchange": s.plan.ksteps}
 
 
-def time_other_configs():
-    """Configs 1-4: median of three timed runs after one warm-up (reported, not the headline)."""
+def time_other_configs(fp64=None, hbm=None, lat=None, sm_mhz=None):
+    """Configs 1-4: median of three timed runs after one warm-up (reported, not the
+    headline), each with the roofline of its step kernel (config_roofline)."""
     import torch
     import paper_2603_15964_b200 as lx
     from paper_2603_15964_b200 import configs
@@ -417,6 +460,11 @@ def time_other_configs():
                 "us_per_step": sp * 1e3 / w.steps, "harvest_ms": hv, "finite": fin}
         out[name] = {"N": w.N, "n": w.n, "scheme": w.scheme, "steps": w.steps,
                      "dt": w.delta_t, **res}
+        if fp64 is not None:
+            best = min(v["us_per_step"] for v in res.values())
+            mode = min(res, key=lambda m: res[m]["us_per_step"])
+            out[name]["roofline"] = {"mode": mode, **config_roofline(name, w, best, fp64, hbm, lat,
+                                                                      sm_mhz)}
     return out
 
 
@@ -675,7 +723,8 @@ def main():
     others = {}
     if not args.no_others:
         if world == 1:
-            others = time_other_configs()
+            sm_mhz = clk.summary().get("sm_mhz") or 1965.0
+            others = time_other_configs(fp64, hbm, latency_constants(), float(sm_mhz))
         others["c4_sharded"] = time_c4_sharded(rank, world)
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
