@@ -225,6 +225,63 @@ int lmep_harvest_chunk(int n, int s, int nterms, const double *tables, const int
                        int32_t *status, int32_t *ms, const lmep_coef_map *map, int64_t out_ld,
                        void *stream);
 
+/* All harvest options in one argument block (lmep_harvest_chunk's arguments
+ * plus two):
+ *   half_out   (nullable, s >= 2) also the (w_lin, raw dt/2 phi_1) rows of
+ *              every item at delta_t / 2 -- the ETDRK4 half-step set
+ *              (timestep.py:294-299) -- in the layout of w_out with s = 2
+ *              (layout 1: leading dimension out_ld).  The per-item kernel takes
+ *              them from the same exponential (an even number of scaling reps,
+ *              the iterate after half of them); kernels that emit one set are
+ *              followed by a second launch at delta_t / 2.
+ *   status_any (nullable, device int32, needs `status`) set to 1 when any
+ *              item's status is not LMEP_OK (never cleared: the caller zeroes
+ *              it and may share it between harvests). */
+typedef struct lmep_harvest_args {
+    int32_t n, s, nterms, layout;
+    const double *tables;
+    const int32_t *table_idx;
+    const double *coef;
+    int64_t coef_stride;
+    const double *c0;
+    int64_t c0_stride;
+    const double *L;
+    double delta_t;
+    const int32_t *target_row;
+    int64_t row_default;
+    const uint64_t *frozen;
+    uint64_t frozen_default;
+    int64_t B;
+    int64_t out_ld;
+    double *w_out;
+    int32_t *status;
+    int32_t *ms;
+    const lmep_coef_map *map;
+    double *half_out;
+    int32_t *status_any;
+} lmep_harvest_args;
+
+int lmep_harvest_ex(const lmep_harvest_args *args, void *stream);
+
+/* Set *flag (device int32) to 1 if any of status[0..B) is not LMEP_OK. */
+int lmep_status_any(const int32_t *status, int64_t B, int32_t *flag, void *stream);
+
+/* Ordered linear combination of row arrays, harvest.combine (harvest.py:225-235):
+ *   out[r*ld_out + j] = (((0 + c[0]*in[0][r*ld_in[0] + j]) + c[1]*in[1][...]) + ...)
+ * for r < rows, j < cols, numpy's two roundings per term in list order.  `in`,
+ * `ld_in` and `coef` are HOST arrays of nterm <= 8 entries; the data is device
+ * memory.  timestep.etdrk4_operators (timestep.py:141-156) composes alpha,
+ * beta and gamma with it straight from the harvest output. */
+int lmep_combine(int nterm, const double *const *in, const int64_t *ld_in, const double *coef,
+                 int64_t rows, int64_t cols, double *out, int64_t ld_out, void *stream);
+
+/* Compare every row of a device (N, n) weight array with row `ref`:
+ * out3 (device uint64[3]) = {first equal row, last equal row, count}.  The
+ * shim's compression of reference-style weights into shared / class /
+ * per-node rows reads these three numbers instead of the whole array. */
+int lmep_rows_classify(const double *rows, int64_t N, int n, int64_t ref, uint64_t *out3,
+                       void *stream);
+
 /* Harvest algorithm for d <= 16:
  *   0 (default) = expm-multiply: large single-geometry batches (n in
  *     {7, 9, 11, 13}, B >= 4096; s = 1 with <= 2 tables, or s <= 4 with two

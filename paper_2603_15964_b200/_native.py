@@ -43,7 +43,8 @@ EXPORTS = (
     "lmep_harvest", "lmep_step_linear", "lmep_step_etdrk4", "lmep_step_etd2",
     "lmep_banded_matvec", "lmep_plan", "lmep_rows_to_soa", "lmep_launch_count",
     "lmep_set_harvest_method", "lmep_set_ring_cluster", "lmep_step_etds", "lmep_harvest_mapped", "lmep_harvest_chunk",
-    "lmep_set_pernode_kernel",
+    "lmep_set_pernode_kernel", "lmep_harvest_ex", "lmep_status_any", "lmep_combine",
+    "lmep_rows_classify",
 )
 
 
@@ -71,6 +72,17 @@ class LmepHalo(C.Structure):
 class LmepCoefMap(C.Structure):
     _fields_ = [("node0", C.c_int64), ("nnodes", C.c_int64), ("periodic", C.c_int32),
                 ("reserved", C.c_int32)]
+
+
+class LmepHarvestArgs(C.Structure):
+    _fields_ = [("n", C.c_int32), ("s", C.c_int32), ("nterms", C.c_int32), ("layout", C.c_int32),
+                ("tables", C.c_void_p), ("table_idx", C.c_void_p), ("coef", C.c_void_p),
+                ("coef_stride", C.c_int64), ("c0", C.c_void_p), ("c0_stride", C.c_int64),
+                ("L", C.c_void_p), ("delta_t", C.c_double), ("target_row", C.c_void_p),
+                ("row_default", C.c_int64), ("frozen", C.c_void_p), ("frozen_default", C.c_uint64),
+                ("B", C.c_int64), ("out_ld", C.c_int64), ("w_out", C.c_void_p),
+                ("status", C.c_void_p), ("ms", C.c_void_p), ("map", C.c_void_p),
+                ("half_out", C.c_void_p), ("status_any", C.c_void_p)]
 
 
 class LmepTuning(C.Structure):
@@ -128,6 +140,11 @@ def load(path: str | None = None):
     L.lmep_set_harvest_method.argtypes = [C.c_int]
     L.lmep_set_ring_cluster.argtypes = [C.c_int]
     L.lmep_set_pernode_kernel.argtypes = [C.c_int]
+    L.lmep_harvest_ex.argtypes = [C.POINTER(LmepHarvestArgs), vp]
+    L.lmep_status_any.argtypes = [vp, i64, vp, vp]
+    L.lmep_combine.argtypes = [C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64),
+                               C.POINTER(C.c_double), i64, i64, vp, i64, vp]
+    L.lmep_rows_classify.argtypes = [vp, i64, C.c_int, i64, vp, vp]
     for name in EXPORTS:
         if name not in ("lmep_version", "lmep_status_string", "lmep_last_error",
                         "lmep_launch_count"):

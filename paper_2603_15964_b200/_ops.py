@@ -187,52 +187,69 @@ class HarvestOut:
     rows: torch.Tensor           # layout 0: [B, s, n]; layout 1: [s, n, B]
     ms: torch.Tensor             # [B] int32: pade degree | squarings << 8
     status: torch.Tensor         # [B] int32
+    flag: torch.Tensor | None = None   # [1] int32, set by the library if any status failed
+    half: torch.Tensor | None = None   # (w_lin, dt/2 phi_1) at delta_t / 2: [B, 2, n] / [2, n, B]
 
 
 def harvest(n: int, s: int, delta_t: float, B: int, *, tables=None, table_idx=None, coef=None,
             coef_stride=0, c0=None, c0_stride=0, L=None, rows=None, row_default=0,
             frozen=None, frozen_default=0, layout=0, coef_map=None,
-            into: HarvestOut | None = None, item0: int = 0) -> HarvestOut:
-    """coef_map = (node0, nnodes, periodic): row-scaled coefficients
-    (lmep_harvest_mapped); coef / c0 then index the whole grid.
-    into / item0 (layout 1): write items [item0, item0 + B) of a larger
-    HarvestOut (lmep_harvest_chunk); coef / c0 / rows / frozen are then the
-    slice's own (already offset) arrays."""
+            into: HarvestOut | None = None, item0: int = 0, half: bool = False) -> HarvestOut:
+    """One lmep_harvest_ex call.  coef_map = (node0, nnodes, periodic): row-scaled
+    coefficients; coef / c0 then index the whole grid.  into / item0 (layout 1):
+    write items [item0, item0 + B) of a larger HarvestOut; coef / c0 / rows /
+    frozen are then the slice's own (already offset) arrays.  half: also the
+    half-step set (s >= 2).  The per-item status is reduced on the device into
+    HarvestOut.flag (no host synchronisation)."""
     d = nat.device()
     if into is None:
         out = torch.empty((B, s, n) if layout == 0 else (s, n, B), dtype=F64, device=d)
         ms = torch.empty(B, dtype=torch.int32, device=d)
         status = torch.empty(B, dtype=torch.int32, device=d)
-        res, ld, optr = HarvestOut(out, ms, status), B, nat.ptr(out)
+        flag = torch.zeros(1, dtype=torch.int32, device=d)
+        hv = None
+        if half:
+            hv = torch.empty((B, 2, n) if layout == 0 else (2, n, B), dtype=F64, device=d)
+        res, ld, optr = HarvestOut(out, ms, status, flag, hv), B, nat.ptr(out)
+        hptr = nat.ptr(hv)
     else:
         if layout != 1:
             raise InvalidConfig("chunked harvests write the SoA layout")
         res, ld = into, int(into.rows.shape[2])
         optr = into.rows.data_ptr() + 8 * int(item0)
         ms, status = into.ms[item0:item0 + B], into.status[item0:item0 + B]
-    nterms = 0 if tables is None else int(tables.shape[1])
-    args = (n, s, nterms, nat.ptr(tables), nat.ptr(table_idx), nat.ptr(coef), int(coef_stride),
-            nat.ptr(c0), int(c0_stride), nat.ptr(L), float(delta_t), nat.ptr(rows),
-            int(row_default), nat.ptr(frozen), C.c_uint64(int(frozen_default)), B, layout,
-            optr, nat.ptr(status), nat.ptr(ms))
-    if into is not None:
-        m = None if coef_map is None else \
-            C.byref(nat.LmepCoefMap(int(coef_map[0]), int(coef_map[1]), int(bool(coef_map[2])), 0))
-        st = nat.lib().lmep_harvest_chunk(*args, m, ld, nat.stream_handle())
-    elif coef_map is None:
-        st = nat.lib().lmep_harvest(*args, nat.stream_handle())
-    else:
+        if into.flag is None:
+            into.flag = torch.zeros(1, dtype=torch.int32, device=d)
+        flag = into.flag
+        hptr = None
+        if half:
+            if into.half is None:
+                raise InvalidConfig("the target HarvestOut holds no half-step rows")
+            hptr = into.half.data_ptr() + 8 * int(item0)
+    a = nat.LmepHarvestArgs()
+    a.n, a.s, a.layout = int(n), int(s), int(layout)
+    a.nterms = 0 if tables is None else int(tables.shape[1])
+    a.tables, a.table_idx, a.coef = nat.ptr(tables), nat.ptr(table_idx), nat.ptr(coef)
+    a.coef_stride, a.c0, a.c0_stride = int(coef_stride), nat.ptr(c0), int(c0_stride)
+    a.L, a.delta_t = nat.ptr(L), float(delta_t)
+    a.target_row, a.row_default = nat.ptr(rows), int(row_default)
+    a.frozen, a.frozen_default = nat.ptr(frozen), int(frozen_default)
+    a.B, a.out_ld, a.w_out = int(B), int(ld), optr
+    a.status, a.ms, a.half_out, a.status_any = nat.ptr(status), nat.ptr(ms), hptr, nat.ptr(flag)
+    m = None
+    if coef_map is not None:
         m = nat.LmepCoefMap(int(coef_map[0]), int(coef_map[1]), int(bool(coef_map[2])), 0)
-        st = nat.lib().lmep_harvest_mapped(*args, C.byref(m), nat.stream_handle())
+        a.map = C.addressof(m)
+    st = nat.lib().lmep_harvest_ex(C.byref(a), nat.stream_handle())
     nat.check(st, "lmep_harvest")
     return res
 
 
 @contextmanager
 def deferred_status_checks():
-    """Within the block (this host thread), harvests queue their per-item
-    status instead of synchronising on it; the caller runs check_deferred(list)
-    at its own sync point (a pipeline that enqueues harvest + steps back to back)."""
+    """Within the block (this host thread), harvests queue their status flag
+    instead of synchronising on it; the caller runs check_deferred(list) at its
+    own sync point (a pipeline that enqueues harvest + steps back to back)."""
     prev = getattr(_TLS, "pending", None)
     _TLS.pending = []
     try:
@@ -242,18 +259,20 @@ def deferred_status_checks():
 
 
 def check_deferred(pending: list) -> None:
-    for status, what in pending:
-        if status.numel() and int(status.abs().max().item()) != 0:
+    for flag, what in pending:
+        if int(flag.item()) != 0:
+            pending.clear()
             nat.check(nat.LMEP_NONFINITE, what)
     pending.clear()
 
 
 def raise_on_status(h: HarvestOut, what="matrix exponential overflowed") -> None:
+    """NonFinite if any item failed: reads the library's device flag (4 bytes)."""
     pending = getattr(_TLS, "pending", None)
     if pending is not None:
-        pending.append((h.status, what))
+        pending.append((h.flag, what))
         return
-    if int(h.status.abs().max().item() if h.status.numel() else 0) != 0:
+    if h.flag is not None and int(h.flag.item()) != 0:
         nat.check(nat.LMEP_NONFINITE, what)
 
 
@@ -385,24 +404,39 @@ def stack_rows(parts: list[CompactRows]) -> CompactRows:
 
 
 def compress(dense: torch.Tensor, layout: StencilSet, max_classes: int = 64) -> CompactRows:
-    """(N, n) per-node rows -> the most compact exact representation."""
+    """(N, n) per-node rows -> the most compact exact representation.  The rows
+    equal to the middle one are located by the library (lmep_rows_classify:
+    first / last equal row and their count, 24 bytes back to the host)."""
     N = layout.N
     w = dense.to(dtype=F64).contiguous()
+    out3 = torch.empty(3, dtype=torch.int64, device=w.device)
+    st = nat.lib().lmep_rows_classify(w.data_ptr(), N, layout.n, N // 2, out3.data_ptr(),
+                                      nat.stream_handle())
+    nat.check(st, "lmep_rows_classify")
+    first, last, count = (int(x) for x in out3.tolist())
     mid = w[N // 2]
-    eq = (w == mid).all(dim=1)
-    eqh = to_host(eq)
-    if eqh.all():
-        mode = nat.W_SHARED if layout.periodic else nat.W_CLASS
-        if mode == nat.W_SHARED:
-            return CompactRows(layout, nat.W_SHARED, mid[None].clone())
+    if count == N and layout.periodic:
+        return CompactRows(layout, nat.W_SHARED, mid[None].clone())
     if not layout.periodic:
-        idx = np.flatnonzero(eqh)
-        nl = int(idx[0])
-        nr = int(N - 1 - idx[-1])
-        if eqh[nl:N - nr].all() and nl + nr <= max_classes and nl + nr < N:
+        nl, nr = first, N - 1 - last
+        if count == last - first + 1 and nl + nr <= max_classes and nl + nr < N:
             cl = torch.cat([w[:nl], mid[None], w[N - nr:]], 0)[:, None, :].contiguous()
             return CompactRows(layout, nat.W_CLASS, mid[None].clone(), cl, nl, nr)
     return CompactRows(layout, nat.W_PERNODE, pernode=w.t().contiguous()[None])
+
+
+def combine_into(out: torch.Tensor, ins: list[torch.Tensor], coeffs, rows: int, cols: int,
+                 ld_out: int, ld_in: list[int]) -> None:
+    """out(r, j) = sum_t coeffs[t] * ins[t](r, j) from zeros in list order
+    (harvest.combine, harvest.py:225-235) on the library's combine kernel; the
+    tensors are strided row arrays (row r at r * ld)."""
+    k = len(ins)
+    ptrs = (C.c_void_p * k)(*[t.data_ptr() for t in ins])
+    lds = (C.c_int64 * k)(*[int(x) for x in ld_in])
+    cs = (C.c_double * k)(*[float(c) for c in coeffs])
+    st = nat.lib().lmep_combine(k, ptrs, lds, cs, int(rows), int(cols), out.data_ptr(), int(ld_out),
+                                nat.stream_handle())
+    nat.check(st, "lmep_combine")
 
 
 def combine_rows(parts: list[CompactRows], coeffs) -> CompactRows:
@@ -410,24 +444,26 @@ def combine_rows(parts: list[CompactRows], coeffs) -> CompactRows:
     (harvest.combine, harvest.py:225-235): two roundings per term like numpy."""
     bank = stack_rows(parts)                      # aligns modes / classes
     R = parts[0].R
-    acc_i = acc_c = acc_p = None
-    for i, c in enumerate(coeffs):
-        sl = slice(i * R, (i + 1) * R)
-        c = float(c)
-        if bank.mode == nat.W_PERNODE:
-            t = bank.pernode[sl] * c
-            acc_p = torch.zeros_like(t) + t if acc_p is None else acc_p + t
-        else:
-            t = bank.interior[sl] * c
-            acc_i = torch.zeros_like(t) + t if acc_i is None else acc_i + t
-            if bank.classes is not None:
-                t2 = bank.classes[:, sl] * c
-                acc_c = torch.zeros_like(t2) + t2 if acc_c is None else acc_c + t2
+    K = len(parts)
     if bank.mode == nat.W_PERNODE:
-        return CompactRows(bank.layout, nat.W_PERNODE, pernode=acc_p.contiguous(),
-                           pernode_pad=bank.pernode_pad)
-    return CompactRows(bank.layout, bank.mode, acc_i.contiguous(),
-                       None if acc_c is None else acc_c.contiguous(), bank.nleft, bank.nright)
+        src = bank.pernode                        # [K*R, n, N]
+        blk = src[0].numel() * R
+        out = torch.empty_like(src[:R])
+        combine_into(out, [src[i * R:(i + 1) * R] for i in range(K)], coeffs, 1, blk, blk,
+                     [blk] * K)
+        return CompactRows(bank.layout, nat.W_PERNODE, pernode=out, pernode_pad=bank.pernode_pad)
+    n = bank.n
+    it = torch.empty((R, n), dtype=F64, device=bank.interior.device)
+    combine_into(it, [bank.interior[i * R:(i + 1) * R] for i in range(K)], coeffs, 1, R * n, R * n,
+                 [R * n] * K)
+    cl = None
+    if bank.classes is not None:
+        Cn = bank.classes.shape[0]
+        cl = torch.empty((Cn, R, n), dtype=F64, device=it.device)
+        ldi = K * R * n
+        combine_into(cl, [bank.classes[:, i * R:(i + 1) * R] for i in range(K)], coeffs, Cn, R * n,
+                     R * n, [ldi] * K)
+    return CompactRows(bank.layout, bank.mode, it, cl, bank.nleft, bank.nright)
 
 
 # ---------------------------------------------------------------------------

@@ -30,6 +30,11 @@ __device__ __forceinline__ double macc(double acc, double w, double v)
 void set_last_error(const char *what, cudaError_t e);
 int launch_status(const char *what);
 
+// Device status reductions (rows.cu): *flag = 1 if any status[i] != LMEP_OK;
+// dst[i] = src[i] where dst[i] == LMEP_OK.
+int launch_status_or(const int32_t *status, int64_t B, int32_t *flag, cudaStream_t st);
+int launch_status_merge(int32_t *dst, const int32_t *src, int64_t B, cudaStream_t st);
+
 // Per-device library state (capi.cu).  One process may drive several GPUs
 // (and several host threads may call in concurrently): nothing device-specific
 // is cached process-wide.

@@ -724,15 +724,27 @@ static int launch_harvest(const HarvestParams &P, cudaStream_t st)
 
 int mv_lanes_override() { return device_settings().mv_lanes.load(); }
 
-static int dispatch_harvest(const HarvestParams &P, cudaStream_t st)
+// *half_done (nullable) reports whether the launched kernel also wrote the
+// half-step set P.half_out (only the per-item expm-multiply kernel does)
+static int dispatch_harvest(const HarvestParams &Pin, cudaStream_t st, bool *half_done = nullptr)
 {
-    if (P.B == 0) return LMEP_OK;
+    if (half_done) *half_done = false;
+    if (Pin.B == 0) {
+        if (half_done) *half_done = true;
+        return LMEP_OK;
+    }
+    HarvestParams P = Pin;
+    P.half_out = nullptr;
     const DeviceSettings &ds = device_settings();
     const int method = ds.harvest_method.load();
     if (P.mode != 0 && method != 1 && P.d >= 2 && P.d <= 16 && (P.mode == 2 || P.nterms <= 4)) {
         if (method == 0 && ds.mv_lanes.load() == 0 && ds.mvc.load() && harvest_mvc_eligible(P))
             return launch_harvest_mvc(P, st);
         if (method == 0 && harvest_mvb_eligible(P)) return launch_harvest_mvb(P, st);
+        if (Pin.half_out && Pin.s >= 2) {
+            P.half_out = Pin.half_out;
+            if (half_done) *half_done = true;
+        }
         return launch_harvest_mv(P, st);
     }
     if (P.d <= 8) return launch_harvest<8, 8>(P, st);
@@ -782,6 +794,13 @@ extern "C" int lmep_expm(const double *A, int d, int64_t B, double *E, int32_t *
     return dispatch_harvest(P, (cudaStream_t)stream);
 }
 
+static int harvest_params(HarvestParams &P, int n, int s, int nterms, const double *tables,
+                          const int32_t *table_idx, const double *coef, int64_t coef_stride,
+                          const double *c0, int64_t c0_stride, const double *L, double delta_t,
+                          const int32_t *target_row, int row_default, const uint64_t *frozen,
+                          uint64_t frozen_default, int64_t B, int layout, double *w_out,
+                          int32_t *status, int32_t *ms, const lmep_coef_map *map, int64_t out_ld);
+
 extern "C" int lmep_harvest_chunk(int n, int s, int nterms, const double *tables,
                                   const int32_t *table_idx, const double *coef,
                                   int64_t coef_stride, const double *c0, int64_t c0_stride,
@@ -791,6 +810,64 @@ extern "C" int lmep_harvest_chunk(int n, int s, int nterms, const double *tables
                                   int32_t *status, int32_t *ms, const lmep_coef_map *map,
                                   int64_t out_ld, void *stream)
 {
+    HarvestParams P{};
+    const int rc = harvest_params(P, n, s, nterms, tables, table_idx, coef, coef_stride, c0,
+                                  c0_stride, L, delta_t, target_row, row_default, frozen,
+                                  frozen_default, B, layout, w_out, status, ms, map, out_ld);
+    if (rc) return rc;
+    return dispatch_harvest(P, (cudaStream_t)stream);
+}
+
+// lmep_harvest_ex: the chunk call plus the half-step set and the device flag
+extern "C" int lmep_harvest_ex(const lmep_harvest_args *a, void *stream)
+{
+    if (!a) return LMEP_INVALID_CONFIG;
+    cudaStream_t st = (cudaStream_t)stream;
+    HarvestParams P{};
+    int rc = harvest_params(P, a->n, a->s, a->nterms, a->tables, a->table_idx, a->coef,
+                            a->coef_stride, a->c0, a->c0_stride, a->L, a->delta_t,
+                            a->target_row, (int)a->row_default, a->frozen, a->frozen_default, a->B,
+                            a->layout, a->w_out, a->status, a->ms, a->map,
+                            a->layout == 1 ? a->out_ld : a->B);
+    if (rc) return rc;
+    if (a->half_out && a->s < 2) return LMEP_INVALID_CONFIG;
+    if (a->status_any && !a->status) return LMEP_INVALID_CONFIG;
+    P.half_out = a->half_out;
+    bool half_done = false;
+    rc = dispatch_harvest(P, st, &half_done);
+    if (rc) return rc;
+    if (a->status_any && (rc = launch_status_or(a->status, a->B, a->status_any, st))) return rc;
+    if (a->half_out && !half_done) {
+        // the selected kernel emits one set: a second launch at delta_t / 2, s = 2
+        HarvestParams H{};
+        int32_t *hs = nullptr;
+        if (a->status) {
+            cudaError_t e = cudaMallocAsync((void **)&hs, sizeof(int32_t) * (a->B > 0 ? a->B : 1), st);
+            if (e != cudaSuccess) { set_last_error("cudaMallocAsync", e); return LMEP_CUDA_ERROR; }
+        }
+        rc = harvest_params(H, a->n, 2, a->nterms, a->tables, a->table_idx, a->coef,
+                            a->coef_stride, a->c0, a->c0_stride, a->L, 0.5 * a->delta_t,
+                            a->target_row, (int)a->row_default, a->frozen, a->frozen_default, a->B,
+                            a->layout, a->half_out, hs, nullptr, a->map,
+                            a->layout == 1 ? a->out_ld : a->B);
+        if (!rc) rc = dispatch_harvest(H, st);
+        if (!rc && hs) {
+            rc = launch_status_merge(a->status, hs, a->B, st);
+            if (!rc && a->status_any) rc = launch_status_or(hs, a->B, a->status_any, st);
+        }
+        if (hs) cudaFreeAsync(hs, st);
+        if (rc) return rc;
+    }
+    return LMEP_OK;
+}
+
+static int harvest_params(HarvestParams &P, int n, int s, int nterms, const double *tables,
+                          const int32_t *table_idx, const double *coef, int64_t coef_stride,
+                          const double *c0, int64_t c0_stride, const double *L, double delta_t,
+                          const int32_t *target_row, int row_default, const uint64_t *frozen,
+                          uint64_t frozen_default, int64_t B, int layout, double *w_out,
+                          int32_t *status, int32_t *ms, const lmep_coef_map *map, int64_t out_ld)
+{
     if (layout == 1 && out_ld < B) return LMEP_DIMENSION;
     if (s < 1 || s > 6) return LMEP_INVALID_CONFIG;                 // harvest.py:85-86
     if (n < 1 || n > LMEP_MAX_N || n + s - 1 > LMEP_MAX_DIM) return LMEP_DIMENSION;
@@ -798,7 +875,7 @@ extern "C" int lmep_harvest_chunk(int n, int s, int nterms, const double *tables
     if (layout != 0 && layout != 1) return LMEP_INVALID_CONFIG;
     if (!L && nterms > 0 && (!tables || !coef)) return LMEP_INVALID_CONFIG;
     if (nterms < 0 || nterms > 8) return LMEP_INVALID_CONFIG;
-    HarvestParams P{};
+    P = HarvestParams{};
     P.mode = L ? 2 : 1;
     P.n = n;
     P.s = s;
@@ -829,7 +906,7 @@ extern "C" int lmep_harvest_chunk(int n, int s, int nterms, const double *tables
         P.map_node0 = map->node0;
         P.map_nnodes = map->nnodes;
     }
-    return dispatch_harvest(P, (cudaStream_t)stream);
+    return LMEP_OK;
 }
 
 extern "C" int lmep_harvest_mapped(int n, int s, int nterms, const double *tables,

@@ -30,6 +30,9 @@ struct HarvestParams {
     // reads coef/c0 of node  map_node0 + b - row_b + i  (mod map_nnodes)
     int map_on, map_periodic;
     int64_t map_node0, map_nnodes;
+    // optional (w_lin, raw dt/2 phi_1) rows at delta_t / 2, same layout as out
+    // with s = 2 (lmep_harvest_ex half_out); only the per-item kernel emits them
+    double *half_out;
 };
 
 __device__ __forceinline__ int64_t coef_node(const HarvestParams &P, int64_t b, int row, int i)

@@ -287,6 +287,11 @@ __global__ void __launch_bounds__(128) harvest_mv_kernel(const HarvestParams P)
     int s = 0;
     if (!(nrm <= 1e9)) status = LMEP_NONFINITE;
     else s = nrm > THETA ? (int)ceil(nrm / THETA) : 1;
+    // half-step set: exp(B) = exp(B / reps)^reps, so after reps / 2 of the reps
+    // the iterate is exp(B / 2) e_c -- the same columns at delta_t / 2 (the
+    // augmentation scales with delta_t: (dt/2)^j phi_j(dt/2 L))
+    const bool want_half = P.half_out != nullptr;
+    if (want_half && status == LMEP_OK) s = s < 2 ? 2 : s + (s & 1);
     if (s > 1) {
         const double sc = 1.0 / (double)s;
 #pragma unroll
@@ -382,6 +387,20 @@ __global__ void __launch_bounds__(128) harvest_mv_kernel(const HarvestParams P)
                 ++rep;
                 kt = 1;
                 wprev = INFINITY;
+                if (want_half && qo < 2 && 2 * rep == reps) {
+                    const int eidx = eg[idx];
+#pragma unroll
+                    for (int m = 0; m < R; ++m) {
+                        const int j = q + LPI * m;
+                        double o = acc[m] * mv_pow2(e[m] - eidx);
+                        bad |= (unsigned)!isfinite(o);
+                        if (qo > 0 && ((fz >> j) & 1ull)) o = 0.0;
+                        if (live && j < n) {
+                            if (P.layout == 0) P.half_out[(b * 2 + qo) * n + j] = o;
+                            else P.half_out[((int64_t)qo * n + j) * P.out_ld + b] = o;
+                        }
+                    }
+                }
                 if (rep >= reps) {
                     // back to A's coordinates: exp(A) e_idx = 2^-e_idx D exp(B) e_idx
                     const int eidx = eg[idx];
@@ -425,13 +444,18 @@ __global__ void __launch_bounds__(128) harvest_mv_kernel(const HarvestParams P)
     if (mv_gor<LPI>(bad)) status = LMEP_NONFINITE;
     if (reps == 0 && live) {
         // failed before the iteration: outputs are NaN, the status says why
+        const double qnan = __longlong_as_double(0x7ff8000000000000LL);
         for (int qq = 0; qq < sd; ++qq)
 #pragma unroll
             for (int m = 0; m < R; ++m) {
                 const int j = q + LPI * m;
                 if (j < n) {
-                    if (P.layout == 0) P.out[(b * sd + qq) * n + j] = __longlong_as_double(0x7ff8000000000000LL);
-                    else P.out[((int64_t)qq * n + j) * P.out_ld + b] = __longlong_as_double(0x7ff8000000000000LL);
+                    if (P.layout == 0) P.out[(b * sd + qq) * n + j] = qnan;
+                    else P.out[((int64_t)qq * n + j) * P.out_ld + b] = qnan;
+                    if (want_half && qq < 2) {
+                        if (P.layout == 0) P.half_out[(b * 2 + qq) * n + j] = qnan;
+                        else P.half_out[((int64_t)qq * n + j) * P.out_ld + b] = qnan;
+                    }
                 }
             }
     }

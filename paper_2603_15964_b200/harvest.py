@@ -309,12 +309,15 @@ def _rows_from(plan: _Plan, sset: StencilSet, out: torch.Tensor) -> _ops.Compact
 def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
                     frozen_nodes=(), stats: dict | None = None,
                     node_range: tuple[int, int] | None = None,
-                    pad: int = 0) -> _ops.CompactRows:
+                    pad: int = 0, half: bool = False):
     """Harvest w_lin and the raw dt^j phi_j rows (R = s) for the whole grid.
     node_range=(off, nloc): per-node rows only for the shard's nodes (the
     shared / class modes are grid-wide by construction); pad > 0 (periodic
     per-node only) also harvests the `pad` halo nodes on each side, so a shard
-    can fuse several steps per halo exchange."""
+    can fuse several steps per halo exchange.  half=True (s >= 2) returns
+    (rows, half_rows): also w_lin and the raw dt/2 phi_1 row at delta_t / 2, the
+    ETDRK4 half-step set (timestep.py:294-299), from the same launch
+    (lmep_harvest_ex half_out) on the shared / class paths."""
     if not 1 <= s <= 6:
         raise ValueError(f"augmentation depth must be in [1, 6], got {s}")
     n = sset.n
@@ -322,6 +325,10 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
         raise DimensionMismatch(f"n + s - 1 must be <= {nat.MAX_DIM}")
     varcoef = isinstance(spec, VariableCoefficientSpec)
     plan = _plan(grid, sset, frozen_nodes, force_pernode=varcoef)
+    if half and (plan.mode == nat.W_PERNODE or s < 2):
+        full = harvest_compact(grid, sset, spec, delta_t, s, frozen_nodes, stats, node_range, pad)
+        return full, harvest_compact(grid, sset, spec, delta_t / 2, 2, frozen_nodes, stats,
+                                     node_range, pad)
     terms = tuple((k, 1.0) for k in spec.orders) if varcoef else spec.terms
     if max(k for k, _ in terms) > n - 1:
         from .errors import OrderTooHigh
@@ -335,10 +342,13 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
                          table_idx=_ops.dev_i32(np.arange(T)), coef=_ops.dev_f64(cf or [0.0]),
                          coef_stride=0, c0=_ops.dev_f64([c0]), c0_stride=0,
                          rows=_ops.dev_i32(plan.rows),
-                         frozen=torch.as_tensor(plan.masks.view(np.int64), device=d), layout=0)
+                         frozen=torch.as_tensor(plan.masks.view(np.int64), device=d), layout=0,
+                         half=half)
         _ops.raise_on_status(h)
         if stats is not None:
             stats.setdefault("ms", []).append(h.ms)
+        if half:
+            return _rows_from(plan, sset, h.rows), _rows_from(plan, sset, h.half)
         return _rows_from(plan, sset, h.rows)
     # per-node path: one item per node (of the shard, plus its halo nodes)
     off, N = (0, sset.N) if node_range is None else (int(node_range[0]), int(node_range[1]))
@@ -347,7 +357,7 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
     shared_coords = plan.coords.shape[0] == 1
     uniform_rows = plan.uniform_rows
     if pad:
-        idx = torch.remainder(torch.arange(off - pad, off + N + pad, device=d), sset.N)
+        idx = _wrapped_segments(off - pad, N + 2 * pad, sset.N)
         N += 2 * pad
     else:
         idx = None
@@ -371,9 +381,12 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
         return _ops.CompactRows(sset, nat.W_PERNODE, pernode=h.rows)
     elif varcoef:
         if idx is not None:
-            coef_all = _ops.dev_f64(spec.coef).index_select(0, idx).contiguous()
-            react = None if spec.reaction is None else \
-                _ops.dev_f64(spec.reaction).index_select(0, idx).contiguous()
+            cdev = _ops.dev_f64(spec.coef)
+            coef_all = torch.cat([cdev[a:b] for a, b in idx], 0).contiguous()
+            react = None
+            if spec.reaction is not None:
+                rdev = _ops.dev_f64(spec.reaction)
+                react = torch.cat([rdev[a:b] for a, b in idx], 0).contiguous()
         else:
             coef_all = _ops.dev_f64(spec.coef[sl])
             react = None if spec.reaction is None else _ops.dev_f64(spec.reaction[sl])
@@ -428,6 +441,18 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
             stats.setdefault("ms", []).append(h.ms)
         out[:, :, a:b] = h.rows
     return _ops.CompactRows(sset, nat.W_PERNODE, pernode=out)
+
+
+def _wrapped_segments(start: int, count: int, N: int) -> list[tuple[int, int]]:
+    """Nodes start .. start+count-1 taken mod N, as contiguous [a, b) slices in order."""
+    out = []
+    a = start % N
+    while count > 0:
+        b = min(N, a + count)
+        out.append((a, b))
+        count -= b - a
+        a = 0
+    return out
 
 
 PIPELINE_MIN = 1 << 18      # nodes; smaller host tables go up in one copy

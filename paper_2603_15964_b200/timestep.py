@@ -164,16 +164,45 @@ def etdrk4_operators(ops_full: list[BandedPropagator], ops_half: list[BandedProp
     return w, alpha, beta, gamma, ops_half[0], ops_half[1]
 
 
+_ABG = ((nat.ROW_ALPHA, (1, 2, 3), lambda dt: (1.0, -3.0 / dt, 4.0 / dt**2)),
+        (nat.ROW_BETA, (2, 3), lambda dt: (2.0 / dt, -4.0 / dt**2)),
+        (nat.ROW_GAMMA, (3, 2), lambda dt: (4.0 / dt**2, -1.0 / dt)))
+
+
 def _etdrk4_bank(full: _ops.CompactRows, half: _ops.CompactRows, dt: float,
                  d1: _ops.CompactRows | None) -> _ops.CompactRows:
-    p = [full.row(j) for j in range(4)]
-    alpha = _ops.combine_rows([p[1], p[2], p[3]], [1.0, -3.0 / dt, 4.0 / dt**2])
-    beta = _ops.combine_rows([p[2], p[3]], [2.0 / dt, -4.0 / dt**2])
-    gamma = _ops.combine_rows([p[3], p[2]], [4.0 / dt**2, -1.0 / dt])
-    parts = [p[0], alpha, beta, gamma, half.row(0), half.row(1)]
-    if d1 is not None:
-        parts.append(d1)
-    return _ops.stack_rows(parts)
+    """The fused ETDRK4 bank [w, alpha, beta, gamma, w_half, p1_half(, d1)]:
+    alpha / beta / gamma (timestep.py:141-156, combine's ordered sums,
+    harvest.py:225-235) are composed by the library's combine kernel straight
+    from the harvested phi rows into their slots of the bank."""
+    p0 = full.row(0)
+    if p0.mode == nat.W_PERNODE:
+        zero = _ops.CompactRows(p0.layout, nat.W_PERNODE, pernode=torch.zeros_like(p0.pernode),
+                                pernode_pad=p0.pernode_pad)
+    else:
+        zero = _ops.CompactRows(p0.layout, p0.mode, torch.zeros_like(p0.interior),
+                                None if p0.classes is None else torch.zeros_like(p0.classes),
+                                p0.nleft, p0.nright)
+    parts = [p0, zero, zero, zero, half.row(0), half.row(1)] + ([d1] if d1 is not None else [])
+    bank = _ops.stack_rows(parts)
+    fb = full if bank.mode == nat.W_PERNODE else full.with_classes(bank.nleft, bank.nright)
+    R = bank.R
+    n = bank.n
+    for slot, terms, cof in _ABG:
+        c = cof(dt)
+        if bank.mode == nat.W_PERNODE:
+            blk = fb.pernode[0].numel()
+            _ops.combine_into(bank.pernode[slot], [fb.pernode[t] for t in terms], c, 1, blk, blk,
+                              [blk] * len(terms))
+            continue
+        _ops.combine_into(bank.interior[slot], [fb.interior[t] for t in terms], c, 1, n, n,
+                          [n] * len(terms))
+        if bank.classes is not None:
+            Cn = bank.classes.shape[0]
+            _ops.combine_into(bank.classes[:, slot], [fb.classes[:, t] for t in terms], c, Cn, n,
+                              R * n, [fb.R * n] * len(terms))
+    bank._host_interior = None
+    return bank
 
 
 def assemble_derivative(grid: Grid, stencils, k: int) -> BandedPropagator:
@@ -264,8 +293,7 @@ def prepare(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConf
     if scheme.kind == "linear":
         bank = harvest_compact(grid, sset, spec, delta_t, 1, frozen, stats)
     elif scheme.kind == "etdrk4":
-        full = harvest_compact(grid, sset, spec, delta_t, 4, frozen, stats)
-        half = harvest_compact(grid, sset, spec, delta_t / 2, 2, frozen, stats)
+        full, half = harvest_compact(grid, sset, spec, delta_t, 4, frozen, stats, half=True)
         bank = _etdrk4_bank(full, half, delta_t, d1)
     else:
         s = scheme.s
@@ -274,8 +302,7 @@ def prepare(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConf
         ops = harvest_compact(grid, sset, spec, delta_t, s + 1, frozen, stats)
         parts = {nat.ROW_W + j: ops.row(j) for j in range(s + 1)}
         if s >= 2:
-            full = harvest_compact(grid, sset, spec, delta_t, 4, frozen, stats)
-            half = harvest_compact(grid, sset, spec, delta_t / 2, 2, frozen, stats)
+            full, half = harvest_compact(grid, sset, spec, delta_t, 4, frozen, stats, half=True)
             warm = _etdrk4_bank(full, half, delta_t, d1)
         if d1 is not None:
             parts[nat.ROW_D1] = d1
@@ -320,13 +347,13 @@ class Stepper:
                 self._hout = torch.empty_like(self.hist)
                 self._warm = 0
             # warm-up: s-1 ETDRK4 steps, each storing N(u) in front of the
-            # history (timestep.py:375-378); may straddle advance() calls
+            # history (timestep.py:375-378); may straddle advance() calls.  The
+            # history is newest first, so warm-up step i's N(u_i) lands in slot
+            # s-2-i directly (no shifting of the older entries)
             while self._warm < s - 1 and k > 0:
                 i = self._warm
-                if i > 0:
-                    self.hist[1:i + 1] = self.hist[0:i].clone()
                 out = _ops.step(nat.SCH_ETDRK4, p.warm, self.u, 1, out=self._out,
-                                nl0_out=self.hist[0], **kw)
+                                nl0_out=self.hist[s - 2 - i], **kw)
                 self._out, self.u = self.u, out
                 self._warm += 1
                 self.done += 1

@@ -117,3 +117,104 @@ def test_harvest_method_switch_is_per_device(lx):
     assert nat.lib().lmep_set_harvest_method(3) == nat.LMEP_INVALID_CONFIG
     nat.set_harvest_method("pade")
     nat.set_harvest_method("multiply")
+
+
+# ------------------------------------------------------------------ glue kernels
+@pytest.mark.parametrize("method", ["multiply", "pade"])
+@pytest.mark.parametrize("layout", [0, 1])
+def test_harvest_half_step_set(lx, orc, method, layout):
+    """lmep_harvest_ex half_out: the (w_lin, dt/2 phi_1) rows at delta_t / 2 from
+    the same launch (per-item kernel: even number of scaling reps, the iterate
+    after half of them) or a second launch (Pade), against the oracle's
+    harvest at delta_t / 2 (1e-12), frozen rows included; the full set is
+    unchanged."""
+    from paper_2603_15964_b200 import _ops
+    rng = np.random.default_rng(5)
+    n, s, T = 9, 4, 6
+    h = 0.01
+    tabs, Ls, rows, masks = [], [], [], []
+    for t in range(T):
+        row = int(rng.integers(0, n))
+        x = (np.arange(n) - row) * h * (1 + 0.1 * t)
+        terms = ((1, float(rng.uniform(-1, 1))), (2, float(rng.uniform(0.1, 1))))
+        Ls.append(orc.local_operator(x, terms))
+        rows.append(row)
+        masks.append(1 if (t % 2 and row != 0) else 0)
+    dt = 0.3 * h * h
+    lx._native.set_harvest_method(method)
+    try:
+        hv = _ops.harvest(n, s, dt, T, L=_ops.dev_f64(np.stack(Ls)), rows=_ops.dev_i32(rows),
+                          frozen=torch.as_tensor(np.array(masks, dtype=np.int64), device="cuda"),
+                          layout=layout, half=True)
+        torch.cuda.synchronize()
+    finally:
+        lx._native.set_harvest_method("multiply")
+    full = hv.rows.cpu().numpy()
+    half = hv.half.cpu().numpy()
+    if layout == 1:
+        full, half = full.transpose(2, 0, 1), half.transpose(2, 0, 1)
+    assert int(hv.flag.item()) == 0
+    for t in range(T):
+        fz = [0] if masks[t] else []
+        wl, wp = orc.harvest_phi_weights(Ls[t], dt / 2, 2, rows[t], fz)
+        ref = np.vstack([wl, wp[0]])
+        den = np.abs(ref).max(axis=1)
+        assert (np.abs(half[t] - ref).max(axis=1) / den).max() < 1e-12, (t, method)
+        wl, wp = orc.harvest_phi_weights(Ls[t], dt, s, rows[t], fz)
+        ref = np.vstack([wl] + list(wp))
+        den = np.abs(ref).max(axis=1)
+        assert (np.abs(full[t] - ref).max(axis=1) / den).max() < 1e-12, (t, method)
+
+
+def test_harvest_status_flag(lx):
+    """A non-finite operator sets the library's device flag (lmep_harvest_ex
+    status_any); raise_on_status reads that flag."""
+    from paper_2603_15964_b200 import _ops
+    L = np.zeros((3, 7, 7))
+    L[1, 2, 3] = np.nan
+    hv = _ops.harvest(7, 2, 0.1, 3, L=_ops.dev_f64(L), row_default=3, half=True)
+    assert int(hv.flag.item()) == 1
+    assert hv.status.cpu().numpy().tolist()[1] != 0
+    with pytest.raises(lx.NonFinite):
+        _ops.raise_on_status(hv)
+
+
+def test_combine_kernel_matches_numpy(lx):
+    """lmep_combine = harvest.combine's numpy expression (zeros + c * a, list
+    order, two roundings per term) bit for bit, on strided row arrays."""
+    from paper_2603_15964_b200 import _ops
+    rng = np.random.default_rng(9)
+    A = rng.standard_normal((5, 3, 11)) * 10.0 ** rng.integers(-20, 3, (5, 3, 1))
+    A[0, 0, 0] = -0.0
+    coeffs = [1.0, -3.0 / 7e-11, 4.0 / 7e-11 ** 2]
+    ref = np.zeros((5, 11))
+    for i, c in enumerate(coeffs):
+        ref = ref + c * A[:, i]
+    d = torch.as_tensor(A, device="cuda")
+    out = torch.empty((5, 11), dtype=torch.float64, device="cuda")
+    _ops.combine_into(out, [d[:, i] for i in range(3)], coeffs, 5, 11, 11, [33, 33, 33])
+    assert np.array_equal(out.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("case", ["shared", "class", "pernode"])
+def test_compress_classification(lx, case):
+    """Reference-style (N, n) rows are compressed on the device (lmep_rows_classify)
+    into shared / class / per-node form, and expand back to the same array."""
+    from paper_2603_15964_b200 import _native as nat, _ops
+    from paper_2603_15964_b200.grid import StencilSet
+    N, n = 257, 7
+    rng = np.random.default_rng(2)
+    mid = rng.standard_normal(n)
+    W = np.tile(mid, (N, 1))
+    lay = StencilSet(N, n, 3, case == "shared")
+    if case == "class":
+        W[:4] = rng.standard_normal((4, n))
+        W[N - 3:] = rng.standard_normal((3, n))
+    if case == "pernode":
+        W[100] += 1.0
+    cr = _ops.compress(torch.as_tensor(W, device="cuda"), lay)
+    want = {"shared": nat.W_SHARED, "class": nat.W_CLASS, "pernode": nat.W_PERNODE}[case]
+    assert cr.mode == want
+    if case == "class":
+        assert (cr.nleft, cr.nright) == (4, 3)
+    assert np.array_equal(cr.dense()[0].cpu().numpy(), W)
