@@ -282,6 +282,15 @@ int lmep_combine(int nterm, const double *const *in, const int64_t *ld_in, const
 int lmep_rows_classify(const double *rows, int64_t N, int n, int64_t ref, uint64_t *out3,
                        void *stream);
 
+/* Symbol of one weight row on [0, kmax] (analysis.spectral_footprint,
+ * analysis.py:42-64): for k_i = i kmax / (num_k - 1),
+ *   G(k) = sum_j w[j] exp(i k offsets_h[j]),  |G|,  arg(G exp(i k shift)).
+ * w and offsets_h (offsets times h) are HOST arrays of n <= 32 values; the
+ * four outputs are device arrays of num_k doubles. */
+int lmep_spectral_footprint(const double *w, const double *offsets_h, int n, double kmax,
+                            int num_k, double shift, double *g_re, double *g_im, double *g_abs,
+                            double *dispersion, void *stream);
+
 /* Harvest algorithm for d <= 16:
  *   0 (default) = expm-multiply: large single-geometry batches (n in
  *     {7, 9, 11, 13}, B >= 4096; s = 1 with <= 2 tables, or s <= 4 with two

@@ -44,7 +44,7 @@ EXPORTS = (
     "lmep_banded_matvec", "lmep_plan", "lmep_rows_to_soa", "lmep_launch_count",
     "lmep_set_harvest_method", "lmep_set_ring_cluster", "lmep_step_etds", "lmep_harvest_mapped", "lmep_harvest_chunk",
     "lmep_set_pernode_kernel", "lmep_harvest_ex", "lmep_status_any", "lmep_combine",
-    "lmep_rows_classify",
+    "lmep_rows_classify", "lmep_spectral_footprint",
 )
 
 
@@ -145,6 +145,8 @@ def load(path: str | None = None):
     L.lmep_combine.argtypes = [C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64),
                                C.POINTER(C.c_double), i64, i64, vp, i64, vp]
     L.lmep_rows_classify.argtypes = [vp, i64, C.c_int, i64, vp, vp]
+    L.lmep_spectral_footprint.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int,
+                                          dbl, C.c_int, dbl, vp, vp, vp, vp, vp]
     for name in EXPORTS:
         if name not in ("lmep_version", "lmep_status_string", "lmep_last_error",
                         "lmep_launch_count"):

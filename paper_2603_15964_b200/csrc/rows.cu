@@ -136,3 +136,61 @@ extern "C" int lmep_rows_classify(const double *rows, int64_t N, int n, int64_t 
     classify_kernel<<<grid_for(N, 256), 256, 0, st>>>(rows, N, n, ref, o);
     return launch_status("classify_kernel");
 }
+
+namespace lmep {
+
+struct FootArgs {
+    double w[LMEP_MAX_N];
+    double oh[LMEP_MAX_N];
+    int n, num_k;
+    double kstep, kmax, shift;
+    double *gre, *gim, *gabs, *disp;
+};
+
+// symbol of one weight row (analysis.py:42-64): one thread per wavenumber,
+// k_i = i * kstep (the last one exactly pi / h, like numpy.linspace)
+__global__ void footprint_kernel(const __grid_constant__ FootArgs a)
+{
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.num_k) return;
+    const double k = (i == a.num_k - 1 && a.num_k > 1) ? a.kmax : (double)i * a.kstep;
+    double re = 0.0, im = 0.0;
+    for (int j = 0; j < a.n; ++j) {
+        double s, c;
+        sincos(k * a.oh[j], &s, &c);
+        re = fma(a.w[j], c, re);
+        im = fma(a.w[j], s, im);
+    }
+    double ss, cs;
+    sincos(k * a.shift, &ss, &cs);
+    a.gre[i] = re;
+    a.gim[i] = im;
+    a.gabs[i] = hypot(re, im);
+    a.disp[i] = atan2(re * ss + im * cs, re * cs - im * ss);
+}
+
+}  // namespace lmep
+
+extern "C" int lmep_spectral_footprint(const double *w, const double *offsets_h, int n, double kmax,
+                                       int num_k, double shift, double *g_re, double *g_im,
+                                       double *g_abs, double *dispersion, void *stream)
+{
+    if (!w || !offsets_h || n < 1 || n > LMEP_MAX_N || num_k < 1) return LMEP_INVALID_CONFIG;
+    if (!g_re || !g_im || !g_abs || !dispersion) return LMEP_INVALID_CONFIG;
+    FootArgs a{};
+    for (int j = 0; j < n; ++j) {
+        a.w[j] = w[j];
+        a.oh[j] = offsets_h[j];
+    }
+    a.n = n;
+    a.num_k = num_k;
+    a.kmax = kmax;
+    a.kstep = num_k > 1 ? kmax / (double)(num_k - 1) : 0.0;
+    a.shift = shift;
+    a.gre = g_re;
+    a.gim = g_im;
+    a.gabs = g_abs;
+    a.disp = dispersion;
+    footprint_kernel<<<(unsigned)((num_k + 127) / 128), 128, 0, (cudaStream_t)stream>>>(a);
+    return launch_status("footprint_kernel");
+}

@@ -62,6 +62,16 @@ class Grid:
             h = (self.x_max - self.x_min) / x.size
             if (np.abs(gaps - h) > 1e-14 * abs(h) * x.size).any():
                 raise InvalidGrid("a periodic grid must be uniform")
+        elif self.uniform_spacing is None and x.size >= 3:
+            # a reference-style uniform grid, Grid(nodes=np.linspace(a, b, N)):
+            # equispaced to the rounding of its own construction -> stencil
+            # coordinates offsets * h (position classes, shardable), as
+            # make_uniform_grid's (DESIGN 5.5)
+            h = (x[-1] - x[0]) / (x.size - 1)
+            tol = 8.0 * np.finfo(np.float64).eps * max(abs(x[0]), abs(x[-1]), abs(h))
+            ideal = x[0] + h * np.arange(x.size, dtype=np.float64)
+            if np.abs(x - ideal).max() <= tol:
+                object.__setattr__(self, "uniform_spacing", float(h))
 
     @property
     def size(self) -> int:

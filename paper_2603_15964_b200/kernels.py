@@ -12,9 +12,20 @@ bit-identical to numba's unfused ascending arithmetic; False: FMA),
 ``bc=("neumann", dl, dr)`` for the zero-gradient closure, and
 ``tuning`` (launch shape).  Inputs are never modified; numpy in -> numpy
 out, torch in -> torch out.
+
+Rebinding cost.  Under the reference's own ``run()`` these
+functions are called once per snapshot chunk with the SAME read-only arrays
+(BandedPropagator makes them read-only, harvest.py:59-62).  The recognised
+stencil layout and the compressed device rows are therefore cached on the
+identity of the arrays: numpy arrays only while they are read-only (a writable
+array may change between calls and is re-read), torch tensors on their
+in-place version counter.  Entries die with their arrays (weak references).
 """
 
 from __future__ import annotations
+
+import weakref
+from collections import OrderedDict
 
 import numpy as np
 import torch
@@ -32,6 +43,53 @@ def _dense(a) -> torch.Tensor:
     return _ops.dev_f64(a)
 
 
+class _IdentityCache:
+    """Results keyed on the identity of immutable arrays (see the module doc)."""
+
+    def __init__(self, cap: int = 16):
+        self.cap = cap
+        self.d: OrderedDict = OrderedDict()
+
+    @staticmethod
+    def _key(a, extra):
+        if isinstance(a, np.ndarray):
+            return None if a.flags.writeable else ("np", id(a), extra)
+        if isinstance(a, torch.Tensor):
+            return ("t", id(a), a._version, a.data_ptr(), extra)
+        return None
+
+    def get(self, a, extra, make):
+        k = self._key(a, extra)
+        if k is None:
+            return make()
+        hit = self.d.get(k)
+        if hit is not None and hit[0]() is a:
+            self.d.move_to_end(k)
+            return hit[1]
+        v = make()
+        try:
+            ref = weakref.ref(a, lambda _r, k=k: self.d.pop(k, None))
+        except TypeError:
+            return v
+        self.d[k] = (ref, v)
+        while len(self.d) > self.cap:
+            self.d.popitem(last=False)
+        return v
+
+
+_LAYOUTS = _IdentityCache()
+_ROWS = _IdentityCache()
+
+
+def _layout(members, shape):
+    return _LAYOUTS.get(members, tuple(shape), lambda: _ops.validate_members(members, shape))
+
+
+def _rows(w, layout) -> _ops.CompactRows:
+    key = (layout.N, layout.n, layout.row, layout.periodic)
+    return _ROWS.get(w, key, lambda: _ops.compress(_dense(w), layout))
+
+
 def _bc(pin, pin_lo, pin_hi, bc) -> _ops.BC:
     if bc is not None:
         if bc[0] == "neumann":
@@ -45,7 +103,7 @@ def _bc(pin, pin_lo, pin_hi, bc) -> _ops.BC:
 
 
 def _bank(layout, named: dict[int, object]) -> _ops.CompactRows:
-    rows = {r: _ops.compress(_dense(w), layout) for r, w in named.items()}
+    rows = {r: _rows(w, layout) for r, w in named.items()}
     R = max(rows) + 1
     return _ops.rows_bank_for(layout, rows, R)
 
@@ -57,9 +115,8 @@ def _ret(x: torch.Tensor, like):
 def banded_matvec(weights, members, u, out) -> None:
     """out[i] = sum_j weights[i, j] u[members[i, j]] (kernels.py:23-29); writes out."""
     from .harvest import BandedPropagator, apply
-    lay = _ops.validate_members(members, np.shape(weights))
-    prop = BandedPropagator(periodic=lay.periodic,
-                            _rows=_ops.compress(_dense(weights), lay))
+    lay = _layout(members, np.shape(weights))
+    prop = BandedPropagator(periodic=lay.periodic, _rows=_rows(weights, lay))
     r = apply(prop, u)
     if isinstance(out, torch.Tensor):
         out.copy_(r if isinstance(r, torch.Tensor) else torch.as_tensor(r))
@@ -73,7 +130,7 @@ def run_linear(weights, members, u0, steps, pin=False, pin_lo=0.0, pin_hi=0.0, *
     ``exact=False`` lets the temporally blocked per-node kernels use fused
     multiply-adds (they are FP64-issue-bound); the other linear kernels are
     always exact."""
-    lay = _ops.validate_members(members, np.shape(weights))
+    lay = _layout(members, np.shape(weights))
     bank = _bank(lay, {nat.ROW_W: weights})
     u = _dense(u0)
     out = _ops.step(nat.SCH_LIN, bank, u, int(steps), bc=_bc(pin, pin_lo, pin_hi, bc),
@@ -85,7 +142,7 @@ def run_etdrk4(w_full, w_alpha, w_beta, w_gamma, w_half, w_p1h, d1w, members, ki
                pin=False, pin_lo=0.0, pin_hi=0.0, *, exact=True, bc=None, tuning=None,
                nl0_out=None):
     """Fused four-stage exponential RK loop (kernels.py:62-132)."""
-    lay = _ops.validate_members(members, np.shape(w_full))
+    lay = _layout(members, np.shape(w_full))
     named = {nat.ROW_W: w_full, nat.ROW_ALPHA: w_alpha, nat.ROW_BETA: w_beta,
              nat.ROW_GAMMA: w_gamma, nat.ROW_WHALF: w_half, nat.ROW_P1HALF: w_p1h}
     if int(kind) == NL_CONVECTIVE:
@@ -106,7 +163,7 @@ def run_etd2(ops, d1w, members, kind, u0, hist, steps, delta_t, pin=False, pin_l
     s = len(ops) - 1
     if not 1 <= s <= 5:
         raise InvalidConfig("etd-multistep supports 1 <= s <= 5")
-    lay = _ops.validate_members(members, np.shape(ops[0]))
+    lay = _layout(members, np.shape(ops[0]))
     named = {nat.ROW_W + j: ops[j] for j in range(s + 1)}
     if int(kind) == NL_CONVECTIVE:
         named[nat.ROW_D1] = d1w

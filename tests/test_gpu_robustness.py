@@ -218,3 +218,51 @@ def test_compress_classification(lx, case):
     if case == "class":
         assert (cr.nleft, cr.nright) == (4, 3)
     assert np.array_equal(cr.dense()[0].cpu().numpy(), W)
+
+
+def test_reference_style_linspace_grid_takes_class_path(lx):
+    """Grid(nodes=np.linspace(...), NON_PERIODIC) -- the reference's way to build
+    config 4 -- is recognised as uniform: class rows (not one exponential per
+    node) and a run bit-identical to make_uniform_grid's."""
+    from paper_2603_15964_b200 import _native as nat, configs
+    from paper_2603_15964_b200.harvest import harvest_compact
+    w = configs.c4(N=4096, steps=20)
+    gref = lx.Grid(nodes=np.linspace(-1.0, 1.0, w.N), x_min=-1.0, x_max=1.0,
+                   topology=lx.Topology.NON_PERIODIC)
+    gu = lx.make_uniform_grid(w.N, -1.0, 1.0)
+    assert gref.uniform_spacing == gu.uniform_spacing
+    st = lx.select_stencils(gref, w.n, lx.StencilPolicy.CENTERED)
+    rows = harvest_compact(gref, st, lx.LinearOperatorSpec(w.terms), w.delta_t, 1, (0, w.N - 1))
+    assert rows.mode == nat.W_CLASS
+    prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(w.terms), None, w.u0,
+                                lx.Boundary.neumann(), "cubic")
+    a = lx.run(gref, st, prob, lx.SchemeConfig("etdrk4"), w.delta_t, 20 * w.delta_t)
+    stu = lx.select_stencils(gu, w.n, lx.StencilPolicy.CENTERED)
+    b = lx.run(gu, stu, prob, lx.SchemeConfig("etdrk4"), w.delta_t, 20 * w.delta_t)
+    assert np.array_equal(a.u_final, b.u_final)
+
+
+def test_rebinding_caches_read_only_arrays(lx, orc):
+    """kernels.run_* called repeatedly with the same read-only (N, n) arrays (the
+    reference's run() loop over snapshot chunks) validates the member array
+    and uploads / compresses each weight array once; writable arrays are re-read."""
+    from paper_2603_15964_b200 import kernels
+    N, n, row = 3000, 13, 6
+    rng = np.random.default_rng(4)
+    W = rng.standard_normal((N, n)) / n
+    m = orc.members_for(N, n, row, True)
+    W.setflags(write=False)
+    m.setflags(write=False)
+    u0 = rng.standard_normal(N)
+    kernels._ROWS.d.clear()
+    kernels._LAYOUTS.d.clear()
+    u = u0
+    for _ in range(4):
+        u = kernels.run_linear(W, m, u, 5)
+    assert len(kernels._ROWS.d) == 1 and len(kernels._LAYOUTS.d) == 1
+    assert np.array_equal(u, orc.run_linear(W, m, u0, 20))
+    W2 = W.copy()                                    # writable: never cached
+    kernels.run_linear(W2, m, u0, 1)
+    assert len(kernels._ROWS.d) == 1
+    W2[0, 0] += 1.0
+    assert np.array_equal(kernels.run_linear(W2, m, u0, 3), orc.run_linear(W2, m, u0, 3))

@@ -155,3 +155,25 @@ def test_weight_table_json_parse(golden):
         bad = json.loads(text)
         bad["nodes"][0]["members"] = [5, 3, 1]
         parse_weight_table_json(json.dumps(bad), device="cpu")
+
+
+def test_reference_test_oracles_exported():
+    """phi_scalar / expm_taylor_oracle (expm.py:45-83) keep the reference's names
+    and values: closed forms of phi_j, both branches of phi_scalar."""
+    import math
+    import paper_2603_15964_b200 as lx
+    for z in (0.3, -0.2 + 0.1j, 1.7, -2.5):
+        assert abs(lx.phi_scalar(0, z) - np.exp(z)) < 1e-15 * abs(np.exp(z))
+        p1 = (np.exp(z) - 1) / z
+        assert abs(lx.phi_scalar(1, z) - p1) < 1e-13 * abs(p1)
+        p2 = (np.exp(z) - 1 - z) / z ** 2
+        assert abs(lx.phi_scalar(2, z) - p2) < 1e-10 * abs(p2)
+    assert abs(lx.phi_scalar(3, 0.0) - 1.0 / 6.0) < 1e-16
+    with pytest.raises(ValueError):
+        lx.phi_scalar(9, 0.1)
+    A = np.array([[0.0, 1.0], [-1.0, 0.0]])
+    E = lx.expm_taylor_oracle(A)
+    R = np.array([[math.cos(1), math.sin(1)], [-math.sin(1), math.cos(1)]])
+    assert np.abs(E - R).max() < 1e-15
+    with pytest.raises(lx.NoConvergence):
+        lx.expm_taylor_oracle(50.0 * A, max_terms=5)
