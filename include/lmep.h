@@ -329,6 +329,94 @@ int lmep_set_ring_cluster(int on);
  * order.  Per-device setting; results are bit-identical in the exact mode. */
 int lmep_set_pernode_kernel(int variant);
 
+/* ---- sharded runs (K6): communicator, halo exchange, graphs --------------- */
+
+/* One communicator per rank (one process per GPU) of a 1D slab decomposition
+ * (the reference has no collectives -- timestep.run, timestep.py:
+ * 255-394, advances one array).  Rank r's neighbours are r-1 / r+1, wrapped
+ * on a periodic ring; with world == 1 and periodic != 0 the rank is its own
+ * neighbour on both sides (the self-exchange that checks the data path on one
+ * GPU).  Two transports move the halos:
+ *   LMEP_COMM_NCCL  ncclSend / ncclRecv pairs in one group on the caller's
+ *                   stream (libnccl.so.2 is resolved at run time);
+ *   LMEP_COMM_PEER  CUDA IPC on one node: every rank owns a device mailbox,
+ *                   the exchange STORES its edges straight into the
+ *                   neighbours' mailboxes (one kernel writing peer memory
+ *                   over NVLink), signals with an interprocess event and
+ *                   copies its own mailbox out after waiting for the
+ *                   neighbours' events.  Mailboxes are double buffered; all
+ *                   exchanges of a communicator must be issued in one stream
+ *                   order.  Not capturable in a CUDA graph (the ranks meet on
+ *                   the host before each wait).
+ * Bootstrap is out of band, as with ncclUniqueId: the caller moves a few
+ * bytes between the ranks with whatever it has (MPI, a torch.distributed
+ * store, a file). */
+typedef struct lmep_comm lmep_comm;
+enum { LMEP_COMM_NCCL = 0, LMEP_COMM_PEER = 1 };
+#define LMEP_COMM_ID_BYTES 128     /* ncclUniqueId                                    */
+#define LMEP_COMM_BLOB_BYTES 512   /* one rank's IPC handles (PEER transport)         */
+#define LMEP_COMM_MAX_FIELDS 8     /* arrays exchanged together (u + ETD history)     */
+
+/* NCCL: rank 0 fills id (host, LMEP_COMM_ID_BYTES) and hands it to every rank. */
+int lmep_comm_unique_id(void *id);
+
+/* Create rank `rank` of `world` on the calling thread's current device.
+ * NCCL: `id` from lmep_comm_unique_id (collective: every rank calls).
+ * PEER: id is ignored; max_width = the widest halo (doubles per field and
+ * side) the mailboxes must hold; the communicator is usable after
+ * lmep_comm_connect. */
+int lmep_comm_init(lmep_comm **comm, int rank, int world, int periodic, int transport,
+                   const void *id, int64_t max_width);
+/* PEER: this rank's IPC handles (host, LMEP_COMM_BLOB_BYTES) ... */
+int lmep_comm_export(lmep_comm *comm, void *blob);
+/* ... and, once the caller has gathered them, every rank's blobs in rank
+ * order (host, world * LMEP_COMM_BLOB_BYTES).  NCCL: both are no-ops. */
+int lmep_comm_connect(lmep_comm *comm, const void *blobs);
+int lmep_comm_destroy(lmep_comm *comm);
+/* left / right = neighbour ranks, -1 at the ends of an open chain. */
+int lmep_comm_info(const lmep_comm *comm, int *rank, int *world, int *left, int *right,
+                   int *transport);
+
+/* Fill the ghost cells of nfields arrays of nloc doubles each: ghost_left[f]
+ * receives the left neighbour's last `width` values of field f, ghost_right[f]
+ * the right neighbour's first `width` (a rank without a neighbour on a side
+ * leaves that buffer alone).  fields / ghost_left / ghost_right are HOST
+ * arrays of nfields device pointers.  One NCCL group (or one peer-store
+ * kernel) moves all fields.  Asynchronous on `stream`. */
+int lmep_halo_exchange(lmep_comm *comm, int nfields, const double *const *fields, int64_t nloc,
+                       int64_t width, double *const *ghost_left, double *const *ghost_right,
+                       void *stream);
+
+/* Concatenate the slabs on `root`: rank r contributes nloc_r = counts[r]
+ * doubles (counts: HOST array of world entries, the same on every rank); out
+ * (root only) receives them in rank order.  NCCL transport only (PEER runs
+ * gather through the host). */
+int lmep_comm_gather(lmep_comm *comm, const double *u, const int64_t *counts, double *out,
+                     int root, void *stream);
+/* flag[0..count) (device int32) <- max over ranks.  NCCL transport only. */
+int lmep_comm_flag_max(lmep_comm *comm, int32_t *flag, int count, void *stream);
+
+/* A second stream owned by the communicator, for overlapping the exchange
+ * with the interior of the slab: fork makes the side stream wait for the
+ * work queued on `stream` so far, join makes `stream` wait for the side
+ * stream.  Both are capturable (event record + wait). */
+void *lmep_comm_side_stream(lmep_comm *comm);
+int lmep_comm_fork(lmep_comm *comm, void *stream);
+int lmep_comm_join(lmep_comm *comm, void *stream);
+
+/* CUDA graph of a chunk (halo exchange + fused k-step launch, with the
+ * interior / edge split on two streams): begin starts a thread-local capture
+ * on `stream`, every lmep_* call issued on it (and on streams forked from it)
+ * until lmep_graph_end is recorded instead of run.  lmep_graph_launch replays
+ * it.  Device pointers are baked in: capture one graph per ping-pong
+ * direction.  NCCL exchanges are capturable once the communicator has run
+ * one exchange outside a capture. */
+typedef struct lmep_graph lmep_graph;
+int lmep_graph_begin(void *stream);
+int lmep_graph_end(void *stream, lmep_graph **graph);
+int lmep_graph_launch(lmep_graph *graph, void *stream);
+int lmep_graph_destroy(lmep_graph *graph);
+
 /* ---- stepping (K3, K4, K5) ---------------------------------------------- */
 
 /* Linear banded propagation u <- W u for `steps` steps (kernels.py:33-43,

@@ -45,7 +45,13 @@ EXPORTS = (
     "lmep_set_harvest_method", "lmep_set_ring_cluster", "lmep_step_etds", "lmep_harvest_mapped", "lmep_harvest_chunk",
     "lmep_set_pernode_kernel", "lmep_harvest_ex", "lmep_status_any", "lmep_combine",
     "lmep_rows_classify", "lmep_spectral_footprint",
+    "lmep_comm_unique_id", "lmep_comm_init", "lmep_comm_export", "lmep_comm_connect",
+    "lmep_comm_destroy", "lmep_comm_info", "lmep_halo_exchange", "lmep_comm_gather",
+    "lmep_comm_flag_max", "lmep_comm_side_stream", "lmep_comm_fork", "lmep_comm_join",
+    "lmep_graph_begin", "lmep_graph_end", "lmep_graph_launch", "lmep_graph_destroy",
 )
+COMM_NCCL, COMM_PEER = 0, 1
+COMM_ID_BYTES, COMM_BLOB_BYTES, COMM_MAX_FIELDS = 128, 512, 8
 
 
 class LmepGrid(C.Structure):
@@ -147,9 +153,28 @@ def load(path: str | None = None):
     L.lmep_rows_classify.argtypes = [vp, i64, C.c_int, i64, vp, vp]
     L.lmep_spectral_footprint.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int,
                                           dbl, C.c_int, dbl, vp, vp, vp, vp, vp]
+    ip = C.POINTER(C.c_int)
+    L.lmep_comm_unique_id.argtypes = [vp]
+    L.lmep_comm_init.argtypes = [C.POINTER(vp), C.c_int, C.c_int, C.c_int, C.c_int, vp, i64]
+    L.lmep_comm_export.argtypes = [vp, vp]
+    L.lmep_comm_connect.argtypes = [vp, vp]
+    L.lmep_comm_destroy.argtypes = [vp]
+    L.lmep_comm_info.argtypes = [vp, ip, ip, ip, ip, ip]
+    L.lmep_halo_exchange.argtypes = [vp, C.c_int, C.POINTER(vp), i64, i64, C.POINTER(vp),
+                                     C.POINTER(vp), vp]
+    L.lmep_comm_gather.argtypes = [vp, vp, C.POINTER(i64), vp, C.c_int, vp]
+    L.lmep_comm_flag_max.argtypes = [vp, vp, C.c_int, vp]
+    L.lmep_comm_side_stream.argtypes = [vp]
+    L.lmep_comm_side_stream.restype = vp
+    L.lmep_comm_fork.argtypes = [vp, vp]
+    L.lmep_comm_join.argtypes = [vp, vp]
+    L.lmep_graph_begin.argtypes = [vp]
+    L.lmep_graph_end.argtypes = [vp, C.POINTER(vp)]
+    L.lmep_graph_launch.argtypes = [vp, vp]
+    L.lmep_graph_destroy.argtypes = [vp]
     for name in EXPORTS:
         if name not in ("lmep_version", "lmep_status_string", "lmep_last_error",
-                        "lmep_launch_count"):
+                        "lmep_launch_count", "lmep_comm_side_stream"):
             getattr(L, name).restype = C.c_int
     _lib = L
     return L

@@ -14,6 +14,13 @@ void set_last_error(const char *what, cudaError_t e)
     snprintf(g_last_error, sizeof(g_last_error), "%s: %s", what, cudaGetErrorString(e));
 }
 
+void set_last_error_text(const char *what, const char *msg)
+{
+    snprintf(g_last_error, sizeof(g_last_error), "%s: %s", what, msg);
+}
+
+void count_launches(int64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
 int current_device()
 {
     int dev = 0;

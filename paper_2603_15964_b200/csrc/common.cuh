@@ -28,7 +28,9 @@ __device__ __forceinline__ double macc(double acc, double w, double v)
 
 // Host-side error bookkeeping (capi.cu).  The last error is per host thread.
 void set_last_error(const char *what, cudaError_t e);
+void set_last_error_text(const char *what, const char *msg);   // non-CUDA failures (NCCL, IPC)
 int launch_status(const char *what);
+void count_launches(int64_t k);       // kernels replayed by a graph launch
 
 // Device status reductions (rows.cu): *flag = 1 if any status[i] != LMEP_OK;
 // dst[i] = src[i] where dst[i] == LMEP_OK.
