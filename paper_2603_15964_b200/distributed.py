@@ -6,27 +6,37 @@ classes redundantly, or its own nodes' per-node rows) and advances its slab
 with the fused step kernels.  The only data exchange is the halo: before a
 launch that fuses k steps, each rank sends its first and last
 G = k * ext * max(row, n-1-row) nodes to its neighbours (periodic ring or
-open chain) with NCCL point-to-point over NVLink.  A deep halo (k > 1)
-trades a little redundant edge compute for k times fewer exchanges.
+open chain).  A deep halo (k > 1) trades a little redundant edge compute for
+k times fewer exchanges.
 
-The exchange is an object with one method, ``exchange(u_local, ghosts)``,
-so the same driver runs with
+The data plane is the library's communicator (``Comm`` = ``lmep_comm`` of
+include/lmep.h): NCCL send / receive pairs on the step stream, or peer stores
+into CUDA-IPC mailboxes; torch.distributed only carries the bootstrap bytes
+(the NCCL id, the IPC handles).  With a ``CommHalo`` exchanger a chunk is
 
-  * ``NcclHalo``   -- torch.distributed batch_isend_irecv (NCCL on GPUs,
-                      gloo on CPU for the host-side tests);
-  * ``LocalHalo``  -- P virtual shards inside one process (device copies),
-                      used to check sharded == unsharded on a single GPU.
+    fork -> halo exchange (side stream) || interior sub-slab (step stream)
+         -> join -> the two edge strips
+
+and, on the NCCL transport, the whole chunk is replayed from a CUDA graph
+(one graph per ping-pong direction).  Other exchangers share the driver:
+
+  * ``TorchHalo`` -- torch.distributed batch_isend_irecv (gloo on CPU for the
+                     host-side tests, NCCL through torch otherwise);
+  * ``LocalHalo`` -- P virtual shards inside one process (device copies),
+                     used to check sharded == unsharded on a single GPU.
 """
 
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 from . import _native as nat
 from . import _ops
-from .errors import InvalidConfig
+from .errors import InvalidConfig, NonFinite
 from .grid import Grid, as_stencil_set
 from .harvest import harvest_compact
 from .timestep import (Prepared, SchemeConfig, SemiLinearProblem, _bc_for, _etdrk4_bank,
@@ -48,13 +58,172 @@ def neighbours(rank: int, world: int, periodic: bool) -> tuple[int | None, int |
     return left, right
 
 
-class NcclHalo:
+class Comm:
+    """One rank's ``lmep_comm`` (include/lmep.h, "sharded runs")."""
+
+    def __init__(self, rank: int, world: int, periodic: bool, transport: str = "nccl",
+                 unique_id: bytes | None = None, max_width: int = 0):
+        self.rank, self.world, self.periodic, self.transport = rank, world, bool(periodic), transport
+        code = {"nccl": nat.COMM_NCCL, "peer": nat.COMM_PEER}[transport]
+        nat.device()
+        h = C.c_void_p()
+        idb = None
+        if code == nat.COMM_NCCL:
+            if unique_id is None or len(unique_id) != nat.COMM_ID_BYTES:
+                raise InvalidConfig("the NCCL transport needs rank 0's Comm.unique_id()")
+            idb = C.create_string_buffer(bytes(unique_id), nat.COMM_ID_BYTES)
+        nat.check(nat.lib().lmep_comm_init(C.byref(h), rank, world, int(bool(periodic)), code, idb,
+                                           int(max_width)), "lmep_comm_init")
+        self.h = h
+        l, r = C.c_int(), C.c_int()
+        nat.lib().lmep_comm_info(h, None, None, C.byref(l), C.byref(r), None)
+        self.left = None if l.value < 0 else l.value
+        self.right = None if r.value < 0 else r.value
+        self.side_stream = nat.lib().lmep_comm_side_stream(h)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(nat.COMM_ID_BYTES)
+        nat.check(nat.lib().lmep_comm_unique_id(buf), "lmep_comm_unique_id")
+        return buf.raw
+
+    def export(self) -> bytes:
+        buf = C.create_string_buffer(nat.COMM_BLOB_BYTES)
+        nat.check(nat.lib().lmep_comm_export(self.h, buf), "lmep_comm_export")
+        return buf.raw
+
+    def connect(self, blobs: list[bytes] | None) -> None:
+        raw = None
+        if blobs is not None:
+            if len(blobs) != self.world or any(len(b) != nat.COMM_BLOB_BYTES for b in blobs):
+                raise InvalidConfig("connect() needs one exported blob per rank")
+            raw = C.create_string_buffer(b"".join(blobs), self.world * nat.COMM_BLOB_BYTES)
+        nat.check(nat.lib().lmep_comm_connect(self.h, raw), "lmep_comm_connect")
+
+    def exchange(self, fields, width: int, gls, grs, stream: int | None = None) -> None:
+        """Ghost cells of every field (equal-length device vectors) in one call."""
+        k = len(fields)
+        nloc = fields[0].numel()
+        fp = (C.c_void_p * k)(*[f.data_ptr() for f in fields])
+        lp = (C.c_void_p * k)(*[g.data_ptr() for g in gls])
+        rp = (C.c_void_p * k)(*[g.data_ptr() for g in grs])
+        s = nat.stream_handle() if stream is None else stream
+        nat.check(nat.lib().lmep_halo_exchange(self.h, k, fp, nloc, int(width), lp, rp, s),
+                  "lmep_halo_exchange")
+
+    def gather(self, u: torch.Tensor, counts, out: torch.Tensor | None, root: int = 0) -> None:
+        cn = (C.c_int64 * self.world)(*[int(c) for c in counts])
+        nat.check(nat.lib().lmep_comm_gather(self.h, u.data_ptr(), cn, nat.ptr(out), root,
+                                             nat.stream_handle()), "lmep_comm_gather")
+
+    def flag_max(self, flag: torch.Tensor) -> None:
+        nat.check(nat.lib().lmep_comm_flag_max(self.h, flag.data_ptr(), flag.numel(),
+                                               nat.stream_handle()), "lmep_comm_flag_max")
+
+    def fork(self) -> None:
+        nat.check(nat.lib().lmep_comm_fork(self.h, nat.stream_handle()), "lmep_comm_fork")
+
+    def join(self) -> None:
+        nat.check(nat.lib().lmep_comm_join(self.h, nat.stream_handle()), "lmep_comm_join")
+
+    def close(self) -> None:
+        if self.h is not None:
+            nat.lib().lmep_comm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Graph:
+    """A captured chunk (``lmep_graph``): record with ``with Graph.capture() as g``."""
+
+    def __init__(self):
+        self.h = None
+
+    class _Capture:
+        def __init__(self, g):
+            self.g = g
+
+        def __enter__(self):
+            self.s = nat.stream_handle()
+            nat.check(nat.lib().lmep_graph_begin(self.s), "lmep_graph_begin")
+            return self.g
+
+        def __exit__(self, et, ev, tb):
+            h = C.c_void_p()
+            st = nat.lib().lmep_graph_end(self.s, C.byref(h))
+            if et is None:
+                nat.check(st, "lmep_graph_end")
+                self.g.h = h
+            elif st == 0:
+                nat.lib().lmep_graph_destroy(h)
+            return False
+
+    @classmethod
+    def capture(cls):
+        return cls._Capture(cls())
+
+    def launch(self) -> None:
+        nat.check(nat.lib().lmep_graph_launch(self.h, nat.stream_handle()), "lmep_graph_launch")
+
+    def __del__(self):
+        try:
+            if self.h is not None:
+                nat.lib().lmep_graph_destroy(self.h)
+        except Exception:
+            pass
+
+
+def make_comm(rank: int, world: int, periodic: bool, transport: str = "nccl", group=None,
+              max_width: int = 0) -> Comm:
+    """Bootstrap a ``Comm`` over a torch.distributed group: the group only
+    carries the NCCL id (128 bytes from rank 0) or the ranks' IPC handles."""
+    import torch.distributed as dist
+    multi = world > 1
+    if transport == "nccl":
+        box = [Comm.unique_id() if rank == 0 else None]
+        if multi:
+            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group else 0,
+                                       group=group)
+        return Comm(rank, world, periodic, "nccl", unique_id=box[0])
+    c = Comm(rank, world, periodic, "peer", max_width=max_width)
+    blobs = [c.export()]
+    if multi:
+        blobs = [None] * world
+        dist.all_gather_object(blobs, c.export(), group=group)
+    c.connect(blobs)
+    return c
+
+
+class CommHalo:
+    """Halo exchange through the library communicator (NCCL or peer stores)."""
+
+    def __init__(self, comm: Comm):
+        self.comm = comm
+        self.rank, self.world = comm.rank, comm.world
+        self.left, self.right = comm.left, comm.right
+
+    def exchange_many(self, fields, width, gls, grs, stream=None) -> None:
+        if fields[0].numel() < width:
+            raise InvalidConfig(f"slab of {fields[0].numel()} nodes is narrower than the halo {width}")
+        self.comm.exchange(fields, width, gls, grs, stream)
+
+    def exchange(self, u, gl, gr) -> None:
+        self.exchange_many([u], gl.numel(), [gl], [gr])
+
+
+class TorchHalo:
     """Halo exchange over torch.distributed point-to-point (one group call).
 
     Posting order per rank: send right edge -> right, recv left ghosts <- left,
     send left edge -> left, recv right ghosts <- right.  Messages between a
     pair match in posting order, which also makes the 2-rank periodic ring
-    (left == right) come out right.
+    (left == right) come out right.  Device slabs on a gloo group are staged
+    through the host.
     """
 
     def __init__(self, rank: int, world: int, periodic: bool, group=None):
@@ -66,17 +235,29 @@ class NcclHalo:
         G = gl.numel()
         if u.numel() < G:
             raise InvalidConfig(f"slab of {u.numel()} nodes is narrower than the halo {G}")
+        staged = u.is_cuda and dist.get_backend(self.group) == "gloo"
+        edge = (lambda t: t.cpu()) if staged else (lambda t: t.contiguous())
+        rl = torch.empty(G, dtype=u.dtype) if staged else gl
+        rr = torch.empty(G, dtype=u.dtype) if staged else gr
         ops = []
         if self.right is not None:
-            ops.append(dist.P2POp(dist.isend, u[u.numel() - G:].contiguous(), self.right, self.group))
+            ops.append(dist.P2POp(dist.isend, edge(u[u.numel() - G:]), self.right, self.group))
         if self.left is not None:
-            ops.append(dist.P2POp(dist.irecv, gl, self.left, self.group))
-            ops.append(dist.P2POp(dist.isend, u[:G].contiguous(), self.left, self.group))
+            ops.append(dist.P2POp(dist.irecv, rl, self.left, self.group))
+            ops.append(dist.P2POp(dist.isend, edge(u[:G]), self.left, self.group))
         if self.right is not None:
-            ops.append(dist.P2POp(dist.irecv, gr, self.right, self.group))
+            ops.append(dist.P2POp(dist.irecv, rr, self.right, self.group))
         if ops:
             for r in dist.batch_isend_irecv(ops):
                 r.wait()
+        if staged:
+            if self.left is not None:
+                gl.copy_(rl)
+            if self.right is not None:
+                gr.copy_(rr)
+
+
+NcclHalo = TorchHalo          # the name earlier callers used
 
 
 class LocalHalo:
@@ -117,11 +298,17 @@ def _ext(scheme: str, nl: int) -> int:
 
 
 class ShardedStepper:
-    """Advance one slab of a run (the sharded counterpart of timestep.Stepper)."""
+    """Advance one slab of a run (the sharded counterpart of timestep.Stepper).
+
+    u and the multistep history ping-pong between two fixed buffers each, so a
+    chunk (exchange + fused k-step launch) can be replayed from a CUDA graph.
+    ``force_halo`` makes a single periodic rank exchange with itself through
+    the communicator (the real data path on one GPU)."""
 
     def __init__(self, grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
                  delta_t: float, rank: int, world: int, exchanger, *, exact: bool = True,
-                 ksteps: int | None = None, tuning=None):
+                 ksteps: int | None = None, tuning=None, overlap: bool = True,
+                 graph: bool | None = None, force_halo: bool = False):
         sset = as_stencil_set(grid, stencils)
         self.sset, self.rank, self.world = sset, rank, world
         self.exact, self.tuning = exact, tuning
@@ -130,26 +317,38 @@ class ShardedStepper:
         reach = max(sset.row, sset.n - 1 - sset.row)
         ext = _ext(scheme.kind, nl)
         per_node = _is_per_node(grid, problem)
+        self.sharded = world > 1 or (force_halo and grid.periodic)
         # periodic per-node linear rows: the shard also harvests its halo
         # nodes' rows (no communication), so k steps fuse per exchange
         pad_ok = per_node and scheme.kind == "linear" and grid.periodic
         if ksteps is None:
             ksteps = max(1, min(16, nloc // (4 * ext * max(reach, 1))))
-        if per_node and scheme.kind == "linear" and world > 1 and not pad_ok:
+        if per_node and scheme.kind == "linear" and self.sharded and not pad_ok:
             ksteps = 1                      # non-periodic per-node rows: one step per exchange
-        if world == 1:
+        if not self.sharded:
             ksteps = 1 << 30                # no halo: the library plans the launches
-        if per_node and scheme.kind != "linear" and world > 1:
+        if per_node and scheme.kind != "linear" and self.sharded:
             raise InvalidConfig("sharded ETD schemes need shared or class rows")
-        width = ksteps * ext * reach if world > 1 else 0
-        if world > 1 and width > nloc:
+        width = ksteps * ext * reach if self.sharded else 0
+        if self.sharded and width > nloc:
             raise InvalidConfig(f"slab of {nloc} nodes narrower than the halo {width}")
         self.plan = SlabPlan(off, nloc, width, ksteps)
-        pad = ksteps * reach if (pad_ok and world > 1 and ksteps > 1) else 0
+        pad = ksteps * reach if (pad_ok and self.sharded and ksteps > 1) else 0
         self.prep = _prepare_shard(grid, sset, problem, scheme, delta_t, off, nloc, pad)
         self.ex = exchanger
+        # interior / edge split and graph replay need the library communicator
+        # and kernels whose sub-slabs keep their leading dimensions
+        comm_ex = isinstance(exchanger, CommHalo)
+        self.overlap = bool(overlap and comm_ex and self.sharded and not per_node and
+                            scheme.kind in ("linear", "etdrk4"))
+        if graph is None:
+            graph = comm_ex and exchanger.comm.transport == "nccl"
+        self.graph = bool(graph and comm_ex and self.sharded and
+                          exchanger.comm.transport == "nccl")
+        self._graphs: dict = {}
+        self._seen: set = set()
         dev = nat.device()
-        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.flag = torch.zeros(4, dtype=torch.int32, device=dev)
         G = max(width, 1)
         nh = max(scheme.s - 1, 1) if scheme.kind == "etd-multistep" else 1
         self.gl = torch.zeros(G, dtype=torch.float64, device=dev)
@@ -157,8 +356,11 @@ class ShardedStepper:
         self.ql = torch.zeros(nh * G, dtype=torch.float64, device=dev)   # [s-1][width] ghosts
         self.qr = torch.zeros(nh * G, dtype=torch.float64, device=dev)
         self.u = None
+        self._out = None
         self.hist = None
+        self._hout = None
         self.done = 0
+        self._warm_done = 0
         # ping-pong scratch for multi-launch calls (u and the etd2 history)
         self.scratch = torch.empty((nh + 1) * nloc, dtype=torch.float64, device=dev)
 
@@ -167,7 +369,14 @@ class ShardedStepper:
         """Slice the (closed) global initial data for this slab."""
         u = _ops.dev_f64(u0_global)
         u = close_initial(u, self.sset, self.prep.bc)
-        self.u = u[self.plan.off:self.plan.off + self.plan.nloc].contiguous()
+        self.set_local(u[self.plan.off:self.plan.off + self.plan.nloc])
+
+    def set_local(self, u_local: torch.Tensor) -> None:
+        """This slab's initial values (copied: inputs are never written)."""
+        self.u = u_local.clone().contiguous()
+        self._out = torch.empty_like(self.u)
+        self._graphs.clear()
+        self._seen.clear()
 
     def _width(self, k, scheme=None):
         ext = _ext(scheme or self.prep.scheme, self.prep.nl)
@@ -177,60 +386,125 @@ class ShardedStepper:
         return max(self.prep.s - 1, 1) if self.prep.scheme == "etd-multistep" else 1
 
     def _halo(self, k):
-        if self.world == 1:
+        if not self.sharded:
             return None
         w = max(self._width(k), 1)
         nh = self._nh()
         return (self.gl[:w], self.gr[:w], self.ql[:nh * w], self.qr[:nh * w], w)
 
-    def _exchange(self, k, hist=False):
-        if self.world == 1:
+    def _hist_fields(self):
+        p = self.prep
+        if p.scheme == "etd-multistep" and p.s > 1 and self.hist is not None:
+            return [self.hist[i] for i in range(self.hist.shape[0])]
+        return []
+
+    def exchange_phase(self, k: int, stream=None) -> None:
+        """Ghost cells of u (and of the multistep history) for a k-step launch."""
+        if not self.sharded:
             return
         h = self._halo(k)
         w = h[4]
-        if isinstance(self.ex, LocalHalo):
-            self.ex.which = "hist" if hist else "u"
-        if hist:
-            for i in range(self.hist.shape[0]):
-                if isinstance(self.ex, LocalHalo):
-                    self.ex.which = ("hist", i)
-                self.ex.exchange(self.hist[i], h[2][i * w:(i + 1) * w], h[3][i * w:(i + 1) * w])
+        hf = self._hist_fields()
+        if hasattr(self.ex, "exchange_many"):
+            fields = [self.u] + hf
+            gls = [h[0]] + [h[2][i * w:(i + 1) * w] for i in range(len(hf))]
+            grs = [h[1]] + [h[3][i * w:(i + 1) * w] for i in range(len(hf))]
+            self.ex.exchange_many(fields, w, gls, grs, stream)
+            return
+        local = isinstance(self.ex, LocalHalo)
+        if local:
+            self.ex.which = "u"
+        self.ex.exchange(self.u, h[0], h[1])
+        for i, f in enumerate(hf):
+            if local:
+                self.ex.which = ("hist", i)
+            self.ex.exchange(f, h[2][i * w:(i + 1) * w], h[3][i * w:(i + 1) * w])
+
+    def _tuning(self, k):
+        if not self.sharded:
+            return self.tuning              # single shard: library heuristics
+        return {**(self.tuning or {}), "ksteps": k}
+
+    def _launch(self, k: int) -> None:
+        """The k-step launch of the whole slab: self.u -> self._out (no swap)."""
+        p = self.prep
+        kw = dict(bc=p.bc, nl=p.nl, exact=self.exact, tuning=self._tuning(k), flag=self.flag[0:1],
+                  off=self.plan.off, nloc=self.plan.nloc, halo=self._halo(k),
+                  scratch=self.scratch, out=self._out)
+        if p.scheme == "linear":
+            _ops.step(nat.SCH_LIN, p.bank, self.u, k, **kw)
+        elif p.scheme == "etdrk4":
+            _ops.step(nat.SCH_ETDRK4, p.bank, self.u, k, **kw)
         else:
-            self.ex.exchange(self.u, h[0], h[1])
+            if self.hist is None:
+                raise InvalidConfig("call warm_up() before multistep chunks")
+            _ops.step(nat.SCH_ETD2, p.bank, self.u, k, hist=self.hist, delta_t=p.delta_t,
+                      etd_order=p.s, hist_out=self._hout, **kw)
+
+    def _swap(self) -> None:
+        self.u, self._out = self._out, self.u
+        if self.prep.scheme == "etd-multistep" and self.prep.s > 1:
+            self.hist, self._hout = self._hout, self.hist
+
+    def _can_split(self, k: int) -> bool:
+        w = self._width(k)
+        return self.overlap and w >= 1 and self.plan.nloc >= 3 * w
+
+    def _enqueue_split(self, k: int) -> None:
+        """fork -> exchange on the side stream || interior sub-slab on the step
+        stream -> join -> the two edge strips.  The interior's ghosts are this
+        slab's own edge values, so it does not wait for the neighbours."""
+        p, cm = self.prep, self.ex.comm
+        w, nloc, off = self._width(k), self.plan.nloc, self.plan.off
+        u, out = self.u, self._out
+        sch = nat.SCH_LIN if p.scheme == "linear" else nat.SCH_ETDRK4
+        kw = dict(bc=p.bc, nl=p.nl, exact=self.exact, tuning=self._tuning(k))
+        cm.fork()
+        self.exchange_phase(k, stream=cm.side_stream)
+        _ops.step(sch, p.bank, u[w:nloc - w], k, out=out[w:nloc - w], off=off + w,
+                  nloc=nloc - 2 * w, halo=(u[:w], u[nloc - w:], None, None, w),
+                  flag=self.flag[1:2], **kw)
+        cm.join()
+        gl = self.gl[:w] if self.ex.left is not None else None
+        gr = self.gr[:w] if self.ex.right is not None else None
+        _ops.step(sch, p.bank, u[:w], k, out=out[:w], off=off, nloc=w,
+                  halo=(gl, u[w:2 * w], None, None, w), flag=self.flag[2:3], **kw)
+        _ops.step(sch, p.bank, u[nloc - w:], k, out=out[nloc - w:], off=off + nloc - w, nloc=w,
+                  halo=(u[nloc - 2 * w:nloc - w], gr, None, None, w), flag=self.flag[3:4], **kw)
+
+    def _enqueue(self, k: int) -> None:
+        if self._can_split(k):
+            self._enqueue_split(k)
+        else:
+            self.exchange_phase(k)
+            self._launch(k)
 
     def step_chunk(self, k: int) -> None:
         """k <= plan.ksteps steps with one halo exchange.  With LocalHalo the
         caller must run exchange_phase on all shards before compute_phase."""
-        self.exchange_phase(k)
-        self.compute_phase(k)
-
-    def exchange_phase(self, k: int) -> None:
-        p = self.prep
-        self._exchange(k)
-        if p.scheme == "etd-multistep" and self.hist is not None:
-            self._exchange(k, hist=True)
-
-    def _tuning(self, k):
-        if self.world == 1:
-            return self.tuning              # single shard: library heuristics
-        return {**(self.tuning or {}), "ksteps": k}
+        if self.graph and nat.stream_handle() != 0:     # the legacy stream cannot be captured
+            # one graph per (k, ping-pong direction): run a chunk shape once
+            # eagerly (NCCL connects, kernels get their attributes), capture it
+            # the second time it comes up, replay it from then on
+            key = (k, self.u.data_ptr(), 0 if self.hist is None else self.hist.data_ptr())
+            g = self._graphs.get(key)
+            if g is None and key in self._seen:
+                with Graph.capture() as g:
+                    self._enqueue(k)
+                self._graphs[key] = g
+            if g is not None:
+                g.launch()
+            else:
+                self._seen.add(key)
+                self._enqueue(k)
+        else:
+            self._enqueue(k)
+        self._swap()
+        self.done += k
 
     def compute_phase(self, k: int) -> None:
-        p = self.prep
-        kw = dict(bc=p.bc, nl=p.nl, exact=self.exact, tuning=self._tuning(k), flag=self.flag,
-                  off=self.plan.off, nloc=self.plan.nloc, halo=self._halo(k),
-                  scratch=self.scratch)
-        if p.scheme == "linear":
-            self.u = _ops.step(nat.SCH_LIN, p.bank, self.u, k, **kw)
-        elif p.scheme == "etdrk4":
-            self.u = _ops.step(nat.SCH_ETDRK4, p.bank, self.u, k, **kw)
-        else:
-            if self.hist is None:
-                raise InvalidConfig("call warm_up() before multistep chunks")
-            self.u, q = _ops.step(nat.SCH_ETD2, p.bank, self.u, k, hist=self.hist,
-                                  delta_t=p.delta_t, etd_order=p.s, **kw)
-            if p.s > 1:
-                self.hist = q
+        self._launch(k)
+        self._swap()
         self.done += k
 
     # ETD multistep warm-up (timestep.py:375-378): s-1 ETDRK4 steps, each
@@ -242,7 +516,8 @@ class ShardedStepper:
         if self.hist is None:
             self.hist = torch.zeros((self._nh(), self.u.numel()), dtype=torch.float64,
                                     device=self.u.device)
-        if self.world == 1:
+            self._hout = torch.empty_like(self.hist)
+        if not self.sharded:
             return
         w = self._width(1, "etdrk4")
         dev = self.u.device
@@ -258,16 +533,18 @@ class ShardedStepper:
         if i > 0:
             self.hist[1:i + 1] = self.hist[0:i].clone()
         halo = None
-        if self.world > 1:
+        if self.sharded:
             w = self._width(1, "etdrk4")
             halo = (self.wl, self.wr, self.wl, self.wr, w)
-        kw = dict(bc=p.bc, nl=p.nl, exact=self.exact, tuning=self._tuning(1), flag=self.flag,
-                  off=self.plan.off, nloc=self.plan.nloc, halo=halo)
-        self.u = _ops.step(nat.SCH_ETDRK4, p.warm, self.u, 1, nl0_out=self.hist[0], **kw)
+        kw = dict(bc=p.bc, nl=p.nl, exact=self.exact, tuning=self._tuning(1), flag=self.flag[0:1],
+                  off=self.plan.off, nloc=self.plan.nloc, halo=halo, out=self._out)
+        _ops.step(nat.SCH_ETDRK4, p.warm, self.u, 1, nl0_out=self.hist[0], **kw)
+        self.u, self._out = self._out, self.u
         self.done += 1
+        self._warm_done = i + 1
 
     def nonfinite(self) -> bool:
-        return bool(self.flag.item())
+        return bool(self.flag.max().item())
 
 
 def _is_per_node(grid: Grid, problem: SemiLinearProblem) -> bool:
@@ -345,80 +622,149 @@ def run_virtual_shards(grid: Grid, stencils, problem: SemiLinearProblem, scheme:
 
 
 def run_sharded(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
-                delta_t: float, t_final: float, *, group=None, exact: bool = True,
-                ksteps: int | None = None):
-    """``timestep.run`` over all ranks of a torch.distributed group (one GPU per
-    rank): per-rank harvest, slab stepping with NCCL halo exchange, and the
-    final state gathered on rank 0.  Returns a SimulationResult (snapshots:
-    initial and final state) on rank 0 and None elsewhere."""
-    import time
+                delta_t: float, t_final: float, snapshot_stride: float | None = None, *,
+                group=None, exact: bool = True, ksteps: int | None = None,
+                transport: str = "nccl", overlap: bool = True, graph: bool | None = None):
+    """``timestep.run`` (timestep.py:255-394) over all ranks of a
+    torch.distributed group, one GPU per rank: per-rank harvest, slab stepping
+    with halo exchange, snapshots gathered on rank 0.
 
-    import numpy as np
+    transport: "nccl" / "peer" = the library communicator (the group only
+    carries its bootstrap bytes), "torch" = torch.distributed point-to-point
+    (gloo groups stage the halos through the host).  Returns a
+    SimulationResult on rank 0 and None elsewhere; every rank raises NonFinite
+    when the run blows up (rank 0's carries the last finite snapshot, as
+    timestep.py:345-348)."""
+    dev = nat.device()
+    cur = torch.cuda.current_stream(dev)
+    if cur.cuda_stream == 0:
+        # graphs cannot be captured on the legacy default stream: run on a
+        # stream of our own, ordered after the caller's work
+        own = torch.cuda.Stream(dev)
+        own.wait_stream(cur)
+        with torch.cuda.stream(own):
+            res = run_sharded(grid, stencils, problem, scheme, delta_t, t_final, snapshot_stride,
+                              group=group, exact=exact, ksteps=ksteps, transport=transport,
+                              overlap=overlap, graph=graph)
+        cur.wait_stream(own)
+        return res
     import torch.distributed as dist
 
     from .timestep import SimulationResult, _steps_for
 
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    multi = dist.is_available() and dist.is_initialized()
+    rank = dist.get_rank(group) if multi else 0
+    world = dist.get_world_size(group) if multi else 1
     if t_final <= 0 or delta_t <= 0:
         raise InvalidConfig("dt and t_final must be positive")
     steps = _steps_for(t_final, delta_t, "final time")
-    dev = nat.device()
-    torch.cuda.synchronize(dev)
-    t0 = time.perf_counter_ns()
-    st = ShardedStepper(grid, stencils, problem, scheme, delta_t, rank, world,
-                        NcclHalo(rank, world, grid.periodic, group), exact=exact, ksteps=ksteps)
-    torch.cuda.synchronize(dev)
-    harvest_ns = time.perf_counter_ns() - t0
-    st.set_initial(problem.initial)
-    t0 = time.perf_counter_ns()
-    advance_all(st, steps)
-    torch.cuda.synchronize(dev)
-    step_ns = time.perf_counter_ns() - t0
-    u = gather_slabs(st, group)
-    if world > 1:
-        bad = torch.tensor([int(st.nonfinite())], device=dev)
-        dist.all_reduce(bad, group=group)
-        nonfinite = bool(bad.item())
+    if snapshot_stride is None:
+        snap_every = steps
     else:
-        nonfinite = st.nonfinite()
+        snap_every = _steps_for(snapshot_stride, delta_t, "snapshot stride")
+        if snap_every == 0:
+            raise InvalidConfig("snapshot stride must be at least one step")
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    torch.cuda.synchronize(dev)
+    ev[0].record(cur)
+    comm = None
+    if world == 1:
+        ex = None
+    elif transport == "torch":
+        ex = TorchHalo(rank, world, grid.periodic, group)
+    else:
+        # mailbox capacity (peer): the widest halo any chunk can ask for
+        sset = as_stencil_set(grid, stencils)
+        reach = max(sset.row, sset.n - 1 - sset.row)
+        comm = make_comm(rank, world, grid.periodic, transport, group,
+                         max_width=16 * 8 * max(reach, 1))
+        ex = CommHalo(comm)
+    st = ShardedStepper(grid, stencils, problem, scheme, delta_t, rank, world, ex, exact=exact,
+                        ksteps=ksteps, overlap=overlap, graph=graph)
+    ev[1].record(cur)
+    st.set_initial(problem.initial)
+    N = st.sset.N
+    counts = [partition(N, world, r)[1] for r in range(world)]
+    nsnap = 1 + (-(-steps // snap_every) if snap_every else 0)
+    snaps = torch.empty((nsnap, N), dtype=torch.float64, pin_memory=True) if rank == 0 else None
+    gbuf = torch.empty(N, dtype=torch.float64, device=dev) if (rank == 0 and world > 1) else None
+
+    def snapshot(i):
+        u = gather_slabs(st, group, comm=comm, counts=counts, out=gbuf)
+        if rank == 0:
+            snaps[i].copy_(u, non_blocking=True)
+
+    def any_nonfinite() -> bool:
+        if world == 1:
+            return st.nonfinite()
+        bad = st.flag.max().reshape(1).to(torch.int32)
+        if comm is not None and comm.transport == "nccl":
+            comm.flag_max(bad)
+            return bool(bad.item())
+        box = [None] * world
+        dist.all_gather_object(box, int(bad.item()), group=group)
+        return any(box)
+
+    times = [0.0]
+    snapshot(0)
+    step_ns, done = 0, 0
+    try:
+        while done < steps:
+            k = min(snap_every, steps - done)
+            ev[2].record(cur)
+            advance_all(st, k)
+            ev[3].record(cur)
+            cur.synchronize()
+            step_ns += int(ev[2].elapsed_time(ev[3]) * 1e6)
+            done += k
+            if any_nonfinite():
+                state = snaps[len(times) - 1].numpy().copy() if rank == 0 else None
+                raise NonFinite("time integration blew up", state=state, time=times[-1])
+            times.append(done * delta_t)
+            snapshot(len(times) - 1)
+        cur.synchronize()
+    finally:
+        harvest_ns = int(ev[0].elapsed_time(ev[1]) * 1e6)
+        st._graphs.clear()
+        if comm is not None:
+            comm.close()
     if rank != 0:
         return None
-    u0 = np.asarray(problem.initial.cpu() if isinstance(problem.initial, torch.Tensor)
-                    else problem.initial, dtype=np.float64)
-    if nonfinite:
-        from .errors import NonFinite
-        raise NonFinite("time integration blew up", state=u0, time=0.0)
-    return SimulationResult(times=np.array([0.0, steps * delta_t]),
-                            snapshots=np.stack([u0, _ops.to_host(u)]), steps=steps,
+    return SimulationResult(times=np.array(times), snapshots=snaps.numpy(), steps=steps,
                             harvest_ns=harvest_ns, step_ns=step_ns)
 
 
 def advance_all(st: ShardedStepper, steps: int) -> None:
-    """All of a rank's steps: (warm-up,) then chunks of plan.ksteps, one halo
-    exchange each."""
-    done = 0
-    if st.prep.scheme == "etd-multistep" and st.hist is None:
-        nw = min(st.warm_up_steps(), steps)
-        if nw == 0:
+    """`steps` more steps of a rank: (warm-up,) then chunks of plan.ksteps, one
+    halo exchange each."""
+    todo = steps
+    if st.prep.scheme == "etd-multistep":
+        if st.hist is None and st.warm_up_steps() == 0:
             st.warm_up_exchange()             # allocates the (unused) history
-        for i in range(nw):
+        while st._warm_done < st.warm_up_steps() and todo > 0:
             st.warm_up_exchange()
-            st.warm_up_compute(i)
-        done = st.done
-    while done < steps:
-        k = min(st.plan.ksteps, steps - done)
+            st.warm_up_compute(st._warm_done)
+            todo -= 1
+    while todo > 0:
+        k = min(st.plan.ksteps, todo)
         st.step_chunk(k)
-        done += k
+        todo -= k
 
 
-def gather_slabs(st: ShardedStepper, group=None) -> torch.Tensor | None:
-    """Concatenate the slabs on rank 0 (padded all_gather: slab sizes differ by <= 1)."""
+def gather_slabs(st: ShardedStepper, group=None, *, comm: Comm | None = None, counts=None,
+                 out: torch.Tensor | None = None) -> torch.Tensor | None:
+    """The global state on rank 0 (None elsewhere).  With an NCCL communicator
+    the slabs go straight into `out` on the device; otherwise a padded
+    all_gather of the group (through the host on gloo groups)."""
     import torch.distributed as dist
     if st.world == 1:
         return st.u
+    if comm is not None and comm.transport == "nccl":
+        comm.gather(st.u, counts, out if st.rank == 0 else None, 0)
+        return out if st.rank == 0 else None
     m = -(-st.sset.N // st.world)
-    buf = torch.zeros(m, dtype=torch.float64, device=st.u.device)
+    host = dist.get_backend(group) == "gloo"
+    buf = torch.zeros(m, dtype=torch.float64, device="cpu" if host else st.u.device)
     buf[:st.plan.nloc] = st.u
     parts = [torch.empty_like(buf) for _ in range(st.world)]
     dist.all_gather(parts, buf, group=group)

@@ -138,6 +138,158 @@ def test_virtual_shards_bitwise(P):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_comm_self_exchange(transport):
+    """A periodic 1-rank ring exchanges with itself through the library
+    communicator: the real NCCL group / peer-store path on one GPU."""
+    from paper_2603_15964_b200.distributed import Comm
+    if transport == "nccl":
+        c = Comm(0, 1, True, "nccl", unique_id=Comm.unique_id())
+    else:
+        c = Comm(0, 1, True, "peer", max_width=64)
+        c.connect([c.export()])
+    assert (c.left, c.right) == (0, 0)
+    dev = torch.device("cuda")
+    nloc, W = 1000, 37
+    f = [torch.arange(nloc, dtype=torch.float64, device=dev) * (i + 1) + 0.5 for i in range(3)]
+    for rep in range(5):                       # several exchanges: both mailbox halves
+        gl = [torch.full((W,), -1.0, dtype=torch.float64, device=dev) for _ in f]
+        gr = [torch.full((W,), -1.0, dtype=torch.float64, device=dev) for _ in f]
+        c.exchange(f, W, gl, gr)
+        torch.cuda.synchronize()
+        for i in range(3):
+            assert torch.equal(gl[i], f[i][nloc - W:]) and torch.equal(gr[i], f[i][:W]), (rep, i)
+        f = [x + 1.0 for x in f]
+    if transport == "nccl":
+        out = torch.empty(nloc, dtype=torch.float64, device=dev)
+        c.gather(f[0], [nloc], out, 0)
+        flag = torch.tensor([0, 1, 0], dtype=torch.int32, device=dev)
+        c.flag_max(flag)
+        torch.cuda.synchronize()
+        assert torch.equal(out, f[0]) and flag.tolist() == [0, 1, 0]
+    # a chain end has no neighbours: nothing moves
+    e = Comm(0, 1, False, "peer", max_width=8)
+    e.connect(None)
+    assert (e.left, e.right) == (None, None)
+    e.close()
+    c.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_self_ring_stepper_bitwise(transport):
+    """ShardedStepper on a 1-rank periodic ring with forced halos through the
+    communicator -- interior / edge split on two streams, chunks replayed from
+    CUDA graphs on NCCL -- is bit-identical to the unsharded stepper."""
+    from paper_2603_15964_b200 import _ops
+    from paper_2603_15964_b200.distributed import Comm, CommHalo, ShardedStepper, advance_all
+    from paper_2603_15964_b200.timestep import Stepper, prepare
+    if transport == "nccl":
+        c = Comm(0, 1, True, "nccl", unique_id=Comm.unique_id())
+    else:
+        c = Comm(0, 1, True, "peer", max_width=4096)
+        c.connect([c.export()])
+    try:
+        for name, g, st, prob, scheme, dt, steps in _cases():
+            if not g.periodic:
+                continue
+            ref = Stepper(prepare(g, st, prob, scheme, dt), _ops.dev_f64(prob.initial))
+            ref.advance(5 * steps + 3)
+            for k in (None, 2):
+                s = ShardedStepper(g, st, prob, scheme, dt, 0, 1, CommHalo(c), ksteps=k,
+                                   force_halo=True)
+                assert s.sharded and s.plan.width > 0
+                s.set_initial(prob.initial)
+                own = torch.cuda.Stream()               # graphs need a non-default stream
+                own.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(own):
+                    advance_all(s, 5 * steps + 3)
+                torch.cuda.synchronize()
+                assert torch.equal(s.u, ref.u), (name, k, float((s.u - ref.u).abs().max()))
+                if transport == "nccl" and k == 2:
+                    assert len(s._graphs) == 2, name           # both ping-pong directions replayed
+                assert not s.nonfinite()
+                s._graphs.clear()
+    finally:
+        c.close()
+
+
+def _rank_main(rank, world, port, transport, q):
+    """One rank of the 2-process runs below; both ranks drive cuda:0."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ.setdefault("LMEP_PEER_TIMEOUT_S", "60")
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2603_15964_b200 as lx
+        from paper_2603_15964_b200.distributed import run_sharded
+        from paper_2603_15964_b200.errors import NonFinite
+        torch.cuda.set_device(0)
+        res = {}
+        for name, g, st, prob, scheme, dt, steps in _cases():
+            if name in ("c2-etd1", "c2-etd5", "c5-rowscaled"):
+                continue
+            T = (3 * steps + 1) * dt
+            stride = steps * dt
+            a = run_sharded(g, st, prob, scheme, dt, T, stride, transport=transport)
+            if rank == 0:
+                b = lx.run(g, st, prob, scheme, dt, T, stride)
+                res[name] = (bool(np.array_equal(a.snapshots, b.snapshots)),
+                             bool(np.array_equal(a.times, b.times)), a.steps == b.steps,
+                             a.harvest_ns > 0 and a.step_ns > 0)
+        # blow-up: every rank raises; rank 0 carries the last finite snapshot, as run()
+        name, g, st, prob, scheme, dt, steps = [c for c in _cases() if c[0] == "c2-etd2"][0]
+        bad = 400.0 * dt
+        try:
+            run_sharded(g, st, prob, scheme, bad, 40 * bad, 10 * bad, transport=transport)
+            res["blowup"] = "no error"
+        except NonFinite as e:
+            if rank == 0:
+                try:
+                    lx.run(g, st, prob, scheme, bad, 40 * bad, 10 * bad)
+                    res["blowup"] = "run() did not raise"
+                except NonFinite as e2:
+                    res["blowup"] = (bool(np.array_equal(e.state, e2.state)), e.time == e2.time)
+            else:
+                res["blowup"] = (e.state is None,)
+        q.put((rank, res))
+    except Exception as e:                                      # noqa: BLE001
+        import traceback
+        q.put((rank, {"error": traceback.format_exc()}))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("transport", ["peer", "torch"])
+def test_run_sharded_two_processes(transport):
+    """run_sharded over two processes (both on cuda:0; the peer transport moves
+    the halos through CUDA-IPC mailboxes, "torch" stages them through a gloo
+    group) reproduces run() bit for bit: every snapshot, times, step count, and
+    the NonFinite state of a blown-up run."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, transport, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    try:
+        out = dict(q.get(timeout=420) for _ in range(2))
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    for r in (0, 1):
+        assert "error" not in out[r], out[r]["error"]
+    r0 = out[0]
+    for name in ("c1-linear", "c5-pernode", "c4-neumann", "c3-kdv", "c2-etd2", "c2-etd3"):
+        assert r0[name] == (True, True, True, True), (name, r0[name])
+    assert r0["blowup"] == (True, True), r0["blowup"]
+    assert out[1]["blowup"] == (True,)
+
+
+@pytest.mark.gpu
 def test_run_sharded_single_rank_nccl():
     """The NCCL entry point end to end on a 1-rank group matches run()."""
     import paper_2603_15964_b200 as lx
