@@ -244,7 +244,7 @@ class C5:
         self.last = {}
 
     def device_pass(self):
-        from paper_2603_15964_b200.distributed import NcclHalo, ShardedStepper, advance_all
+        from paper_2603_15964_b200.distributed import ShardedStepper, advance_all
         e0, e1, e2 = self.ev
         from paper_2603_15964_b200 import _ops
         e0.record()
@@ -252,14 +252,23 @@ class C5:
         # harvest and the steps: the host enqueues the steps while it runs)
         with _ops.deferred_status_checks() as pending:
             st = ShardedStepper(self.grid, self.sset, self.prob, self.scheme, self.w.delta_t,
-                                self.rank, self.world, NcclHalo(self.rank, self.world, True),
-                                exact=self.exact)
+                                self.rank, self.world, self.halo(), exact=self.exact)
         e1.record()
-        st.u = self.u0[self.off:self.off + self.nloc].clone()
+        st.set_local(self.u0[self.off:self.off + self.nloc])
         advance_all(st, self.w.steps)
         e2.record()
         self.last = {"stepper": st, "pending": pending}
         return st.u
+
+    def halo(self):
+        """The halo exchanger of a sharded pass: the library communicator (NCCL
+        send / receive on the step stream, lmep_comm), made once per rank."""
+        if self.world == 1:
+            return None
+        if not hasattr(self, "_halo"):
+            from paper_2603_15964_b200.distributed import CommHalo, make_comm
+            self._halo = CommHalo(make_comm(self.rank, self.world, True, "nccl"))
+        return self._halo
 
     def check(self):
         """The deferred harvest status and the finiteness of the last pass."""
@@ -356,8 +365,8 @@ class C5:
 
     @property
     def d2h_bytes(self):
-        # run(): snapshots u0 and u_final (timestep.py:313,350); run_sharded: final slab
-        return 2 * self.u0_host.nbytes if self.world == 1 else 8 * self.nloc
+        # run() / run_sharded: snapshots u0 and u_final on rank 0 (timestep.py:313,350)
+        return 2 * self.u0_host.nbytes
 
 
 def time_c5_onestep(steps=20):
@@ -394,25 +403,34 @@ def time_c4_sharded(rank, world):
     import torch
     import paper_2603_15964_b200 as lx
     from paper_2603_15964_b200 import configs
-    from paper_2603_15964_b200.distributed import NcclHalo, ShardedStepper, advance_all
+    from paper_2603_15964_b200.distributed import CommHalo, ShardedStepper, advance_all, make_comm
     w = configs.c4()
     g = lx.make_uniform_grid(w.N, -1.0, 1.0)
     st = lx.select_stencils(g, w.n, lx.StencilPolicy.CENTERED)
     prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(w.terms), None, w.u0, lx.Boundary.neumann(),
                                 "cubic")
+    comm = make_comm(rank, world, False, "nccl") if world > 1 else None
     s = ShardedStepper(g, st, prob, lx.SchemeConfig("etdrk4"), w.delta_t, rank, world,
-                       NcclHalo(rank, world, False))
+                       CommHalo(comm) if comm else None)
     s.set_initial(w.u0)
-    advance_all(s, 20)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    advance_all(s, w.steps)
-    e1.record()
+    own = torch.cuda.Stream()                     # chunks replay from CUDA graphs
+    own.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(own):
+        advance_all(s, 4 * s.plan.ksteps)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        advance_all(s, w.steps)
+        e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    return {"N": w.N, "steps": w.steps, "us_per_step": ms * 1e3 / w.steps,
-            "updates_per_s": w.N * w.steps / (ms * 1e-3), "ksteps_per_exchange": s.plan.ksteps}
+    out = {"N": w.N, "steps": w.steps, "us_per_step": ms * 1e3 / w.steps,
+           "updates_per_s": w.N * w.steps / (ms * 1e-3), "ksteps_per_exchange": s.plan.ksteps,
+           "transport": "lmep_comm (NCCL)" if comm else "none (one slab)", "overlap": s.overlap, "graphs": len(s._graphs)}
+    s._graphs.clear()
+    if comm:
+        comm.close()
+    return out
 
 
 def time_other_configs(fp64=None, hbm=None, lat=None, sm_mhz=None):

@@ -332,7 +332,9 @@ __global__ void __launch_bounds__(256, 2) lin_pernode_tb_kernel(const __grid_con
 // tma: the persistent kernel (step_lin_tma.cu, 3 x 512 nodes), else 3 x 256
 int tb_nodes_per_cta(int n, bool tma)
 {
-    return n == 13 || n == 11 || n == 9 || n == 7 ? 3 * (tma ? 512 : 256) : 0;
+    if (!(n == 13 || n == 11 || n == 9 || n == 7)) return 0;
+    if (tma && device_settings().pernode_kernel.load() == 3) return 6 * 128;   // two CTAs per SM
+    return 3 * (tma ? 512 : 256);
 }
 
 int launch_lin_pernode_tb(const StepParams &p, bool exact, cudaStream_t st)

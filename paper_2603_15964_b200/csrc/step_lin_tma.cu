@@ -217,8 +217,8 @@ __global__ void __launch_bounds__(NT, 1) lin_pernode_tma_kernel(const __grid_con
 // free at a 48-byte lane stride).  The accumulation order is the same
 // ascending chain as every other per-node kernel (bit-identical in EX).
 // ---------------------------------------------------------------------------
-template <int NS, int EL, int J, int NT, bool EX>
-__global__ void __launch_bounds__(NT, 1) lin_pernode_tmx_kernel(const __grid_constant__ StepParams p)
+template <int NS, int EL, int J, int NT, bool EX, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_constant__ StepParams p)
 {
     constexpr int ER = NS - 1 - EL;
     static_assert(EL <= J && ER <= J && J % 2 == 0, "halo must come from the adjacent threads");
@@ -296,38 +296,72 @@ __global__ void __launch_bounds__(NT, 1) lin_pernode_tmx_kernel(const __grid_con
             double *Qb = Q + (s & 1) * (J * QS);
 #pragma unroll
             for (int j = 0; j < J; ++j) Qb[j * QS + 1 + tid] = x[j];
-            __syncthreads();
-            double win[W];
+            if constexpr (!EX) {
+                // Fused mode: node j's sum splits into the products with this
+                // thread's own values (window slots EL .. EL+J-1: J taps per
+                // node) and the products with the neighbours' halo values.  The
+                // own chains of the first half of the nodes run between the
+                // stores and the barrier, the second half right after the halo
+                // loads are issued, so neither the barrier nor the shared-memory
+                // latency leaves the FP64 pipe idle; then the halo chains.
+                double own[J], hal[J];
+                auto own_chain = [&](int j) {
+                    // taps c with EL <= j + c < EL + J (window slots of this thread's values)
+                    double a = 0.0;
 #pragma unroll
-            for (int m = 0; m < EL; ++m) win[m] = Qb[(J - EL + m) * QS + tid];          // t-1
+                    for (int c = 0; c < NS; ++c) {
+                        const int i = j + c;
+                        if (i >= EL && i < EL + J) a = fma(w[j][c], x[i - EL], a);
+                    }
+                    return a;
+                };
 #pragma unroll
-            for (int j = 0; j < J; ++j) win[EL + j] = x[j];
+                for (int j = 0; j < J / 2; ++j) own[j] = own_chain(j);
+                __syncthreads();
+                double hl[EL > 0 ? EL : 1], hr[ER > 0 ? ER : 1];
 #pragma unroll
-            for (int m = 0; m < ER; ++m) win[EL + J + m] = Qb[m * QS + 2 + tid];        // t+1
-            // the J chains interleaved tap by tap: J independent FMAs per tap
-            // hide the FP64 latency.  EX keeps each node's ascending chain (the
-            // reference order); the fused mode splits it into two half chains
-            // (taps [0, H) and [H, n)) joined by one add: 2J independent chains
-            double acc[J], acc2[J];
-            constexpr int H = EX ? NS : (NS + 1) / 2;
+                for (int m = 0; m < EL; ++m) hl[m] = Qb[(J - EL + m) * QS + tid];          // t-1
 #pragma unroll
-            for (int j = 0; j < J; ++j) {
-                acc[j] = EX ? xmul(w[j][0], win[j]) : w[j][0] * win[j];
-                if constexpr (!EX) acc2[j] = w[j][H] * win[j + H];
-            }
+                for (int m = 0; m < ER; ++m) hr[m] = Qb[m * QS + 2 + tid];                 // t+1
 #pragma unroll
-            for (int c = 1; c < H; ++c) {
+                for (int j = J / 2; j < J; ++j) own[j] = own_chain(j);
+                // halo chains, tap by tap across the nodes (independent FMAs back to back):
+                // left taps c < EL - j read hl[j + c], right taps c > EL+J-1-j read hr[j+c-EL-J]
 #pragma unroll
-                for (int j = 0; j < J; ++j) {
-                    if constexpr (EX) acc[j] = xadd(acc[j], xmul(w[j][c], win[j + c]));
-                    else {
-                        acc[j] = fma(w[j][c], win[j + c], acc[j]);
-                        if (H + c < NS) acc2[j] = fma(w[j][H + c], win[j + H + c], acc2[j]);
+                for (int j = 0; j < J; ++j) hal[j] = 0.0;
+#pragma unroll
+                for (int c = 0; c < NS; ++c) {
+#pragma unroll
+                    for (int j = 0; j < J; ++j) {
+                        const int i = j + c;
+                        if (i < EL) hal[j] = fma(w[j][c], hl[i], hal[j]);
+                        else if (i >= EL + J) hal[j] = fma(w[j][c], hr[i - EL - J], hal[j]);
                     }
                 }
-            }
 #pragma unroll
-            for (int j = 0; j < J; ++j) x[j] = EX ? acc[j] : acc[j] + acc2[j];
+                for (int j = 0; j < J; ++j) x[j] = own[j] + hal[j];
+            } else {
+                __syncthreads();
+                double win[W];
+#pragma unroll
+                for (int m = 0; m < EL; ++m) win[m] = Qb[(J - EL + m) * QS + tid];          // t-1
+#pragma unroll
+                for (int j = 0; j < J; ++j) win[EL + j] = x[j];
+#pragma unroll
+                for (int m = 0; m < ER; ++m) win[EL + J + m] = Qb[m * QS + 2 + tid];        // t+1
+                // each node's ascending chain (the reference order), the J chains
+                // interleaved tap by tap
+                double acc[J];
+#pragma unroll
+                for (int j = 0; j < J; ++j) acc[j] = xmul(w[j][0], win[j]);
+#pragma unroll
+                for (int c = 1; c < NS; ++c) {
+#pragma unroll
+                    for (int j = 0; j < J; ++j) acc[j] = xadd(acc[j], xmul(w[j][c], win[j + c]));
+                }
+#pragma unroll
+                for (int j = 0; j < J; ++j) x[j] = acc[j];
+            }
         }
         // outputs: staged nodes [K eL, K eL + (t1 - t0)) -> u_out[t0 ...]
 #pragma unroll
@@ -344,18 +378,18 @@ __global__ void __launch_bounds__(NT, 1) lin_pernode_tmx_kernel(const __grid_con
 
 // (n, row) pairs with both halo widths <= 6 that the register-resident kernel
 // is instantiated for: the centred stencils and the n = 7 one-sided ones
-template <bool EX>
+template <bool EX, int NT, int MINB>
 static int launch_tmx(const StepParams &p, unsigned grid, cudaStream_t st)
 {
-    constexpr int J = 6, NT = 256;
+    constexpr int J = 6;
     const size_t shm = (size_t)(p.n * (J * NT + 4) + tma_ulen(p.n, J * NT) + 2 * J * (NT + 2)) * 8;
     void (*k)(StepParams) = nullptr;
-    if (p.n == 13 && p.row == 6) k = lin_pernode_tmx_kernel<13, 6, J, NT, EX>;
-    else if (p.n == 11 && p.row == 5) k = lin_pernode_tmx_kernel<11, 5, J, NT, EX>;
-    else if (p.n == 9 && p.row == 4) k = lin_pernode_tmx_kernel<9, 4, J, NT, EX>;
-    else if (p.n == 7 && p.row == 3) k = lin_pernode_tmx_kernel<7, 3, J, NT, EX>;
-    else if (p.n == 7 && p.row == 6) k = lin_pernode_tmx_kernel<7, 6, J, NT, EX>;
-    else if (p.n == 7 && p.row == 0) k = lin_pernode_tmx_kernel<7, 0, J, NT, EX>;
+    if (p.n == 13 && p.row == 6) k = lin_pernode_tmx_kernel<13, 6, J, NT, EX, MINB>;
+    else if (p.n == 11 && p.row == 5) k = lin_pernode_tmx_kernel<11, 5, J, NT, EX, MINB>;
+    else if (p.n == 9 && p.row == 4) k = lin_pernode_tmx_kernel<9, 4, J, NT, EX, MINB>;
+    else if (p.n == 7 && p.row == 3) k = lin_pernode_tmx_kernel<7, 3, J, NT, EX, MINB>;
+    else if (p.n == 7 && p.row == 6) k = lin_pernode_tmx_kernel<7, 6, J, NT, EX, MINB>;
+    else if (p.n == 7 && p.row == 0) k = lin_pernode_tmx_kernel<7, 0, J, NT, EX, MINB>;
     if (!k) return -1;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
     k<<<grid, NT, shm, st>>>(p);
@@ -378,8 +412,16 @@ int launch_lin_pernode_tma(const StepParams &p, bool exact, cudaStream_t st)
     // order (11.7 vs 12.3: two roundings per tap double its FP64 work and the
     // window kernel's 16 warps hide that latency better)
     const int pk = device_settings().pernode_kernel.load();
+    if (pk == 3) {
+        // two CTAs of 128 threads per SM, each on its own 768-node tile: while one
+        // exchanges halos through shared memory the other keeps the FP64 pipe busy
+        const unsigned g2 = (unsigned)(ntiles < 2 * nsm ? ntiles : 2 * nsm);
+        const int rc = exact ? launch_tmx<true, 128, 2>(p, g2, st) : launch_tmx<false, 128, 2>(p, g2, st);
+        if (rc >= 0) return rc;
+        return LMEP_INVALID_CONFIG;
+    }
     if (pk == 1 || (pk == 2 && !exact)) {
-        const int rc = exact ? launch_tmx<true>(p, grid, st) : launch_tmx<false>(p, grid, st);
+        const int rc = exact ? launch_tmx<true, 256, 1>(p, grid, st) : launch_tmx<false, 256, 1>(p, grid, st);
         if (rc >= 0) return rc;                  // else: (n, row) not instantiated
     }
 #define LMEP_TMA_CASE(NS_)                                                                        \
@@ -409,7 +451,7 @@ int launch_lin_pernode_tma(const StepParams &p, bool exact, cudaStream_t st)
 
 extern "C" int lmep_set_pernode_kernel(int variant)
 {
-    if (variant < 0 || variant > 2) return LMEP_INVALID_CONFIG;
+    if (variant < 0 || variant > 3) return LMEP_INVALID_CONFIG;
     lmep::device_settings().pernode_kernel.store(variant);
     return LMEP_OK;
 }
