@@ -38,7 +38,9 @@ namespace lmep {
 enum { SCH_LIN = 0, SCH_ETDRK4 = 1, SCH_ETD2 = 2 };
 constexpr int STEP_THREADS = 256;
 constexpr int SLOT_PAD = 24;
-constexpr int STEP_P_ETDRK4 = 5;   // consecutive outputs per thread (odd: conflict-free)
+constexpr int STEP_P_ETDRK4 = 7;   // consecutive outputs per thread (odd: conflict-free)
+constexpr int STEP_P_ETDRK4_CV = 5; // convective N: wider stencils, one more window per stage
+constexpr int step_p_etdrk4(int nl) { return nl == LMEP_NL_CONVECTIVE ? STEP_P_ETDRK4_CV : STEP_P_ETDRK4; }
 constexpr int STEP_P_ETD2 = 1;
 
 struct StepParams {
@@ -295,6 +297,10 @@ __device__ __forceinline__ void fast_pointwise(int lo, int hi, Epi &&epi)
     }
 }
 
+}  // namespace lmep
+#include "step_rk4.cuh"
+namespace lmep {
+
 template <int SCH, int NS, bool EX, int P, int NLK, bool PN, int ETDS = 2>
 __global__ void __launch_bounds__(STEP_THREADS, SCH == SCH_LIN ? 1 : 2)
 step_kernel(const __grid_constant__ StepParams p)
@@ -361,7 +367,30 @@ step_kernel(const __grid_constant__ StepParams p)
 #define S(q) (sm + (q) * slen)
 
     // ---- stage u (and the etd2 history) into shared memory -------------
-    for (int idx = tid; idx < len; idx += nt) {
+    // ETDRK4 tiles that lie inside one shard without wrapping: the loads of a
+    // thread are issued back to back (one memory latency per tile, not one per
+    // element; the dependent load -> store loop below cost 15% of the C4 kernel)
+    bool staged = false;
+    if constexpr (SCH == SCH_ETDRK4) {
+        if (!ring && p.hl == nullptr && p.hr == nullptr && base >= p.off && gend <= p.off + p.nloc) {
+            const double *src = p.u_in + (base - p.off);
+            constexpr int UB = 8;
+            for (int i0 = tid; i0 < len; i0 += UB * nt) {
+                double v[UB];
+#pragma unroll
+                for (int j = 0; j < UB; ++j) v[j] = i0 + j * nt < len ? __ldg(src + i0 + j * nt) : 0.0;
+#pragma unroll
+                for (int j = 0; j < UB; ++j) {
+                    if (i0 + j * nt < len) {
+                        S(0)[i0 + j * nt] = v[j];
+                        if constexpr (!cv) S(1)[i0 + j * nt] = nlp<EX>(nlk, v[j], 0.0);
+                    }
+                }
+            }
+            staged = true;
+        }
+    }
+    for (int idx = tid; !staged && idx < len; idx += nt) {
         const int64_t g = base + idx;
         const double u = load_node(p, p.u_in, p.hl, p.hr, g);
         S(0)[idx] = u;
@@ -467,6 +496,13 @@ step_kernel(const __grid_constant__ StepParams p)
         if constexpr (!PN && NS > 0) {
             // (a non-periodic tile clear of the boundary classes holds no pinned node)
             const bool fast = !ring && (p.periodic || (base >= p.L_int && gend <= p.R_int));
+            // one chunk of P staged nodes per thread: the register-resident passes
+            // (step_rk4.cuh); CTA-uniform
+            if (fast && (len - eL + P - 1) / P <= nt) {
+                if constexpr (cv) etdrk4_regs_convective<NS, P, EX>(p, sm, slen, len, K, O0, O1, base);
+                else etdrk4_regs_pointwise<NS, P, EX, NLK>(p, sm, slen, len, K, O0, O1, base);
+                return;
+            }
             if (fast) {
                 if constexpr (cv) {
                     sl[U] = 0; sl[N0] = 1; sl[WH] = 2; sl[A] = 3; sl[N3] = 3; sl[N1] = 4; sl[S12] = 4;

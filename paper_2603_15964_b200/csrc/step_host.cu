@@ -30,7 +30,7 @@ int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded
     const int n = g.n, eL = g.row, eR = n - 1 - g.row;
     const int ext = step_ext(sch, nl);
     const int ns = nslots(sch, etds);
-    const int P = pernode ? 1 : (sch == SCH_ETD2 ? STEP_P_ETD2 : (sch == SCH_ETDRK4 ? STEP_P_ETDRK4 : 5));
+    const int P = pernode ? 1 : (sch == SCH_ETD2 ? STEP_P_ETD2 : (sch == SCH_ETDRK4 ? step_p_etdrk4(nl) : 5));
     const int64_t rad = (int64_t)ext * (eL + eR);
     // ring mode: whole periodic grid on one CTA for all steps
     const int64_t ring_bytes = (int64_t)ns * (g.N + n + SLOT_PAD + P) * 8;
@@ -44,7 +44,7 @@ int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded
         t.ksteps = (int32_t)std::max<int64_t>(1, steps);
         return LMEP_OK;
     }
-    int64_t tile = t.tile, k = t.ksteps;
+    int64_t tile = t.tile, k = t.ksteps, rk4_k = 0;
     if (pernode && sch == SCH_LIN && g.periodic && tb_nodes_per_cta(n, false) > 0 && steps > 1 &&
         t.tile == 0 && (!sharded || pernode_pad >= steps * std::max(eL, eR))) {
         // per-node rows held in registers for k steps: single shard with an
@@ -74,7 +74,16 @@ int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded
         // ETDRK4: + halo ~ 256 chunks of 5; large unsharded grids take wider tiles
         // with several steps per launch (C4 2^24: 254 -> 192 us/step, C3 2^20:
         // 36.7 -> 33.0, tools/prof_cases.py sweeps over tile x k)
-        else tile = (!sharded && g.nloc >= (int64_t)1800 * 2 * nsm) ? 1800 : 1200;
+        else {
+            // register-resident ETDRK4 passes (step_rk4.cuh): one chunk of P staged
+            // nodes per thread, so tile + k * rad <= 256 P; large unsharded grids
+            // fuse several steps per launch
+            const bool big = !sharded && g.nloc >= (int64_t)1800 * 2 * nsm;
+            const int64_t kk = k > 0 ? k : (big ? (nl == LMEP_NL_CONVECTIVE ? 3 : 6) : 1);
+            tile = (int64_t)STEP_THREADS * P - kk * rad;
+            if (tile < 512 || pernode) tile = big ? 1800 : 1200;
+            else if (big) rk4_k = kk;
+        }
         // small grids: enough tiles to cover the SMs
         while (tile > 256 && (g.nloc + tile - 1) / tile < 2 * nsm) tile /= 2;
         tile = std::min<int64_t>(tile, g.nloc);
@@ -87,7 +96,7 @@ int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded
             // latency-bound small grids: deeper halos, fewer launches (ETD2 C2 at
             // 2^16: k 4 -> 8, 2.57 -> 2.12 us/step FMA)
             k = std::max<int64_t>(1, tile / ((sch == SCH_ETD2 ? 2 : 4) * std::max<int64_t>(rad, 1)));
-        else if (sch == SCH_ETDRK4 && !sharded && tile == 1800) k = nl == LMEP_NL_CONVECTIVE ? 2 : 6;
+        else if (rk4_k > 0) k = rk4_k;
         k = std::min<int64_t>(k, std::max<int64_t>(steps, 1));
         k = std::max<int64_t>(k, 1);
     }
@@ -102,7 +111,11 @@ int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded
     if (t.threads <= 0 && sch != SCH_LIN) {
         // one chunk of P nodes per thread for the widest pass of a step:
         // a pass is a single round, nobody waits for a second one at the barrier
-        const int64_t widest = tile + (int64_t)ext * (eL + eR);
+        int64_t widest = tile + (int64_t)ext * (eL + eR);
+        // ETDRK4: the register-resident passes keep one chunk per thread over the
+        // whole staged range (tile + k * rad) when that fits the CTA
+        if (sch == SCH_ETDRK4 && !pernode && tile + k * rad <= (int64_t)STEP_THREADS * P)
+            widest = tile + k * rad;
         int64_t th = ((widest + P - 1) / P + 31) / 32 * 32;
         t.threads = (int32_t)std::max<int64_t>(32, std::min<int64_t>(256, th));
     }
@@ -232,7 +245,7 @@ int run_steps(const StepCall &c)
     p.tile = t.tile;
     p.threads = t.threads > 0 ? t.threads : STEP_THREADS;
     if (p.threads % 32 != 0 || p.threads > STEP_THREADS) return LMEP_INVALID_CONFIG;
-    const int P = pernode ? 1 : (c.sch == SCH_ETD2 ? STEP_P_ETD2 : (c.sch == SCH_ETDRK4 ? STEP_P_ETDRK4 : 5));
+    const int P = pernode ? 1 : (c.sch == SCH_ETD2 ? STEP_P_ETD2 : (c.sch == SCH_ETDRK4 ? step_p_etdrk4(c.nl) : 5));
     const int64_t rad = (int64_t)p.ext * (p.eL + p.eR);
     p.slot_len = t.ring ? (g.N + g.n + SLOT_PAD + P) : (t.tile + (int64_t)t.ksteps * rad + SLOT_PAD + P);
     p.slot_len = (p.slot_len + 3) & ~int64_t(3);
