@@ -217,6 +217,11 @@ __global__ void __launch_bounds__(NT, 1) lin_pernode_tma_kernel(const __grid_con
 // free at a 48-byte lane stride).  The accumulation order is the same
 // ascending chain as every other per-node kernel (bit-identical in EX).
 // ---------------------------------------------------------------------------
+#ifdef LMEP_TMX_TIMING
+// diagnostic builds (-DLMEP_TMX_TIMING): per-tile phase timestamps of two CTAs
+__device__ long long g_tmx_timing[512];
+#endif
+
 template <int NS, int EL, int J, int NT, bool EX, int MINB = 1>
 __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_constant__ StepParams p)
 {
@@ -262,7 +267,13 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
     for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
         const TileRange r = tile_range(p, tile, K, eL, eR);
         const int org = eL + ((eL - r.o) & 1);
+#ifdef LMEP_TMX_TIMING
+        long long tq0 = clock64();
+#endif
         mbar_wait(&bar, (uint32_t)(it & 1));
+#ifdef LMEP_TMX_TIMING
+        long long tq1 = clock64();
+#endif
         // rows and initial values of this thread's J staged nodes -> registers
         // (nodes past the staged range keep finite placeholders; their results
         // only reach nodes that are never stored)
@@ -290,7 +301,13 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
         for (int j = 0; j < J; ++j) x[j] = Ub[org + (l0 + j < r.len ? l0 + j : K * eL)];
         __syncthreads();                         // R and Ub free for the next tile's copies
         const int64_t nxt = tile + gridDim.x;
+#ifdef LMEP_TMX_TIMING
+        long long tq2 = clock64();
+#endif
         if (tid == 0 && nxt < ntiles) issue(nxt);
+#ifdef LMEP_TMX_TIMING
+        long long tq3 = clock64();
+#endif
 
         for (int s = 0; s < K; ++s) {
             double *Qb = Q + (s & 1) * (J * QS);
@@ -364,6 +381,9 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
             }
         }
         // outputs: staged nodes [K eL, K eL + (t1 - t0)) -> u_out[t0 ...]
+#ifdef LMEP_TMX_TIMING
+        long long tq4 = clock64();
+#endif
 #pragma unroll
         for (int j = 0; j < J; ++j) {
             const int64_t i = r.t0 + (int64_t)(l0 + j - K * eL);
@@ -372,6 +392,12 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
                 bad |= !isfinite(x[j]);
             }
         }
+#ifdef LMEP_TMX_TIMING
+        if (tid == 32 && (blockIdx.x == 0 || blockIdx.x == 77) && it < 30) {
+            long long *o = g_tmx_timing + (blockIdx.x ? 256 : 0) + it * 6;
+            o[0] = tq0; o[1] = tq1; o[2] = tq2; o[3] = tq3; o[4] = tq4; o[5] = clock64();
+        }
+#endif
     }
     if (bad) *p.flag = 1;
 }
@@ -448,6 +474,13 @@ int launch_lin_pernode_tma(const StepParams &p, bool exact, cudaStream_t st)
 }
 
 }  // namespace lmep
+
+#ifdef LMEP_TMX_TIMING
+extern "C" int lmep_debug_tmx_timing(long long *host_out)
+{
+    return cudaMemcpyFromSymbol(host_out, lmep::g_tmx_timing, sizeof(long long) * 512) == cudaSuccess ? 0 : 4;
+}
+#endif
 
 extern "C" int lmep_set_pernode_kernel(int variant)
 {

@@ -322,7 +322,11 @@ class ShardedStepper:
         # nodes' rows (no communication), so k steps fuse per exchange
         pad_ok = per_node and scheme.kind == "linear" and grid.periodic
         if ksteps is None:
-            ksteps = max(1, min(16, nloc // (4 * ext * max(reach, 1))))
+            # steps per exchange: 16 for the one-pass schemes; the ETDRK4 kernel keeps
+            # one chunk of nodes per thread, so its staged range (tile + k * halo) is
+            # bounded and it takes the single-GPU plan's 6 (pointwise N) / 3 (convective)
+            cap = 16 if scheme.kind != "etdrk4" else (3 if nl == nat.NL_CONVECTIVE else 6)
+            ksteps = max(1, min(cap, nloc // (4 * ext * max(reach, 1))))
         if per_node and scheme.kind == "linear" and self.sharded and not pad_ok:
             ksteps = 1                      # non-periodic per-node rows: one step per exchange
         if not self.sharded:

@@ -1,0 +1,75 @@
+// probe: the C5 step's DFMA pattern (78 distinct weight registers, 18-value window,
+// 12 chains) without any shared memory or barrier: clocks per "step" per SM sub-partition
+#include <cstdio>
+#include <cuda_runtime.h>
+template <int MODE>
+__global__ void __launch_bounds__(256, 1) pat(const double *wsrc, double *out, int iters, long long *cyc)
+{
+    constexpr int J = 6, NS = 13, W = 18;
+    double w[J][NS], x[J], win[W];
+    for (int j = 0; j < J; ++j)
+        for (int c = 0; c < NS; ++c) w[j][c] = wsrc[(j * NS + c) * 256 + threadIdx.x];
+    for (int j = 0; j < J; ++j) x[j] = 1.0 + 1e-3 * j + 1e-6 * threadIdx.x;
+    __syncthreads();
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int m = 0; m < 6; ++m) win[m] = x[m] * 0.5;
+#pragma unroll
+        for (int j = 0; j < J; ++j) win[6 + j] = x[j];
+#pragma unroll
+        for (int m = 0; m < 6; ++m) win[12 + m] = x[m] * 0.25;
+        double acc[J], acc2[J];
+        if (MODE == 0) {           // two half chains per node, tap-major
+            constexpr int H = 7;
+#pragma unroll
+            for (int j = 0; j < J; ++j) { acc[j] = w[j][0] * win[j]; acc2[j] = w[j][H] * win[j + H]; }
+#pragma unroll
+            for (int c = 1; c < H; ++c)
+#pragma unroll
+                for (int j = 0; j < J; ++j) {
+                    acc[j] = fma(w[j][c], win[j + c], acc[j]);
+                    if (H + c < NS) acc2[j] = fma(w[j][H + c], win[j + H + c], acc2[j]);
+                }
+#pragma unroll
+            for (int j = 0; j < J; ++j) x[j] = acc[j] + acc2[j];
+        } else if (MODE == 1) {    // window-major: each window value feeds all its nodes back to back
+#pragma unroll
+            for (int j = 0; j < J; ++j) acc[j] = 0.0;
+#pragma unroll
+            for (int i = 0; i < W; ++i)
+#pragma unroll
+                for (int j = 0; j < J; ++j) {
+                    const int c = i - j;
+                    if (c >= 0 && c < NS) acc[j] = fma(w[j][c], win[i], acc[j]);
+                }
+#pragma unroll
+            for (int j = 0; j < J; ++j) x[j] = acc[j];
+        }
+    }
+    long long t1 = clock64();
+    double s = 0;
+    for (int j = 0; j < J; ++j) s += x[j];
+    out[blockIdx.x * 256 + threadIdx.x] = s;
+    if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+int main()
+{
+    double *w, *o; long long *c;
+    cudaMalloc(&w, 78 * 256 * 8); cudaMalloc(&o, 148 * 256 * 8); cudaMalloc(&c, 148 * 8);
+    double *h = new double[78 * 256];
+    for (int i = 0; i < 78 * 256; ++i) h[i] = 0.05 + 1e-4 * (i % 97);
+    cudaMemcpy(w, h, 78 * 256 * 8, cudaMemcpyHostToDevice);
+    const int iters = 2000;
+    long long hc[148];
+    for (int mode = 0; mode < 2; ++mode) {
+        for (int rep = 0; rep < 2; ++rep) {
+            if (mode == 0) pat<0><<<148, 256>>>(w, o, iters, c); else pat<1><<<148, 256>>>(w, o, iters, c);
+            cudaDeviceSynchronize();
+        }
+        cudaMemcpy(hc, c, 148 * 8, cudaMemcpyDeviceToHost);
+        printf("mode %d: %.1f clk per step (8 warps/SM, 84 D-ops per warp-step; FP64 floor 336) err=%s\n", mode,
+               (double)hc[0] / iters, cudaGetErrorString(cudaGetLastError()));
+    }
+    return 0;
+}
