@@ -129,6 +129,14 @@ typedef struct {
     const double *hist_left;   /* etd2 history ghosts */
     const double *hist_right;
     int64_t width;
+    /* Fused peer stores (optional, linear and ETDRK4 launches with shared / class
+     * rows): besides u_out, the launch stores its first push_width results at
+     * push_left[0 ..] and its last push_width results at push_right[0 ..] --
+     * the neighbours' mailbox slots from lmep_comm_targets, i.e. peer memory over
+     * NVLink -- so the next chunk's halo needs no exchange kernel at all. */
+    double *push_left;
+    double *push_right;
+    int64_t push_width;
 } lmep_halo;
 
 /* Optional launch shape.  0 = library heuristic. */
@@ -386,6 +394,27 @@ int lmep_comm_info(const lmep_comm *comm, int *rank, int *world, int *left, int 
 int lmep_halo_exchange(lmep_comm *comm, int nfields, const double *const *fields, int64_t nloc,
                        int64_t width, double *const *ghost_left, double *const *ghost_right,
                        void *stream);
+
+/* PEER transport, piecewise (what lmep_halo_exchange does in one call is
+ * push + wait + a copy out of the mailbox):
+ *   lmep_comm_targets  where this rank's edges of field f go for its NEXT signal:
+ *                      the neighbours' mailbox slots (peer pointers; NULL without
+ *                      a neighbour).  A step launch given them as lmep_halo.push_*
+ *                      stores its edges there itself.
+ *   lmep_comm_push     store the edges of `fields` there with the library's kernel
+ *                      and signal (the first chunk, or after a standalone step).
+ *   lmep_comm_signal   the edges are stored (stream order): record the
+ *                      interprocess event and publish the exchange number.
+ *   lmep_comm_wait     make `stream` wait for the neighbours' signal that matches
+ *                      this rank's latest one (the host meets them first).
+ *   lmep_comm_ghosts   this rank's own mailbox slots of that exchange: pass them as
+ *                      lmep_halo.left / right, no copy. */
+int lmep_comm_targets(lmep_comm *comm, int field, double **to_left, double **to_right);
+int lmep_comm_push(lmep_comm *comm, int nfields, const double *const *fields, int64_t nloc,
+                   int64_t width, void *stream);
+int lmep_comm_signal(lmep_comm *comm, void *stream);
+int lmep_comm_wait(lmep_comm *comm, void *stream);
+int lmep_comm_ghosts(lmep_comm *comm, int field, const double **left, const double **right);
 
 /* Concatenate the slabs on `root`: rank r contributes nloc_r = counts[r]
  * doubles (counts: HOST array of world entries, the same on every rank); out

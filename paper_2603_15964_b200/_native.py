@@ -49,6 +49,8 @@ EXPORTS = (
     "lmep_comm_destroy", "lmep_comm_info", "lmep_halo_exchange", "lmep_comm_gather",
     "lmep_comm_flag_max", "lmep_comm_side_stream", "lmep_comm_fork", "lmep_comm_join",
     "lmep_graph_begin", "lmep_graph_end", "lmep_graph_launch", "lmep_graph_destroy",
+    "lmep_comm_targets", "lmep_comm_push", "lmep_comm_signal", "lmep_comm_wait",
+    "lmep_comm_ghosts",
 )
 COMM_NCCL, COMM_PEER = 0, 1
 COMM_ID_BYTES, COMM_BLOB_BYTES, COMM_MAX_FIELDS = 128, 512, 8
@@ -72,7 +74,8 @@ class LmepBC(C.Structure):
 
 class LmepHalo(C.Structure):
     _fields_ = [("left", C.c_void_p), ("right", C.c_void_p), ("hist_left", C.c_void_p),
-                ("hist_right", C.c_void_p), ("width", C.c_int64)]
+                ("hist_right", C.c_void_p), ("width", C.c_int64), ("push_left", C.c_void_p),
+                ("push_right", C.c_void_p), ("push_width", C.c_int64)]
 
 
 class LmepCoefMap(C.Structure):
@@ -164,6 +167,11 @@ def load(path: str | None = None):
                                      C.POINTER(vp), vp]
     L.lmep_comm_gather.argtypes = [vp, vp, C.POINTER(i64), vp, C.c_int, vp]
     L.lmep_comm_flag_max.argtypes = [vp, vp, C.c_int, vp]
+    L.lmep_comm_targets.argtypes = [vp, C.c_int, C.POINTER(vp), C.POINTER(vp)]
+    L.lmep_comm_push.argtypes = [vp, C.c_int, C.POINTER(vp), i64, i64, vp]
+    L.lmep_comm_signal.argtypes = [vp, vp]
+    L.lmep_comm_wait.argtypes = [vp, vp]
+    L.lmep_comm_ghosts.argtypes = [vp, C.c_int, C.POINTER(vp), C.POINTER(vp)]
     L.lmep_comm_side_stream.argtypes = [vp]
     L.lmep_comm_side_stream.restype = vp
     L.lmep_comm_fork.argtypes = [vp, vp]

@@ -470,13 +470,21 @@ def combine_rows(parts: list[CompactRows], coeffs) -> CompactRows:
 # stepping (K3-K5)
 # ---------------------------------------------------------------------------
 def c_halo(halo) -> nat.LmepHalo | None:
-    """halo = (left, right, hist_left, hist_right, width) device tensors (or None)."""
+    """halo = (left, right, hist_left, hist_right, width[, push_left, push_right,
+    push_width]): device tensors, raw device pointers (mailbox slots of the
+    communicator) or None."""
     if halo is None:
         return None
+
+    def ptr(x):
+        return x if (x is None or isinstance(x, int)) else x.data_ptr()
+
     h = nat.LmepHalo()
-    h.left, h.right = nat.ptr(halo[0]), nat.ptr(halo[1])
-    h.hist_left, h.hist_right = nat.ptr(halo[2]), nat.ptr(halo[3])
+    h.left, h.right = ptr(halo[0]), ptr(halo[1])
+    h.hist_left, h.hist_right = ptr(halo[2]), ptr(halo[3])
     h.width = int(halo[4])
+    if len(halo) > 5:
+        h.push_left, h.push_right, h.push_width = ptr(halo[5]), ptr(halo[6]), int(halo[7])
     return h
 
 

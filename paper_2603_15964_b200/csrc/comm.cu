@@ -324,32 +324,46 @@ int exchange_nccl(lmep_comm *c, int nf, const double *const *fields, int64_t nlo
     return LMEP_OK;
 }
 
-int exchange_peer(lmep_comm *c, int nf, const double *const *fields, int64_t nloc, int64_t W,
-                  double *const *gl, double *const *gr, cudaStream_t st)
+// --- PEER primitives.  c->seq counts this rank's signals; exchange number e
+// uses mailbox half e & 1. ---------------------------------------------------
+int peer_check(lmep_comm *c, const char *what, cudaStream_t st)
 {
-    if (!c->connected) return LMEP_INVALID_CONFIG;
-    if (W > c->max_width) return LMEP_DIMENSION;
+    if (c->transport != LMEP_COMM_PEER || !c->connected) return LMEP_INVALID_CONFIG;
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone) {
-        set_last_error_text("lmep_halo_exchange", "the PEER transport cannot be captured in a graph");
+        set_last_error_text(what, "the PEER transport cannot be captured in a graph");
         return LMEP_INVALID_CONFIG;
     }
+    return LMEP_OK;
+}
+
+// where this rank's edges go for the NEXT signal: my right edge becomes the right
+// neighbour's left ghosts (its side 0), my left edge the left neighbour's right
+// ghosts (its side 1)
+void peer_targets(lmep_comm *c, int field, double **to_left, double **to_right)
+{
+    const int half = (int)((c->seq + 1) & 1);
+    const int64_t fo = (int64_t)field * c->max_width;
+    *to_left = c->left >= 0 ? slot(c->lnk_left.mailbox, c, half, 1) + fo : nullptr;
+    *to_right = c->right >= 0 ? slot(c->lnk_right.mailbox, c, half, 0) + fo : nullptr;
+}
+
+// the edges of the next exchange are stored (by the push kernel, or by a step
+// kernel's fused peer stores): record the event, publish the exchange number
+int peer_signal(lmep_comm *c, cudaStream_t st)
+{
     const uint64_t seq = ++c->seq;
-    const int half = (int)(seq & 1);
-    PushArgs pa{};
-    for (int f = 0; f < nf; ++f) pa.src[f] = fields[f];
-    // my right edge becomes the right neighbour's left ghosts (its side 0); my
-    // left edge the left neighbour's right ghosts (its side 1)
-    pa.to_left = c->left >= 0 ? slot(c->lnk_left.mailbox, c, half, 1) : nullptr;
-    pa.to_right = c->right >= 0 ? slot(c->lnk_right.mailbox, c, half, 0) : nullptr;
-    pa.nloc = nloc; pa.width = W; pa.slot_ld = c->max_width; pa.nfields = nf;
-    const int64_t total = 2 * W * nf;
-    const unsigned blocks = (unsigned)std::min<int64_t>((total + kPushThreads - 1) / kPushThreads, 1184);
-    halo_push_kernel<<<blocks, kPushThreads, 0, st>>>(pa);
-    int rc = launch_status("halo_push_kernel");
-    if (rc) return rc;
-    CUDA_TRY(cudaEventRecord(c->ev[half], st));
+    CUDA_TRY(cudaEventRecord(c->ev[seq & 1], st));
     c->page->posted.store(seq, std::memory_order_release);
+    return LMEP_OK;
+}
+
+// the stream waits for the neighbours' signal number c->seq
+int peer_wait(lmep_comm *c, cudaStream_t st)
+{
+    const uint64_t seq = c->seq;
+    const int half = (int)(seq & 1);
+    int rc;
     if (c->left >= 0) {
         if ((rc = wait_posted(c->lnk_left, seq))) return rc;
         CUDA_TRY(cudaStreamWaitEvent(st, c->lnk_left.ev[half], 0));
@@ -358,12 +372,41 @@ int exchange_peer(lmep_comm *c, int nf, const double *const *fields, int64_t nlo
         if ((rc = wait_posted(c->lnk_right, seq))) return rc;
         CUDA_TRY(cudaStreamWaitEvent(st, c->lnk_right.ev[half], 0));
     }
+    return LMEP_OK;
+}
+
+int peer_push(lmep_comm *c, int nf, const double *const *fields, int64_t nloc, int64_t W,
+              cudaStream_t st)
+{
+    if (W > c->max_width) return LMEP_DIMENSION;
+    PushArgs pa{};
+    for (int f = 0; f < nf; ++f) pa.src[f] = fields[f];
+    peer_targets(c, 0, &pa.to_left, &pa.to_right);
+    pa.nloc = nloc; pa.width = W; pa.slot_ld = c->max_width; pa.nfields = nf;
+    const int64_t total = 2 * W * nf;
+    const unsigned blocks = (unsigned)std::min<int64_t>((total + kPushThreads - 1) / kPushThreads, 1184);
+    halo_push_kernel<<<blocks, kPushThreads, 0, st>>>(pa);
+    int rc = launch_status("halo_push_kernel");
+    if (rc) return rc;
+    return peer_signal(c, st);
+}
+
+int exchange_peer(lmep_comm *c, int nf, const double *const *fields, int64_t nloc, int64_t W,
+                  double *const *gl, double *const *gr, cudaStream_t st)
+{
+    int rc = peer_check(c, "lmep_halo_exchange", st);
+    if (rc) return rc;
+    if ((rc = peer_push(c, nf, fields, nloc, W, st))) return rc;
+    if ((rc = peer_wait(c, st))) return rc;
+    const int half = (int)(c->seq & 1);
     PullArgs pl{};
     for (int f = 0; f < nf; ++f) { pl.gl[f] = gl[f]; pl.gr[f] = gr[f]; }
     pl.from_left = slot(c->mailbox, c, half, 0);
     pl.from_right = slot(c->mailbox, c, half, 1);
     pl.width = W; pl.slot_ld = c->max_width; pl.nfields = nf;
     pl.has_left = c->left >= 0; pl.has_right = c->right >= 0;
+    const int64_t total = 2 * W * nf;
+    const unsigned blocks = (unsigned)std::min<int64_t>((total + kPushThreads - 1) / kPushThreads, 1184);
     halo_pull_kernel<<<blocks, kPushThreads, 0, st>>>(pl);
     return launch_status("halo_pull_kernel");
 }
@@ -541,6 +584,53 @@ extern "C" int lmep_halo_exchange(lmep_comm *c, int nfields, const double *const
     if (c->transport == LMEP_COMM_NCCL)
         return exchange_nccl(c, nfields, fields, nloc, width, ghost_left, ghost_right, st);
     return exchange_peer(c, nfields, fields, nloc, width, ghost_left, ghost_right, st);
+}
+
+// ---- PEER: the pieces of an exchange, for step launches that store their own
+// edges into the neighbours' mailboxes (lmep_halo.push_*) --------------------
+extern "C" int lmep_comm_push(lmep_comm *c, int nfields, const double *const *fields, int64_t nloc,
+                              int64_t width, void *stream)
+{
+    if (!c || !fields || nfields < 1 || nfields > LMEP_COMM_MAX_FIELDS) return LMEP_INVALID_CONFIG;
+    if (width < 1 || nloc < width) return LMEP_DIMENSION;
+    int rc = peer_check(c, "lmep_comm_push", (cudaStream_t)stream);
+    if (rc) return rc;
+    return peer_push(c, nfields, fields, nloc, width, (cudaStream_t)stream);
+}
+
+extern "C" int lmep_comm_signal(lmep_comm *c, void *stream)
+{
+    if (!c) return LMEP_INVALID_CONFIG;
+    int rc = peer_check(c, "lmep_comm_signal", (cudaStream_t)stream);
+    if (rc) return rc;
+    return peer_signal(c, (cudaStream_t)stream);
+}
+
+extern "C" int lmep_comm_wait(lmep_comm *c, void *stream)
+{
+    if (!c) return LMEP_INVALID_CONFIG;
+    int rc = peer_check(c, "lmep_comm_wait", (cudaStream_t)stream);
+    if (rc) return rc;
+    return peer_wait(c, (cudaStream_t)stream);
+}
+
+extern "C" int lmep_comm_ghosts(lmep_comm *c, int field, const double **left, const double **right)
+{
+    if (!c || c->transport != LMEP_COMM_PEER || !c->connected) return LMEP_INVALID_CONFIG;
+    if (field < 0 || field >= LMEP_COMM_MAX_FIELDS) return LMEP_INVALID_CONFIG;
+    const int half = (int)(c->seq & 1);
+    const int64_t fo = (int64_t)field * c->max_width;
+    if (left) *left = c->left >= 0 ? slot(c->mailbox, c, half, 0) + fo : nullptr;
+    if (right) *right = c->right >= 0 ? slot(c->mailbox, c, half, 1) + fo : nullptr;
+    return LMEP_OK;
+}
+
+extern "C" int lmep_comm_targets(lmep_comm *c, int field, double **to_left, double **to_right)
+{
+    if (!c || c->transport != LMEP_COMM_PEER || !c->connected) return LMEP_INVALID_CONFIG;
+    if (field < 0 || field >= LMEP_COMM_MAX_FIELDS || !to_left || !to_right) return LMEP_INVALID_CONFIG;
+    peer_targets(c, field, to_left, to_right);
+    return LMEP_OK;
 }
 
 extern "C" int lmep_comm_gather(lmep_comm *c, const double *u, const int64_t *counts, double *out,

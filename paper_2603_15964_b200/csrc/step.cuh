@@ -63,6 +63,8 @@ struct StepParams {
     double *q_out;
     const double *hl, *hr, *qhl, *qhr;          // ghost buffers (sharded) or null
     int64_t G;
+    double *push_l, *push_r;                    // fused peer stores of the slab edges (or null)
+    int64_t push_w;
     double *nl0_out;
     double dt;
     double dtj[6];                              // etd-s: dt**j as Python computes it
@@ -89,6 +91,17 @@ __device__ __forceinline__ double nlp(int kind, double u, double du)
     if (kind == LMEP_NL_CONVECTIVE) return EX ? xmul(-u, du) : (-u) * du;
     if (kind == LMEP_NL_CUBIC) return EX ? xmul(xmul(-u, u), u) : ((-u) * u) * u;
     return 0.0;
+}
+
+// result of owned local node li: u_out, plus the neighbours' mailboxes when the
+// launch carries fused peer stores (lmep_halo.push_*: first / last push_w nodes)
+__device__ __forceinline__ void store_out(const StepParams &p, int64_t li, double v)
+{
+    p.u_out[li] = v;
+    if (p.push_w > 0) {
+        if (p.push_l && li < p.push_w) p.push_l[li] = v;
+        if (p.push_r && li >= p.nloc - p.push_w) p.push_r[li - (p.nloc - p.push_w)] = v;
+    }
 }
 
 __device__ __forceinline__ int64_t wrap(int64_t g, int64_t N)
@@ -462,7 +475,7 @@ step_kernel(const __grid_constant__ StepParams p)
                 bool bad = false;
                 for (int64_t i = O0 + tid; i < O1; i += nt) {
                     const double v = S(iU)[i - base];
-                    p.u_out[i - p.off] = v;
+                    store_out(p, i - p.off, v);
                     bad |= !isfinite(v);
                 }
                 if (bad) *p.flag = 1;
@@ -484,7 +497,7 @@ step_kernel(const __grid_constant__ StepParams p)
         }
         for (int64_t i = O0 + tid; i < O1; i += nt) {
             const double v = S(iU)[i - base];
-            p.u_out[i - p.off] = v;
+            store_out(p, i - p.off, v);
             if (!isfinite(v)) *p.flag = 1;
         }
     } else if constexpr (SCH == SCH_ETDRK4) {
@@ -604,7 +617,7 @@ step_kernel(const __grid_constant__ StepParams p)
                 bool bad = false;
                 for (int64_t i = O0 + tid; i < O1; i += nt) {
                     const double v = S(sl[U])[i - base];
-                    p.u_out[i - p.off] = v;
+                    store_out(p, i - p.off, v);
                     bad |= !isfinite(v);
                 }
                 if (bad) *p.flag = 1;
@@ -758,7 +771,7 @@ step_kernel(const __grid_constant__ StepParams p)
         }
         for (int64_t i = O0 + tid; i < O1; i += nt) {
             const double v = S(sl[U])[i - base];
-            p.u_out[i - p.off] = v;
+            store_out(p, i - p.off, v);
             if (!isfinite(v)) *p.flag = 1;
         }
     } else {  // SCH_ETD2: exponential multistep of order ETDS (timestep.py:187-215)
@@ -916,7 +929,7 @@ step_kernel(const __grid_constant__ StepParams p)
         for (int i = 1; i < so; ++i) XQ[i - 1] = S(iq[i - 1]);
         for (int64_t i = O0 + tid; i < O1; i += nt) {
             const double v = S(iU)[i - base];
-            p.u_out[i - p.off] = v;
+            store_out(p, i - p.off, v);
 #pragma unroll
             for (int j = 1; j < so; ++j) p.q_out[(int64_t)(j - 1) * p.qld + (i - p.off)] = XQ[j - 1][i - base];
             bad |= !isfinite(v);

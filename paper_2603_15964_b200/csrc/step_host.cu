@@ -322,6 +322,13 @@ int run_steps(const StepCall &c)
             p.hl = c.halo->left; p.hr = c.halo->right;
             p.qhl = c.halo->hist_left; p.qhr = c.halo->hist_right;
             p.G = c.halo->width;
+            if (c.halo->push_width > 0 && (c.halo->push_left || c.halo->push_right)) {
+                // fused peer stores: the shared / class-row step_kernel launches only
+                if (pernode || c.sch == SCH_ETD2 || c.halo->push_width > g.nloc) return LMEP_INVALID_CONFIG;
+                p.push_l = c.halo->push_left;
+                p.push_r = c.halo->push_right;
+                p.push_w = c.halo->push_width;
+            }
         }
         if (tma_path)
             rc = launch_lin_pernode_tma(p, (c.flags & LMEP_FLAG_EXACT) != 0, c.stream);      // persistent, TMA-pipelined (C5)

@@ -155,7 +155,7 @@ __device__ __forceinline__ void etdrk4_regs_pointwise(const StepParams &p, doubl
     bool bad = false;
     for (int64_t i = O0 + threadIdx.x; i < O1; i += blockDim.x) {
         const double v = XU[i - base];
-        p.u_out[i - p.off] = v;
+        store_out(p, i - p.off, v);
         bad |= !isfinite(v);
     }
     if (bad) *p.flag = 1;
@@ -268,7 +268,7 @@ __device__ __forceinline__ void etdrk4_regs_convective(const StepParams &p, doub
     bool bad = false;
     for (int64_t i = O0 + threadIdx.x; i < O1; i += blockDim.x) {
         const double v = XU[i - base];
-        p.u_out[i - p.off] = v;
+        store_out(p, i - p.off, v);
         bad |= !isfinite(v);
     }
     if (bad) *p.flag = 1;

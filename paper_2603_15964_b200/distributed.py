@@ -111,6 +111,33 @@ class Comm:
         nat.check(nat.lib().lmep_halo_exchange(self.h, k, fp, nloc, int(width), lp, rp, s),
                   "lmep_halo_exchange")
 
+    # ---- peer transport, piecewise (fused peer stores in the step launches) ----
+    def targets(self, field: int = 0):
+        """Peer pointers where this rank's left / right edge goes for its next signal."""
+        a, b = C.c_void_p(), C.c_void_p()
+        nat.check(nat.lib().lmep_comm_targets(self.h, field, C.byref(a), C.byref(b)),
+                  "lmep_comm_targets")
+        return a.value, b.value
+
+    def ghosts(self, field: int = 0):
+        """This rank's own mailbox slots of the latest exchange (left, right ghosts)."""
+        a, b = C.c_void_p(), C.c_void_p()
+        nat.check(nat.lib().lmep_comm_ghosts(self.h, field, C.byref(a), C.byref(b)),
+                  "lmep_comm_ghosts")
+        return a.value, b.value
+
+    def push(self, fields, width: int) -> None:
+        k = len(fields)
+        fp = (C.c_void_p * k)(*[f.data_ptr() for f in fields])
+        nat.check(nat.lib().lmep_comm_push(self.h, k, fp, fields[0].numel(), int(width),
+                                           nat.stream_handle()), "lmep_comm_push")
+
+    def signal(self) -> None:
+        nat.check(nat.lib().lmep_comm_signal(self.h, nat.stream_handle()), "lmep_comm_signal")
+
+    def wait(self) -> None:
+        nat.check(nat.lib().lmep_comm_wait(self.h, nat.stream_handle()), "lmep_comm_wait")
+
     def gather(self, u: torch.Tensor, counts, out: torch.Tensor | None, root: int = 0) -> None:
         cn = (C.c_int64 * self.world)(*[int(c) for c in counts])
         nat.check(nat.lib().lmep_comm_gather(self.h, u.data_ptr(), cn, nat.ptr(out), root,
@@ -349,16 +376,24 @@ class ShardedStepper:
             graph = comm_ex and exchanger.comm.transport == "nccl"
         self.graph = bool(graph and comm_ex and self.sharded and
                           exchanger.comm.transport == "nccl")
+        # peer transport: the step launches store their edges into the neighbours'
+        # mailboxes themselves and read their ghosts straight out of their own
+        self.fused = bool(self.overlap and exchanger.comm.transport == "peer")
+        self._pushed_w = 0
+        self._side = None
         self._graphs: dict = {}
         self._seen: set = set()
         dev = nat.device()
         self.flag = torch.zeros(4, dtype=torch.int32, device=dev)
         G = max(width, 1)
         nh = max(scheme.s - 1, 1) if scheme.kind == "etd-multistep" else 1
-        self.gl = torch.zeros(G, dtype=torch.float64, device=dev)
-        self.gr = torch.zeros(G, dtype=torch.float64, device=dev)
-        self.ql = torch.zeros(nh * G, dtype=torch.float64, device=dev)   # [s-1][width] ghosts
-        self.qr = torch.zeros(nh * G, dtype=torch.float64, device=dev)
+        # ghost cells (u and the [s-1][width] multistep history): one slab has none
+        if self.sharded:
+            ghosts = torch.zeros((2 + 2 * nh) * G, dtype=torch.float64, device=dev)
+            self.gl, self.gr = ghosts[:G], ghosts[G:2 * G]
+            self.ql, self.qr = ghosts[2 * G:(2 + nh) * G], ghosts[(2 + nh) * G:]
+        else:
+            self.gl = self.gr = self.ql = self.qr = None
         self.u = None
         self._out = None
         self.hist = None
@@ -381,6 +416,7 @@ class ShardedStepper:
         self._out = torch.empty_like(self.u)
         self._graphs.clear()
         self._seen.clear()
+        self._pushed_w = 0
 
     def _width(self, k, scheme=None):
         ext = _ext(scheme or self.prep.scheme, self.prep.nl)
@@ -476,16 +512,62 @@ class ShardedStepper:
         _ops.step(sch, p.bank, u[nloc - w:], k, out=out[nloc - w:], off=off + nloc - w, nloc=w,
                   halo=(u[nloc - 2 * w:nloc - w], gr, None, None, w), flag=self.flag[3:4], **kw)
 
-    def _enqueue(self, k: int) -> None:
-        if self._can_split(k):
+    def _enqueue_fused(self, k: int, k_next: int) -> None:
+        """Peer transport: no exchange kernels between chunks.  The interior
+        sub-slab starts at once on the side stream; the step stream waits for
+        the neighbours' signal, runs the two edge strips with their ghosts read
+        in place from this rank's mailbox, and those launches store the next
+        chunk's edges straight into the neighbours' mailboxes (peer memory)."""
+        p, cm = self.prep, self.ex.comm
+        w, nloc, off = self._width(k), self.plan.nloc, self.plan.off
+        u, out = self.u, self._out
+        if self._pushed_w < w:              # first chunk: the edges go through the push kernel
+            cm.push([u], w)
+        wn = min(self._width(k_next), w) if k_next > 0 else 0
+        tl, tr = cm.targets(0) if wn else (None, None)
+        sch = nat.SCH_LIN if p.scheme == "linear" else nat.SCH_ETDRK4
+        kw = dict(bc=p.bc, nl=p.nl, exact=self.exact, tuning=self._tuning(k))
+        if nloc >= 3 * w:
+            if self._side is None:
+                self._side = torch.cuda.ExternalStream(cm.side_stream)
+            cm.fork()
+            with torch.cuda.stream(self._side):
+                _ops.step(sch, p.bank, u[w:nloc - w], k, out=out[w:nloc - w], off=off + w,
+                          nloc=nloc - 2 * w, halo=(u[:w], u[nloc - w:], None, None, w),
+                          flag=self.flag[1:2], **kw)
+            cm.wait()
+            gl, gr = cm.ghosts(0)
+            _ops.step(sch, p.bank, u[:w], k, out=out[:w], off=off, nloc=w,
+                      halo=(gl, u[w:2 * w], None, None, w, tl, None, wn), flag=self.flag[2:3], **kw)
+            _ops.step(sch, p.bank, u[nloc - w:], k, out=out[nloc - w:], off=off + nloc - w, nloc=w,
+                      halo=(u[nloc - 2 * w:nloc - w], gr, None, None, w, None, tr, wn),
+                      flag=self.flag[3:4], **kw)
+            if wn:
+                cm.signal()
+            cm.join()
+        else:
+            cm.wait()
+            gl, gr = cm.ghosts(0)
+            _ops.step(sch, p.bank, u, k, out=out, off=off, nloc=nloc,
+                      halo=(gl, gr, None, None, w, tl, tr, wn), flag=self.flag[1:2], **kw)
+            if wn:
+                cm.signal()
+        self._pushed_w = wn
+
+    def _enqueue(self, k: int, k_next: int = 0) -> None:
+        if self.fused:
+            self._enqueue_fused(k, k_next)
+        elif self._can_split(k):
             self._enqueue_split(k)
         else:
             self.exchange_phase(k)
             self._launch(k)
 
-    def step_chunk(self, k: int) -> None:
-        """k <= plan.ksteps steps with one halo exchange.  With LocalHalo the
-        caller must run exchange_phase on all shards before compute_phase."""
+    def step_chunk(self, k: int, k_next: int = 0) -> None:
+        """k <= plan.ksteps steps with one halo exchange (k_next: the size of the
+        chunk that follows, so a fused launch can store its halo ahead).  With
+        LocalHalo the caller must run exchange_phase on all shards before
+        compute_phase."""
         if self.graph and nat.stream_handle() != 0:     # the legacy stream cannot be captured
             # one graph per (k, ping-pong direction): run a chunk shape once
             # eagerly (NCCL connects, kernels get their attributes), capture it
@@ -502,7 +584,7 @@ class ShardedStepper:
                 self._seen.add(key)
                 self._enqueue(k)
         else:
-            self._enqueue(k)
+            self._enqueue(k, k_next)
         self._swap()
         self.done += k
 
@@ -751,7 +833,7 @@ def advance_all(st: ShardedStepper, steps: int) -> None:
             todo -= 1
     while todo > 0:
         k = min(st.plan.ksteps, todo)
-        st.step_chunk(k)
+        st.step_chunk(k, min(st.plan.ksteps, todo - k))
         todo -= k
 
 

@@ -199,6 +199,10 @@ def test_self_ring_stepper_bitwise(transport):
                 s = ShardedStepper(g, st, prob, scheme, dt, 0, 1, CommHalo(c), ksteps=k,
                                    force_halo=True)
                 assert s.sharded and s.plan.width > 0
+                if name in ("c1-linear", "c3-kdv"):
+                    # shared rows: interior / edge split; on the peer transport the
+                    # edge launches store the next halo into the mailboxes themselves
+                    assert s.overlap and s.fused == (transport == "peer")
                 s.set_initial(prob.initial)
                 own = torch.cuda.Stream()               # graphs need a non-default stream
                 own.wait_stream(torch.cuda.current_stream())
