@@ -446,6 +446,14 @@ int lmep_graph_end(void *stream, lmep_graph **graph);
 int lmep_graph_launch(lmep_graph *graph, void *stream);
 int lmep_graph_destroy(lmep_graph *graph);
 
+/* ETD2 (order 2) on a periodic grid with shared rows whose slabs of N / #SMs
+ * nodes fit three nodes per thread (N up to ~75k; BASELINE config 2): 1
+ * (default) = the whole run in ONE cooperative launch, state resident on chip,
+ * neighbour CTAs trading halos through L2 every K <= 24 steps
+ * (step_etd2_persist.cu); 0 = the tiled launches.  Per-device; bit-identical
+ * either way in the exact mode. */
+int lmep_set_etd2_persistent(int on);
+
 /* ---- stepping (K3, K4, K5) ---------------------------------------------- */
 
 /* Linear banded propagation u <- W u for `steps` steps (kernels.py:33-43,

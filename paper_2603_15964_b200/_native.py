@@ -50,7 +50,7 @@ EXPORTS = (
     "lmep_comm_flag_max", "lmep_comm_side_stream", "lmep_comm_fork", "lmep_comm_join",
     "lmep_graph_begin", "lmep_graph_end", "lmep_graph_launch", "lmep_graph_destroy",
     "lmep_comm_targets", "lmep_comm_push", "lmep_comm_signal", "lmep_comm_wait",
-    "lmep_comm_ghosts",
+    "lmep_comm_ghosts", "lmep_set_etd2_persistent",
 )
 COMM_NCCL, COMM_PEER = 0, 1
 COMM_ID_BYTES, COMM_BLOB_BYTES, COMM_MAX_FIELDS = 128, 512, 8
@@ -149,6 +149,7 @@ def load(path: str | None = None):
     L.lmep_set_harvest_method.argtypes = [C.c_int]
     L.lmep_set_ring_cluster.argtypes = [C.c_int]
     L.lmep_set_pernode_kernel.argtypes = [C.c_int]
+    L.lmep_set_etd2_persistent.argtypes = [C.c_int]
     L.lmep_harvest_ex.argtypes = [C.POINTER(LmepHarvestArgs), vp]
     L.lmep_status_any.argtypes = [vp, i64, vp, vp]
     L.lmep_combine.argtypes = [C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_int64),
@@ -242,6 +243,12 @@ def set_pernode_kernel(variant: str) -> None:
     registers, slot-major halo exchange) or "window" (shared-memory windows)."""
     check(lib().lmep_set_pernode_kernel({"registers": 1, "window": 0, "auto": 2, "registers2": 3}[variant]),
           "lmep_set_pernode_kernel")
+
+
+def set_etd2_persistent(on: bool) -> None:
+    """ETD2 on mid-size periodic grids: one cooperative launch for the whole run
+    (default) or the tiled launches."""
+    check(lib().lmep_set_etd2_persistent(1 if on else 0), "lmep_set_etd2_persistent")
 
 
 def set_ring_cluster(on: bool) -> None:

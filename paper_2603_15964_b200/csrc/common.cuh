@@ -52,6 +52,7 @@ struct DeviceSettings {
     std::atomic<int> mvc{1};              // constant-table kernel when eligible
     std::atomic<int> ring_cluster{1};     // linear ring mode on a thread-block cluster
     std::atomic<int> pernode_kernel{2};   // TMA per-node steps: 1 registers, 0 window, 2 auto
+    std::atomic<int> etd2_persistent{1};  // ETD2 on mid-size periodic grids: one cooperative launch
 };
 DeviceSettings &device_settings();
 

@@ -971,6 +971,7 @@ int launch_lin_pernode(const StepParams &p, cudaStream_t st);
 int launch_lin_pernode_tb(const StepParams &p, bool exact, cudaStream_t st);
 int tb_nodes_per_cta(int n, bool tma);
 int launch_lin_pernode_tma(const StepParams &p, bool exact, cudaStream_t st);
+int try_launch_etd2_persistent(StepParams &p, int nl, bool exact, int64_t steps, cudaStream_t st);
 #define STEP_DECL(S, L) \
     int launch_scheme_##S##_##L(bool exact, const StepParams &p, dim3 grid, size_t shm, cudaStream_t st);
 STEP_DECL(etdrk4, none)

@@ -275,6 +275,17 @@ int run_steps(const StepCall &c)
     cudaMemsetAsync(flag, 0, sizeof(int), c.stream);
     p.flag = flag;
 
+    // ETD2 on a mid-size periodic grid with shared rows (C2): the whole run in one
+    // cooperative launch, the state resident on chip (step_etd2_persist.cu)
+    if (c.sch == SCH_ETD2 && c.etds == 2 && !sharded && !t.ring && g.periodic &&
+        w.mode == LMEP_W_SHARED && bck == LMEP_BC_NONE && !(c.tuning && (c.tuning->tile > 0 || c.tuning->ksteps > 0))) {
+        p.u_in = c.u_in; p.u_out = c.u_out; p.q_in = c.q_in; p.q_out = c.q_out;
+        const int prc = try_launch_etd2_persistent(p, c.nl, (c.flags & LMEP_FLAG_EXACT) != 0, c.steps, c.stream);
+        if (prc >= 0) {
+            if (own_flag) cudaFreeAsync(own_flag, c.stream);
+            return prc;
+        }
+    }
     const int64_t kmax = t.ksteps;
     const int64_t nlaunch = (c.steps + kmax - 1) / kmax;
     if (sharded) {

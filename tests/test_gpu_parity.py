@@ -673,6 +673,51 @@ def test_burgers_etd_multistep_orders(lx, golden, s):
     assert np.array_equal(a.u_final, b.u_final)
 
 
+@pytest.mark.parametrize("N,n,kind,steps", [(65536, 9, "convective", 203), (20000, 13, "convective", 37),
+                                            (30011, 7, "cubic", 50), (40960, 11, "none", 33),
+                                            (9001, 7, "cubic", 20),
+                                            (70000, 9, "convective", 17)])
+def test_etd2_persistent_launch_bitwise(lx, N, n, kind, steps):
+    """ETD2 on mid-size periodic grids runs as ONE cooperative launch with the
+    state resident on chip (step_etd2_persist.cu, config 2's schedule); it must
+    reproduce the tiled launches bit for bit in the exact order (u and the
+    history), and stay within 1e-12 of them with fused multiply-adds."""
+    import torch
+    from paper_2603_15964_b200 import _native as nat, _ops
+    from paper_2603_15964_b200.timestep import Stepper, prepare
+    g = lx.make_periodic_grid(N, 0.0, 2 * math.pi)
+    st = lx.select_stencils(g, n, lx.StencilPolicy.CENTERED)
+    rng = np.random.default_rng(N + n)
+    u0 = np.sin(g.nodes) + 0.1 * np.sin(7 * g.nodes + rng.uniform(0, 6.0))
+    prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(((2, 0.01),)), None, u0,
+                                lx.Boundary.periodic(), kind)
+    dt = 0.5 * (2 * math.pi / N) ** 2 / 0.01
+    prep = prepare(g, st, prob, lx.SchemeConfig("etd-multistep", s=2), dt)
+    out = {}
+    for exact in (True, False):
+        for on in (True, False):
+            nat.set_etd2_persistent(on)
+            try:
+                sp = Stepper(prep, _ops.dev_f64(u0), exact=exact)
+                L0 = nat.lib().lmep_launch_count()
+                sp.advance(steps)
+                torch.cuda.synchronize()
+                launches = nat.lib().lmep_launch_count() - L0
+            finally:
+                nat.set_etd2_persistent(True)
+            assert not sp.nonfinite()
+            out[(exact, on)] = (sp.u.clone(), sp.hist.clone(), launches)
+    # warm-up ETDRK4 step + one launch for all the multistep steps (grids too small
+    # for 64 nodes per SM keep the tiled launches)
+    if N >= 20000:
+        assert out[(True, True)][2] == 2 and out[(True, False)][2] > 2, [v[2] for v in out.values()]
+    assert torch.equal(out[(True, True)][0], out[(True, False)][0])
+    assert torch.equal(out[(True, True)][1], out[(True, False)][1])
+    a, b = out[(False, True)][0].cpu().numpy(), out[(False, False)][0].cpu().numpy()
+    assert rel_l2(a, b) < 1e-12
+    assert rel_l2(a, out[(True, True)][0].cpu().numpy()) < 1e-10
+
+
 @pytest.mark.parametrize("s", [1, 2, 3, 4, 5])
 def test_etd_multistep_linear_consistency(lx, s):
     """With N == 0 every order reduces to the linear propagator exactly in
