@@ -464,6 +464,10 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
             cur.wait_event(wait)
         st.advance(k)
         ev_b.record(cur)
+        # the snapshot's D2H is queued behind the steps at once (its row of snaps is
+        # only reported when the checks below pass), so the copy starts the moment
+        # the last launch ends instead of after the host has read the flags
+        new_ev = snapshot(len(times))
         cur.synchronize()
         if harvest_ns is None:
             # the harvest's status first: a failed exponential surfaces as the
@@ -477,7 +481,7 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
             raise NonFinite("time integration blew up", state=snaps[len(times) - 1].numpy().copy(),
                             time=times[-1])
         times.append(done * delta_t)
-        prev_ev, snap_ev = snap_ev, snapshot(len(times) - 1)
+        prev_ev, snap_ev = snap_ev, new_ev
     if harvest_ns is None:
         # zero steps (t_final below the dt rounding tolerance, _steps_for): the
         # harvest still ran and its status and time are reported (timestep.py:284)

@@ -9,7 +9,7 @@ for c in ${2:-c1 c2 c3 c4}; do
   timeout 300 python tools/prof_cases.py $c --reps $R $F > $O/$c.json 2>&1 || continue
   case $c in
     c1) K="regex:ring_lin"; S=1 ;;
-    c2) K="regex:step_kernel"; S=3 ;;
+    c2) K="regex:etd2_persist"; S=1 ;;
     *) K="regex:step_kernel"; S=3 ;;
   esac
   timeout 900 ncu --set full --clock-control none --import-source on -k $K -s $S -c 1 -o $O/$c \
