@@ -416,7 +416,7 @@ def time_c4_sharded(rank, world):
     own = torch.cuda.Stream()                     # chunks replay from CUDA graphs
     own.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(own):
-        advance_all(s, 4 * s.plan.ksteps)
+        advance_all(s, 24)                        # warm-up: both graph directions captured
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -706,8 +706,10 @@ def main():
         step_bytes = step_bytes_total / launches_steps
         step_note = (f"rows held in registers for {min(ks)}-{max(ks)} steps per launch: "
                      f"{step_bytes_total / (bench.nloc * w.steps):.1f} B/point-step against 120 for "
-                     "one step per launch (roofline_step_onestep); after blocking the kernel is "
-                     "bound by the per-step halo exchange + barrier and the FP64 pipe, see "
+                     "one step per launch (roofline_step_onestep); after blocking HBM is no longer "
+                     "the bound (ncu DRAM 23%, the TMA stream fully hidden): the rows fill the "
+                     "register file at two warps per scheduler, whose FMA chains alone take 482 of "
+                     "the 652 clk per step (tools/dfma_pattern.cu, tools/tmx_timing.py); see "
                      "roofline_step_fp64")
     else:
         step_bytes = bench.nloc * (8 * w.n + 16)           # u in/out + 13 rows per node
