@@ -40,7 +40,8 @@ constexpr int STEP_THREADS = 256;
 constexpr int SLOT_PAD = 24;
 constexpr int STEP_P_ETDRK4 = 7;   // consecutive outputs per thread (odd: conflict-free)
 constexpr int STEP_P_ETDRK4_CV = 5; // convective N: wider stencils, one more window per stage
-constexpr int step_p_etdrk4(int nl) { return nl == LMEP_NL_CONVECTIVE ? STEP_P_ETDRK4_CV : STEP_P_ETDRK4; }
+// pointwise N: 7 nodes per thread at n = 7 (C4), 5 for wider stencils (7 spills at 128 registers)
+constexpr int step_p_etdrk4(int nl, int n) { return (nl == LMEP_NL_CONVECTIVE || n != 7) ? STEP_P_ETDRK4_CV : STEP_P_ETDRK4; }
 constexpr int STEP_P_ETD2 = 1;
 
 struct StepParams {

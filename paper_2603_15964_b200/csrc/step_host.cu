@@ -30,7 +30,7 @@ int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded
     const int n = g.n, eL = g.row, eR = n - 1 - g.row;
     const int ext = step_ext(sch, nl);
     const int ns = nslots(sch, etds);
-    const int P = pernode ? 1 : (sch == SCH_ETD2 ? STEP_P_ETD2 : (sch == SCH_ETDRK4 ? step_p_etdrk4(nl) : 5));
+    const int P = pernode ? 1 : (sch == SCH_ETD2 ? STEP_P_ETD2 : (sch == SCH_ETDRK4 ? step_p_etdrk4(nl, n) : 5));
     const int64_t rad = (int64_t)ext * (eL + eR);
     // ring mode: whole periodic grid on one CTA for all steps
     const int64_t ring_bytes = (int64_t)ns * (g.N + n + SLOT_PAD + P) * 8;
@@ -245,7 +245,7 @@ int run_steps(const StepCall &c)
     p.tile = t.tile;
     p.threads = t.threads > 0 ? t.threads : STEP_THREADS;
     if (p.threads % 32 != 0 || p.threads > STEP_THREADS) return LMEP_INVALID_CONFIG;
-    const int P = pernode ? 1 : (c.sch == SCH_ETD2 ? STEP_P_ETD2 : (c.sch == SCH_ETDRK4 ? step_p_etdrk4(c.nl) : 5));
+    const int P = pernode ? 1 : (c.sch == SCH_ETD2 ? STEP_P_ETD2 : (c.sch == SCH_ETDRK4 ? step_p_etdrk4(c.nl, g.n) : 5));
     const int64_t rad = (int64_t)p.ext * (p.eL + p.eR);
     p.slot_len = t.ring ? (g.N + g.n + SLOT_PAD + P) : (t.tile + (int64_t)t.ksteps * rad + SLOT_PAD + P);
     p.slot_len = (p.slot_len + 3) & ~int64_t(3);

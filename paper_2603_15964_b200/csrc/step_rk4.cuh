@@ -100,7 +100,9 @@ __device__ __forceinline__ void etdrk4_regs_pointwise(const StepParams &p, doubl
         __syncthreads();
         // The a window of pass C is already final during B: it is loaded there and
         // held in registers across the barrier, so C starts on Wh a while its t2
-        // window is in flight.  (Doing the same for s12 in D spills at 128 registers.)
+        // window is in flight.  (Doing the same for s12 in D, or for wider stencils,
+        // spills at 128 registers.)
+        constexpr bool PRE = NS <= 7;
         double aw[W];
         if (act) {                                        // B: b from the n1 window; t2, s12
             double n1w[W], n0c[P], n1c[P];
@@ -112,8 +114,10 @@ __device__ __forceinline__ void etdrk4_regs_pointwise(const StepParams &p, doubl
                 n0c[q] = XU[l0 + q];
                 n1c[q] = XN[l0 + q];
             }
+            if constexpr (PRE) {
 #pragma unroll
-            for (int i = 0; i < W; ++i) aw[i] = xa[i];
+                for (int i = 0; i < W; ++i) aw[i] = xa[i];
+            }
 #pragma unroll
             for (int q = 0; q < P; ++q) {
                 const double b = band_add<NS, EX>(whu[q], p.wi[LMEP_ROW_P1HALF], n1w, q);
@@ -126,6 +130,11 @@ __device__ __forceinline__ void etdrk4_regs_pointwise(const StepParams &p, doubl
         if (act) {                                        // C: c = Wh a + P1h t2, n3 = N(c)
             double tw[W], wa[P];
             const double *xt = XT2 + (l0 - eL);
+            if constexpr (!PRE) {
+                const double *xa = XA + (l0 - eL);
+#pragma unroll
+                for (int i = 0; i < W; ++i) aw[i] = xa[i];
+            }
 #pragma unroll
             for (int i = 0; i < W; ++i) tw[i] = xt[i];
 #pragma unroll
