@@ -241,7 +241,7 @@ def set_pernode_kernel(variant: str) -> None:
     """Persistent per-node linear step kernel: "auto" (default: registers for
     fused multiply-adds, window for the exact order), "registers" (values in
     registers, slot-major halo exchange) or "window" (shared-memory windows)."""
-    check(lib().lmep_set_pernode_kernel({"registers": 1, "window": 0, "auto": 2, "registers2": 3}[variant]),
+    check(lib().lmep_set_pernode_kernel({"registers": 1, "window": 0, "auto": 2, "registers2": 3, "registers4": 4}[variant]),
           "lmep_set_pernode_kernel")
 
 

@@ -226,11 +226,11 @@ template <int NS, int EL, int J, int NT, bool EX, int MINB = 1>
 __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_constant__ StepParams p)
 {
     constexpr int ER = NS - 1 - EL;
-    static_assert(EL <= J && ER <= J && J % 2 == 0, "halo must come from the adjacent threads");
+    static_assert(EL <= 2 * J && ER <= 2 * J && J % 2 == 0, "halo must come from the two nearest threads per side");
     constexpr int SPAN = J * NT;
     constexpr int RS = SPAN + 4;                 // row slice stride (even: 16-byte aligned)
     constexpr int UL = tma_ulen(NS, SPAN);
-    constexpr int QS = NT + 2;                   // exchange slot stride (thread t at 1 + t)
+    constexpr int QS = NT + 4;                   // exchange slot stride (thread t at 2 + t)
     constexpr int W = EL + J + ER;               // window
     extern __shared__ __align__(16) double sm[];
     double *R = sm;                              // [NS][RS]
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
         for (int s = 0; s < K; ++s) {
             double *Qb = Q + (s & 1) * (J * QS);
 #pragma unroll
-            for (int j = 0; j < J; ++j) Qb[j * QS + 1 + tid] = x[j];
+            for (int j = 0; j < J; ++j) Qb[j * QS + 2 + tid] = x[j];
             if constexpr (!EX) {
                 // Fused mode: node j's sum splits into the products with this
                 // thread's own values (window slots EL .. EL+J-1: J taps per
@@ -336,10 +336,19 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
                 for (int j = 0; j < J / 2; ++j) own[j] = own_chain(j);
                 __syncthreads();
                 double hl[EL > 0 ? EL : 1], hr[ER > 0 ? ER : 1];
+                // window slot EL + o is staged node J tid + o: slot (o mod J) of thread
+                // tid + floor(o / J) -- the one or two nearest threads on each side
 #pragma unroll
-                for (int m = 0; m < EL; ++m) hl[m] = Qb[(J - EL + m) * QS + tid];          // t-1
+                for (int m = 0; m < EL; ++m) {
+                    const int o = m - EL;                                  // -EL .. -1
+                    const int dt = -((-o + J - 1) / J);                    // floor(o / J)
+                    hl[m] = Qb[(o - dt * J) * QS + 2 + tid + dt];
+                }
 #pragma unroll
-                for (int m = 0; m < ER; ++m) hr[m] = Qb[m * QS + 2 + tid];                 // t+1
+                for (int m = 0; m < ER; ++m) {
+                    const int o = J + m;
+                    hr[m] = Qb[(o % J) * QS + 2 + tid + o / J];
+                }
 #pragma unroll
                 for (int j = J / 2; j < J; ++j) own[j] = own_chain(j);
                 // halo chains, tap by tap across the nodes (independent FMAs back to back):
@@ -361,11 +370,17 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
                 __syncthreads();
                 double win[W];
 #pragma unroll
-                for (int m = 0; m < EL; ++m) win[m] = Qb[(J - EL + m) * QS + tid];          // t-1
+                for (int m = 0; m < EL; ++m) {
+                    const int o = m - EL, dt = -((-o + J - 1) / J);
+                    win[m] = Qb[(o - dt * J) * QS + 2 + tid + dt];
+                }
 #pragma unroll
                 for (int j = 0; j < J; ++j) win[EL + j] = x[j];
 #pragma unroll
-                for (int m = 0; m < ER; ++m) win[EL + J + m] = Qb[m * QS + 2 + tid];        // t+1
+                for (int m = 0; m < ER; ++m) {
+                    const int o = J + m;
+                    win[EL + J + m] = Qb[(o % J) * QS + 2 + tid + o / J];
+                }
                 // each node's ascending chain (the reference order), the J chains
                 // interleaved tap by tap
                 double acc[J];
@@ -404,11 +419,10 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
 
 // (n, row) pairs with both halo widths <= 6 that the register-resident kernel
 // is instantiated for: the centred stencils and the n = 7 one-sided ones
-template <bool EX, int NT, int MINB>
+template <bool EX, int NT, int MINB, int J = 6>
 static int launch_tmx(const StepParams &p, unsigned grid, cudaStream_t st)
 {
-    constexpr int J = 6;
-    const size_t shm = (size_t)(p.n * (J * NT + 4) + tma_ulen(p.n, J * NT) + 2 * J * (NT + 2)) * 8;
+    const size_t shm = (size_t)(p.n * (J * NT + 4) + tma_ulen(p.n, J * NT) + 2 * J * (NT + 4)) * 8;
     void (*k)(StepParams) = nullptr;
     if (p.n == 13 && p.row == 6) k = lin_pernode_tmx_kernel<13, 6, J, NT, EX, MINB>;
     else if (p.n == 11 && p.row == 5) k = lin_pernode_tmx_kernel<11, 5, J, NT, EX, MINB>;
@@ -443,6 +457,13 @@ int launch_lin_pernode_tma(const StepParams &p, bool exact, cudaStream_t st)
         // exchanges halos through shared memory the other keeps the FP64 pipe busy
         const unsigned g2 = (unsigned)(ntiles < 2 * nsm ? ntiles : 2 * nsm);
         const int rc = exact ? launch_tmx<true, 128, 2>(p, g2, st) : launch_tmx<false, 128, 2>(p, g2, st);
+        if (rc >= 0) return rc;
+        return LMEP_INVALID_CONFIG;
+    }
+    if (pk == 4) {
+        // four nodes per thread, 384 threads (three warps per scheduler): the halo
+        // comes from the two nearest threads on each side
+        const int rc = exact ? launch_tmx<true, 384, 1, 4>(p, grid, st) : launch_tmx<false, 384, 1, 4>(p, grid, st);
         if (rc >= 0) return rc;
         return LMEP_INVALID_CONFIG;
     }
@@ -484,7 +505,7 @@ extern "C" int lmep_debug_tmx_timing(long long *host_out)
 
 extern "C" int lmep_set_pernode_kernel(int variant)
 {
-    if (variant < 0 || variant > 3) return LMEP_INVALID_CONFIG;
+    if (variant < 0 || variant > 4) return LMEP_INVALID_CONFIG;
     lmep::device_settings().pernode_kernel.store(variant);
     return LMEP_OK;
 }

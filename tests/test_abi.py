@@ -58,3 +58,29 @@ def test_no_cuda_fails_loudly():
         pytest.skip("GPU present")
     with pytest.raises(errors.LocalExpError):
         _native.device()
+
+
+def test_comm_entry_points_validate_without_a_gpu():
+    """The sharded-run entry points reject bad handles / arguments before any
+    CUDA call, and creating a communicator without a device fails loudly."""
+    import ctypes as C
+    import torch
+    from paper_2603_15964_b200 import _native as nat
+    lib = nat.load()
+    assert lib.lmep_halo_exchange(None, 1, None, 10, 2, None, None, None) == nat.LMEP_INVALID_CONFIG
+    assert lib.lmep_comm_gather(None, None, None, None, 0, None) == nat.LMEP_INVALID_CONFIG
+    assert lib.lmep_comm_flag_max(None, None, 1, None) == nat.LMEP_INVALID_CONFIG
+    assert lib.lmep_comm_info(None, None, None, None, None, None) == nat.LMEP_INVALID_CONFIG
+    assert lib.lmep_comm_signal(None, None) == nat.LMEP_INVALID_CONFIG
+    assert lib.lmep_comm_wait(None, None) == nat.LMEP_INVALID_CONFIG
+    assert lib.lmep_graph_launch(None, None) == nat.LMEP_INVALID_CONFIG
+    assert lib.lmep_comm_destroy(None) == nat.LMEP_OK and lib.lmep_graph_destroy(None) == nat.LMEP_OK
+    h = C.c_void_p()
+    # rank outside the world, unknown transport, NCCL without an id, PEER without a width
+    for args in [(3, 2, 1, nat.COMM_NCCL, None, 0), (0, 1, 1, 7, None, 0), (0, 0, 1, nat.COMM_PEER, None, 8)]:
+        assert lib.lmep_comm_init(C.byref(h), *args) == nat.LMEP_INVALID_CONFIG, args
+    if not torch.cuda.is_available():
+        from paper_2603_15964_b200 import errors
+        from paper_2603_15964_b200.distributed import Comm
+        with pytest.raises(errors.LocalExpError):
+            Comm(0, 1, True, "peer", max_width=8)
