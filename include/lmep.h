@@ -324,8 +324,11 @@ int lmep_set_harvest_method(int method);
 
 /* Ring mode of the linear scheme (a periodic grid resident on chip for all
  * steps, BASELINE config 1): 1 (default) = one thread-block cluster of 8 CTAs
- * exchanging halos through distributed shared memory every kb steps when
- * N % 8 == 0 (ring_lin_cluster_kernel), 0 = one CTA (ring_lin_kernel).
+ * exchanging halos through distributed shared memory every kb steps -- small
+ * rings (N % 32 == 0, N up to ~3000) with warp-private slabs held in registers
+ * and windows built by warp shuffles (ring_lin_warp_kernel), larger ones with
+ * one node per thread in shared memory (ring_lin_cluster_kernel, N % 8 == 0);
+ * 2 = the shared-memory cluster kernel only; 0 = one CTA (ring_lin_kernel).
  * Per-device setting (the current device); results are bit-identical either way. */
 int lmep_set_ring_cluster(int on);
 

@@ -251,6 +251,8 @@ def set_etd2_persistent(on: bool) -> None:
     check(lib().lmep_set_etd2_persistent(1 if on else 0), "lmep_set_etd2_persistent")
 
 
-def set_ring_cluster(on: bool) -> None:
-    """Linear ring mode on one thread-block cluster (default) or one CTA."""
-    check(lib().lmep_set_ring_cluster(1 if on else 0), "lmep_set_ring_cluster")
+def set_ring_cluster(on) -> None:
+    """Linear ring mode on one thread-block cluster (True / 1, default: small rings
+    on warp-private register slabs), the shared-memory cluster kernel only (2) or
+    one CTA (False / 0)."""
+    check(lib().lmep_set_ring_cluster(int(on)), "lmep_set_ring_cluster")

@@ -314,13 +314,16 @@ int exchange_nccl(lmep_comm *c, int nf, const double *const *fields, int64_t nlo
     // posting order, so the 2-rank ring (left == right) and the 1-rank
     // self-exchange come out right.
     NCCL_TRY(api->GroupStart());
-    for (int f = 0; f < nf; ++f) {
-        if (c->right >= 0) NCCL_TRY(api->Send(fields[f] + nloc - W, W, ncclDouble, c->right, c->nccl, st));
-        if (c->left >= 0) NCCL_TRY(api->Recv(gl[f], W, ncclDouble, c->left, c->nccl, st));
-        if (c->left >= 0) NCCL_TRY(api->Send(fields[f], W, ncclDouble, c->left, c->nccl, st));
-        if (c->right >= 0) NCCL_TRY(api->Recv(gr[f], W, ncclDouble, c->right, c->nccl, st));
+    ncclResult_t r = ncclSuccess;
+    for (int f = 0; f < nf && r == ncclSuccess; ++f) {
+        if (c->right >= 0) r = api->Send(fields[f] + nloc - W, W, ncclDouble, c->right, c->nccl, st);
+        if (r == ncclSuccess && c->left >= 0) r = api->Recv(gl[f], W, ncclDouble, c->left, c->nccl, st);
+        if (r == ncclSuccess && c->left >= 0) r = api->Send(fields[f], W, ncclDouble, c->left, c->nccl, st);
+        if (r == ncclSuccess && c->right >= 0) r = api->Recv(gr[f], W, ncclDouble, c->right, c->nccl, st);
     }
-    NCCL_TRY(api->GroupEnd());
+    const ncclResult_t e = api->GroupEnd();          // always closes the group
+    if (r != ncclSuccess) return nccl_fail("ncclSend/ncclRecv", r);
+    if (e != ncclSuccess) return nccl_fail("ncclGroupEnd", e);
     return LMEP_OK;
 }
 

@@ -25,8 +25,6 @@
 //   B  windows N_k, g:  u' = (W u + P1 N_k) + (P2 g) / dt   in place of u
 // EX instantiations keep the reference's roundings (bit-identical to the tiled
 // path and to the numba / Python loops).
-#include <stdlib.h>
-
 #include "step.cuh"
 
 namespace lmep {
@@ -211,7 +209,12 @@ int launch_pe(bool exact, const StepParams &p, const PersistArgs &a, int G, size
     const void *fn = exact ? (const void *)etd2_persist_kernel<NS, NLK, true>
                            : (const void *)etd2_persist_kernel<NS, NLK, false>;
     cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(G), dim3(PE_NT), args, shm, st);
-    if (e != cudaSuccess) { set_last_error("cudaLaunchCooperativeKernel", e); return LMEP_CUDA_ERROR; }
+    if (e != cudaSuccess) {
+        // not co-resident on this device (or no cooperative launch in this context):
+        // the caller takes the tiled launches
+        cudaGetLastError();
+        return -1;
+    }
     return launch_status("etd2_persist_kernel");
 }
 
@@ -249,8 +252,7 @@ int try_launch_etd2_persistent(StepParams &p, int nl, bool exact, int64_t steps,
         const int g2 = (int)((p.N + T - 1) / T);
         if (g2 != G) continue;                               // this G leaves an empty CTA
         const int last = (int)(p.N - (int64_t)(G - 1) * T);
-        const char *ek = getenv("LMEP_PE_K");                  // tuning experiments
-        K = (int)std::min<int64_t>(ek ? atoi(ek) : 24, steps);
+        K = (int)std::min<int64_t>(24, steps);
         while (K > 1 && (T + 2 * K * ext * reach > PE_CAP || K * ext * reach > last)) --K;
         H = K * ext * reach;
         if (T + 2 * H <= PE_CAP && H <= last) break;

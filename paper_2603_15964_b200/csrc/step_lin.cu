@@ -125,6 +125,145 @@ __global__ void __launch_bounds__(1024) ring_lin_cluster_kernel(const __grid_con
     if (bad) *p.flag = 1;
 }
 
+// Ring mode, warp-private slabs (small rings, BASELINE config 1): the same
+// cluster of C CTAs, but inside a block of kb steps nothing is shared at all.
+// Every WARP owns N / (4 C) consecutive nodes and carries its own halo of
+// kb * eL / kb * eR nodes; each lane keeps J consecutive staged nodes in
+// REGISTERS and builds its windows with warp shuffles from the one or two
+// lanes next to it.  A step is shuffles + the n-tap chain: no shared-memory
+// round trip and no barrier (the one-node-per-thread kernel above spent a
+// store, a CTA barrier and n loads per step).  The warp's stale edge lanes
+// move inward by eL / eR nodes per step and never reach its owned nodes.
+// Between blocks the warps publish their owned nodes in the CTA's shared
+// memory and gather the next halos from their own and the neighbouring CTAs'
+// (DSMEM), two cluster barriers per block as above.  Arithmetic: the
+// reference's ascending unfused chain, bit-identical.
+template <int NS, int EL, int J>
+__global__ void __launch_bounds__(128) ring_lin_warp_kernel(const __grid_constant__ StepParams p, int kb)
+{
+    constexpr int W = J + NS - 1;                               // staged offsets -EL .. J-1+ER
+    cg::cluster_group cl = cg::this_cluster();
+    const int C = (int)cl.num_blocks(), r = (int)cl.block_rank();
+    const int N = (int)p.N, M = N / C, mw = M / 4;
+    const int HL = EL * kb;
+    extern __shared__ double csm[];
+    // [2][M] this CTA's nodes between blocks, double buffered: block b gathers from
+    // half b & 1 and publishes into the other, so ONE cluster barrier per block
+    // orders both (every gather of half b & 1 precedes that barrier, and the next
+    // store into it follows the barrier after)
+    double *own = csm;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (int i = tid; i < M; i += 128) own[i] = p.u_in[(int64_t)r * M + i];
+    double w[NS];
+#pragma unroll
+    for (int j = 0; j < NS; ++j) w[j] = p.wi[LMEP_ROW_W][j];
+    // lane's staged nodes: ring index g0 + j, j < J (the warp's range starts HL before its owned nodes)
+    const int ws = r * M + wid * mw;                            // first owned node of this warp
+    int gr[J], gi[J];                                           // owner CTA and index of each staged node
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+        int g = (ws - HL + lane * J + j) % N;
+        if (g < 0) g += N;
+        gr[j] = g / M;
+        gi[j] = g % M;
+    }
+    cl.sync();
+    const int K = p.ksteps;
+    double x[J];
+    int half = 0;
+    for (int s0 = 0; s0 < K; s0 += kb, half ^= 1) {
+        const int ks = K - s0 < kb ? K - s0 : kb;
+#pragma unroll
+        for (int j = 0; j < J; ++j) x[j] = cl.map_shared_rank(own + half * M, gr[j])[gi[j]];
+        for (int st = 0; st < ks; ++st) {
+            double win[W];                                      // staged offsets -EL .. J-1+ER of this lane
+#pragma unroll
+            for (int i = 0; i < W; ++i) {
+                const int o = i - EL;
+                if (o < 0) {
+                    const int d = (-o + J - 1) / J;             // lanes to the left
+                    win[i] = __shfl_up_sync(FULL, x[o + d * J], d);
+                } else if (o < J) {
+                    win[i] = x[o];
+                } else {
+                    win[i] = __shfl_down_sync(FULL, x[o % J], o / J);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                double acc = xmul(w[0], win[j]);
+#pragma unroll
+                for (int c = 1; c < NS; ++c) acc = xadd(acc, xmul(w[c], win[j + c]));
+                x[j] = acc;
+            }
+        }
+        // owned nodes of the warp: staged offsets HL .. HL + mw - 1
+        double *nxt = own + (half ^ 1) * M;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+            const int so = lane * J + j - HL;
+            if (so >= 0 && so < mw) nxt[wid * mw + so] = x[j];
+        }
+        cl.sync();                                              // published; the old half is free
+    }
+    bool bad = false;
+    const double *fin = own + half * M;
+    for (int i = tid; i < M; i += 128) {
+        const double v = fin[i];
+        p.u_out[(int64_t)r * M + i] = v;
+        bad |= !isfinite(v);
+    }
+    if (bad) *p.flag = 1;
+}
+
+template <int J>
+static int launch_ring_warp_j(const StepParams &p, int kb, cudaStream_t st)
+{
+    void (*k)(StepParams, int) = nullptr;
+    if (p.n == 7 && p.row == 6) k = ring_lin_warp_kernel<7, 6, J>;
+    else if (p.n == 7 && p.row == 3) k = ring_lin_warp_kernel<7, 3, J>;
+    else if (p.n == 7 && p.row == 0) k = ring_lin_warp_kernel<7, 0, J>;
+    else if (p.n == 9 && p.row == 4) k = ring_lin_warp_kernel<9, 4, J>;
+    else if (p.n == 11 && p.row == 5) k = ring_lin_warp_kernel<11, 5, J>;
+    else if (p.n == 13 && p.row == 6) k = ring_lin_warp_kernel<13, 6, J>;
+    if (!k) return -1;
+    constexpr int C = 8;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = (size_t)2 * (p.N / C) * sizeof(double);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k, p, kb);
+    if (e != cudaSuccess) { set_last_error("cudaLaunchKernelEx(ring_lin_warp_kernel)", e); return LMEP_CUDA_ERROR; }
+    return launch_status("ring_lin_warp_kernel");
+}
+
+// small rings: N a multiple of 32 (8 CTAs x 4 warps) whose per-warp slab plus a
+// halo of at least 4 steps fits J <= 4 nodes per lane
+static int launch_ring_warp(const StepParams &p, cudaStream_t st)
+{
+    const int variant = device_settings().ring_cluster.load();
+    if (variant == 2) return -1;                                // 2: the shared-memory cluster kernel
+    if (p.N % 32 != 0) return -1;
+    const int mw = (int)(p.N / 32), reach2 = p.eL + p.eR;
+    if (reach2 == 0) return -1;
+    for (int J = 4; J >= 3; --J) {                              // deepest halo first: fewer cluster barriers
+        const int kb = (32 * J - mw) / reach2;
+        if (kb < 4) continue;
+        // (halo of the first lanes must come from real nodes: kb * eL, kb * eR <= N)
+        if ((int64_t)kb * std::max(p.eL, p.eR) > p.N) continue;
+        return J == 3 ? launch_ring_warp_j<3>(p, kb, st) : launch_ring_warp_j<4>(p, kb, st);
+    }
+    return -1;
+}
+
 static int launch_ring_cluster(const StepParams &p, cudaStream_t st)
 {
     constexpr int C = 8;
@@ -167,7 +306,9 @@ int launch_scheme_lin(bool pernode, const StepParams &p, dim3 grid, size_t shm, 
     if (p.ring && p.off == 0 && p.hl == nullptr && p.hr == nullptr && p.wmode == LMEP_W_SHARED &&
         (p.n == 7 || p.n == 9 || p.n == 11 || p.n == 13)) {
         if (device_settings().ring_cluster.load()) {
-            const int rc = launch_ring_cluster(p, st);
+            int rc = launch_ring_warp(p, st);        // small rings: warp-private slabs in registers
+            if (rc >= 0) return rc;
+            rc = launch_ring_cluster(p, st);
             if (rc >= 0) return rc;                  // else: shape not eligible, one-CTA kernel
         }
         constexpr int RP = 3;
@@ -368,7 +509,7 @@ int launch_lin_pernode_tb(const StepParams &p, bool exact, cudaStream_t st)
 
 extern "C" int lmep_set_ring_cluster(int on)
 {
-    if (on != 0 && on != 1) return LMEP_INVALID_CONFIG;
+    if (on < 0 || on > 2) return LMEP_INVALID_CONFIG;
     lmep::device_settings().ring_cluster.store(on);
     return LMEP_OK;
 }

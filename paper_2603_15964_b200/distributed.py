@@ -763,7 +763,7 @@ def run_sharded(grid: Grid, stencils, problem: SemiLinearProblem, scheme: Scheme
         sset = as_stencil_set(grid, stencils)
         reach = max(sset.row, sset.n - 1 - sset.row)
         comm = make_comm(rank, world, grid.periodic, transport, group,
-                         max_width=16 * 8 * max(reach, 1))
+                         max_width=max(16, ksteps or 0) * 8 * max(reach, 1))
         ex = CommHalo(comm)
     st = ShardedStepper(grid, stencils, problem, scheme, delta_t, rank, world, ex, exact=exact,
                         ksteps=ksteps, overlap=overlap, graph=graph)

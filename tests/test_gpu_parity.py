@@ -563,13 +563,17 @@ def test_c1_launch_shapes_bitwise(lx, golden, orc, tuning):
     assert np.array_equal(u, orc.run_linear(W, m, golden["c1_u0"], 123))
 
 
-@pytest.mark.parametrize("cluster", [True, False])
+@pytest.mark.parametrize("cluster", [1, 2, 0])
 @pytest.mark.parametrize("n,row,N", [(9, 4, 777), (11, 10, 1000), (13, 6, 2048), (7, 0, 96),
-                                     (7, 6, 1024), (9, 8, 4096)])
+                                     (7, 6, 1024), (9, 8, 4096), (7, 3, 1024), (9, 4, 2400),
+                                     (11, 5, 512), (13, 6, 3200), (7, 6, 64)])
 def test_ring_linear_widths_bitwise(lx, orc, n, row, N, cluster):
-    """The single-CTA ring kernel (ring_lin_kernel) over stencil widths, rows
-    (upwind, centred, downwind ghosts) and sizes that are not multiples of its
-    3-node windows: bit-identical to the reference loop (kernels.py:33-43)."""
+    """The ring kernels -- warp-private register slabs on a cluster
+    (ring_lin_warp_kernel, 1 where eligible), one node per thread on a cluster
+    (ring_lin_cluster_kernel, 2) and the single-CTA kernel (ring_lin_kernel, 0)
+    -- over stencil widths, rows (upwind, centred, downwind ghosts) and sizes
+    that are not multiples of their windows: bit-identical to the reference
+    loop (kernels.py:33-43)."""
     rng = np.random.default_rng(n * 1000 + N)
     w = rng.standard_normal(n) / n
     m = orc.members_for(N, n, row, True)

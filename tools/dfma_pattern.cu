@@ -33,6 +33,28 @@ __global__ void __launch_bounds__(256, 1) pat(const double *wsrc, double *out, i
                 }
 #pragma unroll
             for (int j = 0; j < J; ++j) x[j] = acc[j] + acc2[j];
+        } else if (MODE == 2 || MODE == 3 || MODE == 4) {   // S partial chains per node (3, 1, 4), tap-major
+            constexpr int S = MODE == 2 ? 3 : (MODE == 3 ? 1 : 4);
+            constexpr int L = (NS + S - 1) / S;
+            double a[J][S];
+#pragma unroll
+            for (int j = 0; j < J; ++j)
+#pragma unroll
+                for (int q = 0; q < S; ++q) a[j][q] = 0.0;
+#pragma unroll
+            for (int c = 0; c < L; ++c)
+#pragma unroll
+                for (int q = 0; q < S; ++q)
+#pragma unroll
+                    for (int j = 0; j < J; ++j)
+                        if (q * L + c < NS) a[j][q] = fma(w[j][q * L + c], win[j + q * L + c], a[j][q]);
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+                double t = a[j][0];
+#pragma unroll
+                for (int q = 1; q < S; ++q) t += a[j][q];
+                x[j] = t;
+            }
         } else if (MODE == 1) {    // window-major: each window value feeds all its nodes back to back
 #pragma unroll
             for (int j = 0; j < J; ++j) acc[j] = 0.0;
@@ -100,13 +122,17 @@ int main()
     cudaMemcpy(w, h, 78 * 256 * 8, cudaMemcpyHostToDevice);
     const int iters = 2000;
     long long hc[148];
-    for (int mode = 0; mode < 2; ++mode) {
+    for (int mode = 0; mode < 5; ++mode) {
         for (int rep = 0; rep < 2; ++rep) {
-            if (mode == 0) pat<0><<<148, 256>>>(w, o, iters, c); else pat<1><<<148, 256>>>(w, o, iters, c);
+            if (mode == 0) pat<0><<<148, 256>>>(w, o, iters, c);
+            else if (mode == 1) pat<1><<<148, 256>>>(w, o, iters, c);
+            else if (mode == 2) pat<2><<<148, 256>>>(w, o, iters, c);
+            else if (mode == 3) pat<3><<<148, 256>>>(w, o, iters, c);
+            else pat<4><<<148, 256>>>(w, o, iters, c);
             cudaDeviceSynchronize();
         }
         cudaMemcpy(hc, c, 148 * 8, cudaMemcpyDeviceToHost);
-        printf("mode %d: %.1f clk per step (8 warps/SM, 84 D-ops per warp-step; FP64 floor 336) err=%s\n", mode,
+        printf("mode %d (0: 2 chains/node, 1: window-major 1 chain, 2: 3 chains, 3: 1 chain tap-major, 4: 4 chains): %.1f clk per step (8 warps/SM; FP64 floor ~336) err=%s\n", mode,
                (double)hc[0] / iters, cudaGetErrorString(cudaGetLastError()));
     }
     for (int rep = 0; rep < 2; ++rep) { pat_pair<<<148, 512>>>(w, o, iters, c); cudaDeviceSynchronize(); }
