@@ -356,7 +356,7 @@ class C5:
                           self.w.steps * self.w.delta_t, exact=self.exact)
         from paper_2603_15964_b200.distributed import run_sharded
         return run_sharded(self.grid, self.sset, prob, self.scheme, self.w.delta_t,
-                           self.w.steps * self.w.delta_t, exact=self.exact)
+                           self.w.steps * self.w.delta_t, exact=self.exact, comm=self.halo().comm)
 
     @property
     def h2d_bytes(self):

@@ -710,14 +710,16 @@ def run_virtual_shards(grid: Grid, stencils, problem: SemiLinearProblem, scheme:
 def run_sharded(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
                 delta_t: float, t_final: float, snapshot_stride: float | None = None, *,
                 group=None, exact: bool = True, ksteps: int | None = None,
-                transport: str = "nccl", overlap: bool = True, graph: bool | None = None):
+                transport: str = "nccl", overlap: bool = True, graph: bool | None = None,
+                comm: Comm | None = None):
     """``timestep.run`` (timestep.py:255-394) over all ranks of a
     torch.distributed group, one GPU per rank: per-rank harvest, slab stepping
     with halo exchange, snapshots gathered on rank 0.
 
     transport: "nccl" / "peer" = the library communicator (the group only
     carries its bootstrap bytes), "torch" = torch.distributed point-to-point
-    (gloo groups stage the halos through the host).  Returns a
+    (gloo groups stage the halos through the host); comm = an existing
+    communicator of the group to reuse (creating one costs a collective).  Returns a
     SimulationResult on rank 0 and None elsewhere; every rank raises NonFinite
     when the run blows up (rank 0's carries the last finite snapshot, as
     timestep.py:345-348)."""
@@ -731,7 +733,7 @@ def run_sharded(grid: Grid, stencils, problem: SemiLinearProblem, scheme: Scheme
         with torch.cuda.stream(own):
             res = run_sharded(grid, stencils, problem, scheme, delta_t, t_final, snapshot_stride,
                               group=group, exact=exact, ksteps=ksteps, transport=transport,
-                              overlap=overlap, graph=graph)
+                              overlap=overlap, graph=graph, comm=comm)
         cur.wait_stream(own)
         return res
     import torch.distributed as dist
@@ -753,9 +755,11 @@ def run_sharded(grid: Grid, stencils, problem: SemiLinearProblem, scheme: Scheme
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     torch.cuda.synchronize(dev)
     ev[0].record(cur)
-    comm = None
+    own_comm = comm is None
     if world == 1:
-        ex = None
+        ex, comm = None, None
+    elif comm is not None:
+        ex = CommHalo(comm)
     elif transport == "torch":
         ex = TorchHalo(rank, world, grid.periodic, group)
     else:
@@ -812,7 +816,7 @@ def run_sharded(grid: Grid, stencils, problem: SemiLinearProblem, scheme: Scheme
     finally:
         harvest_ns = int(ev[0].elapsed_time(ev[1]) * 1e6)
         st._graphs.clear()
-        if comm is not None:
+        if comm is not None and own_comm:
             comm.close()
     if rank != 0:
         return None

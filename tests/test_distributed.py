@@ -230,12 +230,18 @@ def _rank_main(rank, world, port, transport, q):
         from paper_2603_15964_b200.errors import NonFinite
         torch.cuda.set_device(0)
         res = {}
+        # periodic runs share one communicator (the ring); the open chain makes its own
+        ring = None
+        if transport == "peer":
+            from paper_2603_15964_b200.distributed import make_comm
+            ring = make_comm(rank, world, True, "peer", max_width=16 * 8 * 6)
         for name, g, st, prob, scheme, dt, steps in _cases():
             if name in ("c2-etd1", "c2-etd5", "c5-rowscaled"):
                 continue
             T = (3 * steps + 1) * dt
             stride = steps * dt
-            a = run_sharded(g, st, prob, scheme, dt, T, stride, transport=transport)
+            a = run_sharded(g, st, prob, scheme, dt, T, stride, transport=transport,
+                            comm=ring if g.periodic else None)
             if rank == 0:
                 b = lx.run(g, st, prob, scheme, dt, T, stride)
                 res[name] = (bool(np.array_equal(a.snapshots, b.snapshots)),
@@ -256,6 +262,8 @@ def _rank_main(rank, world, port, transport, q):
                     res["blowup"] = (bool(np.array_equal(e.state, e2.state)), e.time == e2.time)
             else:
                 res["blowup"] = (e.state is None,)
+        if ring is not None:
+            ring.close()
         q.put((rank, res))
     except Exception as e:                                      # noqa: BLE001
         import traceback
