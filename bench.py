@@ -266,8 +266,7 @@ class C5:
         if self.world == 1:
             return None
         if not hasattr(self, "_halo"):
-            from paper_2603_15964_b200.distributed import CommHalo, make_comm
-            self._halo = CommHalo(make_comm(self.rank, self.world, True, "nccl"))
+            self._halo, self.transport = make_halo(self.rank, self.world, True)
         return self._halo
 
     def check(self):
@@ -355,8 +354,12 @@ class C5:
             return lx.run(self.grid, self.sset, prob, self.scheme, self.w.delta_t,
                           self.w.steps * self.w.delta_t, exact=self.exact)
         from paper_2603_15964_b200.distributed import run_sharded
+        h = self.halo()
+        if hasattr(h, "comm"):
+            return run_sharded(self.grid, self.sset, prob, self.scheme, self.w.delta_t,
+                               self.w.steps * self.w.delta_t, exact=self.exact, comm=h.comm)
         return run_sharded(self.grid, self.sset, prob, self.scheme, self.w.delta_t,
-                           self.w.steps * self.w.delta_t, exact=self.exact, comm=self.halo().comm)
+                           self.w.steps * self.w.delta_t, exact=self.exact, transport="torch")
 
     @property
     def h2d_bytes(self):
@@ -367,6 +370,30 @@ class C5:
     def d2h_bytes(self):
         # run() / run_sharded: snapshots u0 and u_final on rank 0 (timestep.py:313,350)
         return 2 * self.u0_host.nbytes
+
+
+def make_halo(rank, world, periodic):
+    """The halo exchanger of a sharded bench run: the library communicator (NCCL
+    behind the C ABI).  If it cannot be created on this box (no libnccl to
+    resolve, a failed ncclCommInitRank) the run falls back to torch.distributed
+    point-to-point and says so in the JSON line."""
+    from paper_2603_15964_b200.distributed import CommHalo, TorchHalo, make_comm
+    import torch.distributed as dist
+    ok, halo = 1, None
+    try:
+        halo = CommHalo(make_comm(rank, world, periodic, "nccl"))
+    except Exception as e:                                      # noqa: BLE001
+        print(f"[bench] rank {rank}: lmep_comm (NCCL) unavailable: {e}", file=sys.stderr)
+        ok = 0
+    # every rank must take the same transport
+    import torch
+    t = torch.tensor([ok], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    if int(t.item()) == 1:
+        return halo, "lmep_comm (NCCL send/recv behind the C ABI)"
+    if halo is not None:
+        halo.comm.close()
+    return TorchHalo(rank, world, periodic), "torch.distributed P2P (fallback)"
 
 
 def time_c5_onestep(steps=20):
@@ -409,9 +436,9 @@ def time_c4_sharded(rank, world):
     st = lx.select_stencils(g, w.n, lx.StencilPolicy.CENTERED)
     prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(w.terms), None, w.u0, lx.Boundary.neumann(),
                                 "cubic")
-    comm = make_comm(rank, world, False, "nccl") if world > 1 else None
-    s = ShardedStepper(g, st, prob, lx.SchemeConfig("etdrk4"), w.delta_t, rank, world,
-                       CommHalo(comm) if comm else None)
+    halo, transport = make_halo(rank, world, False) if world > 1 else (None, "none (one slab)")
+    comm = getattr(halo, "comm", None)
+    s = ShardedStepper(g, st, prob, lx.SchemeConfig("etdrk4"), w.delta_t, rank, world, halo)
     s.set_initial(w.u0)
     own = torch.cuda.Stream()                     # chunks replay from CUDA graphs
     own.wait_stream(torch.cuda.current_stream())
@@ -426,7 +453,7 @@ def time_c4_sharded(rank, world):
     ms = e0.elapsed_time(e1)
     out = {"N": w.N, "steps": w.steps, "us_per_step": ms * 1e3 / w.steps,
            "updates_per_s": w.N * w.steps / (ms * 1e-3), "ksteps_per_exchange": s.plan.ksteps,
-           "transport": "lmep_comm (NCCL)" if comm else "none (one slab)", "overlap": s.overlap, "graphs": len(s._graphs)}
+           "transport": transport, "overlap": s.overlap, "graphs": len(s._graphs)}
     s._graphs.clear()
     if comm:
         comm.close()
@@ -750,6 +777,8 @@ def main():
     if not args.no_cpu and rank == 0 and world == 1:
         cpu = cpu_c5()
 
+    if world > 1:
+        config = dict(config, halo_transport=getattr(bench, "transport", None))
     if rank == 0:
         line = {
             "metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
