@@ -471,6 +471,20 @@ int lmep_step_linear(const lmep_grid *grid, const lmep_weights *w, const lmep_bc
                      double *scratch, int64_t steps, int32_t flags,
                      const lmep_tuning *tuning, int32_t *nonfinite, void *stream);
 
+/* lmep_step_linear whose result also lands in HOST memory (the snapshot
+ * timestep.run takes after each chunk, timestep.py:341-350): host_out (nloc
+ * doubles; page-locked for the copies to be asynchronous) receives u_out
+ * through copy_stream.  On the persistent per-node kernels (config 5) the last
+ * launch is issued as `parts` launches over consecutive tile ranges and every
+ * range is copied as soon as its launch has finished, so the device-to-host
+ * copy overlaps the tail of the steps; every other path copies once behind the
+ * last launch.  The caller synchronises copy_stream before reading host_out. */
+int lmep_step_linear_host(const lmep_grid *grid, const lmep_weights *w, const lmep_bc *bc,
+                          const lmep_halo *halo, const double *u_in, double *u_out,
+                          double *scratch, int64_t steps, int32_t flags,
+                          const lmep_tuning *tuning, int32_t *nonfinite, void *stream,
+                          double *host_out, int parts, void *copy_stream);
+
 /* Fused four-stage ETDRK4 (kernels.py:62-132, run_etdrk4): rows W, ALPHA, BETA,
  * GAMMA, WHALF, P1HALF (and D1 for LMEP_NL_CONVECTIVE).  nl0_out (nullable)
  * receives N(u_in) on the owned nodes (the history entry the ETD multistep

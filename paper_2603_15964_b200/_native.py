@@ -50,7 +50,7 @@ EXPORTS = (
     "lmep_comm_flag_max", "lmep_comm_side_stream", "lmep_comm_fork", "lmep_comm_join",
     "lmep_graph_begin", "lmep_graph_end", "lmep_graph_launch", "lmep_graph_destroy",
     "lmep_comm_targets", "lmep_comm_push", "lmep_comm_signal", "lmep_comm_wait",
-    "lmep_comm_ghosts", "lmep_set_etd2_persistent",
+    "lmep_comm_ghosts", "lmep_set_etd2_persistent", "lmep_step_linear_host",
 )
 COMM_NCCL, COMM_PEER = 0, 1
 COMM_ID_BYTES, COMM_BLOB_BYTES, COMM_MAX_FIELDS = 128, 512, 8
@@ -138,6 +138,7 @@ def load(path: str | None = None):
     G, W, B, H, T = (C.POINTER(LmepGrid), C.POINTER(LmepWeights), C.POINTER(LmepBC),
                      C.POINTER(LmepHalo), C.POINTER(LmepTuning))
     L.lmep_step_linear.argtypes = [G, W, B, H, vp, vp, vp, i64, i32, T, vp, vp]
+    L.lmep_step_linear_host.argtypes = [G, W, B, H, vp, vp, vp, i64, i32, T, vp, vp, vp, C.c_int, vp]
     L.lmep_step_etdrk4.argtypes = [G, W, B, H, C.c_int, vp, vp, vp, i64, vp, i32, T, vp, vp]
     L.lmep_step_etd2.argtypes = [G, W, B, H, C.c_int, dbl, vp, vp, vp, vp, vp, i64, i32, T, vp,
                                  vp]

@@ -533,7 +533,8 @@ def step(scheme: int, rows: CompactRows, u: torch.Tensor, steps: int, *, bc: BC 
          delta_t: float = 0.0, nl0_out: torch.Tensor | None = None, tuning=None,
          flag: torch.Tensor | None = None, out: torch.Tensor | None = None,
          hist_out: torch.Tensor | None = None, scratch: torch.Tensor | None = None,
-         off: int = 0, nloc: int | None = None, halo=None, etd_order: int = 2):
+         off: int = 0, nloc: int | None = None, halo=None, etd_order: int = 2,
+         host_out: torch.Tensor | None = None, copy_stream: int | None = None, host_parts: int = 4):
     """Run `steps` steps of a scheme on the whole grid, or on the shard
     [off, off+nloc) with ghost cells `halo` (see c_halo).
     Returns the new u (and the new history for ETD2)."""
@@ -552,6 +553,14 @@ def step(scheme: int, rows: CompactRows, u: torch.Tensor, steps: int, *, bc: BC 
     s = nat.stream_handle()
     fp = nat.ptr(flag)
     if scheme == nat.SCH_LIN:
+        if host_out is not None and steps > 0:
+            # the result also lands in (page-locked) host memory through copy_stream,
+            # range by range behind the last launch (lmep_step_linear_host)
+            st = L.lmep_step_linear_host(C.byref(g), C.byref(w), C.byref(b), hp, nat.ptr(u),
+                                         nat.ptr(out), nat.ptr(scratch), int(steps), flags, tp, fp,
+                                         s, host_out.data_ptr(), int(host_parts), copy_stream)
+            nat.check(st, "lmep_step_linear_host")
+            return out
         st = L.lmep_step_linear(C.byref(g), C.byref(w), C.byref(b), hp, nat.ptr(u),
                                 nat.ptr(out), nat.ptr(scratch), int(steps), flags, tp, fp, s)
         nat.check(st, "lmep_step_linear")

@@ -66,6 +66,7 @@ struct StepParams {
     int64_t G;
     double *push_l, *push_r;                    // fused peer stores of the slab edges (or null)
     int64_t push_w;
+    int64_t tile_lo, tile_hi;                   // persistent per-node kernels: tiles of this launch (hi = 0: all)
     double *nl0_out;
     double dt;
     double dtj[6];                              // etd-s: dt**j as Python computes it

@@ -153,6 +153,11 @@ struct StepCall {
     int32_t *nonfinite;
     double *nl0_out;
     cudaStream_t stream;
+    // lmep_step_linear_host: the result also lands in host memory, the last launch
+    // split into `parts` tile ranges whose copies overlap the remaining ranges
+    double *host_out = nullptr;
+    int parts = 1;
+    cudaStream_t copy_stream = nullptr;
 };
 
 int run_steps(const StepCall &c)
@@ -306,6 +311,7 @@ int run_steps(const StepCall &c)
     const dim3 grid(t.ring ? 1u : (unsigned)((g.nloc + t.tile - 1) / t.tile));
     const double *src = c.u_in, *qsrc = c.q_in;
     int rc = LMEP_OK;
+    bool host_copied = false;
     int64_t done = 0;
     // persistent TMA per-node kernel: the steps spread evenly over the launches, each
     // launch's tile widened to the span its k leaves (tile + k (n-1) = span): C5's
@@ -341,7 +347,31 @@ int run_steps(const StepCall &c)
                 p.push_w = c.halo->push_width;
             }
         }
-        if (tma_path)
+        if (tma_path && c.host_out && L == nlaunch - 1 && c.parts > 1) {
+            // last launch, result wanted on the host: one launch per tile range, each
+            // range copied on the copy stream as soon as its launch has finished
+            const int64_t ntl = (g.nloc + p.tile - 1) / p.tile;
+            const int parts = (int)std::min<int64_t>(c.parts, std::max<int64_t>(1, ntl / (2 * num_sms())));
+            cudaEvent_t ev;
+            for (int part = 0; part < parts && rc == LMEP_OK; ++part) {
+                p.tile_lo = ntl * part / parts;
+                p.tile_hi = ntl * (part + 1) / parts;
+                rc = launch_lin_pernode_tma(p, (c.flags & LMEP_FLAG_EXACT) != 0, c.stream);
+                if (rc) break;
+                const int64_t a = p.tile_lo * p.tile, b = std::min<int64_t>(g.nloc, p.tile_hi * p.tile);
+                if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+                    cudaEventRecord(ev, c.stream) != cudaSuccess ||
+                    cudaStreamWaitEvent(c.copy_stream, ev, 0) != cudaSuccess ||
+                    cudaMemcpyAsync(c.host_out + a, dst + a, (size_t)(b - a) * 8, cudaMemcpyDeviceToHost,
+                                    c.copy_stream) != cudaSuccess) {
+                    set_last_error("lmep_step_linear_host (part copy)", cudaGetLastError());
+                    rc = LMEP_CUDA_ERROR;
+                }
+                cudaEventDestroy(ev);                // released once the recorded work completes
+            }
+            p.tile_lo = p.tile_hi = 0;
+            host_copied = true;
+        } else if (tma_path)
             rc = launch_lin_pernode_tma(p, (c.flags & LMEP_FLAG_EXACT) != 0, c.stream);      // persistent, TMA-pipelined (C5)
         else if (c.sch == SCH_LIN && pernode && p.bc == LMEP_BC_NONE && g.periodic &&
             t.threads == 256 && t.tile + (int64_t)t.ksteps * (g.n - 1) == tb_nodes_per_cta(g.n, false))
@@ -354,6 +384,19 @@ int run_steps(const StepCall &c)
         src = dst;
         qsrc = qdst;
         done += k;
+    }
+    if (rc == LMEP_OK && c.host_out && !host_copied) {
+        // every other path: one copy behind the last launch
+        cudaEvent_t ev;
+        if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventRecord(ev, c.stream) != cudaSuccess ||
+            cudaStreamWaitEvent(c.copy_stream, ev, 0) != cudaSuccess ||
+            cudaMemcpyAsync(c.host_out, c.u_out, (size_t)g.nloc * 8, cudaMemcpyDeviceToHost,
+                            c.copy_stream) != cudaSuccess) {
+            set_last_error("lmep_step_linear_host (copy)", cudaGetLastError());
+            rc = LMEP_CUDA_ERROR;
+        }
+        cudaEventDestroy(ev);
     }
     if (own_scr) cudaFreeAsync(own_scr, c.stream);
     if (own_flag) cudaFreeAsync(own_flag, c.stream);
@@ -385,6 +428,21 @@ extern "C" int lmep_step_linear(const lmep_grid *grid, const lmep_weights *w, co
     // per-node kernels (FP64-issue-bound); every other linear kernel is always exact
     c.u_in = u_in; c.u_out = u_out; c.scratch = scratch; c.steps = steps; c.flags = flags;
     c.tuning = tuning; c.nonfinite = nonfinite; c.stream = (cudaStream_t)stream;
+    return run_steps(c);
+}
+
+extern "C" int lmep_step_linear_host(const lmep_grid *grid, const lmep_weights *w, const lmep_bc *bc,
+                                     const lmep_halo *halo, const double *u_in, double *u_out,
+                                     double *scratch, int64_t steps, int32_t flags,
+                                     const lmep_tuning *tuning, int32_t *nonfinite, void *stream,
+                                     double *host_out, int parts, void *copy_stream)
+{
+    if (!host_out || parts < 1 || steps < 1) return LMEP_INVALID_CONFIG;
+    StepCall c{};
+    c.sch = SCH_LIN; c.grid = grid; c.w = w; c.bc = bc; c.halo = halo; c.nl = 0;
+    c.u_in = u_in; c.u_out = u_out; c.scratch = scratch; c.steps = steps; c.flags = flags;
+    c.tuning = tuning; c.nonfinite = nonfinite; c.stream = (cudaStream_t)stream;
+    c.host_out = host_out; c.parts = parts; c.copy_stream = (cudaStream_t)copy_stream;
     return run_steps(c);
 }
 

@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(NT, 1) lin_pernode_tma_kernel(const __grid_con
     const int tid = threadIdx.x;
     const int K = p.ksteps;
     const int eL = p.row, eR = NS - 1 - p.row;
-    const int64_t ntiles = (p.nloc + p.tile - 1) / p.tile;
+    const int64_t ntiles = p.tile_hi > 0 ? p.tile_hi : (p.nloc + p.tile - 1) / p.tile;
 
     for (int i = tid; i < NS * RS + 3 * UL; i += NT) sm[i] = 0.0;
     if (tid == 0) {
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(NT, 1) lin_pernode_tma_kernel(const __grid_con
         copy_wrapped(Ub + b * UL + org - r.o, p.u_in, p.N, r.start, r.cnt, &bar);
     };
 
-    int64_t tile = blockIdx.x;
+    int64_t tile = p.tile_lo + blockIdx.x;
     if (tid == 0 && tile < ntiles) issue(tile, 0);
     bool bad = false;
     for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
     const int tid = threadIdx.x;
     const int K = p.ksteps;
     const int eL = EL, eR = ER;
-    const int64_t ntiles = (p.nloc + p.tile - 1) / p.tile;
+    const int64_t ntiles = p.tile_hi > 0 ? p.tile_hi : (p.nloc + p.tile - 1) / p.tile;
 
     for (int i = tid; i < NS * RS + UL + 2 * J * QS; i += NT) sm[i] = 0.0;
     if (tid == 0) {
@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
         copy_wrapped(Ub + org - r.o, p.u_in, p.N, r.start, r.cnt, &bar);
     };
 
-    int64_t tile = blockIdx.x;
+    int64_t tile = p.tile_lo + blockIdx.x;
     if (tid == 0 && tile < ntiles) issue(tile);
     bool bad = false;
     for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
@@ -442,7 +442,7 @@ int launch_lin_pernode_tma(const StepParams &p, bool exact, cudaStream_t st)
 {
     constexpr int J = 3, NT = 512;
     const size_t shm = tma_smem_bytes(p.n, J * NT);
-    const int64_t ntiles = (p.nloc + p.tile - 1) / p.tile;
+    const int64_t ntiles = (p.tile_hi > 0 ? p.tile_hi : (p.nloc + p.tile - 1) / p.tile) - p.tile_lo;
     const int nsm = device_sm_count();
     const unsigned grid = (unsigned)(ntiles < nsm ? ntiles : nsm);
     if ((p.N & 1) || (p.wld & 1) || ((uintptr_t)p.wp & 15) || ((uintptr_t)p.u_in & 15))

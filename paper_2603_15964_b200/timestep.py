@@ -327,14 +327,19 @@ class Stepper:
         self._scr = torch.empty(max(prep.s, 2) * N, dtype=torch.float64, device=u0.device)
         self._hout = None
 
-    def advance(self, k: int) -> None:
+    def advance(self, k: int, host_out: torch.Tensor | None = None,
+                copy_stream: int | None = None) -> None:
+        """k more steps.  host_out (linear scheme): a page-locked host vector that
+        also receives the result through copy_stream (a raw stream handle), copied
+        range by range behind the last launch (lmep_step_linear_host)."""
         p = self.p
         kw = dict(bc=p.bc, nl=p.nl, exact=self.exact, tuning=self.tuning, flag=self.flag,
                   scratch=self._scr)
         if k <= 0:
             return
         if p.scheme == "linear":
-            out = _ops.step(nat.SCH_LIN, p.bank, self.u, k, out=self._out, **kw)
+            out = _ops.step(nat.SCH_LIN, p.bank, self.u, k, out=self._out, host_out=host_out,
+                            copy_stream=copy_stream, **kw)
             self._out, self.u = self.u, out
         elif p.scheme == "etdrk4":
             out = _ops.step(nat.SCH_ETDRK4, p.bank, self.u, k, out=self._out, **kw)
@@ -462,12 +467,20 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
         wait = prev_ev if prep.scheme in ("linear", "etdrk4") else snap_ev
         if wait is not None:
             cur.wait_event(wait)
-        st.advance(k)
-        ev_b.record(cur)
-        # the snapshot's D2H is queued behind the steps at once (its row of snaps is
-        # only reported when the checks below pass), so the copy starts the moment
-        # the last launch ends instead of after the host has read the flags
-        new_ev = snapshot(len(times))
+        if prep.scheme == "linear":
+            # the library copies the snapshot itself, range by range behind the last
+            # launch (its tail overlaps the copy), straight into the page-locked row
+            st.advance(k, host_out=snaps[len(times)], copy_stream=cp.cuda_stream)
+            ev_b.record(cur)
+            st.u.record_stream(cp)
+            new_ev = cp.record_event()
+        else:
+            st.advance(k)
+            ev_b.record(cur)
+            # the snapshot's D2H is queued behind the steps at once (its row of snaps
+            # is only reported when the checks below pass), so the copy starts the
+            # moment the last launch ends instead of after the host has read the flags
+            new_ev = snapshot(len(times))
         cur.synchronize()
         if harvest_ns is None:
             # the harvest's status first: a failed exponential surfaces as the
