@@ -381,7 +381,10 @@ def make_halo(rank, world, periodic):
     import torch.distributed as dist
     ok, halo = 1, None
     try:
-        halo = CommHalo(make_comm(rank, world, periodic, "nccl"))
+        # LMEP_BENCH_TRANSPORT=peer: the CUDA-IPC mailboxes (with LMEP_BENCH_BACKEND=gloo and
+        # LMEP_BENCH_ONE_DEVICE=1 the multi-rank bench path runs on a single GPU)
+        halo = CommHalo(make_comm(rank, world, periodic, os.environ.get("LMEP_BENCH_TRANSPORT", "nccl"),
+                                  max_width=16 * 8 * 6))
     except Exception as e:                                      # noqa: BLE001
         print(f"[bench] rank {rank}: lmep_comm (NCCL) unavailable: {e}", file=sys.stderr)
         ok = 0
@@ -390,7 +393,8 @@ def make_halo(rank, world, periodic):
     t = torch.tensor([ok], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MIN)
     if int(t.item()) == 1:
-        return halo, "lmep_comm (NCCL send/recv behind the C ABI)"
+        return halo, ("lmep_comm (NCCL send/recv behind the C ABI)" if halo.comm.transport == "nccl"
+                      else "lmep_comm (CUDA-IPC peer mailboxes behind the C ABI)")
     if halo is not None:
         halo.comm.close()
     return TorchHalo(rank, world, periodic), "torch.distributed P2P (fallback)"
@@ -664,8 +668,8 @@ def main():
     import torch
     import torch.distributed as dist
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(0 if os.environ.get("LMEP_BENCH_ONE_DEVICE") else local)
+        dist.init_process_group(os.environ.get("LMEP_BENCH_BACKEND", "nccl"))
     else:
         torch.cuda.set_device(0)
     from paper_2603_15964_b200 import _native
@@ -738,6 +742,19 @@ def main():
                      "register file at two warps per scheduler, whose FMA chains alone take 482 of "
                      "the 652 clk per step (tools/dfma_pattern.cu, tools/tmx_timing.py); see "
                      "roofline_step_fp64")
+    elif world > 1:
+        # sharded slabs: lin_pernode_tb_kernel, rows in registers for the k steps a halo
+        # exchange covers (the slab also harvests its halo nodes' rows); 768-node spans
+        st_last = bench.last.get("stepper")
+        kx = int(st_last.plan.ksteps) if st_last is not None else 16
+        span = 768
+        launches_steps = -(-w.steps // kx)
+        step_bytes = bench.nloc * (8 * w.n + 8) * span / (span - kx * (w.n - 1)) + bench.nloc * 8
+        step_kernel = (f"lin_pernode_tb_kernel<13,3> (rows in registers, {kx} steps per halo "
+                       "exchange and launch)")
+        per_launch_ms = step_ms / launches_steps
+        step_note = (f"this rank's slab ({bench.nloc} nodes): rows + u of the staged ranges once per "
+                     f"{kx} steps; launch time includes the halo exchange before it")
     else:
         step_bytes = bench.nloc * (8 * w.n + 16)           # u in/out + 13 rows per node
         step_kernel = "lin_pernode_kernel<13,4> (per-node rows, one step per launch)"
