@@ -67,6 +67,7 @@ struct StepParams {
     double *push_l, *push_r;                    // fused peer stores of the slab edges (or null)
     int64_t push_w;
     int64_t tile_lo, tile_hi;                   // persistent per-node kernels: tiles of this launch (hi = 0: all)
+    int64_t ext_off;                            // ... on a slab: u_in / rows start ext_off nodes before the owned ones
     double *nl0_out;
     double dt;
     double dtj[6];                              // etd-s: dt**j as Python computes it

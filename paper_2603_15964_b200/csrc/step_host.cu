@@ -25,7 +25,7 @@ static int num_sms() { return device_sm_count(); }
 static const int64_t kSmemBudget = 200 * 1024;  // bytes per CTA we allow ourselves
 
 int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded, bool pernode,
-                lmep_tuning &t, int64_t pernode_pad, int etds, bool tma_ok)
+                lmep_tuning &t, int64_t pernode_pad, int etds, bool tma_ok, bool slab_tma = false)
 {
     const int n = g.n, eL = g.row, eR = n - 1 - g.row;
     const int ext = step_ext(sch, nl);
@@ -56,7 +56,9 @@ int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded
         // tools/c5_ksweep2.py: k = 16 11.1, 25 10.2, 40 10.6 us/step)
         const int64_t kdef = (!sharded && (g.N % 2) == 0 && g.N >= tb_nodes_per_cta(n, true)) ? 25 : 16;
         k = sharded ? steps : (t.ksteps > 0 ? t.ksteps : std::min<int64_t>(kdef, steps));
-        const bool tma = tma_ok && !sharded && (g.N % 2) == 0 && g.N >= tb_nodes_per_cta(n, true);
+        // (slab_tma: a slab whose ghosts sit right next to it and whose extended range
+        // fits the span takes the persistent kernel too)
+        const bool tma = tma_ok && (sharded ? slab_tma : ((g.N % 2) == 0 && g.N >= tb_nodes_per_cta(n, true)));
         const int64_t span = tb_nodes_per_cta(n, tma);
         while (k > 1 && span - k * (n - 1) < span / 2) --k;
         t.tile = (int32_t)(span - k * (n - 1));
@@ -203,9 +205,22 @@ int run_steps(const StepCall &c)
     if (sharded) { t.ring = 0; }
     // the TMA kernel bulk-copies u_in and the rows: both 16-byte aligned (a
     // contiguous view at an odd element offset takes the register-blocked kernel)
-    const bool tma_ok = ((uintptr_t)c.u_in & 15) == 0 && ((uintptr_t)w.pernode & 15) == 0;
+    bool tma_ok = ((uintptr_t)c.u_in & 15) == 0 && ((uintptr_t)w.pernode & 15) == 0;
+    // a slab of a sharded per-node run whose ghost cells are stored right around it
+    // ([ghosts | u | ghosts] contiguous, as wide as the row table's pad): the
+    // persistent TMA kernels read that extended array like a whole grid
+    bool slab_tma = false;
+    if (sharded && pernode && c.sch == SCH_LIN && g.periodic && bck == LMEP_BC_NONE && c.halo->left &&
+        c.halo->right) {
+        const int64_t G = c.halo->width;
+        slab_tma = c.halo->left + G == c.u_in && c.halo->right == c.u_in + g.nloc && w.pernode_pad == G &&
+                   (g.nloc % 2) == 0 && ((uintptr_t)c.halo->left & 15) == 0 &&
+                   ((uintptr_t)w.pernode & 15) == 0 && g.nloc + 2 * G >= tb_nodes_per_cta(g.n, true) &&
+                   device_settings().pernode_kernel.load() != 3;
+        if (slab_tma) tma_ok = true;
+    }
     int st = plan_launch(g, c.sch, c.nl, c.steps, sharded, pernode, t, pernode ? w.pernode_pad : 0,
-                         c.etds, tma_ok);
+                         c.etds, tma_ok, slab_tma);
     if (st) return st;
 
     // host staging of the (large) parameter block, one per calling thread: the
@@ -317,7 +332,7 @@ int run_steps(const StepCall &c)
     // launch's tile widened to the span its k leaves (tile + k (n-1) = span): C5's
     // 200 steps run as 8 x 15 + 5 x 16 instead of 12 x 16 + 8
     const bool tma_path = c.sch == SCH_LIN && pernode && p.bc == LMEP_BC_NONE && g.periodic &&
-                          !sharded && t.threads == 256 &&
+                          (!sharded || slab_tma) && t.threads == 256 &&
                           t.tile + (int64_t)t.ksteps * (g.n - 1) == tb_nodes_per_cta(g.n, true);
     for (int64_t L = 0; L < nlaunch; ++L) {
         int64_t k = std::min<int64_t>(kmax, c.steps - done);
@@ -335,7 +350,12 @@ int run_steps(const StepCall &c)
         p.q_in = qsrc;
         p.q_out = qdst;
         p.nl0_out = (L == 0) ? c.nl0_out : nullptr;
-        if (sharded) {
+        if (sharded && tma_path) {
+            // the slab's extended arrays: u from its left ghosts on, the padded row table
+            p.u_in = c.halo->left;
+            p.ext_off = c.halo->width;
+            p.N = g.nloc + 2 * c.halo->width;
+        } else if (sharded) {
             p.hl = c.halo->left; p.hr = c.halo->right;
             p.qhl = c.halo->hist_left; p.qhr = c.halo->hist_right;
             p.G = c.halo->width;

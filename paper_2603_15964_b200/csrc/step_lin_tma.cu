@@ -81,8 +81,11 @@ struct TileRange {
 __device__ __forceinline__ TileRange tile_range(const StepParams &p, int64_t tile, int K, int eL, int eR)
 {
     TileRange r;
-    r.t0 = tile * p.tile;
-    r.t1 = r.t0 + p.tile < p.nloc ? r.t0 + p.tile : p.nloc;
+    // slabs (p.ext_off > 0): u_in and the row table are the slab's extended arrays
+    // [ghosts | owned | ghosts] of p.N nodes, the owned nodes ext_off .. ext_off+nloc-1;
+    // the staged ranges never wrap there
+    r.t0 = p.ext_off + tile * p.tile;
+    r.t1 = r.t0 + p.tile < p.ext_off + p.nloc ? r.t0 + p.tile : p.ext_off + p.nloc;
     r.len = (int)(r.t1 - r.t0) + K * (eL + eR);
     int64_t b = (r.t0 - (int64_t)K * eL) % p.N;
     if (b < 0) b += p.N;
@@ -124,7 +127,8 @@ __global__ void __launch_bounds__(NT, 1) lin_pernode_tma_kernel(const __grid_con
     const int eL = p.row, eR = NS - 1 - p.row;
     const int64_t ntiles = p.tile_hi > 0 ? p.tile_hi : (p.nloc + p.tile - 1) / p.tile;
 
-    for (int i = tid; i < NS * RS + 3 * UL; i += NT) sm[i] = 0.0;
+    // (the row slices are always overwritten by the bulk copies before they are read)
+    for (int i = tid; i < 3 * UL; i += NT) Ub[i] = 0.0;
     if (tid == 0) {
         mbar_init(&bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -192,7 +196,7 @@ __global__ void __launch_bounds__(NT, 1) lin_pernode_tma_kernel(const __grid_con
         }
         for (int64_t i = r.t0 + tid; i < r.t1; i += NT) {
             const double v = U0[eL + (int)(i - r.t0) + K * eL];
-            p.u_out[i] = v;
+            p.u_out[i - p.ext_off] = v;
             bad |= !isfinite(v);
         }
     }
@@ -242,7 +246,8 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
     const int eL = EL, eR = ER;
     const int64_t ntiles = p.tile_hi > 0 ? p.tile_hi : (p.nloc + p.tile - 1) / p.tile;
 
-    for (int i = tid; i < NS * RS + UL + 2 * J * QS; i += NT) sm[i] = 0.0;
+    // (the row slices are always overwritten by the bulk copies before they are read)
+    for (int i = tid; i < UL + 2 * J * QS; i += NT) Ub[i] = 0.0;
     if (tid == 0) {
         mbar_init(&bar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -403,7 +408,7 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
         for (int j = 0; j < J; ++j) {
             const int64_t i = r.t0 + (int64_t)(l0 + j - K * eL);
             if (i >= r.t0 && i < r.t1) {
-                p.u_out[i] = x[j];
+                p.u_out[i - p.ext_off] = x[j];
                 bad |= !isfinite(x[j]);
             }
         }

@@ -353,6 +353,8 @@ class ShardedStepper:
             # one chunk of nodes per thread, so its staged range (tile + k * halo) is
             # bounded and it takes the single-GPU plan's 6 (pointwise N) / 3 (convective)
             cap = 16 if scheme.kind != "etdrk4" else (3 if nl == nat.NL_CONVECTIVE else 6)
+            if pad_ok and nloc >= 4096:
+                cap = 24                    # the persistent per-node kernels' sweet spot (1536-node spans)
             ksteps = max(1, min(cap, nloc // (4 * ext * max(reach, 1))))
         if per_node and scheme.kind == "linear" and self.sharded and not pad_ok:
             ksteps = 1                      # non-periodic per-node rows: one step per exchange
@@ -387,13 +389,18 @@ class ShardedStepper:
         self.flag = torch.zeros(4, dtype=torch.int32, device=dev)
         G = max(width, 1)
         nh = max(scheme.s - 1, 1) if scheme.kind == "etd-multistep" else 1
-        # ghost cells (u and the [s-1][width] multistep history): one slab has none
+        # ghost cells: u's sit right around it -- both ping-pong buffers are extended
+        # arrays [G ghosts | nloc | G ghosts], so a slab reads like a whole grid (the
+        # persistent per-node kernels bulk-copy straight across the seam); the
+        # [s-1][width] multistep history ghosts are separate.  One slab has none.
+        self._G = G if self.sharded else 0
+        self._ext = None
         if self.sharded:
-            ghosts = torch.zeros((2 + 2 * nh) * G, dtype=torch.float64, device=dev)
-            self.gl, self.gr = ghosts[:G], ghosts[G:2 * G]
-            self.ql, self.qr = ghosts[2 * G:(2 + nh) * G], ghosts[(2 + nh) * G:]
+            self._ext = [torch.zeros(nloc + 2 * G, dtype=torch.float64, device=dev) for _ in range(2)]
+            hg = torch.zeros(2 * nh * G, dtype=torch.float64, device=dev)
+            self.ql, self.qr = hg[:nh * G], hg[nh * G:]
         else:
-            self.gl = self.gr = self.ql = self.qr = None
+            self.ql = self.qr = None
         self.u = None
         self._out = None
         self.hist = None
@@ -412,8 +419,13 @@ class ShardedStepper:
 
     def set_local(self, u_local: torch.Tensor) -> None:
         """This slab's initial values (copied: inputs are never written)."""
-        self.u = u_local.clone().contiguous()
-        self._out = torch.empty_like(self.u)
+        if self._ext is not None:
+            G, n = self._G, self.plan.nloc
+            self.u, self._out = self._ext[0][G:G + n], self._ext[1][G:G + n]
+            self.u.copy_(u_local)
+        else:
+            self.u = u_local.clone().contiguous()
+            self._out = torch.empty_like(self.u)
         self._graphs.clear()
         self._seen.clear()
         self._pushed_w = 0
@@ -430,7 +442,14 @@ class ShardedStepper:
             return None
         w = max(self._width(k), 1)
         nh = self._nh()
-        return (self.gl[:w], self.gr[:w], self.ql[:nh * w], self.qr[:nh * w], w)
+        gl, gr = self._ghosts(w)
+        return (gl, gr, self.ql[:nh * w], self.qr[:nh * w], w)
+
+    def _ghosts(self, w: int):
+        """The w ghost cells on each side of the current u, inside its extended buffer."""
+        G, n = self._G, self.plan.nloc
+        ext = self._ext[0] if self.u.data_ptr() == self._ext[0][G:].data_ptr() else self._ext[1]
+        return ext[G - w:G], ext[G + n:G + n + w]
 
     def _hist_fields(self):
         p = self.prep
@@ -505,8 +524,9 @@ class ShardedStepper:
                   nloc=nloc - 2 * w, halo=(u[:w], u[nloc - w:], None, None, w),
                   flag=self.flag[1:2], **kw)
         cm.join()
-        gl = self.gl[:w] if self.ex.left is not None else None
-        gr = self.gr[:w] if self.ex.right is not None else None
+        gl, gr = self._ghosts(w)
+        gl = gl if self.ex.left is not None else None
+        gr = gr if self.ex.right is not None else None
         _ops.step(sch, p.bank, u[:w], k, out=out[:w], off=off, nloc=w,
                   halo=(gl, u[w:2 * w], None, None, w), flag=self.flag[2:3], **kw)
         _ops.step(sch, p.bank, u[nloc - w:], k, out=out[nloc - w:], off=off + nloc - w, nloc=w,
