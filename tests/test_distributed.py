@@ -138,6 +138,38 @@ def test_virtual_shards_bitwise(P):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 3, 5])
+def test_virtual_shards_pernode_slabs_bitwise(P):
+    """Per-node linear slabs wide enough for the persistent TMA kernels (ghosts stored
+    right around the slab, 24 steps per exchange; odd-sized slabs take the
+    register-blocked kernel): bit-identical to the unsharded steps, exact and
+    fused arithmetic alike (the per-node kernels compute each node the same way
+    whatever the tiling)."""
+    import paper_2603_15964_b200 as lx
+    from paper_2603_15964_b200 import _ops, configs
+    from paper_2603_15964_b200.distributed import ShardedStepper, run_virtual_shards
+    from paper_2603_15964_b200.timestep import Stepper, prepare
+    w = configs.c5(N=16384 + 2 * P)
+    c, nu = w.coef
+    g = lx.make_periodic_grid(w.N, 0.0, 1.0)
+    st = lx.select_stencils(g, w.n, lx.StencilPolicy.CENTERED)
+    prob = lx.SemiLinearProblem(lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1)), None,
+                                w.u0, lx.Boundary.periodic(), "none")
+    scheme = lx.SchemeConfig("linear")
+    s0 = ShardedStepper(g, st, prob, scheme, w.delta_t, 0, P, None)
+    k0 = 24 if s0.plan.nloc >= 4096 else 16
+    assert s0.plan.ksteps == k0 and s0.plan.width == k0 * 6
+    for exact in (True, False):
+        ref = Stepper(prepare(g, st, prob, scheme, w.delta_t), _ops.dev_f64(prob.initial), exact=exact)
+        ref.advance(61)
+        u = run_virtual_shards(g, st, prob, scheme, w.delta_t, 61, P, exact=exact)
+        if exact:
+            assert torch.equal(u, ref.u), (P, float((u - ref.u).abs().max()))
+        else:
+            assert float((u - ref.u).norm() / ref.u.norm()) < 1e-13
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("transport", ["nccl", "peer"])
 def test_comm_self_exchange(transport):
     """A periodic 1-rank ring exchanges with itself through the library
