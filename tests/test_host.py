@@ -177,3 +177,32 @@ def test_reference_test_oracles_exported():
     assert np.abs(E - R).max() < 1e-15
     with pytest.raises(lx.NoConvergence):
         lx.expm_taylor_oracle(50.0 * A, max_terms=5)
+
+
+@pytest.mark.parametrize("n,row,nl,P", [(7, 3, 2, 7), (11, 5, 1, 5), (13, 6, 2, 5), (9, 4, 0, 5),
+                                        (7, 3, 1, 5)])
+def test_plan_etdrk4_one_chunk_per_thread(n, row, nl, P):
+    """lmep_plan (host logic only): the register-resident ETDRK4 passes need the whole
+    staged range, tile + k * radius, covered by one chunk of P nodes per thread."""
+    from paper_2603_15964_b200 import _native as nat
+    ext = 8 if nl == nat.NL_CONVECTIVE else 4
+    rad = ext * (n - 1)
+    for N in (1 << 20, 1 << 24):
+        pl = _ops.plan(StencilSet(N, n, row, True), nat.SCH_ETDRK4, nl, nat.W_SHARED, 1000)
+        staged = pl["tile"] + pl["ksteps"] * rad
+        assert pl["ring"] == 0 and pl["ksteps"] >= 1
+        assert staged <= 256 * P and pl["threads"] * P >= staged, pl
+        assert pl["threads"] % 32 == 0 and pl["threads"] <= 256
+
+
+def test_plan_small_grids_and_per_node():
+    """Ring mode for grids that fit one CTA's shared memory, the persistent per-node
+    kernels' 1536-node spans (tile + k (n-1)) for large per-node linear grids."""
+    from paper_2603_15964_b200 import _native as nat
+    pl = _ops.plan(StencilSet(1024, 7, 6, True), nat.SCH_LIN, nat.NL_NONE, nat.W_SHARED, 1000)
+    assert pl["ring"] == 1 and pl["tile"] == 1024
+    pl = _ops.plan(StencilSet(1 << 22, 13, 6, True), nat.SCH_LIN, nat.NL_NONE, nat.W_PERNODE, 200)
+    assert pl["ring"] == 0 and pl["ksteps"] == 25 and pl["tile"] + pl["ksteps"] * 12 == 1536
+    # a non-periodic grid never takes ring mode
+    pl = _ops.plan(StencilSet(1024, 7, 3, False), nat.SCH_LIN, nat.NL_NONE, nat.W_SHARED, 10)
+    assert pl["ring"] == 0
