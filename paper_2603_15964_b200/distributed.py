@@ -510,27 +510,31 @@ class ShardedStepper:
         return self.overlap and w >= 1 and self.plan.nloc >= 3 * w
 
     def _enqueue_split(self, k: int) -> None:
-        """fork -> exchange on the side stream || interior sub-slab on the step
-        stream -> join -> the two edge strips.  The interior's ghosts are this
-        slab's own edge values, so it does not wait for the neighbours."""
+        """fork -> side stream: halo exchange, then the two edge strips || step
+        stream: the interior sub-slab -> join.  The interior's ghosts are this
+        slab's own edge values, so it does not wait for the neighbours, and the
+        strips (one or two CTAs each) run beside it instead of behind it."""
         p, cm = self.prep, self.ex.comm
         w, nloc, off = self._width(k), self.plan.nloc, self.plan.off
         u, out = self.u, self._out
         sch = nat.SCH_LIN if p.scheme == "linear" else nat.SCH_ETDRK4
         kw = dict(bc=p.bc, nl=p.nl, exact=self.exact, tuning=self._tuning(k))
+        if self._side is None:
+            self._side = torch.cuda.ExternalStream(cm.side_stream)
         cm.fork()
-        self.exchange_phase(k, stream=cm.side_stream)
+        with torch.cuda.stream(self._side):
+            self.exchange_phase(k)
+            gl, gr = self._ghosts(w)
+            gl = gl if self.ex.left is not None else None
+            gr = gr if self.ex.right is not None else None
+            _ops.step(sch, p.bank, u[:w], k, out=out[:w], off=off, nloc=w,
+                      halo=(gl, u[w:2 * w], None, None, w), flag=self.flag[2:3], **kw)
+            _ops.step(sch, p.bank, u[nloc - w:], k, out=out[nloc - w:], off=off + nloc - w, nloc=w,
+                      halo=(u[nloc - 2 * w:nloc - w], gr, None, None, w), flag=self.flag[3:4], **kw)
         _ops.step(sch, p.bank, u[w:nloc - w], k, out=out[w:nloc - w], off=off + w,
                   nloc=nloc - 2 * w, halo=(u[:w], u[nloc - w:], None, None, w),
                   flag=self.flag[1:2], **kw)
         cm.join()
-        gl, gr = self._ghosts(w)
-        gl = gl if self.ex.left is not None else None
-        gr = gr if self.ex.right is not None else None
-        _ops.step(sch, p.bank, u[:w], k, out=out[:w], off=off, nloc=w,
-                  halo=(gl, u[w:2 * w], None, None, w), flag=self.flag[2:3], **kw)
-        _ops.step(sch, p.bank, u[nloc - w:], k, out=out[nloc - w:], off=off + nloc - w, nloc=w,
-                  halo=(u[nloc - 2 * w:nloc - w], gr, None, None, w), flag=self.flag[3:4], **kw)
 
     def _enqueue_fused(self, k: int, k_next: int) -> None:
         """Peer transport: no exchange kernels between chunks.  The interior
