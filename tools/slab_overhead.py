@@ -1,4 +1,6 @@
-"""One config-4-sized slab (2^21 nodes, ETDRK4 cubic) stepped as a rank of a sharded run: a periodic\n1-rank ring exchanging with itself through the library communicator (NCCL with graph replay, peer\nmailboxes with fused stores), against the unsharded stepper on the same grid.  Diagnostic."""
+"""One config-4-sized slab (2^21 nodes, ETDRK4 cubic) stepped as a rank of a sharded run: a periodic
+1-rank ring exchanging with itself through the library communicator (NCCL with graph replay, peer
+mailboxes with fused stores), against the unsharded stepper on the same grid.  Diagnostic."""
 import sys, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
