@@ -419,6 +419,40 @@ int lmep_comm_signal(lmep_comm *comm, void *stream);
 int lmep_comm_wait(lmep_comm *comm, void *stream);
 int lmep_comm_ghosts(lmep_comm *comm, int field, const double **left, const double **right);
 
+/* One chunk (halo exchange + k fused steps) of a sharded linear / ETDRK4 run on
+ * shared or class rows, in one call.  u_in / u_out are the slab's nloc values
+ * with `ghost_cells` cells stored right before and after them (extended
+ * arrays [ghosts | owned | ghosts]).  The library does what a caller would do
+ * with the pieces above:
+ *   NCCL  fork; side stream: exchange into the ghost cells around u_in, then
+ *         the two edge strips; step stream: the interior sub-slab (its ghosts
+ *         are the slab's own edge values); join.  Capturable (lmep_graph_*).
+ *   PEER  the edges of u_in go out with lmep_comm_push unless `pushed_cells`
+ *         says the previous chunk already stored them; fork; side stream: the
+ *         interior; step stream: wait for the neighbours, the strips with their
+ *         ghosts read in place from the mailbox and -- when next_steps > 0 --
+ *         the next chunk's halo stored straight into the neighbours'
+ *         mailboxes; signal; join.
+ * Slabs narrower than three halos run unsplit.  nonfinite: device int32[4]
+ * (one flag per launch; the run is finite when all are 0). */
+typedef struct lmep_chunk_args {
+    const lmep_grid *grid;      /* the slab: off, nloc                                 */
+    const lmep_weights *w;      /* LMEP_W_SHARED or LMEP_W_CLASS                       */
+    const lmep_bc *bc;          /* nullable                                            */
+    int32_t scheme;             /* 0 linear, 1 ETDRK4                                  */
+    int32_t nl_kind;            /* LMEP_NL_*                                           */
+    const double *u_in;
+    double *u_out;
+    int64_t ghost_cells;        /* cells stored on each side of u_in / u_out           */
+    int64_t steps;              /* k of this chunk                                     */
+    int64_t next_steps;         /* k of the chunk that follows (0: none)               */
+    int64_t pushed_cells;       /* PEER: edge cells of u_in already in the neighbours' mailboxes */
+    int32_t flags;              /* LMEP_FLAG_*                                         */
+    int32_t reserved;
+    int32_t *nonfinite;
+} lmep_chunk_args;
+int lmep_comm_chunk(lmep_comm *comm, const lmep_chunk_args *args, void *stream);
+
 /* Concatenate the slabs on `root`: rank r contributes nloc_r = counts[r]
  * doubles (counts: HOST array of world entries, the same on every rank); out
  * (root only) receives them in rank order.  NCCL transport only (PEER runs

@@ -50,7 +50,7 @@ EXPORTS = (
     "lmep_comm_flag_max", "lmep_comm_side_stream", "lmep_comm_fork", "lmep_comm_join",
     "lmep_graph_begin", "lmep_graph_end", "lmep_graph_launch", "lmep_graph_destroy",
     "lmep_comm_targets", "lmep_comm_push", "lmep_comm_signal", "lmep_comm_wait",
-    "lmep_comm_ghosts", "lmep_set_etd2_persistent", "lmep_step_linear_host",
+    "lmep_comm_ghosts", "lmep_set_etd2_persistent", "lmep_step_linear_host", "lmep_comm_chunk",
 )
 COMM_NCCL, COMM_PEER = 0, 1
 COMM_ID_BYTES, COMM_BLOB_BYTES, COMM_MAX_FIELDS = 128, 512, 8
@@ -92,6 +92,14 @@ class LmepHarvestArgs(C.Structure):
                 ("B", C.c_int64), ("out_ld", C.c_int64), ("w_out", C.c_void_p),
                 ("status", C.c_void_p), ("ms", C.c_void_p), ("map", C.c_void_p),
                 ("half_out", C.c_void_p), ("status_any", C.c_void_p)]
+
+
+class LmepChunkArgs(C.Structure):
+    _fields_ = [("grid", C.c_void_p), ("w", C.c_void_p), ("bc", C.c_void_p), ("scheme", C.c_int32),
+                ("nl_kind", C.c_int32), ("u_in", C.c_void_p), ("u_out", C.c_void_p),
+                ("ghost_cells", C.c_int64), ("steps", C.c_int64), ("next_steps", C.c_int64),
+                ("pushed_cells", C.c_int64), ("flags", C.c_int32), ("reserved", C.c_int32),
+                ("nonfinite", C.c_void_p)]
 
 
 class LmepTuning(C.Structure):
@@ -174,6 +182,7 @@ def load(path: str | None = None):
     L.lmep_comm_signal.argtypes = [vp, vp]
     L.lmep_comm_wait.argtypes = [vp, vp]
     L.lmep_comm_ghosts.argtypes = [vp, C.c_int, C.POINTER(vp), C.POINTER(vp)]
+    L.lmep_comm_chunk.argtypes = [vp, C.POINTER(LmepChunkArgs), vp]
     L.lmep_comm_side_stream.argtypes = [vp]
     L.lmep_comm_side_stream.restype = vp
     L.lmep_comm_fork.argtypes = [vp, vp]

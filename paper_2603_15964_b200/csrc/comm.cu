@@ -694,6 +694,94 @@ extern "C" int lmep_comm_join(lmep_comm *c, void *stream)
 }
 
 // ---------------------------------------------------------------------------
+// one chunk of a sharded run in one call
+// ---------------------------------------------------------------------------
+extern "C" int lmep_comm_chunk(lmep_comm *c, const lmep_chunk_args *a, void *stream)
+{
+    if (!c || !a || !a->grid || !a->w || !a->u_in || !a->u_out || !a->nonfinite) return LMEP_INVALID_CONFIG;
+    if (a->scheme != SCH_LIN && a->scheme != SCH_ETDRK4) return LMEP_INVALID_CONFIG;
+    if (a->w->mode == LMEP_W_PERNODE || a->steps < 1 || a->next_steps < 0) return LMEP_INVALID_CONFIG;
+    const lmep_grid &G = *a->grid;
+    const int reach = G.row > G.n - 1 - G.row ? G.row : G.n - 1 - G.row;
+    const int ext = a->scheme == SCH_LIN ? 1 : (a->nl_kind == LMEP_NL_CONVECTIVE ? 8 : 4);
+    const int64_t W = a->steps * ext * reach, nloc = G.nloc;
+    const int64_t Wn = std::min<int64_t>(a->next_steps * ext * reach, W);
+    if (W < 1 || W > nloc || W > a->ghost_cells) return LMEP_DIMENSION;
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool hasL = c->left >= 0, hasR = c->right >= 0;
+    lmep_tuning tun{0, (int32_t)a->steps, 0, 0};
+    const double *u = a->u_in;
+    double *o = a->u_out;
+    // k steps of the sub-range [off, off + n) of the slab: an ordinary step call
+    auto sub = [&](int64_t off, int64_t n, const double *gl, const double *gr, double *pl, double *pr,
+                   int64_t pw, int32_t *flag, cudaStream_t s) {
+        lmep_grid g = G;
+        g.off = G.off + off;
+        g.nloc = n;
+        lmep_halo h{gl, gr, nullptr, nullptr, W, pl, pr, pw};
+        StepCall sc{};
+        sc.sch = a->scheme; sc.grid = &g; sc.w = a->w; sc.bc = a->bc;
+        sc.halo = (gl || gr) ? &h : nullptr;
+        sc.nl = a->nl_kind; sc.u_in = u + off; sc.u_out = o + off; sc.steps = a->steps;
+        sc.flags = a->flags; sc.tuning = &tun; sc.nonfinite = flag; sc.stream = s;
+        return run_steps(sc);
+    };
+    if (!hasL && !hasR)                                  // one slab: nothing to exchange
+        return sub(0, nloc, nullptr, nullptr, nullptr, nullptr, 0, a->nonfinite, st);
+    const bool split = nloc >= 3 * W;
+    int rc;
+    if (c->transport == LMEP_COMM_NCCL) {
+        // ghosts are stored right around u_in; exchange and edge strips on the side
+        // stream, beside the interior
+        double *gl = const_cast<double *>(u) - W, *gr = const_cast<double *>(u) + nloc;
+        const double *fields[1] = {u};
+        double *gls[1] = {gl}, *grs[1] = {gr};
+        const double *cgl = hasL ? gl : nullptr, *cgr = hasR ? gr : nullptr;
+        if (!split) {
+            if ((rc = exchange_nccl(c, 1, fields, nloc, W, gls, grs, st))) return rc;
+            return sub(0, nloc, cgl, cgr, nullptr, nullptr, 0, a->nonfinite + 1, st);
+        }
+        if ((rc = lmep_comm_fork(c, st))) return rc;
+        if ((rc = exchange_nccl(c, 1, fields, nloc, W, gls, grs, c->side))) return rc;
+        if ((rc = sub(0, W, cgl, u + W, nullptr, nullptr, 0, a->nonfinite + 2, c->side))) return rc;
+        if ((rc = sub(nloc - W, W, u + nloc - 2 * W, cgr, nullptr, nullptr, 0, a->nonfinite + 3, c->side))) return rc;
+        if ((rc = sub(W, nloc - 2 * W, u, u + nloc - W, nullptr, nullptr, 0, a->nonfinite + 1, st))) return rc;
+        return lmep_comm_join(c, st);
+    }
+    // PEER: no exchange kernel between chunks -- ghosts are read in place from this
+    // rank's mailbox and the edge launches store the next chunk's halo into the
+    // neighbours' mailboxes themselves
+    if ((rc = peer_check(c, "lmep_comm_chunk", st))) return rc;
+    if (W > c->max_width) return LMEP_DIMENSION;
+    if (a->pushed_cells < W) {
+        const double *fields[1] = {u};
+        if ((rc = peer_push(c, 1, fields, nloc, W, st))) return rc;
+    }
+    double *tl = nullptr, *tr = nullptr;
+    if (Wn > 0) peer_targets(c, 0, &tl, &tr);
+    auto ghosts = [&](const double **gl, const double **gr) {
+        const int half = (int)(c->seq & 1);
+        *gl = hasL ? slot(c->mailbox, c, half, 0) : nullptr;
+        *gr = hasR ? slot(c->mailbox, c, half, 1) : nullptr;
+    };
+    const double *gl, *gr;
+    if (!split) {
+        if ((rc = peer_wait(c, st))) return rc;
+        ghosts(&gl, &gr);
+        if ((rc = sub(0, nloc, gl, gr, tl, tr, Wn, a->nonfinite + 1, st))) return rc;
+        return Wn > 0 ? peer_signal(c, st) : LMEP_OK;
+    }
+    if ((rc = lmep_comm_fork(c, st))) return rc;
+    if ((rc = sub(W, nloc - 2 * W, u, u + nloc - W, nullptr, nullptr, 0, a->nonfinite + 1, c->side))) return rc;
+    if ((rc = peer_wait(c, st))) return rc;
+    ghosts(&gl, &gr);
+    if ((rc = sub(0, W, gl, u + W, tl, nullptr, Wn, a->nonfinite + 2, st))) return rc;
+    if ((rc = sub(nloc - W, W, u + nloc - 2 * W, gr, nullptr, tr, Wn, a->nonfinite + 3, st))) return rc;
+    if (Wn > 0 && (rc = peer_signal(c, st))) return rc;
+    return lmep_comm_join(c, st);
+}
+
+// ---------------------------------------------------------------------------
 // graphs
 // ---------------------------------------------------------------------------
 // the library's own launches recorded by the capture in progress on this thread

@@ -68,4 +68,34 @@ inline void mark_device(std::atomic<uint64_t> &mask, int dev)
     mask.fetch_or(1ull << dev, std::memory_order_release);
 }
 
+enum { SCH_LIN = 0, SCH_ETDRK4 = 1, SCH_ETD2 = 2 };
+
+// One stepping request of the host layer (step_host.cu): what the lmep_step_*
+// entry points and the sharded chunk driver (comm.cu) hand to run_steps.
+struct StepCall {
+    int sch;
+    int etds = 2;
+    const lmep_grid *grid;
+    const lmep_weights *w;
+    const lmep_bc *bc;
+    const lmep_halo *halo;
+    int nl;
+    double dt;
+    const double *u_in, *q_in;
+    double *u_out, *q_out, *scratch;
+    int64_t steps;
+    int32_t flags;
+    const lmep_tuning *tuning;
+    int32_t *nonfinite;
+    double *nl0_out;
+    cudaStream_t stream;
+    // lmep_step_linear_host: the result also lands in host memory, the last launch
+    // split into `parts` tile ranges whose copies overlap the remaining ranges
+    double *host_out = nullptr;
+    int parts = 1;
+    cudaStream_t copy_stream = nullptr;
+};
+
+int run_steps(const StepCall &c);
+
 }  // namespace lmep

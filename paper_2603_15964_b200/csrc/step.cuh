@@ -35,7 +35,6 @@
 
 namespace lmep {
 
-enum { SCH_LIN = 0, SCH_ETDRK4 = 1, SCH_ETD2 = 2 };
 constexpr int STEP_THREADS = 256;
 constexpr int SLOT_PAD = 24;
 constexpr int STEP_P_ETDRK4 = 7;   // consecutive outputs per thread (odd: conflict-free)

@@ -138,30 +138,6 @@ static int launch_step(int sch, bool exact, bool pernode, const StepParams &p, d
     return launch_scheme_etd2_none(exact, p, grid, shm, st);
 }
 
-struct StepCall {
-    int sch;
-    int etds = 2;
-    const lmep_grid *grid;
-    const lmep_weights *w;
-    const lmep_bc *bc;
-    const lmep_halo *halo;
-    int nl;
-    double dt;
-    const double *u_in, *q_in;
-    double *u_out, *q_out, *scratch;
-    int64_t steps;
-    int32_t flags;
-    const lmep_tuning *tuning;
-    int32_t *nonfinite;
-    double *nl0_out;
-    cudaStream_t stream;
-    // lmep_step_linear_host: the result also lands in host memory, the last launch
-    // split into `parts` tile ranges whose copies overlap the remaining ranges
-    double *host_out = nullptr;
-    int parts = 1;
-    cudaStream_t copy_stream = nullptr;
-};
-
 int run_steps(const StepCall &c)
 {
     if (!c.grid || !c.w) return LMEP_INVALID_CONFIG;

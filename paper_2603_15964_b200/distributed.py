@@ -382,7 +382,6 @@ class ShardedStepper:
         # mailboxes themselves and read their ghosts straight out of their own
         self.fused = bool(self.overlap and exchanger.comm.transport == "peer")
         self._pushed_w = 0
-        self._side = None
         self._graphs: dict = {}
         self._seen: set = set()
         dev = nat.device()
@@ -505,84 +504,36 @@ class ShardedStepper:
         if self.prep.scheme == "etd-multistep" and self.prep.s > 1:
             self.hist, self._hout = self._hout, self.hist
 
-    def _can_split(self, k: int) -> bool:
-        w = self._width(k)
-        return self.overlap and w >= 1 and self.plan.nloc >= 3 * w
-
-    def _enqueue_split(self, k: int) -> None:
-        """fork -> side stream: halo exchange, then the two edge strips || step
-        stream: the interior sub-slab -> join.  The interior's ghosts are this
-        slab's own edge values, so it does not wait for the neighbours, and the
-        strips (one or two CTAs each) run beside it instead of behind it."""
+    def _enqueue_chunk(self, k: int, k_next: int) -> None:
+        """One chunk in one library call (lmep_comm_chunk): on NCCL, fork -> side
+        stream: halo exchange into the ghost cells around u, then the two edge
+        strips || step stream: the interior sub-slab -> join; on the peer
+        transport no exchange kernel at all -- the interior runs on the side
+        stream while the step stream waits for the neighbours, runs the strips
+        with their ghosts read in place from this rank's mailbox, and those
+        launches store the next chunk's halo straight into the neighbours'
+        mailboxes (peer memory)."""
         p, cm = self.prep, self.ex.comm
-        w, nloc, off = self._width(k), self.plan.nloc, self.plan.off
-        u, out = self.u, self._out
-        sch = nat.SCH_LIN if p.scheme == "linear" else nat.SCH_ETDRK4
-        kw = dict(bc=p.bc, nl=p.nl, exact=self.exact, tuning=self._tuning(k))
-        if self._side is None:
-            self._side = torch.cuda.ExternalStream(cm.side_stream)
-        cm.fork()
-        with torch.cuda.stream(self._side):
-            self.exchange_phase(k)
-            gl, gr = self._ghosts(w)
-            gl = gl if self.ex.left is not None else None
-            gr = gr if self.ex.right is not None else None
-            _ops.step(sch, p.bank, u[:w], k, out=out[:w], off=off, nloc=w,
-                      halo=(gl, u[w:2 * w], None, None, w), flag=self.flag[2:3], **kw)
-            _ops.step(sch, p.bank, u[nloc - w:], k, out=out[nloc - w:], off=off + nloc - w, nloc=w,
-                      halo=(u[nloc - 2 * w:nloc - w], gr, None, None, w), flag=self.flag[3:4], **kw)
-        _ops.step(sch, p.bank, u[w:nloc - w], k, out=out[w:nloc - w], off=off + w,
-                  nloc=nloc - 2 * w, halo=(u[:w], u[nloc - w:], None, None, w),
-                  flag=self.flag[1:2], **kw)
-        cm.join()
-
-    def _enqueue_fused(self, k: int, k_next: int) -> None:
-        """Peer transport: no exchange kernels between chunks.  The interior
-        sub-slab starts at once on the side stream; the step stream waits for
-        the neighbours' signal, runs the two edge strips with their ghosts read
-        in place from this rank's mailbox, and those launches store the next
-        chunk's edges straight into the neighbours' mailboxes (peer memory)."""
-        p, cm = self.prep, self.ex.comm
-        w, nloc, off = self._width(k), self.plan.nloc, self.plan.off
-        u, out = self.u, self._out
-        if self._pushed_w < w:              # first chunk: the edges go through the push kernel
-            cm.push([u], w)
-        wn = min(self._width(k_next), w) if k_next > 0 else 0
-        tl, tr = cm.targets(0) if wn else (None, None)
-        sch = nat.SCH_LIN if p.scheme == "linear" else nat.SCH_ETDRK4
-        kw = dict(bc=p.bc, nl=p.nl, exact=self.exact, tuning=self._tuning(k))
-        if nloc >= 3 * w:
-            if self._side is None:
-                self._side = torch.cuda.ExternalStream(cm.side_stream)
-            cm.fork()
-            with torch.cuda.stream(self._side):
-                _ops.step(sch, p.bank, u[w:nloc - w], k, out=out[w:nloc - w], off=off + w,
-                          nloc=nloc - 2 * w, halo=(u[:w], u[nloc - w:], None, None, w),
-                          flag=self.flag[1:2], **kw)
-            cm.wait()
-            gl, gr = cm.ghosts(0)
-            _ops.step(sch, p.bank, u[:w], k, out=out[:w], off=off, nloc=w,
-                      halo=(gl, u[w:2 * w], None, None, w, tl, None, wn), flag=self.flag[2:3], **kw)
-            _ops.step(sch, p.bank, u[nloc - w:], k, out=out[nloc - w:], off=off + nloc - w, nloc=w,
-                      halo=(u[nloc - 2 * w:nloc - w], gr, None, None, w, None, tr, wn),
-                      flag=self.flag[3:4], **kw)
-            if wn:
-                cm.signal()
-            cm.join()
-        else:
-            cm.wait()
-            gl, gr = cm.ghosts(0)
-            _ops.step(sch, p.bank, u, k, out=out, off=off, nloc=nloc,
-                      halo=(gl, gr, None, None, w, tl, tr, wn), flag=self.flag[1:2], **kw)
-            if wn:
-                cm.signal()
-        self._pushed_w = wn
+        g = _ops.c_grid(self.sset, self.plan.off, self.plan.nloc)
+        w = p.bank.c_weights()
+        b = (p.bc or _ops.BC()).c()
+        a = nat.LmepChunkArgs()
+        a.grid, a.w, a.bc = C.addressof(g), C.addressof(w), C.addressof(b)
+        a.scheme = nat.SCH_LIN if p.scheme == "linear" else nat.SCH_ETDRK4
+        a.nl_kind = p.nl
+        a.u_in, a.u_out = self.u.data_ptr(), self._out.data_ptr()
+        a.ghost_cells = self._G
+        a.steps, a.next_steps = int(k), int(k_next)
+        a.pushed_cells = self._pushed_w
+        a.flags = nat.FLAG_EXACT if self.exact else 0
+        a.nonfinite = self.flag.data_ptr()
+        nat.check(nat.lib().lmep_comm_chunk(cm.h, C.byref(a), nat.stream_handle()), "lmep_comm_chunk")
+        if self.fused:
+            self._pushed_w = min(self._width(k_next), self._width(k)) if k_next > 0 else 0
 
     def _enqueue(self, k: int, k_next: int = 0) -> None:
-        if self.fused:
-            self._enqueue_fused(k, k_next)
-        elif self._can_split(k):
-            self._enqueue_split(k)
+        if self.overlap:
+            self._enqueue_chunk(k, k_next)
         else:
             self.exchange_phase(k)
             self._launch(k)
