@@ -53,7 +53,7 @@ int plan_launch(const lmep_grid &g, int sch, int nl, int64_t steps, bool sharded
         // per halo exchange
         // steps per launch: the rows cross HBM once per launch; past ~25 steps the
         // halo recompute (k (n-1) of the 1536-node span) outweighs it (C5 sweep
-        // tools/c5_ksweep2.py: k = 16 11.1, 25 10.2, 40 10.6 us/step)
+        // tools/c5_variant_sweep.py: k = 16 10.4, 25 9.3, 34 9.4 us/step)
         const int64_t kdef = (!sharded && (g.N % 2) == 0 && g.N >= tb_nodes_per_cta(n, true)) ? 25 : 16;
         k = sharded ? steps : (t.ksteps > 0 ? t.ksteps : std::min<int64_t>(kdef, steps));
         // (slab_tma: a slab whose ghosts sit right next to it and whose extended range
