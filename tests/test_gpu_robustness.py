@@ -2,6 +2,7 @@
 misaligned views, zero-step runs, concurrent host threads on separate streams.
 """
 
+import os
 import threading
 
 import numpy as np
@@ -266,3 +267,22 @@ def test_rebinding_caches_read_only_arrays(lx, orc):
     assert len(kernels._ROWS.d) == 1
     W2[0, 0] += 1.0
     assert np.array_equal(kernels.run_linear(W2, m, u0, 3), orc.run_linear(W2, m, u0, 3))
+
+
+def test_c_program_on_the_c_abi(tmp_path):
+    """tests/c_abi/smoke.c: a C program that links liblmep.so and the CUDA runtime only (no
+    Python, no torch) runs config 1's path -- Fornberg tables, the harvest of the shared row,
+    60 steps -- and matches its own host loop bit for bit."""
+    import shutil
+    import subprocess
+    from paper_2603_15964_b200 import _native
+    from tests.conftest import REPO
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    libdir = os.path.dirname(_native.LIB_PATH)
+    exe = str(tmp_path / "smoke")
+    subprocess.run([nvcc, "-Xcompiler", "-ffp-contract=off", "-I", os.path.join(REPO, "include"),
+                    os.path.join(REPO, "tests", "c_abi", "smoke.c"), "-L", libdir, "-llmep",
+                    "-Xlinker", "-rpath", "-Xlinker", libdir, "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    assert "c-abi smoke ok" in out.stdout and "60 steps bit-identical" in out.stdout
