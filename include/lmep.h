@@ -476,7 +476,9 @@ int lmep_comm_join(lmep_comm *comm, void *stream);
  * until lmep_graph_end is recorded instead of run.  lmep_graph_launch replays
  * it.  Device pointers are baked in: capture one graph per ping-pong
  * direction.  NCCL exchanges are capturable once the communicator has run
- * one exchange outside a capture. */
+ * one exchange outside a capture.  Destroy every graph that captured a
+ * communicator's exchanges BEFORE lmep_comm_destroy: ncclCommDestroy waits
+ * for the graphs that hold its work. */
 typedef struct lmep_graph lmep_graph;
 int lmep_graph_begin(void *stream);
 int lmep_graph_end(void *stream, lmep_graph **graph);

@@ -80,6 +80,7 @@ class Comm:
         self.left = None if l.value < 0 else l.value
         self.right = None if r.value < 0 else r.value
         self.side_stream = nat.lib().lmep_comm_side_stream(h)
+        self._steppers: list = []           # weak references: their graphs go before the communicator
 
     @staticmethod
     def unique_id() -> bytes:
@@ -155,6 +156,13 @@ class Comm:
 
     def close(self) -> None:
         if self.h is not None:
+            # graphs that captured this communicator's NCCL work must be destroyed
+            # first (ncclCommDestroy waits for them)
+            for ref in self._steppers:
+                st = ref()
+                if st is not None:
+                    st._graphs.clear()
+            self._steppers.clear()
             nat.lib().lmep_comm_destroy(self.h)
             self.h = None
 
@@ -384,6 +392,9 @@ class ShardedStepper:
         self._pushed_w = 0
         self._graphs: dict = {}
         self._seen: set = set()
+        if comm_ex:
+            import weakref
+            exchanger.comm._steppers.append(weakref.ref(self))
         dev = nat.device()
         self.flag = torch.zeros(4, dtype=torch.int32, device=dev)
         G = max(width, 1)
@@ -628,8 +639,9 @@ def _prepare_shard(grid, sset, problem, scheme, delta_t, off, nloc, pad=0) -> Pr
     if scheme.kind == "linear":
         bank = harvest_compact(grid, sset, spec, delta_t, 1, frozen, node_range=rng, pad=pad)
     elif scheme.kind == "etdrk4":
-        full = harvest_compact(grid, sset, spec, delta_t, 4, frozen, node_range=rng)
-        half = harvest_compact(grid, sset, spec, delta_t / 2, 2, frozen, node_range=rng)
+        # (the half-step set from the same exponential, exactly as timestep.prepare does:
+        # a separate harvest at dt / 2 agrees to ~1e-16 only)
+        full, half = harvest_compact(grid, sset, spec, delta_t, 4, frozen, node_range=rng, half=True)
         bank = _etdrk4_bank(full, half, delta_t, d1)
     else:
         s = scheme.s
@@ -638,8 +650,7 @@ def _prepare_shard(grid, sset, problem, scheme, delta_t, off, nloc, pad=0) -> Pr
         ops = harvest_compact(grid, sset, spec, delta_t, s + 1, frozen, node_range=rng)
         parts = {nat.ROW_W + j: ops.row(j) for j in range(s + 1)}
         if s >= 2:
-            full = harvest_compact(grid, sset, spec, delta_t, 4, frozen, node_range=rng)
-            half = harvest_compact(grid, sset, spec, delta_t / 2, 2, frozen, node_range=rng)
+            full, half = harvest_compact(grid, sset, spec, delta_t, 4, frozen, node_range=rng, half=True)
             warm = _etdrk4_bank(full, half, delta_t, d1)
         if d1 is not None:
             parts[nat.ROW_D1] = d1

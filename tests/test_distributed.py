@@ -258,6 +258,63 @@ def test_self_ring_stepper_bitwise(transport):
         c.close()
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_chunk_driver_random_shapes_bitwise(transport):
+    """lmep_comm_chunk over seeded random shapes (grid size, stencil width, scheme,
+    steps per exchange, step counts that leave a shorter last chunk, slabs both
+    wider and narrower than three halos): a 1-rank ring through the communicator
+    against the unsharded stepper, bit for bit."""
+    import paper_2603_15964_b200 as lx
+    from paper_2603_15964_b200 import _ops
+    from paper_2603_15964_b200.distributed import Comm, CommHalo, ShardedStepper, advance_all
+    from paper_2603_15964_b200.timestep import Stepper, prepare
+    if transport == "nccl":
+        c = Comm(0, 1, True, "nccl", unique_id=Comm.unique_id())
+    else:
+        c = Comm(0, 1, True, "peer", max_width=2048)
+        c.connect([c.export()])
+    rng = np.random.default_rng(20260315)
+    own = torch.cuda.Stream()
+    try:
+        for case in range(14):
+            n = int(rng.choice([7, 9, 11, 13]))
+            kind = ["linear", "cubic", "convective"][case % 3]
+            k = int(rng.integers(1, 7))
+            reach = (n - 1) // 2
+            ext = {"linear": 1, "cubic": 4, "convective": 8}[kind]
+            w = k * ext * reach
+            # slabs from just over one halo (unsplit) to many halos (interior + strips)
+            N = int(w * rng.choice([1.5, 2.9, 3.0, 3.1, 7.3, 40.0])) + int(rng.integers(0, 5)) + 4 * n
+            steps = int(rng.integers(1, 4)) * k + int(rng.integers(0, k))
+            g = lx.make_periodic_grid(N, 0.0, 2 * math.pi)
+            st = lx.select_stencils(g, n, lx.StencilPolicy.CENTERED)
+            u0 = np.sin(g.nodes) + 0.2 * np.cos(3 * g.nodes + case)
+            h = 2 * math.pi / N
+            if kind == "linear":
+                prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(((1, -1.0), (2, 0.05))), None, u0,
+                                            lx.Boundary.periodic(), "none")
+                scheme, dt = lx.SchemeConfig("linear"), 0.4 * h
+            else:
+                prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(((2, 0.02),)), None, u0,
+                                            lx.Boundary.periodic(), kind)
+                scheme, dt = lx.SchemeConfig("etdrk4"), 0.3 * h * h / 0.02
+            ref = Stepper(prepare(g, st, prob, scheme, dt), _ops.dev_f64(u0))
+            ref.advance(steps)
+            s = ShardedStepper(g, st, prob, scheme, dt, 0, 1, CommHalo(c), ksteps=k, force_halo=True)
+            assert s.overlap and s.plan.width == w
+            s.set_initial(u0)
+            own.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(own):
+                advance_all(s, steps)
+            torch.cuda.synchronize()
+            assert torch.equal(s.u, ref.u), (case, kind, n, N, k, steps, float((s.u - ref.u).abs().max()))
+            assert not s.nonfinite()
+            s._graphs.clear()
+    finally:
+        c.close()
+
+
 def _rank_main(rank, world, port, transport, q):
     """One rank of the 2-process runs below; both ranks drive cuda:0."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
