@@ -677,6 +677,47 @@ def test_burgers_etd_multistep_orders(lx, golden, s):
     assert np.array_equal(a.u_final, b.u_final)
 
 
+@pytest.mark.parametrize("n", [7, 9, 11, 13])
+@pytest.mark.parametrize("kind", ["cubic", "convective", "none"])
+def test_etdrk4_register_passes_vs_staged_passes_bitwise(lx, n, kind):
+    """The register-resident ETDRK4 passes (step_rk4.cuh: one chunk per thread) against
+    the staged passes of the same kernel (forced by a CTA too small to hold the staged
+    range in one round), over stencil widths, N kinds, launch shapes and a clamped grid
+    whose end tiles take the generic path: bit-identical in the exact order, within
+    1e-12 with fused multiply-adds."""
+    import torch
+    from paper_2603_15964_b200 import _ops
+    from paper_2603_15964_b200.timestep import Stepper, prepare
+    N = 6000 + n
+    for periodic in (True, False):
+        if periodic:
+            g = lx.make_periodic_grid(N, 0.0, 2 * math.pi)
+            bnd = lx.Boundary.periodic()
+        else:
+            g = lx.make_uniform_grid(N, 0.0, 2 * math.pi)
+            bnd = lx.Boundary.dirichlet(0.0, 0.0)
+        st = lx.select_stencils(g, n, lx.StencilPolicy.CENTERED)
+        h = 2 * math.pi / N
+        u0 = np.sin(g.nodes) * (1.0 + 0.3 * np.cos(5 * g.nodes))
+        prob = lx.SemiLinearProblem(lx.LinearOperatorSpec(((2, 0.02),)), None, u0, bnd, kind)
+        prep = prepare(g, st, prob, lx.SchemeConfig("etdrk4"), 0.3 * h * h / 0.02)
+        shapes = [{"tile": 1000, "ksteps": 1, "threads": 64},     # staged passes (several rounds)
+                  None,                                           # the library's plan
+                  {"tile": 300, "ksteps": 3}, {"tile": 777, "ksteps": 2}]
+        for exact in (True, False):
+            outs = []
+            for tun in shapes:
+                sp = Stepper(prep, _ops.dev_f64(u0), exact=exact, tuning=tun)
+                sp.advance(7)
+                assert not sp.nonfinite()
+                outs.append(sp.u.clone())
+            for o in outs[1:]:
+                if exact:
+                    assert torch.equal(o, outs[0]), (periodic, float((o - outs[0]).abs().max()))
+                else:
+                    assert float((o - outs[0]).norm() / outs[0].norm()) < 1e-12
+
+
 @pytest.mark.parametrize("N,n,kind,steps", [(65536, 9, "convective", 203), (20000, 13, "convective", 37),
                                             (30011, 7, "cubic", 50), (40960, 11, "none", 33),
                                             (9001, 7, "cubic", 20),
