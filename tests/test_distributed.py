@@ -370,32 +370,34 @@ def _rank_main(rank, world, port, transport, q):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("transport", ["peer", "torch"])
-def test_run_sharded_two_processes(transport):
-    """run_sharded over two processes (both on cuda:0; the peer transport moves
-    the halos through CUDA-IPC mailboxes, "torch" stages them through a gloo
+@pytest.mark.parametrize("world,transport", [(2, "peer"), (2, "torch"), (3, "peer")])
+def test_run_sharded_two_processes(world, transport):
+    """run_sharded over two or three processes (all on cuda:0; the peer transport
+    moves the halos through CUDA-IPC mailboxes, "torch" stages them through a gloo
     group) reproduces run() bit for bit: every snapshot, times, step count, and
-    the NonFinite state of a blown-up run."""
+    the NonFinite state of a blown-up run.  Three ranks give every rank two
+    different neighbours on the ring and a middle rank on the open chain."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, transport, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, transport, q)) for r in range(world)]
     for p in procs:
         p.start()
     try:
-        out = dict(q.get(timeout=420) for _ in range(2))
+        out = dict(q.get(timeout=420) for _ in range(world))
     finally:
         for p in procs:
             p.join(timeout=60)
             if p.is_alive():
                 p.kill()
-    for r in (0, 1):
+    for r in range(world):
         assert "error" not in out[r], out[r]["error"]
     r0 = out[0]
     for name in ("c1-linear", "c5-pernode", "c4-neumann", "c3-kdv", "c2-etd2", "c2-etd3"):
         assert r0[name] == (True, True, True, True), (name, r0[name])
     assert r0["blowup"] == (True, True), r0["blowup"]
-    assert out[1]["blowup"] == (True,)
+    for r in range(1, world):
+        assert out[r]["blowup"] == (True,)
 
 
 @pytest.mark.gpu
