@@ -24,12 +24,13 @@ for exact in (False, True):
     e0.record(); ref.advance(240); e1.record(); torch.cuda.synchronize()
     base = e0.elapsed_time(e1) * 1e3 / 240
     out = {"exact": exact, "unsharded_us_per_step": round(base, 2)}
-    for transport in ("nccl", "peer"):
-        if transport == "nccl":
+    for transport in ("nccl", "nccl-eager", "peer"):
+        if transport.startswith("nccl"):
             c = Comm(0, 1, True, "nccl", unique_id=Comm.unique_id())
         else:
             c = Comm(0, 1, True, "peer", max_width=4096); c.connect([c.export()])
-        s = ShardedStepper(g, st, prob, scheme, dt, 0, 1, CommHalo(c), exact=exact, force_halo=True)
+        s = ShardedStepper(g, st, prob, scheme, dt, 0, 1, CommHalo(c), exact=exact, force_halo=True,
+                           graph=(transport == "nccl"))
         s.set_initial(u0)
         own = torch.cuda.Stream(); own.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(own):
