@@ -521,6 +521,35 @@ int lmep_step_linear_host(const lmep_grid *grid, const lmep_weights *w, const lm
                           const lmep_tuning *tuning, int32_t *nonfinite, void *stream,
                           double *host_out, int parts, void *copy_stream);
 
+/* Streamed linear steps: timestep.run's harvest -> steps -> snapshot sequence
+ * (timestep.py:284-350) as ONE pipeline.  For per-node rows on a periodic
+ * grid (one shard, even N, the persistent per-node kernels' plan; anything
+ * else returns LMEP_INVALID_CONFIG and the caller steps with
+ * lmep_step_linear_host once everything has landed), the rows `w->pernode` and
+ * the initial values `u_in` may still be arriving when stepping starts: the
+ * caller reports, in stream order, that nodes [0, nodes_ready) of both are
+ * valid, and every call launches all the k-step launches whose inputs are
+ * complete, in a skewed space-time order (step_stream.cu).  The call with
+ * nodes_ready = N finishes the ring.  u_in, u_out and scratch are three
+ * distinct N-vectors (16-byte aligned); the result lands in u_out and, range by
+ * range behind the last level's launches, in host_out (nullable, page-locked)
+ * through copy_stream.  Bit-identical to lmep_step_linear on the same rows.
+ * `nonfinite` as in lmep_step_linear (cleared on `stream` by _begin).
+ * _info: level-1 tile size (nodes), frontier margin (nodes), number of launch
+ * levels and SM count, from which a caller sizes its slices (a slice ending at
+ * margin + c * sms * tile gives every level c full waves of tiles).
+ * _end frees the plan (LMEP_INVALID_CONFIG if the ring was never finished) and
+ * reports how many launches it issued. */
+typedef struct lmep_lin_stream lmep_lin_stream;
+int lmep_lin_stream_begin(const lmep_grid *grid, const lmep_weights *w, const double *u_in,
+                          double *u_out, double *scratch, int64_t steps, int32_t flags,
+                          const lmep_tuning *tuning, int32_t *nonfinite, double *host_out,
+                          void *copy_stream, void *stream, lmep_lin_stream **out);
+int lmep_lin_stream_info(const lmep_lin_stream *s, int64_t *tile, int64_t *margin,
+                         int32_t *levels, int32_t *sms);
+int lmep_lin_stream_advance(lmep_lin_stream *s, int64_t nodes_ready, void *stream);
+int lmep_lin_stream_end(lmep_lin_stream *s, int64_t *launches);
+
 /* Fused four-stage ETDRK4 (kernels.py:62-132, run_etdrk4): rows W, ALPHA, BETA,
  * GAMMA, WHALF, P1HALF (and D1 for LMEP_NL_CONVECTIVE).  nl0_out (nullable)
  * receives N(u_in) on the owned nodes (the history entry the ETD multistep

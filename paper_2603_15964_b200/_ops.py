@@ -100,6 +100,134 @@ def drop_deferred(up: DeferredUpload) -> None:
         q.remove(up)
 
 
+class LinearStream:
+    """Consumer of a pipelined per-node harvest: timestep.run's linear scheme
+    from host arrays as one pipeline (lmep_lin_stream, csrc/step_stream.cu).
+    The harvest pipeline (harvest._harvest_pipelined) calls, in order,
+    ``begin`` (the row table exists, nothing harvested yet: the library plans
+    the launch levels and this object sizes the slices), ``upload`` per slice on
+    the upload stream (the slice of the initial state rides with its
+    coefficients), ``ready`` after each slice's harvest is queued (every k-step launch
+    whose inputs are complete is queued behind it; the last slice finishes the
+    ring), and ``uploaded`` once every slice is queued (snapshot 0 goes back
+    down).  The result and its host copy (``host_out``) are bit-identical to
+    Stepper.advance on the same rows.  When the library declines the plan
+    (LMEP_INVALID_CONFIG: not the persistent per-node kernels' case) the object
+    only uploads the initial state and the caller steps afterwards."""
+
+    # slices in waves of (SM count) level-1 tiles: a small first slice (its upload
+    # is the only exposed one), wide middle slices (few launches), a small last
+    # slice (its download is the only exposed one)
+    WAVES = (1.0, 3.0, 6.0, 8.0)
+    LAST_MIN = 2.0
+
+    def __init__(self, u0_host: torch.Tensor, steps: int, exact: bool, tuning, snap0: torch.Tensor,
+                 host_out: torch.Tensor, down: torch.cuda.Stream):
+        d = nat.device()
+        self.N = int(u0_host.numel())
+        self.src = u0_host
+        self.u0 = torch.empty(self.N, dtype=F64, device=d)
+        self.out = torch.empty(self.N, dtype=F64, device=d)
+        self.scr = torch.empty(self.N, dtype=F64, device=d)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=d)
+        self.steps, self.exact, self.tuning = int(steps), bool(exact), tuning
+        self.snap0, self.host_out, self.down = snap0, host_out, down
+        self.handle = None
+        self.active = False
+        self.began = False
+        self.last_landed = None
+        self.snap0_event = None
+        self.marks = []                      # (harvest queued, steps queued) events per slice
+        self.launches = 0
+        self.bounds = None
+
+    def begin(self, layout: StencilSet, rows: torch.Tensor, default_bounds):
+        self.began = True
+        self.rows = rows
+        if rows.shape[0] != 1 or rows.shape[2] != self.N or self.steps < 1:
+            return default_bounds
+        g = c_grid(layout, 0, None)
+        w = nat.LmepWeights(nat.W_PERNODE, 1, 0, 0, None, None, rows.data_ptr(), 0)
+        tun = _tuning(self.tuning)
+        h = C.c_void_p()
+        L = nat.lib()
+        st = L.lmep_lin_stream_begin(C.byref(g), C.byref(w), self.u0.data_ptr(), self.out.data_ptr(),
+                                     self.scr.data_ptr(), self.steps, nat.FLAG_EXACT if self.exact else 0,
+                                     C.byref(tun) if tun is not None else None, self.flag.data_ptr(),
+                                     self.host_out.data_ptr(), self.down.cuda_stream,
+                                     nat.stream_handle(), C.byref(h))
+        if st == nat.LMEP_INVALID_CONFIG:
+            return default_bounds
+        nat.check(st, "lmep_lin_stream_begin")
+        self.handle, self.active = h, True
+        tile, margin, lev, sms = C.c_int64(), C.c_int64(), C.c_int32(), C.c_int32()
+        nat.check(L.lmep_lin_stream_info(h, C.byref(tile), C.byref(margin), C.byref(lev), C.byref(sms)),
+                  "lmep_lin_stream_info")
+        self.bounds = self.slice_bounds(self.N, tile.value, margin.value, sms.value)
+        return self.bounds
+
+    @classmethod
+    def slice_bounds(cls, N: int, tile: int, margin: int, sms: int):
+        """Prefix ends (multiples of 1024 nodes, the harvest's superblock) that give
+        every launch level whole waves of tiles: margin + c * sms * tile."""
+        wave = sms * tile
+        out, a, c = [], 0, 0.0
+        for wv in cls.WAVES:
+            c += wv
+            b = -(-int(margin + c * wave) // 1024) * 1024
+            if b + cls.LAST_MIN * wave >= N:
+                break
+            out.append((a, b))
+            a = b
+        out.append((a, N))
+        return out
+
+    def upload(self, a: int, b: int) -> None:
+        """(on the upload stream) the slice of the initial state."""
+        self.u0[a:b].copy_(self.src[a:b], non_blocking=True)
+
+    def uploaded(self, up: torch.cuda.Stream, ev) -> None:
+        """Every slice is queued on the upload stream `up` (ev: the last one's
+        event): snapshot 0 (timestep.py:313) goes back down behind them, off the
+        stream that carries the result."""
+        with torch.cuda.stream(up):
+            self.snap0.copy_(self.u0, non_blocking=True)
+        self.snap0_event = up.record_event()
+        self.last_landed = ev
+
+    def ready(self, b: int) -> None:
+        """The harvest of nodes [0, b) is queued on the current stream."""
+        if not self.active:
+            return
+        cur = torch.cuda.current_stream()
+        eh = torch.cuda.Event(enable_timing=True)
+        es = torch.cuda.Event(enable_timing=True)
+        eh.record(cur)
+        nat.check(nat.lib().lmep_lin_stream_advance(self.handle, int(b), cur.cuda_stream),
+                  "lmep_lin_stream_advance")
+        es.record(cur)
+        self.marks.append((eh, es))
+
+    def close(self) -> None:
+        if self.handle is not None:
+            n = C.c_int64()
+            st = nat.lib().lmep_lin_stream_end(self.handle, C.byref(n))
+            self.handle = None
+            self.launches = n.value
+            if self.active:
+                nat.check(st, "lmep_lin_stream_end")
+
+
+def set_stream_consumer(ls) -> None:
+    _TLS.stream = ls
+
+
+def take_stream_consumer():
+    ls = getattr(_TLS, "stream", None)
+    _TLS.stream = None
+    return ls
+
+
 def is_host(a) -> bool:
     """True for data that lives in host memory (numpy / CPU tensors)."""
     return not (isinstance(a, torch.Tensor) and a.device.type == "cuda")

@@ -66,6 +66,7 @@ struct StepParams {
     double *push_l, *push_r;                    // fused peer stores of the slab edges (or null)
     int64_t push_w;
     int64_t tile_lo, tile_hi;                   // persistent per-node kernels: tiles of this launch (hi = 0: all)
+    int64_t tile_wrap;                          // ... > 0: tile indices >= tile_wrap continue at tile 0 (a range that wraps)
     int64_t ext_off;                            // ... on a slab: u_in / rows start ext_off nodes before the owned ones
     double *nl0_out;
     double dt;

@@ -81,6 +81,7 @@ struct TileRange {
 __device__ __forceinline__ TileRange tile_range(const StepParams &p, int64_t tile, int K, int eL, int eR)
 {
     TileRange r;
+    if (p.tile_wrap > 0 && tile >= p.tile_wrap) tile -= p.tile_wrap;   // a launch over [lo, wrap + hi')
     // slabs (p.ext_off > 0): u_in and the row table are the slab's extended arrays
     // [ghosts | owned | ghosts] of p.N nodes, the owned nodes ext_off .. ext_off+nloc-1;
     // the staged ranges never wrap there
@@ -436,7 +437,13 @@ static int launch_tmx(const StepParams &p, unsigned grid, cudaStream_t st)
     else if (p.n == 7 && p.row == 6) k = lin_pernode_tmx_kernel<7, 6, J, NT, EX, MINB>;
     else if (p.n == 7 && p.row == 0) k = lin_pernode_tmx_kernel<7, 0, J, NT, EX, MINB>;
     if (!k) return -1;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+    // (the attribute is per device and per kernel: set once for each (n, row) here)
+    static std::atomic<uint64_t> attr_done[LMEP_MAX_N + 1][LMEP_MAX_N + 1];
+    const int dev = current_device();
+    if (!done_on_device(attr_done[p.n][p.row], dev)) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        mark_device(attr_done[p.n][p.row], dev);
+    }
     k<<<grid, NT, shm, st>>>(p);
     return launch_status("lin_pernode_tmx_kernel");
 }

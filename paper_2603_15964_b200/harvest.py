@@ -374,7 +374,7 @@ def harvest_compact(grid: Grid, sset: StencilSet, spec, delta_t: float, s: int,
         # host coefficients: upload in chunks on the copy stream, each chunk's
         # harvest starting as soon as its slice has landed
         h = _harvest_pipelined(spec, sl, N, n, s, delta_t,
-                               lambda: _tables_for(grid, sset, plan, terms)[0], sset.row)
+                               lambda: _tables_for(grid, sset, plan, terms)[0], sset.row, sset)
         _ops.raise_on_status(h)
         if stats is not None:
             stats.setdefault("ms", []).append(h.ms)
@@ -477,7 +477,7 @@ def _pipeline_bounds(N: int):
 
 
 def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
-                       tables_fn, row: int) -> _ops.HarvestOut:
+                       tables_fn, row: int, sset: StencilSet | None = None) -> _ops.HarvestOut:
     """Per-node harvest (one shared window geometry) from HOST coefficients:
     the [N, K] coefficient table goes up in growing slices (_pipeline_bounds;
     multiples of 1024 items, so the block-balanced kernel's superblocks and
@@ -498,25 +498,57 @@ def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
     out = _ops.HarvestOut(torch.empty((s, n, N), dtype=torch.float64, device=d),
                           torch.empty(N, dtype=torch.int32, device=d),
                           torch.empty(N, dtype=torch.int32, device=d))
-    cp.wait_stream(cur)                      # dc / dr were allocated on cur
     bounds = _pipeline_bounds(N)
-    landed = []
-    with torch.cuda.stream(cp):
-        for a, b in bounds:
+    # a streamed linear run (timestep.run): its steps follow the harvest slice by
+    # slice, and it sizes the slices for its launch levels
+    ls = _ops.take_stream_consumer()
+    if ls is not None and (s != 1 or sset is None or sl.start != 0 or N != ls.N or N != sset.N):
+        ls = None
+    if ls is not None:
+        bounds = ls.begin(sset, out.rows, bounds)
+    cp.wait_stream(cur)                      # dc / dr (and the stream's buffers) were allocated on cur
+
+    def upload(i):
+        a, b = bounds[i]
+        with torch.cuda.stream(cp):
             dc[a:b].copy_(hc[a:b], non_blocking=True)
             if dr is not None:
                 dr[a:b].copy_(hr[a:b], non_blocking=True)
-            landed.append(cp.record_event())
-    dc.record_stream(cp)
-    if dr is not None:
-        dr.record_stream(cp)
-    _ops.issue_deferred(cp)                  # e.g. run()'s initial state, behind the slices
-    tables = tables_fn()                     # overlaps the first slices' transfer
-    for (a, b), ev in zip(bounds, landed):
+            if ls is not None:
+                ls.upload(a, b)
+            return cp.record_event()
+
+    def harvest_slice(i, ev):
+        a, b = bounds[i]
         cur.wait_event(ev)
         _ops.harvest(n, s, delta_t, b - a, tables=tables, coef=dc[a:b], coef_stride=K,
                      c0=None if dr is None else dr[a:b], c0_stride=0 if dr is None else 1,
                      row_default=row, frozen_default=0, layout=1, into=out, item0=a)
+        if ls is not None:
+            ls.ready(b)
+
+    if ls is None:
+        # every slice is queued before the tables are built, so PCIe starts at once
+        landed = [upload(i) for i in range(len(bounds))]
+        _ops.issue_deferred(cp)              # e.g. run()'s initial state, behind the slices
+        tables = tables_fn()                 # overlaps the first slices' transfer
+        for i, ev in enumerate(landed):
+            harvest_slice(i, ev)
+    else:
+        # streamed run: the host's own enqueue time is on the critical path until
+        # the first harvest is queued, so the uploads stay just two slices ahead of
+        # the harvests (PCIe never idles: a slice takes longer to land than the
+        # host needs to queue a harvest and its step launches)
+        landed = [upload(i) for i in range(min(2, len(bounds)))]
+        tables = tables_fn()
+        for i in range(len(bounds)):
+            harvest_slice(i, landed[i])
+            if i + 2 < len(bounds):
+                landed.append(upload(i + 2))
+        ls.uploaded(cp, landed[-1])
+    dc.record_stream(cp)
+    if dr is not None:
+        dr.record_stream(cp)
     return out
 
 

@@ -327,6 +327,17 @@ class Stepper:
         self._scr = torch.empty(max(prep.s, 2) * N, dtype=torch.float64, device=u0.device)
         self._hout = None
 
+    @classmethod
+    def resumed(cls, prep: Prepared, u: torch.Tensor, spare: torch.Tensor, scratch: torch.Tensor,
+                flag: torch.Tensor, done: int, exact: bool = True, tuning=None) -> "Stepper":
+        """A linear stepper whose first `done` steps already ran elsewhere (the
+        streamed pipeline): u is the state after them, spare / scratch its buffers."""
+        self = cls.__new__(cls)
+        self.p, self.exact, self.tuning = prep, exact, tuning
+        self.u, self._out, self._scr, self.flag = u, spare, scratch, flag
+        self.hist, self._hout, self.done = None, None, done
+        return self
+
     def advance(self, k: int, host_out: torch.Tensor | None = None,
                 copy_stream: int | None = None) -> None:
         """k more steps.  host_out (linear scheme): a page-locked host vector that
@@ -379,8 +390,13 @@ class Stepper:
 
 def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
         delta_t: float, t_final: float, snapshot_stride: float | None = None, *,
-        exact: bool = True, tuning=None, stats: dict | None = None) -> SimulationResult:
-    """Integrate to t_final with snapshots (timestep.py:255-394), on the GPU."""
+        exact: bool = True, tuning=None, stats: dict | None = None,
+        stream: bool = True) -> SimulationResult:
+    """Integrate to t_final with snapshots (timestep.py:255-394), on the GPU.
+    stream=True: a linear run from host coefficients and host initial data on a
+    periodic grid runs upload, harvest, the first chunk of steps and the
+    snapshot download as one pipeline (csrc/step_stream.cu), bit-identical to
+    the phase-by-phase order on the same rows."""
     if t_final <= 0:
         raise InvalidConfig("t_final must be positive")
     if delta_t <= 0:
@@ -412,7 +428,19 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
     # it goes up at once on its own copy stream.
     lin = problem.linear
     deferred = None
-    if isinstance(lin, VariableCoefficientSpec) and _ops.is_host(lin.coef) and _ops.is_host(u0):
+    ls = None
+    nsnap = 1 + (-(-steps_total // snap_every) if snap_every else 0)
+    # snapshots land straight in one page-locked [S, N] block (returned as is)
+    snaps = torch.empty((nsnap, N), dtype=torch.float64, pin_memory=True)
+    k_first = min(snap_every, steps_total)
+    host_in = isinstance(lin, VariableCoefficientSpec) and _ops.is_host(lin.coef) and _ops.is_host(u0)
+    if host_in and stream and scheme.kind == "linear" and grid.periodic and k_first >= 1 and \
+            problem.boundary.kind == "periodic":
+        # one pipeline: upload || harvest || steps || download, slice by slice
+        # (_ops.LinearStream); the initial state rides up with the coefficients
+        ls = _ops.LinearStream(_ops.host_f64(u0), k_first, exact, tuning, snaps[0], snaps[1], cp1)
+        _ops.set_stream_consumer(ls)
+    elif host_in:
         src = _ops.host_f64(u0)
         deferred = _ops.DeferredUpload(src, torch.empty(N, dtype=torch.float64, device=dev))
         _ops.defer_upload(deferred)
@@ -425,24 +453,58 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
         # host runs ahead and prepares the stepping while the device harvests
         with _ops.deferred_status_checks() as pending:
             prep = prepare(grid, stencils, problem, scheme, delta_t, stats)
+    except BaseException:
+        if ls is not None:
+            ls.active = False
+            ls.close()
+        raise
     finally:
+        _ops.take_stream_consumer()
         if deferred is not None:
             _ops.drop_deferred(deferred)
     if deferred is not None:
         if deferred.event is None:           # the harvest did not pipeline: upload now
             deferred.issue(cp1)
         u0d, ev_u0 = deferred.dst, deferred.event
-    nsnap = 1 + (-(-steps_total // snap_every) if snap_every else 0)
-    # snapshots land straight in one page-locked [S, N] block (returned as is)
-    snaps = torch.empty((nsnap, N), dtype=torch.float64, pin_memory=True)
+    if ls is not None:
+        if not ls.began:                     # the harvest did not pipeline: upload now
+            cp.wait_stream(cur)
+            with torch.cuda.stream(cp):
+                ls.upload(0, N)
+            ls.uploaded(cp, cp.record_event())
+        u0d, ev_u0 = ls.u0, ls.last_landed
     ev_harvest = torch.cuda.Event(enable_timing=True)
     ev_harvest.record(cur)
     harvest_ns = None
+    times = [0.0]
+    step_ns = 0
+    done = 0
 
-    cur.wait_event(ev_u0)
-    u0d.record_stream(cur)
-    st = Stepper(prep, u0d, exact=exact, tuning=tuning)
-    snap_ev = None
+    if ls is not None and ls.active:
+        # the first chunk's steps were queued slice by slice behind the harvest and
+        # both snapshots are on their way down (copy stream 1)
+        ls.close()
+        st = Stepper.resumed(prep, ls.out, ls.u0, ls.scr, ls.flag, k_first, exact=exact, tuning=tuning)
+        cp1.wait_event(ls.snap0_event)
+        snap_ev = prev_ev = cp1.record_event()
+        cur.synchronize()
+        t_prev, harvest_ms, step_ms = ev_start, 0.0, 0.0
+        for eh, es in ls.marks:
+            harvest_ms += t_prev.elapsed_time(eh)
+            step_ms += eh.elapsed_time(es)
+            t_prev = es
+        harvest_ns, step_ns = int(harvest_ms * 1e6), int(step_ms * 1e6)
+        _ops.check_deferred(pending)
+        done = k_first
+        if st.nonfinite():
+            cp1.synchronize()
+            raise NonFinite("time integration blew up", state=snaps[0].numpy().copy(), time=0.0)
+        times.append(done * delta_t)
+    else:
+        cur.wait_event(ev_u0)
+        u0d.record_stream(cur)
+        st = Stepper(prep, u0d, exact=exact, tuning=tuning)
+        snap_ev = None
 
     def snapshot(i):
         # D2H on the copy stream, overlapping the next chunk of steps; the
@@ -453,10 +515,10 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
         st.u.record_stream(cp)
         return cp.record_event()
 
-    times = [0.0]
-    snap_ev, prev_ev = snapshot(0), None
-    step_ns = 0
-    done = 0
+    if done == 0 and ls is not None and ls.began:
+        snap_ev, prev_ev = ls.snap0_event, None          # snapshot 0 is already on its way down
+    elif done == 0:
+        snap_ev, prev_ev = snapshot(0), None
     ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     while done < steps_total:
         k = min(snap_every, steps_total - done)
@@ -502,6 +564,9 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
         harvest_ns = int(ev_start.elapsed_time(ev_harvest) * 1e6)
         _ops.check_deferred(pending)
     cp.synchronize()
+    if ls is not None:
+        cp1.synchronize()
+        ls.snap0_event.synchronize()
     return SimulationResult(times=np.array(times), snapshots=snaps.numpy(), steps=steps_total,
                             harvest_ns=harvest_ns, step_ns=step_ns)
 
