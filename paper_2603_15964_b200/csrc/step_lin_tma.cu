@@ -338,8 +338,14 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
                     }
                     return a;
                 };
+#ifndef LMEP_TMX_ONECHAIN
+#define LMEP_TMX_ONECHAIN 1
+#endif
+#ifndef LMEP_TMX_OWN_PRE
+#define LMEP_TMX_OWN_PRE (J / 2)
+#endif
 #pragma unroll
-                for (int j = 0; j < J / 2; ++j) own[j] = own_chain(j);
+                for (int j = 0; j < LMEP_TMX_OWN_PRE; ++j) own[j] = own_chain(j);
                 __syncthreads();
                 double hl[EL > 0 ? EL : 1], hr[ER > 0 ? ER : 1];
                 // window slot EL + o is staged node J tid + o: slot (o mod J) of thread
@@ -356,22 +362,38 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
                     hr[m] = Qb[(o % J) * QS + 2 + tid + o / J];
                 }
 #pragma unroll
-                for (int j = J / 2; j < J; ++j) own[j] = own_chain(j);
+                for (int j = LMEP_TMX_OWN_PRE; j < J; ++j) own[j] = own_chain(j);
                 // halo chains, tap by tap across the nodes (independent FMAs back to back):
                 // left taps c < EL - j read hl[j + c], right taps c > EL+J-1-j read hr[j+c-EL-J]
 #pragma unroll
-                for (int j = 0; j < J; ++j) hal[j] = 0.0;
+                for (int j = 0; j < J; ++j) hal[j] = LMEP_TMX_ONECHAIN ? own[j] : 0.0;
+                // A DFMA whose three operands are all fresh register pairs costs three
+                // register-file cycles against two issue cycles (tools/rf_probe.cu: 3.0 clk
+                // with no operand reuse, 2.0 with one operand in the reuse cache), so the
+                // order WITHIN each node's chain is chosen such that the k-th product of
+                // every chain reads the same halo value: ptxas interleaves the J chains
+                // round-robin, and products k of consecutive nodes then share that value
+                // through the operand reuse cache (as the own-value chains do by
+                // construction).  Node j takes its right-halo values R_0 .. first (nodes
+                // j >= m share R_m at position m), then its left-halo values L_j .. L_{EL-1}
+                // (nodes j < k share L_{k-1} at position k): 12 fresh halo reads for 42
+                // products at n = 13.
 #pragma unroll
-                for (int c = 0; c < NS; ++c) {
+                for (int k = 0; k < EL + ER; ++k) {
 #pragma unroll
                     for (int j = 0; j < J; ++j) {
-                        const int i = j + c;
-                        if (i < EL) hal[j] = fma(w[j][c], hl[i], hal[j]);
-                        else if (i >= EL + J) hal[j] = fma(w[j][c], hr[i - EL - J], hal[j]);
+                        constexpr int dR = ER - J + 1;                        // node j reads R_0 .. R_{j+dR-1}
+                        const int nr = j + dR < 0 ? 0 : (j + dR > ER ? ER : j + dR);
+                        if (k < nr) {
+                            hal[j] = fma(w[j][EL + J + k - j], hr[k], hal[j]);
+                        } else {
+                            const int i = j + (k - nr);                       // left value L_i, tap i - j
+                            if (i < EL) hal[j] = fma(w[j][i - j], hl[i], hal[j]);
+                        }
                     }
                 }
 #pragma unroll
-                for (int j = 0; j < J; ++j) x[j] = own[j] + hal[j];
+                for (int j = 0; j < J; ++j) x[j] = LMEP_TMX_ONECHAIN ? hal[j] : own[j] + hal[j];
             } else {
                 __syncthreads();
                 double win[W];
