@@ -350,16 +350,18 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
                 double hl[EL > 0 ? EL : 1], hr[ER > 0 ? ER : 1];
                 // window slot EL + o is staged node J tid + o: slot (o mod J) of thread
                 // tid + floor(o / J) -- the one or two nearest threads on each side
+                // (loads in the order the chains consume them: R_0, L_0, R_1, L_1, ...)
 #pragma unroll
-                for (int m = 0; m < EL; ++m) {
-                    const int o = m - EL;                                  // -EL .. -1
-                    const int dt = -((-o + J - 1) / J);                    // floor(o / J)
-                    hl[m] = Qb[(o - dt * J) * QS + 2 + tid + dt];
-                }
-#pragma unroll
-                for (int m = 0; m < ER; ++m) {
-                    const int o = J + m;
-                    hr[m] = Qb[(o % J) * QS + 2 + tid + o / J];
+                for (int m = 0; m < (EL > ER ? EL : ER); ++m) {
+                    if (m < ER) {
+                        const int o = J + m;
+                        hr[m] = Qb[(o % J) * QS + 2 + tid + o / J];
+                    }
+                    if (m < EL) {
+                        const int o = m - EL;                              // -EL .. -1
+                        const int dt = -((-o + J - 1) / J);                // floor(o / J)
+                        hl[m] = Qb[(o - dt * J) * QS + 2 + tid + dt];
+                    }
                 }
 #pragma unroll
                 for (int j = LMEP_TMX_OWN_PRE; j < J; ++j) own[j] = own_chain(j);
