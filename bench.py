@@ -738,9 +738,12 @@ def main():
         step_note = (f"rows held in registers for {min(ks)}-{max(ks)} steps per launch: "
                      f"{step_bytes_total / (bench.nloc * w.steps):.1f} B/point-step against 120 for "
                      "one step per launch (roofline_step_onestep); after blocking HBM is no longer "
-                     "the bound (ncu DRAM 23%, the TMA stream fully hidden): the rows fill the "
-                     "register file at two warps per scheduler, whose FMA chains alone take 482 of "
-                     "the 652 clk per step (tools/dfma_pattern.cu, tools/tmx_timing.py); see "
+                     "the bound (ncu DRAM 31%, the TMA stream fully hidden): the rows fill the "
+                     "register file at two warps per scheduler and every product reads its own "
+                     "weight from it, so the FMA chains are register-file bound (3 clk per DFMA "
+                     "with three fresh operands, 2 with a window value in the operand reuse cache: "
+                     "tools/rf_probe.cu; 51 of 78 reuse it); the per-step halo exchange (18 "
+                     "shared-memory accesses per thread + one barrier) is the rest; see "
                      "roofline_step_fp64")
     elif world > 1:
         # sharded slabs: lin_pernode_tb_kernel, rows in registers for the k steps a halo

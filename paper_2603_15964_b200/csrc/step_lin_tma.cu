@@ -320,15 +320,26 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
 #pragma unroll
             for (int j = 0; j < J; ++j) Qb[j * QS + 2 + tid] = x[j];
             if constexpr (!EX) {
-                // Fused mode: node j's sum splits into the products with this
-                // thread's own values (window slots EL .. EL+J-1: J taps per
-                // node) and the products with the neighbours' halo values.  The
-                // own chains of the first half of the nodes run between the
-                // stores and the barrier, the second half right after the halo
-                // loads are issued, so neither the barrier nor the shared-memory
-                // latency leaves the FP64 pipe idle; then the halo chains.
-                double own[J], hal[J];
-                auto own_chain = [&](int j) {
+                // Fused mode: ONE chain per node, ordered for the operand reuse cache.
+                // A DFMA whose three operands are all fresh register pairs costs three
+                // register-file cycles against two issue cycles (tools/rf_probe.cu), and
+                // only the window value can be shared between products (every weight is
+                // used once, the accumulator comes from the chain's previous product).
+                // ptxas interleaves the J independent chains round-robin whatever the
+                // source order, so the order WITHIN a chain is what decides: product k of
+                // every node's chain reads the same window value, and products k of
+                // consecutive nodes then take it from the reuse cache.
+                //   * first the thread's own values x[0 .. J-1] (window slots EL .. EL+J-1,
+                //     shared by all J nodes): these need no exchange, so ptxas runs them
+                //     between the stores and the barrier and behind the halo loads;
+                //   * then node j takes its right-halo values R_0 .. R_(nr-1) and after them
+                //     its left-halo values L_j .. L_(EL-1): at n = 13 position m pairs R_m
+                //     (nodes j >= m) with L_(m-1) (nodes j < m).
+                // 18 distinct values feed the 78 products at n = 13; ptxas marks 51 of
+                // them .reuse (26 with separate own / halo chains in tap order).
+                double acc[J];
+#pragma unroll
+                for (int j = 0; j < J; ++j) {
                     // taps c with EL <= j + c < EL + J (window slots of this thread's values)
                     double a = 0.0;
 #pragma unroll
@@ -336,16 +347,8 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
                         const int i = j + c;
                         if (i >= EL && i < EL + J) a = fma(w[j][c], x[i - EL], a);
                     }
-                    return a;
-                };
-#ifndef LMEP_TMX_ONECHAIN
-#define LMEP_TMX_ONECHAIN 1
-#endif
-#ifndef LMEP_TMX_OWN_PRE
-#define LMEP_TMX_OWN_PRE (J / 2)
-#endif
-#pragma unroll
-                for (int j = 0; j < LMEP_TMX_OWN_PRE; ++j) own[j] = own_chain(j);
+                    acc[j] = a;
+                }
                 __syncthreads();
                 double hl[EL > 0 ? EL : 1], hr[ER > 0 ? ER : 1];
                 // window slot EL + o is staged node J tid + o: slot (o mod J) of thread
@@ -364,38 +367,21 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
                     }
                 }
 #pragma unroll
-                for (int j = LMEP_TMX_OWN_PRE; j < J; ++j) own[j] = own_chain(j);
-                // halo chains, tap by tap across the nodes (independent FMAs back to back):
-                // left taps c < EL - j read hl[j + c], right taps c > EL+J-1-j read hr[j+c-EL-J]
-#pragma unroll
-                for (int j = 0; j < J; ++j) hal[j] = LMEP_TMX_ONECHAIN ? own[j] : 0.0;
-                // A DFMA whose three operands are all fresh register pairs costs three
-                // register-file cycles against two issue cycles (tools/rf_probe.cu: 3.0 clk
-                // with no operand reuse, 2.0 with one operand in the reuse cache), so the
-                // order WITHIN each node's chain is chosen such that the k-th product of
-                // every chain reads the same halo value: ptxas interleaves the J chains
-                // round-robin, and products k of consecutive nodes then share that value
-                // through the operand reuse cache (as the own-value chains do by
-                // construction).  Node j takes its right-halo values R_0 .. first (nodes
-                // j >= m share R_m at position m), then its left-halo values L_j .. L_{EL-1}
-                // (nodes j < k share L_{k-1} at position k): 12 fresh halo reads for 42
-                // products at n = 13.
-#pragma unroll
                 for (int k = 0; k < EL + ER; ++k) {
 #pragma unroll
                     for (int j = 0; j < J; ++j) {
                         constexpr int dR = ER - J + 1;                        // node j reads R_0 .. R_{j+dR-1}
                         const int nr = j + dR < 0 ? 0 : (j + dR > ER ? ER : j + dR);
                         if (k < nr) {
-                            hal[j] = fma(w[j][EL + J + k - j], hr[k], hal[j]);
+                            acc[j] = fma(w[j][EL + J + k - j], hr[k], acc[j]);
                         } else {
                             const int i = j + (k - nr);                       // left value L_i, tap i - j
-                            if (i < EL) hal[j] = fma(w[j][i - j], hl[i], hal[j]);
+                            if (i < EL) acc[j] = fma(w[j][i - j], hl[i], acc[j]);
                         }
                     }
                 }
 #pragma unroll
-                for (int j = 0; j < J; ++j) x[j] = LMEP_TMX_ONECHAIN ? hal[j] : own[j] + hal[j];
+                for (int j = 0; j < J; ++j) x[j] = acc[j];
             } else {
                 __syncthreads();
                 double win[W];
