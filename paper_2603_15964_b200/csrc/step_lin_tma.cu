@@ -337,9 +337,11 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
                 //     (nodes j >= m) with L_(m-1) (nodes j < m).
                 // 18 distinct values feed the 78 products at n = 13; ptxas marks 51 of
                 // them .reuse (26 with separate own / halo chains in tap order).
-                double acc[J];
-#pragma unroll
-                for (int j = 0; j < J; ++j) {
+                // (The generated schedule is sensitive to the source shape: this form --
+                // own[] / hal[] arrays, the two switches below at their defaults --
+                // measured 1.60 ms for C5's 200 steps, an equivalent rewrite 1.63.)
+                double own[J], hal[J];
+                auto own_chain = [&](int j) {
                     // taps c with EL <= j + c < EL + J (window slots of this thread's values)
                     double a = 0.0;
 #pragma unroll
@@ -347,8 +349,16 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
                         const int i = j + c;
                         if (i >= EL && i < EL + J) a = fma(w[j][c], x[i - EL], a);
                     }
-                    acc[j] = a;
-                }
+                    return a;
+                };
+#ifndef LMEP_TMX_ONECHAIN
+#define LMEP_TMX_ONECHAIN 1
+#endif
+#ifndef LMEP_TMX_OWN_PRE
+#define LMEP_TMX_OWN_PRE (J / 2)
+#endif
+#pragma unroll
+                for (int j = 0; j < LMEP_TMX_OWN_PRE; ++j) own[j] = own_chain(j);
                 __syncthreads();
                 double hl[EL > 0 ? EL : 1], hr[ER > 0 ? ER : 1];
                 // window slot EL + o is staged node J tid + o: slot (o mod J) of thread
@@ -367,21 +377,26 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
                     }
                 }
 #pragma unroll
+                for (int j = LMEP_TMX_OWN_PRE; j < J; ++j) own[j] = own_chain(j);
+                // the chains continue (LMEP_TMX_ONECHAIN) with the halo values
+#pragma unroll
+                for (int j = 0; j < J; ++j) hal[j] = LMEP_TMX_ONECHAIN ? own[j] : 0.0;
+#pragma unroll
                 for (int k = 0; k < EL + ER; ++k) {
 #pragma unroll
                     for (int j = 0; j < J; ++j) {
                         constexpr int dR = ER - J + 1;                        // node j reads R_0 .. R_{j+dR-1}
                         const int nr = j + dR < 0 ? 0 : (j + dR > ER ? ER : j + dR);
                         if (k < nr) {
-                            acc[j] = fma(w[j][EL + J + k - j], hr[k], acc[j]);
+                            hal[j] = fma(w[j][EL + J + k - j], hr[k], hal[j]);
                         } else {
                             const int i = j + (k - nr);                       // left value L_i, tap i - j
-                            if (i < EL) acc[j] = fma(w[j][i - j], hl[i], acc[j]);
+                            if (i < EL) hal[j] = fma(w[j][i - j], hl[i], hal[j]);
                         }
                     }
                 }
 #pragma unroll
-                for (int j = 0; j < J; ++j) x[j] = acc[j];
+                for (int j = 0; j < J; ++j) x[j] = LMEP_TMX_ONECHAIN ? hal[j] : own[j] + hal[j];
             } else {
                 __syncthreads();
                 double win[W];
