@@ -233,6 +233,14 @@ int lmep_harvest_chunk(int n, int s, int nterms, const double *tables, const int
                        int32_t *status, int32_t *ms, const lmep_coef_map *map, int64_t out_ld,
                        void *stream);
 
+/* Slices of ONE harvest (lmep_harvest_chunk / lmep_harvest_ex calls over
+ * consecutive item ranges of one table): while on (per host thread), a
+ * constant-table harvest whose tables, step and shape equal those of the
+ * device's previous one keeps that call's prepared block (the balancing of the
+ * first slice's first item), so the rows equal a one-launch harvest's bit for
+ * bit whatever the slicing, and later slices skip the prep kernel. */
+int lmep_harvest_reuse_prep(int on);
+
 /* All harvest options in one argument block (lmep_harvest_chunk's arguments
  * plus two):
  *   half_out   (nullable, s >= 2) also the (w_lin, raw dt/2 phi_1) rows of

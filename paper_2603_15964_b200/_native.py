@@ -51,7 +51,7 @@ EXPORTS = (
     "lmep_graph_begin", "lmep_graph_end", "lmep_graph_launch", "lmep_graph_destroy",
     "lmep_comm_targets", "lmep_comm_push", "lmep_comm_signal", "lmep_comm_wait",
     "lmep_comm_ghosts", "lmep_set_etd2_persistent", "lmep_step_linear_host", "lmep_comm_chunk",
-    "lmep_lin_stream_begin", "lmep_lin_stream_info", "lmep_lin_stream_advance", "lmep_lin_stream_end",
+    "lmep_harvest_reuse_prep", "lmep_lin_stream_begin", "lmep_lin_stream_info", "lmep_lin_stream_advance", "lmep_lin_stream_end",
 )
 COMM_NCCL, COMM_PEER = 0, 1
 COMM_ID_BYTES, COMM_BLOB_BYTES, COMM_MAX_FIELDS = 128, 512, 8
@@ -148,6 +148,7 @@ def load(path: str | None = None):
                      C.POINTER(LmepHalo), C.POINTER(LmepTuning))
     L.lmep_step_linear.argtypes = [G, W, B, H, vp, vp, vp, i64, i32, T, vp, vp]
     L.lmep_step_linear_host.argtypes = [G, W, B, H, vp, vp, vp, i64, i32, T, vp, vp, vp, C.c_int, vp]
+    L.lmep_harvest_reuse_prep.argtypes = [C.c_int]
     L.lmep_lin_stream_begin.argtypes = [G, W, vp, vp, vp, i64, i32, T, vp, vp, vp, vp, C.POINTER(vp)]
     L.lmep_lin_stream_info.argtypes = [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i32),
                                        C.POINTER(i32)]

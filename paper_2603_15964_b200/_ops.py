@@ -118,7 +118,7 @@ class LinearStream:
     # slices in waves of (SM count) level-1 tiles: a small first slice (its upload
     # is the only exposed one), wide middle slices (few launches), a small last
     # slice (its download is the only exposed one)
-    WAVES = (1.0, 3.0, 6.0, 8.0)
+    WAVES = (1.0, 4.0, 7.0, 7.0)
     LAST_MIN = 2.0
 
     def __init__(self, u0_host: torch.Tensor, steps: int, exact: bool, tuning, snap0: torch.Tensor,

@@ -405,10 +405,25 @@ __global__ void __launch_bounds__(128, 3) harvest_mvc_kernel(const HarvestParams
 // Per-device state: the prep kernel's output block and the event of the
 // device's last constant-table launch.  (__constant__ c_mvc itself is a
 // per-device copy of the module's constant bank.)
+struct MvcKey {
+    const double *tables = nullptr;
+    double dt = 0.0;
+    int n = 0, s = 0, nterms = 0, row = 0, c0 = 0;
+    bool operator==(const MvcKey &o) const
+    {
+        return tables == o.tables && dt == o.dt && n == o.n && s == o.s && nterms == o.nterms &&
+               row == o.row && c0 == o.c0;
+    }
+};
 struct MvcDevice {
     MvcConst *scratch = nullptr;
     cudaEvent_t done = nullptr;
+    MvcKey key;                          // what the device's constant block was prepared for
+    bool valid = false;
 };
+// lmep_harvest_reuse_prep: the calling thread's next constant-table harvests are
+// slices of one harvest and keep the first slice's prepared block
+thread_local int t_reuse_prep = 0;
 MvcDevice g_mvc_dev[kMaxDevices];
 std::mutex g_mvc_mu;
 
@@ -464,9 +479,20 @@ int launch_harvest_mvc(const HarvestParams &P, cudaStream_t st)
         e = cudaStreamWaitEvent(st, D.done, 0);
         if (e != cudaSuccess) { set_last_error("cudaStreamWaitEvent", e); return LMEP_CUDA_ERROR; }
     }
-    mvc_prep_kernel<<<1, 32, 0, st>>>(P, D.scratch);
-    e = cudaMemcpyToSymbolAsync(c_mvc, D.scratch, sizeof(MvcConst), 0, cudaMemcpyDeviceToDevice, st);
-    if (e != cudaSuccess) { set_last_error("cudaMemcpyToSymbolAsync", e); return LMEP_CUDA_ERROR; }
+    MvcKey key;
+    key.tables = P.tables; key.dt = P.delta_t; key.n = P.n; key.s = P.s; key.nterms = P.nterms;
+    key.row = P.row_default; key.c0 = P.c0 != nullptr;
+    // a later slice of the same harvest (same tables, step and shape; the block in
+    // constant memory is still the one prepared for its first slice): the balancing
+    // of that first slice's item serves the whole table, as in a one-launch harvest
+    const bool reuse = t_reuse_prep && D.valid && key == D.key;
+    if (!reuse) {
+        mvc_prep_kernel<<<1, 32, 0, st>>>(P, D.scratch);
+        e = cudaMemcpyToSymbolAsync(c_mvc, D.scratch, sizeof(MvcConst), 0, cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) { set_last_error("cudaMemcpyToSymbolAsync", e); return LMEP_CUDA_ERROR; }
+        D.key = key;
+        D.valid = true;
+    }
     switch (P.n) {
     case 7: launch_mvc_d<7>(P, st); break;
     case 9: launch_mvc_d<9>(P, st); break;
@@ -478,3 +504,9 @@ int launch_harvest_mvc(const HarvestParams &P, cudaStream_t st)
 }
 
 }  // namespace lmep
+
+extern "C" int lmep_harvest_reuse_prep(int on)
+{
+    lmep::t_reuse_prep = on ? 1 : 0;
+    return LMEP_OK;
+}

@@ -67,6 +67,9 @@ struct StepParams {
     int64_t push_w;
     int64_t tile_lo, tile_hi;                   // persistent per-node kernels: tiles of this launch (hi = 0: all)
     int64_t tile_wrap;                          // ... > 0: tile indices >= tile_wrap continue at tile 0 (a range that wraps)
+    int pdl;                                    // ... launched as a programmatic dependent of the launch before it on the
+                                                // stream: 1 = only u_in is that launch's output (the rows may be fetched
+                                                // before it has finished), 2 = the rows may be too
     int64_t ext_off;                            // ... on a slab: u_in / rows start ext_off nodes before the owned ones
     double *nl0_out;
     double dt;

@@ -326,6 +326,9 @@ int run_steps(const StepCall &c)
         p.q_in = qsrc;
         p.q_out = qdst;
         p.nl0_out = (L == 0) ? c.nl0_out : nullptr;
+        // (unsharded) every launch after the first depends on the one before it only
+        // through u: its CTAs start as that one drains and prefetch their first rows
+        p.pdl = (tma_path && !sharded && L > 0) ? 1 : 0;
         if (sharded && tma_path) {
             // the slab's extended arrays: u from its left ghosts on, the padded row table
             p.u_in = c.halo->left;

@@ -71,6 +71,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 
+// programmatic dependent launch: let the next launch on the stream start its
+// prologue as SMs free up / wait until the launch before this one has completed
+// and its stores are visible (no-ops for a launch without the attribute)
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
 // staged range of tile `tile`: global nodes [base, base + len), fetched from
 // the even node `start` = base - o, cnt (even) nodes, wrapping at N
 struct TileRange {
@@ -138,20 +144,26 @@ __global__ void __launch_bounds__(NT, 1) lin_pernode_tma_kernel(const __grid_con
 
     // buffer b's origin: staged node l of a tile at Ub[b*UL + org + l] with
     // org - o even, so the bulk copy destination (org - o) is 16-byte aligned
-    auto issue = [&](int64_t tile, int b) {
+    // dep (first tile of a programmatic dependent launch): 1 = wait for the launch
+    // before this one between the row copies and the u copy, 2 = before both
+    auto issue = [&](int64_t tile, int b, int dep) {
         const TileRange r = tile_range(p, tile, K, eL, eR);
         const int org = eL + ((eL - r.o) & 1);
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         const uint32_t bytes = (uint32_t)r.cnt * 8u * (NS + 1);
+        if (dep == 2) griddep_wait();
         mbar_expect_tx(&bar, bytes);
 #pragma unroll 1
         for (int c = 0; c < NS; ++c)
             copy_wrapped(R + c * RS, p.wp + (int64_t)c * p.wld, p.N, r.start, r.cnt, &bar);
+        if (dep == 1) griddep_wait();
         copy_wrapped(Ub + b * UL + org - r.o, p.u_in, p.N, r.start, r.cnt, &bar);
     };
 
+    if (p.pdl) griddep_launch();
     int64_t tile = p.tile_lo + blockIdx.x;
-    if (tid == 0 && tile < ntiles) issue(tile, 0);
+    if (tid == 0 && tile < ntiles) issue(tile, 0, p.pdl);
+    if (p.pdl) griddep_wait();
     bool bad = false;
     for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
         const TileRange r = tile_range(p, tile, K, eL, eR);
@@ -169,7 +181,7 @@ __global__ void __launch_bounds__(NT, 1) lin_pernode_tma_kernel(const __grid_con
         }
         __syncthreads();                         // R free, previous tile's outputs stored
         const int64_t nxt = tile + gridDim.x;
-        if (tid == 0 && nxt < ntiles) issue(nxt, (it + 1) % 3);
+        if (tid == 0 && nxt < ntiles) issue(nxt, (it + 1) % 3, 0);
 
         double *U0 = Ub + bT * UL + org - eL, *U1 = Ub + bP * UL + org - eL;
         for (int s = 0; s < K; ++s) {
@@ -255,20 +267,24 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
     }
     __syncthreads();
 
-    auto issue = [&](int64_t tile) {
+    auto issue = [&](int64_t tile, int dep) {
         const TileRange r = tile_range(p, tile, K, eL, eR);
         const int org = eL + ((eL - r.o) & 1);
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         const uint32_t bytes = (uint32_t)r.cnt * 8u * (NS + 1);
+        if (dep == 2) griddep_wait();
         mbar_expect_tx(&bar, bytes);
 #pragma unroll 1
         for (int c = 0; c < NS; ++c)
             copy_wrapped(R + c * RS, p.wp + (int64_t)c * p.wld, p.N, r.start, r.cnt, &bar);
+        if (dep == 1) griddep_wait();
         copy_wrapped(Ub + org - r.o, p.u_in, p.N, r.start, r.cnt, &bar);
     };
 
+    if (p.pdl) griddep_launch();
     int64_t tile = p.tile_lo + blockIdx.x;
-    if (tid == 0 && tile < ntiles) issue(tile);
+    if (tid == 0 && tile < ntiles) issue(tile, p.pdl);
+    if (p.pdl) griddep_wait();
     bool bad = false;
     for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
         const TileRange r = tile_range(p, tile, K, eL, eR);
@@ -310,7 +326,7 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
 #ifdef LMEP_TMX_TIMING
         long long tq2 = clock64();
 #endif
-        if (tid == 0 && nxt < ntiles) issue(nxt);
+        if (tid == 0 && nxt < ntiles) issue(nxt, 0);
 #ifdef LMEP_TMX_TIMING
         long long tq3 = clock64();
 #endif
@@ -448,6 +464,25 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
     if (bad) *p.flag = 1;
 }
 
+// launch as a programmatic dependent of the launch before it on the stream
+// (programmatic stream serialization): the CTAs may start while that launch
+// drains and wait for it inside the kernel (griddepcontrol.wait)
+static void launch_dependent(void (*k)(StepParams), unsigned grid, unsigned threads, size_t shm,
+                             cudaStream_t st, const StepParams &p)
+{
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = shm;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, p);
+}
+
 // (n, row) pairs with both halo widths <= 6 that the register-resident kernel
 // is instantiated for: the centred stencils and the n = 7 one-sided ones
 template <bool EX, int NT, int MINB, int J = 6>
@@ -469,7 +504,8 @@ static int launch_tmx(const StepParams &p, unsigned grid, cudaStream_t st)
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
         mark_device(attr_done[p.n][p.row], dev);
     }
-    k<<<grid, NT, shm, st>>>(p);
+    if (p.pdl) launch_dependent(k, grid, NT, shm, st, p);
+    else k<<<grid, NT, shm, st>>>(p);
     return launch_status("lin_pernode_tmx_kernel");
 }
 
@@ -513,11 +549,13 @@ int launch_lin_pernode_tma(const StepParams &p, bool exact, cudaStream_t st)
         if (exact) {                                                                              \
             cudaFuncSetAttribute(lin_pernode_tma_kernel<NS_, J, NT, true>,                        \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);          \
-            lin_pernode_tma_kernel<NS_, J, NT, true><<<grid, NT, shm, st>>>(p);                   \
+            if (p.pdl) launch_dependent(lin_pernode_tma_kernel<NS_, J, NT, true>, grid, NT, shm, st, p); \
+            else lin_pernode_tma_kernel<NS_, J, NT, true><<<grid, NT, shm, st>>>(p);              \
         } else {                                                                                  \
             cudaFuncSetAttribute(lin_pernode_tma_kernel<NS_, J, NT, false>,                       \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);          \
-            lin_pernode_tma_kernel<NS_, J, NT, false><<<grid, NT, shm, st>>>(p);                  \
+            if (p.pdl) launch_dependent(lin_pernode_tma_kernel<NS_, J, NT, false>, grid, NT, shm, st, p); \
+            else lin_pernode_tma_kernel<NS_, J, NT, false><<<grid, NT, shm, st>>>(p);             \
         }                                                                                         \
         break;
     switch (p.n) {

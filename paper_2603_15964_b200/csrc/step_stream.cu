@@ -85,6 +85,9 @@ static int launch_level(lmep_lin_stream *s, int l, int64_t lo, int64_t hi, int64
     p.tile_lo = lo;
     p.tile_hi = hi;
     p.tile_wrap = wrap;
+    // level 1 follows the harvest of its rows; a deeper level follows the level before
+    // it (its rows landed long ago): a programmatic dependent that prefetches them
+    p.pdl = l > 0 ? 1 : 0;
     ++s->launches;
     return launch_lin_pernode_tma(p, s->exact, st);
 }

@@ -482,8 +482,9 @@ def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
     the [N, K] coefficient table goes up in growing slices (_pipeline_bounds;
     multiples of 1024 items, so the block-balanced kernel's superblocks and
     their representative balancing are those of a resident harvest; the
-    constant-table kernel balances each slice's first item, which on C5's
-    fields gives the resident exponents, else rows equal within rounding) on the copy
+    constant-table kernel keeps the first slice's prepared tables for the later
+    slices, lmep_harvest_reuse_prep, so its rows equal a one-launch harvest's bit
+    for bit whatever the slicing) on the copy
     stream, and the harvest of slice i (lmep_harvest_chunk into the shared SoA
     output) overlaps the upload of slice i+1.  Every slice is queued before
     tables_fn() builds the derivative tables, so PCIe starts at once."""
@@ -521,31 +522,42 @@ def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
     def harvest_slice(i, ev):
         a, b = bounds[i]
         cur.wait_event(ev)
+        # later slices keep the first slice's prepared tables (lmep_harvest_reuse_prep):
+        # the rows are those of a one-launch harvest whatever the slicing
+        nat.lib().lmep_harvest_reuse_prep(1 if i > 0 else 0)
         _ops.harvest(n, s, delta_t, b - a, tables=tables, coef=dc[a:b], coef_stride=K,
                      c0=None if dr is None else dr[a:b], c0_stride=0 if dr is None else 1,
                      row_default=row, frozen_default=0, layout=1, into=out, item0=a)
         if ls is not None:
             ls.ready(b)
 
-    if ls is None:
-        # every slice is queued before the tables are built, so PCIe starts at once
-        landed = [upload(i) for i in range(len(bounds))]
-        _ops.issue_deferred(cp)              # e.g. run()'s initial state, behind the slices
-        tables = tables_fn()                 # overlaps the first slices' transfer
-        for i, ev in enumerate(landed):
-            harvest_slice(i, ev)
-    else:
-        # streamed run: the host's own enqueue time is on the critical path until
-        # the first harvest is queued, so the uploads stay just two slices ahead of
-        # the harvests (PCIe never idles: a slice takes longer to land than the
-        # host needs to queue a harvest and its step launches)
-        landed = [upload(i) for i in range(min(2, len(bounds)))]
-        tables = tables_fn()
-        for i in range(len(bounds)):
-            harvest_slice(i, landed[i])
-            if i + 2 < len(bounds):
-                landed.append(upload(i + 2))
-        ls.uploaded(cp, landed[-1])
+    def _run_slices():
+        nonlocal tables
+        if ls is None:
+            # every slice is queued before the tables are built, so PCIe starts at once
+            landed = [upload(i) for i in range(len(bounds))]
+            _ops.issue_deferred(cp)              # e.g. run()'s initial state, behind the slices
+            tables = tables_fn()                 # overlaps the first slices' transfer
+            for i, ev in enumerate(landed):
+                harvest_slice(i, ev)
+        else:
+            # streamed run: the host's own enqueue time is on the critical path until
+            # the first harvest is queued, so the uploads stay just two slices ahead of
+            # the harvests (PCIe never idles: a slice takes longer to land than the
+            # host needs to queue a harvest and its step launches)
+            landed = [upload(i) for i in range(min(2, len(bounds)))]
+            tables = tables_fn()
+            for i in range(len(bounds)):
+                harvest_slice(i, landed[i])
+                if i + 2 < len(bounds):
+                    landed.append(upload(i + 2))
+            ls.uploaded(cp, landed[-1])
+
+    tables = None
+    try:
+        _run_slices()
+    finally:
+        nat.lib().lmep_harvest_reuse_prep(0)
     dc.record_stream(cp)
     if dr is not None:
         dr.record_stream(cp)

@@ -155,3 +155,28 @@ def test_run_streamed_matches_phases(lx, src):
             assert np.array_equal(a.snapshots, b.snapshots), (exact, stride)
             assert np.array_equal(a.times, b.times)
             assert a.harvest_ns > 0 and a.step_ns > 0
+
+
+def test_pipelined_harvest_any_slicing_bitwise(lx, monkeypatch):
+    """The constant-table harvest keeps the first slice's prepared tables for the
+    later slices (lmep_harvest_reuse_prep), so host coefficients harvested slice
+    by slice give the rows of the one-launch harvest bit for bit whatever the
+    slice boundaries -- also on fields whose slices would balance differently
+    on their own first items (a coefficient jump of 1e4 across the grid)."""
+    from paper_2603_15964_b200 import configs, harvest as hv
+    N = 1 << 19
+    w5 = configs.c5(N=N, steps=1)
+    g = lx.make_periodic_grid(N, 0.0, 1.0)
+    st = lx.select_stencils(g, w5.n, lx.StencilPolicy.CENTERED)
+    x = np.asarray(g.nodes)
+    nu = np.where(x < 0.37, 1e-4, 1.0) * (1.0 + 0.3 * np.sin(2 * np.pi * x))
+    c = 0.5 + 0.4 * np.cos(2 * np.pi * x)
+    dt = 0.4 * w5.h ** 2 / nu.max()
+    coef = np.stack([-c, nu], 1)
+    ref = hv.harvest_compact(g, st, lx.VariableCoefficientSpec((1, 2), torch.as_tensor(coef, device="cuda")),
+                             dt, 1)
+    for bounds in ([(0, N)], [(0, 8192), (8192, N)],
+                   [(0, 150 * 1024), (150 * 1024, 333 * 1024), (333 * 1024, N)]):
+        monkeypatch.setattr(hv, "_pipeline_bounds", lambda n, b=bounds: list(b))
+        got = hv.harvest_compact(g, st, lx.VariableCoefficientSpec((1, 2), coef), dt, 1)
+        assert torch.equal(got.pernode, ref.pernode), bounds

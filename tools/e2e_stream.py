@@ -42,8 +42,8 @@ def main():
 
     m, lo, ref = timed(False)
     print(f"phases:   median {m:.3f} ms  min {lo:.3f}  harvest_ns {ref.harvest_ns} step_ns {ref.step_ns}")
-    plans = [(0.5, 2.5, 5, 6, 6), (1, 3, 5, 5, 5), (1, 4, 7, 7), (0.5, 1.5, 4, 6, 6),
-             (2, 6, 8), (1, 3, 6, 8), (0.5, 2.5, 7, 8), (1, 5, 8, 6)]
+    plans = [(1, 3, 6, 8), (1, 3, 5, 6, 5), (1, 2, 4, 6, 6), (2, 5, 7, 6), (1, 4, 7, 7), (2, 6, 8),
+             (1, 3, 6, 6, 4), (1.5, 4.5, 7, 6), (1, 3, 5, 5, 5)]
     for wv in plans:
         _ops.LinearStream.WAVES = wv
         m, lo, r = timed(True)
