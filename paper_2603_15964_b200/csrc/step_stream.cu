@@ -215,6 +215,19 @@ extern "C" int lmep_lin_stream_advance(lmep_lin_stream *s, int64_t nodes_ready, 
         if (s->jhi[l] < 0) {
             rc = launch_level(s, l, 0, nt, 0, st);
             if (rc == LMEP_OK && l == last) rc = copy_out(s, 0, N, st);
+        } else if (l == last && s->host_out) {
+            // the last launch of all: in up to three tile ranges, each copied to the
+            // host while the next one runs (only the last range's copy is exposed)
+            const int64_t lo = s->jhi[l], hi = nt + s->jlo[l];
+            const int64_t waves = (hi - lo) / std::max(1, device_sm_count());
+            const int parts = (int)std::max<int64_t>(1, std::min<int64_t>(3, waves));
+            for (int q = 0; q < parts && rc == LMEP_OK; ++q) {
+                const int64_t a = lo + (hi - lo) * q / parts, b = lo + (hi - lo) * (q + 1) / parts;
+                if (b <= a) continue;
+                rc = launch_level(s, l, a, b, nt, st);
+                if (rc == LMEP_OK && a < nt) rc = copy_out(s, a * T, std::min(b, nt) * T < N ? std::min(b, nt) * T : N, st);
+                if (rc == LMEP_OK && b > nt) rc = copy_out(s, std::max<int64_t>(a - nt, 0) * T, (b - nt) * T, st);
+            }
         } else {
             if (nt + s->jlo[l] > s->jhi[l]) rc = launch_level(s, l, s->jhi[l], nt + s->jlo[l], nt, st);
             if (rc == LMEP_OK && l == last) {
