@@ -272,7 +272,22 @@ def _coords0_host(grid: Grid, sset: StencilSet, plan) -> np.ndarray:
     return _ops.to_host(plan.coords[0])
 
 
+_PLANS: dict = {}
+
+
 def _plan(grid: Grid, sset: StencilSet, frozen_nodes=(), force_pernode=False) -> _Plan:
+    N, n, row = sset.N, sset.n, sset.row
+    if grid.periodic and len(frozen_nodes) == 0:
+        # one window geometry for the whole ring: the plan depends on (n, row, h) only
+        key = (bool(force_pernode), n, row, float(grid.spacing), torch.cuda.current_device())
+        hit = _PLANS.get(key)
+        if hit is None:
+            hit = _PLANS[key] = _plan_uncached(grid, sset, (), force_pernode)
+        return hit
+    return _plan_uncached(grid, sset, frozen_nodes, force_pernode)
+
+
+def _plan_uncached(grid: Grid, sset: StencilSet, frozen_nodes=(), force_pernode=False) -> _Plan:
     N, n, row = sset.N, sset.n, sset.row
     frozen = sorted({int(i) for i in frozen_nodes})
     if grid.periodic and not frozen and not force_pernode:
