@@ -446,12 +446,22 @@ __global__ void __launch_bounds__(NT, MINB) lin_pernode_tmx_kernel(const __grid_
 #ifdef LMEP_TMX_TIMING
         long long tq4 = clock64();
 #endif
+        // (pairs of nodes as one 16-byte store where the pair is aligned and owned: a
+        // thread's J values are contiguous in u_out, lanes 8 J bytes apart, so every
+        // store instruction touches 32 sectors whatever its width)
+        {
+            double *uo = p.u_out + (r.t0 - p.ext_off) + (l0 - K * eL);
+            const bool vec = (((uintptr_t)uo) & 15) == 0;
 #pragma unroll
-        for (int j = 0; j < J; ++j) {
-            const int64_t i = r.t0 + (int64_t)(l0 + j - K * eL);
-            if (i >= r.t0 && i < r.t1) {
-                p.u_out[i - p.ext_off] = x[j];
-                bad |= !isfinite(x[j]);
+            for (int j = 0; j < J; j += 2) {
+                const int64_t i = r.t0 + (int64_t)(l0 + j - K * eL);
+                if (vec && i >= r.t0 && i + 1 < r.t1) {
+                    *reinterpret_cast<double2 *>(uo + j) = make_double2(x[j], x[j + 1]);
+                    bad |= !isfinite(x[j]) | !isfinite(x[j + 1]);
+                } else {
+                    if (i >= r.t0 && i < r.t1) { uo[j] = x[j]; bad |= !isfinite(x[j]); }
+                    if (i + 1 >= r.t0 && i + 1 < r.t1) { uo[j + 1] = x[j + 1]; bad |= !isfinite(x[j + 1]); }
+                }
             }
         }
 #ifdef LMEP_TMX_TIMING
