@@ -180,3 +180,22 @@ def test_pipelined_harvest_any_slicing_bitwise(lx, monkeypatch):
         monkeypatch.setattr(hv, "_pipeline_bounds", lambda n, b=bounds: list(b))
         got = hv.harvest_compact(g, st, lx.VariableCoefficientSpec((1, 2), coef), dt, 1)
         assert torch.equal(got.pernode, ref.pernode), bounds
+
+
+def test_run_streamed_fallbacks(lx):
+    """run(stream=True) where the pipeline does not apply -- a one-step first chunk
+    (the library declines the plan) and a grid too small for a pipelined harvest
+    (the initial state goes up in one copy) -- gives the phase-by-phase result."""
+    from paper_2603_15964_b200 import configs
+    sch = lx.SchemeConfig("linear")
+    for N, steps, stride in ((1 << 19, 5, 1), (1 << 14, 30, 10)):
+        w5 = configs.c5(N=N, steps=1)
+        c, nu = w5.coef
+        g = lx.make_periodic_grid(N, 0.0, 1.0)
+        st = lx.select_stencils(g, w5.n, lx.StencilPolicy.CENTERED)
+        prob = lx.SemiLinearProblem(lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1)), None,
+                                    np.array(w5.u0), lx.Boundary.periodic(), "none")
+        a = lx.run(g, st, prob, sch, w5.delta_t, steps * w5.delta_t, stride * w5.delta_t)
+        b = lx.run(g, st, prob, sch, w5.delta_t, steps * w5.delta_t, stride * w5.delta_t, stream=False)
+        assert a.snapshots.shape == b.snapshots.shape == (1 + steps // stride, N)
+        assert np.array_equal(a.snapshots, b.snapshots), (N, steps)
