@@ -49,7 +49,7 @@ int device_sm_count();                // SM count of the current device (cached 
 struct DeviceSettings {
     std::atomic<int> harvest_method{0};   // 0 auto (expm-multiply for d <= 16), 1 Pade
     std::atomic<int> mv_lanes{0};         // block / per-item lanes override (0 = heuristic)
-    std::atomic<int> mvc{1};              // constant-table kernel when eligible
+    std::atomic<int> mvc{1};              // constant-table kernel when eligible (2: without its polynomial kernel)
     std::atomic<int> ring_cluster{1};     // linear ring mode on a thread-block cluster
     std::atomic<int> pernode_kernel{2};   // TMA per-node steps: 1 registers, 0 window, 2 auto
     std::atomic<int> etd2_persistent{1};  // ETD2 on mid-size periodic grids: one cooperative launch

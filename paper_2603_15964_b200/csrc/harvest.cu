@@ -944,12 +944,13 @@ extern "C" int lmep_set_harvest_method(int method)
     // 8 / 2 / 4 lanes per item (tuning); 9 auto without the constant-table
     // kernel.  (2 / 3 named the retired first-generation kernel.)  Applies to
     // the calling thread's current device.
-    if (method < 0 || method > 9 || method == 2 || method == 3) return LMEP_INVALID_CONFIG;
+    // 10 = auto with the constant-table kernel's Taylor series only (no polynomial kernel)
+    if (method < 0 || method > 10 || method == 2 || method == 3) return LMEP_INVALID_CONFIG;
     lmep::DeviceSettings &ds = lmep::device_settings();
-    ds.mvc.store(method == 0 ? 1 : 0);
+    ds.mvc.store(method == 0 ? 1 : (method == 10 ? 2 : 0));
     ds.mv_lanes.store((method == 4 || method == 6) ? 8 : (method == 7 ? 2 : (method == 8 ? 4 : 0)));
     if (method == 4) method = 5;
-    if (method >= 6) method = 0;   // 6..9
+    if (method >= 6) method = 0;   // 6..10
     ds.harvest_method.store(method);
     return LMEP_OK;
 }

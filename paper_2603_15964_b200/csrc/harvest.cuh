@@ -33,6 +33,10 @@ struct HarvestParams {
     // optional (w_lin, raw dt/2 phi_1) rows at delta_t / 2, same layout as out
     // with s = 2 (lmep_harvest_ex half_out); only the per-item kernel emits them
     double *half_out;
+    // constant-table kernels: work list between the polynomial kernel and the Taylor
+    // kernel behind it (device: [0] = number of 128-item blocks handed back, then
+    // their indices); null = every item
+    int32_t *pending;
 };
 
 __device__ __forceinline__ int64_t coef_node(const HarvestParams &P, int64_t b, int row, int i)

@@ -34,6 +34,7 @@
 // block kernel are identical over the grid (C5), so nothing is lost.
 #include <math.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "harvest.cuh"
@@ -46,6 +47,8 @@ namespace {
 constexpr int MVC_D = 16;
 constexpr int MVC_NT = 2;
 constexpr double MVC_THETA = 4.0;
+constexpr int MVC_PN = 13;             // polynomial kernel: n <= 13
+constexpr int MVC_PV = 14;             // ... words of up to 13 factors (the last anti-diagonal is the check)
 
 struct MvcConst {
     double tt[MVC_NT][MVC_D][MVC_D];   // tt[t][j][c] = T_t[c][j] 2^(e_c - e_j)  (row j of T'^T)
@@ -65,6 +68,13 @@ struct MvcConst {
     double ax[4];
     double rsa[MVC_D];
     int e[MVC_D];
+    // polynomial kernel (s = 1, two tables): exp(a A_0 + b A_1) e_r = sum a^p b^q V_pq with
+    // V_pq = (A_0 V_(p-1)q + A_1 V_p(q-1)) / (p + q), A_t = dt c_t(item 0) T'_t^T
+    alignas(16) double pv[MVC_PV][MVC_PV][MVC_PN + 1]; // V_pq (p + q < MVC_PV; 16-byte rows), zero where numerically nilpotent
+    double psc[MVC_PN + 1];            // 2^(e_j - e_row): back from the balanced coordinates
+    float lvn[MVC_PV][MVC_PV];         // log2 |V_pq|_inf (-1e30: zero)
+    double cinv[MVC_NT];               // 1 / c_t(item 0): the kernel's a, b are c_t(item) cinv[t]
+    int poly_ok;                       // the series terminates inside the table (p + q < MVC_PV)
 };
 
 __constant__ MvcConst c_mvc;
@@ -209,6 +219,186 @@ __global__ void mvc_prep_kernel(const HarvestParams P, MvcConst *out)
     }
 }
 
+// ---- tables of the polynomial kernel (one CTA of MVC_PV warps, behind the
+// prep kernel: reads its balanced tables from `out`) -------------------------
+// For derivative tables the local operators are nilpotent (a word of more
+// than n - 1 derivative matrices annihilates the window's interpolant), so
+// exp(dt L_b)^T e_r is a POLYNOMIAL in the item's two coefficients: the
+// vectors V_pq are shared by every item.  Warp p computes V_p(k-p) of
+// anti-diagonal k from anti-diagonal k - 1.  A computed V_pq that is below the
+// rounding error of its own recurrence is exactly zero in exact arithmetic and
+// is stored as zero; the kernel is used when the series terminates inside the
+// table (poly_ok).
+__global__ void __launch_bounds__(32 * MVC_PV) mvc_poly_prep_kernel(const HarvestParams P, MvcConst *out)
+{
+    __shared__ double As[MVC_NT][MVC_PN][MVC_PN + 1];
+    __shared__ double Vs[MVC_PV][MVC_PV][MVC_PN + 1];
+    __shared__ double vinf[MVC_PV][MVC_PV];
+    __shared__ double an[MVC_NT];
+    __shared__ int bad;
+    const int j = threadIdx.x & 31, wid = threadIdx.x >> 5, n = P.n, row = P.row_default;
+    if (threadIdx.x == 0) bad = 0;
+    if (wid < MVC_NT) {
+        const int t = wid;
+        double cn = P.coef[t];
+        if (!(fabs(cn) > 0.0) || !isfinite(cn)) cn = 1.0;
+        if (j == 0) out->cinv[t] = 1.0 / cn;
+        double sum = 0.0;
+        if (j < n)
+            for (int c = 0; c < n; ++c) {
+                const double a = (P.delta_t * cn) * out->tt[t][j][c];
+                As[t][j][c] = a;
+                sum += fabs(a);
+            }
+        for (int o = 16; o > 0; o >>= 1) sum = fmax(sum, __shfl_xor_sync(FULL, sum, o));
+        if (j == 0) an[t] = sum;
+    }
+    for (int i = threadIdx.x; i < MVC_PV * MVC_PV * (MVC_PN + 1); i += blockDim.x) (&Vs[0][0][0])[i] = 0.0;
+    for (int i = threadIdx.x; i < MVC_PV * MVC_PV; i += blockDim.x) (&vinf[0][0])[i] = 0.0;
+    __syncthreads();
+    if (threadIdx.x == 0) { Vs[0][0][row] = 1.0; vinf[0][0] = 1.0; }
+    __syncthreads();
+#pragma unroll 1
+    for (int k = 1; k < MVC_PV; ++k) {
+        const int p = wid, q = k - wid;
+        if (q >= 0) {
+            double v = 0.0, ref = 0.0;
+            if (j < n) {
+                if (p > 0)
+                    for (int c = 0; c < n; ++c) v = fma(As[0][j][c], Vs[p - 1][q][c], v);
+                if (q > 0)
+                    for (int c = 0; c < n; ++c) v = fma(As[1][j][c], Vs[p][q - 1][c], v);
+                v /= (double)k;
+            }
+            if (p > 0) ref += an[0] * vinf[p - 1][q];
+            if (q > 0) ref += an[1] * vinf[p][q - 1];
+            ref /= (double)k;
+            double vi = j < n ? fabs(v) : 0.0;
+            for (int o = 16; o > 0; o >>= 1) {
+                const double w2 = __shfl_xor_sync(FULL, vi, o);
+                vi = (w2 > vi || w2 != w2) ? w2 : vi;
+            }
+            if (!isfinite(vi) && j == 0) bad = 1;
+            if (!(vi > 0x1p-46 * ref)) { v = 0.0; vi = 0.0; }        // numerically nilpotent
+            if (j < n) Vs[p][q][j] = v;
+            if (j == 0) vinf[p][q] = vi;
+        }
+        __syncthreads();
+    }
+    // the series must end inside the table: the last anti-diagonal is all zero
+    bool pok = P.s == 1 && P.nterms == 2 && P.c0 == nullptr && n <= MVC_PN && !bad;
+    for (int p = 0; p < MVC_PV; ++p)
+        if (vinf[p][MVC_PV - 1 - p] != 0.0) pok = false;
+    for (int i = threadIdx.x; i < MVC_PV * MVC_PV; i += blockDim.x) {
+        const int p = i / MVC_PV, q = i % MVC_PV;
+        const bool in = p + q < MVC_PV;
+        const double vi = in ? vinf[p][q] : 0.0;
+        out->lvn[p][q] = (vi > 0.0 && isfinite(vi)) ? (float)log2(vi) : -1e30f;
+        for (int c = 0; c <= MVC_PN; ++c) out->pv[p][q][c] = (in && pok && c < MVC_PN) ? Vs[p][q][c] : 0.0;
+    }
+    if (threadIdx.x <= MVC_PN)
+        out->psc[threadIdx.x] = threadIdx.x < n ? mv_pow2(out->e[threadIdx.x] - out->e[row]) : 0.0;
+    if (threadIdx.x == 0) out->poly_ok = pok ? 1 : 0;
+}
+
+// Polynomial kernel (w_lin of two-table operators, harvest.py:97-121 per node):
+// one item per lane evaluates  w = sum_pq a^p b^q V_pq  (a, b its two
+// coefficients over item 0's) as nested Horner sums -- 13 independent chains,
+// the table entries as constant-bank operands -- over the columns a warp-wide
+// magnitude test keeps: at n = 13 with a diffusion-dominated step (config 5)
+// 19 of the 91 columns.  A warp whose largest term exceeds 2^6 (cancellation)
+// or whose coefficients are not finite hands its items to the Taylor kernel
+// (status LMEP_PENDING), as does every item when the series does not
+// terminate inside the table.
+template <int N>
+__global__ void __launch_bounds__(128) harvest_poly_kernel(const HarvestParams P)
+{
+    // column selection once per CTA, from the CTA-wide coefficient magnitudes
+    __shared__ unsigned smax[2];
+    __shared__ int sq[MVC_PV];             // sq[p]: highest significant q of row p (-1: none)
+    __shared__ int sflag;                  // 1: hand the CTA's items to the Taylor kernel
+    int64_t braw = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = braw < P.B;
+    const int64_t b = live ? braw : P.B - 1;
+    if (threadIdx.x < 2) smax[threadIdx.x] = 0u;
+    if (threadIdx.x < MVC_PV) sq[threadIdx.x] = -1;
+    if (threadIdx.x == 0) sflag = c_mvc.poly_ok ? 0 : 1;
+    __syncthreads();
+    const double a = P.coef[b * P.coef_stride] * c_mvc.cinv[0];
+    const double be = P.coef[b * P.coef_stride + 1] * c_mvc.cinv[1];
+    // (upper bounds from the high words; NaN / Inf sort last)
+    const unsigned ha = __reduce_max_sync(FULL, mv_hiabs(a)), hb = __reduce_max_sync(FULL, mv_hiabs(be));
+    if ((threadIdx.x & 31) == 0) { atomicMax(&smax[0], ha); atomicMax(&smax[1], hb); }
+    __syncthreads();
+    if (threadIdx.x < MVC_PV - 1) {
+        const float xa = (float)__hiloint2double((int)smax[0], -1), xb = (float)__hiloint2double((int)smax[1], -1);
+        const float la = xa > 0.f ? log2f(xa) : -1e30f, lb = xb > 0.f ? log2f(xb) : -1e30f;
+        const int p = threadIdx.x;
+        int qtop = -1;
+        bool big = false;
+        for (int q = 0; p + q < MVC_PV - 1; ++q) {
+            const float lv = c_mvc.lvn[p][q];
+            if (lv > -1e29f) {
+                const float t = (p ? p * la : 0.f) + (q ? q * lb : 0.f) + lv;
+                if (t > -60.f) qtop = q;
+                if (!(t <= 6.f)) big = true;
+            }
+        }
+        sq[p] = qtop;
+        if (big) sflag = 1;
+    }
+    __syncthreads();
+    if (sflag) {
+        // the CTA's items go to the Taylor kernel: one entry in its work list
+        if (threadIdx.x == 0) P.pending[1 + atomicAdd(P.pending, 1)] = (int)blockIdx.x;
+        return;
+    }
+    // (through a ballot / shuffles so that the compiler sees warp-uniform loop
+    // bounds and feeds the table entries as uniform-register operands)
+    const int myq = (threadIdx.x & 31) < MVC_PV ? sq[threadIdx.x & 31] : -1;
+    const unsigned has = __ballot_sync(FULL, myq >= 0);
+    const int Pw = has ? 31 - __clz((int)has) : 0;
+    double w[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) w[j] = 0.0;
+    int cols = 0;
+#pragma unroll 1
+    for (int p = Pw; p >= 0; --p) {
+        const int qt = __shfl_sync(FULL, myq, p);
+        // s = sum_q be^q V_pq by Horner from the top; columns above qt are skipped
+        // (uniform branches), the table entries are constant-bank operands at
+        // compile-time offsets from row p
+        double s[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) s[j] = 0.0;
+        const double (*row_p)[MVC_PN + 1] = c_mvc.pv[p];
+#pragma unroll
+        for (int q = MVC_PV - 2; q >= 0; --q) {
+            if (q <= qt) {
+#pragma unroll
+                for (int j = 0; j < N; ++j) s[j] = fma(s[j], be, row_p[q][j]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < N; ++j) w[j] = fma(w[j], a, s[j]);
+        cols += qt + 1;
+    }
+    if (!live) return;
+    const int n = P.n;
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        const double o = w[j] * c_mvc.psc[j];
+        bad |= !isfinite(o);
+        if (j < n) {
+            if (P.layout == 0) P.out[b * n + j] = o;
+            else P.out[(int64_t)j * P.out_ld + b] = o;
+        }
+    }
+    P.status[b] = bad ? LMEP_NONFINITE : LMEP_OK;
+    if (P.ms) P.ms[b] = cols;            // scaling field 0: a polynomial item, `cols` Horner columns
+}
+
 // 3 CTAs per SM (<= 168 registers): 12 warps hide the DFMA and constant-load
 // latency better than 8 warps at the unbounded 174 (measured 1.01 vs 1.09 ms).
 // N = n (the operator block), PA = s - 1 augmentation columns (phi rows).
@@ -216,7 +406,13 @@ template <int N, int NT, bool C0, int PA>
 __global__ void __launch_bounds__(128, 3) harvest_mvc_kernel(const HarvestParams P)
 {
     constexpr int D = N + PA;
-    const int64_t braw = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t braw = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    // (behind the polynomial kernel: a small grid walks the list of 128-item
+    // blocks that kernel handed back, pending[0] entries from pending[1] on)
+    const int nwork = P.pending ? P.pending[0] : 1;
+#pragma unroll 1
+    for (int work = blockIdx.x; work < (P.pending ? nwork : (int)blockIdx.x + 1); work += gridDim.x) {
+    if (P.pending) braw = (int64_t)P.pending[1 + work] * blockDim.x + threadIdx.x;
     const bool live = braw < P.B;
     const int64_t b = live ? braw : P.B - 1;
     const int row = P.row_default;
@@ -396,10 +592,12 @@ __global__ void __launch_bounds__(128, 3) harvest_mvc_kernel(const HarvestParams
             }
         }
     }
-    if (!live) return;
-    if (bad) status = LMEP_NONFINITE;
-    if (P.status) P.status[b] = status;
-    if (P.ms) P.ms[b] = nmv | (min(s, 255) << 24);
+    if (live) {
+        if (bad) status = LMEP_NONFINITE;
+        if (P.status) P.status[b] = status;
+        if (P.ms) P.ms[b] = nmv | (min(s, 255) << 24);
+    }
+    }
 }
 
 // Per-device state: the prep kernel's output block and the event of the
@@ -420,6 +618,8 @@ struct MvcDevice {
     cudaEvent_t done = nullptr;
     MvcKey key;                          // what the device's constant block was prepared for
     bool valid = false;
+    int32_t *pending = nullptr;          // work list between the polynomial and the Taylor kernel
+    int64_t pending_cap = 0;
 };
 // lmep_harvest_reuse_prep: the calling thread's next constant-table harvests are
 // slices of one harvest and keep the first slice's prepared block
@@ -482,22 +682,59 @@ int launch_harvest_mvc(const HarvestParams &P, cudaStream_t st)
     MvcKey key;
     key.tables = P.tables; key.dt = P.delta_t; key.n = P.n; key.s = P.s; key.nterms = P.nterms;
     key.row = P.row_default; key.c0 = P.c0 != nullptr;
+    // w_lin of two-table operators: the polynomial kernel first, the Taylor kernel
+    // behind it on whatever it handed back
+    const bool poly = P.s == 1 && P.nterms == 2 && P.c0 == nullptr && P.status != nullptr &&
+                      P.n <= MVC_PN && device_settings().mvc.load() == 1;
+    key.c0 |= poly ? 2 : 0;              // (a block prepared without the polynomial tables is not reused for it)
     // a later slice of the same harvest (same tables, step and shape; the block in
     // constant memory is still the one prepared for its first slice): the balancing
     // of that first slice's item serves the whole table, as in a one-launch harvest
     const bool reuse = t_reuse_prep && D.valid && key == D.key;
     if (!reuse) {
         mvc_prep_kernel<<<1, 32, 0, st>>>(P, D.scratch);
+        if (poly) mvc_poly_prep_kernel<<<1, 32 * MVC_PV, 0, st>>>(P, D.scratch);
         e = cudaMemcpyToSymbolAsync(c_mvc, D.scratch, sizeof(MvcConst), 0, cudaMemcpyDeviceToDevice, st);
         if (e != cudaSuccess) { set_last_error("cudaMemcpyToSymbolAsync", e); return LMEP_CUDA_ERROR; }
         D.key = key;
         D.valid = true;
     }
-    switch (P.n) {
-    case 7: launch_mvc_d<7>(P, st); break;
-    case 9: launch_mvc_d<9>(P, st); break;
-    case 11: launch_mvc_d<11>(P, st); break;
-    default: launch_mvc_d<13>(P, st); break;
+    HarvestParams Q = P;
+    if (poly) {
+        const unsigned blocks = (unsigned)((P.B + 127) / 128);
+        // work list of the blocks the polynomial kernel hands back (grown on demand)
+        if (D.pending_cap < (int64_t)blocks + 1) {
+            if (D.pending) { cudaStreamSynchronize(st); cudaFree(D.pending); }
+            D.pending_cap = std::max<int64_t>((int64_t)blocks + 1, 1 << 16);
+            if (cudaMalloc((void **)&D.pending, D.pending_cap * sizeof(int32_t)) != cudaSuccess) {
+                D.pending = nullptr; D.pending_cap = 0;
+                set_last_error("harvest_mvc work list", cudaGetLastError());
+                return LMEP_CUDA_ERROR;
+            }
+        }
+        cudaMemsetAsync(D.pending, 0, sizeof(int32_t), st);
+        Q.pending = D.pending;
+        switch (P.n) {
+        case 7: harvest_poly_kernel<7><<<blocks, 128, 0, st>>>(Q); break;
+        case 9: harvest_poly_kernel<9><<<blocks, 128, 0, st>>>(Q); break;
+        case 11: harvest_poly_kernel<11><<<blocks, 128, 0, st>>>(Q); break;
+        default: harvest_poly_kernel<13><<<blocks, 128, 0, st>>>(Q); break;
+        }
+        // the Taylor kernel on what is left: a grid of at most six CTAs per SM
+        const unsigned g = std::min<unsigned>(blocks, 6u * (unsigned)device_sm_count());
+        switch (Q.n) {
+        case 7: harvest_mvc_kernel<7, 2, false, 0><<<g, 128, 0, st>>>(Q); break;
+        case 9: harvest_mvc_kernel<9, 2, false, 0><<<g, 128, 0, st>>>(Q); break;
+        case 11: harvest_mvc_kernel<11, 2, false, 0><<<g, 128, 0, st>>>(Q); break;
+        default: harvest_mvc_kernel<13, 2, false, 0><<<g, 128, 0, st>>>(Q); break;
+        }
+    } else {
+        switch (Q.n) {
+        case 7: launch_mvc_d<7>(Q, st); break;
+        case 9: launch_mvc_d<9>(Q, st); break;
+        case 11: launch_mvc_d<11>(Q, st); break;
+        default: launch_mvc_d<13>(Q, st); break;
+        }
     }
     cudaEventRecord(D.done, st);
     return launch_status("harvest_mvc_kernel");
