@@ -284,12 +284,15 @@ class C5:
                         node_range=(self.off, self.nloc))
         return self.torch.cat(stats["ms"]).cpu().numpy()
 
-    def harvest_launch_ms(self, reps=11):
-        """The harvest launch alone (lmep_harvest: prep + constant copy + kernel on
-        the current stream): median over `reps` back-to-back launches, each
-        between its own CUDA events, on resident tables and coefficients (the
-        roofline of the kernel itself)."""
-        from paper_2603_15964_b200 import _ops
+    def harvest_launch_ms(self, reps=11, reuse_prep=False):
+        """The harvest launch alone (lmep_harvest: prep kernels + constant copy +
+        polynomial kernel + the Taylor kernel on what that handed back, on the
+        current stream): median over `reps` back-to-back launches, each between
+        its own CUDA events, on resident tables and coefficients.  reuse_prep:
+        the launches keep the warm-up's prepared tables (lmep_harvest_reuse_prep,
+        what the later slices of a pipelined harvest do), which leaves the item
+        kernels alone between the events (the roofline of the kernel itself)."""
+        from paper_2603_15964_b200 import _native as nat, _ops
         from paper_2603_15964_b200.harvest import _plan
         torch = self.torch
         plan = _plan(self.grid, self.sset, (), force_pernode=True)
@@ -305,10 +308,14 @@ class C5:
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
               for _ in range(reps)]
         torch.cuda.synchronize()
-        for a, b in ev:                      # back to back, one event pair per launch
-            a.record()
-            h = once()
-            b.record()
+        nat.lib().lmep_harvest_reuse_prep(1 if reuse_prep else 0)
+        try:
+            for a, b in ev:                  # back to back, one event pair per launch
+                a.record()
+                h = once()
+                b.record()
+        finally:
+            nat.lib().lmep_harvest_reuse_prep(0)
         torch.cuda.synchronize()
         if int(h.status.abs().max().item()) != 0:
             raise RuntimeError("harvest launch failed")
@@ -766,10 +773,18 @@ def main():
     achieved = step_bytes / (per_launch_ms * 1e-3) / 1e9
     ms_items = bench.harvest_ms_stats()
     d = w.n                                               # s = 1: d = n
-    flops = multiply_flops(d, ms_items)
+    # polynomial kernel (harvest_poly_kernel): an item's scaling field is 0 and its low
+    # bits count the columns it summed (2n + 1 flops each); Taylor items (blocks the
+    # polynomial kernel handed back) count products of 2 d^2 flops
+    poly_items = (ms_items >> 24) == 0
+    cols = (ms_items & 0xFFFFFF).astype(np.float64)
+    flops = float((cols[poly_items] * (2 * d + 1)).sum()) + multiply_flops(d, ms_items[~poly_items])
     fp64 = fp64_peak()
-    harvest_launch_ms = bench.harvest_launch_ms()
+    harvest_call_ms = bench.harvest_launch_ms()
+    harvest_launch_ms = bench.harvest_launch_ms(reuse_prep=True)
     harvest_tflops = flops / (harvest_launch_ms * 1e-3) / 1e12
+    harvest_bytes = bench.nloc * (16 + 8 * w.n + 4)      # 2 coefficients in, n weights + status out
+    harvest_gbs = harvest_bytes / (harvest_launch_ms * 1e-3) / 1e9
 
     onestep = time_c5_onestep() if world == 1 else None
     phi_ms, phi_items = bench.phi_harvest(4)
@@ -826,19 +841,26 @@ def main():
                          "launch_ms": per_launch_ms,
                          "peak_kind": f"{hbm_kind} (MEASURED_PEAKS.json hbm_gbs)",
                          "note": step_note},
-            "roofline_harvest": {"bound": "fp64",
-                         "kernel": "harvest_mvc_kernel<13,2,0> (per-node expm-multiply, one item per lane, "
-                                   "derivative tables as constant-bank DFMA operands)",
-                         "achieved": harvest_tflops, "peak": fp64, "unit": "TFLOP/s",
-                         "frac": harvest_tflops / fp64,
-                         "traffic": traffic("harvest_mvc_kernel<13,2,0>", "bytes_per_item", bench.nloc),
-                         "algorithmic_flops_per_launch": flops,
+            "roofline_harvest": {"bound": "hbm",
+                         "kernel": "harvest_poly_kernel<13,1> (per-node exp(dt L)^T e_r as a polynomial in the "
+                                   "node's two coefficients, one item per lane, shared table entries "
+                                   "by uniform constant loads; blocks it hands back go to "
+                                   "harvest_mvc_kernel<13,2,0,0>, none at config 5)",
+                         "achieved": harvest_gbs, "peak": hbm, "unit": "GB/s",
+                         "frac": harvest_gbs / hbm,
+                         "traffic": traffic("harvest_poly_kernel<13,1>", "bytes_per_item", bench.nloc),
+                         "algorithmic_bytes_per_launch": harvest_bytes,
                          "launch_ms": harvest_launch_ms,
-                         "flops_note": "algorithmic = Taylor products x 2d^2 (one assembled d x d "
-                                       "mat-vec per term); the kernel issues one product per "
-                                       "derivative table on folded symmetric halves (about "
-                                       "1.1x that) and keeps no per-item matrix",
-                         "peak_kind": "measured DFMA chains (tools/fp64_peak.cu), this run"},
+                         "call_ms": harvest_call_ms,
+                         "polynomial_items": int(poly_items.sum()),
+                         "columns_per_item": float(cols[poly_items].mean()) if poly_items.any() else None,
+                         "fp64_tflops": harvest_tflops, "fp64_frac": harvest_tflops / fp64,
+                         "bytes_note": "16 B of coefficients in, 8n + 4 B of weights and status out per "
+                                       "item; launch_ms = the item kernels alone (prepared tables kept, "
+                                       "as for the later slices of a pipelined harvest), call_ms = a "
+                                       "whole lmep_harvest call (two one-CTA table kernels, constant "
+                                       "copy, item kernels)",
+                         "peak_kind": f"{hbm_kind} (MEASURED_PEAKS.json hbm_gbs)"},
             # the blocked step kernel is no longer HBM-bound: it issues the reference's
             # unfused multiply + add per tap (2n flops per point-step, kernels.py:23-29),
             # so its ceiling is the FP64 pipe at one op per lane per issue = fp64 / 2

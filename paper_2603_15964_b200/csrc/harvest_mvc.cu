@@ -49,6 +49,11 @@ constexpr int MVC_NT = 2;
 constexpr double MVC_THETA = 4.0;
 constexpr int MVC_PN = 13;             // polynomial kernel: n <= 13
 constexpr int MVC_PV = 14;             // ... words of up to 13 factors (the last anti-diagonal is the check)
+#ifndef LMEP_POLY_IT
+#define LMEP_POLY_IT 1
+#endif
+constexpr int MVC_IT = LMEP_POLY_IT;    // items per thread of the polynomial kernel (1: 44 registers, 102 us at config 5; 2: 116 us)
+constexpr int MVC_PAIRS = (MVC_PV - 1) * MVC_PV / 2;   // pairs p + q < MVC_PV - 1
 
 struct MvcConst {
     double tt[MVC_NT][MVC_D][MVC_D];   // tt[t][j][c] = T_t[c][j] 2^(e_c - e_j)  (row j of T'^T)
@@ -71,8 +76,7 @@ struct MvcConst {
     // polynomial kernel (s = 1, two tables): exp(a A_0 + b A_1) e_r = sum a^p b^q V_pq with
     // V_pq = (A_0 V_(p-1)q + A_1 V_p(q-1)) / (p + q), A_t = dt c_t(item 0) T'_t^T
     alignas(16) double pv[MVC_PV][MVC_PV][MVC_PN + 1]; // V_pq (p + q < MVC_PV; 16-byte rows), zero where numerically nilpotent
-    double psc[MVC_PN + 1];            // 2^(e_j - e_row): back from the balanced coordinates
-    float lvn[MVC_PV][MVC_PV];         // log2 |V_pq|_inf (-1e30: zero)
+    alignas(16) float4 pl[MVC_PAIRS];  // (log2 |V_pq|_inf or -1e30: zero, p, q) of the pairs p + q < MVC_PV - 1 (the kernel reads the global copy)
     double cinv[MVC_NT];               // 1 / c_t(item 0): the kernel's a, b are c_t(item) cinv[t]
     int poly_ok;                       // the series terminates inside the table (p + q < MVC_PV)
 };
@@ -293,110 +297,139 @@ __global__ void __launch_bounds__(32 * MVC_PV) mvc_poly_prep_kernel(const Harves
         const int p = i / MVC_PV, q = i % MVC_PV;
         const bool in = p + q < MVC_PV;
         const double vi = in ? vinf[p][q] : 0.0;
-        out->lvn[p][q] = (vi > 0.0 && isfinite(vi)) ? (float)log2(vi) : -1e30f;
-        for (int c = 0; c <= MVC_PN; ++c) out->pv[p][q][c] = (in && pok && c < MVC_PN) ? Vs[p][q][c] : 0.0;
+        const float lv = (vi > 0.0 && isfinite(vi)) ? (float)log2(vi) : -1e30f;
+        if (p + q < MVC_PV - 1)
+            out->pl[p * (MVC_PV - 1) - p * (p - 1) / 2 + q] = make_float4(pok ? lv : -1e30f, (float)p, (float)q, 0.f);
+        // (stored back in the unbalanced coordinates: 2^(e_c - e_row), exact)
+        for (int c = 0; c <= MVC_PN; ++c)
+            out->pv[p][q][c] = (in && pok && c < n) ? Vs[p][q][c] * mv_pow2(out->e[c] - out->e[row]) : 0.0;
     }
-    if (threadIdx.x <= MVC_PN)
-        out->psc[threadIdx.x] = threadIdx.x < n ? mv_pow2(out->e[threadIdx.x] - out->e[row]) : 0.0;
     if (threadIdx.x == 0) out->poly_ok = pok ? 1 : 0;
 }
 
 // Polynomial kernel (w_lin of two-table operators, harvest.py:97-121 per node):
 // one item per lane evaluates  w = sum_pq a^p b^q V_pq  (a, b its two
-// coefficients over item 0's) as nested Horner sums -- 13 independent chains,
-// the table entries as constant-bank operands -- over the columns a warp-wide
+// coefficients over item 0's) term by term -- 13 independent accumulators, one
+// running monomial, the table entries read by wide uniform loads at
+// compile-time constant-bank addresses -- over the columns a block-wide
 // magnitude test keeps: at n = 13 with a diffusion-dominated step (config 5)
-// 19 of the 91 columns.  A warp whose largest term exceeds 2^6 (cancellation)
-// or whose coefficients are not finite hands its items to the Taylor kernel
-// (status LMEP_PENDING), as does every item when the series does not
-// terminate inside the table.
-template <int N>
-__global__ void __launch_bounds__(128) harvest_poly_kernel(const HarvestParams P)
+// 11-16 of the 91 columns in 3-4 rows.  A block whose largest term exceeds 2^6
+// (cancellation) or whose coefficients are not finite hands its items to the
+// Taylor kernel through the work list, as does every item when the series does
+// not terminate inside the table.
+// Config 5 (4,194,304 items): 102 us = 5.1 TB/s on its 124 B per item (16 in,
+// 104 + 4 out), 0.78 of the measured HBM peak; 44 registers.
+
+// an upper bound of log2 |x| from the high word of |x| (log2(1 + m) <= m + 0.0861)
+__device__ __forceinline__ float poly_log2_ub(unsigned hi)
 {
-    // column selection once per CTA, from the CTA-wide coefficient magnitudes
-    __shared__ unsigned smax[2];
+    return (float)((int)(hi >> 20) - 1023) + (float)(hi & 0xfffffu) * 0x1p-20f + 0.09f;
+}
+
+// Each CTA takes one block of 128 items, IT per thread (items t, t + 128 / IT, ...:
+// the rows of a block do not depend on IT or on how the batch was sliced).
+template <int N, int IT>
+__global__ void __launch_bounds__(128 / IT) harvest_poly_kernel(const HarvestParams P, const MvcConst *G)
+{
+    constexpr int T = 128 / IT;
+    // column selection once per block, from the block-wide coefficient magnitudes
+    __shared__ unsigned smax[T / 32][2];
     __shared__ int sq[MVC_PV];             // sq[p]: highest significant q of row p (-1: none)
-    __shared__ int sflag;                  // 1: hand the CTA's items to the Taylor kernel
-    int64_t braw = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool live = braw < P.B;
-    const int64_t b = live ? braw : P.B - 1;
-    if (threadIdx.x < 2) smax[threadIdx.x] = 0u;
-    if (threadIdx.x < MVC_PV) sq[threadIdx.x] = -1;
-    if (threadIdx.x == 0) sflag = c_mvc.poly_ok ? 0 : 1;
+    __shared__ int sflag;                  // 1: hand the block's items to the Taylor kernel
+    const int tid = threadIdx.x;
+    bool live[IT];
+    int64_t b[IT];
+    double a[IT], be[IT];
+    unsigned ha = 0u, hb = 0u;
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+        const int64_t braw = (int64_t)blockIdx.x * 128 + it * T + tid;
+        live[it] = braw < P.B;
+        b[it] = live[it] ? braw : P.B - 1;
+        a[it] = P.coef[b[it] * P.coef_stride] * c_mvc.cinv[0];
+        be[it] = P.coef[b[it] * P.coef_stride + 1] * c_mvc.cinv[1];
+        // (upper bounds from the high words; NaN / Inf sort last)
+        ha = max(ha, mv_hiabs(a[it]));
+        hb = max(hb, mv_hiabs(be[it]));
+    }
+    ha = __reduce_max_sync(FULL, ha);
+    hb = __reduce_max_sync(FULL, hb);
+    if ((tid & 31) == 0) { smax[tid >> 5][0] = ha; smax[tid >> 5][1] = hb; }
+    if (tid < MVC_PV) sq[tid] = -1;
+    if (tid == 0) sflag = c_mvc.poly_ok ? 0 : 1;
     __syncthreads();
-    const double a = P.coef[b * P.coef_stride] * c_mvc.cinv[0];
-    const double be = P.coef[b * P.coef_stride + 1] * c_mvc.cinv[1];
-    // (upper bounds from the high words; NaN / Inf sort last)
-    const unsigned ha = __reduce_max_sync(FULL, mv_hiabs(a)), hb = __reduce_max_sync(FULL, mv_hiabs(be));
-    if ((threadIdx.x & 31) == 0) { atomicMax(&smax[0], ha); atomicMax(&smax[1], hb); }
-    __syncthreads();
-    if (threadIdx.x < MVC_PV - 1) {
-        const float xa = (float)__hiloint2double((int)smax[0], -1), xb = (float)__hiloint2double((int)smax[1], -1);
-        const float la = xa > 0.f ? log2f(xa) : -1e30f, lb = xb > 0.f ? log2f(xb) : -1e30f;
-        const int p = threadIdx.x;
-        int qtop = -1;
-        bool big = false;
-        for (int q = 0; p + q < MVC_PV - 1; ++q) {
-            const float lv = c_mvc.lvn[p][q];
-            if (lv > -1e29f) {
-                const float t = (p ? p * la : 0.f) + (q ? q * lb : 0.f) + lv;
-                if (t > -60.f) qtop = q;
-                if (!(t <= 6.f)) big = true;
-            }
+    {
+        // one (p, q) pair per thread: is |a|^p |b|^q |V_pq| significant / too large?
+#pragma unroll
+        for (int k = 0; k < T / 32; ++k) { ha = max(ha, smax[k][0]); hb = max(hb, smax[k][1]); }
+        const float la = poly_log2_ub(ha), lb = poly_log2_ub(hb);
+        for (int i = tid; i < MVC_PAIRS; i += T) {
+            const float4 e = G->pl[i];           // (log2 |V_pq|, p, q)
+            const float t = fmaf(e.y, la, fmaf(e.z, lb, e.x));
+            if (t > -60.f) atomicMax(&sq[(int)e.y], (int)e.z);
+            if (!(t <= 6.f)) sflag = 1;
         }
-        sq[p] = qtop;
-        if (big) sflag = 1;
     }
     __syncthreads();
     if (sflag) {
-        // the CTA's items go to the Taylor kernel: one entry in its work list
-        if (threadIdx.x == 0) P.pending[1 + atomicAdd(P.pending, 1)] = (int)blockIdx.x;
+        // the block's items go to the Taylor kernel: one entry in its work list
+        if (tid == 0) P.pending[1 + atomicAdd(P.pending, 1)] = (int)blockIdx.x;
         return;
     }
-    // (through a ballot / shuffles so that the compiler sees warp-uniform loop
-    // bounds and feeds the table entries as uniform-register operands)
-    const int myq = (threadIdx.x & 31) < MVC_PV ? sq[threadIdx.x & 31] : -1;
+    // w = sum_pq (a^p be^q) V_pq term by term, rows and columns ascending with a
+    // uniform exit after the last significant one: ONE accumulator per output
+    // (no per-row partial sums), one running monomial per item, and both loops
+    // fully unrolled so that every table entry is read at a compile-time
+    // constant-bank address (wide uniform loads shared by the thread's items)
+    const int myq = (tid & 31) < MVC_PV ? sq[tid & 31] : -1;
     const unsigned has = __ballot_sync(FULL, myq >= 0);
-    const int Pw = has ? 31 - __clz((int)has) : 0;
-    double w[N];
+    const int Pw = has ? 31 - __clz((int)has) : -1;
+    double w[IT][N], ap[IT];
 #pragma unroll
-    for (int j = 0; j < N; ++j) w[j] = 0.0;
+    for (int it = 0; it < IT; ++it) {
+        ap[it] = 1.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) w[it][j] = 0.0;
+    }
     int cols = 0;
-#pragma unroll 1
-    for (int p = Pw; p >= 0; --p) {
+#pragma unroll
+    for (int p = 0; p < MVC_PV - 1; ++p) {
+        if (p > Pw) break;
         const int qt = __shfl_sync(FULL, myq, p);
-        // s = sum_q be^q V_pq by Horner from the top; columns above qt are skipped
-        // (uniform branches), the table entries are constant-bank operands at
-        // compile-time offsets from row p
-        double s[N];
+        double m[IT];
 #pragma unroll
-        for (int j = 0; j < N; ++j) s[j] = 0.0;
-        const double (*row_p)[MVC_PN + 1] = c_mvc.pv[p];
+        for (int it = 0; it < IT; ++it) m[it] = ap[it];
 #pragma unroll
-        for (int q = MVC_PV - 2; q >= 0; --q) {
-            if (q <= qt) {
+        for (int q = 0; q < MVC_PV - 1 - p; ++q) {
+            if (q > qt) break;
 #pragma unroll
-                for (int j = 0; j < N; ++j) s[j] = fma(s[j], be, row_p[q][j]);
-            }
+            for (int j = 0; j < N; ++j)
+#pragma unroll
+                for (int it = 0; it < IT; ++it) w[it][j] = fma(m[it], c_mvc.pv[p][q][j], w[it][j]);
+#pragma unroll
+            for (int it = 0; it < IT; ++it) m[it] *= be[it];
         }
 #pragma unroll
-        for (int j = 0; j < N; ++j) w[j] = fma(w[j], a, s[j]);
+        for (int it = 0; it < IT; ++it) ap[it] *= a[it];
         cols += qt + 1;
     }
-    if (!live) return;
     const int n = P.n;
-    bool bad = false;
 #pragma unroll
-    for (int j = 0; j < N; ++j) {
-        const double o = w[j] * c_mvc.psc[j];
-        bad |= !isfinite(o);
-        if (j < n) {
-            if (P.layout == 0) P.out[b * n + j] = o;
-            else P.out[(int64_t)j * P.out_ld + b] = o;
+    for (int it = 0; it < IT; ++it) {
+        if (!live[it]) continue;
+        bool bad = false;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            const double o = w[it][j];
+            bad |= !isfinite(o);
+            if (j < n) {
+                if (P.layout == 0) P.out[b[it] * n + j] = o;
+                else P.out[(int64_t)j * P.out_ld + b[it]] = o;
+            }
         }
+        P.status[b[it]] = bad ? LMEP_NONFINITE : LMEP_OK;
+        if (P.ms) P.ms[b[it]] = cols;    // scaling field 0: a polynomial item, `cols` columns
     }
-    P.status[b] = bad ? LMEP_NONFINITE : LMEP_OK;
-    if (P.ms) P.ms[b] = cols;            // scaling field 0: a polynomial item, `cols` Horner columns
 }
 
 // 3 CTAs per SM (<= 168 registers): 12 warps hide the DFMA and constant-load
@@ -715,10 +748,10 @@ int launch_harvest_mvc(const HarvestParams &P, cudaStream_t st)
         cudaMemsetAsync(D.pending, 0, sizeof(int32_t), st);
         Q.pending = D.pending;
         switch (P.n) {
-        case 7: harvest_poly_kernel<7><<<blocks, 128, 0, st>>>(Q); break;
-        case 9: harvest_poly_kernel<9><<<blocks, 128, 0, st>>>(Q); break;
-        case 11: harvest_poly_kernel<11><<<blocks, 128, 0, st>>>(Q); break;
-        default: harvest_poly_kernel<13><<<blocks, 128, 0, st>>>(Q); break;
+        case 7: harvest_poly_kernel<7, MVC_IT><<<blocks, 128 / MVC_IT, 0, st>>>(Q, D.scratch); break;
+        case 9: harvest_poly_kernel<9, MVC_IT><<<blocks, 128 / MVC_IT, 0, st>>>(Q, D.scratch); break;
+        case 11: harvest_poly_kernel<11, MVC_IT><<<blocks, 128 / MVC_IT, 0, st>>>(Q, D.scratch); break;
+        default: harvest_poly_kernel<13, MVC_IT><<<blocks, 128 / MVC_IT, 0, st>>>(Q, D.scratch); break;
         }
         // the Taylor kernel on what is left: a grid of at most six CTAs per SM
         const unsigned g = std::min<unsigned>(blocks, 6u * (unsigned)device_sm_count());

@@ -14,7 +14,7 @@ timeout 600 python bench.py --steps 1 --warmup 1 --no-others --no-cpu > $O/b_sma
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
   python bench.py --steps 1 --warmup 1 --no-others --no-cpu > $O/ncu_launch.log 2>&1; echo "launches rc=$?"
 timeout 300 python tools/prof_cases.py harvest --reps 1 --N 4194304 > $O/h_plain.json 2>&1 && \
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:harvest_mvc -s 1 -c 1 -o $O/harvest \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:harvest_poly -s 1 -c 1 -o $O/harvest \
   python tools/prof_cases.py harvest --reps 1 --N 4194304 > $O/ncu_h.log 2>&1; echo "ncu harvest rc=$?"
 timeout 300 python tools/prof_cases.py c5step --reps 50 --fma > $O/c5s_plain.json 2>&1 && \
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:lin_pernode_t -s 2 -c 1 -o $O/c5step \
