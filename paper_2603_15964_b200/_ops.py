@@ -120,13 +120,34 @@ class LinearStream:
     # slice (its download is the only exposed one)
     WAVES = (1.0, 4.0, 7.0, 7.0)
     LAST_MIN = 2.0
+    # prefixes (nodes) of the coefficient table and the initial state that go up
+    # from the constructor, before the harvest is planned: PCIe works while the
+    # host plans (the first covers the first slice, multiples of 1024)
+    EAGER = (192 * 1024, 1024 * 1024)
 
     def __init__(self, u0_host: torch.Tensor, steps: int, exact: bool, tuning, snap0: torch.Tensor,
-                 host_out: torch.Tensor, down: torch.cuda.Stream):
+                 host_out: torch.Tensor, down: torch.cuda.Stream, coef_host: torch.Tensor | None = None):
         d = nat.device()
         self.N = int(u0_host.numel())
         self.src = u0_host
         self.u0 = torch.empty(self.N, dtype=F64, device=d)
+        # eager prefixes: [(end, event)] in rising order; coef_dev is the device
+        # table the pipelined harvest then fills (harvest._harvest_pipelined)
+        self.coef_src, self.coef_dev, self.eager = coef_host, None, []
+        if coef_host is not None and coef_host.dim() == 2 and coef_host.shape[0] == self.N and self.EAGER:
+            self.coef_dev = torch.empty(tuple(coef_host.shape), dtype=F64, device=d)
+            up = copy_stream()
+            up.wait_stream(torch.cuda.current_stream(d))
+            a = 0
+            with torch.cuda.stream(up):
+                for e in self.EAGER:
+                    b = min(self.N, int(e))
+                    if b <= a:
+                        break
+                    self.coef_dev[a:b].copy_(coef_host[a:b], non_blocking=True)
+                    self.u0[a:b].copy_(u0_host[a:b], non_blocking=True)
+                    self.eager.append((b, up.record_event()))
+                    a = b
         self.out = torch.empty(self.N, dtype=F64, device=d)
         self.scr = torch.empty(self.N, dtype=F64, device=d)
         self.flag = torch.zeros(1, dtype=torch.int32, device=d)
@@ -185,6 +206,16 @@ class LinearStream:
     def upload(self, a: int, b: int) -> None:
         """(on the upload stream) the slice of the initial state."""
         self.u0[a:b].copy_(self.src[a:b], non_blocking=True)
+
+    def eager_end(self) -> int:
+        return self.eager[-1][0] if self.eager else 0
+
+    def eager_event(self, b: int):
+        """The event behind which nodes [0, b) have landed, if an eager prefix covers them."""
+        for end, ev in self.eager:
+            if b <= end:
+                return ev
+        return None
 
     def uploaded(self, up: torch.cuda.Stream, ev) -> None:
         """Every slice is queued on the upload stream `up` (ev: the last one's

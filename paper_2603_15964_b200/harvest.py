@@ -522,10 +522,20 @@ def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
         ls = None
     if ls is not None:
         bounds = ls.begin(sset, out.rows, bounds)
+    # prefixes the streamed run already sent up from its constructor (same host table)
+    eager = ls is not None and ls.eager and hr is None and ls.coef_src is not None and \
+        ls.coef_src.data_ptr() == hc.data_ptr() and tuple(ls.coef_dev.shape) == (N, K)
+    if eager:
+        dc = ls.coef_dev
     cp.wait_stream(cur)                      # dc / dr (and the stream's buffers) were allocated on cur
 
     def upload(i):
         a, b = bounds[i]
+        if eager:
+            ev = ls.eager_event(b)
+            if ev is not None:
+                return ev
+            a = max(a, ls.eager_end())
         with torch.cuda.stream(cp):
             dc[a:b].copy_(hc[a:b], non_blocking=True)
             if dr is not None:
@@ -560,12 +570,15 @@ def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
             # the first harvest is queued, so the uploads stay just two slices ahead of
             # the harvests (PCIe never idles: a slice takes longer to land than the
             # host needs to queue a harvest and its step launches)
-            landed = [upload(i) for i in range(min(2, len(bounds)))]
+            # With an eager prefix already on its way (LinearStream's constructor) the
+            # upload stream is the critical path instead: every slice is queued at once.
+            ahead = len(bounds) if eager else 2
+            landed = [upload(i) for i in range(min(ahead, len(bounds)))]
             tables = tables_fn()
             for i in range(len(bounds)):
                 harvest_slice(i, landed[i])
-                if i + 2 < len(bounds):
-                    landed.append(upload(i + 2))
+                if i + ahead < len(bounds):
+                    landed.append(upload(i + ahead))
             ls.uploaded(cp, landed[-1])
 
     tables = None

@@ -438,7 +438,8 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
             problem.boundary.kind == "periodic":
         # one pipeline: upload || harvest || steps || download, slice by slice
         # (_ops.LinearStream); the initial state rides up with the coefficients
-        ls = _ops.LinearStream(_ops.host_f64(u0), k_first, exact, tuning, snaps[0], snaps[1], cp1)
+        ls = _ops.LinearStream(_ops.host_f64(u0), k_first, exact, tuning, snaps[0], snaps[1], cp1,
+                               coef_host=_ops.host_f64(lin.coef) if lin.reaction is None else None)
         _ops.set_stream_consumer(ls)
     elif host_in:
         src = _ops.host_f64(u0)
