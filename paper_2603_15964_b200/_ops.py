@@ -50,11 +50,14 @@ _COPY_STREAMS: dict = {}
 
 def copy_stream(which: int = 0) -> torch.cuda.Stream:
     """Side streams host<->device transfers overlap on (per device): 0 carries
-    harvest inputs and snapshots, 1 the initial state."""
+    harvest inputs and snapshots, 1 the initial state; 2 is the side stream a
+    streamed run's harvests are queued on."""
     d = nat.device()
     key = (d.index if d.index is not None else torch.cuda.current_device(), which)
     if key not in _COPY_STREAMS:
-        _COPY_STREAMS[key] = torch.cuda.Stream(device=d)
+        # stream 2 (harvests beside a streamed run's step launches) has priority: its
+        # CTAs go first whenever a persistent step kernel hands SMs back
+        _COPY_STREAMS[key] = torch.cuda.Stream(device=d, priority=-1 if which == 2 else 0)
     return _COPY_STREAMS[key]
 
 
@@ -118,7 +121,7 @@ class LinearStream:
     # slices in waves of (SM count) level-1 tiles: a small first slice (its upload
     # is the only exposed one), wide middle slices (few launches), a small last
     # slice (its download is the only exposed one)
-    WAVES = (1.0, 4.0, 7.0, 7.0)
+    WAVES = (1.0, 3.0, 6.0, 6.0, 4.0)
     LAST_MIN = 2.0
     # prefixes (nodes) of the coefficient table and the initial state that go up
     # from the constructor, before the harvest is planned: PCIe works while the
@@ -131,6 +134,7 @@ class LinearStream:
         self.N = int(u0_host.numel())
         self.src = u0_host
         self.u0 = torch.empty(self.N, dtype=F64, device=d)
+        self.snap0, self.host_out, self.down = snap0, host_out, down
         # eager prefixes: [(end, event)] in rising order; coef_dev is the device
         # table the pipelined harvest then fills (harvest._harvest_pipelined)
         self.coef_src, self.coef_dev, self.eager = coef_host, None, []
@@ -147,6 +151,7 @@ class LinearStream:
                     self.coef_dev[a:b].copy_(coef_host[a:b], non_blocking=True)
                     self.u0[a:b].copy_(u0_host[a:b], non_blocking=True)
                     self.eager.append((b, up.record_event()))
+                    self.snap_slice(a, b, self.eager[-1][1])
                     a = b
         self.out = torch.empty(self.N, dtype=F64, device=d)
         self.scr = torch.empty(self.N, dtype=F64, device=d)
@@ -217,13 +222,24 @@ class LinearStream:
                 return ev
         return None
 
+    def snap_slice(self, a: int, b: int, ev) -> None:
+        """Nodes [a, b) of the initial state have landed behind `ev`: that part of
+        snapshot 0 (timestep.py:313) goes back down at once on the download
+        stream, while the uploads keep the other direction of the link busy
+        (behind the uploads it would hold the result's download up at the end)."""
+        self.down.wait_event(ev)
+        with torch.cuda.stream(self.down):
+            self.snap0[a:b].copy_(self.u0[a:b], non_blocking=True)
+        self._snapped = getattr(self, "_snapped", 0) + (b - a)
+
     def uploaded(self, up: torch.cuda.Stream, ev) -> None:
         """Every slice is queued on the upload stream `up` (ev: the last one's
-        event): snapshot 0 (timestep.py:313) goes back down behind them, off the
-        stream that carries the result."""
-        with torch.cuda.stream(up):
-            self.snap0.copy_(self.u0, non_blocking=True)
-        self.snap0_event = up.record_event()
+        event); snapshot 0 is complete behind snap0_event."""
+        if getattr(self, "_snapped", 0) != self.N:       # (not sent slice by slice)
+            self.down.wait_event(ev)
+            with torch.cuda.stream(self.down):
+                self.snap0.copy_(self.u0, non_blocking=True)
+        self.snap0_event = self.down.record_event()
         self.last_landed = ev
 
     def ready(self, b: int) -> None:

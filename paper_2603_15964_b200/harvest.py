@@ -542,18 +542,32 @@ def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
                 dr[a:b].copy_(hr[a:b], non_blocking=True)
             if ls is not None:
                 ls.upload(a, b)
-            return cp.record_event()
+            ev = cp.record_event()
+        if ls is not None:
+            ls.snap_slice(a, b, ev)
+        return ev
+
+    # streamed run: the harvests run on a side stream (they depend on the uploads
+    # only), so the harvest of slice i+1 overlaps the step launches of slice i on
+    # the compute stream; the steps of a slice wait for its harvest's event
+    hs = _ops.copy_stream(2) if ls is not None and ls.active else cur
+    if hs is not cur:
+        hs.wait_stream(cur)
 
     def harvest_slice(i, ev):
         a, b = bounds[i]
-        cur.wait_event(ev)
+        hs.wait_event(ev)
         # later slices keep the first slice's prepared tables (lmep_harvest_reuse_prep):
         # the rows are those of a one-launch harvest whatever the slicing
         nat.lib().lmep_harvest_reuse_prep(1 if i > 0 else 0)
-        _ops.harvest(n, s, delta_t, b - a, tables=tables, coef=dc[a:b], coef_stride=K,
-                     c0=None if dr is None else dr[a:b], c0_stride=0 if dr is None else 1,
-                     row_default=row, frozen_default=0, layout=1, into=out, item0=a)
+        with torch.cuda.stream(hs):
+            _ops.harvest(n, s, delta_t, b - a, tables=tables, coef=dc[a:b], coef_stride=K,
+                         c0=None if dr is None else dr[a:b], c0_stride=0 if dr is None else 1,
+                         row_default=row, frozen_default=0, layout=1, into=out, item0=a)
         if ls is not None:
+            if hs is not cur:
+                cur.wait_event(hs.record_event())
+                cur.wait_event(ev)               # (the slice of the initial state)
             ls.ready(b)
 
     def _run_slices():
@@ -571,14 +585,27 @@ def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
             # the harvests (PCIe never idles: a slice takes longer to land than the
             # host needs to queue a harvest and its step launches)
             # With an eager prefix already on its way (LinearStream's constructor) the
-            # upload stream is the critical path instead: every slice is queued at once.
-            ahead = len(bounds) if eager else 2
-            landed = [upload(i) for i in range(min(ahead, len(bounds)))]
-            tables = tables_fn()
-            for i in range(len(bounds)):
-                harvest_slice(i, landed[i])
-                if i + ahead < len(bounds):
-                    landed.append(upload(i + ahead))
+            # first harvest is queued before anything else (its slice is covered by
+            # the prefix) and every later slice goes up right behind it, at once: the
+            # upload stream never idles and the compute stream starts ~75 us earlier.
+            if eager:
+                landed = []
+                while len(landed) < len(bounds) and ls.eager_event(bounds[len(landed)][1]) is not None:
+                    landed.append(upload(len(landed)))           # (events only, nothing to copy)
+                tables = tables_fn()
+                for i in range(len(bounds)):
+                    if i >= len(landed):
+                        landed.extend(upload(j) for j in range(len(landed), len(bounds)))
+                    harvest_slice(i, landed[i])
+                    if i == 0:
+                        landed.extend(upload(j) for j in range(len(landed), len(bounds)))
+            else:
+                landed = [upload(i) for i in range(min(2, len(bounds)))]
+                tables = tables_fn()
+                for i in range(len(bounds)):
+                    harvest_slice(i, landed[i])
+                    if i + 2 < len(bounds):
+                        landed.append(upload(i + 2))
             ls.uploaded(cp, landed[-1])
 
     tables = None
@@ -589,6 +616,11 @@ def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
     dc.record_stream(cp)
     if dr is not None:
         dr.record_stream(cp)
+    if hs is not cur:
+        cur.wait_stream(hs)
+        for t in (dc, dr, out.rows, out.status, out.ms, out.flag, tables):
+            if isinstance(t, torch.Tensor) and t.is_cuda:
+                t.record_stream(hs)
     return out
 
 
