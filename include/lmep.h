@@ -558,6 +558,21 @@ int lmep_lin_stream_info(const lmep_lin_stream *s, int64_t *tile, int64_t *margi
 int lmep_lin_stream_advance(lmep_lin_stream *s, int64_t nodes_ready, void *stream);
 int lmep_lin_stream_end(lmep_lin_stream *s, int64_t *launches);
 
+/* Slice transfers of a streamed run (timestep.py:284-313: the uploads of the
+ * coefficient table and the initial state, and snapshot 0).  lmep_upload_slice
+ * queues, on up_stream, coef_bytes of coefficients (event ev_coef behind them)
+ * and u_bytes of the initial state (event ev_all behind both), and, on
+ * down_stream behind ev_all, the copy of that part of the initial state into
+ * snap_host (nullable).  Host buffers should be page-locked.  Events come from
+ * lmep_event_create (no timing) and may be re-recorded once their waiters have
+ * been queued; lmep_stream_wait_event makes a stream wait for one. */
+int lmep_event_create(void **ev);
+int lmep_event_destroy(void *ev);
+int lmep_stream_wait_event(void *stream, void *ev);
+int lmep_upload_slice(void *coef_dev, const void *coef_host, size_t coef_bytes,
+                      void *u_dev, const void *u_host, void *snap_host, size_t u_bytes,
+                      void *up_stream, void *down_stream, void *ev_coef, void *ev_all);
+
 /* Fused four-stage ETDRK4 (kernels.py:62-132, run_etdrk4): rows W, ALPHA, BETA,
  * GAMMA, WHALF, P1HALF (and D1 for LMEP_NL_CONVECTIVE).  nl0_out (nullable)
  * receives N(u_in) on the owned nodes (the history entry the ETD multistep

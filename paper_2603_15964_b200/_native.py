@@ -52,6 +52,7 @@ EXPORTS = (
     "lmep_comm_targets", "lmep_comm_push", "lmep_comm_signal", "lmep_comm_wait",
     "lmep_comm_ghosts", "lmep_set_etd2_persistent", "lmep_step_linear_host", "lmep_comm_chunk",
     "lmep_harvest_reuse_prep", "lmep_lin_stream_begin", "lmep_lin_stream_info", "lmep_lin_stream_advance", "lmep_lin_stream_end",
+    "lmep_event_create", "lmep_event_destroy", "lmep_stream_wait_event", "lmep_upload_slice",
 )
 COMM_NCCL, COMM_PEER = 0, 1
 COMM_ID_BYTES, COMM_BLOB_BYTES, COMM_MAX_FIELDS = 128, 512, 8
@@ -154,6 +155,10 @@ def load(path: str | None = None):
                                        C.POINTER(i32)]
     L.lmep_lin_stream_advance.argtypes = [vp, i64, vp]
     L.lmep_lin_stream_end.argtypes = [vp, C.POINTER(i64)]
+    L.lmep_event_create.argtypes = [C.POINTER(vp)]
+    L.lmep_event_destroy.argtypes = [vp]
+    L.lmep_stream_wait_event.argtypes = [vp, vp]
+    L.lmep_upload_slice.argtypes = [vp, vp, C.c_size_t, vp, vp, vp, C.c_size_t, vp, vp, vp, vp]
     L.lmep_step_etdrk4.argtypes = [G, W, B, H, C.c_int, vp, vp, vp, i64, vp, i32, T, vp, vp]
     L.lmep_step_etd2.argtypes = [G, W, B, H, C.c_int, dbl, vp, vp, vp, vp, vp, i64, i32, T, vp,
                                  vp]

@@ -51,7 +51,7 @@ _COPY_STREAMS: dict = {}
 def copy_stream(which: int = 0) -> torch.cuda.Stream:
     """Side streams host<->device transfers overlap on (per device): 0 carries
     harvest inputs and snapshots, 1 the initial state; 2 is the side stream a
-    streamed run's harvests are queued on."""
+    streamed run's harvests are queued on, 3 the one its snapshot 0 goes down on."""
     d = nat.device()
     key = (d.index if d.index is not None else torch.cuda.current_device(), which)
     if key not in _COPY_STREAMS:
@@ -103,6 +103,17 @@ def drop_deferred(up: DeferredUpload) -> None:
         q.remove(up)
 
 
+_EVENT_POOL: dict = {}
+
+
+def stream_wait(stream: torch.cuda.Stream, ev) -> None:
+    """stream waits for ev: a torch event or a raw one (lmep_event_create)."""
+    if isinstance(ev, torch.cuda.Event):
+        stream.wait_event(ev)
+    else:
+        nat.check(nat.lib().lmep_stream_wait_event(stream.cuda_stream, ev), "lmep_stream_wait_event")
+
+
 class LinearStream:
     """Consumer of a pipelined per-node harvest: timestep.run's linear scheme
     from host arrays as one pipeline (lmep_lin_stream, csrc/step_stream.cu).
@@ -138,21 +149,22 @@ class LinearStream:
         # eager prefixes: [(end, event)] in rising order; coef_dev is the device
         # table the pipelined harvest then fills (harvest._harvest_pipelined)
         self.coef_src, self.coef_dev, self.eager = coef_host, None, []
+        self._snapped = 0
+        self._nev = 0
+        # snapshot 0 goes down on its own stream: on the result's stream its slices
+        # (queued with the uploads, up front) would sit in front of every result copy
+        self.snap_stream = copy_stream(3)
         if coef_host is not None and coef_host.dim() == 2 and coef_host.shape[0] == self.N and self.EAGER:
             self.coef_dev = torch.empty(tuple(coef_host.shape), dtype=F64, device=d)
             up = copy_stream()
             up.wait_stream(torch.cuda.current_stream(d))
             a = 0
-            with torch.cuda.stream(up):
-                for e in self.EAGER:
-                    b = min(self.N, int(e))
-                    if b <= a:
-                        break
-                    self.coef_dev[a:b].copy_(coef_host[a:b], non_blocking=True)
-                    self.u0[a:b].copy_(u0_host[a:b], non_blocking=True)
-                    self.eager.append((b, up.record_event()))
-                    self.snap_slice(a, b, self.eager[-1][1])
-                    a = b
+            for e in self.EAGER:
+                b = min(self.N, int(e))
+                if b <= a:
+                    break
+                self.eager.append((b, self.send(self.coef_dev, coef_host, a, b, up)))
+                a = b
         self.out = torch.empty(self.N, dtype=F64, device=d)
         self.scr = torch.empty(self.N, dtype=F64, device=d)
         self.flag = torch.zeros(1, dtype=torch.int32, device=d)
@@ -216,31 +228,50 @@ class LinearStream:
         return self.eager[-1][0] if self.eager else 0
 
     def eager_event(self, b: int):
-        """The event behind which nodes [0, b) have landed, if an eager prefix covers them."""
+        """The events (coefficients, coefficients + initial state) behind which nodes
+        [0, b) have landed, if an eager prefix covers them."""
         for end, ev in self.eager:
             if b <= end:
                 return ev
         return None
 
-    def snap_slice(self, a: int, b: int, ev) -> None:
-        """Nodes [a, b) of the initial state have landed behind `ev`: that part of
-        snapshot 0 (timestep.py:313) goes back down at once on the download
-        stream, while the uploads keep the other direction of the link busy
-        (behind the uploads it would hold the result's download up at the end)."""
-        self.down.wait_event(ev)
-        with torch.cuda.stream(self.down):
-            self.snap0[a:b].copy_(self.u0[a:b], non_blocking=True)
-        self._snapped = getattr(self, "_snapped", 0) + (b - a)
+    def send(self, coef_dev: torch.Tensor, coef_host: torch.Tensor, a: int, b: int,
+             up: torch.cuda.Stream):
+        """Queue nodes [a, b) on the link in one library call (lmep_upload_slice):
+        their coefficients and their part of the initial state go up on `up`, that
+        part of snapshot 0 (timestep.py:313) goes back down at once on the snapshot
+        stream while the uploads keep the other direction busy (behind all the
+        uploads it would hold the result's download up at the end).  Returns the
+        raw events (coefficients landed, everything landed)."""
+        ec, ev = self._event(), self._event()
+        cb = coef_host.stride(0) * 8
+        nat.check(nat.lib().lmep_upload_slice(
+            coef_dev.data_ptr() + a * cb, coef_host.data_ptr() + a * cb, (b - a) * cb,
+            self.u0.data_ptr() + 8 * a, self.src.data_ptr() + 8 * a, self.snap0.data_ptr() + 8 * a,
+            8 * (b - a), up.cuda_stream, self.snap_stream.cuda_stream, ec, ev), "lmep_upload_slice")
+        self._snapped += b - a
+        return ec, ev
 
-    def uploaded(self, up: torch.cuda.Stream, ev) -> None:
-        """Every slice is queued on the upload stream `up` (ev: the last one's
-        event); snapshot 0 is complete behind snap0_event."""
-        if getattr(self, "_snapped", 0) != self.N:       # (not sent slice by slice)
-            self.down.wait_event(ev)
-            with torch.cuda.stream(self.down):
+    def _event(self):
+        """A raw event of the per-device pool (re-recorded run after run: a run ends
+        synchronised, and a wait keeps the state it was queued behind)."""
+        pool = _EVENT_POOL.setdefault(self.u0.device.index, [])
+        if self._nev == len(pool):
+            h = C.c_void_p()
+            nat.check(nat.lib().lmep_event_create(C.byref(h)), "lmep_event_create")
+            pool.append(h)
+        self._nev += 1
+        return pool[self._nev - 1]
+
+    def uploaded(self, up: torch.cuda.Stream) -> None:
+        """Every slice is queued on the upload stream `up`; snapshot 0 is complete
+        behind snap0_event."""
+        self.last_landed = up.record_event()
+        if self._snapped != self.N:                      # (not sent slice by slice)
+            self.snap_stream.wait_event(self.last_landed)
+            with torch.cuda.stream(self.snap_stream):
                 self.snap0.copy_(self.u0, non_blocking=True)
-        self.snap0_event = self.down.record_event()
-        self.last_landed = ev
+        self.snap0_event = self.snap_stream.record_event()
 
     def ready(self, b: int) -> None:
         """The harvest of nodes [0, b) is queued on the current stream."""

@@ -249,3 +249,56 @@ extern "C" int lmep_lin_stream_end(lmep_lin_stream *s, int64_t *launches)
     delete s;
     return rc;
 }
+
+// ---- slice transfers of a streamed run --------------------------------------
+// One call queues what a slice needs on the link: its coefficients and its part
+// of the initial state go up on `up_stream` (an event behind each: the harvest
+// of the slice waits for the first only), and that part of snapshot 0
+// (timestep.py:313) goes back down on `down_stream` behind the second.  The
+// host side of a streamed run is on the critical path until the first harvest
+// is queued; a slice costs one library call instead of a dozen host-API calls
+// from Python.
+extern "C" int lmep_event_create(void **ev)
+{
+    if (!ev) return LMEP_INVALID_CONFIG;
+    cudaEvent_t e;
+    const cudaError_t rc = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (rc != cudaSuccess) { set_last_error("cudaEventCreateWithFlags", rc); return LMEP_CUDA_ERROR; }
+    *ev = (void *)e;
+    return LMEP_OK;
+}
+
+extern "C" int lmep_event_destroy(void *ev)
+{
+    if (ev) cudaEventDestroy((cudaEvent_t)ev);
+    return LMEP_OK;
+}
+
+extern "C" int lmep_stream_wait_event(void *stream, void *ev)
+{
+    if (!ev) return LMEP_INVALID_CONFIG;
+    const cudaError_t rc = cudaStreamWaitEvent((cudaStream_t)stream, (cudaEvent_t)ev, 0);
+    if (rc != cudaSuccess) { set_last_error("cudaStreamWaitEvent", rc); return LMEP_CUDA_ERROR; }
+    return LMEP_OK;
+}
+
+extern "C" int lmep_upload_slice(void *coef_dev, const void *coef_host, size_t coef_bytes,
+                                 void *u_dev, const void *u_host, void *snap_host, size_t u_bytes,
+                                 void *up_stream, void *down_stream, void *ev_coef, void *ev_all)
+{
+    if (!ev_coef || !ev_all || (coef_bytes && (!coef_dev || !coef_host)) ||
+        (u_bytes && (!u_dev || !u_host)))
+        return LMEP_INVALID_CONFIG;
+    cudaStream_t up = (cudaStream_t)up_stream, down = (cudaStream_t)down_stream;
+    cudaError_t rc = cudaSuccess;
+    if (coef_bytes) rc = cudaMemcpyAsync(coef_dev, coef_host, coef_bytes, cudaMemcpyHostToDevice, up);
+    if (rc == cudaSuccess) rc = cudaEventRecord((cudaEvent_t)ev_coef, up);
+    if (rc == cudaSuccess && u_bytes) rc = cudaMemcpyAsync(u_dev, u_host, u_bytes, cudaMemcpyHostToDevice, up);
+    if (rc == cudaSuccess) rc = cudaEventRecord((cudaEvent_t)ev_all, up);
+    if (rc == cudaSuccess && snap_host && u_bytes) {
+        rc = cudaStreamWaitEvent(down, (cudaEvent_t)ev_all, 0);
+        if (rc == cudaSuccess) rc = cudaMemcpyAsync(snap_host, u_dev, u_bytes, cudaMemcpyDeviceToHost, down);
+    }
+    if (rc != cudaSuccess) { set_last_error("lmep_upload_slice", rc); return LMEP_CUDA_ERROR; }
+    return LMEP_OK;
+}

@@ -530,22 +530,27 @@ def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
     cp.wait_stream(cur)                      # dc / dr (and the stream's buffers) were allocated on cur
 
     def upload(i):
+        """Queue slice i's transfers; returns (coefficients landed, everything landed):
+        the harvest of a slice starts behind the first, while its initial state is
+        still on the link."""
         a, b = bounds[i]
         if eager:
             ev = ls.eager_event(b)
             if ev is not None:
                 return ev
             a = max(a, ls.eager_end())
+        if ls is not None and dr is None:
+            return ls.send(dc, hc, a, b, cp)         # one library call per slice
         with torch.cuda.stream(cp):
             dc[a:b].copy_(hc[a:b], non_blocking=True)
             if dr is not None:
                 dr[a:b].copy_(hr[a:b], non_blocking=True)
-            if ls is not None:
-                ls.upload(a, b)
+            ec = cp.record_event()
+            if ls is None:
+                return ec, ec
+            ls.upload(a, b)
             ev = cp.record_event()
-        if ls is not None:
-            ls.snap_slice(a, b, ev)
-        return ev
+        return ec, ev
 
     # streamed run: the harvests run on a side stream (they depend on the uploads
     # only), so the harvest of slice i+1 overlaps the step launches of slice i on
@@ -554,9 +559,10 @@ def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
     if hs is not cur:
         hs.wait_stream(cur)
 
-    def harvest_slice(i, ev):
+    def harvest_slice(i, evs):
         a, b = bounds[i]
-        hs.wait_event(ev)
+        ec, ev = evs
+        _ops.stream_wait(hs, ec)
         # later slices keep the first slice's prepared tables (lmep_harvest_reuse_prep):
         # the rows are those of a one-launch harvest whatever the slicing
         nat.lib().lmep_harvest_reuse_prep(1 if i > 0 else 0)
@@ -567,7 +573,7 @@ def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
         if ls is not None:
             if hs is not cur:
                 cur.wait_event(hs.record_event())
-                cur.wait_event(ev)               # (the slice of the initial state)
+                _ops.stream_wait(cur, ev)        # (the slice of the initial state)
             ls.ready(b)
 
     def _run_slices():
@@ -606,7 +612,7 @@ def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
                     harvest_slice(i, landed[i])
                     if i + 2 < len(bounds):
                         landed.append(upload(i + 2))
-            ls.uploaded(cp, landed[-1])
+            ls.uploaded(cp)
 
     tables = None
     try:

@@ -472,7 +472,7 @@ def run(grid: Grid, stencils, problem: SemiLinearProblem, scheme: SchemeConfig,
             cp.wait_stream(cur)
             with torch.cuda.stream(cp):
                 ls.upload(0, N)
-            ls.uploaded(cp, cp.record_event())
+            ls.uploaded(cp)
         u0d, ev_u0 = ls.u0, ls.last_landed
     ev_harvest = torch.cuda.Event(enable_timing=True)
     ev_harvest.record(cur)
