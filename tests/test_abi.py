@@ -84,3 +84,15 @@ def test_comm_entry_points_validate_without_a_gpu():
         from paper_2603_15964_b200.distributed import Comm
         with pytest.raises(errors.LocalExpError):
             Comm(0, 1, True, "peer", max_width=8)
+
+
+def test_slice_transfer_entry_points_validate_without_a_gpu():
+    """lmep_upload_slice / lmep_stream_wait_event / lmep_event_create reject missing
+    events and buffers before any CUDA call."""
+    from paper_2603_15964_b200 import _native as nat
+    lib = nat.load()
+    assert lib.lmep_upload_slice(None, None, 0, None, None, None, 0, None, None, None, None) == \
+        nat.LMEP_INVALID_CONFIG
+    assert lib.lmep_stream_wait_event(None, None) == nat.LMEP_INVALID_CONFIG
+    assert lib.lmep_event_create(None) == nat.LMEP_INVALID_CONFIG
+    assert lib.lmep_event_destroy(None) == nat.LMEP_OK

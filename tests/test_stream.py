@@ -199,3 +199,49 @@ def test_run_streamed_fallbacks(lx):
         b = lx.run(g, st, prob, sch, w5.delta_t, steps * w5.delta_t, stride * w5.delta_t, stream=False)
         assert a.snapshots.shape == b.snapshots.shape == (1 + steps // stride, N)
         assert np.array_equal(a.snapshots, b.snapshots), (N, steps)
+
+
+def test_run_streamed_with_reaction_and_slice_upload(lx):
+    """A streamed run whose operator carries a reaction term (no eager prefix: the
+    reaction table rides with the slices through the torch copy path) against the
+    phase-by-phase order, and lmep_upload_slice on its own: coefficients and
+    initial state land behind their events, the snapshot copy comes back."""
+    from paper_2603_15964_b200 import configs, _native as nat, _ops
+    N = 1 << 19
+    w5 = configs.c5(N=N, steps=1)
+    c, nu = w5.coef
+    g = lx.make_periodic_grid(N, 0.0, 1.0)
+    st = lx.select_stencils(g, w5.n, lx.StencilPolicy.CENTERED)
+    x = np.asarray(g.nodes)
+    spec = lx.VariableCoefficientSpec((1, 2), np.stack([-c, nu], 1), reaction=-0.5 * (1.0 + np.sin(2 * np.pi * x)))
+    prob = lx.SemiLinearProblem(spec, None, np.array(w5.u0), lx.Boundary.periodic(), "none")
+    sch = lx.SchemeConfig("linear")
+    a = lx.run(g, st, prob, sch, w5.delta_t, 60 * w5.delta_t)
+    b = lx.run(g, st, prob, sch, w5.delta_t, 60 * w5.delta_t, stream=False)
+    assert np.array_equal(a.snapshots[0], np.array(w5.u0))
+    assert np.array_equal(a.snapshots, b.snapshots)
+
+    L = nat.lib()
+    M, K = 3000, 2
+    hc = torch.arange(M * K, dtype=torch.float64).reshape(M, K).pin_memory()
+    hu = (torch.arange(M, dtype=torch.float64) * 0.5).pin_memory()
+    snap = torch.full((M,), float("nan"), dtype=torch.float64).pin_memory()
+    dc = torch.full((M, K), float("nan"), dtype=torch.float64, device="cuda")
+    du = torch.full((M,), float("nan"), dtype=torch.float64, device="cuda")
+    up, down = _ops.copy_stream(0), _ops.copy_stream(3)
+    torch.cuda.synchronize()
+    ec, ev = C.c_void_p(), C.c_void_p()
+    assert L.lmep_event_create(C.byref(ec)) == nat.LMEP_OK and L.lmep_event_create(C.byref(ev)) == nat.LMEP_OK
+    a0, b0 = 1000, 2500
+    st_ = L.lmep_upload_slice(dc.data_ptr() + a0 * K * 8, hc.data_ptr() + a0 * K * 8, (b0 - a0) * K * 8,
+                              du.data_ptr() + a0 * 8, hu.data_ptr() + a0 * 8, snap.data_ptr() + a0 * 8,
+                              (b0 - a0) * 8, up.cuda_stream, down.cuda_stream, ec, ev)
+    assert st_ == nat.LMEP_OK
+    cur = torch.cuda.current_stream()
+    _ops.stream_wait(cur, ev)
+    got_c, got_u = dc.clone(), du.clone()          # (behind the event on the current stream)
+    torch.cuda.synchronize()
+    assert torch.equal(got_c[a0:b0].cpu(), hc[a0:b0]) and torch.equal(got_u[a0:b0].cpu(), hu[a0:b0])
+    assert torch.isnan(got_c[:a0]).all() and torch.isnan(got_u[b0:]).all()
+    assert torch.equal(snap[a0:b0], hu[a0:b0]) and torch.isnan(snap[:a0]).all() and torch.isnan(snap[b0:]).all()
+    assert L.lmep_event_destroy(ec) == nat.LMEP_OK and L.lmep_event_destroy(ev) == nat.LMEP_OK

@@ -42,10 +42,9 @@ def main():
 
     m, lo, ref = timed(False)
     print(f"phases:   median {m:.3f} ms  min {lo:.3f}  harvest_ns {ref.harvest_ns} step_ns {ref.step_ns}")
-    plans = [(1, 3, 6, 8), (1, 3, 5, 6, 5), (1, 2, 4, 6, 6), (2, 5, 7, 6), (1, 4, 7, 7), (2, 6, 8),
-             (1, 3, 6, 6, 4), (1.5, 4.5, 7, 6), (1, 3, 5, 5, 5),
-             (1, 3, 5, 5, 4, 3), (1, 2, 3, 4, 4, 4, 3), (1, 3, 5, 6, 4, 2), (1, 4, 6, 6, 4),
-             (1, 4, 7, 7, 2), (1, 4, 6, 5, 3, 2), (1, 3, 4, 4, 4, 3, 2)]
+    plans = [(1, 4, 7, 7), (1, 3, 6, 6, 4), (1, 3, 5, 5, 5), (1, 3, 4, 5, 5, 3), (1, 2, 3, 4, 5, 5),
+             (1, 3, 4, 4, 4, 4), (1, 2, 4, 5, 5, 3), (1, 3, 4, 5, 4, 3, 1.5), (1, 2, 3, 4, 4, 4, 3),
+             (1, 3, 5, 6, 4, 2), (0.5, 1.5, 3, 4, 5, 5, 2), (1, 3, 4, 5, 6, 2.5)]
     if "--last-min" in sys.argv:
         _ops.LinearStream.LAST_MIN = float(sys.argv[sys.argv.index("--last-min") + 1])
     for wv in plans:
