@@ -413,21 +413,25 @@ __global__ void __launch_bounds__(128 / IT) harvest_poly_kernel(const HarvestPar
         for (int it = 0; it < IT; ++it) ap[it] *= a[it];
         cols += qt + 1;
     }
-    const int n = P.n;
+    // (N == P.n: the launcher instantiates the kernel per stencil width)
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
         if (!live[it]) continue;
-        bool bad = false;
+        // any Inf / NaN among the outputs turns the zero-weighted sum into NaN
+        double chk = 0.0;
 #pragma unroll
-        for (int j = 0; j < N; ++j) {
-            const double o = w[it][j];
-            bad |= !isfinite(o);
-            if (j < n) {
-                if (P.layout == 0) P.out[b[it] * n + j] = o;
-                else P.out[(int64_t)j * P.out_ld + b[it]] = o;
-            }
+        for (int j = 0; j < N; ++j) chk = fma(w[it][j], 0.0, chk);
+        if (P.layout == 0) {
+            double *o = P.out + b[it] * N;
+#pragma unroll
+            for (int j = 0; j < N; ++j) o[j] = w[it][j];
+        } else {
+            double *o = P.out + b[it];
+            const int64_t ld = P.out_ld;
+#pragma unroll
+            for (int j = 0; j < N; ++j) o[j * ld] = w[it][j];
         }
-        P.status[b[it]] = bad ? LMEP_NONFINITE : LMEP_OK;
+        P.status[b[it]] = chk == 0.0 ? LMEP_OK : LMEP_NONFINITE;
         if (P.ms) P.ms[b[it]] = cols;    // scaling field 0: a polynomial item, `cols` columns
     }
 }
@@ -718,7 +722,8 @@ int launch_harvest_mvc(const HarvestParams &P, cudaStream_t st)
     // w_lin of two-table operators: the polynomial kernel first, the Taylor kernel
     // behind it on whatever it handed back
     const bool poly = P.s == 1 && P.nterms == 2 && P.c0 == nullptr && P.status != nullptr &&
-                      P.n <= MVC_PN && device_settings().mvc.load() == 1;
+                      (P.n == 7 || P.n == 9 || P.n == 11 || P.n == 13) && P.n <= MVC_PN &&
+                      device_settings().mvc.load() == 1;
     key.c0 |= poly ? 2 : 0;              // (a block prepared without the polynomial tables is not reused for it)
     // a later slice of the same harvest (same tables, step and shape; the block in
     // constant memory is still the one prepared for its first slice): the balancing
