@@ -9,9 +9,18 @@ namespace lmep {
 __global__ void status_or_kernel(const int32_t *__restrict__ st, int64_t B, int32_t *flag)
 {
     bool bad = false;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B;
-         i += (int64_t)gridDim.x * blockDim.x)
-        bad |= st[i] != LMEP_OK;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+    // 16-byte loads over the aligned body, scalar loads over what is left
+    const int64_t head = min(B, (int64_t)((16 - ((uintptr_t)st & 15)) & 15) / 4);
+    const int64_t nv = (B - head) / 4;
+    const int4 *v = reinterpret_cast<const int4 *>(st + head);
+    for (int64_t i = tid; i < nv; i += nth) {
+        const int4 q = v[i];
+        bad |= (q.x | q.y | q.z | q.w) != LMEP_OK;
+    }
+    for (int64_t i = tid; i < head; i += nth) bad |= st[i] != LMEP_OK;
+    for (int64_t i = head + 4 * nv + tid; i < B; i += nth) bad |= st[i] != LMEP_OK;
     if (__any_sync(FULL, bad) && (threadIdx.x & 31) == 0) *flag = 1;
 }
 

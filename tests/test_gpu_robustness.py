@@ -286,3 +286,28 @@ def test_c_program_on_the_c_abi(tmp_path):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stderr
     assert "c-abi smoke ok" in out.stdout and "60 steps bit-identical" in out.stdout
+
+
+@pytest.mark.gpu
+def test_status_any_every_alignment():
+    """lmep_status_any (16-byte loads over the aligned body, scalar head and tail):
+    a single failed item is found wherever it sits, for every offset of the status
+    array within a 16-byte line and sizes around the vector width; clean arrays
+    leave the flag alone."""
+    import torch
+    from paper_2603_15964_b200 import _native as nat
+    L = nat.lib()
+    nat.device()
+    base = torch.zeros(5000, dtype=torch.int32, device="cuda")
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for off in range(5):
+        for B in (1, 2, 3, 4, 5, 7, 8, 9, 31, 1024, 4093):
+            view = base[off:off + B]
+            for bad in sorted({0, B // 2, B - 1}):
+                flag.zero_()
+                assert L.lmep_status_any(view.data_ptr(), B, flag.data_ptr(), nat.stream_handle()) == 0
+                assert int(flag.item()) == 0, (off, B)
+                view[bad] = nat.LMEP_NONFINITE
+                assert L.lmep_status_any(view.data_ptr(), B, flag.data_ptr(), nat.stream_handle()) == 0
+                assert int(flag.item()) == 1, (off, B, bad)
+                view[bad] = 0
