@@ -52,7 +52,7 @@ constexpr int MVC_PV = 14;             // ... words of up to 13 factors (the las
 #ifndef LMEP_POLY_IT
 #define LMEP_POLY_IT 1
 #endif
-constexpr int MVC_IT = LMEP_POLY_IT;    // items per thread of the polynomial kernel (1: 44 registers, 102 us at config 5; 2: 116 us)
+constexpr int MVC_IT = LMEP_POLY_IT;    // items per thread of the polynomial kernel (1: 48 registers, 94 us at config 5; 2 measured slower)
 constexpr int MVC_PAIRS = (MVC_PV - 1) * MVC_PV / 2;   // pairs p + q < MVC_PV - 1
 
 struct MvcConst {
@@ -317,8 +317,8 @@ __global__ void __launch_bounds__(32 * MVC_PV) mvc_poly_prep_kernel(const Harves
 // (cancellation) or whose coefficients are not finite hands its items to the
 // Taylor kernel through the work list, as does every item when the series does
 // not terminate inside the table.
-// Config 5 (4,194,304 items): 102 us = 5.1 TB/s on its 124 B per item (16 in,
-// 104 + 4 out), 0.78 of the measured HBM peak; 44 registers.
+// Config 5 (4,194,304 items): 94 us = 5.5 TB/s on its 124 B per item (16 in,
+// 104 + 4 out), 0.85 of the measured HBM peak; 48 registers.
 
 // an upper bound of log2 |x| from the high word of |x| (log2(1 + m) <= m + 0.0861)
 __device__ __forceinline__ float poly_log2_ub(unsigned hi)
