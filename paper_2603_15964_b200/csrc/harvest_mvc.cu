@@ -49,6 +49,9 @@ constexpr int MVC_NT = 2;
 constexpr double MVC_THETA = 4.0;
 constexpr int MVC_PN = 13;             // polynomial kernel: n <= 13
 constexpr int MVC_PV = 14;             // ... words of up to 13 factors (the last anti-diagonal is the check)
+#ifndef LMEP_POLY_MINB
+#define LMEP_POLY_MINB 11
+#endif
 #ifndef LMEP_POLY_IT
 #define LMEP_POLY_IT 1
 #endif
@@ -329,7 +332,7 @@ __device__ __forceinline__ float poly_log2_ub(unsigned hi)
 // Each CTA takes one block of 128 items, IT per thread (items t, t + 128 / IT, ...:
 // the rows of a block do not depend on IT or on how the batch was sliced).
 template <int N, int IT>
-__global__ void __launch_bounds__(128 / IT) harvest_poly_kernel(const HarvestParams P, const MvcConst *G)
+__global__ void __launch_bounds__(128 / IT, LMEP_POLY_MINB) harvest_poly_kernel(const HarvestParams P, const MvcConst *__restrict__ G)
 {
     constexpr int T = 128 / IT;
     // column selection once per block, from the block-wide coefficient magnitudes
@@ -364,7 +367,7 @@ __global__ void __launch_bounds__(128 / IT) harvest_poly_kernel(const HarvestPar
         for (int k = 0; k < T / 32; ++k) { ha = max(ha, smax[k][0]); hb = max(hb, smax[k][1]); }
         const float la = poly_log2_ub(ha), lb = poly_log2_ub(hb);
         for (int i = tid; i < MVC_PAIRS; i += T) {
-            const float4 e = G->pl[i];           // (log2 |V_pq|, p, q)
+            const float4 e = __ldg(&G->pl[i]);   // (log2 |V_pq|, p, q)
             const float t = fmaf(e.y, la, fmaf(e.z, lb, e.x));
             if (t > -60.f) atomicMax(&sq[(int)e.y], (int)e.z);
             if (!(t <= 6.f)) sflag = 1;
