@@ -81,6 +81,7 @@ struct MvcConst {
     alignas(16) double pv[MVC_PV][MVC_PV][MVC_PN + 1]; // V_pq (p + q < MVC_PV; 16-byte rows), zero where numerically nilpotent
     alignas(16) float4 pl[MVC_PAIRS];  // (log2 |V_pq|_inf or -1e30: zero, p, q) of the pairs p + q < MVC_PV - 1 (the kernel reads the global copy)
     double cinv[MVC_NT];               // 1 / c_t(item 0): the kernel's a, b are c_t(item) cinv[t]
+    double cf[MVC_PV][4];              // phi rows: cf[k][r] = dt^r k! / (k + r)!  (the dt^r phi_r row sums the degree-k terms with it)
     int poly_ok;                       // the series terminates inside the table (p + q < MVC_PV)
 };
 
@@ -293,7 +294,7 @@ __global__ void __launch_bounds__(32 * MVC_PV) mvc_poly_prep_kernel(const Harves
         __syncthreads();
     }
     // the series must end inside the table: the last anti-diagonal is all zero
-    bool pok = P.s == 1 && P.nterms == 2 && P.c0 == nullptr && n <= MVC_PN && !bad;
+    bool pok = P.s >= 1 && P.s <= 4 && P.nterms == 2 && P.c0 == nullptr && n <= MVC_PN && !bad;
     for (int p = 0; p < MVC_PV; ++p)
         if (vinf[p][MVC_PV - 1 - p] != 0.0) pok = false;
     for (int i = threadIdx.x; i < MVC_PV * MVC_PV; i += blockDim.x) {
@@ -306,6 +307,14 @@ __global__ void __launch_bounds__(32 * MVC_PV) mvc_poly_prep_kernel(const Harves
         // (stored back in the unbalanced coordinates: 2^(e_c - e_row), exact)
         for (int c = 0; c <= MVC_PN; ++c)
             out->pv[p][q][c] = (in && pok && c < n) ? Vs[p][q][c] * mv_pow2(out->e[c] - out->e[row]) : 0.0;
+    }
+    if (threadIdx.x < MVC_PV) {
+        const int k = threadIdx.x;
+        double c = 1.0;
+        for (int r = 0; r < 4; ++r) {
+            out->cf[k][r] = c;
+            c *= P.delta_t / (double)(k + r + 1);
+        }
     }
     if (threadIdx.x == 0) out->poly_ok = pok ? 1 : 0;
 }
@@ -331,8 +340,8 @@ __device__ __forceinline__ float poly_log2_ub(unsigned hi)
 
 // Each CTA takes one block of 128 items, IT per thread (items t, t + 128 / IT, ...:
 // the rows of a block do not depend on IT or on how the batch was sliced).
-template <int N, int IT>
-__global__ void __launch_bounds__(128 / IT, LMEP_POLY_MINB) harvest_poly_kernel(const HarvestParams P, const MvcConst *__restrict__ G)
+template <int N, int IT, int S>
+__global__ void __launch_bounds__(128 / IT, S == 1 ? LMEP_POLY_MINB : 1) harvest_poly_kernel(const HarvestParams P, const MvcConst *__restrict__ G)
 {
     constexpr int T = 128 / IT;
     // column selection once per block, from the block-wide coefficient magnitudes
@@ -387,12 +396,17 @@ __global__ void __launch_bounds__(128 / IT, LMEP_POLY_MINB) harvest_poly_kernel(
     const int myq = (tid & 31) < MVC_PV ? sq[tid & 31] : -1;
     const unsigned has = __ballot_sync(FULL, myq >= 0);
     const int Pw = has ? 31 - __clz((int)has) : -1;
-    double w[IT][N], ap[IT];
+    // phi rows (S > 1): the dt^r phi_r row is the same sum with the degree-k terms
+    // weighted by cf[k][r] = dt^r k! / (k + r)!, so every table entry feeds S
+    // accumulators (one more multiply per term and row)
+    double w[S][IT][N], ap[IT];
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
         ap[it] = 1.0;
 #pragma unroll
-        for (int j = 0; j < N; ++j) w[it][j] = 0.0;
+        for (int r = 0; r < S; ++r)
+#pragma unroll
+            for (int j = 0; j < N; ++j) w[r][it][j] = 0.0;
     }
     int cols = 0;
 #pragma unroll
@@ -405,10 +419,21 @@ __global__ void __launch_bounds__(128 / IT, LMEP_POLY_MINB) harvest_poly_kernel(
 #pragma unroll
         for (int q = 0; q < MVC_PV - 1 - p; ++q) {
             if (q > qt) break;
+            double mr[S][IT];
 #pragma unroll
-            for (int j = 0; j < N; ++j)
+            for (int it = 0; it < IT; ++it) {
+                mr[0][it] = m[it];
 #pragma unroll
-                for (int it = 0; it < IT; ++it) w[it][j] = fma(m[it], c_mvc.pv[p][q][j], w[it][j]);
+                for (int r = 1; r < S; ++r) mr[r][it] = m[it] * c_mvc.cf[p + q][r];
+            }
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                const double v = c_mvc.pv[p][q][j];
+#pragma unroll
+                for (int r = 0; r < S; ++r)
+#pragma unroll
+                    for (int it = 0; it < IT; ++it) w[r][it][j] = fma(mr[r][it], v, w[r][it][j]);
+            }
 #pragma unroll
             for (int it = 0; it < IT; ++it) m[it] *= be[it];
         }
@@ -423,16 +448,22 @@ __global__ void __launch_bounds__(128 / IT, LMEP_POLY_MINB) harvest_poly_kernel(
         // any Inf / NaN among the outputs turns the zero-weighted sum into NaN
         double chk = 0.0;
 #pragma unroll
-        for (int j = 0; j < N; ++j) chk = fma(w[it][j], 0.0, chk);
-        if (P.layout == 0) {
-            double *o = P.out + b[it] * N;
+        for (int r = 0; r < S; ++r)
 #pragma unroll
-            for (int j = 0; j < N; ++j) o[j] = w[it][j];
+            for (int j = 0; j < N; ++j) chk = fma(w[r][it][j], 0.0, chk);
+        if (P.layout == 0) {
+            double *o = P.out + b[it] * (S * N);
+#pragma unroll
+            for (int r = 0; r < S; ++r)
+#pragma unroll
+                for (int j = 0; j < N; ++j) o[r * N + j] = w[r][it][j];
         } else {
             double *o = P.out + b[it];
             const int64_t ld = P.out_ld;
 #pragma unroll
-            for (int j = 0; j < N; ++j) o[j * ld] = w[it][j];
+            for (int r = 0; r < S; ++r)
+#pragma unroll
+                for (int j = 0; j < N; ++j) o[(r * N + j) * ld] = w[r][it][j];
         }
         P.status[b[it]] = chk == 0.0 ? LMEP_OK : LMEP_NONFINITE;
         if (P.ms) P.ms[b[it]] = cols;    // scaling field 0: a polynomial item, `cols` columns
@@ -691,6 +722,29 @@ void launch_mvc_d(const HarvestParams &P, cudaStream_t st)
     }
 }
 
+template <int N>
+void launch_poly(const HarvestParams &Q, const MvcConst *scratch, unsigned blocks, unsigned g, cudaStream_t st)
+{
+    switch (Q.s) {
+    case 1:
+        harvest_poly_kernel<N, MVC_IT, 1><<<blocks, 128 / MVC_IT, 0, st>>>(Q, scratch);
+        harvest_mvc_kernel<N, 2, false, 0><<<g, 128, 0, st>>>(Q);
+        break;
+    case 2:
+        harvest_poly_kernel<N, 1, 2><<<blocks, 128, 0, st>>>(Q, scratch);
+        harvest_mvc_kernel<N, 2, false, 1><<<g, 128, 0, st>>>(Q);
+        break;
+    case 3:
+        harvest_poly_kernel<N, 1, 3><<<blocks, 128, 0, st>>>(Q, scratch);
+        harvest_mvc_kernel<N, 2, false, 2><<<g, 128, 0, st>>>(Q);
+        break;
+    default:
+        harvest_poly_kernel<N, 1, 4><<<blocks, 128, 0, st>>>(Q, scratch);
+        harvest_mvc_kernel<N, 2, false, 3><<<g, 128, 0, st>>>(Q);
+        break;
+    }
+}
+
 }  // namespace
 
 bool harvest_mvc_eligible(const HarvestParams &P)
@@ -724,7 +778,8 @@ int launch_harvest_mvc(const HarvestParams &P, cudaStream_t st)
     key.row = P.row_default; key.c0 = P.c0 != nullptr;
     // w_lin of two-table operators: the polynomial kernel first, the Taylor kernel
     // behind it on whatever it handed back
-    const bool poly = P.s == 1 && P.nterms == 2 && P.c0 == nullptr && P.status != nullptr &&
+    const bool poly = P.s >= 1 && P.s <= 4 && P.nterms == 2 && P.c0 == nullptr && P.status != nullptr &&
+                      P.half_out == nullptr &&
                       (P.n == 7 || P.n == 9 || P.n == 11 || P.n == 13) && P.n <= MVC_PN &&
                       device_settings().mvc.load() == 1;
     key.c0 |= poly ? 2 : 0;              // (a block prepared without the polynomial tables is not reused for it)
@@ -755,19 +810,13 @@ int launch_harvest_mvc(const HarvestParams &P, cudaStream_t st)
         }
         cudaMemsetAsync(D.pending, 0, sizeof(int32_t), st);
         Q.pending = D.pending;
-        switch (P.n) {
-        case 7: harvest_poly_kernel<7, MVC_IT><<<blocks, 128 / MVC_IT, 0, st>>>(Q, D.scratch); break;
-        case 9: harvest_poly_kernel<9, MVC_IT><<<blocks, 128 / MVC_IT, 0, st>>>(Q, D.scratch); break;
-        case 11: harvest_poly_kernel<11, MVC_IT><<<blocks, 128 / MVC_IT, 0, st>>>(Q, D.scratch); break;
-        default: harvest_poly_kernel<13, MVC_IT><<<blocks, 128 / MVC_IT, 0, st>>>(Q, D.scratch); break;
-        }
-        // the Taylor kernel on what is left: a grid of at most six CTAs per SM
+        // the Taylor kernel behind it on what is left: a grid of at most six CTAs per SM
         const unsigned g = std::min<unsigned>(blocks, 6u * (unsigned)device_sm_count());
-        switch (Q.n) {
-        case 7: harvest_mvc_kernel<7, 2, false, 0><<<g, 128, 0, st>>>(Q); break;
-        case 9: harvest_mvc_kernel<9, 2, false, 0><<<g, 128, 0, st>>>(Q); break;
-        case 11: harvest_mvc_kernel<11, 2, false, 0><<<g, 128, 0, st>>>(Q); break;
-        default: harvest_mvc_kernel<13, 2, false, 0><<<g, 128, 0, st>>>(Q); break;
+        switch (P.n) {
+        case 7: launch_poly<7>(Q, D.scratch, blocks, g, st); break;
+        case 9: launch_poly<9>(Q, D.scratch, blocks, g, st); break;
+        case 11: launch_poly<11>(Q, D.scratch, blocks, g, st); break;
+        default: launch_poly<13>(Q, D.scratch, blocks, g, st); break;
         }
     } else {
         switch (Q.n) {
