@@ -252,10 +252,12 @@ def set_harvest_method(method: str) -> None:
     block-balanced kernel harvest_mvb), "mvb" (auto without harvest_mvc),
     "mvitem" (per-item balanced expm-multiply only, 4 lanes per item), "mv8"
     (the same with 8 lanes per item for d > 8), "mvb2" / "mvb4" / "mvb8" (the
-    block kernel at 2 / 4 / 8 lanes per item) or "pade" (full expm per warp).
+    block kernel at 2 / 4 / 8 lanes per item), "mvc-taylor" (auto with the
+    constant-table Taylor kernel only, without the polynomial kernel in front of
+    it) or "pade" (full expm per warp).
     Applies to the current CUDA device."""
     code = {"multiply": 0, "auto": 0, "pade": 1, "mv8": 4, "mvitem": 5, "mvb8": 6, "mvb2": 7,
-            "mvb4": 8, "mvb": 9}[method]
+            "mvb4": 8, "mvb": 9, "mvc-taylor": 10}[method]
     check(lib().lmep_set_harvest_method(code), "lmep_set_harvest_method")
 
 

@@ -1187,3 +1187,43 @@ def test_weight_table_binary_device_roundtrip(lx, tmp_path):
     a = _ops.step(nat.SCH_LIN, rows, u0, 10)
     b = _ops.step(nat.SCH_LIN, back, u0, 10)
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("n", [7, 13])
+@pytest.mark.parametrize("scale", [1.0, 4.0])
+def test_polynomial_phi_rows(lx, orc, n, scale):
+    """Per-node phi rows (s = 2..4, harvest.py:97-121 per node) of two-table operators
+    on the polynomial kernel -- the dt^r phi_r row as the w_lin sum with its degree-k
+    terms weighted by dt^r k!/(k+r)! -- against the oracle on sampled nodes (1e-12) and
+    against the Taylor kernel on every node; at 4 dt part of the blocks goes back to
+    the Taylor kernel through the work list."""
+    from paper_2603_15964_b200 import configs, _native as nat
+    from paper_2603_15964_b200.harvest import harvest_compact
+    N = 1 << 16
+    w5 = configs.c5(N=N, steps=1)
+    c, nu = w5.coef
+    g = lx.make_periodic_grid(N, 0.0, 1.0)
+    st = lx.select_stencils(g, n, lx.StencilPolicy.CENTERED)
+    row = (n - 1) // 2
+    dt = w5.delta_t * scale
+    spec = lx.VariableCoefficientSpec((1, 2), torch.as_tensor(np.stack([-c, nu], 1), device="cuda"))
+    x = (np.arange(n) - row) * w5.h
+    D1 = np.array([orc.fornberg_weights(xi, x, 2)[1] for xi in x])
+    D2 = np.array([orc.fornberg_weights(xi, x, 2)[2] for xi in x])
+    idx = np.arange(0, N, 509)
+    for s in (2, 3, 4):
+        stats = {}
+        Wd = harvest_compact(g, st, spec, dt, s, (), stats).pernode                 # [s][n][N]
+        ms = torch.cat(stats["ms"]).cpu().numpy()
+        assert ((ms >> 24) == 0).any()                       # polynomial items
+        try:
+            nat.lib().lmep_set_harvest_method(10)             # constant tables, Taylor kernel only
+            Wt = harvest_compact(g, st, spec, dt, s).pernode
+        finally:
+            nat.lib().lmep_set_harvest_method(0)
+        rel = ((Wd - Wt).abs().amax(1) / Wt.abs().amax(1)).max().item()
+        assert rel < 1e-12, (s, rel)
+        W = Wd.permute(2, 0, 1).cpu().numpy()
+        ref = orc.harvest_batch_vc(D1, D2, -c[idx], nu[idx], dt, s, row, reduced=True)
+        worst = max(_rows_rel(W[i], ref[k]) for k, i in enumerate(idx))
+        assert worst < W_TOL, (s, worst)
