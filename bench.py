@@ -894,6 +894,7 @@ def main():
                                    "frac": 2 * w.n * w.N * w.steps / (step_ms * 1e-3) / 1e12 /
                                    (fp64 / 2 if args.exact else fp64)},
             "e2e": {"value": e2e_val, "unit": unit, "passes_ms": [round(x, 4) for x in e2e_ms],
+                    "median_ms": float(np.median(e2e_ms)),   # (value is over the mean of the passes)
                     "h2d_bytes_per_step": bench.h2d_bytes,
                     "d2h_bytes_per_step": bench.d2h_bytes},
             "gpu_launches": launches,
