@@ -633,6 +633,7 @@ def main():
                           "(4194304 harvests), 200 linear steps, dt=0.5h^2/max(nu)",
               "N": 1 << 22, "n": 13, "steps_per_pass": 200, "harvests_per_pass": 1 << 22,
               "l2": "inputs larger than L2 (436 MB per-node rows streamed each step)",
+              "spinup": "0.5 s (40 passes when sharded) of untimed passes before the W warm-up passes",
               "parallelism": f"slab-sharded x{args.gpus} (NCCL halo exchange)" if args.gpus > 1
               else "single",
               "step_arith": "exact (unfused mul+add, bit-identical to numba)" if args.exact
@@ -683,6 +684,15 @@ def main():
     lib = _native.load()
 
     bench = C5(rank, world, exact=args.exact)
+    # spin-up before the W warm-up passes: three passes are 5 ms of device work, too
+    # little for a GPU that has just been handed over to leave its idle power state
+    # (a first run on a fresh box read 3.5e11 against 4.6e11 for the next one)
+    t_spin, n_spin = time.perf_counter(), 0
+    # (sharded runs: a fixed count, every rank must issue the same number of passes)
+    while (n_spin < 40) if world > 1 else (time.perf_counter() - t_spin < 0.5):
+        bench.device_pass()
+        torch.cuda.synchronize()
+        n_spin += 1
     for _ in range(args.warmup):
         bench.device_pass()
     torch.cuda.synchronize()
@@ -797,15 +807,18 @@ def main():
     phi_bytes = bench.nloc * (16 + 4 * 8 * w.n + 4)      # 2 coefficients in, 4 rows of n + status out
 
     # e2e through the public API
-    for _ in range(max(2, args.warmup)):
-        bench.e2e_pass()
-    e2e_ms = []
     # (as timeit does: no cyclic-GC pass inside a timed pass -- the host side of a
-    # pass is Python, and a generation-2 collection costs about a millisecond)
+    # pass is Python, and a generation-2 collection costs about a millisecond; the
+    # warm-up passes run in the same state, each synchronised like a timed one)
     import gc
     gc.collect()
     gc.disable()
+    e2e_ms = []
     try:
+        for _ in range(max(2, args.warmup)):
+            torch.cuda.synchronize()
+            bench.e2e_pass()
+            torch.cuda.synchronize()
         for _ in range(args.steps):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
