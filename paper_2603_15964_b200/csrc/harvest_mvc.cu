@@ -341,7 +341,7 @@ __device__ __forceinline__ float poly_log2_ub(unsigned hi)
 // Each CTA takes one block of 128 items, IT per thread (items t, t + 128 / IT, ...:
 // the rows of a block do not depend on IT or on how the batch was sliced).
 template <int N, int IT, int S>
-__global__ void __launch_bounds__(128 / IT, S == 1 ? LMEP_POLY_MINB : 1) harvest_poly_kernel(const HarvestParams P, const MvcConst *__restrict__ G)
+__global__ void __launch_bounds__(128 / IT, S == 1 ? LMEP_POLY_MINB : (S == 2 ? 6 : (S == 3 ? 5 : 4))) harvest_poly_kernel(const HarvestParams P, const MvcConst *__restrict__ G)
 {
     constexpr int T = 128 / IT;
     // column selection once per block, from the block-wide coefficient magnitudes
