@@ -201,14 +201,15 @@ def _geometry(key, make):
         if len(_GEOMETRY) >= 64:
             _GEOMETRY.clear()
         v = make()
-        _GEOMETRY[key] = (v, torch.cuda.current_stream().record_event())
+        _GEOMETRY[key] = (v, torch.cuda.current_stream().record_event(), nat.stream_handle())
         return v
-    v, ev = hit
-    cur = torch.cuda.current_stream()
-    cur.wait_event(ev)
-    t = v[0] if isinstance(v, tuple) else v
-    if t.numel():
-        t.record_stream(cur)               # stays allocated for this stream's readers
+    v, ev, made_on = hit
+    if nat.stream_handle() != made_on:       # (same stream: its own order is enough)
+        cur = torch.cuda.current_stream()
+        cur.wait_event(ev)
+        t = v[0] if isinstance(v, tuple) else v
+        if t.numel():
+            t.record_stream(cur)           # stays allocated for this stream's readers
     return v
 
 
