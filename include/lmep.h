@@ -20,6 +20,7 @@
 #ifndef LMEP_H
 #define LMEP_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus

@@ -96,3 +96,15 @@ def test_slice_transfer_entry_points_validate_without_a_gpu():
     assert lib.lmep_stream_wait_event(None, None) == nat.LMEP_INVALID_CONFIG
     assert lib.lmep_event_create(None) == nat.LMEP_INVALID_CONFIG
     assert lib.lmep_event_destroy(None) == nat.LMEP_OK
+
+
+def test_header_is_plain_c(tmp_path):
+    """include/lmep.h on its own compiles as C99 (a cgo / ctypes-side binding
+    includes nothing else first)."""
+    import subprocess
+    src = tmp_path / "hdr.c"
+    src.write_text('#include "lmep.h"\nint main(void) { return 0; }\n')
+    inc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+    r = subprocess.run(["gcc", "-fsyntax-only", "-std=c99", "-Wall", "-Werror", "-I", inc, str(src)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
