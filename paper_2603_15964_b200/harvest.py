@@ -510,7 +510,6 @@ def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
     K = len(spec.orders)
     hc = _ops.host_f64(spec.coef)[sl]
     hr = None if spec.reaction is None else _ops.host_f64(spec.reaction)[sl]
-    dc = torch.empty((N, K), dtype=torch.float64, device=d)
     dr = None if hr is None else torch.empty(N, dtype=torch.float64, device=d)
     out = _ops.HarvestOut(torch.empty((s, n, N), dtype=torch.float64, device=d),
                           torch.empty(N, dtype=torch.int32, device=d),
@@ -526,8 +525,7 @@ def _harvest_pipelined(spec, sl: slice, N: int, n: int, s: int, delta_t: float,
     # prefixes the streamed run already sent up from its constructor (same host table)
     eager = ls is not None and ls.eager and hr is None and ls.coef_src is not None and \
         ls.coef_src.data_ptr() == hc.data_ptr() and tuple(ls.coef_dev.shape) == (N, K)
-    if eager:
-        dc = ls.coef_dev
+    dc = ls.coef_dev if eager else torch.empty((N, K), dtype=torch.float64, device=d)
     cp.wait_stream(cur)                      # dc / dr (and the stream's buffers) were allocated on cur
 
     def upload(i):
